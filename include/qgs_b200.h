@@ -1,0 +1,168 @@
+/*
+ * qgs_b200 -- C ABI of the B200 (sm_100a) Quadratic Gaussian Splatting tile
+ * rasterizer.
+ *
+ * The reference path is pure Python: qgsplat.rasterizer.prepare / forward /
+ * backward (/root/reference/pkg/src/qgsplat/rasterizer.py:123,198,230) over
+ * numba kernels (raster_kernels.py:83 forward_kernel, :505 backward_kernel,
+ * :673 merge_pair_grads, :684 tile_sort_depths).  This library replaces that
+ * path one stage per entry point; the Python drop-in
+ * (paper_2411_16392_b200/rasterizer.py) binds it with ctypes.
+ * shows the binding a qgsplat maintainer would add.
+ *
+ * Conventions
+ *   - Every pointer is DEVICE memory unless stated; the caller owns and
+ *     allocates all buffers (sizes come from the *_bytes queries).  The
+ *     library never calls cudaMalloc and never synchronises the stream.
+ *   - All calls are asynchronous on `stream` and return 0 on success or a
+ *     negative QGS_E_* code; qgs_last_error() gives a thread-local message.
+ *   - Per-primitive parameters are fp32; geometry that feeds integer
+ *     outputs (screen boxes, tile sort keys) is computed in fp64 on device.
+ */
+#ifndef QGS_B200_H
+#define QGS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *qgs_stream_t; /* == cudaStream_t */
+
+#define QGS_TILE 16          /* bounds.py:19 */
+#define QGS_KG_STRIDE 24     /* floats per primitive in the kernel-gradient buffer */
+#define QGS_AUX_PLANES 12    /* float64 planes per pixel kept for the backward */
+
+enum {
+    QGS_OK = 0,
+    QGS_E_ARG = -1,          /* invalid argument / size */
+    QGS_E_CUDA = -2,         /* a CUDA launch or API call failed */
+    QGS_E_CAPACITY = -3,     /* a workspace is too small */
+};
+
+/* Pinhole camera (cameras.py:15-94).  center = -R_wc^T t_wc, computed by the
+ * caller exactly as Camera.center does (cameras.py:48-51). */
+typedef struct qgs_camera {
+    double fx, fy, cx, cy;
+    int32_t width, height;
+    double R_wc[9];          /* row-major world->camera rotation */
+    double t_wc[3];
+    double center[3];
+} qgs_camera;
+
+/* RenderSettings (rasterizer.py:22-30). */
+typedef struct qgs_settings {
+    double background[3];
+    double t_near_clip, alpha_floor, alpha_clamp, t_term;
+    int32_t resort, euclidean_density;
+} qgs_settings;
+
+/* Raw primitive parameters, PrimitiveSet layout (model.py:126-141), fp32. */
+typedef struct qgs_params {
+    const float *centers;      /* P*3 */
+    const float *quats;        /* P*4, (w, x, y, z), not necessarily unit */
+    const float *raw_scales;   /* P*3 */
+    const float *raw_signs;    /* P*3 */
+    const float *raw_opacity;  /* P */
+    const float *sh;           /* P*3*sh_coeffs, channel-major per primitive */
+    int32_t P;
+    int32_t sh_coeffs;         /* (deg+1)^2 in {1, 4, 9, 16} */
+} qgs_params;
+
+/* Forward outputs, RenderTargets (rasterizer.py:61-74).  Maps are H*W
+ * row-major (x3 interleaved for colour/normal). */
+typedef struct qgs_targets {
+    float *color;              /* color_raw + T * background */
+    float *color_raw;
+    float *alpha, *depth, *depth_sq, *depth_median;
+    float *normal;
+    float *curvature, *distortion, *transmittance;
+    int32_t *n_fragments;      /* H*W */
+    int32_t *violations;       /* per tile (tiles_x*tiles_y) */
+    double *aux;               /* QGS_AUX_PLANES*H*W float64 blend sums; required by
+                                  qgs_backward, may be NULL for a forward-only call */
+} qgs_targets;
+
+/* Upstream map gradients (rasterizer.py:230-250); NULL = all zero. */
+typedef struct qgs_upstream {
+    const float *color;        /* H*W*3 */
+    const float *alpha, *depth;
+    const float *normal;       /* H*W*3 */
+    const float *curvature, *distortion;
+} qgs_upstream;
+
+/* Raw-parameter gradients, GradientBuffer (rasterizer.py:77-108); fp32,
+ * ACCUMULATED (+=) so several views sum on device before one all-reduce. */
+typedef struct qgs_grads {
+    float *centers, *quats, *raw_scales, *raw_signs, *raw_opacity, *sh;
+    float *screen_center;      /* P*2 */
+} qgs_grads;
+
+/* ---- stage 1: per-primitive preprocessing (rasterizer.py:124-158,
+ *      bounds.py:272-292, sh.py:82-88).  Writes the per-primitive state into
+ *      `prep` (qgs_prep_bytes(P) bytes) and the total (tile, primitive) pair
+ *      count into *d_n_pairs (device int64).  Raises QGS_E_ARG on
+ *      non-finite raw scales/signs is NOT checked on device: the Python
+ *      layer validates (model.py:37-38). */
+size_t qgs_prep_bytes(int32_t P);
+int qgs_preprocess(const qgs_params *prims, const qgs_camera *cam,
+                   const qgs_settings *st, void *prep, int64_t *d_n_pairs,
+                   qgs_stream_t stream);
+
+/* ---- stage 2: key duplication + per-tile (depth key, id) sort
+ *      (rasterizer.py:159-181, raster_kernels.py:684-716).  tile_offsets has
+ *      tiles_x*tiles_y+1 entries, tile_prims n_pairs entries; both
+ *      bit-identical to the reference's np.lexsort((prim, key, tile)). */
+size_t qgs_bin_workspace_bytes(int32_t P, int64_t n_pairs, int32_t n_tiles);
+int qgs_bin(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settings *st,
+            int64_t n_pairs, void *workspace, size_t workspace_bytes,
+            int32_t *tile_offsets, int32_t *tile_prims, qgs_stream_t stream);
+/* Debug/parity: the float64 sort key of every sorted pair (same order as
+ * tile_prims), recomputed from (tile, prim). */
+int qgs_sorted_keys(const void *prep, int32_t P, const qgs_camera *cam,
+                    const qgs_settings *st, const int32_t *tile_offsets,
+                    const int32_t *tile_prims, int64_t n_pairs, double *keys,
+                    qgs_stream_t stream);
+/* Unit-level key kernel: keys of explicit (tile, prim) pairs from CALLER-GIVEN
+ * float64 prepared arrays (the oracle's), for the bit-exact key test. */
+int qgs_tile_keys_f64(int64_t n, const int64_t *pair_tiles, const int64_t *pair_prims,
+                      int32_t tiles_x, const double *ohat, const double *M,
+                      const double *wv, const double *sv, const uint8_t *planar,
+                      const double *vert_u, const double *vert_v, const double *dist,
+                      const qgs_camera *cam, const qgs_settings *st, double *keys,
+                      qgs_stream_t stream);
+
+/* ---- stage 3: forward raster (raster_kernels.py:83-286, rasterizer.py:198-227) */
+int qgs_forward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settings *st,
+                const int32_t *tile_offsets, const int32_t *tile_prims,
+                const qgs_targets *out, qgs_stream_t stream);
+
+/* ---- stage 4: backward raster (raster_kernels.py:289-681).  kg is
+ *      P*QGS_KG_STRIDE floats, zeroed by the caller; slots: ohat 0-2,
+ *      M 3-11 (with the Nmat^T terms folded in), w 12-14 and s 15-17 (with
+ *      the lambda terms folded in), alpha 18, colour 19-21. */
+int qgs_backward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settings *st,
+                 const int32_t *tile_offsets, const int32_t *tile_prims,
+                 const qgs_targets *fwd, const qgs_upstream *up, float *kg,
+                 qgs_stream_t stream);
+
+/* ---- stage 5: chain to raw parameters (rasterizer.py:270-334). */
+int qgs_chain(const qgs_params *prims, const void *prep, const float *kg,
+              const qgs_camera *cam, const qgs_grads *out, qgs_stream_t stream);
+
+/* Per-primitive debug export of the prepared state (parity tests):
+ * scales P*3 (f64), alphas P (f64), colors P*3 (f64), pix_bbox P*4 (i32),
+ * planar P (u8). Any pointer may be NULL. */
+int qgs_export_prep(const void *prep, int32_t P, double *scales, double *alphas,
+                    double *colors, int32_t *pix_bbox, uint8_t *planar,
+                    qgs_stream_t stream);
+
+const char *qgs_last_error(void);
+int qgs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QGS_B200_H */

@@ -1,0 +1,106 @@
+"""ctypes binding of libqgs_b200.so (include/qgs_b200.h).
+
+The library is built in-tree by paper_2411_16392_b200/build.py.  There is no
+CPU fallback: if the shared object is missing or fails to load, importing
+the rasterizer raises.
+"""
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libqgs_b200.so")
+
+KG_STRIDE = 24
+AUX_PLANES = 12
+TILE = 16
+
+vp = ctypes.c_void_p
+f64 = ctypes.c_double
+i32 = ctypes.c_int32
+i64 = ctypes.c_int64
+
+
+class Camera(ctypes.Structure):
+    _fields_ = [("fx", f64), ("fy", f64), ("cx", f64), ("cy", f64),
+                ("width", i32), ("height", i32),
+                ("R_wc", f64 * 9), ("t_wc", f64 * 3), ("center", f64 * 3)]
+
+
+class Settings(ctypes.Structure):
+    _fields_ = [("background", f64 * 3), ("t_near_clip", f64), ("alpha_floor", f64),
+                ("alpha_clamp", f64), ("t_term", f64), ("resort", i32),
+                ("euclidean_density", i32)]
+
+
+class Params(ctypes.Structure):
+    _fields_ = [("centers", vp), ("quats", vp), ("raw_scales", vp), ("raw_signs", vp),
+                ("raw_opacity", vp), ("sh", vp), ("P", i32), ("sh_coeffs", i32)]
+
+
+class Targets(ctypes.Structure):
+    _fields_ = [(n, vp) for n in ("color", "color_raw", "alpha", "depth", "depth_sq",
+                                  "depth_median", "normal", "curvature", "distortion",
+                                  "transmittance", "n_fragments", "violations", "aux")]
+
+
+class Upstream(ctypes.Structure):
+    _fields_ = [(n, vp) for n in ("color", "alpha", "depth", "normal", "curvature",
+                                  "distortion")]
+
+
+class Grads(ctypes.Structure):
+    _fields_ = [(n, vp) for n in ("centers", "quats", "raw_scales", "raw_signs",
+                                  "raw_opacity", "sh", "screen_center")]
+
+
+class QGSError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with "
+                          "`python -m paper_2411_16392_b200.build` (no CPU fallback exists)")
+    L = ctypes.CDLL(LIB_PATH)
+    P = ctypes.POINTER
+    sigs = {
+        "qgs_prep_bytes": (ctypes.c_size_t, [i32]),
+        "qgs_preprocess": (ctypes.c_int, [P(Params), P(Camera), P(Settings), vp, vp, vp]),
+        "qgs_bin_workspace_bytes": (ctypes.c_size_t, [i32, i64, i32]),
+        "qgs_bin": (ctypes.c_int, [vp, i32, P(Camera), P(Settings), i64, vp, ctypes.c_size_t,
+                                   vp, vp, vp]),
+        "qgs_sorted_keys": (ctypes.c_int, [vp, i32, P(Camera), P(Settings), vp, vp, i64, vp, vp]),
+        "qgs_tile_keys_f64": (ctypes.c_int, [i64, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp,
+                                             P(Camera), P(Settings), vp, vp]),
+        "qgs_forward": (ctypes.c_int, [vp, i32, P(Camera), P(Settings), vp, vp, P(Targets), vp]),
+        "qgs_backward": (ctypes.c_int, [vp, i32, P(Camera), P(Settings), vp, vp, P(Targets),
+                                        P(Upstream), vp, vp]),
+        "qgs_chain": (ctypes.c_int, [P(Params), vp, vp, P(Camera), P(Grads), vp]),
+        "qgs_export_prep": (ctypes.c_int, [vp, i32, vp, vp, vp, vp, vp, vp]),
+        "qgs_last_error": (ctypes.c_char_p, []),
+        "qgs_version": (ctypes.c_int, []),
+    }
+    for name, (res, args) in sigs.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+EXPORTS = ("qgs_prep_bytes", "qgs_preprocess", "qgs_bin_workspace_bytes", "qgs_bin",
+           "qgs_sorted_keys", "qgs_tile_keys_f64", "qgs_forward", "qgs_backward", "qgs_chain",
+           "qgs_export_prep", "qgs_last_error", "qgs_version")
+
+
+def check(rc, what):
+    if rc != 0:
+        msg = load().qgs_last_error().decode(errors="replace")
+        raise QGSError(f"{what} failed ({rc}): {msg}")

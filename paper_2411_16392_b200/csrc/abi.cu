@@ -1,0 +1,270 @@
+// extern "C" entry points of libqgs_b200.so (declared in include/qgs_b200.h).
+#include <cstdio>
+#include <string>
+
+#include "kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg)
+{
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(const char *where, cudaError_t e)
+{
+    return fail(QGS_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define QGS_CK(call)                                                     \
+    do {                                                                 \
+        cudaError_t e_ = (call);                                         \
+        if (e_ != cudaSuccess) return cuda_fail(#call, e_);              \
+    } while (0)
+#define QGS_LAUNCHED(name)                                               \
+    do {                                                                 \
+        cudaError_t e_ = cudaGetLastError();                             \
+        if (e_ != cudaSuccess) return cuda_fail(name, e_);               \
+    } while (0)
+
+inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// prep = [PrepView arrays][scan block sums]
+size_t scan_blocks(int32_t P) { return (size_t)cdiv(P > 0 ? P : 1, qgs::SCAN_ITEMS); }
+
+int64_t *scan_sums_ptr(void *prep, int32_t P)
+{
+    return reinterpret_cast<int64_t *>(static_cast<char *>(prep) + qgs::prep_bytes(P));
+}
+
+struct BinWs {
+    int *diff;
+    int32_t *cursor;
+    uint64_t *bucket, *tmp;
+    size_t bytes;
+};
+
+BinWs bin_ws(void *base, int32_t tiles_x, int32_t tiles_y, int64_t n_pairs)
+{
+    char *b = static_cast<char *>(base);
+    BinWs w;
+    size_t o = 0;
+    size_t ndiff = (size_t)(tiles_x + 1) * (tiles_y + 1);
+    w.diff = reinterpret_cast<int *>(b + o);        o += qgs::align256(ndiff * sizeof(int));
+    w.cursor = reinterpret_cast<int32_t *>(b + o);  o += qgs::align256((size_t)tiles_x * tiles_y * 4);
+    w.bucket = reinterpret_cast<uint64_t *>(b + o); o += qgs::align256((size_t)n_pairs * 8);
+    w.tmp = reinterpret_cast<uint64_t *>(b + o);    o += qgs::align256((size_t)n_pairs * 8);
+    w.bytes = o;
+    return w;
+}
+
+bool smem_configured = false;
+
+int configure()
+{
+    if (smem_configured) return 0;
+    QGS_CK(cudaFuncSetAttribute(qgs::tile_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)qgs::sort_smem_bytes()));
+    QGS_CK(cudaFuncSetAttribute(qgs::raster_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)qgs::raster_smem_bytes()));
+    QGS_CK(cudaFuncSetAttribute(qgs::raster_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)qgs::raster_smem_bytes()));
+    smem_configured = true;
+    return 0;
+}
+
+int check_cam(const qgs_camera *cam)
+{
+    if (!cam) return fail(QGS_E_ARG, "camera is NULL");
+    if (cam->width <= 0 || cam->height <= 0 || cam->width > 32767 || cam->height > 32767)
+        return fail(QGS_E_ARG, "image size must be in [1, 32767]");
+    if (!(cam->fx > 0 && cam->fy > 0)) return fail(QGS_E_ARG, "focal lengths must be positive");
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *qgs_last_error(void) { return g_err.c_str(); }
+int qgs_version(void) { return 1; }
+
+size_t qgs_prep_bytes(int32_t P)
+{
+    return qgs::prep_bytes(P) + qgs::align256(scan_blocks(P) * sizeof(int64_t));
+}
+
+int qgs_preprocess(const qgs_params *prims, const qgs_camera *cam, const qgs_settings *st,
+                   void *prep, int64_t *d_n_pairs, qgs_stream_t stream)
+{
+    if (!prims || !st || !prep || !d_n_pairs) return fail(QGS_E_ARG, "NULL argument");
+    if (int rc = check_cam(cam)) return rc;
+    if (prims->P < 0) return fail(QGS_E_ARG, "P < 0");
+    if (prims->sh_coeffs != 1 && prims->sh_coeffs != 4 && prims->sh_coeffs != 9 &&
+        prims->sh_coeffs != 16)
+        return fail(QGS_E_ARG, "sh_coeffs must be 1, 4, 9 or 16");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int P = prims->P;
+    qgs::PrepView pv = qgs::prep_view(prep, P);
+    qgs::CamK ck = qgs::make_camk(*cam);
+    if (P == 0) {
+        QGS_CK(cudaMemsetAsync(d_n_pairs, 0, sizeof(int64_t), s));
+        QGS_CK(cudaMemsetAsync(pv.pair_off, 0, sizeof(int64_t), s));
+        return 0;
+    }
+    qgs::preprocess_kernel<<<cdiv(P, 128), 128, 0, s>>>(*prims, ck, pv);
+    QGS_LAUNCHED("preprocess_kernel");
+    const int nb = (int)scan_blocks(P);
+    int64_t *sums = scan_sums_ptr(prep, P);
+    qgs::scan_sums_kernel<<<nb, qgs::SCAN_THREADS, 0, s>>>(pv.ntiles, P, sums);
+    qgs::scan_top_kernel<<<1, qgs::SCAN_THREADS, 0, s>>>(sums, nb, d_n_pairs, pv.pair_off, P);
+    qgs::scan_out_kernel<<<nb, qgs::SCAN_THREADS, 0, s>>>(pv.ntiles, P, sums, pv.pair_off);
+    QGS_LAUNCHED("scan kernels");
+    return 0;
+}
+
+size_t qgs_bin_workspace_bytes(int32_t P, int64_t n_pairs, int32_t n_tiles)
+{
+    (void)P;
+    // diff grid is at most (n_tiles + tiles_x + tiles_y + 1) entries; bound it by 2*n_tiles + 2*32768
+    size_t ndiff = 2 * (size_t)n_tiles + 65538;
+    return qgs::align256(ndiff * sizeof(int)) + qgs::align256((size_t)n_tiles * 4) +
+           2 * qgs::align256((size_t)n_pairs * 8) + 256;
+}
+
+int qgs_bin(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settings *st,
+            int64_t n_pairs, void *workspace, size_t workspace_bytes, int32_t *tile_offsets,
+            int32_t *tile_prims, qgs_stream_t stream)
+{
+    if (!prep || !st || !tile_offsets) return fail(QGS_E_ARG, "NULL argument");
+    if (int rc = check_cam(cam)) return rc;
+    if (n_pairs < 0 || n_pairs > 0x7fffffffLL) return fail(QGS_E_ARG, "n_pairs out of int32 range");
+    if (int rc = configure()) return rc;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    qgs::CamK ck = qgs::make_camk(*cam);
+    qgs::SetK sk = qgs::make_setk(*st);
+    const int n_tiles = ck.tiles_x * ck.tiles_y;
+    BinWs ws = bin_ws(workspace, ck.tiles_x, ck.tiles_y, n_pairs);
+    if (ws.bytes > workspace_bytes) return fail(QGS_E_CAPACITY, "bin workspace too small");
+    qgs::PrepView pv = qgs::prep_view(const_cast<void *>(prep), P);
+    QGS_CK(cudaMemsetAsync(ws.diff, 0, (size_t)(ck.tiles_x + 1) * (ck.tiles_y + 1) * sizeof(int), s));
+    if (P > 0) {
+        qgs::tile_diff_kernel<<<cdiv(P, 256), 256, 0, s>>>(pv.bbox, P, ck.tiles_x, ws.diff);
+        QGS_LAUNCHED("tile_diff_kernel");
+    }
+    qgs::tile_offsets_kernel<<<1, 1024, 0, s>>>(ws.diff, ck.tiles_x, ck.tiles_y, tile_offsets,
+                                                 ws.cursor);
+    QGS_LAUNCHED("tile_offsets_kernel");
+    if (n_pairs == 0) return 0;
+    const int grid = (int)std::min<long long>(cdiv(n_pairs, 256), 148LL * 32);
+    qgs::pair_key_kernel<<<grid, 256, 0, s>>>(pv, P, n_pairs, ck, sk, ws.cursor, ws.bucket);
+    QGS_LAUNCHED("pair_key_kernel");
+    qgs::tile_sort_kernel<<<n_tiles, qgs::SORT_THREADS, qgs::sort_smem_bytes(), s>>>(
+        tile_offsets, ws.bucket, ws.tmp, pv, ck, sk, tile_prims);
+    QGS_LAUNCHED("tile_sort_kernel");
+    return 0;
+}
+
+int qgs_sorted_keys(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settings *st,
+                    const int32_t *tile_offsets, const int32_t *tile_prims, int64_t n_pairs,
+                    double *keys, qgs_stream_t stream)
+{
+    (void)n_pairs;
+    if (int rc = check_cam(cam)) return rc;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    qgs::CamK ck = qgs::make_camk(*cam);
+    qgs::SetK sk = qgs::make_setk(*st);
+    qgs::PrepView pv = qgs::prep_view(const_cast<void *>(prep), P);
+    const int n_tiles = ck.tiles_x * ck.tiles_y;
+    qgs::sorted_keys_kernel<<<n_tiles, 128, 0, s>>>(pv, tile_offsets, tile_prims, n_tiles, ck, sk,
+                                                   keys);
+    QGS_LAUNCHED("sorted_keys_kernel");
+    return 0;
+}
+
+int qgs_tile_keys_f64(int64_t n, const int64_t *pair_tiles, const int64_t *pair_prims,
+                      int32_t tiles_x, const double *ohat, const double *M, const double *wv,
+                      const double *sv, const uint8_t *planar, const double *vert_u,
+                      const double *vert_v, const double *dist, const qgs_camera *cam,
+                      const qgs_settings *st, double *keys, qgs_stream_t stream)
+{
+    if (int rc = check_cam(cam)) return rc;
+    if (n <= 0) return 0;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    qgs::CamK ck = qgs::make_camk(*cam);
+    if (tiles_x != ck.tiles_x) return fail(QGS_E_ARG, "tiles_x does not match the camera");
+    qgs::SetK sk = qgs::make_setk(*st);
+    const int grid = (int)std::min<long long>(cdiv(n, 256), 148LL * 32);
+    qgs::tile_keys_f64_kernel<<<grid, 256, 0, s>>>(n, pair_tiles, pair_prims, ohat, M, wv, sv,
+                                                  planar, vert_u, vert_v, dist, ck, sk, keys);
+    QGS_LAUNCHED("tile_keys_f64_kernel");
+    return 0;
+}
+
+int qgs_forward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settings *st,
+                const int32_t *tile_offsets, const int32_t *tile_prims, const qgs_targets *out,
+                qgs_stream_t stream)
+{
+    if (!prep || !st || !out || !tile_offsets) return fail(QGS_E_ARG, "NULL argument");
+    if (int rc = check_cam(cam)) return rc;
+    if (int rc = configure()) return rc;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    qgs::CamK ck = qgs::make_camk(*cam);
+    qgs::SetK sk = qgs::make_setk(*st);
+    qgs::PrepView pv = qgs::prep_view(const_cast<void *>(prep), P);
+    qgs::raster_fwd_kernel<<<ck.tiles_x * ck.tiles_y, qgs::RASTER_THREADS,
+                             qgs::raster_smem_bytes(), s>>>(pv.rec, tile_offsets, tile_prims, ck,
+                                                            sk, *out);
+    QGS_LAUNCHED("raster_fwd_kernel");
+    return 0;
+}
+
+int qgs_backward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settings *st,
+                 const int32_t *tile_offsets, const int32_t *tile_prims, const qgs_targets *fwd,
+                 const qgs_upstream *up, float *kg, qgs_stream_t stream)
+{
+    if (!prep || !st || !fwd || !up || !kg || !tile_offsets) return fail(QGS_E_ARG, "NULL argument");
+    if (!fwd->aux) return fail(QGS_E_ARG, "backward needs the forward's aux planes");
+    if (int rc = check_cam(cam)) return rc;
+    if (int rc = configure()) return rc;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    qgs::CamK ck = qgs::make_camk(*cam);
+    qgs::SetK sk = qgs::make_setk(*st);
+    qgs::PrepView pv = qgs::prep_view(const_cast<void *>(prep), P);
+    qgs::raster_bwd_kernel<<<ck.tiles_x * ck.tiles_y, qgs::RASTER_THREADS,
+                             qgs::raster_smem_bytes(), s>>>(pv.rec, tile_offsets, tile_prims, ck,
+                                                            sk, *fwd, *up, kg);
+    QGS_LAUNCHED("raster_bwd_kernel");
+    return 0;
+}
+
+int qgs_chain(const qgs_params *prims, const void *prep, const float *kg, const qgs_camera *cam,
+              const qgs_grads *out, qgs_stream_t stream)
+{
+    (void)prep;
+    if (!prims || !kg || !out) return fail(QGS_E_ARG, "NULL argument");
+    if (int rc = check_cam(cam)) return rc;
+    if (prims->P == 0) return 0;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    qgs::CamK ck = qgs::make_camk(*cam);
+    qgs::chain_kernel<<<cdiv(prims->P, 128), 128, 0, s>>>(*prims, ck, kg, *out);
+    QGS_LAUNCHED("chain_kernel");
+    return 0;
+}
+
+int qgs_export_prep(const void *prep, int32_t P, double *scales, double *alphas, double *colors,
+                    int32_t *pix_bbox, uint8_t *planar, qgs_stream_t stream)
+{
+    if (P == 0) return 0;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    qgs::PrepView pv = qgs::prep_view(const_cast<void *>(prep), P);
+    qgs::export_prep_kernel<<<cdiv(P, 128), 128, 0, s>>>(pv, P, scales, alphas, colors, pix_bbox,
+                                                        planar);
+    QGS_LAUNCHED("export_prep_kernel");
+    return 0;
+}
+
+}  // extern "C"

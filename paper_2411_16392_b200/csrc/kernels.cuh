@@ -1,0 +1,46 @@
+// Kernel declarations shared between the translation units and abi.cu.
+#pragma once
+#include "qgs_common.cuh"
+
+namespace qgs {
+
+// preprocess.cu
+__global__ void preprocess_kernel(qgs_params prm, CamK cam, PrepView pv);
+__global__ void chain_kernel(qgs_params prm, CamK cam, const float *kg, qgs_grads out);
+__global__ void export_prep_kernel(PrepView pv, int P, double *scales, double *alphas,
+                                   double *colors, int32_t *bbox, uint8_t *planar);
+
+// binning.cu
+constexpr int SCAN_THREADS = 1024;
+constexpr int SCAN_ITEMS = SCAN_THREADS * 4;
+__global__ void scan_sums_kernel(const int32_t *in, int n, int64_t *sums);
+__global__ void scan_top_kernel(int64_t *sums, int nb, int64_t *d_total, int64_t *out, int n);
+__global__ void scan_out_kernel(const int32_t *in, int n, const int64_t *sums, int64_t *out);
+__global__ void tile_diff_kernel(const int4 *bbox, int P, int tiles_x, int *diff);
+__global__ void tile_offsets_kernel(int *diff, int tiles_x, int tiles_y, int32_t *tile_offsets,
+                                    int32_t *cursor);
+__global__ void pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
+                                int32_t *cursor, uint64_t *bucket);
+__global__ void tile_sort_kernel(const int32_t *tile_offsets, uint64_t *keys, uint64_t *tmp,
+                                 PrepView pv, CamK cam, SetK st, int32_t *tile_prims);
+__global__ void sorted_keys_kernel(PrepView pv, const int32_t *tile_offsets,
+                                   const int32_t *tile_prims, int n_tiles, CamK cam, SetK st,
+                                   double *keys);
+__global__ void tile_keys_f64_kernel(int64_t n, const int64_t *pair_tiles,
+                                     const int64_t *pair_prims, const double *ohat,
+                                     const double *M, const double *wv, const double *sv,
+                                     const uint8_t *planar, const double *vu, const double *vv,
+                                     const double *dist, CamK cam, SetK st, double *keys);
+size_t sort_smem_bytes();
+constexpr int SORT_THREADS = 512;
+
+// raster.cu
+__global__ void raster_fwd_kernel(const PrimRec *recs, const int32_t *tile_offsets,
+                                  const int32_t *tile_prims, CamK cam, SetK st, qgs_targets out);
+__global__ void raster_bwd_kernel(const PrimRec *recs, const int32_t *tile_offsets,
+                                  const int32_t *tile_prims, CamK cam, SetK st, qgs_targets fwd,
+                                  qgs_upstream upst, float *kg);
+size_t raster_smem_bytes();
+constexpr int RASTER_THREADS = 256;
+
+}  // namespace qgs

@@ -1,0 +1,405 @@
+// K1 per-primitive preprocessing and K7 chain-to-raw-parameters.
+//
+// One thread per primitive, float64 throughout; this translation unit is
+// compiled with -fmad=false so products and sums round exactly as the
+// reference's numpy expressions do (rasterizer.py:124-158, bounds.py:167-292,
+// model.py:29-110, sh.py:22-99).  Outputs: the fp64 geometry used by the sort
+// keys, the 128-byte fp32 raster record, the inclusive pixel box and the
+// number of 16x16 tiles the box covers.
+#include "qgs_common.cuh"
+
+namespace qgs {
+
+__device__ inline double sign0(double v) { return v < 0.0 ? -1.0 : 1.0; }
+
+// quat_to_rot (model.py:70-87), normalised (w, x, y, z) -> row-major R
+__device__ inline void quat_rot(const float *q4, double R[9], double qn[4], double &norm)
+{
+    double w = q4[0], x = q4[1], y = q4[2], z = q4[3];
+    norm = sqrt(w * w + x * x + y * y + z * z);
+    w = w / norm; x = x / norm; y = y / norm; z = z / norm;
+    qn[0] = w; qn[1] = x; qn[2] = y; qn[3] = z;
+    R[0] = 1 - 2 * (y * y + z * z);
+    R[1] = 2 * (x * y - w * z);
+    R[2] = 2 * (x * z + w * y);
+    R[3] = 2 * (x * y + w * z);
+    R[4] = 1 - 2 * (x * x + z * z);
+    R[5] = 2 * (y * z - w * x);
+    R[6] = 2 * (x * z - w * y);
+    R[7] = 2 * (y * z + w * x);
+    R[8] = 1 - 2 * (x * x + y * y);
+}
+
+// activate_scales (model.py:29-45)
+__device__ inline void activate(const float *rs, const float *rg, double s[3], bool clamped[3])
+{
+    for (int k = 0; k < 3; ++k) {
+        s[k] = tanh((double)rg[k]) * exp((double)rs[k]);
+        clamped[k] = false;
+    }
+    for (int k = 0; k < 2; ++k)
+        if (fabs(s[k]) < 1e-4) { clamped[k] = true; s[k] = sign0(s[k]) * 1e-4; }
+}
+
+// real SH basis, degrees 0..3 (sh.py:22-46)
+__device__ inline void sh_basis(int K, double x, double y, double z, double Y[16])
+{
+    const double C0 = 0.28209479177387814, C1 = 0.4886025119029199;
+    Y[0] = C0;
+    if (K > 1) { Y[1] = -C1 * y; Y[2] = C1 * z; Y[3] = -C1 * x; }
+    if (K > 4) {
+        Y[4] = 1.0925484305920792 * x * y;
+        Y[5] = -1.0925484305920792 * y * z;
+        Y[6] = 0.31539156525252005 * (2 * z * z - x * x - y * y);
+        Y[7] = -1.0925484305920792 * x * z;
+        Y[8] = 0.5462742152960396 * (x * x - y * y);
+    }
+    if (K > 9) {
+        Y[9] = -0.5900435899266435 * y * (3 * x * x - y * y);
+        Y[10] = 2.890611442640554 * x * y * z;
+        Y[11] = -0.4570457994644658 * y * (4 * z * z - x * x - y * y);
+        Y[12] = 0.3731763325901154 * z * (2 * z * z - 3 * x * x - 3 * y * y);
+        Y[13] = -0.4570457994644658 * x * (4 * z * z - x * x - y * y);
+        Y[14] = 1.445305721320277 * z * (x * x - y * y);
+        Y[15] = -0.5900435899266435 * x * (x * x - 3 * y * y);
+    }
+}
+
+// d basis / d dir (sh.py:49-79), J[k][3]
+__device__ inline void sh_basis_jac(int K, double x, double y, double z, double J[16][3])
+{
+    const double C1 = 0.4886025119029199;
+    for (int k = 0; k < K; ++k) J[k][0] = J[k][1] = J[k][2] = 0.0;
+    if (K > 1) { J[1][1] = -C1; J[2][2] = C1; J[3][0] = -C1; }
+    if (K > 4) {
+        const double a = 1.0925484305920792, b = -1.0925484305920792, c = 0.31539156525252005,
+                     d = -1.0925484305920792, e = 0.5462742152960396;
+        J[4][0] = a * y; J[4][1] = a * x;
+        J[5][1] = b * z; J[5][2] = b * y;
+        J[6][0] = -2 * c * x; J[6][1] = -2 * c * y; J[6][2] = 4 * c * z;
+        J[7][0] = d * z; J[7][2] = d * x;
+        J[8][0] = 2 * e * x; J[8][1] = -2 * e * y;
+    }
+    if (K > 9) {
+        const double c0 = -0.5900435899266435, c1 = 2.890611442640554, c2 = -0.4570457994644658,
+                     c3 = 0.3731763325901154, c4 = -0.4570457994644658, c5 = 1.445305721320277,
+                     c6 = -0.5900435899266435;
+        J[9][0] = 6 * c0 * x * y; J[9][1] = c0 * (3 * x * x - 3 * y * y);
+        J[10][0] = c1 * y * z; J[10][1] = c1 * x * z; J[10][2] = c1 * x * y;
+        J[11][0] = -2 * c2 * x * y; J[11][1] = c2 * (4 * z * z - x * x - 3 * y * y);
+        J[11][2] = 8 * c2 * y * z;
+        J[12][0] = -6 * c3 * x * z; J[12][1] = -6 * c3 * y * z;
+        J[12][2] = c3 * (6 * z * z - 3 * x * x - 3 * y * y);
+        J[13][0] = c4 * (4 * z * z - 3 * x * x - y * y); J[13][1] = -2 * c4 * x * y;
+        J[13][2] = 8 * c4 * x * z;
+        J[14][0] = 2 * c5 * x * z; J[14][1] = -2 * c5 * y * z; J[14][2] = c5 * (x * x - y * y);
+        J[15][0] = c6 * (3 * x * x - 3 * y * y); J[15][1] = -6 * c6 * x * y;
+    }
+}
+
+// inline solve_radius_for_sigma (geodesic.py:80-91 as bounds.py:177-178)
+__device__ inline double support_radius(double a, double sig)
+{
+    return 14.0 * sig / (6.0 + sqrt(36.0 + 112.0 * a * sig));
+}
+
+// pixel AABB of 8 local corners (bounds.py:234-269); returns false when empty
+__device__ inline void project_box(const double cs[8][3], const double R[9], const double c[3],
+                                   const CamK &cam, long long box[4])
+{
+    bool any = false, all = true;
+    double umin = 1e18, vmin = 1e18, umax = -1e18, vmax = -1e18;
+    for (int k = 0; k < 8; ++k) {
+        double w0 = R[0] * cs[k][0] + R[1] * cs[k][1] + R[2] * cs[k][2] + c[0];
+        double w1 = R[3] * cs[k][0] + R[4] * cs[k][1] + R[5] * cs[k][2] + c[1];
+        double w2 = R[6] * cs[k][0] + R[7] * cs[k][1] + R[8] * cs[k][2] + c[2];
+        double X = w0 * cam.Rwc[0] + w1 * cam.Rwc[1] + w2 * cam.Rwc[2] + cam.twc[0];
+        double Y = w0 * cam.Rwc[3] + w1 * cam.Rwc[4] + w2 * cam.Rwc[5] + cam.twc[1];
+        double Z = w0 * cam.Rwc[6] + w1 * cam.Rwc[7] + w2 * cam.Rwc[8] + cam.twc[2];
+        if (Z > 1e-6) {
+            any = true;
+            double u = cam.fx * X / Z + cam.cx, v = cam.fy * Y / Z + cam.cy;
+            umin = fmin(umin, u); umax = fmax(umax, u);
+            vmin = fmin(vmin, v); vmax = fmax(vmax, v);
+        } else {
+            all = false;
+        }
+    }
+    double lu = fmin(fmax(floor(umin - 0.5), 0.0), (double)(cam.W - 1));
+    double hu = fmin(fmax(ceil(umax - 0.5), 0.0), (double)(cam.W - 1));
+    double lv = fmin(fmax(floor(vmin - 0.5), 0.0), (double)(cam.H - 1));
+    double hv = fmin(fmax(ceil(vmax - 0.5), 0.0), (double)(cam.H - 1));
+    box[0] = (long long)lu; box[1] = (long long)hu; box[2] = (long long)lv; box[3] = (long long)hv;
+    if (any && !all) { box[0] = 0; box[1] = cam.W - 1; box[2] = 0; box[3] = cam.H - 1; }
+    if (!any || box[0] > box[1] || box[2] > box[3]) { box[0] = 0; box[1] = -1; box[2] = 0; box[3] = -1; }
+}
+
+// tight_bboxes_batch for one primitive (bounds.py:272-292)
+__device__ inline void tight_box(const double s[3], const double R[9], const double c[3],
+                                 const CamK &cam, long long out[4])
+{
+    double m1 = fabs(s[0]), m2 = fabs(s[1]), m3 = fabs(s[2]);
+    double a0 = s[2] * sign0(s[0]) / (s[0] * s[0]);
+    double a1 = s[2] * sign0(s[1]) / (s[1] * s[1]);
+    bool flat = m3 < 1e-6;
+    double big = fmax(m1, m2), small = fmin(m1, m2);
+    // loose support box
+    double amin = a0 * a1 < 0 ? 0.0 : fmin(fabs(a0), fabs(a1));
+    double amax = fmax(fabs(a0), fabs(a1));
+    double r1 = flat ? 3.0 * m1 : support_radius(amin, 3.0 * m1);
+    double r2 = flat ? 3.0 * m2 : support_radius(amin, 3.0 * m2);
+    double zb = fmax(0.0, (21.0 * big - 6.0 * support_radius(amax, 3.0 * small)) / 4.0);
+    double zlo = flat ? 0.0 : ((a0 < 0 || a1 < 0) ? -zb : 0.0);
+    double zhi = flat ? 0.0 : ((a0 > 0 || a1 > 0) ? zb : 0.0);
+    double cs[8][3];
+    int k = 0;
+    for (int ex = -1; ex <= 1; ex += 2)
+        for (int ey = -1; ey <= 1; ey += 2)
+            for (int ez = 0; ez < 2; ++ez) {
+                cs[k][0] = ex * r1; cs[k][1] = ey * r2; cs[k][2] = ez ? zhi : zlo;
+                ++k;
+            }
+    long long loose[4];
+    project_box(cs, R, c, cam, loose);
+    // tangent-plane frustum (elliptic case)
+    bool ok = (m3 >= 1e-6) && (a0 * a1 > 0) && (fmin(fabs(a0), fabs(a1)) >= 1e-9);
+    for (int j = 0; j < 4; ++j) out[j] = loose[j];
+    if (!ok) {
+        if (out[0] > out[1] || out[2] > out[3]) { out[0] = 0; out[1] = -1; out[2] = 0; out[3] = -1; }
+        return;
+    }
+    double zs = a0 > 0 ? 1.0 : -1.0;
+    double A0 = fabs(a0), A1 = fabs(a1);
+    double q1 = support_radius(A0, 3.0 * m1), q2 = support_radius(A1, 3.0 * m2);
+    double zb2 = fmax(0.0, (21.0 * big - 6.0 * support_radius(fmax(A0, A1), 3.0 * small)) / 4.0);
+    double h = fmax(zb2, fmax(A0 * (q1 * q1), A1 * (q2 * q2)));
+    double e1 = (h / A0 + q1 * q1) / (2.0 * q1), e2 = (h / A1 + q2 * q2) / (2.0 * q2);
+    k = 0;
+    for (int ex = -1; ex <= 1; ex += 2)
+        for (int ey = -1; ey <= 1; ey += 2) {
+            cs[k][0] = ex * q1 / 2; cs[k][1] = ey * q2 / 2; cs[k][2] = 0.0;
+            cs[k + 4][0] = ex * e1; cs[k + 4][1] = ey * e2; cs[k + 4][2] = zs * h;
+            ++k;
+        }
+    long long fr[4];
+    project_box(cs, R, c, cam, fr);
+    bool live_l = loose[0] <= loose[1];
+    if (live_l && fr[0] <= fr[1]) {
+        out[0] = max(loose[0], fr[0]); out[1] = min(loose[1], fr[1]);
+        out[2] = max(loose[2], fr[2]); out[3] = min(loose[3], fr[3]);
+    }
+    if (live_l && (fr[0] > fr[1] || fr[2] > fr[3])) { out[0] = 0; out[1] = -1; out[2] = 0; out[3] = -1; }
+    if (out[0] > out[1] || out[2] > out[3]) { out[0] = 0; out[1] = -1; out[2] = 0; out[3] = -1; }
+}
+
+__global__ void preprocess_kernel(qgs_params prm, CamK cam, PrepView pv)
+{
+    int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= prm.P) return;
+    const float *cf = prm.centers + 3 * p;
+    double c[3] = {cf[0], cf[1], cf[2]};
+    double s[3];
+    bool clamped[3];
+    activate(prm.raw_scales + 3 * p, prm.raw_signs + 3 * p, s, clamped);
+    double alpha = 1.0 / (1.0 + exp(-(double)prm.raw_opacity[p]));
+    double R[9], qn[4], qnorm;
+    quat_rot(prm.quats + 4 * p, R, qn, qnorm);
+    bool planar = fabs(s[2]) < 1e-6;
+    double w1 = sign0(s[0]) / (s[0] * s[0]);
+    double w2 = sign0(s[1]) / (s[1] * s[1]);
+    double iw3 = planar ? 0.0 : 1.0 / s[2];
+    double lam1 = s[2] * w1, lam2 = s[2] * w2;
+    double e[3] = {cam.eye[0] - c[0], cam.eye[1] - c[1], cam.eye[2] - c[2]};
+    Geo64 g;
+    for (int i = 0; i < 3; ++i) g.ohat[i] = R[0 + i] * e[0] + R[3 + i] * e[1] + R[6 + i] * e[2];
+    // M = R^T R_cw, R_cw = R_wc^T  ->  M[i][k] = sum_j R[j][i] Rwc[k][j]
+    for (int i = 0; i < 3; ++i)
+        for (int kk = 0; kk < 3; ++kk)
+            g.M[3 * i + kk] = R[0 + i] * cam.Rwc[3 * kk + 0] + R[3 + i] * cam.Rwc[3 * kk + 1] +
+                              R[6 + i] * cam.Rwc[3 * kk + 2];
+    g.wv[0] = w1; g.wv[1] = w2; g.wv[2] = iw3;
+    g.sv[0] = s[0]; g.sv[1] = s[1]; g.sv[2] = s[2];
+    double v[3] = {c[0] - cam.eye[0], c[1] - cam.eye[1], c[2] - cam.eye[2]};
+    double dist = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+    dist = fmax(dist, 1e-12);
+    g.dist = dist;
+    double vd[3] = {v[0] / dist, v[1] / dist, v[2] / dist};
+    // SH colour (sh.py:82-88)
+    int K = prm.sh_coeffs;
+    double Y[16];
+    sh_basis(K, vd[0], vd[1], vd[2], Y);
+    const float *shp = prm.sh + (size_t)p * 3 * K;
+    for (int ch = 0; ch < 3; ++ch) {
+        double acc = 0.0;
+        for (int k = 0; k < K; ++k) acc += (double)shp[ch * K + k] * Y[k];
+        acc = acc + 0.5;
+        g.col[ch] = acc < 0 ? 0.0 : acc;
+    }
+    g.alpha = alpha;
+    g.planar = planar ? 1.0 : 0.0;
+    // projected vertex (cameras.py:73-79)
+    double X = c[0] * cam.Rwc[0] + c[1] * cam.Rwc[1] + c[2] * cam.Rwc[2] + cam.twc[0];
+    double Yc = c[0] * cam.Rwc[3] + c[1] * cam.Rwc[4] + c[2] * cam.Rwc[5] + cam.twc[1];
+    double Z = c[0] * cam.Rwc[6] + c[1] * cam.Rwc[7] + c[2] * cam.Rwc[8] + cam.twc[2];
+    g.vert_u = cam.fx * X / Z + cam.cx;
+    g.vert_v = cam.fy * Yc / Z + cam.cy;
+    for (int i = 0; i < 6; ++i) g.pad[i] = 0.0;
+    pv.geo[p] = g;
+
+    long long box[4];
+    tight_box(s, R, c, cam, box);
+    pv.bbox[p] = make_int4((int)box[0], (int)box[1], (int)box[2], (int)box[3]);
+    int nt = 0;
+    if (box[0] <= box[1])
+        nt = (int)((box[1] / TILE - box[0] / TILE + 1) * (box[3] / TILE - box[2] / TILE + 1));
+    pv.ntiles[p] = nt;
+
+    PrimRec r;
+    for (int i = 0; i < 9; ++i) r.M[i] = (float)g.M[i];
+    r.ox = (float)g.ohat[0]; r.oy = (float)g.ohat[1]; r.oz = (float)g.ohat[2];
+    r.w1 = (float)w1; r.w2 = (float)w2; r.iw3 = (float)iw3;
+    r.s1 = (float)s[0]; r.s2 = (float)s[1]; r.s3 = (float)s[2];
+    r.lam1 = (float)lam1; r.lam2 = (float)lam2;
+    r.alpha = (float)alpha;
+    r.C = (float)(w1 * g.ohat[0] * g.ohat[0] + w2 * g.ohat[1] * g.ohat[1] - iw3 * g.ohat[2]);
+    for (int ch = 0; ch < 3; ++ch) r.col[ch] = (float)g.col[ch];
+    if (box[0] <= box[1]) {
+        r.bb_u = (uint32_t)box[0] | ((uint32_t)box[1] << 16);
+        r.bb_v = (uint32_t)box[2] | ((uint32_t)box[3] << 16);
+    } else {
+        r.bb_u = 0xffffu; r.bb_v = 0xffffu;   // umin > umax: never inside
+    }
+    r.flags = planar ? 1u : 0u;
+    double s12 = fabs(s[0] * s[1]);
+    r.s12 = (float)s12;
+    r.ell9 = (float)(9.0 * s12 * s12);
+    r.pad[0] = r.pad[1] = 0.f;
+    pv.rec[p] = r;
+}
+
+// ------------------------------------------------------------- K7 chain
+
+__global__ void chain_kernel(qgs_params prm, CamK cam, const float *__restrict__ kg,
+                             qgs_grads out)
+{
+    int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= prm.P) return;
+    const float *g = kg + (size_t)p * KG;
+    double gk[22];
+    bool any = false;
+    for (int i = 0; i < 22; ++i) { gk[i] = g[i]; any |= g[i] != 0.f; }
+    if (!any) return;   // no fragment of this primitive was composited
+
+    const float *cf = prm.centers + 3 * p;
+    double c[3] = {cf[0], cf[1], cf[2]};
+    double s[3];
+    bool clamped[3];
+    activate(prm.raw_scales + 3 * p, prm.raw_signs + 3 * p, s, clamped);
+    double alpha = 1.0 / (1.0 + exp(-(double)prm.raw_opacity[p]));
+    double R[9], qn[4], qnorm;
+    quat_rot(prm.quats + 4 * p, R, qn, qnorm);
+    bool planar = fabs(s[2]) < 1e-6;
+    double w1 = sign0(s[0]) / (s[0] * s[0]);
+    double w2 = sign0(s[1]) / (s[1] * s[1]);
+
+    // w_k = sign(s_k)/s_k^2, iw3 = 1/s3  (rasterizer.py:294-297)
+    double gs0 = gk[KG_S + 0] + gk[KG_W + 0] * (-2.0 * w1 / s[0]);
+    double gs1 = gk[KG_S + 1] + gk[KG_W + 1] * (-2.0 * w2 / s[1]);
+    double gs2 = gk[KG_S + 2] + (planar ? 0.0 : gk[KG_W + 2] * (-1.0 / (s[2] * s[2])));
+    double gsv[3] = {gs0, gs1, gs2};
+    for (int k = 0; k < 3; ++k) {
+        double th = tanh((double)prm.raw_signs[3 * p + k]);
+        double ex = exp((double)prm.raw_scales[3 * p + k]);
+        out.raw_scales[3 * p + k] += clamped[k] ? 0.f : (float)(gsv[k] * (th * ex));
+        out.raw_signs[3 * p + k] += clamped[k] ? 0.f : (float)(gsv[k] * ((1.0 - th * th) * ex));
+    }
+    out.raw_opacity[p] += (float)(gk[KG_ALPHA] * alpha * (1.0 - alpha));
+
+    // rotation: g_R[a][b] = sum_k Rwc[k][a] g_M[b][k] + (eye - c)_a g_ohat_b
+    double e[3] = {cam.eye[0] - c[0], cam.eye[1] - c[1], cam.eye[2] - c[2]};
+    double gR[9];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) {
+            double acc = 0.0;
+            for (int k = 0; k < 3; ++k) acc += cam.Rwc[3 * k + a] * gk[KG_M + 3 * b + k];
+            gR[3 * a + b] = acc + e[a] * gk[KG_OHAT + b];
+        }
+    // quat_rot_backward (model.py:90-110)
+    double w = qn[0], x = qn[1], y = qn[2], z = qn[3];
+    const double dW[9] = {0, -2 * z, 2 * y, 2 * z, 0, -2 * x, -2 * y, 2 * x, 0};
+    const double dX[9] = {0, 2 * y, 2 * z, 2 * y, -4 * x, -2 * w, 2 * z, 2 * w, -4 * x};
+    const double dY[9] = {-4 * y, 2 * x, 2 * w, 2 * x, 0, 2 * z, -2 * w, 2 * z, -4 * y};
+    const double dZ[9] = {-4 * z, -2 * w, 2 * x, 2 * w, -4 * z, 2 * y, 2 * x, 2 * y, 0};
+    double gu[4] = {0, 0, 0, 0};
+    for (int i = 0; i < 9; ++i) {
+        gu[0] += gR[i] * dW[i]; gu[1] += gR[i] * dX[i];
+        gu[2] += gR[i] * dY[i]; gu[3] += gR[i] * dZ[i];
+    }
+    double dq = gu[0] * qn[0] + gu[1] * qn[1] + gu[2] * qn[2] + gu[3] * qn[3];
+    for (int i = 0; i < 4; ++i) out.quats[4 * p + i] += (float)((gu[i] - qn[i] * dq) / qnorm);
+
+    // centres through ohat and the SH view direction
+    double gc[3];
+    for (int i = 0; i < 3; ++i)
+        gc[i] = -(R[3 * i + 0] * gk[KG_OHAT + 0] + R[3 * i + 1] * gk[KG_OHAT + 1] +
+                  R[3 * i + 2] * gk[KG_OHAT + 2]);
+    double v[3] = {c[0] - cam.eye[0], c[1] - cam.eye[1], c[2] - cam.eye[2]};
+    double dist = fmax(sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]), 1e-12);
+    double vd[3] = {v[0] / dist, v[1] / dist, v[2] / dist};
+    int K = prm.sh_coeffs;
+    double Y[16], J[16][3];
+    sh_basis(K, vd[0], vd[1], vd[2], Y);
+    sh_basis_jac(K, vd[0], vd[1], vd[2], J);
+    const float *shp = prm.sh + (size_t)p * 3 * K;
+    float *gsh = out.sh + (size_t)p * 3 * K;
+    double gdir[3] = {0, 0, 0};
+    for (int ch = 0; ch < 3; ++ch) {
+        double raw = 0.0;
+        for (int k = 0; k < K; ++k) raw += (double)shp[ch * K + k] * Y[k];
+        raw += 0.5;
+        double gcol = raw < 0 ? 0.0 : gk[KG_COLOR + ch];
+        if (gcol == 0.0) continue;
+        for (int k = 0; k < K; ++k) {
+            gsh[ch * K + k] += (float)(gcol * Y[k]);
+            for (int d = 0; d < 3; ++d) gdir[d] += gcol * shp[ch * K + k] * J[k][d];
+        }
+    }
+    double dd = gdir[0] * vd[0] + gdir[1] * vd[1] + gdir[2] * vd[2];
+    for (int i = 0; i < 3; ++i) gc[i] += (gdir[i] - vd[i] * dd) / dist;
+    for (int i = 0; i < 3; ++i) out.centers[3 * p + i] += (float)gc[i];
+
+    // screen-space centre gradient (rasterizer.py:323-333)
+    double X = c[0] * cam.Rwc[0] + c[1] * cam.Rwc[1] + c[2] * cam.Rwc[2] + cam.twc[0];
+    double Yc = c[0] * cam.Rwc[3] + c[1] * cam.Rwc[4] + c[2] * cam.Rwc[5] + cam.twc[1];
+    double Z = c[0] * cam.Rwc[6] + c[1] * cam.Rwc[7] + c[2] * cam.Rwc[8] + cam.twc[2];
+    double Zs = fabs(Z) < 1e-9 ? 1e-9 : Z;
+    double gu_s = 0.0, gv_s = 0.0;
+    for (int i = 0; i < 3; ++i) {
+        double Ju = cam.fx * (cam.Rwc[i] / Zs - X * cam.Rwc[6 + i] / (Zs * Zs));
+        double Jv = cam.fy * (cam.Rwc[3 + i] / Zs - Yc * cam.Rwc[6 + i] / (Zs * Zs));
+        gu_s += Ju * gc[i];
+        gv_s += Jv * gc[i];
+    }
+    out.screen_center[2 * p + 0] += (float)(gu_s * (2.0 / cam.W));
+    out.screen_center[2 * p + 1] += (float)(gv_s * (2.0 / cam.H));
+}
+
+// ------------------------------------------------------------- exports
+
+__global__ void export_prep_kernel(PrepView pv, int P, double *scales, double *alphas,
+                                   double *colors, int32_t *bbox, uint8_t *planar)
+{
+    int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    const Geo64 &g = pv.geo[p];
+    if (scales) for (int i = 0; i < 3; ++i) scales[3 * p + i] = g.sv[i];
+    if (alphas) alphas[p] = g.alpha;
+    if (colors) for (int i = 0; i < 3; ++i) colors[3 * p + i] = g.col[i];
+    if (bbox) {
+        int4 b = pv.bbox[p];
+        bbox[4 * p] = b.x; bbox[4 * p + 1] = b.y; bbox[4 * p + 2] = b.z; bbox[4 * p + 3] = b.w;
+    }
+    if (planar) planar[p] = g.planar != 0.0 ? 1 : 0;
+}
+
+}  // namespace qgs

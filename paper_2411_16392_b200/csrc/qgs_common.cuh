@@ -1,0 +1,388 @@
+// Shared device code for the sm_100a QGS tile rasterizer.
+//
+// Per-primitive state lives in one caller-owned "prep" buffer:
+//   Geo64[P]   float64 geometry (feeds screen boxes and tile sort keys; these
+//              integer/ordering outputs must be bit-identical to the reference)
+//   PrimRec[P] 128-byte fp32 record consumed by the raster kernels
+//   int4[P]    inclusive pixel box (umin, umax, vmin, vmax); empty = (0,-1,0,-1)
+//   int32[P]   tiles covered;  int64[P+1] exclusive scan = pair offsets
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/qgs_b200.h"
+
+namespace qgs {
+
+constexpr int TILE = 16;            // bounds.py:19
+constexpr int RING = 8;             // raster_kernels.py:26 BUFFER_SIZE
+constexpr int KG = QGS_KG_STRIDE;   // kernel-gradient floats per primitive
+constexpr int AUX = QGS_AUX_PLANES;
+
+// kernel-gradient slots (raster_kernels.py:29-37 with Nmat and lambda folded)
+enum { KG_OHAT = 0, KG_M = 3, KG_W = 12, KG_S = 15, KG_ALPHA = 18, KG_COLOR = 19 };
+// fp64 aux planes written by the forward for the backward
+enum { AX_C0 = 0, AX_A = 3, AX_D = 4, AX_D2 = 5, AX_N0 = 6, AX_K = 9, AX_DIST = 10, AX_T = 11 };
+enum { BR_QUAD = 0, BR_LINEAR = 1, BR_PLANAR = 2 };
+
+struct Geo64 {            // 32 doubles, 256 B
+    double ohat[3];
+    double M[9];          // local-from-camera rotation R^T R_cw (row-major)
+    double wv[3];         // w1, w2, iw3
+    double sv[3];         // activated signed scales
+    double vert_u, vert_v, dist;
+    double alpha;
+    double col[3];
+    double planar;        // 1.0 / 0.0
+    double pad[6];
+};
+
+struct __align__(16) PrimRec {   // 32 floats, 128 B
+    float M[9];           // 0-8
+    float ox, oy, oz;     // 9-11
+    float w1, w2, iw3;    // 12-14
+    float s1, s2, s3;     // 15-17
+    float lam1, lam2;     // 18-19
+    float alpha;          // 20
+    float C;              // 21 ray-quadric constant term, rounded once from fp64
+    float col[3];         // 22-24
+    uint32_t bb_u;        // 25 umin | umax << 16
+    uint32_t bb_v;        // 26 vmin | vmax << 16
+    uint32_t flags;       // 27 bit0 planar
+    float s12;            // 28 |s1 s2|
+    float ell9;           // 29 9 (s1 s2)^2
+    float pad[2];
+};
+static_assert(sizeof(PrimRec) == 128, "PrimRec must be 128 B");
+static_assert(sizeof(Geo64) == 256, "Geo64 must be 256 B");
+
+struct PrepView {
+    Geo64 *geo;
+    PrimRec *rec;
+    int4 *bbox;
+    int32_t *ntiles;
+    int64_t *pair_off;    // P+1
+};
+
+__host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+__host__ __device__ inline PrepView prep_view(void *base, int32_t P)
+{
+    char *b = static_cast<char *>(base);
+    PrepView v;
+    size_t o = 0;
+    v.geo = reinterpret_cast<Geo64 *>(b + o);      o += align256(sizeof(Geo64) * (size_t)P);
+    v.rec = reinterpret_cast<PrimRec *>(b + o);    o += align256(sizeof(PrimRec) * (size_t)P);
+    v.bbox = reinterpret_cast<int4 *>(b + o);      o += align256(sizeof(int4) * (size_t)P);
+    v.ntiles = reinterpret_cast<int32_t *>(b + o); o += align256(sizeof(int32_t) * (size_t)P);
+    v.pair_off = reinterpret_cast<int64_t *>(b + o);
+    return v;
+}
+
+__host__ __device__ inline size_t prep_bytes(int32_t P)
+{
+    return align256(sizeof(Geo64) * (size_t)P) + align256(sizeof(PrimRec) * (size_t)P) +
+           align256(sizeof(int4) * (size_t)P) + align256(sizeof(int32_t) * (size_t)P) +
+           align256(sizeof(int64_t) * ((size_t)P + 1)) + 256;
+}
+
+// Camera / settings as kernel arguments (by value).
+struct CamK {
+    double fx, fy, cx, cy;
+    int W, H, tiles_x, tiles_y;
+    double Rwc[9], twc[3], eye[3];
+};
+
+struct SetK {
+    double bg[3];
+    double t_clip, alpha_floor, alpha_clamp, t_term;
+    int resort, euclid;
+};
+
+inline CamK make_camk(const qgs_camera &c)
+{
+    CamK k;
+    k.fx = c.fx; k.fy = c.fy; k.cx = c.cx; k.cy = c.cy;
+    k.W = c.width; k.H = c.height;
+    k.tiles_x = (c.width + TILE - 1) / TILE;
+    k.tiles_y = (c.height + TILE - 1) / TILE;
+    for (int i = 0; i < 9; ++i) k.Rwc[i] = c.R_wc[i];
+    for (int i = 0; i < 3; ++i) { k.twc[i] = c.t_wc[i]; k.eye[i] = c.center[i]; }
+    return k;
+}
+
+inline SetK make_setk(const qgs_settings &s)
+{
+    SetK k;
+    for (int i = 0; i < 3; ++i) k.bg[i] = s.background[i];
+    k.t_clip = s.t_near_clip; k.alpha_floor = s.alpha_floor;
+    k.alpha_clamp = s.alpha_clamp; k.t_term = s.t_term;
+    k.resort = s.resort; k.euclid = s.euclidean_density;
+    return k;
+}
+
+// ----------------------------------------------------------------- fp64
+// These follow the reference operation order exactly (intersect.py:31-115,
+// geodesic.py:23-31,51-59).  Translation units that use them are compiled
+// with -fmad=false so nothing is contracted into an FMA.
+
+__device__ inline double arc_length64(double a, double rho)
+{
+    double u = 2.0 * a * rho;
+    if (fabs(u) < 1e-3) {
+        double u2 = u * u;
+        return rho * (1.0 + u2 / 6.0 - u2 * u2 / 40.0);
+    }
+    double r = sqrt(u * u + 1.0);
+    return (log(r + u) + u * r) / (4.0 * a);
+}
+
+__device__ inline double sigma_dir64(double s1, double s2, double c, double s)
+{
+    double m = (s2 * c) * (s2 * c) + (s1 * s) * (s1 * s);
+    return fabs(s1 * s2) / sqrt(m);
+}
+
+// fragment_geometry restricted to what the sort key needs: (valid, t).
+__device__ inline bool hit_depth64(const double *wv, const double *sv, const double *oh,
+                                   double dx, double dy, double dz, bool planar, bool euclid,
+                                   double t_clip, double &t_out)
+{
+    if (planar) {
+        if (fabs(dz) < 1e-12) return false;
+        double t = -oh[2] / dz;
+        if (t <= t_clip) return false;
+        double x = oh[0] + t * dx, y = oh[1] + t * dy;
+        double rho = sqrt(x * x + y * y), c = 1.0, s = 0.0;
+        if (rho > 1e-12) { c = x / rho; s = y / rho; }
+        double sig = sigma_dir64(sv[0], sv[1], c, s);
+        if (rho > 3.0 * sig) return false;
+        t_out = t;
+        return true;
+    }
+    double w1 = wv[0], w2 = wv[1], iw3 = wv[2], ox = oh[0], oy = oh[1], oz = oh[2];
+    double A = w1 * dx * dx + w2 * dy * dy;
+    double B = 2.0 * (w1 * ox * dx + w2 * oy * dy) - iw3 * dz;
+    double C = w1 * ox * ox + w2 * oy * oy - iw3 * oz;
+    double r0 = 0.0, r1 = 0.0;
+    int cnt;
+    if (fabs(A) < 1e-6) {
+        if (fabs(B) < 1e-12) cnt = 0;
+        else { cnt = 1; r0 = -C / B; }
+    } else {
+        double disc = B * B - 4.0 * A * C;
+        if (disc < 0.0) cnt = 0;
+        else {
+            double sa = A > 0.0 ? 1.0 : -1.0;
+            double sq = sqrt(disc);
+            r0 = (-B - sa * sq) / (2.0 * A);
+            r1 = (-B + sa * sq) / (2.0 * A);
+            cnt = disc == 0.0 ? 1 : 2;
+        }
+    }
+    double s1 = sv[0], s2 = sv[1], s3 = sv[2], s1s2 = s1 * s2;
+    for (int k = 0; k < cnt; ++k) {
+        double t = k == 0 ? r0 : r1;
+        if (t <= t_clip) continue;
+        double x = ox + t * dx, y = oy + t * dy;
+        double m = (s2 * x) * (s2 * x) + (s1 * y) * (s1 * y);
+        if (m > 9.0 * s1s2 * s1s2) continue;
+        double rho = sqrt(x * x + y * y), c = 1.0, s = 0.0;
+        if (rho > 1e-12) { c = x / rho; s = y / rho; }
+        double a = s3 * (w1 * c * c + w2 * s * s);
+        double l = euclid ? rho : arc_length64(a, rho);
+        double sig = sigma_dir64(s1, s2, c, s);
+        if (l <= 3.0 * sig) { t_out = t; return true; }
+    }
+    return false;
+}
+
+// tile_sort_depths (raster_kernels.py:684-716) for one (tile, primitive).
+__device__ inline double tile_key64(const double *ohat, const double *M, const double *wv,
+                                    const double *sv, bool planar, double vu, double vv,
+                                    double dist, int tile, const CamK &cam, bool euclid,
+                                    double t_clip)
+{
+    int ty = tile / cam.tiles_x, tx = tile - ty * cam.tiles_x;
+    long long ulo = tx * TILE, uhi = min(cam.W, tx * TILE + TILE) - 1;
+    long long vlo = ty * TILE, vhi = min(cam.H, ty * TILE + TILE) - 1;
+    long long iu = (long long)floor(vu), iv = (long long)floor(vv);
+    iu = iu < ulo ? ulo : (iu > uhi ? uhi : iu);
+    iv = iv < vlo ? vlo : (iv > vhi ? vhi : iv);
+    double u = (double)iu, v = (double)iv;
+    double ddx = (u + 0.5 - cam.cx) / cam.fx, ddy = (v + 0.5 - cam.cy) / cam.fy;
+    double nrm = sqrt(ddx * ddx + ddy * ddy + 1.0);
+    double cx = ddx / nrm, cy = ddy / nrm, cz = 1.0 / nrm;
+    double dx = M[0] * cx + M[1] * cy + M[2] * cz;
+    double dy = M[3] * cx + M[4] * cy + M[5] * cz;
+    double dz = M[6] * cx + M[7] * cy + M[8] * cz;
+    double t;
+    if (hit_depth64(wv, sv, ohat, dx, dy, dz, planar, euclid, t_clip, t)) return t;
+    return dist;
+}
+
+__device__ inline double tile_key_geo(const Geo64 &g, int tile, const CamK &cam, bool euclid,
+                                      double t_clip)
+{
+    return tile_key64(g.ohat, g.M, g.wv, g.sv, g.planar != 0.0, g.vert_u, g.vert_v, g.dist,
+                      tile, cam, euclid, t_clip);
+}
+
+// ----------------------------------------------------------------- fp32
+// Raster-side shading.  Same selection rule as fragment_geometry
+// (intersect.py:58-115) evaluated in fp32 with cancellation-free roots and a
+// longer arc-length series.
+
+struct Hit {
+    float t, x, y, rho, cth, sth, a, l, sig, G, dhx, dhy, dhz;
+    int branch;
+};
+
+// arc length of z = a r^2 over [0, rho]; series below |u| = 0.3 (error < 1e-8)
+__device__ __forceinline__ float arc32(float a, float rho)
+{
+    float u = 2.f * a * rho;
+    if (fabsf(u) < 0.3f) {
+        float u2 = u * u;
+        return rho * (1.f + u2 * (1.f / 6.f + u2 * (-1.f / 40.f + u2 * (1.f / 112.f - u2 * (5.f / 1152.f)))));
+    }
+    float r = sqrtf(fmaf(u, u, 1.f));
+    float as = copysignf(logf(fabsf(u) + r), u);
+    return (as + u * r) / (4.f * a);
+}
+
+// (dl/da, dl/drho) on the same branch
+__device__ __forceinline__ void arc32_grad(float a, float rho, float l, float &dla, float &dlr)
+{
+    float u = 2.f * a * rho;
+    if (fabsf(u) < 0.3f) {
+        float u2 = u * u;
+        // d/du of the series times d u/d a = 2 rho, etc.
+        float fp = u * (1.f / 3.f + u2 * (-1.f / 10.f + u2 * (3.f / 56.f - u2 * (5.f / 144.f))));
+        dla = 2.f * rho * rho * fp;
+        dlr = 1.f + u2 * (0.5f + u2 * (-0.125f + u2 * (1.f / 16.f - u2 * (5.f / 128.f))));
+        return;
+    }
+    float r = sqrtf(fmaf(u, u, 1.f));
+    dla = (rho * r - l) / a;
+    dlr = r;
+}
+
+__device__ __forceinline__ void local_dir32(const PrimRec &r, float dx, float dy, float dz,
+                                            float &hx, float &hy, float &hz)
+{
+    hx = fmaf(r.M[0], dx, fmaf(r.M[1], dy, r.M[2] * dz));
+    hy = fmaf(r.M[3], dx, fmaf(r.M[4], dy, r.M[5] * dz));
+    hz = fmaf(r.M[6], dx, fmaf(r.M[7], dy, r.M[8] * dz));
+}
+
+// test one candidate depth; fills h on acceptance
+__device__ __forceinline__ bool accept_root(const PrimRec &r, float t, float hx, float hy,
+                                            bool euclid, float t_clip, Hit &h)
+{
+    if (!(t > t_clip)) return false;
+    float x = fmaf(t, hx, r.ox), y = fmaf(t, hy, r.oy);
+    float ex = r.s2 * x, ey = r.s1 * y;
+    float m = fmaf(ex, ex, ey * ey);
+    if (m > r.ell9) return false;
+    float rho = sqrtf(fmaf(x, x, y * y));
+    float c = 1.f, s = 0.f;
+    if (rho > 1e-12f) { float ir = 1.f / rho; c = x * ir; s = y * ir; }
+    float a = r.s3 * fmaf(r.w1 * c, c, r.w2 * s * s);
+    float l = euclid ? rho : arc32(a, rho);
+    float sc = r.s2 * c, ss = r.s1 * s;
+    float sig = r.s12 * rsqrtf(fmaf(sc, sc, ss * ss));
+    if (!(l <= 3.f * sig)) return false;
+    h.t = t; h.x = x; h.y = y; h.rho = rho; h.cth = c; h.sth = s; h.a = a; h.l = l; h.sig = sig;
+    h.G = expf(-(l * l) / (2.f * sig * sig));
+    return true;
+}
+
+// ray/primitive hit with the near-then-far rule; d is the camera-frame ray
+__device__ __forceinline__ bool hit32(const PrimRec &r, float dx, float dy, float dz,
+                                      bool euclid, float t_clip, Hit &h)
+{
+    float hx, hy, hz;
+    local_dir32(r, dx, dy, dz, hx, hy, hz);
+    h.dhx = hx; h.dhy = hy; h.dhz = hz;
+    if (r.flags & 1u) {
+        h.branch = BR_PLANAR;
+        if (fabsf(hz) < 1e-12f) return false;
+        float t = -r.oz / hz;
+        if (!(t > t_clip)) return false;
+        float x = fmaf(t, hx, r.ox), y = fmaf(t, hy, r.oy);
+        float rho = sqrtf(fmaf(x, x, y * y));
+        float c = 1.f, s = 0.f;
+        if (rho > 1e-12f) { float ir = 1.f / rho; c = x * ir; s = y * ir; }
+        float sc = r.s2 * c, ss = r.s1 * s;
+        float sig = r.s12 * rsqrtf(fmaf(sc, sc, ss * ss));
+        if (rho > 3.f * sig) return false;
+        h.t = t; h.x = x; h.y = y; h.rho = rho; h.cth = c; h.sth = s; h.a = 0.f; h.l = rho;
+        h.sig = sig;
+        h.G = expf(-(rho * rho) / (2.f * sig * sig));
+        return true;
+    }
+    float A = fmaf(r.w1 * hx, hx, r.w2 * hy * hy);
+    float B = 2.f * fmaf(r.w1 * r.ox, hx, r.w2 * r.oy * hy) - r.iw3 * hz;
+    float C = r.C;
+    if (fabsf(A) < 1e-6f) {
+        h.branch = BR_LINEAR;
+        if (fabsf(B) < 1e-12f) return false;
+        return accept_root(r, -C / B, hx, hy, euclid, t_clip, h);
+    }
+    h.branch = BR_QUAD;
+    float disc = fmaf(B, B, -4.f * A * C);
+    if (disc < 0.f) return false;
+    float sq = sqrtf(disc);
+    float q = -0.5f * (B + copysignf(sq, B));
+    float ra = q / A, rb = (q != 0.f) ? C / q : ra;
+    float tn = fminf(ra, rb), tf = fmaxf(ra, rb);
+    if (accept_root(r, tn, hx, hy, euclid, t_clip, h)) return true;
+    if (disc == 0.f) return false;
+    return accept_root(r, tf, hx, hy, euclid, t_clip, h);
+}
+
+// camera-frame camera-facing normal and Gaussian curvature at a hit
+__device__ __forceinline__ void normal_curv32(const PrimRec &r, const Hit &h, float dx, float dy,
+                                              float dz, float nl[3], float nc[3], float &K,
+                                              float &inrm, float &flip)
+{
+    if (h.branch == BR_PLANAR) {
+        nl[0] = 0.f; nl[1] = 0.f; nl[2] = -1.f; K = 0.f; inrm = 1.f;
+    } else {
+        float nx = 2.f * r.w1 * h.x, ny = 2.f * r.w2 * h.y, nz = -r.iw3;
+        inrm = rsqrtf(fmaf(nx, nx, fmaf(ny, ny, nz * nz)));
+        nl[0] = nx * inrm; nl[1] = ny * inrm; nl[2] = nz * inrm;
+        float l1x = r.lam1 * h.x, l2y = r.lam2 * h.y;
+        float den = 1.f + 4.f * fmaf(l1x, l1x, l2y * l2y);
+        K = 4.f * r.lam1 * r.lam2 / (den * den);
+    }
+    // Nmat = M^T (camera-from-local)
+    nc[0] = fmaf(r.M[0], nl[0], fmaf(r.M[3], nl[1], r.M[6] * nl[2]));
+    nc[1] = fmaf(r.M[1], nl[0], fmaf(r.M[4], nl[1], r.M[7] * nl[2]));
+    nc[2] = fmaf(r.M[2], nl[0], fmaf(r.M[5], nl[1], r.M[8] * nl[2]));
+    flip = 1.f;
+    if (fmaf(nc[0], dx, fmaf(nc[1], dy, nc[2] * dz)) > 0.f) {
+        flip = -1.f; nc[0] = -nc[0]; nc[1] = -nc[1]; nc[2] = -nc[2];
+    }
+}
+
+// camera-frame unit ray of pixel (u, v): fp64, rounded once (cameras.py:53-59)
+__device__ __forceinline__ void pixel_dir(const CamK &cam, int u, int v, float &dx, float &dy,
+                                          float &dz)
+{
+    double a = ((double)u + 0.5 - cam.cx) / cam.fx;
+    double b = ((double)v + 0.5 - cam.cy) / cam.fy;
+    double n = sqrt(a * a + b * b + 1.0);
+    dx = (float)(a / n); dy = (float)(b / n); dz = (float)(1.0 / n);
+}
+
+__device__ __forceinline__ bool in_box(const PrimRec &r, int u, int v)
+{
+    int umin = (int)(r.bb_u & 0xffffu), umax = (int)(r.bb_u >> 16);
+    int vmin = (int)(r.bb_v & 0xffffu), vmax = (int)(r.bb_v >> 16);
+    return u >= umin && u <= umax && v >= vmin && v <= vmax;
+}
+
+}  // namespace qgs

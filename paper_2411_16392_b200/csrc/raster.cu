@@ -1,0 +1,566 @@
+// K5 forward and K6 backward tile raster kernels.
+//
+// Reference: raster_kernels.py:83-286 (forward_kernel), :289-502
+// (_grad_fragment), :505-670 (backward_kernel), :673-681 (merge).
+//
+// One CTA per 16x16 tile, one thread per pixel; each warp owns an 8x4 pixel
+// block so that lanes see spatially coherent fragment streams.  The tile's
+// depth-sorted primitive list is streamed in batches of 256 fp32 records
+// staged in shared memory (8 lanes per 128-byte record, fully coalesced).
+// Per pixel, accepted fragments go through the 8-entry min-depth ring
+// (depth + primitive id in registers, statically indexed); an emitted
+// fragment is re-shaded from its record, so the ring costs 16 registers.
+//
+// Precision: shading is fp32 (cancellation-free roots, long arc-length
+// series); transmittance, blend weights and the eleven blend sums are fp64,
+// which keeps T_i, w_i and the backward's suffix sums (vtot - prefix, the
+// front-to-back rewrite of raster_kernels.py:340) accurate to ~1e-15 instead
+// of the ~1e-7 * |vtot| an fp32 prefix would give.
+//
+// The backward replays exactly the same stream (same inline functions, same
+// decisions) and reduces each emitted fragment's 22 kernel-level gradient
+// slots across the warp's lanes that emitted the same primitive (match_any +
+// shared-memory transpose) before one float atomic per slot.
+#include "qgs_common.cuh"
+
+namespace qgs {
+
+constexpr int RT = 256;       // threads per tile CTA
+constexpr int BATCH = 256;    // records staged per batch
+constexpr unsigned FULL = 0xffffffffu;
+
+struct RasterSmem {
+    PrimRec rec[BATCH];
+    int prim[BATCH];
+    float red[RT / 32][32][KG];
+    int viol;
+};
+
+__device__ __forceinline__ void pixel_of(int tile, int tiles_x, int &u, int &v)
+{
+    int ty = tile / tiles_x, tx = tile - ty * tiles_x;
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    u = tx * TILE + (w & 1) * 8 + (lane & 7);
+    v = ty * TILE + (w >> 1) * 4 + (lane >> 3);
+}
+
+// stage records [b0, b0+nb) of the tile list into shared memory
+__device__ __forceinline__ void load_batch(RasterSmem &sm, const PrimRec *__restrict__ recs,
+                                           const int32_t *__restrict__ list, int b0, int nb)
+{
+    for (int j = threadIdx.x; j < nb; j += RT) sm.prim[j] = list[b0 + j];
+    __syncthreads();
+    // 8 lanes per record, 16 B each: a warp moves 4 whole 128 B records per step
+    const float4 *src = reinterpret_cast<const float4 *>(recs);
+    float4 *dst = reinterpret_cast<float4 *>(sm.rec);
+    for (int k = threadIdx.x; k < nb * 8; k += RT) {
+        int j = k >> 3, q = k & 7;
+        dst[j * 8 + q] = __ldg(src + (size_t)sm.prim[j] * 8 + q);
+    }
+    __syncthreads();
+}
+
+struct Ring {
+    float t[RING];
+    int p[RING];
+    int n;
+};
+
+// push an accepted fragment; returns true with (et, ep) when one is emitted
+// (raster_kernels.py:159-226: first minimum, strict <, emit incoming if nearer)
+__device__ __forceinline__ bool ring_push(Ring &R, float t, int prim, float &et, int &ep)
+{
+    if (R.n < RING) {
+#pragma unroll
+        for (int k = 0; k < RING; ++k)
+            if (k == R.n) { R.t[k] = t; R.p[k] = prim; }
+        R.n++;
+        return false;
+    }
+    float m = R.t[0];
+    int jm = 0;
+#pragma unroll
+    for (int k = 1; k < RING; ++k)
+        if (R.t[k] < m) { m = R.t[k]; jm = k; }
+    if (t < m) { et = t; ep = prim; return true; }
+#pragma unroll
+    for (int k = 0; k < RING; ++k)
+        if (k == jm) { et = R.t[k]; ep = R.p[k]; R.t[k] = t; R.p[k] = prim; }
+    return true;
+}
+
+// drain one entry (raster_kernels.py:227-270: first minimum, swap with last)
+__device__ __forceinline__ void ring_pop(Ring &R, float &et, int &ep)
+{
+    float m = R.t[0];
+    int jm = 0;
+#pragma unroll
+    for (int k = 1; k < RING; ++k)
+        if (k < R.n && R.t[k] < m) { m = R.t[k]; jm = k; }
+    R.n--;
+    float tl = 0.f;
+    int pl = 0;
+#pragma unroll
+    for (int k = 0; k < RING; ++k)
+        if (k == R.n) { tl = R.t[k]; pl = R.p[k]; }
+#pragma unroll
+    for (int k = 0; k < RING; ++k)
+        if (k == jm) { et = R.t[k]; ep = R.p[k]; R.t[k] = tl; R.p[k] = pl; }
+}
+
+struct Cfg {
+    float t_clip, alpha_floor, alpha_clamp;
+    double alpha_clamp64, t_term;
+    bool euclid, resort;
+};
+
+__device__ __forceinline__ Cfg make_cfg(const SetK &st)
+{
+    Cfg c;
+    c.t_clip = (float)st.t_clip;
+    c.alpha_floor = (float)st.alpha_floor;
+    c.alpha_clamp = (float)st.alpha_clamp;
+    c.alpha_clamp64 = st.alpha_clamp;
+    c.t_term = st.t_term;
+    c.euclid = st.euclid != 0;
+    c.resort = st.resort != 0;
+    return c;
+}
+
+// candidate test shared by both passes (raster_kernels.py:121-130, 58-63)
+__device__ __forceinline__ bool accept(const PrimRec &r, int u, int v, float dx, float dy, float dz,
+                                       const Cfg &c, float &t)
+{
+    if (!in_box(r, u, v)) return false;
+    Hit h;
+    if (!hit32(r, dx, dy, dz, c.euclid, c.t_clip, h)) return false;
+    if (r.alpha * h.G < c.alpha_floor) return false;
+    t = h.t;
+    return true;
+}
+
+// candidate step: accept + ring; returns whether a fragment is emitted
+__device__ __forceinline__ bool stream_step(const PrimRec &r, int prim, int u, int v, float dx,
+                                            float dy, float dz, const Cfg &c, Ring &R, float &et,
+                                            int &ep)
+{
+    float t;
+    if (!accept(r, u, v, dx, dy, dz, c, t)) return false;
+    if (!c.resort) { et = t; ep = prim; return true; }
+    return ring_push(R, t, prim, et, ep);
+}
+
+struct Frag {
+    Hit h;
+    float abar;
+    double abar64;
+    bool clamped;
+    float nl[3], nc[3], K, inrm, flip;
+};
+
+// re-shade an emitted fragment (raster_kernels.py:40-80)
+__device__ __forceinline__ void shade_full(const PrimRec &r, float dx, float dy, float dz,
+                                           const Cfg &c, Frag &f)
+{
+    hit32(r, dx, dy, dz, c.euclid, c.t_clip, f.h);
+    float abar = r.alpha * f.h.G;
+    f.clamped = abar > c.alpha_clamp;
+    f.abar = f.clamped ? c.alpha_clamp : abar;
+    f.abar64 = f.clamped ? c.alpha_clamp64 : (double)abar;
+    normal_curv32(r, f.h, dx, dy, dz, f.nl, f.nc, f.K, f.inrm, f.flip);
+}
+
+// ================================================================ forward
+
+__global__ void __launch_bounds__(RT, 2)
+raster_fwd_kernel(const PrimRec *__restrict__ recs, const int32_t *__restrict__ tile_offsets,
+                  const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets out)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    RasterSmem &sm = *reinterpret_cast<RasterSmem *>(smem_raw);
+    const int tile = blockIdx.x;
+    int u, v;
+    pixel_of(tile, cam.tiles_x, u, v);
+    const bool inside = u < cam.W && v < cam.H;
+    const Cfg c = make_cfg(st);
+    float dx = 0.f, dy = 0.f, dz = 1.f;
+    if (inside) pixel_dir(cam, u, v, dx, dy, dz);
+    if (threadIdx.x == 0) sm.viol = 0;
+
+    double T = 1.0, ac0 = 0, ac1 = 0, ac2 = 0, aa = 0, ad = 0, ad2 = 0, an0 = 0, an1 = 0,
+           an2 = 0, ak = 0, adist = 0;
+    float median = 0.f, last_t = -3.0e38f;
+    int nfrag = 0, viol = 0;
+    Ring R;
+    R.n = 0;
+    bool alive = inside;
+
+    auto composite = [&](const PrimRec &r, float et) {
+        Frag f;
+        shade_full(r, dx, dy, dz, c, f);
+        if ((double)et < (double)last_t - 1e-12) viol++;
+        if (et > last_t) last_t = et;
+        double t = (double)et, w = f.abar64 * T;
+        ac0 += w * (double)r.col[0];
+        ac1 += w * (double)r.col[1];
+        ac2 += w * (double)r.col[2];
+        adist += w * (t * t * aa - 2.0 * t * ad + ad2);   // uses sums before this fragment
+        aa += w;
+        ad += w * t;
+        ad2 += w * t * t;
+        an0 += w * (double)f.nc[0];
+        an1 += w * (double)f.nc[1];
+        an2 += w * (double)f.nc[2];
+        ak += w * (double)f.K;
+        if (T > 0.5) median = et;
+        T *= 1.0 - f.abar64;
+        nfrag++;
+        if (T < c.t_term) alive = false;
+    };
+
+    const int start = tile_offsets[tile], end = tile_offsets[tile + 1];
+    for (int b0 = start; b0 < end; b0 += BATCH) {
+        if (__syncthreads_count(alive) == 0) break;
+        const int nb = min(BATCH, end - b0);
+        load_batch(sm, recs, tile_prims, b0, nb);
+        if (!alive) continue;
+        for (int j = 0; j < nb; ++j) {
+            float et;
+            int ep;
+            if (stream_step(sm.rec[j], sm.prim[j], u, v, dx, dy, dz, c, R, et, ep)) {
+                composite(ep == sm.prim[j] ? sm.rec[j] : recs[ep], et);
+                if (!alive) break;
+            }
+        }
+    }
+    while (alive && R.n > 0) {
+        float et;
+        int ep;
+        ring_pop(R, et, ep);
+        composite(recs[ep], et);
+    }
+
+    if (inside) {
+        const int W = cam.W, npx = cam.W * cam.H, px = v * W + u;
+        out.color_raw[3 * px + 0] = (float)ac0;
+        out.color_raw[3 * px + 1] = (float)ac1;
+        out.color_raw[3 * px + 2] = (float)ac2;
+        out.color[3 * px + 0] = (float)(ac0 + T * st.bg[0]);
+        out.color[3 * px + 1] = (float)(ac1 + T * st.bg[1]);
+        out.color[3 * px + 2] = (float)(ac2 + T * st.bg[2]);
+        out.alpha[px] = (float)aa;
+        out.depth[px] = (float)ad;
+        out.depth_sq[px] = (float)ad2;
+        out.depth_median[px] = median;
+        out.normal[3 * px + 0] = (float)an0;
+        out.normal[3 * px + 1] = (float)an1;
+        out.normal[3 * px + 2] = (float)an2;
+        out.curvature[px] = (float)ak;
+        out.distortion[px] = (float)adist;
+        out.transmittance[px] = (float)T;
+        out.n_fragments[px] = nfrag;
+        if (out.aux) {
+            double *a = out.aux;
+            a[(AX_C0 + 0) * (size_t)npx + px] = ac0;
+            a[(AX_C0 + 1) * (size_t)npx + px] = ac1;
+            a[(AX_C0 + 2) * (size_t)npx + px] = ac2;
+            a[AX_A * (size_t)npx + px] = aa;
+            a[AX_D * (size_t)npx + px] = ad;
+            a[AX_D2 * (size_t)npx + px] = ad2;
+            a[(AX_N0 + 0) * (size_t)npx + px] = an0;
+            a[(AX_N0 + 1) * (size_t)npx + px] = an1;
+            a[(AX_N0 + 2) * (size_t)npx + px] = an2;
+            a[AX_K * (size_t)npx + px] = ak;
+            a[AX_DIST * (size_t)npx + px] = adist;
+            a[AX_T * (size_t)npx + px] = T;
+        }
+    }
+    __syncthreads();
+    if (viol) atomicAdd(&sm.viol, viol);
+    __syncthreads();
+    if (threadIdx.x == 0 && out.violations) out.violations[tile] = sm.viol;
+}
+
+// =============================================================== backward
+
+struct Up {
+    float c0, c1, c2, a, d, n0, n1, n2, k, dist;
+};
+
+// _grad_fragment (raster_kernels.py:289-502) for one emitted fragment, fp32,
+// with Nmat^T folded into the M slots and lambda into the s / w slots.
+__device__ __forceinline__ void frag_grad(const PrimRec &r, const Frag &f, float dx, float dy,
+                                          float dz, float w, float g_abar, float tdev,
+                                          const Up &up, bool euclid, float g[KG])
+{
+    const Hit &h = f.h;
+    const float t = h.t, x = h.x, y = h.y, rho = h.rho, cth = h.cth, sth = h.sth;
+    g[KG_COLOR + 0] = w * up.c0;
+    g[KG_COLOR + 1] = w * up.c1;
+    g[KG_COLOR + 2] = w * up.c2;
+    float g_t = up.d * w + up.dist * 2.f * w * tdev;
+    float gcx = w * up.n0, gcy = w * up.n1, gcz = w * up.n2;
+    float g_K = w * up.k;
+    float g_G = 0.f;
+    g[KG_ALPHA] = 0.f;
+    if (!f.clamped) {
+        g[KG_ALPHA] = g_abar * h.G;
+        g_G = g_abar * r.alpha;
+    }
+    const float sig = h.sig, l = h.l;
+    const float isig2 = 1.f / (sig * sig);
+    const float g_l = g_G * h.G * (-l * isig2);
+    const float g_sig = g_G * h.G * (l * l * isig2 / sig);
+    // sigma(s1, s2, cth, sth) (geodesic.py:62-71)
+    const float s1 = r.s1, s2 = r.s2, s3 = r.s3;
+    const float m = fmaf(s2 * cth, s2 * cth, (s1 * sth) * (s1 * sth));
+    const float im = 1.f / m;
+    g[KG_S + 0] = g_sig * sig * (1.f / s1 - s1 * sth * sth * im);
+    g[KG_S + 1] = g_sig * sig * (1.f / s2 - s2 * cth * cth * im);
+    float g_cth = g_sig * (-sig * s2 * s2 * cth * im);
+    float g_sth = g_sig * (-sig * s1 * s1 * sth * im);
+    float g_x = 0.f, g_y = 0.f, g_rho = 0.f, g_a = 0.f;
+    if (euclid || h.branch == BR_PLANAR) {
+        g_rho = g_l;
+    } else {
+        float dla, dlr;
+        arc32_grad(h.a, rho, l, dla, dlr);
+        g_a = g_l * dla;
+        g_rho = g_l * dlr;
+    }
+    float g_w1 = 0.f, g_w2 = 0.f, g_iw3 = 0.f;
+    float gM[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) gM[i] = 0.f;
+    if (h.branch != BR_PLANAR) {
+        const float w1 = r.w1, w2 = r.w2;
+        float gs3 = g_a * fmaf(w1 * cth, cth, w2 * sth * sth);
+        g_w1 = g_a * s3 * cth * cth;
+        g_w2 = g_a * s3 * sth * sth;
+        g_cth += g_a * 2.f * s3 * w1 * cth;
+        g_sth += g_a * 2.f * s3 * w2 * sth;
+        // curvature K(lam1, lam2, x, y) (surface.py:27-32)
+        const float l1 = r.lam1, l2 = r.lam2;
+        const float den = 1.f + 4.f * (l1 * l1 * x * x + l2 * l2 * y * y);
+        const float iden = 1.f / den, iden2 = iden * iden, iden3 = iden2 * iden;
+        const float g_l1 = g_K * (4.f * l2 * iden2 - 64.f * l1 * l1 * l2 * x * x * iden3);
+        const float g_l2 = g_K * (4.f * l1 * iden2 - 64.f * l1 * l2 * l2 * y * y * iden3);
+        g_x += g_K * (-16.f * f.K * l1 * l1 * x * iden);
+        g_y += g_K * (-16.f * f.K * l2 * l2 * y * iden);
+        // lambda_k = s3 w_k folded in (rasterizer.py:290-293)
+        gs3 += g_l1 * w1 + g_l2 * w2;
+        g_w1 += g_l1 * s3;
+        g_w2 += g_l2 * s3;
+        g[KG_S + 2] = gs3;
+        // camera normal nc = flip * Nmat nl, Nmat = M^T; g_Nmat[i][j] -> g_M[j][i]
+        const float fl = f.flip;
+        const float g_nlx = fl * fmaf(r.M[0], gcx, fmaf(r.M[1], gcy, r.M[2] * gcz));
+        const float g_nly = fl * fmaf(r.M[3], gcx, fmaf(r.M[4], gcy, r.M[5] * gcz));
+        const float g_nlz = fl * fmaf(r.M[6], gcx, fmaf(r.M[7], gcy, r.M[8] * gcz));
+        const float fgc[3] = {fl * gcx, fl * gcy, fl * gcz};
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) gM[3 * j + i] += fgc[i] * f.nl[j];
+        const float dot = fmaf(f.nl[0], g_nlx, fmaf(f.nl[1], g_nly, f.nl[2] * g_nlz));
+        const float g_ntx = (g_nlx - f.nl[0] * dot) * f.inrm;
+        const float g_nty = (g_nly - f.nl[1] * dot) * f.inrm;
+        const float g_ntz = (g_nlz - f.nl[2] * dot) * f.inrm;
+        g_w1 += 2.f * x * g_ntx;
+        g_x += 2.f * w1 * g_ntx;
+        g_w2 += 2.f * y * g_nty;
+        g_y += 2.f * w2 * g_nty;
+        g_iw3 += -g_ntz;
+    } else {
+        g[KG_S + 2] = 0.f;
+        const float fl = f.flip;
+        gM[6 + 0] += -fl * gcx;
+        gM[6 + 1] += -fl * gcy;
+        gM[6 + 2] += -fl * gcz;
+    }
+    // polar coordinates of the hit
+    if (rho > 1e-12f) {
+        const float ir = 1.f / rho;
+        g_x += (g_cth * sth * sth - g_sth * cth * sth) * ir;
+        g_y += (-g_cth * cth * sth + g_sth * cth * cth) * ir;
+    }
+    g_x += g_rho * cth;
+    g_y += g_rho * sth;
+    // hit point x = ohat + t dhat
+    const float hx = h.dhx, hy = h.dhy, hz = h.dhz;
+    const float g_tt = g_t + g_x * hx + g_y * hy;
+    float g_o0 = g_x, g_o1 = g_y, g_o2 = 0.f;
+    float g_d0 = g_x * t, g_d1 = g_y * t, g_d2 = 0.f;
+    const float ox = r.ox, oy = r.oy, oz = r.oz;
+    if (h.branch == BR_PLANAR) {
+        g_o2 += -g_tt / hz;
+        g_d2 += g_tt * oz / (hz * hz);
+    } else {
+        const float w1 = r.w1, w2 = r.w2, iw3 = r.iw3;
+        const float A = fmaf(w1 * hx, hx, w2 * hy * hy);
+        const float B = 2.f * fmaf(w1 * ox, hx, w2 * oy * hy) - iw3 * hz;
+        float gA, gB, gC;
+        if (h.branch == BR_LINEAR) {
+            const float iB = 1.f / B;
+            gA = 0.f;
+            gB = -g_tt * t * iB;
+            gC = -g_tt * iB;
+        } else {
+            const float iq = 1.f / fmaf(2.f * A, t, B);
+            gA = -g_tt * t * t * iq;
+            gB = -g_tt * t * iq;
+            gC = -g_tt * iq;
+        }
+        g_w1 += gA * hx * hx + gB * 2.f * ox * hx + gC * ox * ox;
+        g_w2 += gA * hy * hy + gB * 2.f * oy * hy + gC * oy * oy;
+        g_iw3 += -gB * hz - gC * oz;
+        g_o0 += gB * 2.f * w1 * hx + gC * 2.f * w1 * ox;
+        g_o1 += gB * 2.f * w2 * hy + gC * 2.f * w2 * oy;
+        g_o2 += -gC * iw3;
+        g_d0 += gA * 2.f * w1 * hx + gB * 2.f * w1 * ox;
+        g_d1 += gA * 2.f * w2 * hy + gB * 2.f * w2 * oy;
+        g_d2 += -gB * iw3;
+    }
+    g[KG_W + 0] = g_w1;
+    g[KG_W + 1] = g_w2;
+    g[KG_W + 2] = g_iw3;
+    g[KG_OHAT + 0] = g_o0;
+    g[KG_OHAT + 1] = g_o1;
+    g[KG_OHAT + 2] = g_o2;
+    const float gd[3] = {g_d0, g_d1, g_d2}, dd[3] = {dx, dy, dz};
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) g[KG_M + 3 * i + j] = gM[3 * i + j] + gd[i] * dd[j];
+    g[22] = 0.f;
+    g[23] = 0.f;
+}
+
+// sum the slots of lanes that emitted the same primitive; one atomic per slot
+__device__ __forceinline__ void warp_accumulate(RasterSmem &sm, bool emit, int prim,
+                                                const float g[KG], float *__restrict__ kg)
+{
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (emit) {
+        float4 *dst = reinterpret_cast<float4 *>(sm.red[w][lane]);
+#pragma unroll
+        for (int q = 0; q < KG / 4; ++q) dst[q] = make_float4(g[4 * q], g[4 * q + 1], g[4 * q + 2], g[4 * q + 3]);
+    }
+    const unsigned key = emit ? (unsigned)prim : 0xffffffffu;
+    const unsigned peers = __match_any_sync(FULL, key);
+    unsigned leaders = __ballot_sync(FULL, emit && (peers & ((1u << lane) - 1u)) == 0);
+    __syncwarp();
+    while (leaders) {
+        const int ld = __ffs(leaders) - 1;
+        leaders &= leaders - 1;
+        const unsigned grp = __shfl_sync(FULL, peers, ld);
+        const int gp = __shfl_sync(FULL, prim, ld);
+        if (lane < 22) {
+            float s = 0.f;
+            for (unsigned mm = grp; mm; mm &= mm - 1) s += sm.red[w][__ffs(mm) - 1][lane];
+            atomicAdd(kg + (size_t)gp * KG + lane, s);
+        }
+    }
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(RT, 2)
+raster_bwd_kernel(const PrimRec *__restrict__ recs, const int32_t *__restrict__ tile_offsets,
+                  const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets fwd,
+                  qgs_upstream upst, float *__restrict__ kg)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    RasterSmem &sm = *reinterpret_cast<RasterSmem *>(smem_raw);
+    const int tile = blockIdx.x;
+    int u, v;
+    pixel_of(tile, cam.tiles_x, u, v);
+    const bool inside = u < cam.W && v < cam.H;
+    const Cfg c = make_cfg(st);
+    const int npx = cam.W * cam.H, px = inside ? v * cam.W + u : 0;
+
+    Up up = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    if (inside) {
+        if (upst.color) { up.c0 = upst.color[3 * px]; up.c1 = upst.color[3 * px + 1]; up.c2 = upst.color[3 * px + 2]; }
+        if (upst.alpha) up.a = upst.alpha[px];
+        if (upst.depth) up.d = upst.depth[px];
+        if (upst.normal) { up.n0 = upst.normal[3 * px]; up.n1 = upst.normal[3 * px + 1]; up.n2 = upst.normal[3 * px + 2]; }
+        if (upst.curvature) up.k = upst.curvature[px];
+        if (upst.distortion) up.dist = upst.distortion[px];
+    }
+    // raster_kernels.py:537-540: pixels without upstream contribute nothing
+    const bool has_up = up.c0 != 0.f || up.c1 != 0.f || up.c2 != 0.f || up.a != 0.f ||
+                        up.d != 0.f || up.n0 != 0.f || up.n1 != 0.f || up.n2 != 0.f ||
+                        up.k != 0.f || up.dist != 0.f;
+    // colour gradient reaches the composited colour incl. background
+    // (rasterizer.py:246-250): u_alpha -= u_color . bg
+    const double ua64 = (double)up.a - ((double)up.c0 * st.bg[0] + (double)up.c1 * st.bg[1] +
+                                        (double)up.c2 * st.bg[2]);
+    up.a = (float)ua64;
+
+    float dx = 0.f, dy = 0.f, dz = 1.f;
+    double F0 = 0, F1 = 0, F2 = 0, vtot = 0;
+    if (inside && has_up) {
+        pixel_dir(cam, u, v, dx, dy, dz);
+        const double *a = fwd.aux;
+        F0 = a[AX_A * (size_t)npx + px];
+        F1 = a[AX_D * (size_t)npx + px];
+        F2 = a[AX_D2 * (size_t)npx + px];
+        vtot = (double)up.c0 * a[(AX_C0 + 0) * (size_t)npx + px] +
+               (double)up.c1 * a[(AX_C0 + 1) * (size_t)npx + px] +
+               (double)up.c2 * a[(AX_C0 + 2) * (size_t)npx + px] + ua64 * F0 +
+               (double)up.d * F1 + (double)up.n0 * a[(AX_N0 + 0) * (size_t)npx + px] +
+               (double)up.n1 * a[(AX_N0 + 1) * (size_t)npx + px] +
+               (double)up.n2 * a[(AX_N0 + 2) * (size_t)npx + px] +
+               (double)up.k * a[AX_K * (size_t)npx + px] +
+               (double)up.dist * 2.0 * a[AX_DIST * (size_t)npx + px];
+    }
+    double T = 1.0, pref = 0.0;
+    Ring R;
+    R.n = 0;
+    bool alive = inside && has_up;
+
+    auto emit_grad = [&](bool emit, const PrimRec &r, int ep, float et) {
+        float g[KG];
+        if (emit) {
+            Frag f;
+            shade_full(r, dx, dy, dz, c, f);
+            const double t = (double)et, w = f.abar64 * T;
+            const double V = (double)up.c0 * r.col[0] + (double)up.c1 * r.col[1] +
+                             (double)up.c2 * r.col[2] + ua64 + (double)up.d * t +
+                             (double)up.n0 * f.nc[0] + (double)up.n1 * f.nc[1] +
+                             (double)up.n2 * f.nc[2] + (double)up.k * f.K +
+                             (double)up.dist * (t * t * F0 - 2.0 * t * F1 + F2);
+            pref += w * V;
+            const float g_abar = (float)(T * V) - (float)(vtot - pref) / (float)(1.0 - f.abar64);
+            frag_grad(r, f, dx, dy, dz, (float)w, g_abar, (float)(t * F0 - F1), up, c.euclid, g);
+            T *= 1.0 - f.abar64;
+            if (T < c.t_term) alive = false;
+        }
+        warp_accumulate(sm, emit, ep, g, kg);
+    };
+
+    const int start = tile_offsets[tile], end = tile_offsets[tile + 1];
+    for (int b0 = start; b0 < end; b0 += BATCH) {
+        if (__syncthreads_count(alive) == 0) break;
+        const int nb = min(BATCH, end - b0);
+        load_batch(sm, recs, tile_prims, b0, nb);
+        for (int j = 0; j < nb; ++j) {
+            if (!__any_sync(FULL, alive)) break;
+            float et = 0.f;
+            int ep = -1;
+            bool emit = alive && stream_step(sm.rec[j], sm.prim[j], u, v, dx, dy, dz, c, R, et, ep);
+            if (__any_sync(FULL, emit)) emit_grad(emit, (emit && ep == sm.prim[j]) ? sm.rec[j] : recs[emit ? ep : 0], ep, et);
+        }
+    }
+    while (__any_sync(FULL, alive && R.n > 0)) {
+        float et = 0.f;
+        int ep = -1;
+        bool emit = alive && R.n > 0;
+        if (emit) ring_pop(R, et, ep);
+        emit_grad(emit, recs[emit ? ep : 0], ep, et);
+    }
+}
+
+size_t raster_smem_bytes() { return sizeof(RasterSmem); }
+
+}  // namespace qgs

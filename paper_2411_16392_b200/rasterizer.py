@@ -1,0 +1,381 @@
+"""Drop-in for qgsplat.rasterizer on B200 (sm_100a).
+
+Same module-level API as /root/reference/pkg/src/qgsplat/rasterizer.py:
+``RenderSettings`` (:22), ``PreparedView`` (:33), ``RenderTargets`` (:61),
+``GradientBuffer`` (:77, with zeros / iadd / finite), ``zero_upstream``
+(:111), ``prepare`` (:123), ``forward`` (:198), ``backward`` (:230) and
+``render`` (:337), with the same argument and return signatures.  Inputs may
+be the reference's own numpy PrimitiveSet / Camera objects; outputs are
+CUDA tensors (fp32 maps, int32 counts) with ``to_numpy()`` helpers.
+
+Every stage runs in libqgs_b200.so (include/qgs_b200.h) on the current torch
+CUDA stream; the only host synchronisation per view is the read of the
+(tile, primitive) pair count that sizes the sort buffers.
+"""
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .model import ParameterError, PrimitiveSet
+
+T_NEAR_CLIP = 0.01   # intersect.py:22
+TILE = 16            # bounds.py:19
+
+
+@dataclass
+class RenderSettings:
+    background: np.ndarray = field(default_factory=lambda: np.zeros(3))
+    t_near_clip: float = T_NEAR_CLIP
+    alpha_floor: float = 1.0 / 255.0
+    alpha_clamp: float = 0.999
+    t_term: float = 1e-4
+    resort: bool = True
+    euclidean_density: bool = False
+
+
+# ----------------------------------------------------------------- helpers
+
+def _stream():
+    return ctypes_ptr(torch.cuda.current_stream().cuda_stream)
+
+
+def ctypes_ptr(x):
+    import ctypes
+    return ctypes.c_void_p(x)
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _cam_struct(cam):
+    w2c = np.asarray(cam.world_to_camera, dtype=np.float64)
+    R, t = w2c[:3, :3], w2c[:3, 3]
+    center = -R.T @ t            # cameras.py:48-51
+    c = _lib.Camera()
+    c.fx, c.fy, c.cx, c.cy = float(cam.fx), float(cam.fy), float(cam.cx), float(cam.cy)
+    c.width, c.height = int(cam.width), int(cam.height)
+    c.R_wc[:] = [float(v) for v in R.ravel()]
+    c.t_wc[:] = [float(v) for v in t]
+    c.center[:] = [float(v) for v in center]
+    return c
+
+
+def _settings_struct(st):
+    s = _lib.Settings()
+    s.background[:] = [float(v) for v in np.asarray(st.background, dtype=np.float64).ravel()[:3]]
+    s.t_near_clip, s.alpha_floor = float(st.t_near_clip), float(st.alpha_floor)
+    s.alpha_clamp, s.t_term = float(st.alpha_clamp), float(st.t_term)
+    s.resort, s.euclidean_density = int(bool(st.resort)), int(bool(st.euclidean_density))
+    return s
+
+
+class DevicePrimitives:
+    """Raw primitive parameters resident on the GPU as contiguous fp32."""
+
+    FIELDS = PrimitiveSet.FIELDS
+
+    def __init__(self, centers, quats, raw_scales, raw_signs, raw_opacity, sh):
+        self.centers, self.quats = centers, quats
+        self.raw_scales, self.raw_signs = raw_scales, raw_signs
+        self.raw_opacity, self.sh = raw_opacity, sh
+
+    @staticmethod
+    def from_host(prims, device=None, non_blocking=False):
+        if isinstance(prims, DevicePrimitives):
+            return prims
+        device = device or torch.device("cuda", torch.cuda.current_device())
+        out = []
+        for f in PrimitiveSet.FIELDS:
+            a = getattr(prims, f)
+            if isinstance(a, torch.Tensor):
+                t = a.to(device=device, dtype=torch.float32, non_blocking=non_blocking)
+            else:
+                t = torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float32)))
+                t = t.to(device=device, non_blocking=non_blocking)
+            out.append(t.contiguous())
+        return DevicePrimitives(*out)
+
+    def __len__(self):
+        return self.centers.shape[0]
+
+    @property
+    def sh_coeffs(self):
+        return self.sh.shape[2]
+
+    def params_struct(self):
+        p = _lib.Params()
+        p.centers, p.quats = _ptr(self.centers), _ptr(self.quats)
+        p.raw_scales, p.raw_signs = _ptr(self.raw_scales), _ptr(self.raw_signs)
+        p.raw_opacity, p.sh = _ptr(self.raw_opacity), _ptr(self.sh)
+        p.P, p.sh_coeffs = len(self), self.sh_coeffs
+        return p
+
+
+def _validate(prims):
+    """model.py:37-38: non-finite raw scales / signs raise ParameterError."""
+    for f in ("raw_scales", "raw_signs"):
+        a = getattr(prims, f)
+        ok = bool(torch.isfinite(a).all()) if isinstance(a, torch.Tensor) else \
+            bool(np.isfinite(np.asarray(a)).all())
+        if not ok:
+            raise ParameterError("non-finite raw scale/sign")
+
+
+# ------------------------------------------------------------------- types
+
+@dataclass
+class PreparedView:
+    cam: object
+    settings: RenderSettings
+    prims: object                 # the caller's PrimitiveSet (reference kept, not copied)
+    dev: DevicePrimitives
+    prep: torch.Tensor            # opaque per-primitive device state (qgs_prep_bytes)
+    n_pairs: int
+    tile_offsets: torch.Tensor    # int32 (tiles_x*tiles_y + 1,)
+    tile_prims: torch.Tensor      # int32 (n_pairs,)
+    tiles_x: int
+    tiles_y: int
+    _cam_c: object = None
+    _st_c: object = None
+
+    def _export(self):
+        P = len(self.dev)
+        dev = self.prep.device
+        sc = torch.empty((P, 3), dtype=torch.float64, device=dev)
+        al = torch.empty((P,), dtype=torch.float64, device=dev)
+        co = torch.empty((P, 3), dtype=torch.float64, device=dev)
+        bb = torch.empty((P, 4), dtype=torch.int32, device=dev)
+        pl = torch.empty((P,), dtype=torch.uint8, device=dev)
+        _lib.check(_lib.load().qgs_export_prep(_ptr(self.prep), P, _ptr(sc), _ptr(al), _ptr(co),
+                                               _ptr(bb), _ptr(pl), _stream()), "export_prep")
+        return sc, al, co, bb, pl
+
+    @property
+    def scales(self):
+        return self._export()[0]
+
+    @property
+    def alphas(self):
+        return self._export()[1]
+
+    @property
+    def colors(self):
+        return self._export()[2]
+
+    @property
+    def pix_bbox(self):
+        return self._export()[3]
+
+    @property
+    def planar(self):
+        return self._export()[4]
+
+    def sorted_keys(self):
+        """float64 sort key of every entry of tile_prims (parity/debug)."""
+        keys = torch.empty((max(self.n_pairs, 1),), dtype=torch.float64, device=self.prep.device)
+        _lib.check(_lib.load().qgs_sorted_keys(
+            _ptr(self.prep), len(self.dev), self._cam_c, self._st_c, _ptr(self.tile_offsets),
+            _ptr(self.tile_prims), self.n_pairs, _ptr(keys), _stream()), "sorted_keys")
+        return keys[: self.n_pairs]
+
+
+_MAPS = ("color", "color_raw", "alpha", "depth", "depth_sq", "depth_median", "normal",
+         "curvature", "distortion", "transmittance", "n_fragments")
+
+
+@dataclass
+class RenderTargets:
+    color: torch.Tensor           # blended colour + background, (H, W, 3)
+    color_raw: torch.Tensor
+    alpha: torch.Tensor
+    depth: torch.Tensor           # sum omega_i t_i
+    depth_sq: torch.Tensor
+    depth_median: torch.Tensor
+    normal: torch.Tensor          # camera-frame blended normal
+    curvature: torch.Tensor
+    distortion: torch.Tensor
+    transmittance: torch.Tensor
+    n_fragments: torch.Tensor
+    violations: torch.Tensor      # per tile (int32)
+    aux: torch.Tensor             # (12, H, W) float64 blend sums for the backward
+
+    @property
+    def order_violations(self):
+        return int(self.violations.sum().item())
+
+    def to_numpy(self):
+        d = {k: getattr(self, k).cpu().numpy() for k in _MAPS}
+        d["order_violations"] = self.order_violations
+        return d
+
+
+@dataclass
+class GradientBuffer:
+    centers: torch.Tensor
+    quats: torch.Tensor
+    raw_scales: torch.Tensor
+    raw_signs: torch.Tensor
+    raw_opacity: torch.Tensor
+    sh: torch.Tensor
+    screen_center: torch.Tensor   # ndc-scale projected centre gradient, (P, 2)
+
+    GROUPS = ("centers", "quats", "raw_scales", "raw_signs", "raw_opacity", "sh")
+
+    @staticmethod
+    def zeros(prims, device=None):
+        if isinstance(prims, DevicePrimitives):
+            device = prims.centers.device
+            shp = {f: tuple(getattr(prims, f).shape) for f in DevicePrimitives.FIELDS}
+        else:
+            device = device or torch.device("cuda", torch.cuda.current_device())
+            shp = {f: tuple(np.shape(getattr(prims, f))) for f in PrimitiveSet.FIELDS}
+        z = {f: torch.zeros(s, dtype=torch.float32, device=device) for f, s in shp.items()}
+        return GradientBuffer(**z, screen_center=torch.zeros((shp["centers"][0], 2),
+                                                             dtype=torch.float32, device=device))
+
+    def iadd(self, other):
+        for f in self.GROUPS + ("screen_center",):
+            getattr(self, f).add_(getattr(other, f))
+        return self
+
+    def finite(self):
+        return all(bool(torch.isfinite(getattr(self, f)).all()) for f in self.GROUPS)
+
+    def grads_struct(self):
+        g = _lib.Grads()
+        for f in self.GROUPS + ("screen_center",):
+            setattr(g, f, _ptr(getattr(self, f)))
+        return g
+
+    def flat(self):
+        """The six raw groups packed into one fp32 vector (all-reduce layout)."""
+        return torch.cat([getattr(self, f).reshape(-1) for f in self.GROUPS])
+
+    def to_numpy(self):
+        return {f: getattr(self, f).cpu().numpy() for f in self.GROUPS + ("screen_center",)}
+
+
+def zero_upstream(cam, device=None):
+    device = device or torch.device("cuda", torch.cuda.current_device())
+    H, W = int(cam.height), int(cam.width)
+    z = lambda *s: torch.zeros(s, dtype=torch.float32, device=device)  # noqa: E731
+    return {"color": z(H, W, 3), "alpha": z(H, W), "depth": z(H, W), "normal": z(H, W, 3),
+            "curvature": z(H, W), "distortion": z(H, W)}
+
+
+# ------------------------------------------------------------------ stages
+
+def prepare(prims, cam, settings: RenderSettings = None, validate=True) -> PreparedView:
+    """rasterizer.py:123-195: preprocessing, key duplication and tile sort."""
+    settings = settings or RenderSettings()
+    L = _lib.load()
+    if validate:
+        _validate(prims)
+    dev = DevicePrimitives.from_host(prims)
+    device = dev.centers.device
+    P = len(dev)
+    cam_c, st_c = _cam_struct(cam), _settings_struct(settings)
+    tiles_x = (int(cam.width) + TILE - 1) // TILE
+    tiles_y = (int(cam.height) + TILE - 1) // TILE
+    prep = torch.empty((L.qgs_prep_bytes(P),), dtype=torch.uint8, device=device)
+    n_dev = torch.empty((1,), dtype=torch.int64, device=device)
+    pp = dev.params_struct()
+    _lib.check(L.qgs_preprocess(pp, cam_c, st_c, _ptr(prep), _ptr(n_dev), _stream()),
+               "qgs_preprocess")
+    n_pairs = int(n_dev.item())              # the one host sync per view
+    n_tiles = tiles_x * tiles_y
+    ws_bytes = L.qgs_bin_workspace_bytes(P, n_pairs, n_tiles)
+    ws = torch.empty((ws_bytes,), dtype=torch.uint8, device=device)
+    tile_offsets = torch.empty((n_tiles + 1,), dtype=torch.int32, device=device)
+    tile_prims = torch.empty((max(n_pairs, 1),), dtype=torch.int32, device=device)
+    _lib.check(L.qgs_bin(_ptr(prep), P, cam_c, st_c, n_pairs, _ptr(ws), ws_bytes,
+                         _ptr(tile_offsets), _ptr(tile_prims), _stream()), "qgs_bin")
+    return PreparedView(cam=cam, settings=settings, prims=prims, dev=dev, prep=prep,
+                        n_pairs=n_pairs, tile_offsets=tile_offsets,
+                        tile_prims=tile_prims[:n_pairs], tiles_x=tiles_x, tiles_y=tiles_y,
+                        _cam_c=cam_c, _st_c=st_c)
+
+
+def forward(prep: PreparedView, keep_aux=True) -> RenderTargets:
+    """rasterizer.py:198-227."""
+    cam = prep.cam
+    H, W = int(cam.height), int(cam.width)
+    device = prep.prep.device
+    f32 = lambda *s: torch.empty(s, dtype=torch.float32, device=device)  # noqa: E731
+    tg = RenderTargets(
+        color=f32(H, W, 3), color_raw=f32(H, W, 3), alpha=f32(H, W), depth=f32(H, W),
+        depth_sq=f32(H, W), depth_median=f32(H, W), normal=f32(H, W, 3), curvature=f32(H, W),
+        distortion=f32(H, W), transmittance=f32(H, W),
+        n_fragments=torch.empty((H, W), dtype=torch.int32, device=device),
+        violations=torch.empty((prep.tiles_x * prep.tiles_y,), dtype=torch.int32, device=device),
+        aux=torch.empty((_lib.AUX_PLANES, H, W) if keep_aux else (1,), dtype=torch.float64,
+                        device=device))
+    t = _lib.Targets()
+    for k in _MAPS + ("violations",):
+        setattr(t, k, _ptr(getattr(tg, k)))
+    t.aux = _ptr(tg.aux) if keep_aux else None
+    _lib.check(_lib.load().qgs_forward(_ptr(prep.prep), len(prep.dev), prep._cam_c, prep._st_c,
+                                       _ptr(prep.tile_offsets), _ptr(prep.tile_prims), t,
+                                       _stream()), "qgs_forward")
+    return tg
+
+
+def _up_tensor(a, shape, device):
+    if a is None:
+        return None
+    if isinstance(a, torch.Tensor):
+        t = a.to(device=device, dtype=torch.float32)
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float32))).to(device)
+    if tuple(t.shape) != shape:
+        raise ValueError(f"upstream shape {tuple(t.shape)} != {shape}")
+    return t.contiguous()
+
+
+def kernel_grads(prep: PreparedView, targets: RenderTargets, upstream) -> torch.Tensor:
+    """backward_kernel + merge (raster_kernels.py:505-681): (P, 24) fp32 slots."""
+    cam = prep.cam
+    H, W = int(cam.height), int(cam.width)
+    device = prep.prep.device
+    shapes = {"color": (H, W, 3), "alpha": (H, W), "depth": (H, W), "normal": (H, W, 3),
+              "curvature": (H, W), "distortion": (H, W)}
+    ups = {k: _up_tensor(upstream.get(k), s, device) for k, s in shapes.items()}
+    u = _lib.Upstream()
+    for k, v in ups.items():
+        setattr(u, k, _ptr(v))
+    t = _lib.Targets()
+    for k in _MAPS + ("violations",):
+        setattr(t, k, _ptr(getattr(targets, k)))
+    if targets.aux.dim() != 3:
+        raise ValueError("backward needs forward(prep, keep_aux=True)")
+    t.aux = _ptr(targets.aux)
+    kg = torch.zeros((len(prep.dev), _lib.KG_STRIDE), dtype=torch.float32, device=device)
+    _lib.check(_lib.load().qgs_backward(_ptr(prep.prep), len(prep.dev), prep._cam_c, prep._st_c,
+                                        _ptr(prep.tile_offsets), _ptr(prep.tile_prims), t, u,
+                                        _ptr(kg), _stream()), "qgs_backward")
+    return kg
+
+
+def chain(prep: PreparedView, kg: torch.Tensor, out: GradientBuffer = None) -> GradientBuffer:
+    """_chain_to_raw (rasterizer.py:270-334); accumulates into `out`."""
+    out = out if out is not None else GradientBuffer.zeros(prep.dev)
+    _lib.check(_lib.load().qgs_chain(prep.dev.params_struct(), _ptr(prep.prep), _ptr(kg),
+                                     prep._cam_c, out.grads_struct(), _stream()), "qgs_chain")
+    return out
+
+
+def backward(prep: PreparedView, targets: RenderTargets, upstream,
+             out: GradientBuffer = None) -> GradientBuffer:
+    """rasterizer.py:230-267.  With `out`, gradients are accumulated into it
+    (several views on one device sum before a single all-reduce)."""
+    return chain(prep, kernel_grads(prep, targets, upstream), out)
+
+
+def render(prims, cam, settings=None):
+    """Convenience one-shot forward (rasterizer.py:337-340)."""
+    prep = prepare(prims, cam, settings)
+    return forward(prep), prep
