@@ -159,6 +159,16 @@ int qgs_export_prep(const void *prep, int32_t P, double *scales, double *alphas,
                     double *colors, int32_t *pix_bbox, uint8_t *planar,
                     qgs_stream_t stream);
 
+/* Diagnostics: replay one pixel's fragment stream (same device functions as
+ * the raster kernels) and record up to `max` accepted candidates (tile-list
+ * order) and emitted fragments (compositing order, with T before each).
+ * counts[0] = accepted, counts[1] = emitted. */
+int qgs_trace_pixel(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settings *st,
+                    const int32_t *tile_offsets, const int32_t *tile_prims, int32_t u, int32_t v,
+                    int32_t max, int32_t *acc_prim, float *acc_t, float *acc_abar,
+                    int32_t *em_prim, float *em_t, float *em_abar, double *em_T,
+                    int32_t *counts, qgs_stream_t stream);
+
 const char *qgs_last_error(void);
 int qgs_version(void);
 

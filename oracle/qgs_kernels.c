@@ -688,3 +688,53 @@ int qo_num_threads(void)
     return 1;
 #endif
 }
+
+/* ------------------------------------------------------------ diagnostics
+ * Per-pixel trace: every accepted candidate (tile-list order) and every
+ * emitted fragment (compositing order) with its transmittance before it. */
+typedef struct {
+    qo_fwd_px px;
+    int max, n;
+    int64_t *prim;
+    double *t, *abar, *T;
+} qo_trace_ctx;
+
+static int trace_visit(void *vctx, int64_t pos, int64_t p, const qo_frag *f)
+{
+    qo_trace_ctx *c = (qo_trace_ctx *)vctx;
+    if (c->n < c->max) {
+        c->prim[c->n] = p; c->t[c->n] = f->h.t; c->abar[c->n] = f->abar; c->T[c->n] = c->px.T;
+    }
+    c->n++;
+    return fwd_visit(&c->px, pos, p, f);
+}
+
+int qo_trace_pixel(int64_t W, const double *dirs, const int64_t *tile_offsets,
+                   const int64_t *tile_prims, int64_t tiles_x, const qo_prims *pr,
+                   const qo_settings *st, int64_t u, int64_t v, int max,
+                   int64_t *acc_prim, double *acc_t, double *acc_abar, int *n_acc,
+                   int64_t *em_prim, double *em_t, double *em_abar, double *em_T)
+{
+    int64_t tile = (v / 16) * tiles_x + u / 16, px = v * W + u;
+    const double *d = dirs + 3 * px;
+    int na = 0;
+    for (int64_t i = tile_offsets[tile]; i < tile_offsets[tile + 1]; ++i) {
+        int64_t p = tile_prims[i];
+        const int64_t *bb = pr->bbox + 4 * p;
+        if (u < bb[0] || u > bb[1] || v < bb[2] || v > bb[3]) continue;
+        qo_frag f;
+        shade(pr, p, d[0], d[1], d[2], st, &f);
+        if (!f.h.valid) continue;
+        if (na < max) { acc_prim[na] = p; acc_t[na] = f.h.t; acc_abar[na] = f.abar; }
+        na++;
+    }
+    *n_acc = na;
+    qo_trace_ctx c;
+    memset(&c, 0, sizeof c);
+    c.px.colors = pr->colors; c.px.T = 1.0; c.px.t_term = st->t_term;
+    c.max = max; c.prim = em_prim; c.t = em_t; c.abar = em_abar; c.T = em_T;
+    qo_entry ring[QO_RING];
+    pixel_stream(pr, tile_prims, tile_offsets[tile], tile_offsets[tile + 1], u, v, d, st,
+                 trace_visit, &c, ring);
+    return c.n;
+}

@@ -96,6 +96,9 @@ def lib():
         L.qo_tile_keys.argtypes = [i64, vp, vp, i64, ctypes.POINTER(_Prims), vp, vp, vp,
                                    d, d, d, d, i64, i64, ctypes.c_int, d, vp]
         L.qo_num_threads.restype = ctypes.c_int
+        L.qo_trace_pixel.restype = ctypes.c_int
+        L.qo_trace_pixel.argtypes = [i64, vp, vp, vp, i64, ctypes.POINTER(_Prims),
+                                     ctypes.POINTER(_Settings), i64, i64, ctypes.c_int] + [vp] * 8
         _lib = L
     return _lib
 
@@ -637,6 +640,22 @@ def chain(vw, kg):
 def backward(vw, targets, upstream):
     """rasterizer.py:230-267."""
     return chain(vw, kernel_grads(vw, targets, upstream))
+
+
+def trace_pixel(vw, u, v, max_frags=4096):
+    """Accepted candidates and emitted fragments of one pixel (diagnostics)."""
+    ap, at, aa = np.zeros(max_frags, np.int64), np.zeros(max_frags), np.zeros(max_frags)
+    ep, et, ea, eT = (np.zeros(max_frags, np.int64), np.zeros(max_frags), np.zeros(max_frags),
+                      np.zeros(max_frags))
+    na = ctypes.c_int(0)
+    cs, cst = vw._cstruct(), _settings(vw.settings)
+    ne = lib().qo_trace_pixel(vw.cam.width, _p(vw.dirs), _p(vw.tile_offsets), _p(vw.tile_prims),
+                              vw.tiles_x, ctypes.byref(cs), ctypes.byref(cst), int(u), int(v),
+                              max_frags, _p(ap), _p(at), _p(aa), ctypes.byref(na), _p(ep), _p(et),
+                              _p(ea), _p(eT))
+    na, ne = min(na.value, max_frags), min(ne, max_frags)
+    return ({"prim": ap[:na], "t": at[:na], "abar": aa[:na]},
+            {"prim": ep[:ne], "t": et[:ne], "abar": ea[:ne], "T": eT[:ne]})
 
 
 def render(prims, cam, settings=None):

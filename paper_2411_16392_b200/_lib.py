@@ -84,6 +84,8 @@ def load():
                                         P(Upstream), vp, vp]),
         "qgs_chain": (ctypes.c_int, [P(Params), vp, vp, P(Camera), P(Grads), vp]),
         "qgs_export_prep": (ctypes.c_int, [vp, i32, vp, vp, vp, vp, vp, vp]),
+        "qgs_trace_pixel": (ctypes.c_int, [vp, i32, P(Camera), P(Settings), vp, vp, i32, i32,
+                                           i32] + [vp] * 9),
         "qgs_last_error": (ctypes.c_char_p, []),
         "qgs_version": (ctypes.c_int, []),
     }
@@ -97,7 +99,7 @@ def load():
 
 EXPORTS = ("qgs_prep_bytes", "qgs_preprocess", "qgs_bin_workspace_bytes", "qgs_bin",
            "qgs_sorted_keys", "qgs_tile_keys_f64", "qgs_forward", "qgs_backward", "qgs_chain",
-           "qgs_export_prep", "qgs_last_error", "qgs_version")
+           "qgs_export_prep", "qgs_trace_pixel", "qgs_last_error", "qgs_version")
 
 
 def check(rc, what):

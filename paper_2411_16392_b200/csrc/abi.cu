@@ -255,6 +255,25 @@ int qgs_chain(const qgs_params *prims, const void *prep, const float *kg, const 
     return 0;
 }
 
+int qgs_trace_pixel(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settings *st,
+                    const int32_t *tile_offsets, const int32_t *tile_prims, int32_t u, int32_t v,
+                    int32_t max, int32_t *acc_prim, float *acc_t, float *acc_abar,
+                    int32_t *em_prim, float *em_t, float *em_abar, double *em_T,
+                    int32_t *counts, qgs_stream_t stream)
+{
+    if (int rc = check_cam(cam)) return rc;
+    if (u < 0 || v < 0 || u >= cam->width || v >= cam->height) return fail(QGS_E_ARG, "pixel outside image");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    qgs::CamK ck = qgs::make_camk(*cam);
+    qgs::SetK sk = qgs::make_setk(*st);
+    qgs::PrepView pv = qgs::prep_view(const_cast<void *>(prep), P);
+    qgs::trace_pixel_kernel<<<1, 32, 0, s>>>(pv.rec, tile_offsets, tile_prims, ck, sk, u, v, max,
+                                            acc_prim, acc_t, acc_abar, em_prim, em_t, em_abar,
+                                            em_T, counts);
+    QGS_LAUNCHED("trace_pixel_kernel");
+    return 0;
+}
+
 int qgs_export_prep(const void *prep, int32_t P, double *scales, double *alphas, double *colors,
                     int32_t *pix_bbox, uint8_t *planar, qgs_stream_t stream)
 {

@@ -40,6 +40,11 @@ __global__ void raster_fwd_kernel(const PrimRec *recs, const int32_t *tile_offse
 __global__ void raster_bwd_kernel(const PrimRec *recs, const int32_t *tile_offsets,
                                   const int32_t *tile_prims, CamK cam, SetK st, qgs_targets fwd,
                                   qgs_upstream upst, float *kg);
+__global__ void trace_pixel_kernel(const PrimRec *recs, const int32_t *tile_offsets,
+                                   const int32_t *tile_prims, CamK cam, SetK st, int u, int v,
+                                   int max, int *acc_prim, float *acc_t, float *acc_abar,
+                                   int *em_prim, float *em_t, float *em_abar, double *em_T,
+                                   int *counts);
 size_t raster_smem_bytes();
 constexpr int RASTER_THREADS = 256;
 

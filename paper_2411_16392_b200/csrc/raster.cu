@@ -561,6 +561,63 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const int32_t *__restrict__ 
     }
 }
 
+// ============================================================ diagnostics
+// Single-thread replay of one pixel's stream with the same inline functions:
+// records every accepted candidate and every emitted fragment (with T before).
+__global__ void trace_pixel_kernel(const PrimRec *__restrict__ recs,
+                                   const int32_t *__restrict__ tile_offsets,
+                                   const int32_t *__restrict__ tile_prims, CamK cam, SetK st,
+                                   int u, int v, int max, int *acc_prim, float *acc_t,
+                                   float *acc_abar, int *em_prim, float *em_t, float *em_abar,
+                                   double *em_T, int *counts)
+{
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const Cfg c = make_cfg(st);
+    float dx, dy, dz;
+    pixel_dir(cam, u, v, dx, dy, dz);
+    const int tile = (v / TILE) * cam.tiles_x + u / TILE;
+    Ring R;
+    R.n = 0;
+    double T = 1.0;
+    int na = 0, ne = 0;
+    bool alive = true;
+    auto record = [&](int ep, float et) {
+        Frag f;
+        shade_full(recs[ep], dx, dy, dz, c, f);
+        if (ne < max) { em_prim[ne] = ep; em_t[ne] = et; em_abar[ne] = f.abar; em_T[ne] = T; }
+        ne++;
+        T *= 1.0 - f.abar64;
+        if (T < c.t_term) alive = false;
+    };
+    for (int i = tile_offsets[tile]; i < tile_offsets[tile + 1] && alive; ++i) {
+        const int p = tile_prims[i];
+        const PrimRec &r = recs[p];
+        float t;
+        if (accept(r, u, v, dx, dy, dz, c, t)) {
+            if (na < max) {
+                Hit h;
+                hit32(r, dx, dy, dz, c.euclid, c.t_clip, h);
+                acc_prim[na] = p; acc_t[na] = t; acc_abar[na] = r.alpha * h.G;
+            }
+            na++;
+            float et;
+            int ep;
+            bool emit;
+            if (!c.resort) { et = t; ep = p; emit = true; }
+            else emit = ring_push(R, t, p, et, ep);
+            if (emit) record(ep, et);
+        }
+    }
+    while (alive && R.n > 0) {
+        float et;
+        int ep;
+        ring_pop(R, et, ep);
+        record(ep, et);
+    }
+    counts[0] = na;
+    counts[1] = ne;
+}
+
 size_t raster_smem_bytes() { return sizeof(RasterSmem); }
 
 }  // namespace qgs

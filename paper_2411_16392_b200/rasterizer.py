@@ -174,6 +174,26 @@ class PreparedView:
     def planar(self):
         return self._export()[4]
 
+    def trace_pixel(self, u, v, max_frags=4096):
+        """Replay pixel (u, v): accepted candidates and emitted fragments."""
+        dev = self.prep.device
+        i = lambda: torch.zeros((max_frags,), dtype=torch.int32, device=dev)  # noqa: E731
+        f = lambda: torch.zeros((max_frags,), dtype=torch.float32, device=dev)  # noqa: E731
+        ap, at, aa, ep, et, ea = i(), f(), f(), i(), f(), f()
+        eT = torch.zeros((max_frags,), dtype=torch.float64, device=dev)
+        cnt = torch.zeros((2,), dtype=torch.int32, device=dev)
+        _lib.check(_lib.load().qgs_trace_pixel(
+            _ptr(self.prep), len(self.dev), self._cam_c, self._st_c, _ptr(self.tile_offsets),
+            _ptr(self.tile_prims), int(u), int(v), max_frags, *(_ptr(x) for x in
+                                                                (ap, at, aa, ep, et, ea, eT, cnt)),
+            _stream()), "trace_pixel")
+        na, ne = (int(x) for x in cnt.cpu())
+        na, ne = min(na, max_frags), min(ne, max_frags)
+        return ({"prim": ap[:na].cpu().numpy(), "t": at[:na].cpu().numpy(),
+                 "abar": aa[:na].cpu().numpy()},
+                {"prim": ep[:ne].cpu().numpy(), "t": et[:ne].cpu().numpy(),
+                 "abar": ea[:ne].cpu().numpy(), "T": eT[:ne].cpu().numpy()})
+
     def sorted_keys(self):
         """float64 sort key of every entry of tile_prims (parity/debug)."""
         keys = torch.empty((max(self.n_pairs, 1),), dtype=torch.float64, device=self.prep.device)

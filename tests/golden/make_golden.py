@@ -44,8 +44,8 @@ def _keys_hook(*a):
     _captured["keys_unsorted"] = out.copy()
     _captured["pair_tiles_unsorted"] = np.asarray(a[0]).copy()
     _captured["pair_prims_unsorted"] = np.asarray(a[1]).copy()
-    _captured["vert_u"] = np.asarray(a[9]).copy()
-    _captured["vert_v"] = np.asarray(a[10]).copy()
+    _captured["vert_u"] = np.asarray(a[8]).copy()
+    _captured["vert_v"] = np.asarray(a[9]).copy()
     return out
 
 
