@@ -216,7 +216,7 @@ int qgs_forward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_se
     qgs::SetK sk = qgs::make_setk(*st);
     qgs::PrepView pv = qgs::prep_view(const_cast<void *>(prep), P);
     qgs::raster_fwd_kernel<<<ck.tiles_x * ck.tiles_y, qgs::RASTER_THREADS,
-                             qgs::raster_smem_bytes(), s>>>(pv.rec, tile_offsets, tile_prims, ck,
+                             qgs::raster_smem_bytes(), s>>>(pv.rec, pv.geo, tile_offsets, tile_prims, ck,
                                                             sk, *out);
     QGS_LAUNCHED("raster_fwd_kernel");
     return 0;
@@ -235,7 +235,7 @@ int qgs_backward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_s
     qgs::SetK sk = qgs::make_setk(*st);
     qgs::PrepView pv = qgs::prep_view(const_cast<void *>(prep), P);
     qgs::raster_bwd_kernel<<<ck.tiles_x * ck.tiles_y, qgs::RASTER_THREADS,
-                             qgs::raster_smem_bytes(), s>>>(pv.rec, tile_offsets, tile_prims, ck,
+                             qgs::raster_smem_bytes(), s>>>(pv.rec, pv.geo, tile_offsets, tile_prims, ck,
                                                             sk, *fwd, *up, kg);
     QGS_LAUNCHED("raster_bwd_kernel");
     return 0;
@@ -267,7 +267,7 @@ int qgs_trace_pixel(const void *prep, int32_t P, const qgs_camera *cam, const qg
     qgs::CamK ck = qgs::make_camk(*cam);
     qgs::SetK sk = qgs::make_setk(*st);
     qgs::PrepView pv = qgs::prep_view(const_cast<void *>(prep), P);
-    qgs::trace_pixel_kernel<<<1, 32, 0, s>>>(pv.rec, tile_offsets, tile_prims, ck, sk, u, v, max,
+    qgs::trace_pixel_kernel<<<1, 32, 0, s>>>(pv.rec, pv.geo, tile_offsets, tile_prims, ck, sk, u, v, max,
                                             acc_prim, acc_t, acc_abar, em_prim, em_t, em_abar,
                                             em_T, counts);
     QGS_LAUNCHED("trace_pixel_kernel");

@@ -35,12 +35,12 @@ size_t sort_smem_bytes();
 constexpr int SORT_THREADS = 512;
 
 // raster.cu
-__global__ void raster_fwd_kernel(const PrimRec *recs, const int32_t *tile_offsets,
+__global__ void raster_fwd_kernel(const PrimRec *recs, const Geo64 *geo, const int32_t *tile_offsets,
                                   const int32_t *tile_prims, CamK cam, SetK st, qgs_targets out);
-__global__ void raster_bwd_kernel(const PrimRec *recs, const int32_t *tile_offsets,
+__global__ void raster_bwd_kernel(const PrimRec *recs, const Geo64 *geo, const int32_t *tile_offsets,
                                   const int32_t *tile_prims, CamK cam, SetK st, qgs_targets fwd,
                                   qgs_upstream upst, float *kg);
-__global__ void trace_pixel_kernel(const PrimRec *recs, const int32_t *tile_offsets,
+__global__ void trace_pixel_kernel(const PrimRec *recs, const Geo64 *geo, const int32_t *tile_offsets,
                                    const int32_t *tile_prims, CamK cam, SetK st, int u, int v,
                                    int max, int *acc_prim, float *acc_t, float *acc_abar,
                                    int *em_prim, float *em_t, float *em_abar, double *em_T,

@@ -229,160 +229,5 @@ __device__ inline double tile_key_geo(const Geo64 &g, int tile, const CamK &cam,
                       tile, cam, euclid, t_clip);
 }
 
-// ----------------------------------------------------------------- fp32
-// Raster-side shading.  Same selection rule as fragment_geometry
-// (intersect.py:58-115) evaluated in fp32 with cancellation-free roots and a
-// longer arc-length series.
-
-struct Hit {
-    float t, x, y, rho, cth, sth, a, l, sig, G, dhx, dhy, dhz;
-    int branch;
-};
-
-// arc length of z = a r^2 over [0, rho]; series below |u| = 0.3 (error < 1e-8)
-__device__ __forceinline__ float arc32(float a, float rho)
-{
-    float u = 2.f * a * rho;
-    if (fabsf(u) < 0.3f) {
-        float u2 = u * u;
-        return rho * (1.f + u2 * (1.f / 6.f + u2 * (-1.f / 40.f + u2 * (1.f / 112.f - u2 * (5.f / 1152.f)))));
-    }
-    float r = sqrtf(fmaf(u, u, 1.f));
-    float as = copysignf(logf(fabsf(u) + r), u);
-    return (as + u * r) / (4.f * a);
-}
-
-// (dl/da, dl/drho) on the same branch
-__device__ __forceinline__ void arc32_grad(float a, float rho, float l, float &dla, float &dlr)
-{
-    float u = 2.f * a * rho;
-    if (fabsf(u) < 0.3f) {
-        float u2 = u * u;
-        // d/du of the series times d u/d a = 2 rho, etc.
-        float fp = u * (1.f / 3.f + u2 * (-1.f / 10.f + u2 * (3.f / 56.f - u2 * (5.f / 144.f))));
-        dla = 2.f * rho * rho * fp;
-        dlr = 1.f + u2 * (0.5f + u2 * (-0.125f + u2 * (1.f / 16.f - u2 * (5.f / 128.f))));
-        return;
-    }
-    float r = sqrtf(fmaf(u, u, 1.f));
-    dla = (rho * r - l) / a;
-    dlr = r;
-}
-
-__device__ __forceinline__ void local_dir32(const PrimRec &r, float dx, float dy, float dz,
-                                            float &hx, float &hy, float &hz)
-{
-    hx = fmaf(r.M[0], dx, fmaf(r.M[1], dy, r.M[2] * dz));
-    hy = fmaf(r.M[3], dx, fmaf(r.M[4], dy, r.M[5] * dz));
-    hz = fmaf(r.M[6], dx, fmaf(r.M[7], dy, r.M[8] * dz));
-}
-
-// test one candidate depth; fills h on acceptance
-__device__ __forceinline__ bool accept_root(const PrimRec &r, float t, float hx, float hy,
-                                            bool euclid, float t_clip, Hit &h)
-{
-    if (!(t > t_clip)) return false;
-    float x = fmaf(t, hx, r.ox), y = fmaf(t, hy, r.oy);
-    float ex = r.s2 * x, ey = r.s1 * y;
-    float m = fmaf(ex, ex, ey * ey);
-    if (m > r.ell9) return false;
-    float rho = sqrtf(fmaf(x, x, y * y));
-    float c = 1.f, s = 0.f;
-    if (rho > 1e-12f) { float ir = 1.f / rho; c = x * ir; s = y * ir; }
-    float a = r.s3 * fmaf(r.w1 * c, c, r.w2 * s * s);
-    float l = euclid ? rho : arc32(a, rho);
-    float sc = r.s2 * c, ss = r.s1 * s;
-    float sig = r.s12 * rsqrtf(fmaf(sc, sc, ss * ss));
-    if (!(l <= 3.f * sig)) return false;
-    h.t = t; h.x = x; h.y = y; h.rho = rho; h.cth = c; h.sth = s; h.a = a; h.l = l; h.sig = sig;
-    h.G = expf(-(l * l) / (2.f * sig * sig));
-    return true;
-}
-
-// ray/primitive hit with the near-then-far rule; d is the camera-frame ray
-__device__ __forceinline__ bool hit32(const PrimRec &r, float dx, float dy, float dz,
-                                      bool euclid, float t_clip, Hit &h)
-{
-    float hx, hy, hz;
-    local_dir32(r, dx, dy, dz, hx, hy, hz);
-    h.dhx = hx; h.dhy = hy; h.dhz = hz;
-    if (r.flags & 1u) {
-        h.branch = BR_PLANAR;
-        if (fabsf(hz) < 1e-12f) return false;
-        float t = -r.oz / hz;
-        if (!(t > t_clip)) return false;
-        float x = fmaf(t, hx, r.ox), y = fmaf(t, hy, r.oy);
-        float rho = sqrtf(fmaf(x, x, y * y));
-        float c = 1.f, s = 0.f;
-        if (rho > 1e-12f) { float ir = 1.f / rho; c = x * ir; s = y * ir; }
-        float sc = r.s2 * c, ss = r.s1 * s;
-        float sig = r.s12 * rsqrtf(fmaf(sc, sc, ss * ss));
-        if (rho > 3.f * sig) return false;
-        h.t = t; h.x = x; h.y = y; h.rho = rho; h.cth = c; h.sth = s; h.a = 0.f; h.l = rho;
-        h.sig = sig;
-        h.G = expf(-(rho * rho) / (2.f * sig * sig));
-        return true;
-    }
-    float A = fmaf(r.w1 * hx, hx, r.w2 * hy * hy);
-    float B = 2.f * fmaf(r.w1 * r.ox, hx, r.w2 * r.oy * hy) - r.iw3 * hz;
-    float C = r.C;
-    if (fabsf(A) < 1e-6f) {
-        h.branch = BR_LINEAR;
-        if (fabsf(B) < 1e-12f) return false;
-        return accept_root(r, -C / B, hx, hy, euclid, t_clip, h);
-    }
-    h.branch = BR_QUAD;
-    float disc = fmaf(B, B, -4.f * A * C);
-    if (disc < 0.f) return false;
-    float sq = sqrtf(disc);
-    float q = -0.5f * (B + copysignf(sq, B));
-    float ra = q / A, rb = (q != 0.f) ? C / q : ra;
-    float tn = fminf(ra, rb), tf = fmaxf(ra, rb);
-    if (accept_root(r, tn, hx, hy, euclid, t_clip, h)) return true;
-    if (disc == 0.f) return false;
-    return accept_root(r, tf, hx, hy, euclid, t_clip, h);
-}
-
-// camera-frame camera-facing normal and Gaussian curvature at a hit
-__device__ __forceinline__ void normal_curv32(const PrimRec &r, const Hit &h, float dx, float dy,
-                                              float dz, float nl[3], float nc[3], float &K,
-                                              float &inrm, float &flip)
-{
-    if (h.branch == BR_PLANAR) {
-        nl[0] = 0.f; nl[1] = 0.f; nl[2] = -1.f; K = 0.f; inrm = 1.f;
-    } else {
-        float nx = 2.f * r.w1 * h.x, ny = 2.f * r.w2 * h.y, nz = -r.iw3;
-        inrm = rsqrtf(fmaf(nx, nx, fmaf(ny, ny, nz * nz)));
-        nl[0] = nx * inrm; nl[1] = ny * inrm; nl[2] = nz * inrm;
-        float l1x = r.lam1 * h.x, l2y = r.lam2 * h.y;
-        float den = 1.f + 4.f * fmaf(l1x, l1x, l2y * l2y);
-        K = 4.f * r.lam1 * r.lam2 / (den * den);
-    }
-    // Nmat = M^T (camera-from-local)
-    nc[0] = fmaf(r.M[0], nl[0], fmaf(r.M[3], nl[1], r.M[6] * nl[2]));
-    nc[1] = fmaf(r.M[1], nl[0], fmaf(r.M[4], nl[1], r.M[7] * nl[2]));
-    nc[2] = fmaf(r.M[2], nl[0], fmaf(r.M[5], nl[1], r.M[8] * nl[2]));
-    flip = 1.f;
-    if (fmaf(nc[0], dx, fmaf(nc[1], dy, nc[2] * dz)) > 0.f) {
-        flip = -1.f; nc[0] = -nc[0]; nc[1] = -nc[1]; nc[2] = -nc[2];
-    }
-}
-
-// camera-frame unit ray of pixel (u, v): fp64, rounded once (cameras.py:53-59)
-__device__ __forceinline__ void pixel_dir(const CamK &cam, int u, int v, float &dx, float &dy,
-                                          float &dz)
-{
-    double a = ((double)u + 0.5 - cam.cx) / cam.fx;
-    double b = ((double)v + 0.5 - cam.cy) / cam.fy;
-    double n = sqrt(a * a + b * b + 1.0);
-    dx = (float)(a / n); dy = (float)(b / n); dz = (float)(1.0 / n);
-}
-
-__device__ __forceinline__ bool in_box(const PrimRec &r, int u, int v)
-{
-    int umin = (int)(r.bb_u & 0xffffu), umax = (int)(r.bb_u >> 16);
-    int vmin = (int)(r.bb_v & 0xffffu), vmax = (int)(r.bb_v >> 16);
-    return u >= umin && u <= umax && v >= vmin && v <= vmax;
-}
 
 }  // namespace qgs

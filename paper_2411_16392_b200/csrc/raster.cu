@@ -4,24 +4,24 @@
 // (_grad_fragment), :505-670 (backward_kernel), :673-681 (merge).
 //
 // One CTA per 16x16 tile, one thread per pixel; each warp owns an 8x4 pixel
-// block so that lanes see spatially coherent fragment streams.  The tile's
+// block so lanes see spatially coherent fragment streams.  The tile's
 // depth-sorted primitive list is streamed in batches of 256 fp32 records
 // staged in shared memory (8 lanes per 128-byte record, fully coalesced).
-// Per pixel, accepted fragments go through the 8-entry min-depth ring
-// (depth + primitive id in registers, statically indexed); an emitted
-// fragment is re-shaded from its record, so the ring costs 16 registers.
+// Accepted fragments go through the per-pixel 8-entry min-depth ring (fp64
+// depth + primitive id, kept in shared memory); an emitted fragment is
+// re-shaded at its stored fp64 depth (shade.cuh: shade_at).
 //
-// Precision: shading is fp32 (cancellation-free roots, long arc-length
-// series); transmittance, blend weights and the eleven blend sums are fp64,
-// which keeps T_i, w_i and the backward's suffix sums (vtot - prefix, the
-// front-to-back rewrite of raster_kernels.py:340) accurate to ~1e-15 instead
-// of the ~1e-7 * |vtot| an fp32 prefix would give.
+// Precision: candidate tests are fp32 with an fp64 depth refinement of every
+// accepted root (shade.cuh); transmittance, blend weights and the eleven
+// blend sums are fp64, which keeps T_i, w_i and the backward's suffix sums
+// (vtot - prefix, the front-to-back rewrite of raster_kernels.py:340) exact to
+// ~1e-15 instead of the ~1e-7 |vtot| an fp32 prefix would give.
 //
 // The backward replays exactly the same stream (same inline functions, same
 // decisions) and reduces each emitted fragment's 22 kernel-level gradient
-// slots across the warp's lanes that emitted the same primitive (match_any +
+// slots across the warp lanes that emitted the same primitive (match_any +
 // shared-memory transpose) before one float atomic per slot.
-#include "qgs_common.cuh"
+#include "shade.cuh"
 
 namespace qgs {
 
@@ -32,6 +32,9 @@ constexpr unsigned FULL = 0xffffffffu;
 struct RasterSmem {
     PrimRec rec[BATCH];
     int prim[BATCH];
+    double ring_t[RING][RT];  // per-thread ring, [slot][thread]: conflict-free
+    int ring_p[RING][RT];
+    double d64[3][RT];        // per-thread fp64 ray direction
     float red[RT / 32][32][KG];
     int viol;
 };
@@ -60,52 +63,52 @@ __device__ __forceinline__ void load_batch(RasterSmem &sm, const PrimRec *__rest
     __syncthreads();
 }
 
+// Per-thread ring view into shared memory.
 struct Ring {
-    float t[RING];
-    int p[RING];
+    double *t;   // &ring_t[0][tid], stride RT
+    int *p;
     int n;
 };
 
-// push an accepted fragment; returns true with (et, ep) when one is emitted
+// push an accepted fragment; true with (et, ep) when one is emitted
 // (raster_kernels.py:159-226: first minimum, strict <, emit incoming if nearer)
-__device__ __forceinline__ bool ring_push(Ring &R, float t, int prim, float &et, int &ep)
+__device__ __forceinline__ bool ring_push(Ring &R, double t, int prim, double &et, int &ep)
 {
     if (R.n < RING) {
-#pragma unroll
-        for (int k = 0; k < RING; ++k)
-            if (k == R.n) { R.t[k] = t; R.p[k] = prim; }
+        R.t[R.n * RT] = t;
+        R.p[R.n * RT] = prim;
         R.n++;
         return false;
     }
-    float m = R.t[0];
+    double m = R.t[0];
     int jm = 0;
 #pragma unroll
-    for (int k = 1; k < RING; ++k)
-        if (R.t[k] < m) { m = R.t[k]; jm = k; }
+    for (int k = 1; k < RING; ++k) {
+        double tk = R.t[k * RT];
+        if (tk < m) { m = tk; jm = k; }
+    }
     if (t < m) { et = t; ep = prim; return true; }
-#pragma unroll
-    for (int k = 0; k < RING; ++k)
-        if (k == jm) { et = R.t[k]; ep = R.p[k]; R.t[k] = t; R.p[k] = prim; }
+    et = m;
+    ep = R.p[jm * RT];
+    R.t[jm * RT] = t;
+    R.p[jm * RT] = prim;
     return true;
 }
 
 // drain one entry (raster_kernels.py:227-270: first minimum, swap with last)
-__device__ __forceinline__ void ring_pop(Ring &R, float &et, int &ep)
+__device__ __forceinline__ void ring_pop(Ring &R, double &et, int &ep)
 {
-    float m = R.t[0];
+    double m = R.t[0];
     int jm = 0;
-#pragma unroll
-    for (int k = 1; k < RING; ++k)
-        if (k < R.n && R.t[k] < m) { m = R.t[k]; jm = k; }
+    for (int k = 1; k < R.n; ++k) {
+        double tk = R.t[k * RT];
+        if (tk < m) { m = tk; jm = k; }
+    }
+    et = m;
+    ep = R.p[jm * RT];
     R.n--;
-    float tl = 0.f;
-    int pl = 0;
-#pragma unroll
-    for (int k = 0; k < RING; ++k)
-        if (k == R.n) { tl = R.t[k]; pl = R.p[k]; }
-#pragma unroll
-    for (int k = 0; k < RING; ++k)
-        if (k == jm) { et = R.t[k]; ep = R.p[k]; R.t[k] = tl; R.p[k] = pl; }
+    R.t[jm * RT] = R.t[R.n * RT];
+    R.p[jm * RT] = R.p[R.n * RT];
 }
 
 struct Cfg {
@@ -128,24 +131,25 @@ __device__ __forceinline__ Cfg make_cfg(const SetK &st)
 }
 
 // candidate test shared by both passes (raster_kernels.py:121-130, 58-63)
-__device__ __forceinline__ bool accept(const PrimRec &r, int u, int v, float dx, float dy, float dz,
-                                       const Cfg &c, float &t)
+__device__ __forceinline__ bool accept(const PrimRec &r, const Geo64 &g, const double d64[3],
+                                       int u, int v, float dx, float dy, float dz, const Cfg &c,
+                                       double &t)
 {
     if (!in_box(r, u, v)) return false;
     Hit h;
-    if (!hit32(r, dx, dy, dz, c.euclid, c.t_clip, h)) return false;
+    if (!hit_refined(r, g, d64, dx, dy, dz, c.euclid, c.t_clip, h)) return false;
     if (r.alpha * h.G < c.alpha_floor) return false;
-    t = h.t;
+    t = h.t64;
     return true;
 }
 
 // candidate step: accept + ring; returns whether a fragment is emitted
-__device__ __forceinline__ bool stream_step(const PrimRec &r, int prim, int u, int v, float dx,
-                                            float dy, float dz, const Cfg &c, Ring &R, float &et,
-                                            int &ep)
+__device__ __forceinline__ bool stream_step(const PrimRec &r, const Geo64 &g, int prim,
+                                            const double d64[3], int u, int v, float dx, float dy,
+                                            float dz, const Cfg &c, Ring &R, double &et, int &ep)
 {
-    float t;
-    if (!accept(r, u, v, dx, dy, dz, c, t)) return false;
+    double t;
+    if (!accept(r, g, d64, u, v, dx, dy, dz, c, t)) return false;
     if (!c.resort) { et = t; ep = prim; return true; }
     return ring_push(R, t, prim, et, ep);
 }
@@ -158,11 +162,15 @@ struct Frag {
     float nl[3], nc[3], K, inrm, flip;
 };
 
-// re-shade an emitted fragment (raster_kernels.py:40-80)
-__device__ __forceinline__ void shade_full(const PrimRec &r, float dx, float dy, float dz,
-                                           const Cfg &c, Frag &f)
+// re-shade an emitted fragment at its fp64 depth (raster_kernels.py:40-80)
+__device__ __forceinline__ void shade_emitted(const PrimRec &r, const Geo64 &g, const double d64[3],
+                                              float dx, float dy, float dz, double t64,
+                                              const Cfg &c, Frag &f)
 {
-    hit32(r, dx, dy, dz, c.euclid, c.t_clip, f.h);
+    double dh[3];
+    local_dir64(g, d64, dh);
+    shade_at(r, g, dh, t64, c.euclid, f.h);
+    f.h.G = expf(-(f.h.l * f.h.l) / (2.f * f.h.sig * f.h.sig));
     float abar = r.alpha * f.h.G;
     f.clamped = abar > c.alpha_clamp;
     f.abar = f.clamped ? c.alpha_clamp : abar;
@@ -170,10 +178,18 @@ __device__ __forceinline__ void shade_full(const PrimRec &r, float dx, float dy,
     normal_curv32(r, f.h, dx, dy, dz, f.nl, f.nc, f.K, f.inrm, f.flip);
 }
 
+__device__ __forceinline__ void load_dir(RasterSmem &sm, double d[3])
+{
+    d[0] = sm.d64[0][threadIdx.x];
+    d[1] = sm.d64[1][threadIdx.x];
+    d[2] = sm.d64[2][threadIdx.x];
+}
+
 // ================================================================ forward
 
 __global__ void __launch_bounds__(RT, 2)
-raster_fwd_kernel(const PrimRec *__restrict__ recs, const int32_t *__restrict__ tile_offsets,
+raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
+                  const int32_t *__restrict__ tile_offsets,
                   const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets out)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -184,27 +200,35 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const int32_t *__restrict__ 
     const bool inside = u < cam.W && v < cam.H;
     const Cfg c = make_cfg(st);
     float dx = 0.f, dy = 0.f, dz = 1.f;
-    if (inside) pixel_dir(cam, u, v, dx, dy, dz);
+    {
+        double d[3] = {0.0, 0.0, 1.0};
+        if (inside) pixel_dir64(cam, u, v, d);
+        sm.d64[0][threadIdx.x] = d[0]; sm.d64[1][threadIdx.x] = d[1]; sm.d64[2][threadIdx.x] = d[2];
+        dx = (float)d[0]; dy = (float)d[1]; dz = (float)d[2];
+    }
     if (threadIdx.x == 0) sm.viol = 0;
 
     double T = 1.0, ac0 = 0, ac1 = 0, ac2 = 0, aa = 0, ad = 0, ad2 = 0, an0 = 0, an1 = 0,
            an2 = 0, ak = 0, adist = 0;
-    float median = 0.f, last_t = -3.0e38f;
+    float median = 0.f;
+    double last_t = -1.0e300;
     int nfrag = 0, viol = 0;
-    Ring R;
-    R.n = 0;
+    Ring R{&sm.ring_t[0][threadIdx.x], &sm.ring_p[0][threadIdx.x], 0};
     bool alive = inside;
 
-    auto composite = [&](const PrimRec &r, float et) {
+    auto composite = [&](int ep, double t) {
+        double d[3];
+        load_dir(sm, d);
         Frag f;
-        shade_full(r, dx, dy, dz, c, f);
-        if ((double)et < (double)last_t - 1e-12) viol++;
-        if (et > last_t) last_t = et;
-        double t = (double)et, w = f.abar64 * T;
+        shade_emitted(recs[ep], geo[ep], d, dx, dy, dz, t, c, f);
+        const PrimRec &r = recs[ep];
+        if (t < last_t - 1e-12) viol++;
+        if (t > last_t) last_t = t;
+        const double w = f.abar64 * T;
         ac0 += w * (double)r.col[0];
         ac1 += w * (double)r.col[1];
         ac2 += w * (double)r.col[2];
-        adist += w * (t * t * aa - 2.0 * t * ad + ad2);   // uses sums before this fragment
+        adist += w * (t * t * aa - 2.0 * t * ad + ad2);   // sums before this fragment
         aa += w;
         ad += w * t;
         ad2 += w * t * t;
@@ -212,7 +236,7 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const int32_t *__restrict__ 
         an1 += w * (double)f.nc[1];
         an2 += w * (double)f.nc[2];
         ak += w * (double)f.K;
-        if (T > 0.5) median = et;
+        if (T > 0.5) median = (float)t;
         T *= 1.0 - f.abar64;
         nfrag++;
         if (T < c.t_term) alive = false;
@@ -224,20 +248,23 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const int32_t *__restrict__ 
         const int nb = min(BATCH, end - b0);
         load_batch(sm, recs, tile_prims, b0, nb);
         if (!alive) continue;
+        double d[3];
+        load_dir(sm, d);
         for (int j = 0; j < nb; ++j) {
-            float et;
+            double et;
             int ep;
-            if (stream_step(sm.rec[j], sm.prim[j], u, v, dx, dy, dz, c, R, et, ep)) {
-                composite(ep == sm.prim[j] ? sm.rec[j] : recs[ep], et);
+            const int p = sm.prim[j];
+            if (stream_step(sm.rec[j], geo[p], p, d, u, v, dx, dy, dz, c, R, et, ep)) {
+                composite(ep, et);
                 if (!alive) break;
             }
         }
     }
     while (alive && R.n > 0) {
-        float et;
+        double et;
         int ep;
         ring_pop(R, et, ep);
-        composite(recs[ep], et);
+        composite(ep, et);
     }
 
     if (inside) {
@@ -397,20 +424,10 @@ __device__ __forceinline__ void frag_grad(const PrimRec &r, const Frag &f, float
         g_d2 += g_tt * oz / (hz * hz);
     } else {
         const float w1 = r.w1, w2 = r.w2, iw3 = r.iw3;
-        const float A = fmaf(w1 * hx, hx, w2 * hy * hy);
-        const float B = 2.f * fmaf(w1 * ox, hx, w2 * oy * hy) - iw3 * hz;
-        float gA, gB, gC;
-        if (h.branch == BR_LINEAR) {
-            const float iB = 1.f / B;
-            gA = 0.f;
-            gB = -g_tt * t * iB;
-            gC = -g_tt * iB;
-        } else {
-            const float iq = 1.f / fmaf(2.f * A, t, B);
-            gA = -g_tt * t * t * iq;
-            gB = -g_tt * t * iq;
-            gC = -g_tt * iq;
-        }
+        const float iq = 1.f / h.q;    // dF/dt (quad) or B (linear), accurate from fp64
+        const float gA = h.branch == BR_LINEAR ? 0.f : -g_tt * t * t * iq;
+        const float gB = -g_tt * t * iq;
+        const float gC = -g_tt * iq;
         g_w1 += gA * hx * hx + gB * 2.f * ox * hx + gC * ox * ox;
         g_w2 += gA * hy * hy + gB * 2.f * oy * hy + gC * oy * oy;
         g_iw3 += -gB * hz - gC * oz;
@@ -465,7 +482,8 @@ __device__ __forceinline__ void warp_accumulate(RasterSmem &sm, bool emit, int p
 }
 
 __global__ void __launch_bounds__(RT, 2)
-raster_bwd_kernel(const PrimRec *__restrict__ recs, const int32_t *__restrict__ tile_offsets,
+raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
+                  const int32_t *__restrict__ tile_offsets,
                   const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets fwd,
                   qgs_upstream upst, float *__restrict__ kg)
 {
@@ -498,9 +516,14 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const int32_t *__restrict__ 
     up.a = (float)ua64;
 
     float dx = 0.f, dy = 0.f, dz = 1.f;
+    {
+        double d[3] = {0.0, 0.0, 1.0};
+        if (inside) pixel_dir64(cam, u, v, d);
+        sm.d64[0][threadIdx.x] = d[0]; sm.d64[1][threadIdx.x] = d[1]; sm.d64[2][threadIdx.x] = d[2];
+        dx = (float)d[0]; dy = (float)d[1]; dz = (float)d[2];
+    }
     double F0 = 0, F1 = 0, F2 = 0, vtot = 0;
     if (inside && has_up) {
-        pixel_dir(cam, u, v, dx, dy, dz);
         const double *a = fwd.aux;
         F0 = a[AX_A * (size_t)npx + px];
         F1 = a[AX_D * (size_t)npx + px];
@@ -515,16 +538,18 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const int32_t *__restrict__ 
                (double)up.dist * 2.0 * a[AX_DIST * (size_t)npx + px];
     }
     double T = 1.0, pref = 0.0;
-    Ring R;
-    R.n = 0;
+    Ring R{&sm.ring_t[0][threadIdx.x], &sm.ring_p[0][threadIdx.x], 0};
     bool alive = inside && has_up;
 
-    auto emit_grad = [&](bool emit, const PrimRec &r, int ep, float et) {
+    auto emit_grad = [&](bool emit, int ep, double t) {
         float g[KG];
         if (emit) {
+            double d[3];
+            load_dir(sm, d);
             Frag f;
-            shade_full(r, dx, dy, dz, c, f);
-            const double t = (double)et, w = f.abar64 * T;
+            const PrimRec &r = recs[ep];
+            shade_emitted(r, geo[ep], d, dx, dy, dz, t, c, f);
+            const double w = f.abar64 * T;
             const double V = (double)up.c0 * r.col[0] + (double)up.c1 * r.col[1] +
                              (double)up.c2 * r.col[2] + ua64 + (double)up.d * t +
                              (double)up.n0 * f.nc[0] + (double)up.n1 * f.nc[1] +
@@ -544,47 +569,52 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const int32_t *__restrict__ 
         if (__syncthreads_count(alive) == 0) break;
         const int nb = min(BATCH, end - b0);
         load_batch(sm, recs, tile_prims, b0, nb);
+        double d[3];
+        load_dir(sm, d);
         for (int j = 0; j < nb; ++j) {
             if (!__any_sync(FULL, alive)) break;
-            float et = 0.f;
+            double et = 0.0;
             int ep = -1;
-            bool emit = alive && stream_step(sm.rec[j], sm.prim[j], u, v, dx, dy, dz, c, R, et, ep);
-            if (__any_sync(FULL, emit)) emit_grad(emit, (emit && ep == sm.prim[j]) ? sm.rec[j] : recs[emit ? ep : 0], ep, et);
+            const int p = sm.prim[j];
+            bool emit = alive && stream_step(sm.rec[j], geo[p], p, d, u, v, dx, dy, dz, c, R, et, ep);
+            if (__any_sync(FULL, emit)) emit_grad(emit, ep, et);
         }
     }
     while (__any_sync(FULL, alive && R.n > 0)) {
-        float et = 0.f;
+        double et = 0.0;
         int ep = -1;
         bool emit = alive && R.n > 0;
         if (emit) ring_pop(R, et, ep);
-        emit_grad(emit, recs[emit ? ep : 0], ep, et);
+        emit_grad(emit, ep, et);
     }
 }
 
 // ============================================================ diagnostics
 // Single-thread replay of one pixel's stream with the same inline functions:
 // records every accepted candidate and every emitted fragment (with T before).
-__global__ void trace_pixel_kernel(const PrimRec *__restrict__ recs,
+__global__ void trace_pixel_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
                                    const int32_t *__restrict__ tile_offsets,
                                    const int32_t *__restrict__ tile_prims, CamK cam, SetK st,
                                    int u, int v, int max, int *acc_prim, float *acc_t,
                                    float *acc_abar, int *em_prim, float *em_t, float *em_abar,
                                    double *em_T, int *counts)
 {
+    __shared__ double ring_t[RING][RT];
+    __shared__ int ring_p[RING][RT];
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const Cfg c = make_cfg(st);
-    float dx, dy, dz;
-    pixel_dir(cam, u, v, dx, dy, dz);
+    double d[3];
+    pixel_dir64(cam, u, v, d);
+    const float dx = (float)d[0], dy = (float)d[1], dz = (float)d[2];
     const int tile = (v / TILE) * cam.tiles_x + u / TILE;
-    Ring R;
-    R.n = 0;
+    Ring R{&ring_t[0][0], &ring_p[0][0], 0};
     double T = 1.0;
     int na = 0, ne = 0;
     bool alive = true;
-    auto record = [&](int ep, float et) {
+    auto record = [&](int ep, double et) {
         Frag f;
-        shade_full(recs[ep], dx, dy, dz, c, f);
-        if (ne < max) { em_prim[ne] = ep; em_t[ne] = et; em_abar[ne] = f.abar; em_T[ne] = T; }
+        shade_emitted(recs[ep], geo[ep], d, dx, dy, dz, et, c, f);
+        if (ne < max) { em_prim[ne] = ep; em_t[ne] = (float)et; em_abar[ne] = f.abar; em_T[ne] = T; }
         ne++;
         T *= 1.0 - f.abar64;
         if (T < c.t_term) alive = false;
@@ -592,15 +622,15 @@ __global__ void trace_pixel_kernel(const PrimRec *__restrict__ recs,
     for (int i = tile_offsets[tile]; i < tile_offsets[tile + 1] && alive; ++i) {
         const int p = tile_prims[i];
         const PrimRec &r = recs[p];
-        float t;
-        if (accept(r, u, v, dx, dy, dz, c, t)) {
+        double t;
+        if (accept(r, geo[p], d, u, v, dx, dy, dz, c, t)) {
             if (na < max) {
-                Hit h;
-                hit32(r, dx, dy, dz, c.euclid, c.t_clip, h);
-                acc_prim[na] = p; acc_t[na] = t; acc_abar[na] = r.alpha * h.G;
+                Frag f;
+                shade_emitted(r, geo[p], d, dx, dy, dz, t, c, f);
+                acc_prim[na] = p; acc_t[na] = (float)t; acc_abar[na] = f.abar;
             }
             na++;
-            float et;
+            double et;
             int ep;
             bool emit;
             if (!c.resort) { et = t; ep = p; emit = true; }
@@ -609,7 +639,7 @@ __global__ void trace_pixel_kernel(const PrimRec *__restrict__ recs,
         }
     }
     while (alive && R.n > 0) {
-        float et;
+        double et;
         int ep;
         ring_pop(R, et, ep);
         record(ep, et);

@@ -1,0 +1,251 @@
+// Raster-side shading of one (pixel ray, primitive) pair.
+//
+// Selection rule of fragment_geometry (intersect.py:58-115) and _shade
+// (raster_kernels.py:40-80).  Two stages:
+//
+//  1. Coarse fp32 test on every candidate: roots of A t^2 + B t + C (C
+//     precomputed per primitive in fp64) and the 3-sigma test with a 5%
+//     margin.  This polynomial form cancels badly (terms ~ w |o|^2 ~ 1e3-1e4
+//     summing to ~1 at the hit), so it only decides which roots are worth a
+//     precise look.
+//  2. Refinement in fp64 of each root that passes: one fp32 and two fp64
+//     Newton steps on the POINT-evaluated implicit function
+//     F(x) = w1 x^2 + w2 y^2 - iw3 z at x = ohat + t dhat (no cancellation),
+//     giving the depth t64 to ~1e-15.  The hit point is re-derived from t64
+//     in fp64 (shade_at), rounded once to fp32, and the exact selection
+//     (t > t_clip, ellipse pre-reject, l <= 3 sigma) and the Gaussian weight
+//     are evaluated from it.
+//
+// shade_at(t64) is also what re-shades an emitted fragment, so candidate
+// time and emission time see bit-identical values.  The ring orders by t64,
+// matching the reference's float64 depth order except at exact ties.
+#pragma once
+
+#include "qgs_common.cuh"
+
+namespace qgs {
+
+struct Hit {
+    double t64;
+    float t, x, y, rho, cth, sth, a, l, sig, G;
+    float q;                  // dt-denominator: F'(t) (quad), B (linear), dhz (planar)
+    float dhx, dhy, dhz;
+    int branch;
+};
+
+// arc length of z = a r^2 over [0, rho]; series below |u| = 0.3 (error < 1e-8)
+__device__ __forceinline__ float arc32(float a, float rho)
+{
+    float u = 2.f * a * rho;
+    if (fabsf(u) < 0.3f) {
+        float u2 = u * u;
+        return rho * (1.f + u2 * (1.f / 6.f + u2 * (-1.f / 40.f + u2 * (1.f / 112.f - u2 * (5.f / 1152.f)))));
+    }
+    float r = sqrtf(fmaf(u, u, 1.f));
+    float as = copysignf(logf(fabsf(u) + r), u);
+    return (as + u * r) / (4.f * a);
+}
+
+// (dl/da, dl/drho) on the same branch
+__device__ __forceinline__ void arc32_grad(float a, float rho, float l, float &dla, float &dlr)
+{
+    float u = 2.f * a * rho;
+    if (fabsf(u) < 0.3f) {
+        float u2 = u * u;
+        float fp = u * (1.f / 3.f + u2 * (-1.f / 10.f + u2 * (3.f / 56.f - u2 * (5.f / 144.f))));
+        dla = 2.f * rho * rho * fp;
+        dlr = 1.f + u2 * (0.5f + u2 * (-0.125f + u2 * (1.f / 16.f - u2 * (5.f / 128.f))));
+        return;
+    }
+    float r = sqrtf(fmaf(u, u, 1.f));
+    dla = (rho * r - l) / a;
+    dlr = r;
+}
+
+// polar coordinates, curvature coefficient, geodesic length and sigma at a
+// local point; returns the 3-sigma test (factor `k` widens it)
+__device__ __forceinline__ bool eval_point(const PrimRec &r, float x, float y, bool planar,
+                                           bool euclid, float k, Hit &h)
+{
+    float rho = sqrtf(fmaf(x, x, y * y));
+    float c = 1.f, s = 0.f;
+    if (rho > 1e-12f) { float ir = 1.f / rho; c = x * ir; s = y * ir; }
+    float a = planar ? 0.f : r.s3 * fmaf(r.w1 * c, c, r.w2 * s * s);
+    float l = (planar || euclid) ? rho : arc32(a, rho);
+    float sc = r.s2 * c, ss = r.s1 * s;
+    float sig = r.s12 * rsqrtf(fmaf(sc, sc, ss * ss));
+    h.x = x; h.y = y; h.rho = rho; h.cth = c; h.sth = s; h.a = a; h.l = l; h.sig = sig;
+    return l <= k * 3.f * sig;
+}
+
+__device__ __forceinline__ bool ellipse_out(const PrimRec &r, float x, float y, float k)
+{
+    float ex = r.s2 * x, ey = r.s1 * y;
+    return fmaf(ex, ex, ey * ey) > k * r.ell9;
+}
+
+// Exact evaluation at a given fp64 depth (candidate confirmation and
+// re-shading of emitted fragments).  dh64 = M d in fp64.
+__device__ __forceinline__ void shade_at(const PrimRec &r, const Geo64 &g, const double dh[3],
+                                         double t64, bool euclid, Hit &h)
+{
+    const bool planar = (r.flags & 1u) != 0;
+    double x = g.ohat[0] + t64 * dh[0];
+    double y = g.ohat[1] + t64 * dh[1];
+    h.t64 = t64;
+    h.t = (float)t64;
+    h.dhx = (float)dh[0]; h.dhy = (float)dh[1]; h.dhz = (float)dh[2];
+    if (planar) {
+        h.branch = BR_PLANAR;
+        h.q = (float)dh[2];
+    } else {
+        double w1 = g.wv[0], w2 = g.wv[1], iw3 = g.wv[2];
+        double A = w1 * dh[0] * dh[0] + w2 * dh[1] * dh[1];
+        double Fp = 2.0 * (w1 * x * dh[0] + w2 * y * dh[1]) - iw3 * dh[2];
+        if (fabs(A) < 1e-6) { h.branch = BR_LINEAR; h.q = (float)(Fp - 2.0 * A * t64); }
+        else { h.branch = BR_QUAD; h.q = (float)Fp; }
+    }
+    eval_point(r, (float)x, (float)y, planar, euclid, 1.f, h);
+}
+
+__device__ __forceinline__ void local_dir64(const Geo64 &g, const double d[3], double dh[3])
+{
+    dh[0] = g.M[0] * d[0] + g.M[1] * d[1] + g.M[2] * d[2];
+    dh[1] = g.M[3] * d[0] + g.M[4] * d[1] + g.M[5] * d[2];
+    dh[2] = g.M[6] * d[0] + g.M[7] * d[1] + g.M[8] * d[2];
+}
+
+// fp64 Newton on the point-evaluated implicit function starting at t0.
+// Linear branch (|A| < 1e-6, intersect.py:42-45) solves B t + C = 0 exactly
+// like the reference (the A t^2 term is removed from F); planar solves
+// oz + t dhz = 0.
+__device__ __forceinline__ double refine_depth(const Geo64 &g, const double dh[3], bool planar,
+                                               float t0)
+{
+    const double ox = g.ohat[0], oy = g.ohat[1], oz = g.ohat[2];
+    double t = (double)t0;
+    if (planar) {
+        float idz = 1.f / (float)dh[2];
+        for (int it = 0; it < 2; ++it) t -= (oz + t * dh[2]) * (double)idz;
+        return t;
+    }
+    const double w1 = g.wv[0], w2 = g.wv[1], iw3 = g.wv[2];
+    const double A = w1 * dh[0] * dh[0] + w2 * dh[1] * dh[1];
+    const double Alin = fabs(A) < 1e-6 ? A : 0.0;   // removed on the linear branch
+#pragma unroll
+    for (int it = 0; it < 3; ++it) {
+        double x = ox + t * dh[0], y = oy + t * dh[1], z = oz + t * dh[2];
+        double F = w1 * x * x + w2 * y * y - iw3 * z - Alin * t * t;
+        double Fp = 2.0 * (w1 * x * dh[0] + w2 * y * dh[1]) - iw3 * dh[2] - 2.0 * Alin * t;
+        t -= F * (double)(1.f / (float)Fp);
+    }
+    return t;
+}
+
+// Full candidate test: coarse fp32 roots, fp64 refinement, exact selection.
+// Returns the selected hit (valid, before the alpha floor) or false.
+__device__ __forceinline__ bool hit_refined(const PrimRec &r, const Geo64 &g, const double d64[3],
+                                            float dx, float dy, float dz, bool euclid,
+                                            float t_clip, Hit &h)
+{
+    constexpr float K = 1.05f;            // coarse margin on the 3-sigma tests
+    const bool planar = (r.flags & 1u) != 0;
+    float hx = fmaf(r.M[0], dx, fmaf(r.M[1], dy, r.M[2] * dz));
+    float hy = fmaf(r.M[3], dx, fmaf(r.M[4], dy, r.M[5] * dz));
+    float hz = fmaf(r.M[6], dx, fmaf(r.M[7], dy, r.M[8] * dz));
+    float roots[2];
+    int cnt = 0;
+    if (planar) {
+        if (fabsf(hz) < 1e-12f) return false;
+        roots[0] = -r.oz / hz;
+        cnt = 1;
+    } else {
+        float A = fmaf(r.w1 * hx, hx, r.w2 * hy * hy);
+        float B = 2.f * fmaf(r.w1 * r.ox, hx, r.w2 * r.oy * hy) - r.iw3 * hz;
+        float C = r.C;
+        if (fabsf(A) < 1e-6f) {
+            if (fabsf(B) < 1e-12f) return false;
+            roots[0] = -C / B;
+            cnt = 1;
+        } else {
+            float disc = fmaf(B, B, -4.f * A * C);
+            if (disc < 0.f) return false;
+            float sq = sqrtf(disc);
+            float q = -0.5f * (B + copysignf(sq, B));
+            float ra = q / A, rb = (q != 0.f) ? C / q : ra;
+            roots[0] = fminf(ra, rb);
+            roots[1] = fmaxf(ra, rb);
+            cnt = disc == 0.f ? 1 : 2;
+        }
+    }
+    double dh[3];
+    bool have_dh = false;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        if (k >= cnt) break;
+        const float t = roots[k];
+        if (!(t > t_clip * 0.99f)) continue;
+        float x = fmaf(t, hx, r.ox), y = fmaf(t, hy, r.oy);
+        if (!planar && ellipse_out(r, x, y, K * K)) continue;
+        Hit c;
+        if (!eval_point(r, x, y, planar, euclid, K, c)) continue;
+        // precise look
+        if (!have_dh) {
+            local_dir64(g, d64, dh);
+            have_dh = true;
+            if (planar && fabs(dh[2]) < 1e-12) return false;
+        }
+        double t64 = refine_depth(g, dh, planar, t);
+        if (!(t64 > (double)t_clip)) continue;
+        shade_at(r, g, dh, t64, euclid, h);
+        if (!planar && ellipse_out(r, h.x, h.y, 1.f)) continue;
+        if (!(h.l <= 3.f * h.sig)) continue;
+        h.G = expf(-(h.l * h.l) / (2.f * h.sig * h.sig));
+        return true;
+    }
+    return false;
+}
+
+// camera-frame camera-facing normal and Gaussian curvature at a hit
+__device__ __forceinline__ void normal_curv32(const PrimRec &r, const Hit &h, float dx, float dy,
+                                              float dz, float nl[3], float nc[3], float &K,
+                                              float &inrm, float &flip)
+{
+    if (h.branch == BR_PLANAR) {
+        nl[0] = 0.f; nl[1] = 0.f; nl[2] = -1.f; K = 0.f; inrm = 1.f;
+    } else {
+        float nx = 2.f * r.w1 * h.x, ny = 2.f * r.w2 * h.y, nz = -r.iw3;
+        inrm = rsqrtf(fmaf(nx, nx, fmaf(ny, ny, nz * nz)));
+        nl[0] = nx * inrm; nl[1] = ny * inrm; nl[2] = nz * inrm;
+        float l1x = r.lam1 * h.x, l2y = r.lam2 * h.y;
+        float den = 1.f + 4.f * fmaf(l1x, l1x, l2y * l2y);
+        K = 4.f * r.lam1 * r.lam2 / (den * den);
+    }
+    // Nmat = M^T (camera-from-local)
+    nc[0] = fmaf(r.M[0], nl[0], fmaf(r.M[3], nl[1], r.M[6] * nl[2]));
+    nc[1] = fmaf(r.M[1], nl[0], fmaf(r.M[4], nl[1], r.M[7] * nl[2]));
+    nc[2] = fmaf(r.M[2], nl[0], fmaf(r.M[5], nl[1], r.M[8] * nl[2]));
+    flip = 1.f;
+    if (fmaf(nc[0], dx, fmaf(nc[1], dy, nc[2] * dz)) > 0.f) {
+        flip = -1.f; nc[0] = -nc[0]; nc[1] = -nc[1]; nc[2] = -nc[2];
+    }
+}
+
+// camera-frame unit ray of pixel (u, v) in fp64 with the reference's
+// operation order (cameras.py:53-59), no FMA contraction
+__device__ __forceinline__ void pixel_dir64(const CamK &cam, int u, int v, double d[3])
+{
+    double a = __ddiv_rn(__dsub_rn(__dadd_rn((double)u, 0.5), cam.cx), cam.fx);
+    double b = __ddiv_rn(__dsub_rn(__dadd_rn((double)v, 0.5), cam.cy), cam.fy);
+    double n = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b)), 1.0));
+    d[0] = __ddiv_rn(a, n); d[1] = __ddiv_rn(b, n); d[2] = __ddiv_rn(1.0, n);
+}
+
+__device__ __forceinline__ bool in_box(const PrimRec &r, int u, int v)
+{
+    int umin = (int)(r.bb_u & 0xffffu), umax = (int)(r.bb_u >> 16);
+    int vmin = (int)(r.bb_v & 0xffffu), vmax = (int)(r.bb_v >> 16);
+    return u >= umin && u <= umax && v >= vmin && v <= vmax;
+}
+
+}  // namespace qgs
