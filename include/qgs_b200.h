@@ -141,7 +141,8 @@ int qgs_forward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_se
 
 /* ---- stage 4: backward raster (raster_kernels.py:289-681).  kg is
  *      P*QGS_KG_STRIDE floats, zeroed by the caller; slots: ohat 0-2,
- *      M 3-11 (with the Nmat^T terms folded in), w 12-14 and s 15-17 (with
+ *      X 3-11 (local-frame rotation accumulator, g_R = R X; replaces the
+ *      reference's M and Nmat slots), w 12-14 and s 15-17 (with
  *      the lambda terms folded in), alpha 18, colour 19-21. */
 int qgs_backward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settings *st,
                  const int32_t *tile_offsets, const int32_t *tile_prims,

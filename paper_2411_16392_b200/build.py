@@ -27,7 +27,6 @@ UNITS = {
     "raster.cu": ["-fmad=true"],
     "abi.cu": [],
 }
-HEADERS = ["qgs_common.cuh", "kernels.cuh"]
 
 
 def nvcc():
@@ -46,7 +45,8 @@ def _stale(target, deps):
 
 def build(force=False, verbose=False):
     os.makedirs(OBJ, exist_ok=True)
-    hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INCLUDE, "qgs_b200.h")]
+    hdrs = [os.path.join(CSRC, h) for h in sorted(os.listdir(CSRC)) if h.endswith(".cuh")]
+    hdrs.append(os.path.join(INCLUDE, "qgs_b200.h"))
     objs = []
     for unit, flags in UNITS.items():
         src = os.path.join(CSRC, unit)

@@ -226,7 +226,9 @@ int qgs_backward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_s
                  const int32_t *tile_offsets, const int32_t *tile_prims, const qgs_targets *fwd,
                  const qgs_upstream *up, float *kg, qgs_stream_t stream)
 {
-    if (!prep || !st || !fwd || !up || !kg || !tile_offsets) return fail(QGS_E_ARG, "NULL argument");
+    if (!prep || !st || !fwd || !up || !tile_offsets || (!kg && P > 0))
+        return fail(QGS_E_ARG, "NULL argument");
+    if (P == 0) return 0;
     if (!fwd->aux) return fail(QGS_E_ARG, "backward needs the forward's aux planes");
     if (int rc = check_cam(cam)) return rc;
     if (int rc = configure()) return rc;
@@ -245,9 +247,10 @@ int qgs_chain(const qgs_params *prims, const void *prep, const float *kg, const 
               const qgs_grads *out, qgs_stream_t stream)
 {
     (void)prep;
-    if (!prims || !kg || !out) return fail(QGS_E_ARG, "NULL argument");
+    if (!prims || !out) return fail(QGS_E_ARG, "NULL argument");
     if (int rc = check_cam(cam)) return rc;
     if (prims->P == 0) return 0;
+    if (!kg) return fail(QGS_E_ARG, "NULL argument");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     qgs::CamK ck = qgs::make_camk(*cam);
     qgs::chain_kernel<<<cdiv(prims->P, 128), 128, 0, s>>>(*prims, ck, kg, *out);

@@ -315,14 +315,16 @@ __global__ void chain_kernel(qgs_params prm, CamK cam, const float *__restrict__
     }
     out.raw_opacity[p] += (float)(gk[KG_ALPHA] * alpha * (1.0 - alpha));
 
-    // rotation: g_R[a][b] = sum_k Rwc[k][a] g_M[b][k] + (eye - c)_a g_ohat_b
-    double e[3] = {cam.eye[0] - c[0], cam.eye[1] - c[1], cam.eye[2] - c[2]};
+    // rotation (rasterizer.py:308-311): the raster kernel accumulates
+    // X = sum x_loc (x) g_ohat + dhat (x) dl + g_nl (x) nl, which equals
+    // R^T [R_cw g_M^T + (eye - c) g_ohat^T + R_cw g_Nmat] of the reference,
+    // so g_R = R X.
     double gR[9];
     for (int a = 0; a < 3; ++a)
         for (int b = 0; b < 3; ++b) {
             double acc = 0.0;
-            for (int k = 0; k < 3; ++k) acc += cam.Rwc[3 * k + a] * gk[KG_M + 3 * b + k];
-            gR[3 * a + b] = acc + e[a] * gk[KG_OHAT + b];
+            for (int j = 0; j < 3; ++j) acc += R[3 * a + j] * gk[KG_M + 3 * j + b];
+            gR[3 * a + b] = acc;
         }
     // quat_rot_backward (model.py:90-110)
     double w = qn[0], x = qn[1], y = qn[2], z = qn[3];

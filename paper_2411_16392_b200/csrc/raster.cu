@@ -356,9 +356,13 @@ __device__ __forceinline__ void frag_grad(const PrimRec &r, const Frag &f, float
         g_rho = g_l * dlr;
     }
     float g_w1 = 0.f, g_w2 = 0.f, g_iw3 = 0.f;
-    float gM[9];
-#pragma unroll
-    for (int i = 0; i < 9; ++i) gM[i] = 0.f;
+    float g_nl[3];            // d L / d (local unit normal), = flip * M * g_nc
+    {
+        const float fl = f.flip;
+        g_nl[0] = fl * fmaf(r.M[0], gcx, fmaf(r.M[1], gcy, r.M[2] * gcz));
+        g_nl[1] = fl * fmaf(r.M[3], gcx, fmaf(r.M[4], gcy, r.M[5] * gcz));
+        g_nl[2] = fl * fmaf(r.M[6], gcx, fmaf(r.M[7], gcy, r.M[8] * gcz));
+    }
     if (h.branch != BR_PLANAR) {
         const float w1 = r.w1, w2 = r.w2;
         float gs3 = g_a * fmaf(w1 * cth, cth, w2 * sth * sth);
@@ -379,20 +383,11 @@ __device__ __forceinline__ void frag_grad(const PrimRec &r, const Frag &f, float
         g_w1 += g_l1 * s3;
         g_w2 += g_l2 * s3;
         g[KG_S + 2] = gs3;
-        // camera normal nc = flip * Nmat nl, Nmat = M^T; g_Nmat[i][j] -> g_M[j][i]
-        const float fl = f.flip;
-        const float g_nlx = fl * fmaf(r.M[0], gcx, fmaf(r.M[1], gcy, r.M[2] * gcz));
-        const float g_nly = fl * fmaf(r.M[3], gcx, fmaf(r.M[4], gcy, r.M[5] * gcz));
-        const float g_nlz = fl * fmaf(r.M[6], gcx, fmaf(r.M[7], gcy, r.M[8] * gcz));
-        const float fgc[3] = {fl * gcx, fl * gcy, fl * gcz};
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-#pragma unroll
-            for (int j = 0; j < 3; ++j) gM[3 * j + i] += fgc[i] * f.nl[j];
-        const float dot = fmaf(f.nl[0], g_nlx, fmaf(f.nl[1], g_nly, f.nl[2] * g_nlz));
-        const float g_ntx = (g_nlx - f.nl[0] * dot) * f.inrm;
-        const float g_nty = (g_nly - f.nl[1] * dot) * f.inrm;
-        const float g_ntz = (g_nlz - f.nl[2] * dot) * f.inrm;
+        // through the normalisation of ntilde = (2 w1 x, 2 w2 y, -iw3)
+        const float dot = fmaf(f.nl[0], g_nl[0], fmaf(f.nl[1], g_nl[1], f.nl[2] * g_nl[2]));
+        const float g_ntx = (g_nl[0] - f.nl[0] * dot) * f.inrm;
+        const float g_nty = (g_nl[1] - f.nl[1] * dot) * f.inrm;
+        const float g_ntz = (g_nl[2] - f.nl[2] * dot) * f.inrm;
         g_w1 += 2.f * x * g_ntx;
         g_x += 2.f * w1 * g_ntx;
         g_w2 += 2.f * y * g_nty;
@@ -400,10 +395,6 @@ __device__ __forceinline__ void frag_grad(const PrimRec &r, const Frag &f, float
         g_iw3 += -g_ntz;
     } else {
         g[KG_S + 2] = 0.f;
-        const float fl = f.flip;
-        gM[6 + 0] += -fl * gcx;
-        gM[6 + 1] += -fl * gcy;
-        gM[6 + 2] += -fl * gcz;
     }
     // polar coordinates of the hit
     if (rho > 1e-12f) {
@@ -413,44 +404,52 @@ __device__ __forceinline__ void frag_grad(const PrimRec &r, const Frag &f, float
     }
     g_x += g_rho * cth;
     g_y += g_rho * sth;
-    // hit point x = ohat + t dhat
+    // Hit point x = ohat + t dhat and the root t(ohat, dhat, w): the
+    // reference's gA dh^2 + gB 2 o dh + gC o^2 (raster_kernels.py:464-482)
+    // collapses exactly to the point form k x^2 with k = -g_tt / F'(t); the
+    // point form keeps fp32 accuracy (the polynomial form cancels terms
+    // ~|o|^2 down to ~x^2).
     const float hx = h.dhx, hy = h.dhy, hz = h.dhz;
     const float g_tt = g_t + g_x * hx + g_y * hy;
-    float g_o0 = g_x, g_o1 = g_y, g_o2 = 0.f;
-    float g_d0 = g_x * t, g_d1 = g_y * t, g_d2 = 0.f;
-    const float ox = r.ox, oy = r.oy, oz = r.oz;
+    const float k = -g_tt / h.q;
+    float go[3], dl[3] = {0.f, 0.f, 0.f};   // d L / d ohat; dhat term beyond t * go
     if (h.branch == BR_PLANAR) {
-        g_o2 += -g_tt / hz;
-        g_d2 += g_tt * oz / (hz * hz);
+        go[0] = g_x; go[1] = g_y; go[2] = k;     // F = oz + t dhz
     } else {
         const float w1 = r.w1, w2 = r.w2, iw3 = r.iw3;
-        const float iq = 1.f / h.q;    // dF/dt (quad) or B (linear), accurate from fp64
-        const float gA = h.branch == BR_LINEAR ? 0.f : -g_tt * t * t * iq;
-        const float gB = -g_tt * t * iq;
-        const float gC = -g_tt * iq;
-        g_w1 += gA * hx * hx + gB * 2.f * ox * hx + gC * ox * ox;
-        g_w2 += gA * hy * hy + gB * 2.f * oy * hy + gC * oy * oy;
-        g_iw3 += -gB * hz - gC * oz;
-        g_o0 += gB * 2.f * w1 * hx + gC * 2.f * w1 * ox;
-        g_o1 += gB * 2.f * w2 * hy + gC * 2.f * w2 * oy;
-        g_o2 += -gC * iw3;
-        g_d0 += gA * 2.f * w1 * hx + gB * 2.f * w1 * ox;
-        g_d1 += gA * 2.f * w2 * hy + gB * 2.f * w2 * oy;
-        g_d2 += -gB * iw3;
+        go[0] = g_x + k * 2.f * w1 * x;
+        go[1] = g_y + k * 2.f * w2 * y;
+        go[2] = -k * iw3;
+        if (h.branch == BR_LINEAR) {
+            // t = -C/B ignores A: dhat gets t*(2 w o) instead of t*(2 w x)
+            g_w1 += k * (x * x - t * t * hx * hx);
+            g_w2 += k * (y * y - t * t * hy * hy);
+            dl[0] = -k * t * t * 2.f * w1 * hx;
+            dl[1] = -k * t * t * 2.f * w2 * hy;
+        } else {
+            g_w1 += k * x * x;
+            g_w2 += k * y * y;
+        }
+        g_iw3 += -k * h.z;
     }
     g[KG_W + 0] = g_w1;
     g[KG_W + 1] = g_w2;
     g[KG_W + 2] = g_iw3;
-    g[KG_OHAT + 0] = g_o0;
-    g[KG_OHAT + 1] = g_o1;
-    g[KG_OHAT + 2] = g_o2;
-    const float gd[3] = {g_d0, g_d1, g_d2}, dd[3] = {dx, dy, dz};
+    g[KG_OHAT + 0] = go[0];
+    g[KG_OHAT + 1] = go[1];
+    g[KG_OHAT + 2] = go[2];
+    // X = x_loc (x) g_ohat + dhat (x) dl + g_nl (x) nl, so that the chain's
+    // rotation gradient is g_R = R X (no cancellation between the ohat and
+    // M = R^T R_cw paths, which are each ~|eye - c| / |x| larger than it).
+    const float xl[3] = {x, y, h.z}, dh3[3] = {hx, hy, hz};
 #pragma unroll
-    for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
 #pragma unroll
-        for (int j = 0; j < 3; ++j) g[KG_M + 3 * i + j] = gM[3 * i + j] + gd[i] * dd[j];
+        for (int b = 0; b < 3; ++b)
+            g[KG_M + 3 * j + b] = fmaf(xl[j], go[b], fmaf(dh3[j], dl[b], g_nl[j] * f.nl[b]));
     g[22] = 0.f;
     g[23] = 0.f;
+    (void)dx; (void)dy; (void)dz;
 }
 
 // sum the slots of lanes that emitted the same primitive; one atomic per slot

@@ -27,7 +27,7 @@ namespace qgs {
 
 struct Hit {
     double t64;
-    float t, x, y, rho, cth, sth, a, l, sig, G;
+    float t, x, y, z, rho, cth, sth, a, l, sig, G;
     float q;                  // dt-denominator: F'(t) (quad), B (linear), dhz (planar)
     float dhx, dhy, dhz;
     int branch;
@@ -92,6 +92,7 @@ __device__ __forceinline__ void shade_at(const PrimRec &r, const Geo64 &g, const
     const bool planar = (r.flags & 1u) != 0;
     double x = g.ohat[0] + t64 * dh[0];
     double y = g.ohat[1] + t64 * dh[1];
+    h.z = (float)(g.ohat[2] + t64 * dh[2]);
     h.t64 = t64;
     h.t = (float)t64;
     h.dhx = (float)dh[0]; h.dhy = (float)dh[1]; h.dhz = (float)dh[2];
@@ -142,6 +143,51 @@ __device__ __forceinline__ double refine_depth(const Geo64 &g, const double dh[3
     return t;
 }
 
+// exact selection + weight at an fp64 depth; false if the root is rejected
+__device__ __forceinline__ bool confirm_root(const PrimRec &r, const Geo64 &g, const double dh[3],
+                                             double t64, bool planar, bool euclid, float t_clip,
+                                             Hit &h)
+{
+    if (!(t64 > (double)t_clip)) return false;
+    shade_at(r, g, dh, t64, euclid, h);
+    if (!planar && ellipse_out(r, h.x, h.y, 1.f)) return false;
+    if (!(h.l <= 3.f * h.sig)) return false;
+    h.G = expf(-(h.l * h.l) / (2.f * h.sig * h.sig));
+    return true;
+}
+
+// Near-tangent rays: the fp32 discriminant is within its rounding band of
+// zero, so root existence is decided in fp64 with the reference's own closed
+// form (intersect.py:39-55).  Rare.
+__device__ __noinline__ bool hit_marginal(const PrimRec &r, const Geo64 &g, const double d64[3],
+                                          bool euclid, float t_clip, Hit &h)
+{
+    double dh[3];
+    local_dir64(g, d64, dh);
+    const double w1 = g.wv[0], w2 = g.wv[1], iw3 = g.wv[2];
+    const double ox = g.ohat[0], oy = g.ohat[1], oz = g.ohat[2];
+    const double A = w1 * dh[0] * dh[0] + w2 * dh[1] * dh[1];
+    const double B = 2.0 * (w1 * ox * dh[0] + w2 * oy * dh[1]) - iw3 * dh[2];
+    const double C = w1 * ox * ox + w2 * oy * oy - iw3 * oz;
+    double roots[2];
+    int cnt;
+    if (fabs(A) < 1e-6) {
+        if (fabs(B) < 1e-12) return false;
+        roots[0] = -C / B;
+        cnt = 1;
+    } else {
+        const double disc = B * B - 4.0 * A * C;
+        if (disc < 0.0) return false;
+        const double sa = A > 0.0 ? 1.0 : -1.0, sq = sqrt(disc);
+        roots[0] = (-B - sa * sq) / (2.0 * A);
+        roots[1] = (-B + sa * sq) / (2.0 * A);
+        cnt = disc == 0.0 ? 1 : 2;
+    }
+    for (int k = 0; k < cnt; ++k)
+        if (confirm_root(r, g, dh, roots[k], false, euclid, t_clip, h)) return true;
+    return false;
+}
+
 // Full candidate test: coarse fp32 roots, fp64 refinement, exact selection.
 // Returns the selected hit (valid, before the alpha floor) or false.
 __device__ __forceinline__ bool hit_refined(const PrimRec &r, const Geo64 &g, const double d64[3],
@@ -169,6 +215,10 @@ __device__ __forceinline__ bool hit_refined(const PrimRec &r, const Geo64 &g, co
             cnt = 1;
         } else {
             float disc = fmaf(B, B, -4.f * A * C);
+            // fp32 rounding of disc is ~1e-7 max(B^2, |4AC|); inside a 1e-5 band
+            // the sign is decided in fp64
+            if (fabsf(disc) <= 1e-5f * fmaxf(B * B, fabsf(4.f * A * C)))
+                return hit_marginal(r, g, d64, euclid, t_clip, h);
             if (disc < 0.f) return false;
             float sq = sqrtf(disc);
             float q = -0.5f * (B + copysignf(sq, B));
@@ -196,12 +246,7 @@ __device__ __forceinline__ bool hit_refined(const PrimRec &r, const Geo64 &g, co
             if (planar && fabs(dh[2]) < 1e-12) return false;
         }
         double t64 = refine_depth(g, dh, planar, t);
-        if (!(t64 > (double)t_clip)) continue;
-        shade_at(r, g, dh, t64, euclid, h);
-        if (!planar && ellipse_out(r, h.x, h.y, 1.f)) continue;
-        if (!(h.l <= 3.f * h.sig)) continue;
-        h.G = expf(-(h.l * h.l) / (2.f * h.sig * h.sig));
-        return true;
+        if (confirm_root(r, g, dh, t64, planar, euclid, t_clip, h)) return true;
     }
     return false;
 }

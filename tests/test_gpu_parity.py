@@ -86,7 +86,10 @@ def test_sorted_keys_end_to_end(rz, name):
     prep = rz.prepare(gc.prims, gc.cam, _settings(rz, gc))
     got = prep.sorted_keys().cpu().numpy()
     ulp = np.abs(got.view(np.int64) - vw.keys.view(np.int64))
-    assert ulp.max() <= 64, f"max key difference {ulp.max()} ulp"
+    rel = np.abs(got - vw.keys) / np.abs(vw.keys)
+    exact = float((ulp == 0).mean())
+    assert rel.max() <= 1e-9, (f"max key rel diff {rel.max():.2e} ({ulp.max()} ulp), "
+                               f"{exact:.1%} bit-identical")
 
 
 @pytest.mark.parametrize("name", SCENES)
