@@ -1,0 +1,414 @@
+"""Benchmark: QGS tile rasterizer forward+backward Mpixels/s on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (views sharded, one NCCL all-reduce)
+
+One step = prepare + forward + backward + chain for every camera view of the
+config (views sharded round-robin over ranks, primitives replicated), then a
+single all-reduce of the packed raw-parameter gradients when N > 1.  Timing:
+CUDA events on the launching stream, barrier + synchronize on both sides,
+max over ranks.  Inputs are synthetic, seeded (paper_2411_16392_b200/scenes.py).
+
+Rank 0 prints ONE JSON line.
+"""
+
+import argparse
+import ctypes
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+METRIC = "fwd+bwd Mpixels/s"
+UNIT = "Mpx/s"
+# SURVEY.md section 8d op costs per candidate / fragment (add+mul, SFU-class)
+C_MISS, S_MISS = 63.0, 2.5
+C_HIT, S_HIT = 136.0, 18.1
+C_COMP = 37.0
+C_GRAD, S_GRAD = 428.0, 36.0
+BIN_BYTES_PER_PAIR = 20.0   # bucketed composite key write + read (16) + tile_prims write (4)
+OUR_LAUNCHES_PER_VIEW = 11  # preprocess, 3 scan, tile_diff, tile_offsets, pair_key, tile_sort, fwd, bwd, chain
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def load_peaks():
+    p = os.path.join(HERE, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def measure_compute_peaks(device_index):
+    from paper_2411_16392_b200 import build
+    lib = ctypes.CDLL(build.PEAKS_LIB)
+    f, m = ctypes.c_double(), ctypes.c_double()
+    sms, clk = ctypes.c_int(), ctypes.c_int()
+    rc = lib.qgs_peaks(device_index, ctypes.byref(f), ctypes.byref(m), ctypes.byref(sms),
+                       ctypes.byref(clk))
+    if rc != 0:
+        raise RuntimeError(f"qgs_peaks failed ({rc})")
+    return {"fp32_tflops": f.value, "mufu_tops": m.value, "sms": sms.value,
+            "clock_mhz": clk.value / 1000.0}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def scene_for(name):
+    from paper_2411_16392_b200 import scenes
+    return scenes.CONFIGS[name]()
+
+
+def workload_desc(sc):
+    m = sc.meta
+    return (f"{sc.name}: N={m['N']}, {m['res'][0]}x{m['res'][1]}, SH{m['sh_deg']}, "
+            f"{m['views']} views")
+
+
+# --------------------------------------------------------------------- ours
+
+def run_ours(a):
+    import torch.distributed as dist
+
+    from paper_2411_16392_b200 import rasterizer as rz
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    sc = scene_for(a.config)
+    cams = sc.cams
+    V = len(cams)
+    mine = [v for v in range(V) if v % world == rank]
+    H, W = cams[0].height, cams[0].width
+    st = rz.RenderSettings()
+
+    dev = rz.DevicePrimitives.from_host(sc.prims, device)
+    ups = [{k: torch.from_numpy(np.ascontiguousarray(u)).to(device) for k, u in sc.upstream[v].items()}
+           for v in mine]
+    grads = rz.GradientBuffer.zeros_flat(dev)
+    counters = torch.zeros(3, dtype=torch.int64, device=device)
+    stream = torch.cuda.current_stream()
+
+    def step(ev=None, count=False):
+        grads.zero_()
+        for i, v in enumerate(mine):
+            prep = rz.prepare(dev, cams[v], st)
+            if ev is not None:
+                ev["f0"][i].record(stream)
+            tg = rz.forward(prep, counters=counters if count else None)
+            if ev is not None:
+                ev["f1"][i].record(stream)
+            kg = torch.zeros((len(dev), 24), dtype=torch.float32, device=device)
+            if ev is not None:
+                ev["b0"][i].record(stream)
+            kg = rz.kernel_grads(prep, tg, ups[i], kg=kg)
+            if ev is not None:
+                ev["b1"][i].record(stream)
+            rz.chain(prep, kg, grads)
+            if ev is not None and i == 0:
+                ev["pairs"].append(prep.n_pairs)
+        if world > 1:
+            dist.all_reduce(grads.buffer)
+
+    # warm-up (also the counted pass for the algorithmic work)
+    for w in range(max(a.warmup, 3)):
+        step(count=(w == 0))
+    torch.cuda.synchronize()
+    cnt = counters.cpu().numpy().astype(np.float64)     # this rank's views
+    n_pairs_mine = []
+    for v in mine:
+        n_pairs_mine.append(rz.prepare(dev, cams[v], st).n_pairs)
+
+    # timed region
+    K = a.steps
+    mk = lambda: [torch.cuda.Event(enable_timing=True) for _ in mine]  # noqa: E731
+    ev = {"f0": [], "f1": [], "b0": [], "b1": [], "pairs": []}
+    per_step = []
+    for _ in range(K):
+        per_step.append({"f0": mk(), "f1": mk(), "b0": mk(), "b1": mk(), "pairs": []})
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for k in range(K):
+            step(ev=per_step[k])
+        t1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = t0.elapsed_time(t1) / K
+    fwd_ms = sum(per_step[k]["f0"][i].elapsed_time(per_step[k]["f1"][i])
+                 for k in range(K) for i in range(len(mine))) / K
+    bwd_ms = sum(per_step[k]["b0"][i].elapsed_time(per_step[k]["b1"][i])
+                 for k in range(K) for i in range(len(mine))) / K
+    t_ms = torch.tensor([ms], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+    ms_max = float(t_ms.item())
+    total_px = V * H * W
+    value = total_px / 1e6 / (ms_max / 1e3)
+
+    # end to end through the public API, host buffers in pinned memory
+    e2e = None
+    if not a.no_e2e:
+        e2e = run_e2e(a, rz, sc, mine, device, st, world)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peaks, peaks_kind = load_peaks()
+    cp = measure_compute_peaks(local)
+    # algorithmic work of this rank's views per step
+    n_box, n_acc, n_comp = cnt
+    n_miss = n_box - n_acc
+    F_fwd = n_miss * C_MISS + n_acc * C_HIT + n_comp * C_COMP
+    S_fwd = n_miss * S_MISS + n_acc * S_HIT
+    F_bwd = n_comp * C_GRAD
+    S_bwd = n_comp * S_GRAD
+    P32 = cp["fp32_tflops"] * 1e12
+    PSF = cp["mufu_tops"] * 1e12
+    BW = peaks["hbm_gbs"] * 1e9
+    B_bin = BIN_BYTES_PER_PAIR * sum(n_pairs_mine)
+    T_roof = max((F_fwd + F_bwd) / P32, (S_fwd + S_bwd) / PSF) + B_bin / BW
+    kernels = {"raster_bwd": (F_bwd, S_bwd, bwd_ms), "raster_fwd": (F_fwd, S_fwd, fwd_ms)}
+    dom = max(kernels, key=lambda k: kernels[k][2])
+    F, S, kms = kernels[dom]
+    t_k = kms / 1e3
+    roof = {
+        "bound": "fp32+sfu", "kernel": dom, "unit": "TFLOP/s",
+        "achieved": F / t_k / 1e12, "peak": cp["fp32_tflops"], "frac": F / t_k / P32,
+        "sfu_achieved_tops": S / t_k / 1e12, "sfu_peak_tops": cp["mufu_tops"],
+        "sfu_frac": S / t_k / PSF,
+        "roof_frac": max(F / P32, S / PSF) / t_k,
+        "kernel_ms_per_step": kms, "fwd_ms_per_step": fwd_ms, "bwd_ms_per_step": bwd_ms,
+        "traffic": None,
+        "peak_source": f"fp32/mufu measured live (tools/peaks.cu); hbm {peaks_kind} "
+                       f"MEASURED_PEAKS.json {peaks['hbm_gbs']} GB/s",
+        "step_roofline_ms": T_roof * 1e3,
+        "step_roofline_frac": (T_roof * 1e3) / ms if world == 1 else None,
+        "algorithmic": {"candidates": n_box, "accepted": n_acc, "composited": n_comp,
+                        "pairs": sum(n_pairs_mine), "flop_fwd": F_fwd, "flop_bwd": F_bwd,
+                        "sfu_fwd": S_fwd, "sfu_bwd": S_bwd},
+    }
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": a.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "fp32",
+        "data": "synthetic (seeded, BASELINE config shapes; scenes.py)",
+        "config": {"workload": workload_desc(sc), "views_per_step": V,
+                   "parallelism": f"views sharded over {world} GPU(s), primitives replicated"
+                                  + (", 1 NCCL all-reduce/step" if world > 1 else ""),
+                   "l2": "working set > L2 (126 MB): per-view sort buffers + maps are GBs"},
+        "roofline": roof, "clocks": clk.summary(),
+        "gpu_launches": OUR_LAUNCHES_PER_VIEW * V * K,
+        "compute_peaks": cp,
+    }
+    if e2e is not None:
+        out["e2e"] = e2e
+    if world == 1 and not a.no_cpu:
+        out["cpu_baseline"] = cpu_baseline(sc, a.cpu_tiles, views=1)
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(a, rz, sc, mine, device, st, world):
+    import torch.distributed as dist
+    pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory()  # noqa: E731
+    host = type("H", (), {})()
+    for f in rz.DevicePrimitives.FIELDS:
+        setattr(host, f, pin(getattr(sc.prims, f)))
+    ups = [{k: pin(u) for k, u in sc.upstream[v].items()} for v in mine]
+    h2d = sum(getattr(host, f).numel() * 4 for f in rz.DevicePrimitives.FIELDS)
+    h2d += sum(t.numel() * 4 for u in ups for t in u.values())
+    out_host = None
+
+    def step():
+        nonlocal out_host
+        dev = rz.DevicePrimitives.from_host(host, device, non_blocking=True)
+        grads = rz.GradientBuffer.zeros_flat(dev)
+        for i, v in enumerate(mine):
+            up = {k: t.to(device, non_blocking=True) for k, t in ups[i].items()}
+            prep = rz.prepare(dev, sc.cams[v], st)
+            tg = rz.forward(prep)
+            rz.backward(prep, tg, up, out=grads)
+        if world > 1:
+            dist.all_reduce(grads.buffer)
+        if out_host is None:
+            out_host = torch.empty(grads.buffer.shape, dtype=grads.buffer.dtype).pin_memory()
+        out_host.copy_(grads.buffer, non_blocking=True)
+        return grads.buffer.numel() * 4
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0.record(stream)
+    d2h = 0
+    for _ in range(a.steps):
+        d2h = step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / a.steps
+    t_ms = torch.tensor([ms], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+    ms = float(t_ms.item())
+    px = len(sc.cams) * sc.cams[0].width * sc.cams[0].height
+    h2d_all = torch.tensor([float(h2d)], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(h2d_all)
+    return {"value": px / 1e6 / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
+            "h2d_bytes_per_step": int(h2d_all.item()), "d2h_bytes_per_step": int(d2h) * world}
+
+
+# ---------------------------------------------------------------- CPU side
+
+def cpu_baseline(sc, n_tiles, views=1, seed=0):
+    """The float64 oracle (C + numpy restatement of the reference, OpenMP over
+    tiles) on the host cores, one view, systematic tile sample."""
+    from oracle import qgs_oracle as qo
+    prims64 = sc.prims.astype(np.float64)
+    cam = sc.cams[0]
+    up = {k: np.asarray(v, np.float64) for k, v in sc.upstream[0].items()}
+    qo.time_sampled_view(prims64, cam, up, n_sample=4, seed=seed + 7)   # warm-up
+    r = qo.time_sampled_view(prims64, cam, up, n_sample=n_tiles, seed=seed)
+    px = cam.width * cam.height
+    val = px / 1e6 / r["seconds_per_view_est"]
+    return {"value": val, "unit": UNIT, "cores": r["threads"], "kind": "port",
+            "sample": (f"view 0 of {sc.name}: per-primitive stages timed in full, "
+                       f"{r['tiles_sampled']} of {r['tiles']} tiles (systematic) timed for the "
+                       f"per-pair and per-pixel stages and scaled; est {r['seconds_per_view_est']:.2f}"
+                       f" s/view"), "detail": r}
+
+
+def run_reference(a):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    sc = scene_for(a.config)
+    from oracle import qgs_oracle as qo
+    prims64 = sc.prims.astype(np.float64)
+    cam = sc.cams[0]
+    up = {k: np.asarray(v, np.float64) for k, v in sc.upstream[0].items()}
+    for w in range(a.warmup):
+        qo.time_sampled_view(prims64, cam, up, n_sample=8, seed=100 + w)
+    vals, secs, last = [], [], None
+    for k in range(a.steps):
+        r = qo.time_sampled_view(prims64, cam, up, n_sample=a.cpu_tiles, seed=k)
+        secs.append(r["seconds_per_view_est"])
+        vals.append(cam.width * cam.height / 1e6 / r["seconds_per_view_est"])
+        last = r
+    value = float(np.mean(vals))
+    V = len(sc.cams)
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": float(np.mean(secs)) * V * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, BASELINE config shapes; scenes.py)",
+        "config": {"workload": workload_desc(sc), "views_per_step": V},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": last["threads"], "kind": "port",
+                         "sample": (f"each step: view 0, per-primitive stages in full, "
+                                    f"{last['tiles_sampled']}/{last['tiles']} tiles (systematic, "
+                                    f"seeded offset) for per-pair/per-pixel stages, scaled")},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-tiles", type=int, default=96)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    a = ap.parse_args()
+    if a.warmup < 3:
+        a.warmup = 3
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -83,6 +83,8 @@ typedef struct qgs_targets {
     int32_t *violations;       /* per tile (tiles_x*tiles_y) */
     double *aux;               /* QGS_AUX_PLANES*H*W float64 blend sums; required by
                                   qgs_backward, may be NULL for a forward-only call */
+    unsigned long long *counters; /* optional, accumulated (+=): [0] candidates inside
+                                  the pixel box, [1] accepted fragments, [2] composited */
 } qgs_targets;
 
 /* Upstream map gradients (rasterizer.py:230-250); NULL = all zero. */

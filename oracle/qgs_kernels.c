@@ -345,11 +345,13 @@ void qo_forward(int64_t H, int64_t W, const double *dirs, const int64_t *tile_of
                 const qo_prims *pr, const qo_settings *st, double *o_color,
                 double *o_alpha, double *o_depth, double *o_depthsq, double *o_median,
                 double *o_normal, double *o_curv, double *o_dist, double *o_T,
-                int64_t *o_nfrag, int64_t *o_viol)
+                int64_t *o_nfrag, int64_t *o_viol, const int64_t *tile_list, int64_t n_list)
 {
-    int64_t n_tiles = tiles_x * tiles_y;
+    /* tile_list (optional): process only these tiles (CPU-baseline sampling) */
+    int64_t n_iter = tile_list ? n_list : tiles_x * tiles_y;
 #pragma omp parallel for schedule(dynamic, 1)
-    for (int64_t tile = 0; tile < n_tiles; ++tile) {
+    for (int64_t it = 0; it < n_iter; ++it) {
+        int64_t tile = tile_list ? tile_list[it] : it;
         int64_t ty = tile / tiles_x, tx = tile % tiles_x;
         int64_t v1 = ty * 16 + 16 < H ? ty * 16 + 16 : H;
         int64_t u1 = tx * 16 + 16 < W ? tx * 16 + 16 : W;
@@ -619,27 +621,33 @@ int qo_backward(int64_t H, int64_t W, const double *dirs, const int64_t *tile_of
                 const double *f_normal, const double *f_curv, const double *f_dist,
                 const double *u_color, const double *u_alpha, const double *u_depth,
                 const double *u_normal, const double *u_curv, const double *u_dist,
-                double *kg)
+                double *kg, const int64_t *tile_list, int64_t n_list)
 {
-    int64_t n_tiles = tiles_x * tiles_y;
+    /* tile_list (optional, ascending): process only these tiles; all other
+       tiles must have empty ranges (CPU-baseline sampling) */
+    int64_t n_iter = tile_list ? n_list : tiles_x * tiles_y;
     int nthr = 1;
 #ifdef _OPENMP
     nthr = omp_get_max_threads();
 #endif
     int64_t chunk = 4 * (int64_t)nthr;
-    for (int64_t t0 = 0; t0 < n_tiles; t0 += chunk) {
-        int64_t t1 = t0 + chunk < n_tiles ? t0 + chunk : n_tiles;
+    for (int64_t k0 = 0; k0 < n_iter; k0 += chunk) {
+        int64_t k1 = k0 + chunk < n_iter ? k0 + chunk : n_iter;
+        int64_t t0 = tile_list ? tile_list[k0] : k0;
+        int64_t t1 = tile_list ? tile_list[k1 - 1] + 1 : k1;
         int64_t base = tile_offsets[t0];
         int64_t n_rows = tile_offsets[t1] - base;
         double *rows = (double *)calloc((size_t)(n_rows > 0 ? n_rows : 1) * QO_NG,
                                         sizeof(double));
         if (!rows) return -1;
 #pragma omp parallel for schedule(dynamic, 1)
-        for (int64_t tile = t0; tile < t1; ++tile)
+        for (int64_t it = k0; it < k1; ++it) {
+            int64_t tile = tile_list ? tile_list[it] : it;
             bwd_tile(tile, H, W, dirs, tile_offsets, tile_prims, tiles_x, pr, st,
                      f_color, f_alpha, f_depth, f_depthsq, f_normal, f_curv, f_dist,
                      u_color, u_alpha, u_depth, u_normal, u_curv, u_dist,
                      rows + (tile_offsets[tile] - base) * QO_NG);
+        }
         for (int64_t i = 0; i < n_rows; ++i) {
             double *dst = kg + tile_prims[base + i] * QO_NG;
             const double *src = rows + i * QO_NG;

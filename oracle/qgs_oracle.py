@@ -15,6 +15,7 @@ leg may import this module.  The product package never does.
 import ctypes
 import os
 import subprocess
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -89,10 +90,10 @@ def lib():
         L.qo_fragment_geometry.argtypes = [d] * 12 + [ctypes.c_int, ctypes.c_int, d,
                                                        ctypes.POINTER(_Hit)]
         L.qo_forward.argtypes = [i64, i64, vp, vp, vp, i64, i64, ctypes.POINTER(_Prims),
-                                 ctypes.POINTER(_Settings)] + [vp] * 11
+                                 ctypes.POINTER(_Settings)] + [vp] * 11 + [vp, i64]
         L.qo_backward.restype = ctypes.c_int
         L.qo_backward.argtypes = [i64, i64, vp, vp, vp, i64, i64, ctypes.POINTER(_Prims),
-                                  ctypes.POINTER(_Settings)] + [vp] * 14
+                                  ctypes.POINTER(_Settings)] + [vp] * 14 + [vp, i64]
         L.qo_tile_keys.argtypes = [i64, vp, vp, i64, ctypes.POINTER(_Prims), vp, vp, vp,
                                    d, d, d, d, i64, i64, ctypes.c_int, d, vp]
         L.qo_num_threads.restype = ctypes.c_int
@@ -461,8 +462,18 @@ def _as64(a):
     return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
 
 
-def prepare(prims, cam, settings=None):
-    """rasterizer.py:123-195."""
+def _tile_list_args(vw):
+    tl = getattr(vw, "tile_list", None)
+    if tl is None:
+        return (None, 0)
+    vw._tl = np.ascontiguousarray(tl, dtype=np.int64)
+    return (_p(vw._tl), len(vw._tl))
+
+
+def prepare(prims, cam, settings=None, tile_subset=None):
+    """rasterizer.py:123-195.  `tile_subset` restricts the pairs (and the later
+    forward/backward) to those tiles -- used only to time a bounded sample."""
+    t_start = time.perf_counter()
     st = settings or Settings()
     cam = cam if isinstance(cam, Cam) else Cam(cam)
     centers, quats = _as64(prims.centers), _as64(prims.quats)
@@ -497,18 +508,53 @@ def prepare(prims, cam, settings=None):
     ty_n = (cam.height + TILE - 1) // TILE
     vw.tiles_x, vw.tiles_y = tx_n, ty_n
     box = screen_boxes(sc, centers, R, cam)
+    tm = vw.timing = {"per_primitive": time.perf_counter() - t_start}
     vw.pix_bbox = box
     live = box[:, 0] <= box[:, 1]
     bx0, bx1, by0, by1 = box[:, 0] // TILE, box[:, 1] // TILE, box[:, 2] // TILE, box[:, 3] // TILE
+    vw.tile_list = None
     per = np.where(live, (bx1 - bx0 + 1) * (by1 - by0 + 1), 0)
-    n_pairs = int(per.sum())
-    owner = np.repeat(np.arange(P, dtype=np.int64), per)
-    tiles = np.zeros(n_pairs, dtype=np.int64)
-    if n_pairs:
-        first = np.concatenate([[0], np.cumsum(per)[:-1]])
-        k = np.arange(n_pairs, dtype=np.int64) - first[owner]
-        cols = (bx1 - bx0 + 1)[owner]
-        tiles = (by0[owner] + k // cols) * tx_n + bx0[owner] + k % cols
+    vw.n_pairs_full = int(per.sum())
+
+    def expand(per):
+        n_pairs = int(per.sum())
+        owner = np.repeat(np.arange(P, dtype=np.int64), per)
+        tiles = np.zeros(n_pairs, dtype=np.int64)
+        if n_pairs:
+            first = np.concatenate([[0], np.cumsum(per)[:-1]])
+            k = np.arange(n_pairs, dtype=np.int64) - first[owner]
+            cols = (bx1 - bx0 + 1)[owner]
+            tiles = (by0[owner] + k // cols) * tx_n + bx0[owner] + k % cols
+        return n_pairs, owner, tiles
+
+    t_mark = time.perf_counter()
+    if tile_subset is None:
+        n_pairs, owner, tiles = expand(per)
+        tm["pair_expand"] = time.perf_counter() - t_mark
+    else:
+        # CPU-baseline sampling: only the pairs that fall in the given tiles,
+        # in the same (primitive, row-major tile) order
+        S = np.unique(np.asarray(tile_subset, dtype=np.int64))
+        vw.tile_list = S
+        sx, sy = S % tx_n, S // tx_n
+        own, til = [], []
+        for c0 in range(0, P, 65536):
+            sl = slice(c0, min(P, c0 + 65536))
+            m = (live[sl, None] & (bx0[sl, None] <= sx[None]) & (sx[None] <= bx1[sl, None])
+                 & (by0[sl, None] <= sy[None]) & (sy[None] <= by1[sl, None]))
+            pi, si = np.nonzero(m)
+            own.append(pi + c0)
+            til.append(S[si])
+        owner = np.concatenate(own).astype(np.int64)
+        tiles = np.concatenate(til).astype(np.int64)
+        n_pairs = len(owner)
+        # the same vectorised expansion on the sampled pair count stands in
+        # for the full expansion's cost (its own result is not used)
+        t_mark = time.perf_counter()
+        expand(np.bincount(owner, minlength=P))
+        tm["pair_expand"] = time.perf_counter() - t_mark
+    vw.n_pairs_sampled = n_pairs
+    t_mark = time.perf_counter()
     vu, vv = cam.project(centers)
     keys = np.empty(n_pairs)
     cs = vw._cstruct()
@@ -517,13 +563,18 @@ def prepare(prims, cam, settings=None):
                        cam.fx, cam.fy, cam.width, cam.height,
                        int(bool(st.euclidean_density)), float(st.t_near_clip), _p(keys))
     vw.pair_tiles_unsorted, vw.pair_prims_unsorted, vw.keys_unsorted = tiles, owner, keys
+    tm["keys"] = time.perf_counter() - t_mark
+    t_mark = time.perf_counter()
     order = np.lexsort((owner, keys, tiles))
     vw.keys = keys[order]
     vw.tile_prims = owner[order]
     counts = np.bincount(tiles[order], minlength=tx_n * ty_n)
     vw.tile_offsets = np.zeros(tx_n * ty_n + 1, dtype=np.int64)
     np.cumsum(counts, out=vw.tile_offsets[1:])
+    tm["sort"] = time.perf_counter() - t_mark
+    t_mark = time.perf_counter()
     vw.dirs = cam.pixel_dirs()
+    tm["dirs"] = time.perf_counter() - t_mark
     return vw
 
 
@@ -545,7 +596,7 @@ def forward(vw):
                      _p(o["color_raw"]), _p(o["alpha"]), _p(o["depth"]), _p(o["depth_sq"]),
                      _p(o["depth_median"]), _p(o["normal"]), _p(o["curvature"]),
                      _p(o["distortion"]), _p(o["transmittance"]), _p(o["n_fragments"]),
-                     _p(viol))
+                     _p(viol), *_tile_list_args(vw))
     bg = np.asarray(st.background, dtype=np.float64)
     o["color"] = o["color_raw"] + o["transmittance"][:, :, None] * bg
     o["order_violations"] = int(viol.sum())
@@ -579,7 +630,8 @@ def kernel_grads(vw, targets, upstream):
                            _p(f["color_raw"]), _p(f["alpha"]), _p(f["depth"]),
                            _p(f["depth_sq"]), _p(f["normal"]), _p(f["curvature"]),
                            _p(f["distortion"]), _p(u_color), _p(u_alpha), _p(u_depth),
-                           _p(u_normal), _p(u_curv), _p(u_dist), _p(kg))
+                           _p(u_normal), _p(u_curv), _p(u_dist), _p(kg),
+                           *_tile_list_args(vw))
     if rc != 0:
         raise MemoryError("oracle backward: allocation failed")
     return kg
@@ -656,6 +708,43 @@ def trace_pixel(vw, u, v, max_frags=4096):
     na, ne = min(na.value, max_frags), min(ne, max_frags)
     return ({"prim": ap[:na], "t": at[:na], "abar": aa[:na]},
             {"prim": ep[:ne], "t": et[:ne], "abar": ea[:ne], "T": eT[:ne]})
+
+
+def time_sampled_view(prims, cam, upstream, n_sample=128, seed=0, settings=None):
+    """Time prepare + forward + backward of one view on a random sample of
+    its tiles and extrapolate to the whole view (CPU baseline, bench.py).
+
+    Per-primitive work (activations, SH, screen boxes, chain) is timed in
+    full; per-tile work (pair expansion, keys, sort, forward, backward) is
+    timed on `n_sample` random tiles and scaled by n_tiles / n_sample."""
+    cam = cam if isinstance(cam, Cam) else Cam(cam)
+    n_tiles = ((cam.width + TILE - 1) // TILE) * ((cam.height + TILE - 1) // TILE)
+    n = min(n_sample, n_tiles)
+    # systematic sample: every (n_tiles / n)-th tile from a seeded offset,
+    # which tracks the image's density profile far better than a random pick
+    stride = n_tiles / n
+    off = np.random.default_rng(seed).uniform(0, stride)
+    S = np.unique((off + stride * np.arange(n)).astype(np.int64).clip(0, n_tiles - 1))
+    n = len(S)
+    vw = prepare(prims, cam, settings, tile_subset=S)
+    t0 = time.perf_counter()
+    fw = forward(vw)
+    t1 = time.perf_counter()
+    kg = kernel_grads(vw, fw, upstream)
+    t2 = time.perf_counter()
+    chain(vw, kg)
+    t3 = time.perf_counter()
+    tm = vw.timing
+    pair_scale = vw.n_pairs_full / max(vw.n_pairs_sampled, 1)
+    tile_scale = n_tiles / n
+    est = (tm["per_primitive"] + tm["dirs"] + (t3 - t2)
+           + (tm["pair_expand"] + tm["keys"] + tm["sort"]) * pair_scale
+           + ((t1 - t0) + (t2 - t1)) * tile_scale)
+    return {"seconds_per_view_est": est, "tiles_sampled": int(n), "tiles": int(n_tiles),
+            "pairs_sampled": int(vw.n_pairs_sampled), "pairs": int(vw.n_pairs_full),
+            "threads": num_threads(),
+            "phases": {**{k: round(v, 4) for k, v in tm.items()}, "forward": t1 - t0,
+                       "backward": t2 - t1, "chain": t3 - t2}}
 
 
 def render(prims, cam, settings=None):

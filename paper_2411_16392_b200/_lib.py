@@ -41,7 +41,8 @@ class Params(ctypes.Structure):
 class Targets(ctypes.Structure):
     _fields_ = [(n, vp) for n in ("color", "color_raw", "alpha", "depth", "depth_sq",
                                   "depth_median", "normal", "curvature", "distortion",
-                                  "transmittance", "n_fragments", "violations", "aux")]
+                                  "transmittance", "n_fragments", "violations", "aux",
+                                  "counters")]
 
 
 class Upstream(ctypes.Structure):

@@ -16,6 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "lib", "obj")
 LIB = os.path.join(HERE, "lib", "libqgs_b200.so")
+PEAKS_LIB = os.path.join(HERE, "lib", "libqgs_peaks.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -59,6 +60,13 @@ def build(force=False, verbose=False):
             subprocess.check_call(cmd)
     if force or _stale(LIB, objs):
         cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.check_call(cmd)
+    # measurement helper (not part of the product ABI): FP32 / MUFU peaks
+    src = os.path.join(os.path.dirname(HERE), "tools", "peaks.cu")
+    if os.path.exists(src) and (force or _stale(PEAKS_LIB, [src])):
+        cmd = [nvcc(), *ARCH, "-O3", "-Xcompiler", "-fPIC", "-shared", src, "-o", PEAKS_LIB]
         if verbose:
             print(" ".join(cmd))
         subprocess.check_call(cmd)

@@ -36,6 +36,7 @@ struct RasterSmem {
     int ring_p[RING][RT];
     double d64[3][RT];        // per-thread fp64 ray direction
     float red[RT / 32][32][KG];
+    unsigned long long cnt[3];
     int viol;
 };
 
@@ -213,8 +214,10 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
     float median = 0.f;
     double last_t = -1.0e300;
     int nfrag = 0, viol = 0;
+    unsigned n_box = 0, n_acc = 0;
     Ring R{&sm.ring_t[0][threadIdx.x], &sm.ring_p[0][threadIdx.x], 0};
     bool alive = inside;
+    if (threadIdx.x < 3) sm.cnt[threadIdx.x] = 0ull;
 
     auto composite = [&](int ep, double t) {
         double d[3];
@@ -254,7 +257,16 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
             double et;
             int ep;
             const int p = sm.prim[j];
-            if (stream_step(sm.rec[j], geo[p], p, d, u, v, dx, dy, dz, c, R, et, ep)) {
+            const PrimRec &r = sm.rec[j];
+            if (!in_box(r, u, v)) continue;
+            n_box++;
+            double t;
+            if (!accept(r, geo[p], d, u, v, dx, dy, dz, c, t)) continue;
+            n_acc++;
+            bool emit;
+            if (!c.resort) { et = t; ep = p; emit = true; }
+            else emit = ring_push(R, t, p, et, ep);
+            if (emit) {
                 composite(ep, et);
                 if (!alive) break;
             }
@@ -304,8 +316,14 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
     }
     __syncthreads();
     if (viol) atomicAdd(&sm.viol, viol);
+    if (out.counters) {
+        atomicAdd(&sm.cnt[0], (unsigned long long)n_box);
+        atomicAdd(&sm.cnt[1], (unsigned long long)n_acc);
+        atomicAdd(&sm.cnt[2], (unsigned long long)nfrag);
+    }
     __syncthreads();
     if (threadIdx.x == 0 && out.violations) out.violations[tile] = sm.viol;
+    if (out.counters && threadIdx.x < 3) atomicAdd(&out.counters[threadIdx.x], sm.cnt[threadIdx.x]);
 }
 
 // =============================================================== backward

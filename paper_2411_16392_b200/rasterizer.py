@@ -257,6 +257,28 @@ class GradientBuffer:
         return GradientBuffer(**z, screen_center=torch.zeros((shp["centers"][0], 2),
                                                              dtype=torch.float32, device=device))
 
+    @staticmethod
+    def zeros_flat(prims: "DevicePrimitives"):
+        """Like zeros(), but the six raw groups are views of ONE flat fp32
+        buffer (``.buffer``) so a multi-GPU step all-reduces it in place."""
+        device = prims.centers.device
+        shp = [tuple(getattr(prims, f).shape) for f in DevicePrimitives.FIELDS]
+        sizes = [int(np.prod(s)) for s in shp]
+        buf = torch.zeros((sum(sizes),), dtype=torch.float32, device=device)
+        views, o = [], 0
+        for s, n in zip(shp, sizes):
+            views.append(buf[o:o + n].view(s))
+            o += n
+        gb = GradientBuffer(*views, screen_center=torch.zeros((shp[0][0], 2), dtype=torch.float32,
+                                                              device=device))
+        gb.buffer = buf
+        return gb
+
+    def zero_(self):
+        for f in self.GROUPS + ("screen_center",):
+            getattr(self, f).zero_()
+        return self
+
     def iadd(self, other):
         for f in self.GROUPS + ("screen_center",):
             getattr(self, f).add_(getattr(other, f))
@@ -320,8 +342,9 @@ def prepare(prims, cam, settings: RenderSettings = None, validate=True) -> Prepa
                         _cam_c=cam_c, _st_c=st_c)
 
 
-def forward(prep: PreparedView, keep_aux=True) -> RenderTargets:
-    """rasterizer.py:198-227."""
+def forward(prep: PreparedView, keep_aux=True, counters=None) -> RenderTargets:
+    """rasterizer.py:198-227.  `counters` (optional uint64/int64 CUDA tensor of
+    3) accumulates [in-box candidates, accepted fragments, composited]."""
     cam = prep.cam
     H, W = int(cam.height), int(cam.width)
     device = prep.prep.device
@@ -338,6 +361,7 @@ def forward(prep: PreparedView, keep_aux=True) -> RenderTargets:
     for k in _MAPS + ("violations",):
         setattr(t, k, _ptr(getattr(tg, k)))
     t.aux = _ptr(tg.aux) if keep_aux else None
+    t.counters = _ptr(counters)
     _lib.check(_lib.load().qgs_forward(_ptr(prep.prep), len(prep.dev), prep._cam_c, prep._st_c,
                                        _ptr(prep.tile_offsets), _ptr(prep.tile_prims), t,
                                        _stream()), "qgs_forward")
@@ -356,8 +380,9 @@ def _up_tensor(a, shape, device):
     return t.contiguous()
 
 
-def kernel_grads(prep: PreparedView, targets: RenderTargets, upstream) -> torch.Tensor:
-    """backward_kernel + merge (raster_kernels.py:505-681): (P, 24) fp32 slots."""
+def kernel_grads(prep: PreparedView, targets: RenderTargets, upstream, kg=None) -> torch.Tensor:
+    """backward_kernel + merge (raster_kernels.py:505-681): (P, 24) fp32 slots,
+    accumulated into `kg` when given (it must then be zeroed by the caller)."""
     cam = prep.cam
     H, W = int(cam.height), int(cam.width)
     device = prep.prep.device
@@ -373,7 +398,8 @@ def kernel_grads(prep: PreparedView, targets: RenderTargets, upstream) -> torch.
     if targets.aux.dim() != 3:
         raise ValueError("backward needs forward(prep, keep_aux=True)")
     t.aux = _ptr(targets.aux)
-    kg = torch.zeros((len(prep.dev), _lib.KG_STRIDE), dtype=torch.float32, device=device)
+    if kg is None:
+        kg = torch.zeros((len(prep.dev), _lib.KG_STRIDE), dtype=torch.float32, device=device)
     _lib.check(_lib.load().qgs_backward(_ptr(prep.prep), len(prep.dev), prep._cam_c, prep._st_c,
                                         _ptr(prep.tile_offsets), _ptr(prep.tile_prims), t, u,
                                         _ptr(kg), _stream()), "qgs_backward")
