@@ -85,6 +85,10 @@ typedef struct qgs_targets {
                                   qgs_backward, may be NULL for a forward-only call */
     unsigned long long *counters; /* optional, accumulated (+=): [0] candidates inside
                                   the pixel box, [1] accepted fragments, [2] composited */
+    uint32_t *accept_mask;     /* n_pairs*8: per sorted pair, the accepted-pixel lane
+                                  mask of each of the tile's 8 warps; written by the
+                                  forward, required by qgs_backward (may be NULL for a
+                                  forward-only call) */
 } qgs_targets;
 
 /* Upstream map gradients (rasterizer.py:230-250); NULL = all zero. */

@@ -25,7 +25,9 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relax
 UNITS = {
     "preprocess.cu": ["-fmad=false"],
     "binning.cu": ["-fmad=false"],
-    "raster.cu": ["-fmad=true"],
+    # approximate reciprocal / sqrt in the fp32 shading (every decision that
+    # must match the reference is confirmed in fp64 first, see shade.cuh)
+    "raster.cu": ["-fmad=true", "-prec-div=false", "-prec-sqrt=false", "-ftz=true"],
     "abi.cu": [],
 }
 

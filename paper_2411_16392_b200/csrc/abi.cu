@@ -69,9 +69,9 @@ int configure()
     QGS_CK(cudaFuncSetAttribute(qgs::tile_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)qgs::sort_smem_bytes()));
     QGS_CK(cudaFuncSetAttribute(qgs::raster_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)qgs::raster_smem_bytes()));
+                                (int)qgs::fwd_smem_bytes()));
     QGS_CK(cudaFuncSetAttribute(qgs::raster_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)qgs::raster_smem_bytes()));
+                                (int)qgs::bwd_smem_bytes()));
     smem_configured = true;
     return 0;
 }
@@ -216,7 +216,7 @@ int qgs_forward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_se
     qgs::SetK sk = qgs::make_setk(*st);
     qgs::PrepView pv = qgs::prep_view(const_cast<void *>(prep), P);
     qgs::raster_fwd_kernel<<<ck.tiles_x * ck.tiles_y, qgs::RASTER_THREADS,
-                             qgs::raster_smem_bytes(), s>>>(pv.rec, pv.geo, tile_offsets, tile_prims, ck,
+                             qgs::fwd_smem_bytes(), s>>>(pv.rec, pv.geo, tile_offsets, tile_prims, ck,
                                                             sk, *out);
     QGS_LAUNCHED("raster_fwd_kernel");
     return 0;
@@ -229,7 +229,7 @@ int qgs_backward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_s
     if (!prep || !st || !fwd || !up || !tile_offsets || (!kg && P > 0))
         return fail(QGS_E_ARG, "NULL argument");
     if (P == 0) return 0;
-    if (!fwd->aux) return fail(QGS_E_ARG, "backward needs the forward's aux planes");
+    if (!fwd->aux || !fwd->accept_mask) return fail(QGS_E_ARG, "backward needs the forward's aux planes and accept mask");
     if (int rc = check_cam(cam)) return rc;
     if (int rc = configure()) return rc;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -237,7 +237,7 @@ int qgs_backward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_s
     qgs::SetK sk = qgs::make_setk(*st);
     qgs::PrepView pv = qgs::prep_view(const_cast<void *>(prep), P);
     qgs::raster_bwd_kernel<<<ck.tiles_x * ck.tiles_y, qgs::RASTER_THREADS,
-                             qgs::raster_smem_bytes(), s>>>(pv.rec, pv.geo, tile_offsets, tile_prims, ck,
+                             qgs::bwd_smem_bytes(), s>>>(pv.rec, pv.geo, tile_offsets, tile_prims, ck,
                                                             sk, *fwd, *up, kg);
     QGS_LAUNCHED("raster_bwd_kernel");
     return 0;

@@ -45,7 +45,8 @@ __global__ void trace_pixel_kernel(const PrimRec *recs, const Geo64 *geo, const 
                                    int max, int *acc_prim, float *acc_t, float *acc_abar,
                                    int *em_prim, float *em_t, float *em_abar, double *em_T,
                                    int *counts);
-size_t raster_smem_bytes();
+size_t fwd_smem_bytes();
+size_t bwd_smem_bytes();
 constexpr int RASTER_THREADS = 256;
 
 }  // namespace qgs

@@ -7,37 +7,57 @@
 // block so lanes see spatially coherent fragment streams.  The tile's
 // depth-sorted primitive list is streamed in batches of 256 fp32 records
 // staged in shared memory (8 lanes per 128-byte record, fully coalesced).
-// Accepted fragments go through the per-pixel 8-entry min-depth ring (fp64
-// depth + primitive id, kept in shared memory); an emitted fragment is
-// re-shaded at its stored fp64 depth (shade.cuh: shade_at).
 //
-// Precision: candidate tests are fp32 with an fp64 depth refinement of every
-// accepted root (shade.cuh); transmittance, blend weights and the eleven
-// blend sums are fp64, which keeps T_i, w_i and the backward's suffix sums
-// (vtot - prefix, the front-to-back rewrite of raster_kernels.py:340) exact to
-// ~1e-15 instead of the ~1e-7 |vtot| an fp32 prefix would give.
+// Forward, per batch:
+//   masks   one thread per staged primitive intersects its pixel box with
+//           each warp's 8x4 block -> a 32-bit lane mask per (entry, warp);
+//           a warp skips entries whose mask is empty without any test
+//   pass 1  coarse fp32 test (shade.cuh: coarse_roots) of every in-box
+//           candidate -> per-thread candidate bitmask; tight, branch-light loop
+//   pass 2  for the set bits in stream order: fp64 depth refinement + exact
+//           selection + alpha floor, then the 8-entry min-depth ring and the
+//           fp64 compositing of emitted fragments (re-shaded at their depth)
+//   record  the accepted-lane mask of every streamed entry is written out,
+//           so the backward replays ONLY accepted candidates
 //
-// The backward replays exactly the same stream (same inline functions, same
-// decisions) and reduces each emitted fragment's 22 kernel-level gradient
-// slots across the warp lanes that emitted the same primitive (match_any +
-// shared-memory transpose) before one float atomic per slot.
+// Precision: transmittance, blend weights and the eleven blend sums are fp64,
+// which keeps T_i, w_i and the backward's suffix sums (vtot - prefix, the
+// front-to-back rewrite of raster_kernels.py:340) exact to ~1e-15.
+//
+// Backward: replays the recorded accepted candidates through the same ring
+// (same inline functions -> same fp64 depths and decisions) and reduces each
+// emitted fragment's 22 kernel-level gradient slots across the warp lanes
+// that emitted the same primitive (match_any + shared-memory transpose)
+// before one float atomic per slot.
 #include "shade.cuh"
 
 namespace qgs {
 
 constexpr int RT = 256;       // threads per tile CTA
-constexpr int BATCH = 256;    // records staged per batch
+constexpr int BATCH = 256;    // records staged per batch (== RT)
+constexpr int NWARP = RT / 32;
 constexpr unsigned FULL = 0xffffffffu;
 
-struct RasterSmem {
+struct FwdSmem {
     PrimRec rec[BATCH];
     int prim[BATCH];
-    double ring_t[RING][RT];  // per-thread ring, [slot][thread]: conflict-free
+    uint32_t lanes[BATCH][NWARP];  // box lane masks (pass 1), then accepted masks
+    double ring_t[RING][RT];       // per-thread ring, [slot][thread]: conflict-free
     int ring_p[RING][RT];
-    double d64[3][RT];        // per-thread fp64 ray direction
-    float red[RT / 32][32][KG];
+    double d64[3][RT];             // per-thread fp64 ray direction
+    uint32_t bits[BATCH / 32][RT]; // per-thread candidate (pass 1) / accepted (pass 2) bits
     unsigned long long cnt[3];
     int viol;
+};
+
+struct BwdSmem {
+    PrimRec rec[BATCH];
+    int prim[BATCH];
+    uint32_t lanes[BATCH][NWARP];  // accepted lane masks recorded by the forward
+    double ring_t[RING][RT];
+    int ring_p[RING][RT];
+    double d64[3][RT];
+    float red[NWARP][32][KG];
 };
 
 __device__ __forceinline__ void pixel_of(int tile, int tiles_x, int &u, int &v)
@@ -49,19 +69,33 @@ __device__ __forceinline__ void pixel_of(int tile, int tiles_x, int &u, int &v)
 }
 
 // stage records [b0, b0+nb) of the tile list into shared memory
-__device__ __forceinline__ void load_batch(RasterSmem &sm, const PrimRec *__restrict__ recs,
+__device__ __forceinline__ void load_batch(PrimRec *srec, int *sprim,
+                                           const PrimRec *__restrict__ recs,
                                            const int32_t *__restrict__ list, int b0, int nb)
 {
-    for (int j = threadIdx.x; j < nb; j += RT) sm.prim[j] = list[b0 + j];
+    for (int j = threadIdx.x; j < nb; j += RT) sprim[j] = list[b0 + j];
     __syncthreads();
     // 8 lanes per record, 16 B each: a warp moves 4 whole 128 B records per step
     const float4 *src = reinterpret_cast<const float4 *>(recs);
-    float4 *dst = reinterpret_cast<float4 *>(sm.rec);
+    float4 *dst = reinterpret_cast<float4 *>(srec);
     for (int k = threadIdx.x; k < nb * 8; k += RT) {
         int j = k >> 3, q = k & 7;
-        dst[j * 8 + q] = __ldg(src + (size_t)sm.prim[j] * 8 + q);
+        dst[j * 8 + q] = __ldg(src + (size_t)sprim[j] * 8 + q);
     }
     __syncthreads();
+}
+
+// lane mask of warp w's 8x4 block covered by the inclusive pixel box
+__device__ __forceinline__ uint32_t box_lanes(const PrimRec &r, int tile, int tiles_x, int w)
+{
+    int ty = tile / tiles_x, tx = tile - ty * tiles_x;
+    int bu = tx * TILE + (w & 1) * 8, bv = ty * TILE + (w >> 1) * 4;
+    int c0 = max((int)(r.bb_u & 0xffffu) - bu, 0), c1 = min((int)(r.bb_u >> 16) - bu, 7);
+    int r0 = max((int)(r.bb_v & 0xffffu) - bv, 0), r1 = min((int)(r.bb_v >> 16) - bv, 3);
+    if (c0 > c1 || r0 > r1) return 0u;
+    uint32_t cols = (0xffu >> (7 - c1)) & (0xffu << c0);
+    uint32_t rows = (0xffffffffu >> (8 * (3 - r1))) & (0xffffffffu << (8 * r0));
+    return (cols * 0x01010101u) & rows;
 }
 
 // Per-thread ring view into shared memory.
@@ -131,12 +165,10 @@ __device__ __forceinline__ Cfg make_cfg(const SetK &st)
     return c;
 }
 
-// candidate test shared by both passes (raster_kernels.py:121-130, 58-63)
+// exact candidate test (raster_kernels.py:121-130, 58-63); t = fp64 depth
 __device__ __forceinline__ bool accept(const PrimRec &r, const Geo64 &g, const double d64[3],
-                                       int u, int v, float dx, float dy, float dz, const Cfg &c,
-                                       double &t)
+                                       float dx, float dy, float dz, const Cfg &c, double &t)
 {
-    if (!in_box(r, u, v)) return false;
     Hit h;
     if (!hit_refined(r, g, d64, dx, dy, dz, c.euclid, c.t_clip, h)) return false;
     if (r.alpha * h.G < c.alpha_floor) return false;
@@ -144,13 +176,10 @@ __device__ __forceinline__ bool accept(const PrimRec &r, const Geo64 &g, const d
     return true;
 }
 
-// candidate step: accept + ring; returns whether a fragment is emitted
-__device__ __forceinline__ bool stream_step(const PrimRec &r, const Geo64 &g, int prim,
-                                            const double d64[3], int u, int v, float dx, float dy,
-                                            float dz, const Cfg &c, Ring &R, double &et, int &ep)
+// ring step for an accepted fragment; returns whether one is emitted
+__device__ __forceinline__ bool ring_step(const Cfg &c, Ring &R, double t, int prim, double &et,
+                                          int &ep)
 {
-    double t;
-    if (!accept(r, g, d64, u, v, dx, dy, dz, c, t)) return false;
     if (!c.resort) { et = t; ep = prim; return true; }
     return ring_push(R, t, prim, et, ep);
 }
@@ -179,11 +208,11 @@ __device__ __forceinline__ void shade_emitted(const PrimRec &r, const Geo64 &g, 
     normal_curv32(r, f.h, dx, dy, dz, f.nl, f.nc, f.K, f.inrm, f.flip);
 }
 
-__device__ __forceinline__ void load_dir(RasterSmem &sm, double d[3])
+__device__ __forceinline__ void load_dir(const double (*d64)[RT], double d[3])
 {
-    d[0] = sm.d64[0][threadIdx.x];
-    d[1] = sm.d64[1][threadIdx.x];
-    d[2] = sm.d64[2][threadIdx.x];
+    d[0] = d64[0][threadIdx.x];
+    d[1] = d64[1][threadIdx.x];
+    d[2] = d64[2][threadIdx.x];
 }
 
 // ================================================================ forward
@@ -194,8 +223,9 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
                   const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets out)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    RasterSmem &sm = *reinterpret_cast<RasterSmem *>(smem_raw);
+    FwdSmem &sm = *reinterpret_cast<FwdSmem *>(smem_raw);
     const int tile = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int u, v;
     pixel_of(tile, cam.tiles_x, u, v);
     const bool inside = u < cam.W && v < cam.H;
@@ -208,6 +238,7 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         dx = (float)d[0]; dy = (float)d[1]; dz = (float)d[2];
     }
     if (threadIdx.x == 0) sm.viol = 0;
+    if (threadIdx.x < 3) sm.cnt[threadIdx.x] = 0ull;
 
     double T = 1.0, ac0 = 0, ac1 = 0, ac2 = 0, aa = 0, ad = 0, ad2 = 0, an0 = 0, an1 = 0,
            an2 = 0, ak = 0, adist = 0;
@@ -217,14 +248,14 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
     unsigned n_box = 0, n_acc = 0;
     Ring R{&sm.ring_t[0][threadIdx.x], &sm.ring_p[0][threadIdx.x], 0};
     bool alive = inside;
-    if (threadIdx.x < 3) sm.cnt[threadIdx.x] = 0ull;
+    const uint32_t lanebit = 1u << lane;
 
     auto composite = [&](int ep, double t) {
         double d[3];
-        load_dir(sm, d);
+        load_dir(sm.d64, d);
         Frag f;
-        shade_emitted(recs[ep], geo[ep], d, dx, dy, dz, t, c, f);
         const PrimRec &r = recs[ep];
+        shade_emitted(r, geo[ep], d, dx, dy, dz, t, c, f);
         if (t < last_t - 1e-12) viol++;
         if (t > last_t) last_t = t;
         const double w = f.abar64 * T;
@@ -249,27 +280,70 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
     for (int b0 = start; b0 < end; b0 += BATCH) {
         if (__syncthreads_count(alive) == 0) break;
         const int nb = min(BATCH, end - b0);
-        load_batch(sm, recs, tile_prims, b0, nb);
-        if (!alive) continue;
-        double d[3];
-        load_dir(sm, d);
-        for (int j = 0; j < nb; ++j) {
-            double et;
-            int ep;
-            const int p = sm.prim[j];
-            const PrimRec &r = sm.rec[j];
-            if (!in_box(r, u, v)) continue;
-            n_box++;
-            double t;
-            if (!accept(r, geo[p], d, u, v, dx, dy, dz, c, t)) continue;
-            n_acc++;
-            bool emit;
-            if (!c.resort) { et = t; ep = p; emit = true; }
-            else emit = ring_push(R, t, p, et, ep);
-            if (emit) {
-                composite(ep, et);
-                if (!alive) break;
+        load_batch(sm.rec, sm.prim, recs, tile_prims, b0, nb);
+        if (threadIdx.x < nb) {
+#pragma unroll
+            for (int w = 0; w < NWARP; ++w)
+                sm.lanes[threadIdx.x][w] = box_lanes(sm.rec[threadIdx.x], tile, cam.tiles_x, w);
+        }
+        __syncthreads();
+
+        // pass 1: coarse test of every in-box candidate
+        const int nwd = (nb + 31) >> 5;
+        for (int wd = 0; wd < nwd; ++wd) {
+            uint32_t bits = 0u;
+            const int jn = min(32, nb - wd * 32);
+            if (__any_sync(FULL, alive)) {
+                for (int jj = 0; jj < jn; ++jj) {
+                    const int j = wd * 32 + jj;
+                    const uint32_t m = sm.lanes[j][warp];
+                    if (m == 0u) continue;            // warp-uniform skip
+                    if (!(m & lanebit) || !alive) continue;
+                    n_box++;
+                    float roots[2], hx, hy, hz;
+                    if (coarse_roots(sm.rec[j], dx, dy, dz, c.euclid, c.t_clip, roots, hx, hy, hz))
+                        bits |= 1u << jj;
+                }
             }
+            sm.bits[wd][threadIdx.x] = bits;
+        }
+
+        // pass 2: exact test, ring and compositing in stream order
+        double d[3];
+        load_dir(sm.d64, d);
+        for (int wd = 0; wd < nwd; ++wd) {
+            uint32_t bits = sm.bits[wd][threadIdx.x], acc = 0u;
+            while (bits && alive) {
+                const int jj = __ffs(bits) - 1;
+                bits &= bits - 1;
+                const int j = wd * 32 + jj;
+                const int p = sm.prim[j];
+                double t;
+                if (!accept(sm.rec[j], geo[p], d, dx, dy, dz, c, t)) continue;
+                acc |= 1u << jj;
+                n_acc++;
+                double et;
+                int ep;
+                if (ring_step(c, R, t, p, et, ep)) composite(ep, et);
+            }
+            sm.bits[wd][threadIdx.x] = acc;
+        }
+
+        // record the accepted lanes of every entry for the backward
+        if (out.accept_mask) {
+            __syncthreads();   // everyone is done reading the box masks
+            for (int wd = 0; wd < nwd; ++wd) {
+                const uint32_t acc = sm.bits[wd][threadIdx.x];
+                const int jn = min(32, nb - wd * 32);
+                for (int jj = 0; jj < jn; ++jj) {
+                    const uint32_t m = __ballot_sync(FULL, (acc >> jj) & 1u);
+                    if (lane == 0) sm.lanes[wd * 32 + jj][warp] = m;
+                }
+            }
+            __syncthreads();
+            const uint4 *src = reinterpret_cast<const uint4 *>(&sm.lanes[0][0]);
+            uint4 *dst = reinterpret_cast<uint4 *>(out.accept_mask + (size_t)b0 * NWARP);
+            for (int k = threadIdx.x; k < nb * (NWARP / 4); k += RT) dst[k] = src[k];
         }
     }
     while (alive && R.n > 0) {
@@ -471,12 +545,12 @@ __device__ __forceinline__ void frag_grad(const PrimRec &r, const Frag &f, float
 }
 
 // sum the slots of lanes that emitted the same primitive; one atomic per slot
-__device__ __forceinline__ void warp_accumulate(RasterSmem &sm, bool emit, int prim,
+__device__ __forceinline__ void warp_accumulate(float (*red)[32][KG], bool emit, int prim,
                                                 const float g[KG], float *__restrict__ kg)
 {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (emit) {
-        float4 *dst = reinterpret_cast<float4 *>(sm.red[w][lane]);
+        float4 *dst = reinterpret_cast<float4 *>(red[w][lane]);
 #pragma unroll
         for (int q = 0; q < KG / 4; ++q) dst[q] = make_float4(g[4 * q], g[4 * q + 1], g[4 * q + 2], g[4 * q + 3]);
     }
@@ -491,7 +565,7 @@ __device__ __forceinline__ void warp_accumulate(RasterSmem &sm, bool emit, int p
         const int gp = __shfl_sync(FULL, prim, ld);
         if (lane < 22) {
             float s = 0.f;
-            for (unsigned mm = grp; mm; mm &= mm - 1) s += sm.red[w][__ffs(mm) - 1][lane];
+            for (unsigned mm = grp; mm; mm &= mm - 1) s += red[w][__ffs(mm) - 1][lane];
             atomicAdd(kg + (size_t)gp * KG + lane, s);
         }
     }
@@ -505,8 +579,9 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
                   qgs_upstream upst, float *__restrict__ kg)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    RasterSmem &sm = *reinterpret_cast<RasterSmem *>(smem_raw);
+    BwdSmem &sm = *reinterpret_cast<BwdSmem *>(smem_raw);
     const int tile = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int u, v;
     pixel_of(tile, cam.tiles_x, u, v);
     const bool inside = u < cam.W && v < cam.H;
@@ -562,7 +637,7 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         float g[KG];
         if (emit) {
             double d[3];
-            load_dir(sm, d);
+            load_dir(sm.d64, d);
             Frag f;
             const PrimRec &r = recs[ep];
             shade_emitted(r, geo[ep], d, dx, dy, dz, t, c, f);
@@ -578,22 +653,34 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
             T *= 1.0 - f.abar64;
             if (T < c.t_term) alive = false;
         }
-        warp_accumulate(sm, emit, ep, g, kg);
+        warp_accumulate(sm.red, emit, ep, g, kg);
     };
 
     const int start = tile_offsets[tile], end = tile_offsets[tile + 1];
     for (int b0 = start; b0 < end; b0 += BATCH) {
         if (__syncthreads_count(alive) == 0) break;
         const int nb = min(BATCH, end - b0);
-        load_batch(sm, recs, tile_prims, b0, nb);
+        {
+            const uint4 *src = reinterpret_cast<const uint4 *>(fwd.accept_mask + (size_t)b0 * NWARP);
+            uint4 *dst = reinterpret_cast<uint4 *>(&sm.lanes[0][0]);
+            for (int k = threadIdx.x; k < nb * (NWARP / 4); k += RT) dst[k] = __ldg(src + k);
+        }
+        load_batch(sm.rec, sm.prim, recs, tile_prims, b0, nb);
         double d[3];
-        load_dir(sm, d);
+        load_dir(sm.d64, d);
         for (int j = 0; j < nb; ++j) {
             if (!__any_sync(FULL, alive)) break;
+            const uint32_t m = sm.lanes[j][warp];
+            if (m == 0u) continue;                    // nobody in this warp accepted it
             double et = 0.0;
             int ep = -1;
-            const int p = sm.prim[j];
-            bool emit = alive && stream_step(sm.rec[j], geo[p], p, d, u, v, dx, dy, dz, c, R, et, ep);
+            bool emit = false;
+            if (alive && (m >> lane & 1u)) {
+                const int p = sm.prim[j];
+                double t = 0.0;
+                accept(sm.rec[j], geo[p], d, dx, dy, dz, c, t);   // same fp64 depth as forward
+                emit = ring_step(c, R, t, p, et, ep);
+            }
             if (__any_sync(FULL, emit)) emit_grad(emit, ep, et);
         }
     }
@@ -640,7 +727,7 @@ __global__ void trace_pixel_kernel(const PrimRec *__restrict__ recs, const Geo64
         const int p = tile_prims[i];
         const PrimRec &r = recs[p];
         double t;
-        if (accept(r, geo[p], d, u, v, dx, dy, dz, c, t)) {
+        if (in_box(r, u, v) && accept(r, geo[p], d, dx, dy, dz, c, t)) {
             if (na < max) {
                 Frag f;
                 shade_emitted(r, geo[p], d, dx, dy, dz, t, c, f);
@@ -665,6 +752,8 @@ __global__ void trace_pixel_kernel(const PrimRec *__restrict__ recs, const Geo64
     counts[1] = ne;
 }
 
-size_t raster_smem_bytes() { return sizeof(RasterSmem); }
+
+size_t fwd_smem_bytes() { return sizeof(FwdSmem); }
+size_t bwd_smem_bytes() { return sizeof(BwdSmem); }
 
 }  // namespace qgs

@@ -188,64 +188,102 @@ __device__ __noinline__ bool hit_marginal(const PrimRec &r, const Geo64 &g, cons
     return false;
 }
 
-// Full candidate test: coarse fp32 roots, fp64 refinement, exact selection.
-// Returns the selected hit (valid, before the alpha floor) or false.
-__device__ __forceinline__ bool hit_refined(const PrimRec &r, const Geo64 &g, const double d64[3],
-                                            float dx, float dy, float dz, bool euclid,
-                                            float t_clip, Hit &h)
+// Coarse fp32 stage (the per-candidate hot path).  Returns a mask: bit k set
+// when root k (0 near, 1 far) passes the widened tests, CR_MARGINAL when the
+// discriminant is inside its fp32 rounding band (decided later in fp64).
+// Uses approximate reciprocal / sqrt / log: it only has to be conservative.
+constexpr unsigned CR_MARGINAL = 4u;
+
+__device__ __forceinline__ float arc32_fast(float a, float rho)
 {
-    constexpr float K = 1.05f;            // coarse margin on the 3-sigma tests
+    float u = 2.f * a * rho;
+    if (fabsf(u) < 0.3f) {
+        float u2 = u * u;
+        return rho * (1.f + u2 * (1.f / 6.f + u2 * (-1.f / 40.f + u2 * (1.f / 112.f))));
+    }
+    float r = sqrtf(fmaf(u, u, 1.f));
+    float as = copysignf(__logf(fabsf(u) + r), u);
+    return __fdividef(as + u * r, 4.f * a);
+}
+
+__device__ __forceinline__ unsigned coarse_roots(const PrimRec &r, float dx, float dy, float dz,
+                                                 bool euclid, float t_clip, float roots[2],
+                                                 float &hx, float &hy, float &hz)
+{
+    constexpr float K = 1.05f;            // margin on the 3-sigma tests
     const bool planar = (r.flags & 1u) != 0;
-    float hx = fmaf(r.M[0], dx, fmaf(r.M[1], dy, r.M[2] * dz));
-    float hy = fmaf(r.M[3], dx, fmaf(r.M[4], dy, r.M[5] * dz));
-    float hz = fmaf(r.M[6], dx, fmaf(r.M[7], dy, r.M[8] * dz));
-    float roots[2];
-    int cnt = 0;
+    hx = fmaf(r.M[0], dx, fmaf(r.M[1], dy, r.M[2] * dz));
+    hy = fmaf(r.M[3], dx, fmaf(r.M[4], dy, r.M[5] * dz));
+    hz = fmaf(r.M[6], dx, fmaf(r.M[7], dy, r.M[8] * dz));
+    int cnt;
     if (planar) {
-        if (fabsf(hz) < 1e-12f) return false;
-        roots[0] = -r.oz / hz;
+        if (fabsf(hz) < 1e-12f) return 0u;
+        roots[0] = __fdividef(-r.oz, hz);
+        roots[1] = roots[0];
         cnt = 1;
     } else {
         float A = fmaf(r.w1 * hx, hx, r.w2 * hy * hy);
         float B = 2.f * fmaf(r.w1 * r.ox, hx, r.w2 * r.oy * hy) - r.iw3 * hz;
         float C = r.C;
         if (fabsf(A) < 1e-6f) {
-            if (fabsf(B) < 1e-12f) return false;
-            roots[0] = -C / B;
+            if (fabsf(B) < 1e-12f) return 0u;
+            roots[0] = __fdividef(-C, B);
+            roots[1] = roots[0];
             cnt = 1;
         } else {
             float disc = fmaf(B, B, -4.f * A * C);
-            // fp32 rounding of disc is ~1e-7 max(B^2, |4AC|); inside a 1e-5 band
-            // the sign is decided in fp64
-            if (fabsf(disc) <= 1e-5f * fmaxf(B * B, fabsf(4.f * A * C)))
-                return hit_marginal(r, g, d64, euclid, t_clip, h);
-            if (disc < 0.f) return false;
-            float sq = sqrtf(disc);
-            float q = -0.5f * (B + copysignf(sq, B));
-            float ra = q / A, rb = (q != 0.f) ? C / q : ra;
+            // fp32 rounding of disc is ~1e-7 max(B^2, |4AC|); inside a 1e-5
+            // band the sign is decided in fp64
+            if (fabsf(disc) <= 1e-5f * fmaxf(B * B, fabsf(4.f * A * C))) return CR_MARGINAL;
+            if (disc < 0.f) return 0u;
+            float q = -0.5f * (B + copysignf(sqrtf(disc), B));
+            float ra = __fdividef(q, A), rb = (q != 0.f) ? __fdividef(C, q) : ra;
             roots[0] = fminf(ra, rb);
             roots[1] = fmaxf(ra, rb);
-            cnt = disc == 0.f ? 1 : 2;
+            cnt = 2;
         }
     }
-    double dh[3];
-    bool have_dh = false;
+    unsigned pass = 0u;
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
         if (k >= cnt) break;
         const float t = roots[k];
         if (!(t > t_clip * 0.99f)) continue;
         float x = fmaf(t, hx, r.ox), y = fmaf(t, hy, r.oy);
-        if (!planar && ellipse_out(r, x, y, K * K)) continue;
-        Hit c;
-        if (!eval_point(r, x, y, planar, euclid, K, c)) continue;
-        // precise look
-        if (!have_dh) {
-            local_dir64(g, d64, dh);
-            have_dh = true;
-            if (planar && fabs(dh[2]) < 1e-12) return false;
-        }
-        double t64 = refine_depth(g, dh, planar, t);
+        float ex = r.s2 * x, ey = r.s1 * y;
+        float m = fmaf(ex, ex, ey * ey);
+        if (!planar && m > (K * K) * r.ell9) continue;
+        float rho2 = fmaf(x, x, y * y);
+        float ir = rsqrtf(fmaxf(rho2, 1e-30f));
+        float rho = rho2 * ir;
+        float c = rho > 1e-12f ? x * ir : 1.f, s = rho > 1e-12f ? y * ir : 0.f;
+        float a = planar ? 0.f : r.s3 * fmaf(r.w1 * c, c, r.w2 * s * s);
+        float l = (planar || euclid) ? rho : arc32_fast(a, rho);
+        float sc = r.s2 * c, ss = r.s1 * s;
+        float sig = r.s12 * rsqrtf(fmaf(sc, sc, ss * ss));
+        if (l <= K * 3.f * sig) pass |= 1u << k;
+    }
+    return pass;
+}
+
+// Full candidate test: coarse fp32 roots, fp64 refinement, exact selection.
+// Returns the selected hit (valid, before the alpha floor) or false.
+__device__ __forceinline__ bool hit_refined(const PrimRec &r, const Geo64 &g, const double d64[3],
+                                            float dx, float dy, float dz, bool euclid,
+                                            float t_clip, Hit &h)
+{
+    float roots[2], hx, hy, hz;
+    const unsigned pass = coarse_roots(r, dx, dy, dz, euclid, t_clip, roots, hx, hy, hz);
+    if (pass == 0u) return false;
+    if (pass & CR_MARGINAL) return hit_marginal(r, g, d64, euclid, t_clip, h);
+    const bool planar = (r.flags & 1u) != 0;
+    double dh[3];
+    local_dir64(g, d64, dh);
+    if (planar && fabs(dh[2]) < 1e-12) return false;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        if (!(pass & (1u << k))) continue;
+        double t64 = refine_depth(g, dh, planar, roots[k]);
         if (confirm_root(r, g, dh, t64, planar, euclid, t_clip, h)) return true;
     }
     return false;

@@ -222,6 +222,7 @@ class RenderTargets:
     n_fragments: torch.Tensor
     violations: torch.Tensor      # per tile (int32)
     aux: torch.Tensor             # (12, H, W) float64 blend sums for the backward
+    accept_mask: torch.Tensor = None   # (n_pairs * 8,) accepted-lane masks for the backward
 
     @property
     def order_violations(self):
@@ -361,6 +362,9 @@ def forward(prep: PreparedView, keep_aux=True, counters=None) -> RenderTargets:
     for k in _MAPS + ("violations",):
         setattr(t, k, _ptr(getattr(tg, k)))
     t.aux = _ptr(tg.aux) if keep_aux else None
+    tg.accept_mask = (torch.empty((max(prep.n_pairs, 1) * 8,), dtype=torch.int32, device=device)
+                      if keep_aux else None)
+    t.accept_mask = _ptr(tg.accept_mask)
     t.counters = _ptr(counters)
     _lib.check(_lib.load().qgs_forward(_ptr(prep.prep), len(prep.dev), prep._cam_c, prep._st_c,
                                        _ptr(prep.tile_offsets), _ptr(prep.tile_prims), t,
@@ -395,9 +399,10 @@ def kernel_grads(prep: PreparedView, targets: RenderTargets, upstream, kg=None) 
     t = _lib.Targets()
     for k in _MAPS + ("violations",):
         setattr(t, k, _ptr(getattr(targets, k)))
-    if targets.aux.dim() != 3:
+    if targets.aux.dim() != 3 or targets.accept_mask is None:
         raise ValueError("backward needs forward(prep, keep_aux=True)")
     t.aux = _ptr(targets.aux)
+    t.accept_mask = _ptr(targets.accept_mask)
     if kg is None:
         kg = torch.zeros((len(prep.dev), _lib.KG_STRIDE), dtype=torch.float32, device=device)
     _lib.check(_lib.load().qgs_backward(_ptr(prep.prep), len(prep.dev), prep._cam_c, prep._st_c,
