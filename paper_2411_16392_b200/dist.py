@@ -1,0 +1,93 @@
+"""Multi-GPU training step: camera views sharded over ranks, primitives
+replicated, ONE all-reduce of the packed raw-parameter gradients per step.
+
+SURVEY.md section 8e.  The reference is single-process (train.py:183-261
+renders one view at a time); views are independent given replicated
+primitives, so rank r takes views {v : v mod W == r}, accumulates its views'
+raw gradients on device (rasterizer.backward(..., out=grads)), and a single
+NCCL all-reduce (SUM) over NVLink makes every rank hold the full gradient.
+The per-view screen-space centre gradient (a densification statistic, not a
+parameter gradient, train.py:239-244) is kept per rank and not reduced.
+
+The same code runs over gloo on CPU in the tests, with the per-view backward
+supplied by the caller.
+"""
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+GROUPS = ("centers", "quats", "raw_scales", "raw_signs", "raw_opacity", "sh")
+
+
+def shard_views(n_views, rank, world):
+    """Round-robin view assignment: rank r renders views r, r+W, r+2W, ..."""
+    if not 0 <= rank < world:
+        raise ValueError(f"rank {rank} outside world of {world}")
+    return list(range(rank, n_views, world))
+
+
+def group_sizes(shapes):
+    return [int(np.prod(shapes[g])) for g in GROUPS]
+
+
+def pack(grads, like=None):
+    """Six raw-gradient groups -> one contiguous fp32 vector (all-reduce layout:
+    centers, quats, raw_scales, raw_signs, raw_opacity, sh)."""
+    parts = []
+    for g in GROUPS:
+        a = grads[g] if isinstance(grads, dict) else getattr(grads, g)
+        t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.asarray(a))
+        parts.append(t.reshape(-1).to(torch.float32))
+    flat = torch.cat(parts)
+    return flat if like is None else flat.to(like.device)
+
+
+def unpack(flat, shapes):
+    out, o = {}, 0
+    for g, n in zip(GROUPS, group_sizes(shapes)):
+        out[g] = flat[o:o + n].reshape(shapes[g])
+        o += n
+    return out
+
+
+def allreduce_(flat, group=None):
+    """In-place SUM over all ranks (NCCL on GPU, gloo on CPU)."""
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+    return flat
+
+
+def sharded_step(n_views, view_backward, rank, world, shapes, device=None, group=None):
+    """One data-parallel step.
+
+    view_backward(v) -> dict of the six raw-gradient arrays for view v (numpy
+    or torch).  Returns the all-reduced gradient as a dict of tensors; every
+    rank ends with the same values."""
+    flat = None
+    for v in shard_views(n_views, rank, world):
+        part = pack(view_backward(v))
+        flat = part if flat is None else flat.add_(part)
+    if flat is None:
+        flat = torch.zeros(sum(group_sizes(shapes)), dtype=torch.float32)
+    if device is not None:
+        flat = flat.to(device)
+    allreduce_(flat, group)
+    return unpack(flat, shapes)
+
+
+def gpu_step(dev_prims, cams, upstreams, settings, rank, world, grads=None, group=None):
+    """The B200 step used by bench.py: this rank's views through the sm_100a
+    rasterizer, gradients accumulated in one flat device buffer, one NCCL
+    all-reduce.  `upstreams[v]` is the upstream dict of view v (device tensors)."""
+    from . import rasterizer as rz
+    if grads is None:
+        grads = rz.GradientBuffer.zeros_flat(dev_prims)
+    else:
+        grads.zero_()
+    for v in shard_views(len(cams), rank, world):
+        prep = rz.prepare(dev_prims, cams[v], settings)
+        tg = rz.forward(prep)
+        rz.backward(prep, tg, upstreams[v], out=grads)
+    allreduce_(grads.buffer, group)
+    return grads
