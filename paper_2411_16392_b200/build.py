@@ -27,7 +27,7 @@ UNITS = {
     "binning.cu": ["-fmad=false"],
     # approximate reciprocal / sqrt in the fp32 shading (every decision that
     # must match the reference is confirmed in fp64 first, see shade.cuh)
-    "raster.cu": ["-fmad=true", "-prec-div=false", "-prec-sqrt=false", "-ftz=true"],
+    "raster_warp.cu": ["-fmad=true", "-prec-div=false", "-prec-sqrt=false", "-ftz=true"],
     "abi.cu": [],
 }
 

@@ -68,10 +68,6 @@ int configure()
     if (smem_configured) return 0;
     QGS_CK(cudaFuncSetAttribute(qgs::tile_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)qgs::sort_smem_bytes()));
-    QGS_CK(cudaFuncSetAttribute(qgs::raster_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)qgs::fwd_smem_bytes()));
-    QGS_CK(cudaFuncSetAttribute(qgs::raster_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)qgs::bwd_smem_bytes()));
     smem_configured = true;
     return 0;
 }
@@ -215,8 +211,10 @@ int qgs_forward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_se
     qgs::CamK ck = qgs::make_camk(*cam);
     qgs::SetK sk = qgs::make_setk(*st);
     qgs::PrepView pv = qgs::prep_view(const_cast<void *>(prep), P);
-    qgs::raster_fwd_kernel<<<ck.tiles_x * ck.tiles_y, qgs::RASTER_THREADS,
-                             qgs::fwd_smem_bytes(), s>>>(pv.rec, pv.geo, tile_offsets, tile_prims, ck,
+    if (out->violations)
+        QGS_CK(cudaMemsetAsync(out->violations, 0, sizeof(int32_t) * ck.tiles_x * ck.tiles_y, s));
+    qgs::raster_fwd_kernel<<<ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE,
+                             qgs::RASTER_THREADS, 0, s>>>(pv.rec, pv.geo, tile_offsets, tile_prims, ck,
                                                             sk, *out);
     QGS_LAUNCHED("raster_fwd_kernel");
     return 0;
@@ -236,8 +234,8 @@ int qgs_backward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_s
     qgs::CamK ck = qgs::make_camk(*cam);
     qgs::SetK sk = qgs::make_setk(*st);
     qgs::PrepView pv = qgs::prep_view(const_cast<void *>(prep), P);
-    qgs::raster_bwd_kernel<<<ck.tiles_x * ck.tiles_y, qgs::RASTER_THREADS,
-                             qgs::bwd_smem_bytes(), s>>>(pv.rec, pv.geo, tile_offsets, tile_prims, ck,
+    qgs::raster_bwd_kernel<<<ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE,
+                             qgs::RASTER_THREADS, 0, s>>>(pv.rec, pv.geo, tile_offsets, tile_prims, ck,
                                                             sk, *fwd, *up, kg);
     QGS_LAUNCHED("raster_bwd_kernel");
     return 0;

@@ -153,26 +153,27 @@ __device__ inline uint32_t key_hi(double key)
     return __float_as_uint(__double2float_rd(key));
 }
 
+// One warp per primitive; lanes stride over the primitive's tiles.
 __global__ void pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
                                 int32_t *cursor, uint64_t *bucket)
 {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_pairs;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        // owning primitive: last p with pair_off[p] <= i
-        int lo = 0, hi = P;  // pair_off[lo] <= i < pair_off[hi]
-        while (hi - lo > 1) {
-            int mid = (lo + hi) >> 1;
-            if (pv.pair_off[mid] <= i) lo = mid; else hi = mid;
+    (void)n_pairs;
+    const int lane = threadIdx.x & 31;
+    const int warps = gridDim.x * (blockDim.x >> 5);
+    for (int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); p < P; p += warps) {
+        const int nt = pv.ntiles[p];
+        if (nt == 0) continue;
+        const int4 b = pv.bbox[p];
+        const int tx0 = b.x / TILE, ty0 = b.z / TILE;
+        const int ncols = b.y / TILE - tx0 + 1;
+        const Geo64 &g = pv.geo[p];
+        for (int local = lane; local < nt; local += 32) {
+            const int row = local / ncols;
+            const int tile = (ty0 + row) * cam.tiles_x + tx0 + (local - row * ncols);
+            const double key = tile_key_geo(g, tile, cam, st.euclid != 0, st.t_clip);
+            const int slot = atomicAdd(&cursor[tile], 1);
+            bucket[slot] = ((uint64_t)key_hi(key) << 32) | (uint32_t)p;
         }
-        int p = lo;
-        int64_t local = i - pv.pair_off[p];
-        int4 b = pv.bbox[p];
-        int tx0 = b.x / TILE, tx1 = b.y / TILE, ty0 = b.z / TILE;
-        int ncols = tx1 - tx0 + 1;
-        int tile = (ty0 + (int)(local / ncols)) * cam.tiles_x + tx0 + (int)(local % ncols);
-        double key = tile_key_geo(pv.geo[p], tile, cam, st.euclid != 0, st.t_clip);
-        int slot = atomicAdd(&cursor[tile], 1);
-        bucket[slot] = ((uint64_t)key_hi(key) << 32) | (uint32_t)p;
     }
 }
 

@@ -45,8 +45,7 @@ __global__ void trace_pixel_kernel(const PrimRec *recs, const Geo64 *geo, const 
                                    int max, int *acc_prim, float *acc_t, float *acc_abar,
                                    int *em_prim, float *em_t, float *em_abar, double *em_T,
                                    int *counts);
-size_t fwd_smem_bytes();
-size_t bwd_smem_bytes();
-constexpr int RASTER_THREADS = 256;
+constexpr int RASTER_THREADS = 32;   // one warp per 8x4 block, 8 blocks per tile
+constexpr int RASTER_BLOCKS_PER_TILE = 8;
 
 }  // namespace qgs

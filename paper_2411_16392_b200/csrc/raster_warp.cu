@@ -1,95 +1,92 @@
-// K5 forward and K6 backward tile raster kernels.
+// K5 forward and K6 backward raster kernels, one warp per 8x4 pixel block.
 //
 // Reference: raster_kernels.py:83-286 (forward_kernel), :289-502
 // (_grad_fragment), :505-670 (backward_kernel), :673-681 (merge).
 //
-// One CTA per 16x16 tile, one thread per pixel; each warp owns an 8x4 pixel
-// block so lanes see spatially coherent fragment streams.  The tile's
-// depth-sorted primitive list is streamed in batches of 256 fp32 records
-// staged in shared memory (8 lanes per 128-byte record, fully coalesced).
+// Work unit = one warp = one 8x4 block of a 16x16 tile (a tile is 8 such
+// blocks); each warp is its own CTA and streams its tile's depth-sorted list
+// independently -- no CTA barriers, and a warp stops as soon as its own 32
+// pixels have terminated.  The list is consumed in batches of 32 fp32
+// records staged in shared memory (8 lanes per 128-byte record, coalesced;
+// the 8 blocks of a tile hit the same lines in L2).
 //
 // Forward, per batch:
-//   masks   one thread per staged primitive intersects its pixel box with
-//           each warp's 8x4 block -> a 32-bit lane mask per (entry, warp);
-//           a warp skips entries whose mask is empty without any test
+//   mask    lane j intersects record j's pixel box with the block -> a 32-bit
+//           lane mask, broadcast by shuffle; empty masks are skipped
 //   pass 1  coarse fp32 test (shade.cuh: coarse_roots) of every in-box
-//           candidate -> per-thread candidate bitmask; tight, branch-light loop
-//   pass 2  for the set bits in stream order: fp64 depth refinement + exact
-//           selection + alpha floor, then the 8-entry min-depth ring and the
-//           fp64 compositing of emitted fragments (re-shaded at their depth)
-//   record  the accepted-lane mask of every streamed entry is written out,
-//           so the backward replays ONLY accepted candidates
+//           candidate -> per-lane candidate bits
+//   pass 2  set bits in stream order: fp64 depth refinement + exact selection
+//           + alpha floor, the 8-entry min-depth ring and fp64 compositing of
+//           emitted fragments (re-shaded at their fp64 depth)
+//   record  accepted-lane mask of every streamed entry (ballot), stored
+//           block-major per tile, so the backward replays ONLY those
 //
-// Precision: transmittance, blend weights and the eleven blend sums are fp64,
-// which keeps T_i, w_i and the backward's suffix sums (vtot - prefix, the
-// front-to-back rewrite of raster_kernels.py:340) exact to ~1e-15.
+// Transmittance, blend weights and the eleven blend sums are fp64: the
+// backward's suffix sums (vtot - prefix, the front-to-back rewrite of
+// raster_kernels.py:340) are exact to ~1e-15.
 //
 // Backward: replays the recorded accepted candidates through the same ring
 // (same inline functions -> same fp64 depths and decisions) and reduces each
-// emitted fragment's 22 kernel-level gradient slots across the warp lanes
-// that emitted the same primitive (match_any + shared-memory transpose)
-// before one float atomic per slot.
+// emitted fragment's 22 kernel-level gradient slots across lanes that emitted
+// the same primitive (match_any + shared-memory transpose) before one float
+// atomic per slot.
 #include "shade.cuh"
 
 namespace qgs {
 
-constexpr int RT = 256;       // threads per tile CTA
-constexpr int BATCH = 256;    // records staged per batch (== RT)
-constexpr int NWARP = RT / 32;
+constexpr int WB = 32;        // entries per batch == lanes
+constexpr int NBLK = 8;       // 8x4 blocks per 16x16 tile
 constexpr unsigned FULL = 0xffffffffu;
 
 struct FwdSmem {
-    PrimRec rec[BATCH];
-    int prim[BATCH];
-    uint32_t lanes[BATCH][NWARP];  // box lane masks (pass 1), then accepted masks
-    double ring_t[RING][RT];       // per-thread ring, [slot][thread]: conflict-free
-    int ring_p[RING][RT];
-    double d64[3][RT];             // per-thread fp64 ray direction
-    uint32_t bits[BATCH / 32][RT]; // per-thread candidate (pass 1) / accepted (pass 2) bits
-    unsigned long long cnt[3];
-    int viol;
+    PrimRec rec[WB];
+    int prim[WB];
+    double ring_t[RING][32];  // per-lane ring, [slot][lane]: conflict-free
+    int ring_p[RING][32];
 };
 
 struct BwdSmem {
-    PrimRec rec[BATCH];
-    int prim[BATCH];
-    uint32_t lanes[BATCH][NWARP];  // accepted lane masks recorded by the forward
-    double ring_t[RING][RT];
-    int ring_p[RING][RT];
-    double d64[3][RT];
-    float red[NWARP][32][KG];
+    PrimRec rec[WB];
+    int prim[WB];
+    double ring_t[RING][32];
+    int ring_p[RING][32];
+    float red[1][32][KG];
 };
 
-__device__ __forceinline__ void pixel_of(int tile, int tiles_x, int &u, int &v)
+// (tile, block) of this CTA and the lane's pixel
+__device__ __forceinline__ void block_pixel(int tiles_x, int &tile, int &blk, int &u, int &v)
 {
-    int ty = tile / tiles_x, tx = tile - ty * tiles_x;
-    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    u = tx * TILE + (w & 1) * 8 + (lane & 7);
-    v = ty * TILE + (w >> 1) * 4 + (lane >> 3);
+    tile = blockIdx.x >> 3;
+    blk = blockIdx.x & 7;
+    const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
+    const int lane = threadIdx.x & 31;
+    u = tx * TILE + (blk & 1) * 8 + (lane & 7);
+    v = ty * TILE + (blk >> 1) * 4 + (lane >> 3);
 }
 
-// stage records [b0, b0+nb) of the tile list into shared memory
-__device__ __forceinline__ void load_batch(PrimRec *srec, int *sprim,
-                                           const PrimRec *__restrict__ recs,
-                                           const int32_t *__restrict__ list, int b0, int nb)
+// stage records list[b0 .. b0+nb) into shared memory; returns lane's prim id
+__device__ __forceinline__ int load_batch32(PrimRec *srec, int *sprim,
+                                            const PrimRec *__restrict__ recs,
+                                            const int32_t *__restrict__ list, int b0, int nb)
 {
-    for (int j = threadIdx.x; j < nb; j += RT) sprim[j] = list[b0 + j];
-    __syncthreads();
-    // 8 lanes per record, 16 B each: a warp moves 4 whole 128 B records per step
+    const int lane = threadIdx.x & 31;
+    const int my = lane < nb ? list[b0 + lane] : 0;
+    sprim[lane] = my;
     const float4 *src = reinterpret_cast<const float4 *>(recs);
     float4 *dst = reinterpret_cast<float4 *>(srec);
-    for (int k = threadIdx.x; k < nb * 8; k += RT) {
-        int j = k >> 3, q = k & 7;
-        dst[j * 8 + q] = __ldg(src + (size_t)sprim[j] * 8 + q);
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+        const int j = it * 4 + (lane >> 3), q = lane & 7;
+        const int pj = __shfl_sync(FULL, my, j);
+        if (j < nb) dst[j * 8 + q] = __ldg(src + (size_t)pj * 8 + q);
     }
-    __syncthreads();
+    __syncwarp();
+    return my;
 }
 
-// lane mask of warp w's 8x4 block covered by the inclusive pixel box
-__device__ __forceinline__ uint32_t box_lanes(const PrimRec &r, int tile, int tiles_x, int w)
+// lane mask of this block covered by the inclusive pixel box of r
+__device__ __forceinline__ uint32_t block_lanes(const PrimRec &r, int bu, int bv)
 {
-    int ty = tile / tiles_x, tx = tile - ty * tiles_x;
-    int bu = tx * TILE + (w & 1) * 8, bv = ty * TILE + (w >> 1) * 4;
     int c0 = max((int)(r.bb_u & 0xffffu) - bu, 0), c1 = min((int)(r.bb_u >> 16) - bu, 7);
     int r0 = max((int)(r.bb_v & 0xffffu) - bv, 0), r1 = min((int)(r.bb_v >> 16) - bv, 3);
     if (c0 > c1 || r0 > r1) return 0u;
@@ -98,9 +95,9 @@ __device__ __forceinline__ uint32_t box_lanes(const PrimRec &r, int tile, int ti
     return (cols * 0x01010101u) & rows;
 }
 
-// Per-thread ring view into shared memory.
+// Per-lane ring view into shared memory.
 struct Ring {
-    double *t;   // &ring_t[0][tid], stride RT
+    double *t;   // &ring_t[0][lane], stride 32
     int *p;
     int n;
 };
@@ -110,8 +107,8 @@ struct Ring {
 __device__ __forceinline__ bool ring_push(Ring &R, double t, int prim, double &et, int &ep)
 {
     if (R.n < RING) {
-        R.t[R.n * RT] = t;
-        R.p[R.n * RT] = prim;
+        R.t[R.n * 32] = t;
+        R.p[R.n * 32] = prim;
         R.n++;
         return false;
     }
@@ -119,14 +116,14 @@ __device__ __forceinline__ bool ring_push(Ring &R, double t, int prim, double &e
     int jm = 0;
 #pragma unroll
     for (int k = 1; k < RING; ++k) {
-        double tk = R.t[k * RT];
+        double tk = R.t[k * 32];
         if (tk < m) { m = tk; jm = k; }
     }
     if (t < m) { et = t; ep = prim; return true; }
     et = m;
-    ep = R.p[jm * RT];
-    R.t[jm * RT] = t;
-    R.p[jm * RT] = prim;
+    ep = R.p[jm * 32];
+    R.t[jm * 32] = t;
+    R.p[jm * 32] = prim;
     return true;
 }
 
@@ -136,14 +133,14 @@ __device__ __forceinline__ void ring_pop(Ring &R, double &et, int &ep)
     double m = R.t[0];
     int jm = 0;
     for (int k = 1; k < R.n; ++k) {
-        double tk = R.t[k * RT];
+        double tk = R.t[k * 32];
         if (tk < m) { m = tk; jm = k; }
     }
     et = m;
-    ep = R.p[jm * RT];
+    ep = R.p[jm * 32];
     R.n--;
-    R.t[jm * RT] = R.t[R.n * RT];
-    R.p[jm * RT] = R.p[R.n * RT];
+    R.t[jm * 32] = R.t[R.n * 32];
+    R.p[jm * 32] = R.p[R.n * 32];
 }
 
 struct Cfg {
@@ -208,37 +205,30 @@ __device__ __forceinline__ void shade_emitted(const PrimRec &r, const Geo64 &g, 
     normal_curv32(r, f.h, dx, dy, dz, f.nl, f.nc, f.K, f.inrm, f.flip);
 }
 
-__device__ __forceinline__ void load_dir(const double (*d64)[RT], double d[3])
+// accepted-mask word of entry j (tile-list position start+j) for block blk:
+// block-major inside the tile so a warp reads its words contiguously
+__device__ __forceinline__ size_t mask_index(int start, int n, int blk, int j)
 {
-    d[0] = d64[0][threadIdx.x];
-    d[1] = d64[1][threadIdx.x];
-    d[2] = d64[2][threadIdx.x];
+    return (size_t)start * NBLK + (size_t)blk * n + j;
 }
 
 // ================================================================ forward
 
-__global__ void __launch_bounds__(RT, 2)
+__global__ void __launch_bounds__(32, 16)
 raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
                   const int32_t *__restrict__ tile_offsets,
                   const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets out)
 {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    FwdSmem &sm = *reinterpret_cast<FwdSmem *>(smem_raw);
-    const int tile = blockIdx.x;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int u, v;
-    pixel_of(tile, cam.tiles_x, u, v);
+    __shared__ FwdSmem sm;
+    const int lane = threadIdx.x & 31;
+    int tile, blk, u, v;
+    block_pixel(cam.tiles_x, tile, blk, u, v);
+    const int bu = u - (lane & 7), bv = v - (lane >> 3);
     const bool inside = u < cam.W && v < cam.H;
     const Cfg c = make_cfg(st);
-    float dx = 0.f, dy = 0.f, dz = 1.f;
-    {
-        double d[3] = {0.0, 0.0, 1.0};
-        if (inside) pixel_dir64(cam, u, v, d);
-        sm.d64[0][threadIdx.x] = d[0]; sm.d64[1][threadIdx.x] = d[1]; sm.d64[2][threadIdx.x] = d[2];
-        dx = (float)d[0]; dy = (float)d[1]; dz = (float)d[2];
-    }
-    if (threadIdx.x == 0) sm.viol = 0;
-    if (threadIdx.x < 3) sm.cnt[threadIdx.x] = 0ull;
+    double d64[3] = {0.0, 0.0, 1.0};
+    if (inside) pixel_dir64(cam, u, v, d64);
+    const float dx = (float)d64[0], dy = (float)d64[1], dz = (float)d64[2];
 
     double T = 1.0, ac0 = 0, ac1 = 0, ac2 = 0, aa = 0, ad = 0, ad2 = 0, an0 = 0, an1 = 0,
            an2 = 0, ak = 0, adist = 0;
@@ -246,16 +236,14 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
     double last_t = -1.0e300;
     int nfrag = 0, viol = 0;
     unsigned n_box = 0, n_acc = 0;
-    Ring R{&sm.ring_t[0][threadIdx.x], &sm.ring_p[0][threadIdx.x], 0};
+    Ring R{&sm.ring_t[0][lane], &sm.ring_p[0][lane], 0};
     bool alive = inside;
     const uint32_t lanebit = 1u << lane;
 
     auto composite = [&](int ep, double t) {
-        double d[3];
-        load_dir(sm.d64, d);
         Frag f;
         const PrimRec &r = recs[ep];
-        shade_emitted(r, geo[ep], d, dx, dy, dz, t, c, f);
+        shade_emitted(r, geo[ep], d64, dx, dy, dz, t, c, f);
         if (t < last_t - 1e-12) viol++;
         if (t > last_t) last_t = t;
         const double w = f.abar64 * T;
@@ -276,75 +264,50 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         if (T < c.t_term) alive = false;
     };
 
-    const int start = tile_offsets[tile], end = tile_offsets[tile + 1];
-    for (int b0 = start; b0 < end; b0 += BATCH) {
-        if (__syncthreads_count(alive) == 0) break;
-        const int nb = min(BATCH, end - b0);
-        load_batch(sm.rec, sm.prim, recs, tile_prims, b0, nb);
-        if (threadIdx.x < nb) {
-#pragma unroll
-            for (int w = 0; w < NWARP; ++w)
-                sm.lanes[threadIdx.x][w] = box_lanes(sm.rec[threadIdx.x], tile, cam.tiles_x, w);
-        }
-        __syncthreads();
+    const int start = tile_offsets[tile], end = tile_offsets[tile + 1], n = end - start;
+    for (int b0 = start; b0 < end; b0 += WB) {
+        if (!__any_sync(FULL, alive)) break;
+        const int nb = min(WB, end - b0);
+        load_batch32(sm.rec, sm.prim, recs, tile_prims, b0, nb);
+        const uint32_t mymask = lane < nb ? block_lanes(sm.rec[lane], bu, bv) : 0u;
 
         // pass 1: coarse test of every in-box candidate
-        const int nwd = (nb + 31) >> 5;
-        for (int wd = 0; wd < nwd; ++wd) {
-            uint32_t bits = 0u;
-            const int jn = min(32, nb - wd * 32);
-            if (__any_sync(FULL, alive)) {
-                for (int jj = 0; jj < jn; ++jj) {
-                    const int j = wd * 32 + jj;
-                    const uint32_t m = sm.lanes[j][warp];
-                    if (m == 0u) continue;            // warp-uniform skip
-                    if (!(m & lanebit) || !alive) continue;
-                    n_box++;
-                    float roots[2], hx, hy, hz;
-                    if (coarse_roots(sm.rec[j], dx, dy, dz, c.euclid, c.t_clip, roots, hx, hy, hz))
-                        bits |= 1u << jj;
-                }
-            }
-            sm.bits[wd][threadIdx.x] = bits;
+        uint32_t bits = 0u;
+        for (int j = 0; j < nb; ++j) {
+            const uint32_t m = __shfl_sync(FULL, mymask, j);
+            if (m == 0u) continue;                    // warp-uniform skip
+            if (!(m & lanebit) || !alive) continue;
+            n_box++;
+            float roots[2], hx, hy, hz;
+            if (coarse_roots(sm.rec[j], dx, dy, dz, c.euclid, c.t_clip, roots, hx, hy, hz))
+                bits |= 1u << j;
         }
 
         // pass 2: exact test, ring and compositing in stream order
-        double d[3];
-        load_dir(sm.d64, d);
-        for (int wd = 0; wd < nwd; ++wd) {
-            uint32_t bits = sm.bits[wd][threadIdx.x], acc = 0u;
-            while (bits && alive) {
-                const int jj = __ffs(bits) - 1;
-                bits &= bits - 1;
-                const int j = wd * 32 + jj;
-                const int p = sm.prim[j];
-                double t;
-                if (!accept(sm.rec[j], geo[p], d, dx, dy, dz, c, t)) continue;
-                acc |= 1u << jj;
-                n_acc++;
-                double et;
-                int ep;
-                if (ring_step(c, R, t, p, et, ep)) composite(ep, et);
-            }
-            sm.bits[wd][threadIdx.x] = acc;
+        uint32_t acc = 0u;
+        while (bits && alive) {
+            const int j = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const int p = sm.prim[j];
+            double t;
+            if (!accept(sm.rec[j], geo[p], d64, dx, dy, dz, c, t)) continue;
+            acc |= 1u << j;
+            n_acc++;
+            double et;
+            int ep;
+            if (ring_step(c, R, t, p, et, ep)) composite(ep, et);
         }
 
         // record the accepted lanes of every entry for the backward
         if (out.accept_mask) {
-            __syncthreads();   // everyone is done reading the box masks
-            for (int wd = 0; wd < nwd; ++wd) {
-                const uint32_t acc = sm.bits[wd][threadIdx.x];
-                const int jn = min(32, nb - wd * 32);
-                for (int jj = 0; jj < jn; ++jj) {
-                    const uint32_t m = __ballot_sync(FULL, (acc >> jj) & 1u);
-                    if (lane == 0) sm.lanes[wd * 32 + jj][warp] = m;
-                }
+            uint32_t mine = 0u;
+            for (int j = 0; j < nb; ++j) {
+                const uint32_t m = __ballot_sync(FULL, (acc >> j) & 1u);
+                if (lane == j) mine = m;
             }
-            __syncthreads();
-            const uint4 *src = reinterpret_cast<const uint4 *>(&sm.lanes[0][0]);
-            uint4 *dst = reinterpret_cast<uint4 *>(out.accept_mask + (size_t)b0 * NWARP);
-            for (int k = threadIdx.x; k < nb * (NWARP / 4); k += RT) dst[k] = src[k];
+            if (lane < nb) out.accept_mask[mask_index(start, n, blk, b0 - start + lane)] = mine;
         }
+        __syncwarp();
     }
     while (alive && R.n > 0) {
         double et;
@@ -388,16 +351,21 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
             a[AX_T * (size_t)npx + px] = T;
         }
     }
-    __syncthreads();
-    if (viol) atomicAdd(&sm.viol, viol);
-    if (out.counters) {
-        atomicAdd(&sm.cnt[0], (unsigned long long)n_box);
-        atomicAdd(&sm.cnt[1], (unsigned long long)n_acc);
-        atomicAdd(&sm.cnt[2], (unsigned long long)nfrag);
+    // per-tile violations and the work counters
+    for (int o = 16; o; o >>= 1) {
+        viol += __shfl_xor_sync(FULL, viol, o);
+        n_box += __shfl_xor_sync(FULL, n_box, o);
+        n_acc += __shfl_xor_sync(FULL, n_acc, o);
+        nfrag += __shfl_xor_sync(FULL, nfrag, o);
     }
-    __syncthreads();
-    if (threadIdx.x == 0 && out.violations) out.violations[tile] = sm.viol;
-    if (out.counters && threadIdx.x < 3) atomicAdd(&out.counters[threadIdx.x], sm.cnt[threadIdx.x]);
+    if (lane == 0) {
+        if (out.violations) atomicAdd(&out.violations[tile], viol);
+        if (out.counters) {
+            atomicAdd(&out.counters[0], (unsigned long long)n_box);
+            atomicAdd(&out.counters[1], (unsigned long long)n_acc);
+            atomicAdd(&out.counters[2], (unsigned long long)nfrag);
+        }
+    }
 }
 
 // =============================================================== backward
@@ -572,18 +540,16 @@ __device__ __forceinline__ void warp_accumulate(float (*red)[32][KG], bool emit,
     __syncwarp();
 }
 
-__global__ void __launch_bounds__(RT, 2)
+__global__ void __launch_bounds__(32, 16)
 raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
                   const int32_t *__restrict__ tile_offsets,
                   const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets fwd,
                   qgs_upstream upst, float *__restrict__ kg)
 {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    BwdSmem &sm = *reinterpret_cast<BwdSmem *>(smem_raw);
-    const int tile = blockIdx.x;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int u, v;
-    pixel_of(tile, cam.tiles_x, u, v);
+    __shared__ BwdSmem sm;
+    const int lane = threadIdx.x & 31;
+    int tile, blk, u, v;
+    block_pixel(cam.tiles_x, tile, blk, u, v);
     const bool inside = u < cam.W && v < cam.H;
     const Cfg c = make_cfg(st);
     const int npx = cam.W * cam.H, px = inside ? v * cam.W + u : 0;
@@ -607,13 +573,9 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
                                         (double)up.c2 * st.bg[2]);
     up.a = (float)ua64;
 
-    float dx = 0.f, dy = 0.f, dz = 1.f;
-    {
-        double d[3] = {0.0, 0.0, 1.0};
-        if (inside) pixel_dir64(cam, u, v, d);
-        sm.d64[0][threadIdx.x] = d[0]; sm.d64[1][threadIdx.x] = d[1]; sm.d64[2][threadIdx.x] = d[2];
-        dx = (float)d[0]; dy = (float)d[1]; dz = (float)d[2];
-    }
+    double d64[3] = {0.0, 0.0, 1.0};
+    if (inside) pixel_dir64(cam, u, v, d64);
+    const float dx = (float)d64[0], dy = (float)d64[1], dz = (float)d64[2];
     double F0 = 0, F1 = 0, F2 = 0, vtot = 0;
     if (inside && has_up) {
         const double *a = fwd.aux;
@@ -630,17 +592,15 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
                (double)up.dist * 2.0 * a[AX_DIST * (size_t)npx + px];
     }
     double T = 1.0, pref = 0.0;
-    Ring R{&sm.ring_t[0][threadIdx.x], &sm.ring_p[0][threadIdx.x], 0};
+    Ring R{&sm.ring_t[0][lane], &sm.ring_p[0][lane], 0};
     bool alive = inside && has_up;
 
     auto emit_grad = [&](bool emit, int ep, double t) {
         float g[KG];
         if (emit) {
-            double d[3];
-            load_dir(sm.d64, d);
             Frag f;
             const PrimRec &r = recs[ep];
-            shade_emitted(r, geo[ep], d, dx, dy, dz, t, c, f);
+            shade_emitted(r, geo[ep], d64, dx, dy, dz, t, c, f);
             const double w = f.abar64 * T;
             const double V = (double)up.c0 * r.col[0] + (double)up.c1 * r.col[1] +
                              (double)up.c2 * r.col[2] + ua64 + (double)up.d * t +
@@ -656,33 +616,30 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         warp_accumulate(sm.red, emit, ep, g, kg);
     };
 
-    const int start = tile_offsets[tile], end = tile_offsets[tile + 1];
-    for (int b0 = start; b0 < end; b0 += BATCH) {
-        if (__syncthreads_count(alive) == 0) break;
-        const int nb = min(BATCH, end - b0);
-        {
-            const uint4 *src = reinterpret_cast<const uint4 *>(fwd.accept_mask + (size_t)b0 * NWARP);
-            uint4 *dst = reinterpret_cast<uint4 *>(&sm.lanes[0][0]);
-            for (int k = threadIdx.x; k < nb * (NWARP / 4); k += RT) dst[k] = __ldg(src + k);
-        }
-        load_batch(sm.rec, sm.prim, recs, tile_prims, b0, nb);
-        double d[3];
-        load_dir(sm.d64, d);
+    const int start = tile_offsets[tile], end = tile_offsets[tile + 1], n = end - start;
+    for (int b0 = start; b0 < end; b0 += WB) {
+        if (!__any_sync(FULL, alive)) break;
+        const int nb = min(WB, end - b0);
+        const uint32_t mymask =
+            lane < nb ? fwd.accept_mask[mask_index(start, n, blk, b0 - start + lane)] : 0u;
+        if (!__any_sync(FULL, mymask != 0u)) continue;   // nothing accepted in this batch
+        load_batch32(sm.rec, sm.prim, recs, tile_prims, b0, nb);
         for (int j = 0; j < nb; ++j) {
+            const uint32_t m = __shfl_sync(FULL, mymask, j);
+            if (m == 0u) continue;                    // nobody in this block accepted it
             if (!__any_sync(FULL, alive)) break;
-            const uint32_t m = sm.lanes[j][warp];
-            if (m == 0u) continue;                    // nobody in this warp accepted it
             double et = 0.0;
             int ep = -1;
             bool emit = false;
             if (alive && (m >> lane & 1u)) {
                 const int p = sm.prim[j];
                 double t = 0.0;
-                accept(sm.rec[j], geo[p], d, dx, dy, dz, c, t);   // same fp64 depth as forward
+                accept(sm.rec[j], geo[p], d64, dx, dy, dz, c, t);   // same fp64 depth as forward
                 emit = ring_step(c, R, t, p, et, ep);
             }
             if (__any_sync(FULL, emit)) emit_grad(emit, ep, et);
         }
+        __syncwarp();
     }
     while (__any_sync(FULL, alive && R.n > 0)) {
         double et = 0.0;
@@ -703,8 +660,8 @@ __global__ void trace_pixel_kernel(const PrimRec *__restrict__ recs, const Geo64
                                    float *acc_abar, int *em_prim, float *em_t, float *em_abar,
                                    double *em_T, int *counts)
 {
-    __shared__ double ring_t[RING][RT];
-    __shared__ int ring_p[RING][RT];
+    __shared__ double ring_t[RING][32];
+    __shared__ int ring_p[RING][32];
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const Cfg c = make_cfg(st);
     double d[3];
@@ -752,8 +709,5 @@ __global__ void trace_pixel_kernel(const PrimRec *__restrict__ recs, const Geo64
     counts[1] = ne;
 }
 
-
-size_t fwd_smem_bytes() { return sizeof(FwdSmem); }
-size_t bwd_smem_bytes() { return sizeof(BwdSmem); }
 
 }  // namespace qgs
