@@ -43,7 +43,11 @@ struct FwdSmem {
     int prim[WB];
     double ring_t[RING][32];  // per-lane ring, [slot][lane]: conflict-free
     int ring_p[RING][32];
+    double d64[3][32];        // fp64 pixel ray (only the exact path reads it)
+    double acc[11][32];       // fp64 blend sums, touched once per composited fragment
 };
+
+enum { A_C0 = 0, A_A = 3, A_D = 4, A_D2 = 5, A_N0 = 6, A_K = 9, A_DIST = 10 };
 
 struct BwdSmem {
     PrimRec rec[WB];
@@ -226,12 +230,17 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
     const int bu = u - (lane & 7), bv = v - (lane >> 3);
     const bool inside = u < cam.W && v < cam.H;
     const Cfg c = make_cfg(st);
-    double d64[3] = {0.0, 0.0, 1.0};
-    if (inside) pixel_dir64(cam, u, v, d64);
-    const float dx = (float)d64[0], dy = (float)d64[1], dz = (float)d64[2];
+    float dx, dy, dz;
+    {
+        double d[3] = {0.0, 0.0, 1.0};
+        if (inside) pixel_dir64(cam, u, v, d);
+        sm.d64[0][lane] = d[0]; sm.d64[1][lane] = d[1]; sm.d64[2][lane] = d[2];
+        dx = (float)d[0]; dy = (float)d[1]; dz = (float)d[2];
+    }
+#pragma unroll
+    for (int k = 0; k < 11; ++k) sm.acc[k][lane] = 0.0;
 
-    double T = 1.0, ac0 = 0, ac1 = 0, ac2 = 0, aa = 0, ad = 0, ad2 = 0, an0 = 0, an1 = 0,
-           an2 = 0, ak = 0, adist = 0;
+    double T = 1.0;
     float median = 0.f;
     double last_t = -1.0e300;
     int nfrag = 0, viol = 0;
@@ -243,21 +252,24 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
     auto composite = [&](int ep, double t) {
         Frag f;
         const PrimRec &r = recs[ep];
-        shade_emitted(r, geo[ep], d64, dx, dy, dz, t, c, f);
+        double d[3] = {sm.d64[0][lane], sm.d64[1][lane], sm.d64[2][lane]};
+        shade_emitted(r, geo[ep], d, dx, dy, dz, t, c, f);
         if (t < last_t - 1e-12) viol++;
         if (t > last_t) last_t = t;
         const double w = f.abar64 * T;
-        ac0 += w * (double)r.col[0];
-        ac1 += w * (double)r.col[1];
-        ac2 += w * (double)r.col[2];
-        adist += w * (t * t * aa - 2.0 * t * ad + ad2);   // sums before this fragment
-        aa += w;
-        ad += w * t;
-        ad2 += w * t * t;
-        an0 += w * (double)f.nc[0];
-        an1 += w * (double)f.nc[1];
-        an2 += w * (double)f.nc[2];
-        ak += w * (double)f.K;
+        double *a = &sm.acc[0][lane];            // stride 32 doubles per sum
+        const double aa = a[A_A * 32], ad = a[A_D * 32], ad2 = a[A_D2 * 32];
+        a[(A_C0 + 0) * 32] += w * (double)r.col[0];
+        a[(A_C0 + 1) * 32] += w * (double)r.col[1];
+        a[(A_C0 + 2) * 32] += w * (double)r.col[2];
+        a[A_DIST * 32] += w * (t * t * aa - 2.0 * t * ad + ad2);   // sums before this fragment
+        a[A_A * 32] = aa + w;
+        a[A_D * 32] = ad + w * t;
+        a[A_D2 * 32] = ad2 + w * t * t;
+        a[(A_N0 + 0) * 32] += w * (double)f.nc[0];
+        a[(A_N0 + 1) * 32] += w * (double)f.nc[1];
+        a[(A_N0 + 2) * 32] += w * (double)f.nc[2];
+        a[A_K * 32] += w * (double)f.K;
         if (T > 0.5) median = (float)t;
         T *= 1.0 - f.abar64;
         nfrag++;
@@ -290,7 +302,8 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
             bits &= bits - 1;
             const int p = sm.prim[j];
             double t;
-            if (!accept(sm.rec[j], geo[p], d64, dx, dy, dz, c, t)) continue;
+            const double d[3] = {sm.d64[0][lane], sm.d64[1][lane], sm.d64[2][lane]};
+            if (!accept(sm.rec[j], geo[p], d, dx, dy, dz, c, t)) continue;
             acc |= 1u << j;
             n_acc++;
             double et;
@@ -318,6 +331,12 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
 
     if (inside) {
         const int W = cam.W, npx = cam.W * cam.H, px = v * W + u;
+        const double ac0 = sm.acc[A_C0][lane], ac1 = sm.acc[A_C0 + 1][lane],
+                     ac2 = sm.acc[A_C0 + 2][lane], aa = sm.acc[A_A][lane],
+                     ad = sm.acc[A_D][lane], ad2 = sm.acc[A_D2][lane],
+                     an0 = sm.acc[A_N0][lane], an1 = sm.acc[A_N0 + 1][lane],
+                     an2 = sm.acc[A_N0 + 2][lane], ak = sm.acc[A_K][lane],
+                     adist = sm.acc[A_DIST][lane];
         out.color_raw[3 * px + 0] = (float)ac0;
         out.color_raw[3 * px + 1] = (float)ac1;
         out.color_raw[3 * px + 2] = (float)ac2;
