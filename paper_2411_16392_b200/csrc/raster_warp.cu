@@ -284,15 +284,26 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         const uint32_t mymask = lane < nb ? block_lanes(sm.rec[lane], bu, bv) : 0u;
 
         // pass 1: coarse test of every in-box candidate
+        // (two candidates per iteration: their branch-free stage-1 chains
+        // interleave, which hides the SQRT/RCP latencies)
         uint32_t bits = 0u;
-        for (int j = 0; j < nb; ++j) {
-            const uint32_t m = __shfl_sync(FULL, mymask, j);
-            if (m == 0u) continue;                    // warp-uniform skip
-            if (!(m & lanebit) || !alive) continue;
-            n_box++;
-            float roots[2], hx, hy, hz;
-            if (coarse_roots(sm.rec[j], dx, dy, dz, c.euclid, c.t_clip, roots, hx, hy, hz))
+        for (int j = 0; j < nb; j += 2) {
+            const int j1 = min(j + 1, nb - 1);
+            const uint32_t m0 = __shfl_sync(FULL, mymask, j);
+            const uint32_t m1 = j + 1 < nb ? __shfl_sync(FULL, mymask, j1) : 0u;
+            if ((m0 | m1) == 0u) continue;            // warp-uniform skip
+            const bool a0 = alive && (m0 & lanebit), a1 = alive && (m1 & lanebit);
+            if (!(a0 || a1)) continue;
+            n_box += (unsigned)a0 + (unsigned)a1;
+            float r0[2], r1[2], hx0, hy0, hx1, hy1;
+            unsigned s0 = coarse_stage1(sm.rec[j], dx, dy, dz, c.t_clip, r0, hx0, hy0);
+            unsigned s1 = coarse_stage1(sm.rec[j1], dx, dy, dz, c.t_clip, r1, hx1, hy1);
+            s0 = a0 ? s0 : 0u;
+            s1 = a1 ? s1 : 0u;
+            if (s0 && ((s0 & CR_MARGINAL) || coarse_stage2(sm.rec[j], c.euclid, s0, r0, hx0, hy0)))
                 bits |= 1u << j;
+            if (s1 && ((s1 & CR_MARGINAL) || coarse_stage2(sm.rec[j1], c.euclid, s1, r1, hx1, hy1)))
+                bits |= 1u << j1;
         }
 
         // pass 2: exact test, ring and compositing in stream order

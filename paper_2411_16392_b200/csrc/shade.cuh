@@ -206,53 +206,61 @@ __device__ __forceinline__ float arc32_fast(float a, float rho)
     return __fdividef(as + u * r, 4.f * a);
 }
 
-__device__ __forceinline__ unsigned coarse_roots(const PrimRec &r, float dx, float dy, float dz,
-                                                 bool euclid, float t_clip, float roots[2],
-                                                 float &hx, float &hy, float &hz)
+constexpr float COARSE_K = 1.05f;         // margin on the 3-sigma tests
+
+// Stage 1, branch-free (selects only) so that two candidates interleave:
+// roots of the ray quadric and the widened ellipse pre-reject of both roots.
+// Returns bit k = root k survives, CR_MARGINAL = near-tangent (fp64 decides).
+__device__ __forceinline__ unsigned coarse_stage1(const PrimRec &r, float dx, float dy, float dz,
+                                                  float t_clip, float roots[2], float &hx,
+                                                  float &hy)
 {
-    constexpr float K = 1.05f;            // margin on the 3-sigma tests
     const bool planar = (r.flags & 1u) != 0;
     hx = fmaf(r.M[0], dx, fmaf(r.M[1], dy, r.M[2] * dz));
     hy = fmaf(r.M[3], dx, fmaf(r.M[4], dy, r.M[5] * dz));
-    hz = fmaf(r.M[6], dx, fmaf(r.M[7], dy, r.M[8] * dz));
-    int cnt;
-    if (planar) {
-        if (fabsf(hz) < 1e-12f) return 0u;
-        roots[0] = __fdividef(-r.oz, hz);
-        roots[1] = roots[0];
-        cnt = 1;
-    } else {
-        float A = fmaf(r.w1 * hx, hx, r.w2 * hy * hy);
-        float B = 2.f * fmaf(r.w1 * r.ox, hx, r.w2 * r.oy * hy) - r.iw3 * hz;
-        float C = r.C;
-        if (fabsf(A) < 1e-6f) {
-            if (fabsf(B) < 1e-12f) return 0u;
-            roots[0] = __fdividef(-C, B);
-            roots[1] = roots[0];
-            cnt = 1;
-        } else {
-            float disc = fmaf(B, B, -4.f * A * C);
-            // fp32 rounding of disc is ~1e-7 max(B^2, |4AC|); inside a 1e-5
-            // band the sign is decided in fp64
-            if (fabsf(disc) <= 1e-5f * fmaxf(B * B, fabsf(4.f * A * C))) return CR_MARGINAL;
-            if (disc < 0.f) return 0u;
-            float q = -0.5f * (B + copysignf(sqrtf(disc), B));
-            float ra = __fdividef(q, A), rb = (q != 0.f) ? __fdividef(C, q) : ra;
-            roots[0] = fminf(ra, rb);
-            roots[1] = fmaxf(ra, rb);
-            cnt = 2;
-        }
-    }
+    const float hz = fmaf(r.M[6], dx, fmaf(r.M[7], dy, r.M[8] * dz));
+    const float A = fmaf(r.w1 * hx, hx, r.w2 * hy * hy);
+    const float B = 2.f * fmaf(r.w1 * r.ox, hx, r.w2 * r.oy * hy) - r.iw3 * hz;
+    const float C = r.C, AC4 = 4.f * A * C;
+    const float disc = fmaf(B, B, -AC4);
+    const bool lin = fabsf(A) < 1e-6f;
+    const bool quad = !planar && !lin;
+    // fp32 rounding of disc is ~1e-7 max(B^2, |4AC|); inside a 1e-5 band the
+    // sign is decided in fp64
+    const bool marg = quad && fabsf(disc) <= 1e-5f * fmaxf(B * B, fabsf(AC4));
+    const float q = -0.5f * (B + copysignf(sqrtf(fmaxf(disc, 0.f)), B));
+    // one reciprocal serves the first root of every branch
+    const float den = planar ? hz : (lin ? B : A);
+    const float num = planar ? -r.oz : (lin ? -C : q);
+    const float ta = __fdividef(num, den);
+    const float tb = __fdividef(C, q);
+    const float t0 = quad ? fminf(ta, tb) : ta;
+    const float t1 = quad ? fmaxf(ta, tb) : ta;
+    const bool ok = planar ? fabsf(hz) >= 1e-12f : (lin ? fabsf(B) >= 1e-12f : disc >= 0.f);
+    const float lim = (COARSE_K * COARSE_K) * r.ell9;
+    const float x0 = fmaf(t0, hx, r.ox), y0 = fmaf(t0, hy, r.oy);
+    const float x1 = fmaf(t1, hx, r.ox), y1 = fmaf(t1, hy, r.oy);
+    const float m0 = fmaf(r.s2 * x0, r.s2 * x0, (r.s1 * y0) * (r.s1 * y0));
+    const float m1 = fmaf(r.s2 * x1, r.s2 * x1, (r.s1 * y1) * (r.s1 * y1));
+    const float tmin = t_clip * 0.99f;
+    const bool in0 = ok && t0 > tmin && (planar || m0 <= lim);
+    const bool in1 = ok && quad && t1 > tmin && m1 <= lim;
+    roots[0] = t0;
+    roots[1] = t1;
+    return marg ? CR_MARGINAL : ((in0 ? 1u : 0u) | (in1 ? 2u : 0u));
+}
+
+// Stage 2: widened geodesic 3-sigma test of the roots that survived stage 1.
+__device__ __forceinline__ unsigned coarse_stage2(const PrimRec &r, bool euclid, unsigned in,
+                                                  const float roots[2], float hx, float hy)
+{
+    const bool planar = (r.flags & 1u) != 0;
     unsigned pass = 0u;
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-        if (k >= cnt) break;
+        if (!(in & (1u << k))) continue;
         const float t = roots[k];
-        if (!(t > t_clip * 0.99f)) continue;
         float x = fmaf(t, hx, r.ox), y = fmaf(t, hy, r.oy);
-        float ex = r.s2 * x, ey = r.s1 * y;
-        float m = fmaf(ex, ex, ey * ey);
-        if (!planar && m > (K * K) * r.ell9) continue;
         float rho2 = fmaf(x, x, y * y);
         float ir = rsqrtf(fmaxf(rho2, 1e-30f));
         float rho = rho2 * ir;
@@ -261,9 +269,19 @@ __device__ __forceinline__ unsigned coarse_roots(const PrimRec &r, float dx, flo
         float l = (planar || euclid) ? rho : arc32_fast(a, rho);
         float sc = r.s2 * c, ss = r.s1 * s;
         float sig = r.s12 * rsqrtf(fmaf(sc, sc, ss * ss));
-        if (l <= K * 3.f * sig) pass |= 1u << k;
+        if (l <= COARSE_K * 3.f * sig) pass |= 1u << k;
     }
     return pass;
+}
+
+__device__ __forceinline__ unsigned coarse_roots(const PrimRec &r, float dx, float dy, float dz,
+                                                 bool euclid, float t_clip, float roots[2],
+                                                 float &hx, float &hy, float &hz)
+{
+    hz = 0.f;
+    const unsigned in = coarse_stage1(r, dx, dy, dz, t_clip, roots, hx, hy);
+    if (in == 0u || (in & CR_MARGINAL)) return in;
+    return coarse_stage2(r, euclid, in, roots, hx, hy);
 }
 
 // Full candidate test: coarse fp32 roots, fp64 refinement, exact selection.
