@@ -45,16 +45,12 @@ struct FwdSmem {
     int ring_p[RING][32];
     double d64[3][32];        // fp64 pixel ray (only the exact path reads it)
     double acc[11][32];       // fp64 blend sums, touched once per composited fragment
+    float pay[RING][5][32];   // ring payload: abar, camera normal (3), curvature
+    float tfirst[WB][32];     // pass 1 -> pass 2: first coarse root that survived
 };
 
-enum { A_C0 = 0, A_A = 3, A_D = 4, A_D2 = 5, A_N0 = 6, A_K = 9, A_DIST = 10 };
-
-struct BwdSmem {
-    PrimRec rec[WB];
-    int prim[WB];
-    double ring_t[RING][32];
-    int ring_p[RING][32];
-    float red[1][32][KG];
+struct Pay {
+    float abar, n0, n1, n2, K;
 };
 
 // (tile, block) of this CTA and the lane's pixel
@@ -146,6 +142,68 @@ __device__ __forceinline__ void ring_pop(Ring &R, double &et, int &ep)
     R.t[jm * 32] = R.t[R.n * 32];
     R.p[jm * 32] = R.p[R.n * 32];
 }
+
+// forward ring with payload (same ordering rule as ring_push / ring_pop)
+__device__ __forceinline__ bool ring_push_pay(Ring &R, float (*pay)[5][32], int lane, double t,
+                                              int prim, const Pay &in, double &et, int &ep,
+                                              Pay &out)
+{
+    if (R.n < RING) {
+        R.t[R.n * 32] = t;
+        R.p[R.n * 32] = prim;
+        pay[R.n][0][lane] = in.abar; pay[R.n][1][lane] = in.n0; pay[R.n][2][lane] = in.n1;
+        pay[R.n][3][lane] = in.n2; pay[R.n][4][lane] = in.K;
+        R.n++;
+        return false;
+    }
+    double m = R.t[0];
+    int jm = 0;
+#pragma unroll
+    for (int k = 1; k < RING; ++k) {
+        double tk = R.t[k * 32];
+        if (tk < m) { m = tk; jm = k; }
+    }
+    if (t < m) { et = t; ep = prim; out = in; return true; }
+    et = m;
+    ep = R.p[jm * 32];
+    out.abar = pay[jm][0][lane]; out.n0 = pay[jm][1][lane]; out.n1 = pay[jm][2][lane];
+    out.n2 = pay[jm][3][lane]; out.K = pay[jm][4][lane];
+    R.t[jm * 32] = t;
+    R.p[jm * 32] = prim;
+    pay[jm][0][lane] = in.abar; pay[jm][1][lane] = in.n0; pay[jm][2][lane] = in.n1;
+    pay[jm][3][lane] = in.n2; pay[jm][4][lane] = in.K;
+    return true;
+}
+
+__device__ __forceinline__ void ring_pop_pay(Ring &R, float (*pay)[5][32], int lane, double &et,
+                                             int &ep, Pay &out)
+{
+    double m = R.t[0];
+    int jm = 0;
+    for (int k = 1; k < R.n; ++k) {
+        double tk = R.t[k * 32];
+        if (tk < m) { m = tk; jm = k; }
+    }
+    et = m;
+    ep = R.p[jm * 32];
+    out.abar = pay[jm][0][lane]; out.n0 = pay[jm][1][lane]; out.n1 = pay[jm][2][lane];
+    out.n2 = pay[jm][3][lane]; out.K = pay[jm][4][lane];
+    R.n--;
+    R.t[jm * 32] = R.t[R.n * 32];
+    R.p[jm * 32] = R.p[R.n * 32];
+#pragma unroll
+    for (int f = 0; f < 5; ++f) pay[jm][f][lane] = pay[R.n][f][lane];
+}
+
+enum { A_C0 = 0, A_A = 3, A_D = 4, A_D2 = 5, A_N0 = 6, A_K = 9, A_DIST = 10 };
+
+struct BwdSmem {
+    PrimRec rec[WB];
+    int prim[WB];
+    double ring_t[RING][32];
+    int ring_p[RING][32];
+    float red[1][32][KG];
+};
 
 struct Cfg {
     float t_clip, alpha_floor, alpha_clamp;
@@ -249,14 +307,12 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
     bool alive = inside;
     const uint32_t lanebit = 1u << lane;
 
-    auto composite = [&](int ep, double t) {
-        Frag f;
+    auto composite = [&](int ep, double t, const Pay &f) {
         const PrimRec &r = recs[ep];
-        double d[3] = {sm.d64[0][lane], sm.d64[1][lane], sm.d64[2][lane]};
-        shade_emitted(r, geo[ep], d, dx, dy, dz, t, c, f);
         if (t < last_t - 1e-12) viol++;
         if (t > last_t) last_t = t;
-        const double w = f.abar64 * T;
+        const double abar64 = f.abar < 0.f ? c.alpha_clamp64 : (double)f.abar;  // <0: clamped
+        const double w = abar64 * T;
         double *a = &sm.acc[0][lane];            // stride 32 doubles per sum
         const double aa = a[A_A * 32], ad = a[A_D * 32], ad2 = a[A_D2 * 32];
         a[(A_C0 + 0) * 32] += w * (double)r.col[0];
@@ -266,12 +322,12 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         a[A_A * 32] = aa + w;
         a[A_D * 32] = ad + w * t;
         a[A_D2 * 32] = ad2 + w * t * t;
-        a[(A_N0 + 0) * 32] += w * (double)f.nc[0];
-        a[(A_N0 + 1) * 32] += w * (double)f.nc[1];
-        a[(A_N0 + 2) * 32] += w * (double)f.nc[2];
+        a[(A_N0 + 0) * 32] += w * (double)f.n0;
+        a[(A_N0 + 1) * 32] += w * (double)f.n1;
+        a[(A_N0 + 2) * 32] += w * (double)f.n2;
         a[A_K * 32] += w * (double)f.K;
         if (T > 0.5) median = (float)t;
-        T *= 1.0 - f.abar64;
+        T *= 1.0 - abar64;
         nfrag++;
         if (T < c.t_term) alive = false;
     };
@@ -286,7 +342,7 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         // pass 1: coarse test of every in-box candidate
         // (two candidates per iteration: their branch-free stage-1 chains
         // interleave, which hides the SQRT/RCP latencies)
-        uint32_t bits = 0u;
+        uint32_t bits = 0u, margb = 0u, secb = 0u;
         for (int j = 0; j < nb; j += 2) {
             const int j1 = min(j + 1, nb - 1);
             const uint32_t m0 = __shfl_sync(FULL, mymask, j);
@@ -300,10 +356,24 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
             unsigned s1 = coarse_stage1(sm.rec[j1], dx, dy, dz, c.t_clip, r1, hx1, hy1);
             s0 = a0 ? s0 : 0u;
             s1 = a1 ? s1 : 0u;
-            if (s0 && ((s0 & CR_MARGINAL) || coarse_stage2(sm.rec[j], c.euclid, s0, r0, hx0, hy0)))
-                bits |= 1u << j;
-            if (s1 && ((s1 & CR_MARGINAL) || coarse_stage2(sm.rec[j1], c.euclid, s1, r1, hx1, hy1)))
-                bits |= 1u << j1;
+            if (s0) {
+                const unsigned p = (s0 & CR_MARGINAL) ? s0 : coarse_stage2(sm.rec[j], c.euclid, s0, r0, hx0, hy0);
+                if (p) {
+                    bits |= 1u << j;
+                    if (p & CR_MARGINAL) margb |= 1u << j;
+                    else sm.tfirst[j][lane] = (p & 1u) ? r0[0] : r0[1];
+                    if ((p & 3u) == 3u) secb |= 1u << j;
+                }
+            }
+            if (s1) {
+                const unsigned p = (s1 & CR_MARGINAL) ? s1 : coarse_stage2(sm.rec[j1], c.euclid, s1, r1, hx1, hy1);
+                if (p) {
+                    bits |= 1u << j1;
+                    if (p & CR_MARGINAL) margb |= 1u << j1;
+                    else sm.tfirst[j1][lane] = (p & 1u) ? r1[0] : r1[1];
+                    if ((p & 3u) == 3u) secb |= 1u << j1;
+                }
+            }
         }
 
         // pass 2: exact test, ring and compositing in stream order
@@ -312,14 +382,31 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
             const int j = __ffs(bits) - 1;
             bits &= bits - 1;
             const int p = sm.prim[j];
-            double t;
+            const PrimRec &r = sm.rec[j];
             const double d[3] = {sm.d64[0][lane], sm.d64[1][lane], sm.d64[2][lane]};
-            if (!accept(sm.rec[j], geo[p], d, dx, dy, dz, c, t)) continue;
+            Hit h;
+            if (!hit_exact_from(r, geo[p], d, dx, dy, dz, c.euclid, c.t_clip, sm.tfirst[j][lane],
+                                (secb >> j) & 1u, (margb >> j) & 1u, h))
+                continue;
+            const float abar = r.alpha * h.G;
+            if (abar < c.alpha_floor) continue;
             acc |= 1u << j;
             n_acc++;
+            // fragment payload now, so compositing never re-shades (raster_kernels.py:58-80)
+            Pay pin;
+            {
+                float nl[3], nc[3], K, inrm, flip;
+                normal_curv32(r, h, dx, dy, dz, nl, nc, K, inrm, flip);
+                pin.abar = abar > c.alpha_clamp ? -c.alpha_clamp : abar;
+                pin.n0 = nc[0]; pin.n1 = nc[1]; pin.n2 = nc[2]; pin.K = K;
+            }
             double et;
             int ep;
-            if (ring_step(c, R, t, p, et, ep)) composite(ep, et);
+            Pay pout;
+            bool emit;
+            if (!c.resort) { et = h.t64; ep = p; pout = pin; emit = true; }
+            else emit = ring_push_pay(R, sm.pay, lane, h.t64, p, pin, et, ep, pout);
+            if (emit) composite(ep, et, pout);
         }
 
         // record the accepted lanes of every entry for the backward
@@ -336,8 +423,9 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
     while (alive && R.n > 0) {
         double et;
         int ep;
-        ring_pop(R, et, ep);
-        composite(ep, et);
+        Pay pout;
+        ring_pop_pay(R, sm.pay, lane, et, ep, pout);
+        composite(ep, et, pout);
     }
 
     if (inside) {

@@ -284,6 +284,28 @@ __device__ __forceinline__ unsigned coarse_roots(const PrimRec &r, float dx, flo
     return coarse_stage2(r, euclid, in, roots, hx, hy);
 }
 
+// Exact test of a candidate whose coarse stage already ran: `t_first` is the
+// first root that survived it, `second` whether root 1 survived too,
+// `marginal` the near-tangent flag.  Same decisions as hit_refined.
+__device__ __forceinline__ bool hit_exact_from(const PrimRec &r, const Geo64 &g,
+                                               const double d64[3], float dx, float dy,
+                                               float dz, bool euclid, float t_clip,
+                                               float t_first, bool second, bool marginal,
+                                               Hit &h)
+{
+    if (marginal) return hit_marginal(r, g, d64, euclid, t_clip, h);
+    const bool planar = (r.flags & 1u) != 0;
+    double dh[3];
+    local_dir64(g, d64, dh);
+    if (planar && fabs(dh[2]) < 1e-12) return false;
+    if (confirm_root(r, g, dh, refine_depth(g, dh, planar, t_first), planar, euclid, t_clip, h))
+        return true;
+    if (!second) return false;
+    float roots[2], hx, hy;
+    coarse_stage1(r, dx, dy, dz, t_clip, roots, hx, hy);
+    return confirm_root(r, g, dh, refine_depth(g, dh, planar, roots[1]), planar, euclid, t_clip, h);
+}
+
 // Full candidate test: coarse fp32 roots, fp64 refinement, exact selection.
 // Returns the selected hit (valid, before the alpha floor) or false.
 __device__ __forceinline__ bool hit_refined(const PrimRec &r, const Geo64 &g, const double d64[3],
