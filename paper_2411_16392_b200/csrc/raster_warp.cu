@@ -34,7 +34,7 @@
 
 namespace qgs {
 
-constexpr int WB = 32;        // entries per batch == lanes
+constexpr int WB = 16;        // entries per batch (<= 32); small keeps smem per warp low
 constexpr int NBLK = 8;       // 8x4 blocks per 16x16 tile
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -71,11 +71,11 @@ __device__ __forceinline__ int load_batch32(PrimRec *srec, int *sprim,
 {
     const int lane = threadIdx.x & 31;
     const int my = lane < nb ? list[b0 + lane] : 0;
-    sprim[lane] = my;
+    if (lane < WB) sprim[lane] = my;
     const float4 *src = reinterpret_cast<const float4 *>(recs);
     float4 *dst = reinterpret_cast<float4 *>(srec);
 #pragma unroll
-    for (int it = 0; it < 8; ++it) {
+    for (int it = 0; it < WB / 4; ++it) {
         const int j = it * 4 + (lane >> 3), q = lane & 7;
         const int pj = __shfl_sync(FULL, my, j);
         if (j < nb) dst[j * 8 + q] = __ldg(src + (size_t)pj * 8 + q);
