@@ -89,6 +89,13 @@ typedef struct qgs_targets {
                                   mask of each of the tile's 8 warps; written by the
                                   forward, required by qgs_backward (may be NULL for a
                                   forward-only call) */
+    int32_t *frag_prim;        /* optional fragment log (NULL = none): for every pixel, the
+                                  primitive of each composited fragment in compositing
+                                  order; layout [raster warp][k < frag_cap][lane], one
+                                  raster warp per 8x4 block, 8 per tile (tile-major) */
+    double *frag_t;            /* same layout: float64 depth of each logged fragment */
+    int32_t frag_cap;          /* fragments logged per pixel; a block with a pixel over
+                                  the cap is replayed from accept_mask by the backward */
 } qgs_targets;
 
 /* Upstream map gradients (rasterizer.py:230-250); NULL = all zero. */

@@ -306,6 +306,7 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
     Ring R{&sm.ring_t[0][lane], &sm.ring_p[0][lane], 0};
     bool alive = inside;
     const uint32_t lanebit = 1u << lane;
+    const bool log_on = out.frag_prim != nullptr && out.frag_t != nullptr;
 
     auto composite = [&](int ep, double t, const Pay &f) {
         const PrimRec &r = recs[ep];
@@ -328,6 +329,11 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         a[A_K * 32] += w * (double)f.K;
         if (T > 0.5) median = (float)t;
         T *= 1.0 - abar64;
+        if (log_on && nfrag < out.frag_cap) {
+            const size_t o = ((size_t)blockIdx.x * out.frag_cap + nfrag) * 32 + lane;
+            out.frag_prim[o] = ep;
+            out.frag_t[o] = t;
+        }
         nfrag++;
         if (T < c.t_term) alive = false;
     };
@@ -733,6 +739,30 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         }
         warp_accumulate(sm.red, emit, ep, g, kg);
     };
+
+    // Fragment log written by the forward: the composited sequence of every
+    // pixel, so no candidate is re-tested and no ring is replayed.
+    {
+        const int nf = alive ? fwd.n_fragments[px] : 0;
+        const int nf_max = __reduce_max_sync(FULL, nf);
+        if (fwd.frag_prim && fwd.frag_t && nf_max <= fwd.frag_cap) {
+            const size_t base = (size_t)blockIdx.x * fwd.frag_cap * 32 + lane;
+            int np_ = -1;
+            double nt_ = 0.0;
+            if (0 < nf) { np_ = fwd.frag_prim[base]; nt_ = fwd.frag_t[base]; }
+            for (int k = 0; k < nf_max; ++k) {
+                const bool emit = k < nf;
+                const int ep = np_;
+                const double et = nt_;
+                if (k + 1 < nf) {                // prefetch the next fragment
+                    np_ = fwd.frag_prim[base + (size_t)(k + 1) * 32];
+                    nt_ = fwd.frag_t[base + (size_t)(k + 1) * 32];
+                }
+                emit_grad(emit, ep, et);
+            }
+            return;
+        }
+    }
 
     const int start = tile_offsets[tile], end = tile_offsets[tile + 1], n = end - start;
     for (int b0 = start; b0 < end; b0 += WB) {

@@ -23,6 +23,11 @@ from .model import ParameterError, PrimitiveSet
 
 T_NEAR_CLIP = 0.01   # intersect.py:22
 TILE = 16            # bounds.py:19
+# Fragment log kept by the forward for the backward: 12 B per logged
+# fragment, at most FRAG_CAP per pixel and FRAG_LOG_BYTES per view (blocks
+# with a deeper pixel are replayed from the accept masks instead).
+FRAG_CAP = 512
+FRAG_LOG_BYTES = 12 << 30
 
 
 @dataclass
@@ -223,6 +228,8 @@ class RenderTargets:
     violations: torch.Tensor      # per tile (int32)
     aux: torch.Tensor             # (12, H, W) float64 blend sums for the backward
     accept_mask: torch.Tensor = None   # (n_pairs * 8,) accepted-lane masks for the backward
+    frag_prim: torch.Tensor = None     # fragment log (blocks, cap, 32) int32 primitive ids
+    frag_t: torch.Tensor = None        # fragment log (blocks, cap, 32) float64 depths
 
     @property
     def order_violations(self):
@@ -365,6 +372,13 @@ def forward(prep: PreparedView, keep_aux=True, counters=None) -> RenderTargets:
     tg.accept_mask = (torch.empty((max(prep.n_pairs, 1) * 8,), dtype=torch.int32, device=device)
                       if keep_aux else None)
     t.accept_mask = _ptr(tg.accept_mask)
+    if keep_aux:
+        blocks = prep.tiles_x * prep.tiles_y * 8
+        cap = int(min(FRAG_CAP, FRAG_LOG_BYTES // (blocks * 32 * 12)))
+        if cap > 0:
+            tg.frag_prim = torch.empty((blocks, cap, 32), dtype=torch.int32, device=device)
+            tg.frag_t = torch.empty((blocks, cap, 32), dtype=torch.float64, device=device)
+            t.frag_prim, t.frag_t, t.frag_cap = _ptr(tg.frag_prim), _ptr(tg.frag_t), cap
     t.counters = _ptr(counters)
     _lib.check(_lib.load().qgs_forward(_ptr(prep.prep), len(prep.dev), prep._cam_c, prep._st_c,
                                        _ptr(prep.tile_offsets), _ptr(prep.tile_prims), t,
@@ -403,6 +417,9 @@ def kernel_grads(prep: PreparedView, targets: RenderTargets, upstream, kg=None) 
         raise ValueError("backward needs forward(prep, keep_aux=True)")
     t.aux = _ptr(targets.aux)
     t.accept_mask = _ptr(targets.accept_mask)
+    if targets.frag_prim is not None:
+        t.frag_prim, t.frag_t = _ptr(targets.frag_prim), _ptr(targets.frag_t)
+        t.frag_cap = targets.frag_prim.shape[1]
     if kg is None:
         kg = torch.zeros((len(prep.dev), _lib.KG_STRIDE), dtype=torch.float32, device=device)
     _lib.check(_lib.load().qgs_backward(_ptr(prep.prep), len(prep.dev), prep._cam_c, prep._st_c,
