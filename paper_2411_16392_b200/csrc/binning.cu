@@ -178,189 +178,229 @@ __global__ void pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, S
 }
 
 // ------------------------------------------------------- per-tile sort
-
+//
+// One CTA per tile, two levels:
+//   1. bucket (MSD) pass: the f32 key bits that vary inside the tile are cut
+//      into nb buckets (nb ~ n/4, a power of two); histogram, scan and an
+//      unstable scatter (shared-memory cursors) into a staging array --
+//      shared memory when the tile fits, else its slice of `tmp` (L2-resident
+//      at these sizes).  Nothing downstream depends on the scatter order.
+//   2. each bucket is sorted by the full composite (f32 key bits, prim id):
+//      <= 32 items by a warp bitonic network in registers, <= SORT_RANK_MAX by
+//      a warp's rank count, larger (degenerate) ones by the whole CTA's rank
+//      count.  Runs of equal f32 keys are then ordered by (fp64 key, prim)
+//      (fix_run), which gives exactly lexsort((prim, key, tile)).
 constexpr int SORT_T = 512;
-constexpr int SORT_IPT = 16;
 constexpr int SORT_W = SORT_T / 32;
-constexpr int CHUNK = SORT_T * SORT_IPT;
+constexpr int SORT_IPT = 4;
+constexpr int SORT_CHUNK = SORT_T * SORT_IPT;     // items per register pass
+constexpr int SORT_SMEM_ITEMS = 8192;             // staged in shared memory up to this
+constexpr int SORT_MAX_BUCKETS = 4096;
+constexpr int SORT_RANK_MAX = 256;
 
 struct SortSmem {
-    uint64_t buf[CHUNK];             // single-chunk segments live here
-    int warp_cnt[SORT_W][256];       // per-warp digit counts -> prefixes
-    int base[256];                   // running output base per digit
-    int hist[256];
+    uint64_t buf[SORT_SMEM_ITEMS];
+    int bstart[SORT_MAX_BUCKETS + 1];
+    int cursor[SORT_MAX_BUCKETS];
     int scan_w[32];
     uint32_t kmin, kmax;
-    int flag;
+    int nbig;
 };
 
-__device__ inline int warp_striped_index(int k)
+__device__ __noinline__ double key64_of(uint64_t v, int tile, const PrepView &pv,
+                                        const CamK &cam, const SetK &st)
 {
-    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    return w * (32 * SORT_IPT) + k * 32 + lane;
+    return tile_key_geo(pv.geo[(uint32_t)v], tile, cam, st.euclid != 0, st.t_clip);
 }
 
-// Stable rank of one chunk (items warp-striped), digits in [0,256), 256 =
-// invalid.  On return, rank[k] = base[d] + (#items of digit d before it in
-// this chunk); then base[d] advances by the chunk's digit counts.
-__device__ void chunk_rank(SortSmem &sm, const int (&dig)[SORT_IPT], int (&rank)[SORT_IPT])
+// Final position of composite x inside its bucket [b0, b1) of `a`: items
+// with a smaller f32 key, plus items with the same f32 key that precede it in
+// (fp64 key, prim) order.  Composites are distinct (prim ids are), and equal
+// f32 keys are rare, so the fp64 keys are recomputed only for those.
+__device__ __forceinline__ int rank_in_bucket(const uint64_t *a, int b0, int b1, uint64_t x,
+                                              int tile, const PrepView &pv, const CamK &cam,
+                                              const SetK &st)
 {
-    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    unsigned lt = (1u << lane) - 1u;
-    for (int d = lane; d < 256; d += 32) sm.warp_cnt[w][d] = 0;
-    __syncwarp();
+    const uint32_t h = (uint32_t)(x >> 32), p = (uint32_t)x;
+    int r = 0;
+    bool have = false;
+    double kx = 0.0;
+    for (int j = b0; j < b1; ++j) {
+        const uint64_t y = a[j];
+        const uint32_t hy = (uint32_t)(y >> 32);
+        if (hy < h) {
+            ++r;
+        } else if (hy == h && y != x) {
+            if (!have) { kx = key64_of(x, tile, pv, cam, st); have = true; }
+            const double ky = key64_of(y, tile, pv, cam, st);
+            r += (ky < kx || (ky == kx && (uint32_t)y < p)) ? 1 : 0;
+        }
+    }
+    return r;
+}
+
+// warp bitonic sort of 32 u64 values, one per lane (ascending by lane)
+__device__ __forceinline__ uint64_t warp_bitonic32(uint64_t x)
+{
+    const int lane = threadIdx.x & 31;
 #pragma unroll
-    for (int k = 0; k < SORT_IPT; ++k) {
-        int d = dig[k];
-        unsigned peers = __match_any_sync(0xffffffffu, d);
-        int before = d < 256 ? sm.warp_cnt[w][d] : 0;
-        rank[k] = before + __popc(peers & lt);
-        __syncwarp();
-        if (d < 256 && (peers & lt) == 0) sm.warp_cnt[w][d] = before + __popc(peers);
-        __syncwarp();
-    }
-    __syncthreads();
-    // per-digit prefix over warps; warp prefix + running base
-    for (int d = threadIdx.x; d < 256; d += SORT_T) {
-        int run = sm.base[d];
-        for (int ww = 0; ww < SORT_W; ++ww) {
-            int c = sm.warp_cnt[ww][d];
-            sm.warp_cnt[ww][d] = run;
-            run += c;
-        }
-        sm.base[d] = run;
-    }
-    __syncthreads();
+    for (int k = 2; k <= 32; k <<= 1) {
 #pragma unroll
-    for (int k = 0; k < SORT_IPT; ++k)
-        if (dig[k] < 256) rank[k] += sm.warp_cnt[w][dig[k]];
-    __syncthreads();
-}
-
-__device__ void digit_base_from_hist(SortSmem &sm)
-{
-    __syncthreads();
-    int v = threadIdx.x < 256 ? sm.hist[threadIdx.x] : 0;
-    int tot;
-    int ex = block_exclusive_scan<int>(v, sm.scan_w, tot);
-    if (threadIdx.x < 256) sm.base[threadIdx.x] = ex;
-    __syncthreads();
-}
-
-// (fp64 key, prim) ordering for an equal-f32 run, insertion sort (stable)
-__device__ void fix_run(uint64_t *a, int len, int tile, const PrepView &pv, const CamK &cam,
-                        const SetK &st)
-{
-    double kk[64];
-    if (len > 64) {
-        // long run of identical f32 keys (degenerate input): sort without caching
-        for (int i = 1; i < len; ++i) {
-            uint64_t x = a[i];
-            double kx = tile_key_geo(pv.geo[(uint32_t)x], tile, cam, st.euclid != 0, st.t_clip);
-            int j = i - 1;
-            while (j >= 0) {
-                uint32_t pj = (uint32_t)a[j];
-                double kj = tile_key_geo(pv.geo[pj], tile, cam, st.euclid != 0, st.t_clip);
-                if (kj > kx || (kj == kx && pj > (uint32_t)x)) { a[j + 1] = a[j]; --j; }
-                else break;
-            }
-            a[j + 1] = x;
-        }
-        return;
-    }
-    for (int i = 0; i < len; ++i)
-        kk[i] = tile_key_geo(pv.geo[(uint32_t)a[i]], tile, cam, st.euclid != 0, st.t_clip);
-    for (int i = 1; i < len; ++i) {
-        uint64_t x = a[i];
-        double kx = kk[i];
-        int j = i - 1;
-        while (j >= 0 && (kk[j] > kx || (kk[j] == kx && (uint32_t)a[j] > (uint32_t)x))) {
-            a[j + 1] = a[j]; kk[j + 1] = kk[j]; --j;
-        }
-        a[j + 1] = x; kk[j + 1] = kx;
-    }
-}
-
-__device__ void fixup_and_emit(uint64_t *a, int n, int tile, const PrepView &pv, const CamK &cam,
-                               const SetK &st, int32_t *out)
-{
-    for (int i = threadIdx.x; i < n; i += SORT_T) {
-        uint32_t h = (uint32_t)(a[i] >> 32);
-        bool head = (i == 0 || (uint32_t)(a[i - 1] >> 32) != h) && i + 1 < n &&
-                    (uint32_t)(a[i + 1] >> 32) == h;
-        if (head) {
-            int j = i + 1;
-            while (j < n && (uint32_t)(a[j] >> 32) == h) ++j;
-            fix_run(a + i, j - i, tile, pv, cam, st);
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const uint64_t y = __shfl_xor_sync(0xffffffffu, x, j);
+            const bool up = (lane & k) == 0;
+            const bool low = (lane & j) == 0;
+            x = (low == up) ? (x < y ? x : y) : (x < y ? y : x);
         }
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < n; i += SORT_T) out[i] = (int32_t)(uint32_t)a[i];
+    return x;
 }
 
-__global__ void __launch_bounds__(SORT_T)
+__global__ void __launch_bounds__(SORT_T, 2)
 tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint64_t *tmp,
                  PrepView pv, CamK cam, SetK st, int32_t *tile_prims)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SortSmem &sm = *reinterpret_cast<SortSmem *>(smem_raw);
-    int tile = blockIdx.x;
-    int start = tile_offsets[tile], n = tile_offsets[tile + 1] - start;
+    const int tile = blockIdx.x;
+    const int start = tile_offsets[tile], n = tile_offsets[tile + 1] - start;
     if (n == 0) return;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint64_t *src = keys + start;
+    int32_t *out = tile_prims + start;
     if (n == 1) {
-        if (threadIdx.x == 0) tile_prims[start] = (int32_t)(uint32_t)keys[start];
+        if (threadIdx.x == 0) out[0] = (int32_t)(uint32_t)src[0];
         return;
     }
-    uint64_t *src = keys + start, *dst = tmp + start;
-    bool single = n <= CHUNK;
-    // key range -> bits to sort
-    if (threadIdx.x == 0) { sm.kmin = 0xffffffffu; sm.kmax = 0u; }
-    __syncthreads();
-    uint32_t lmin = 0xffffffffu, lmax = 0;
-    for (int i = threadIdx.x; i < n; i += SORT_T) {
-        uint64_t v = src[i];
-        if (single) sm.buf[i] = v;
-        uint32_t h = (uint32_t)(v >> 32);
-        lmin = min(lmin, h); lmax = max(lmax, h);
-    }
-    atomicMin(&sm.kmin, lmin);
-    atomicMax(&sm.kmax, lmax);
-    __syncthreads();
-    uint32_t diff = sm.kmin ^ sm.kmax;
-    int bits = diff ? 32 - __clz(diff) : 0;
+    uint64_t *stage = n <= SORT_SMEM_ITEMS ? sm.buf : tmp + start;
+    const bool regs = n <= SORT_CHUNK;     // one register pass holds the whole tile
 
-    for (int shift = 0; shift < bits; shift += 8) {
-        // segment digit histogram -> base offsets
-        for (int d = threadIdx.x; d < 256; d += SORT_T) sm.hist[d] = 0;
-        __syncthreads();
-        const uint64_t *in = single ? sm.buf : src;
-        for (int i = threadIdx.x; i < n; i += SORT_T)
-            atomicAdd(&sm.hist[(uint32_t)(in[i] >> (32 + shift)) & 0xffu], 1);
-        digit_base_from_hist(sm);
-        for (int c0 = 0; c0 < n; c0 += CHUNK) {
-            uint64_t it[SORT_IPT];
-            int dig[SORT_IPT], rank[SORT_IPT];
+    // key range
+    if (threadIdx.x == 0) { sm.kmin = 0xffffffffu; sm.kmax = 0u; sm.nbig = 0; }
+    uint64_t it[SORT_IPT];
+    uint32_t lmin = 0xffffffffu, lmax = 0u;
+    for (int c0 = 0; c0 < n; c0 += SORT_CHUNK) {
 #pragma unroll
-            for (int k = 0; k < SORT_IPT; ++k) {
-                int idx = c0 + warp_striped_index(k);
-                bool ok = idx < n;
-                it[k] = ok ? in[idx] : 0ull;
-                dig[k] = ok ? (int)((uint32_t)(it[k] >> (32 + shift)) & 0xffu) : 256;
+        for (int k = 0; k < SORT_IPT; ++k) {
+            const int i = c0 + k * SORT_T + threadIdx.x;
+            it[k] = i < n ? src[i] : 0ull;
+            if (i < n) {
+                const uint32_t h = (uint32_t)(it[k] >> 32);
+                lmin = min(lmin, h); lmax = max(lmax, h);
             }
-            chunk_rank(sm, dig, rank);   // ends with __syncthreads: all reads done
-            uint64_t *out = single ? sm.buf : dst;
-#pragma unroll
-            for (int k = 0; k < SORT_IPT; ++k)
-                if (dig[k] < 256) out[rank[k]] = it[k];
-            __syncthreads();
         }
-        if (!single) { uint64_t *t = src; src = dst; dst = t; }
     }
-    if (single) {
-        fixup_and_emit(sm.buf, n, tile, pv, cam, st, tile_prims + start);
-    } else {
-        __syncthreads();
-        fixup_and_emit(src, n, tile, pv, cam, st, tile_prims + start);
+    for (int o = 16; o; o >>= 1) {
+        lmin = min(lmin, __shfl_xor_sync(0xffffffffu, lmin, o));
+        lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+    }
+    int nb = 64;
+    while (nb < SORT_MAX_BUCKETS && nb * 4 < n) nb <<= 1;
+    for (int d = threadIdx.x; d < nb; d += SORT_T) sm.cursor[d] = 0;
+    __syncthreads();
+    if (lane == 0) { atomicMin(&sm.kmin, lmin); atomicMax(&sm.kmax, lmax); }
+    __syncthreads();
+    const uint32_t kmin = sm.kmin, range = sm.kmax - sm.kmin;
+    int shift = 0;
+    while ((range >> shift) >= (uint32_t)nb) ++shift;
+
+    // histogram
+    for (int c0 = 0; c0 < n; c0 += SORT_CHUNK) {
+#pragma unroll
+        for (int k = 0; k < SORT_IPT; ++k) {
+            const int i = c0 + k * SORT_T + threadIdx.x;
+            if (i < n) {
+                const uint64_t v = regs ? it[k] : src[i];
+                atomicAdd(&sm.cursor[(((uint32_t)(v >> 32)) - kmin) >> shift], 1);
+            }
+        }
+    }
+    __syncthreads();
+    // exclusive scan of the bucket counts (nb <= 4096 = 8 per thread)
+    {
+        constexpr int PER = SORT_MAX_BUCKETS / SORT_T;
+        int c[PER], sum = 0;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int d = threadIdx.x * PER + q;
+            c[q] = d < nb ? sm.cursor[d] : 0;
+            sum += c[q];
+        }
+        int tot;
+        int ex = block_exclusive_scan<int>(sum, sm.scan_w, tot);
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int d = threadIdx.x * PER + q;
+            if (d < nb) { sm.bstart[d] = ex; sm.cursor[d] = ex; }
+            ex += c[q];
+        }
+        if (threadIdx.x == 0) sm.bstart[nb] = n;
+    }
+    __syncthreads();
+    // scatter into buckets
+    for (int c0 = 0; c0 < n; c0 += SORT_CHUNK) {
+#pragma unroll
+        for (int k = 0; k < SORT_IPT; ++k) {
+            const int i = c0 + k * SORT_T + threadIdx.x;
+            if (i < n) {
+                const uint64_t v = regs ? it[k] : src[i];
+                const int pos = atomicAdd(&sm.cursor[(((uint32_t)(v >> 32)) - kmin) >> shift], 1);
+                stage[pos] = v;
+            }
+        }
+    }
+    __syncthreads();
+
+    // per-bucket sort, warp per bucket
+    for (int b = wid; b < nb; b += SORT_W) {
+        const int b0 = sm.bstart[b], b1 = sm.bstart[b + 1], cnt = b1 - b0;
+        if (cnt == 0) continue;
+        if (cnt == 1) {
+            if (lane == 0) out[b0] = (int32_t)(uint32_t)stage[b0];
+            continue;
+        }
+        if (cnt <= 32) {
+            uint64_t x = lane < cnt ? stage[b0 + lane] : ~0ull;
+            x = warp_bitonic32(x);
+            const uint32_t h = (uint32_t)(x >> 32), p = (uint32_t)x;
+            const uint32_t hn = __shfl_down_sync(0xffffffffu, h, 1);
+            const uint32_t hp = __shfl_up_sync(0xffffffffu, h, 1);
+            const bool tied = lane < cnt && ((lane + 1 < cnt && hn == h) || (lane > 0 && hp == h));
+            if (!__any_sync(0xffffffffu, tied)) {
+                if (lane < cnt) out[b0 + lane] = (int32_t)p;
+                continue;
+            }
+            // equal f32 keys: order each tied group by (fp64 key, prim)
+            const double k = tied ? key64_of(x, tile, pv, cam, st) : 0.0;
+            int r = 0;
+            for (int j = 0; j < cnt; ++j) {
+                const uint32_t hj = __shfl_sync(0xffffffffu, h, j);
+                const uint32_t pj = __shfl_sync(0xffffffffu, p, j);
+                const double kj = __shfl_sync(0xffffffffu, k, j);
+                r += (hj < h || (hj == h && j != lane && (kj < k || (kj == k && pj < p)))) ? 1 : 0;
+            }
+            if (lane < cnt) out[b0 + r] = (int32_t)p;
+            continue;
+        }
+        if (cnt > SORT_RANK_MAX) {
+            if (lane == 0) atomicAdd(&sm.nbig, 1);
+            continue;
+        }
+        for (int i = b0 + lane; i < b1; i += 32) {
+            const uint64_t x = stage[i];
+            out[b0 + rank_in_bucket(stage, b0, b1, x, tile, pv, cam, st)] = (int32_t)(uint32_t)x;
+        }
+    }
+    __syncthreads();
+    if (sm.nbig == 0) return;
+    // degenerate inputs (a bucket over SORT_RANK_MAX): whole-CTA rank count
+    for (int b = 0; b < nb; ++b) {
+        const int b0 = sm.bstart[b], b1 = sm.bstart[b + 1];
+        if (b1 - b0 <= SORT_RANK_MAX) continue;
+        for (int i = b0 + threadIdx.x; i < b1; i += SORT_T) {
+            const uint64_t x = stage[i];
+            out[b0 + rank_in_bucket(stage, b0, b1, x, tile, pv, cam, st)] = (int32_t)(uint32_t)x;
+        }
     }
 }
 

@@ -170,3 +170,23 @@ def test_backward_replay_fallback(rz, name, mode):
     scale = np.abs(a).max(axis=0, keepdims=True) + 1e-30
     assert np.all(np.abs(a - b) <= 1e-5 * scale + 1e-6 * np.abs(a)), \
         float((np.abs(a - b) / scale).max())
+
+
+@pytest.mark.parametrize("copies", [5, 40, 300, 700])
+def test_sort_ties_duplicates(rz, copies):
+    """Duplicated primitives give identical (f32 and fp64) keys: the sort must
+    still equal lexsort((prim, key, tile)), i.e. break ties by primitive id,
+    through every bucket path (warp bitonic, warp rank count, CTA rank count)."""
+    from oracle import qgs_oracle as qo
+    from paper_2411_16392_b200 import scenes
+    from paper_2411_16392_b200.model import PrimitiveSet
+    sc = scenes.small_scene(seed=11, n=16, res=48, sh_deg=1)
+    p = sc.prims
+    idx = np.concatenate([np.arange(len(p)), np.full(copies, 3), np.full(copies // 2, 7)])
+    rng = np.random.default_rng(copies)
+    idx = idx[rng.permutation(len(idx))]
+    dup = PrimitiveSet(*(np.ascontiguousarray(getattr(p, f)[idx]) for f in PrimitiveSet.FIELDS))
+    prep = rz.prepare(dup, sc.cams[0])
+    vw = qo.prepare(dup.astype(np.float64), sc.cams[0])
+    assert np.array_equal(prep.tile_offsets.cpu().numpy().astype(np.int64), vw.tile_offsets)
+    assert np.array_equal(prep.tile_prims.cpu().numpy().astype(np.int64), vw.tile_prims)
