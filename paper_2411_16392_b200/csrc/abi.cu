@@ -44,6 +44,7 @@ struct BinWs {
     int *diff;
     int32_t *cursor;
     uint64_t *bucket, *tmp;
+    double *rays;         // W*H*3 unit pixel rays (fp64) for the key kernel
     size_t bytes;
 };
 
@@ -57,6 +58,7 @@ BinWs bin_ws(void *base, int32_t tiles_x, int32_t tiles_y, int64_t n_pairs)
     w.cursor = reinterpret_cast<int32_t *>(b + o);  o += qgs::align256((size_t)tiles_x * tiles_y * 4);
     w.bucket = reinterpret_cast<uint64_t *>(b + o); o += qgs::align256((size_t)n_pairs * 8);
     w.tmp = reinterpret_cast<uint64_t *>(b + o);    o += qgs::align256((size_t)n_pairs * 8);
+    w.rays = reinterpret_cast<double *>(b + o);     o += qgs::align256((size_t)tiles_x * tiles_y * 256 * 24);
     w.bytes = o;
     return w;
 }
@@ -128,7 +130,7 @@ size_t qgs_bin_workspace_bytes(int32_t P, int64_t n_pairs, int32_t n_tiles)
     // diff grid is at most (n_tiles + tiles_x + tiles_y + 1) entries; bound it by 2*n_tiles + 2*32768
     size_t ndiff = 2 * (size_t)n_tiles + 65538;
     return qgs::align256(ndiff * sizeof(int)) + qgs::align256((size_t)n_tiles * 4) +
-           2 * qgs::align256((size_t)n_pairs * 8) + 256;
+           2 * qgs::align256((size_t)n_pairs * 8) + qgs::align256((size_t)n_tiles * 256 * 24) + 256;
 }
 
 int qgs_bin(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settings *st,
@@ -156,7 +158,9 @@ int qgs_bin(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settin
     QGS_LAUNCHED("tile_offsets_kernel");
     if (n_pairs == 0) return 0;
     const int grid = (int)std::min<long long>(cdiv(n_pairs, 256), 148LL * 32);
-    qgs::pair_key_kernel<<<grid, 256, 0, s>>>(pv, P, n_pairs, ck, sk, ws.cursor, ws.bucket);
+    qgs::pixel_rays_kernel<<<cdiv((long long)ck.W * ck.H, 256), 256, 0, s>>>(ck, ws.rays);
+    QGS_LAUNCHED("pixel_rays_kernel");
+    qgs::pair_key_kernel<<<grid, 256, 0, s>>>(pv, P, n_pairs, ck, sk, ws.rays, ws.cursor, ws.bucket);
     QGS_LAUNCHED("pair_key_kernel");
     qgs::tile_sort_kernel<<<n_tiles, qgs::SORT_THREADS, qgs::sort_smem_bytes(), s>>>(
         tile_offsets, ws.bucket, ws.tmp, pv, ck, sk, tile_prims);

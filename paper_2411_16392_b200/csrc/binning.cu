@@ -153,9 +153,22 @@ __device__ inline uint32_t key_hi(double key)
     return __float_as_uint(__double2float_rd(key));
 }
 
+// unit ray of every pixel centre, fp64 (the key kernel's pixel rays)
+__global__ void pixel_rays_kernel(CamK cam, double *rays)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cam.W * cam.H) return;
+    const int v = i / cam.W, u = i - v * cam.W;
+    double cx, cy, cz;
+    pixel_ray64(cam, u, v, cx, cy, cz);
+    rays[3 * (size_t)i] = cx;
+    rays[3 * (size_t)i + 1] = cy;
+    rays[3 * (size_t)i + 2] = cz;
+}
+
 // One warp per primitive; lanes stride over the primitive's tiles.
 __global__ void pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
-                                int32_t *cursor, uint64_t *bucket)
+                                const double *__restrict__ rays, int32_t *cursor, uint64_t *bucket)
 {
     (void)n_pairs;
     const int lane = threadIdx.x & 31;
@@ -170,7 +183,7 @@ __global__ void pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, S
         for (int local = lane; local < nt; local += 32) {
             const int row = local / ncols;
             const int tile = (ty0 + row) * cam.tiles_x + tx0 + (local - row * ncols);
-            const double key = tile_key_geo(g, tile, cam, st.euclid != 0, st.t_clip);
+            const double key = tile_key_geo(g, tile, cam, st.euclid != 0, st.t_clip, rays);
             const int slot = atomicAdd(&cursor[tile], 1);
             bucket[slot] = ((uint64_t)key_hi(key) << 32) | (uint32_t)p;
         }
@@ -204,7 +217,7 @@ struct SortSmem {
     int cursor[SORT_MAX_BUCKETS];
     int scan_w[32];
     uint32_t kmin, kmax;
-    int nbig;
+    int nbig;             // buckets over SORT_RANK_MAX in the current group
 };
 
 __device__ __noinline__ double key64_of(uint64_t v, int tile, const PrepView &pv,
@@ -254,6 +267,69 @@ __device__ __forceinline__ uint64_t warp_bitonic32(uint64_t x)
         }
     }
     return x;
+}
+
+// Sort buckets [g0, g1): bucket b's items sit at a[bstart[b] - base ...];
+// warp per bucket.  Ends with __syncthreads.
+__device__ void sort_buckets(SortSmem &sm, const uint64_t *a, int base, int g0, int g1, int tile,
+                             const PrepView &pv, const CamK &cam, const SetK &st, int32_t *out)
+{
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int b = g0 + wid; b < g1; b += SORT_W) {
+        const int b0 = sm.bstart[b], b1 = sm.bstart[b + 1], cnt = b1 - b0;
+        const uint64_t *ab = a + (b0 - base);
+        if (cnt == 0) continue;
+        if (cnt == 1) {
+            if (lane == 0) out[b0] = (int32_t)(uint32_t)ab[0];
+            continue;
+        }
+        if (cnt <= 32) {
+            uint64_t x = lane < cnt ? ab[lane] : ~0ull;
+            x = warp_bitonic32(x);
+            const uint32_t h = (uint32_t)(x >> 32), p = (uint32_t)x;
+            const uint32_t hn = __shfl_down_sync(0xffffffffu, h, 1);
+            const uint32_t hp = __shfl_up_sync(0xffffffffu, h, 1);
+            const bool tied = lane < cnt && ((lane + 1 < cnt && hn == h) || (lane > 0 && hp == h));
+            if (!__any_sync(0xffffffffu, tied)) {
+                if (lane < cnt) out[b0 + lane] = (int32_t)p;
+                continue;
+            }
+            // equal f32 keys: order each tied group by (fp64 key, prim)
+            const double k = tied ? key64_of(x, tile, pv, cam, st) : 0.0;
+            int r = 0;
+            for (int j = 0; j < cnt; ++j) {
+                const uint32_t hj = __shfl_sync(0xffffffffu, h, j);
+                const uint32_t pj = __shfl_sync(0xffffffffu, p, j);
+                const double kj = __shfl_sync(0xffffffffu, k, j);
+                r += (hj < h || (hj == h && j != lane && (kj < k || (kj == k && pj < p)))) ? 1 : 0;
+            }
+            if (lane < cnt) out[b0 + r] = (int32_t)p;
+            continue;
+        }
+        if (cnt > SORT_RANK_MAX) {                  // done by the whole CTA below
+            if (lane == 0) atomicAdd(&sm.nbig, 1);
+            continue;
+        }
+        for (int i = lane; i < cnt; i += 32) {
+            const uint64_t x = ab[i];
+            out[b0 + rank_in_bucket(ab, 0, cnt, x, tile, pv, cam, st)] = (int32_t)(uint32_t)x;
+        }
+    }
+    __syncthreads();
+    if (sm.nbig == 0) return;
+    // degenerate inputs (a bucket over SORT_RANK_MAX): whole-CTA rank count
+    for (int b = g0; b < g1; ++b) {
+        const int b0 = sm.bstart[b], cnt = sm.bstart[b + 1] - b0;
+        if (cnt <= SORT_RANK_MAX) continue;
+        const uint64_t *ab = a + (b0 - base);
+        for (int i = threadIdx.x; i < cnt; i += SORT_T) {
+            const uint64_t x = ab[i];
+            out[b0 + rank_in_bucket(ab, 0, cnt, x, tile, pv, cam, st)] = (int32_t)(uint32_t)x;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) sm.nbig = 0;
+    __syncthreads();
 }
 
 __global__ void __launch_bounds__(SORT_T, 2)
@@ -351,55 +427,39 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
     }
     __syncthreads();
 
-    // per-bucket sort, warp per bucket
-    for (int b = wid; b < nb; b += SORT_W) {
-        const int b0 = sm.bstart[b], b1 = sm.bstart[b + 1], cnt = b1 - b0;
-        if (cnt == 0) continue;
-        if (cnt == 1) {
-            if (lane == 0) out[b0] = (int32_t)(uint32_t)stage[b0];
-            continue;
-        }
-        if (cnt <= 32) {
-            uint64_t x = lane < cnt ? stage[b0 + lane] : ~0ull;
-            x = warp_bitonic32(x);
-            const uint32_t h = (uint32_t)(x >> 32), p = (uint32_t)x;
-            const uint32_t hn = __shfl_down_sync(0xffffffffu, h, 1);
-            const uint32_t hp = __shfl_up_sync(0xffffffffu, h, 1);
-            const bool tied = lane < cnt && ((lane + 1 < cnt && hn == h) || (lane > 0 && hp == h));
-            if (!__any_sync(0xffffffffu, tied)) {
-                if (lane < cnt) out[b0 + lane] = (int32_t)p;
+    if (n <= SORT_SMEM_ITEMS) {
+        sort_buckets(sm, stage, 0, 0, nb, tile, pv, cam, st, out);
+    } else {
+        // groups of consecutive buckets that fit in shared memory: one
+        // coalesced bulk load from the L2 staging slice, then warps sort
+        // their buckets out of shared memory
+        int g0 = 0;
+        while (g0 < nb) {
+            const int base = sm.bstart[g0];
+            // last bucket end within SORT_SMEM_ITEMS of base (binary search)
+            int lo = g0 + 1, hi = nb;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (sm.bstart[mid] - base <= SORT_SMEM_ITEMS) lo = mid; else hi = mid - 1;
+            }
+            int g1 = lo;
+            if (sm.bstart[g1] - base > SORT_SMEM_ITEMS) {
+                // one degenerate bucket larger than shared memory: rank it in place
+                const int b1 = sm.bstart[g1];
+                for (int i = base + threadIdx.x; i < b1; i += SORT_T) {
+                    const uint64_t x = stage[i];
+                    out[base + rank_in_bucket(stage, base, b1, x, tile, pv, cam, st)] =
+                        (int32_t)(uint32_t)x;
+                }
+                __syncthreads();
+                g0 = g1;
                 continue;
             }
-            // equal f32 keys: order each tied group by (fp64 key, prim)
-            const double k = tied ? key64_of(x, tile, pv, cam, st) : 0.0;
-            int r = 0;
-            for (int j = 0; j < cnt; ++j) {
-                const uint32_t hj = __shfl_sync(0xffffffffu, h, j);
-                const uint32_t pj = __shfl_sync(0xffffffffu, p, j);
-                const double kj = __shfl_sync(0xffffffffu, k, j);
-                r += (hj < h || (hj == h && j != lane && (kj < k || (kj == k && pj < p)))) ? 1 : 0;
-            }
-            if (lane < cnt) out[b0 + r] = (int32_t)p;
-            continue;
-        }
-        if (cnt > SORT_RANK_MAX) {
-            if (lane == 0) atomicAdd(&sm.nbig, 1);
-            continue;
-        }
-        for (int i = b0 + lane; i < b1; i += 32) {
-            const uint64_t x = stage[i];
-            out[b0 + rank_in_bucket(stage, b0, b1, x, tile, pv, cam, st)] = (int32_t)(uint32_t)x;
-        }
-    }
-    __syncthreads();
-    if (sm.nbig == 0) return;
-    // degenerate inputs (a bucket over SORT_RANK_MAX): whole-CTA rank count
-    for (int b = 0; b < nb; ++b) {
-        const int b0 = sm.bstart[b], b1 = sm.bstart[b + 1];
-        if (b1 - b0 <= SORT_RANK_MAX) continue;
-        for (int i = b0 + threadIdx.x; i < b1; i += SORT_T) {
-            const uint64_t x = stage[i];
-            out[b0 + rank_in_bucket(stage, b0, b1, x, tile, pv, cam, st)] = (int32_t)(uint32_t)x;
+            const int cnt = sm.bstart[g1] - base;
+            for (int i = threadIdx.x; i < cnt; i += SORT_T) sm.buf[i] = stage[base + i];
+            __syncthreads();
+            sort_buckets(sm, sm.buf, base, g0, g1, tile, pv, cam, st, out);
+            g0 = g1;
         }
     }
 }

@@ -19,8 +19,9 @@ __global__ void scan_out_kernel(const int32_t *in, int n, const int64_t *sums, i
 __global__ void tile_diff_kernel(const int4 *bbox, int P, int tiles_x, int *diff);
 __global__ void tile_offsets_kernel(int *diff, int tiles_x, int tiles_y, int32_t *tile_offsets,
                                     int32_t *cursor);
+__global__ void pixel_rays_kernel(CamK cam, double *rays);
 __global__ void pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
-                                int32_t *cursor, uint64_t *bucket);
+                                const double *rays, int32_t *cursor, uint64_t *bucket);
 __global__ void tile_sort_kernel(const int32_t *tile_offsets, uint64_t *keys, uint64_t *tmp,
                                  PrepView pv, CamK cam, SetK st, int32_t *tile_prims);
 __global__ void sorted_keys_kernel(PrepView pv, const int32_t *tile_offsets,

@@ -144,6 +144,48 @@ __device__ inline double sigma_dir64(double s1, double s2, double c, double s)
     return fabs(s1 * s2) / sqrt(m);
 }
 
+// arc length of z = a r^2 over [0, rho] in fp32 (series below |u| = 0.3,
+// asinh form above; relative error ~1e-7)
+__device__ inline float arc_length32(float a, float rho)
+{
+    float u = 2.f * a * rho;
+    if (fabsf(u) < 0.3f) {
+        float u2 = u * u;
+        return rho * (1.f + u2 * (1.f / 6.f + u2 * (-1.f / 40.f + u2 * (1.f / 112.f - u2 * (5.f / 1152.f)))));
+    }
+    float r = sqrtf(u * u + 1.f);
+    return (asinhf(u) + u * r) / (4.f * a);
+}
+
+// The 3-sigma test l <= 3 sigma(theta) at local (x, y) (intersect.py:104-112,
+// geodesic.py:23-31,51-59).  Decided in fp32 when the margin exceeds 1e-4
+// relative (the fp32 evaluation is good to ~1e-6), else by the reference's
+// own float64 expressions -- so the decision is always the float64 one.
+__device__ inline bool within_3sigma64(double x, double y, double s1, double s2, double s3,
+                                       double w1, double w2, bool euclid)
+{
+    {
+        const float xf = (float)x, yf = (float)y;
+        const float r2 = xf * xf + yf * yf;
+        if (r2 > 1e-18f) {
+            const float rho = sqrtf(r2), c = xf / rho, sn = yf / rho;
+            const float a = (float)s3 * ((float)w1 * c * c + (float)w2 * sn * sn);
+            const float l = euclid ? rho : arc_length32(a, rho);
+            const float f1 = (float)s1, f2 = (float)s2;
+            const float sig = fabsf(f1 * f2) / sqrtf((f2 * c) * (f2 * c) + (f1 * sn) * (f1 * sn));
+            const float q = l / (3.f * sig);
+            if (q < 1.f - 1e-4f) return true;
+            if (q > 1.f + 1e-4f) return false;
+        }
+    }
+    double rho = sqrt(x * x + y * y), c = 1.0, s = 0.0;
+    if (rho > 1e-12) { c = x / rho; s = y / rho; }
+    double a = s3 * (w1 * c * c + w2 * s * s);
+    double l = euclid ? rho : arc_length64(a, rho);
+    double sig = sigma_dir64(s1, s2, c, s);
+    return l <= 3.0 * sig;
+}
+
 // fragment_geometry restricted to what the sort key needs: (valid, t).
 __device__ inline bool hit_depth64(const double *wv, const double *sv, const double *oh,
                                    double dx, double dy, double dz, bool planar, bool euclid,
@@ -154,10 +196,7 @@ __device__ inline bool hit_depth64(const double *wv, const double *sv, const dou
         double t = -oh[2] / dz;
         if (t <= t_clip) return false;
         double x = oh[0] + t * dx, y = oh[1] + t * dy;
-        double rho = sqrt(x * x + y * y), c = 1.0, s = 0.0;
-        if (rho > 1e-12) { c = x / rho; s = y / rho; }
-        double sig = sigma_dir64(sv[0], sv[1], c, s);
-        if (rho > 3.0 * sig) return false;
+        if (!within_3sigma64(x, y, sv[0], sv[1], 0.0, 0.0, 0.0, true)) return false;
         t_out = t;
         return true;
     }
@@ -188,21 +227,26 @@ __device__ inline bool hit_depth64(const double *wv, const double *sv, const dou
         double x = ox + t * dx, y = oy + t * dy;
         double m = (s2 * x) * (s2 * x) + (s1 * y) * (s1 * y);
         if (m > 9.0 * s1s2 * s1s2) continue;
-        double rho = sqrt(x * x + y * y), c = 1.0, s = 0.0;
-        if (rho > 1e-12) { c = x / rho; s = y / rho; }
-        double a = s3 * (w1 * c * c + w2 * s * s);
-        double l = euclid ? rho : arc_length64(a, rho);
-        double sig = sigma_dir64(s1, s2, c, s);
-        if (l <= 3.0 * sig) { t_out = t; return true; }
+        if (within_3sigma64(x, y, s1, s2, s3, w1, w2, euclid)) { t_out = t; return true; }
     }
     return false;
 }
 
 // tile_sort_depths (raster_kernels.py:684-716) for one (tile, primitive).
+// unit camera ray of pixel centre (u, v), cameras.py:53-59 operation order
+__device__ inline void pixel_ray64(const CamK &cam, int u, int v, double &cx, double &cy,
+                                   double &cz)
+{
+    double ddx = ((double)u + 0.5 - cam.cx) / cam.fx, ddy = ((double)v + 0.5 - cam.cy) / cam.fy;
+    double nrm = sqrt(ddx * ddx + ddy * ddy + 1.0);
+    cx = ddx / nrm; cy = ddy / nrm; cz = 1.0 / nrm;
+}
+
+// `dirtab` (optional): the W*H*3 table of pixel_ray64, bit-identical.
 __device__ inline double tile_key64(const double *ohat, const double *M, const double *wv,
                                     const double *sv, bool planar, double vu, double vv,
                                     double dist, int tile, const CamK &cam, bool euclid,
-                                    double t_clip)
+                                    double t_clip, const double *dirtab = nullptr)
 {
     int ty = tile / cam.tiles_x, tx = tile - ty * cam.tiles_x;
     long long ulo = tx * TILE, uhi = min(cam.W, tx * TILE + TILE) - 1;
@@ -210,10 +254,13 @@ __device__ inline double tile_key64(const double *ohat, const double *M, const d
     long long iu = (long long)floor(vu), iv = (long long)floor(vv);
     iu = iu < ulo ? ulo : (iu > uhi ? uhi : iu);
     iv = iv < vlo ? vlo : (iv > vhi ? vhi : iv);
-    double u = (double)iu, v = (double)iv;
-    double ddx = (u + 0.5 - cam.cx) / cam.fx, ddy = (v + 0.5 - cam.cy) / cam.fy;
-    double nrm = sqrt(ddx * ddx + ddy * ddy + 1.0);
-    double cx = ddx / nrm, cy = ddy / nrm, cz = 1.0 / nrm;
+    double cx, cy, cz;
+    if (dirtab) {
+        const double *d = dirtab + 3 * ((size_t)iv * cam.W + iu);
+        cx = d[0]; cy = d[1]; cz = d[2];
+    } else {
+        pixel_ray64(cam, (int)iu, (int)iv, cx, cy, cz);
+    }
     double dx = M[0] * cx + M[1] * cy + M[2] * cz;
     double dy = M[3] * cx + M[4] * cy + M[5] * cz;
     double dz = M[6] * cx + M[7] * cy + M[8] * cz;
@@ -223,10 +270,10 @@ __device__ inline double tile_key64(const double *ohat, const double *M, const d
 }
 
 __device__ inline double tile_key_geo(const Geo64 &g, int tile, const CamK &cam, bool euclid,
-                                      double t_clip)
+                                      double t_clip, const double *dirtab = nullptr)
 {
     return tile_key64(g.ohat, g.M, g.wv, g.sv, g.planar != 0.0, g.vert_u, g.vert_v, g.dist,
-                      tile, cam, euclid, t_clip);
+                      tile, cam, euclid, t_clip, dirtab);
 }
 
 
