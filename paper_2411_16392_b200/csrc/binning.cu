@@ -209,7 +209,6 @@ constexpr int SORT_IPT = 4;
 constexpr int SORT_CHUNK = SORT_T * SORT_IPT;     // items per register pass
 constexpr int SORT_SMEM_ITEMS = 8192;             // staged in shared memory up to this
 constexpr int SORT_MAX_BUCKETS = 4096;
-constexpr int SORT_RANK_MAX = 256;
 
 struct SortSmem {
     uint64_t buf[SORT_SMEM_ITEMS];
@@ -217,7 +216,6 @@ struct SortSmem {
     int cursor[SORT_MAX_BUCKETS];
     int scan_w[32];
     uint32_t kmin, kmax;
-    int nbig;             // buckets over SORT_RANK_MAX in the current group
 };
 
 __device__ __noinline__ double key64_of(uint64_t v, int tile, const PrepView &pv,
@@ -252,7 +250,6 @@ __device__ __forceinline__ int rank_in_bucket(const uint64_t *a, int b0, int b1,
     return r;
 }
 
-// warp bitonic sort of 32 u64 values, one per lane (ascending by lane)
 __device__ __forceinline__ uint64_t warp_bitonic32(uint64_t x)
 {
     const int lane = threadIdx.x & 31;
@@ -269,66 +266,22 @@ __device__ __forceinline__ uint64_t warp_bitonic32(uint64_t x)
     return x;
 }
 
-// Sort buckets [g0, g1): bucket b's items sit at a[bstart[b] - base ...];
-// warp per bucket.  Ends with __syncthreads.
-__device__ void sort_buckets(SortSmem &sm, const uint64_t *a, int base, int g0, int g1, int tile,
-                             const PrepView &pv, const CamK &cam, const SetK &st, int32_t *out)
+// Emit the sorted order of buckets [g0, g1) whose items sit in a[0 .. ),
+// bucket b at a[bstart[b] - base ...]: every item finds its own rank inside
+// its bucket (buckets average a few items), item-parallel over the CTA.
+// Ends with __syncthreads.
+__device__ void sort_buckets(SortSmem &sm, const uint64_t *a, int base, int g0, int g1,
+                             uint32_t kmin, int shift, int tile, const PrepView &pv,
+                             const CamK &cam, const SetK &st, int32_t *out)
 {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int b = g0 + wid; b < g1; b += SORT_W) {
-        const int b0 = sm.bstart[b], b1 = sm.bstart[b + 1], cnt = b1 - b0;
-        const uint64_t *ab = a + (b0 - base);
-        if (cnt == 0) continue;
-        if (cnt == 1) {
-            if (lane == 0) out[b0] = (int32_t)(uint32_t)ab[0];
-            continue;
-        }
-        if (cnt <= 32) {
-            uint64_t x = lane < cnt ? ab[lane] : ~0ull;
-            x = warp_bitonic32(x);
-            const uint32_t h = (uint32_t)(x >> 32), p = (uint32_t)x;
-            const uint32_t hn = __shfl_down_sync(0xffffffffu, h, 1);
-            const uint32_t hp = __shfl_up_sync(0xffffffffu, h, 1);
-            const bool tied = lane < cnt && ((lane + 1 < cnt && hn == h) || (lane > 0 && hp == h));
-            if (!__any_sync(0xffffffffu, tied)) {
-                if (lane < cnt) out[b0 + lane] = (int32_t)p;
-                continue;
-            }
-            // equal f32 keys: order each tied group by (fp64 key, prim)
-            const double k = tied ? key64_of(x, tile, pv, cam, st) : 0.0;
-            int r = 0;
-            for (int j = 0; j < cnt; ++j) {
-                const uint32_t hj = __shfl_sync(0xffffffffu, h, j);
-                const uint32_t pj = __shfl_sync(0xffffffffu, p, j);
-                const double kj = __shfl_sync(0xffffffffu, k, j);
-                r += (hj < h || (hj == h && j != lane && (kj < k || (kj == k && pj < p)))) ? 1 : 0;
-            }
-            if (lane < cnt) out[b0 + r] = (int32_t)p;
-            continue;
-        }
-        if (cnt > SORT_RANK_MAX) {                  // done by the whole CTA below
-            if (lane == 0) atomicAdd(&sm.nbig, 1);
-            continue;
-        }
-        for (int i = lane; i < cnt; i += 32) {
-            const uint64_t x = ab[i];
-            out[b0 + rank_in_bucket(ab, 0, cnt, x, tile, pv, cam, st)] = (int32_t)(uint32_t)x;
-        }
+    const int i0 = sm.bstart[g0] - base, i1 = sm.bstart[g1] - base;
+    for (int i = i0 + threadIdx.x; i < i1; i += SORT_T) {
+        const uint64_t x = a[i];
+        const int d = (int)((((uint32_t)(x >> 32)) - kmin) >> shift);
+        const int b0 = sm.bstart[d], b1 = sm.bstart[d + 1];
+        const int r = b1 - b0 == 1 ? 0 : rank_in_bucket(a, b0 - base, b1 - base, x, tile, pv, cam, st);
+        out[b0 + r] = (int32_t)(uint32_t)x;
     }
-    __syncthreads();
-    if (sm.nbig == 0) return;
-    // degenerate inputs (a bucket over SORT_RANK_MAX): whole-CTA rank count
-    for (int b = g0; b < g1; ++b) {
-        const int b0 = sm.bstart[b], cnt = sm.bstart[b + 1] - b0;
-        if (cnt <= SORT_RANK_MAX) continue;
-        const uint64_t *ab = a + (b0 - base);
-        for (int i = threadIdx.x; i < cnt; i += SORT_T) {
-            const uint64_t x = ab[i];
-            out[b0 + rank_in_bucket(ab, 0, cnt, x, tile, pv, cam, st)] = (int32_t)(uint32_t)x;
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) sm.nbig = 0;
     __syncthreads();
 }
 
@@ -352,7 +305,7 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
     const bool regs = n <= SORT_CHUNK;     // one register pass holds the whole tile
 
     // key range
-    if (threadIdx.x == 0) { sm.kmin = 0xffffffffu; sm.kmax = 0u; sm.nbig = 0; }
+    if (threadIdx.x == 0) { sm.kmin = 0xffffffffu; sm.kmax = 0u; }
     uint64_t it[SORT_IPT];
     uint32_t lmin = 0xffffffffu, lmax = 0u;
     for (int c0 = 0; c0 < n; c0 += SORT_CHUNK) {
@@ -428,7 +381,7 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
     __syncthreads();
 
     if (n <= SORT_SMEM_ITEMS) {
-        sort_buckets(sm, stage, 0, 0, nb, tile, pv, cam, st, out);
+        sort_buckets(sm, stage, 0, 0, nb, kmin, shift, tile, pv, cam, st, out);
     } else {
         // groups of consecutive buckets that fit in shared memory: one
         // coalesced bulk load from the L2 staging slice, then warps sort
@@ -458,7 +411,7 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
             const int cnt = sm.bstart[g1] - base;
             for (int i = threadIdx.x; i < cnt; i += SORT_T) sm.buf[i] = stage[base + i];
             __syncthreads();
-            sort_buckets(sm, sm.buf, base, g0, g1, tile, pv, cam, st, out);
+            sort_buckets(sm, sm.buf, base, g0, g1, kmin, shift, tile, pv, cam, st, out);
             g0 = g1;
         }
     }
