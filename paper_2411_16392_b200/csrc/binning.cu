@@ -198,11 +198,12 @@ __global__ void pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, S
 //      unstable scatter (shared-memory cursors) into a staging array --
 //      shared memory when the tile fits, else its slice of `tmp` (L2-resident
 //      at these sizes).  Nothing downstream depends on the scatter order.
-//   2. each bucket is sorted by the full composite (f32 key bits, prim id):
-//      <= 32 items by a warp bitonic network in registers, <= SORT_RANK_MAX by
-//      a warp's rank count, larger (degenerate) ones by the whole CTA's rank
-//      count.  Runs of equal f32 keys are then ordered by (fp64 key, prim)
-//      (fix_run), which gives exactly lexsort((prim, key, tile)).
+//   2. every item ranks itself inside its bucket by the composite (f32 key
+//      bits, prim id) -- buckets hold a few items -- and items with equal f32
+//      keys by (fp64 key, prim) (rank_in_bucket), which gives exactly
+//      lexsort((prim, key, tile)).  Tiles larger than shared memory are
+//      staged in L2 and ranked in groups of whole buckets loaded into
+//      shared memory.
 constexpr int SORT_T = 512;
 constexpr int SORT_W = SORT_T / 32;
 constexpr int SORT_IPT = 4;
@@ -227,45 +228,6 @@ __device__ __noinline__ double key64_of(uint64_t v, int tile, const PrepView &pv
 // Final position of composite x inside its bucket [b0, b1) of `a`: items
 // with a smaller f32 key, plus items with the same f32 key that precede it in
 // (fp64 key, prim) order.  Composites are distinct (prim ids are), and equal
-// f32 keys are rare, so the fp64 keys are recomputed only for those.
-__device__ __forceinline__ int rank_in_bucket(const uint64_t *a, int b0, int b1, uint64_t x,
-                                              int tile, const PrepView &pv, const CamK &cam,
-                                              const SetK &st)
-{
-    const uint32_t h = (uint32_t)(x >> 32), p = (uint32_t)x;
-    int r = 0;
-    bool have = false;
-    double kx = 0.0;
-    for (int j = b0; j < b1; ++j) {
-        const uint64_t y = a[j];
-        const uint32_t hy = (uint32_t)(y >> 32);
-        if (hy < h) {
-            ++r;
-        } else if (hy == h && y != x) {
-            if (!have) { kx = key64_of(x, tile, pv, cam, st); have = true; }
-            const double ky = key64_of(y, tile, pv, cam, st);
-            r += (ky < kx || (ky == kx && (uint32_t)y < p)) ? 1 : 0;
-        }
-    }
-    return r;
-}
-
-__device__ __forceinline__ uint64_t warp_bitonic32(uint64_t x)
-{
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            const uint64_t y = __shfl_xor_sync(0xffffffffu, x, j);
-            const bool up = (lane & k) == 0;
-            const bool low = (lane & j) == 0;
-            x = (low == up) ? (x < y ? x : y) : (x < y ? y : x);
-        }
-    }
-    return x;
-}
-
 // Emit the sorted order of buckets [g0, g1) whose items sit in a[0 .. ),
 // bucket b at a[bstart[b] - base ...]: every item finds its own rank inside
 // its bucket (buckets average a few items), item-parallel over the CTA.
