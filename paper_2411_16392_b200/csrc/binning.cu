@@ -228,6 +228,29 @@ __device__ __noinline__ double key64_of(uint64_t v, int tile, const PrepView &pv
 // Final position of composite x inside its bucket [b0, b1) of `a`: items
 // with a smaller f32 key, plus items with the same f32 key that precede it in
 // (fp64 key, prim) order.  Composites are distinct (prim ids are), and equal
+// f32 keys are rare, so the fp64 keys are recomputed only for those.
+__device__ __forceinline__ int rank_in_bucket(const uint64_t *a, int b0, int b1, uint64_t x,
+                                              int tile, const PrepView &pv, const CamK &cam,
+                                              const SetK &st)
+{
+    const uint32_t h = (uint32_t)(x >> 32), p = (uint32_t)x;
+    int r = 0;
+    bool have = false;
+    double kx = 0.0;
+    for (int j = b0; j < b1; ++j) {
+        const uint64_t y = a[j];
+        const uint32_t hy = (uint32_t)(y >> 32);
+        if (hy < h) {
+            ++r;
+        } else if (hy == h && y != x) {
+            if (!have) { kx = key64_of(x, tile, pv, cam, st); have = true; }
+            const double ky = key64_of(y, tile, pv, cam, st);
+            r += (ky < kx || (ky == kx && (uint32_t)y < p)) ? 1 : 0;
+        }
+    }
+    return r;
+}
+
 // Emit the sorted order of buckets [g0, g1) whose items sit in a[0 .. ),
 // bucket b at a[bstart[b] - base ...]: every item finds its own rank inside
 // its bucket (buckets average a few items), item-parallel over the CTA.
