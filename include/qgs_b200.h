@@ -57,6 +57,8 @@ typedef struct qgs_settings {
     double background[3];
     double t_near_clip, alpha_floor, alpha_clamp, t_term;
     int32_t resort, euclidean_density;
+    int32_t no_cull;         /* extension: 1 disables the forward's conic cull (the
+                                results are identical either way; tests check it) */
 } qgs_settings;
 
 /* Raw primitive parameters, PrimitiveSet layout (model.py:126-141), fp32. */

@@ -113,7 +113,7 @@ int qgs_preprocess(const qgs_params *prims, const qgs_camera *cam, const qgs_set
         QGS_CK(cudaMemsetAsync(pv.pair_off, 0, sizeof(int64_t), s));
         return 0;
     }
-    qgs::preprocess_kernel<<<cdiv(P, 128), 128, 0, s>>>(*prims, ck, pv);
+    qgs::preprocess_kernel<<<cdiv(P, 128), 128, 0, s>>>(*prims, ck, pv, st->euclidean_density);
     QGS_LAUNCHED("preprocess_kernel");
     const int nb = (int)scan_blocks(P);
     int64_t *sums = scan_sums_ptr(prep, P);
@@ -218,8 +218,9 @@ int qgs_forward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_se
     if (out->violations)
         QGS_CK(cudaMemsetAsync(out->violations, 0, sizeof(int32_t) * ck.tiles_x * ck.tiles_y, s));
     qgs::raster_fwd_kernel<<<ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE,
-                             qgs::RASTER_THREADS, 0, s>>>(pv.rec, pv.geo, tile_offsets, tile_prims, ck,
-                                                            sk, *out);
+                             qgs::RASTER_THREADS, 0, s>>>(pv.rec, pv.geo,
+                                                            st->no_cull ? nullptr : pv.conic, tile_offsets,
+                                                            tile_prims, ck, sk, *out);
     QGS_LAUNCHED("raster_fwd_kernel");
     return 0;
 }

@@ -5,7 +5,7 @@
 namespace qgs {
 
 // preprocess.cu
-__global__ void preprocess_kernel(qgs_params prm, CamK cam, PrepView pv);
+__global__ void preprocess_kernel(qgs_params prm, CamK cam, PrepView pv, int euclid);
 __global__ void chain_kernel(qgs_params prm, CamK cam, const float *kg, qgs_grads out);
 __global__ void export_prep_kernel(PrepView pv, int P, double *scales, double *alphas,
                                    double *colors, int32_t *bbox, uint8_t *planar);
@@ -36,7 +36,8 @@ size_t sort_smem_bytes();
 constexpr int SORT_THREADS = 512;   // == binning.cu SORT_T
 
 // raster.cu
-__global__ void raster_fwd_kernel(const PrimRec *recs, const Geo64 *geo, const int32_t *tile_offsets,
+__global__ void raster_fwd_kernel(const PrimRec *recs, const Geo64 *geo, const ConicRec *conics,
+                                  const int32_t *tile_offsets,
                                   const int32_t *tile_prims, CamK cam, SetK st, qgs_targets out);
 __global__ void raster_bwd_kernel(const PrimRec *recs, const Geo64 *geo, const int32_t *tile_offsets,
                                   const int32_t *tile_prims, CamK cam, SetK st, qgs_targets fwd,

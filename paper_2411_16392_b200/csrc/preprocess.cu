@@ -192,7 +192,126 @@ __device__ inline void tight_box(const double s[3], const double R[9], const dou
     if (out[0] > out[1] || out[2] > out[3]) { out[0] = 0; out[1] = -1; out[2] = 0; out[3] = -1; }
 }
 
-__global__ void preprocess_kernel(qgs_params prm, CamK cam, PrepView pv)
+// Bounding ellipsoid of everything the selection rule can accept
+// (intersect.py:58-115), in the primitive's local frame: centre (0, 0, zc),
+// semi-axes ax, ay, az.  A hit at local (x, y, z) on the quadric passes the
+// 3-sigma test l <= 3 sigma(theta), and the arc length l is at least the
+// chord from the vertex, sqrt(rho^2 + z^2), while sigma(theta) <= max|s_i|:
+//   E1: (x/3s1)^2 + (y/3s2)^2 + (z/3 smax)^2 <= rho^2/(9 sigma^2) + z^2/(9 sigma^2) <= 1.
+// Independently rho <= l <= 3 sigma(theta) puts (x, y) in the ellipse
+// (x/3s1)^2 + (y/3s2)^2 <= 1, on which z = s3 (w1 x^2 + w2 y^2) lies in
+// [zlo, zhi]; for 0 < lam < 1 the cylinder-slab is inside
+//   E2: lam (x/3s1)^2 + lam (y/3s2)^2 + (1 - lam) ((z - zc)/h)^2 <= 1.
+// E2 is the only one in Euclidean-density mode (no chord bound) and for
+// planar primitives (h = 0: the disk itself); otherwise the smaller volume.
+__device__ inline void bounding_ellipsoid(const double s[3], bool planar, bool euclid,
+                                          double &zc, double ax[3])
+{
+    const double m1 = fabs(s[0]), m2 = fabs(s[1]), smax = fmax(m1, m2);
+    if (planar) { zc = 0.0; ax[0] = 3.0 * m1; ax[1] = 3.0 * m2; ax[2] = 0.0; return; }
+    // range of w1 x^2 + w2 y^2 = sgn(s1)(x/s1)^2 + sgn(s2)(y/s2)^2 on the ellipse: [lo, hi] * 9
+    const double g1 = s[0] < 0.0 ? -1.0 : 1.0, g2 = s[1] < 0.0 ? -1.0 : 1.0;
+    const double lo = fmin(0.0, fmin(g1, g2)), hi = fmax(0.0, fmax(g1, g2));
+    double z0 = 9.0 * s[2] * (s[2] >= 0.0 ? lo : hi), z1 = 9.0 * s[2] * (s[2] >= 0.0 ? hi : lo);
+    if (!euclid) { z0 = fmax(z0, -3.0 * smax); z1 = fmin(z1, 3.0 * smax); }
+    const double h = 0.5 * (z1 - z0);
+    const double lam = 0.75;
+    // volumes: E1 27 m1 m2 smax, E2 9 m1 m2 h / (lam sqrt(1 - lam))
+    if (!euclid && 27.0 * smax <= 9.0 * h / (lam * sqrt(1.0 - lam))) {
+        zc = 0.0; ax[0] = 3.0 * m1; ax[1] = 3.0 * m2; ax[2] = 3.0 * smax;
+        return;
+    }
+    zc = 0.5 * (z0 + z1);
+    const double il = 1.0 / sqrt(lam);
+    ax[0] = 3.0 * m1 * il; ax[1] = 3.0 * m2 * il; ax[2] = h / sqrt(1.0 - lam);
+}
+
+// 0.1% slack on every axis: the linear-branch root (|A| < 1e-6, t = -C/B)
+// sits A t^2 ~ 1e-5 off the quadric, and fp64 rounding
+__device__ inline void pad_axes(double ax[3]) { for (int k = 0; k < 3; ++k) ax[k] *= 1.001; }
+
+// Pixel-centre conic of the ellipsoid's outline (dual quadric projected:
+// C* = Mq Mq^T - m m^T with [Mq | m] = K [R_wc | t_wc] [R diag(ax) | c + zc R e3],
+// point conic = adj(C*)), translated to the box centre, normalised and
+// widened by the fp32 evaluation margin.  No cull (F = -1) when the
+// ellipsoid reaches the camera plane or contains the eye.
+__device__ inline ConicRec bounding_conic(const double s[3], bool planar, bool euclid,
+                                          const double R[9], const double c[3],
+                                          const CamK &cam, const long long box[4])
+{
+    ConicRec q;
+    q.A = q.B = q.C = q.D = q.E = 0.f;
+    q.F = -1.f;
+    q.uc = 0.5f * (float)(box[0] + box[1]);
+    q.vc = 0.5f * (float)(box[2] + box[3]);
+    if (box[0] > box[1]) return q;
+    double zc, ax[3];
+    bounding_ellipsoid(s, planar, euclid, zc, ax);
+    pad_axes(ax);
+    // centre and axes in camera coordinates
+    double cw[3], Mc[3][3], mc[3];
+    for (int i = 0; i < 3; ++i) cw[i] = c[i] + zc * R[3 * i + 2];
+    for (int i = 0; i < 3; ++i) {
+        mc[i] = cam.Rwc[3 * i] * cw[0] + cam.Rwc[3 * i + 1] * cw[1] + cam.Rwc[3 * i + 2] * cw[2] + cam.twc[i];
+        for (int k = 0; k < 3; ++k)
+            Mc[i][k] = (cam.Rwc[3 * i] * R[k] + cam.Rwc[3 * i + 1] * R[3 + k] +
+                        cam.Rwc[3 * i + 2] * R[6 + k]) * ax[k];
+    }
+    // in front of the camera plane with margin, eye outside
+    const double zr = sqrt(Mc[2][0] * Mc[2][0] + Mc[2][1] * Mc[2][1] + Mc[2][2] * Mc[2][2]);
+    if (!(mc[2] - zr > 1e-6 * fmax(mc[2], 1e-30))) return q;
+    // homogeneous pixel map: rows u = fx X + cx Z, v = fy Y + cy Z, w = Z
+    double Mq[3][3], m[3];
+    for (int k = 0; k < 3; ++k) {
+        Mq[0][k] = cam.fx * Mc[0][k] + cam.cx * Mc[2][k];
+        Mq[1][k] = cam.fy * Mc[1][k] + cam.cy * Mc[2][k];
+        Mq[2][k] = Mc[2][k];
+    }
+    m[0] = cam.fx * mc[0] + cam.cx * mc[2];
+    m[1] = cam.fy * mc[1] + cam.cy * mc[2];
+    m[2] = mc[2];
+    // translate so pixel (u, v) centre = (u0 + U, v0 + V), u0 = uc + 0.5
+    const double u0 = (double)q.uc + 0.5, v0 = (double)q.vc + 0.5;
+    for (int k = 0; k < 3; ++k) {
+        Mq[0][k] -= u0 * Mq[2][k];
+        Mq[1][k] -= v0 * Mq[2][k];
+    }
+    m[0] -= u0 * m[2];
+    m[1] -= v0 * m[2];
+    double D[3][3];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            D[i][j] = Mq[i][0] * Mq[j][0] + Mq[i][1] * Mq[j][1] + Mq[i][2] * Mq[j][2] - m[i] * m[j];
+    // point conic = adjugate of the dual conic
+    double P00 = D[1][1] * D[2][2] - D[1][2] * D[2][1];
+    double P01 = D[0][2] * D[2][1] - D[0][1] * D[2][2];
+    double P02 = D[0][1] * D[1][2] - D[0][2] * D[1][1];
+    double P11 = D[0][0] * D[2][2] - D[0][2] * D[2][0];
+    double P12 = D[0][2] * D[1][0] - D[0][0] * D[1][2];
+    double P22 = D[0][0] * D[1][1] - D[0][1] * D[1][0];
+    // inside must be negative: evaluate at the projected centre
+    const double cu = m[0] / m[2], cv = m[1] / m[2];
+    const double at_c = P00 * cu * cu + 2.0 * P01 * cu * cv + P11 * cv * cv + 2.0 * P02 * cu +
+                        2.0 * P12 * cv + P22;
+    const double sg = at_c > 0.0 ? -1.0 : 1.0;
+    const double nrm = fmax(fabs(P00), fabs(P11));
+    if (!(nrm > 0.0) || !(P00 * P11 - P01 * P01 > 0.0)) return q;   // not an ellipse: no cull
+    const double k = sg / nrm;
+    const double A = P00 * k, B = 2.0 * P01 * k, C = P11 * k, Dd = 2.0 * P02 * k,
+                 E = 2.0 * P12 * k, F = P22 * k;
+    const double hu = 0.5 * (double)(box[1] - box[0]) + 1.0, hv = 0.5 * (double)(box[3] - box[2]) + 1.0;
+    const double mag = fabs(A) * hu * hu + fabs(B) * hu * hv + fabs(C) * hv * hv + fabs(Dd) * hu +
+                       fabs(E) * hv + fabs(F);
+    q.A = (float)A; q.B = (float)B; q.C = (float)C; q.D = (float)Dd; q.E = (float)E;
+    q.F = (float)(F - 2e-5 * mag);
+    if (!isfinite(q.A + q.B + q.C + q.D + q.E + q.F)) {
+        q.A = q.B = q.C = q.D = q.E = 0.f;
+        q.F = -1.f;
+    }
+    return q;
+}
+
+__global__ void preprocess_kernel(qgs_params prm, CamK cam, PrepView pv, int euclid)
 {
     int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= prm.P) return;
@@ -275,6 +394,7 @@ __global__ void preprocess_kernel(qgs_params prm, CamK cam, PrepView pv)
     r.ell9 = (float)(9.0 * s12 * s12);
     r.pad[0] = r.pad[1] = 0.f;
     pv.rec[p] = r;
+    pv.conic[p] = bounding_conic(s, planar, euclid != 0, R, c, cam, box);
 }
 
 // ------------------------------------------------------------- K7 chain

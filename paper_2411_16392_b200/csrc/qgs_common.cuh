@@ -57,9 +57,21 @@ struct __align__(16) PrimRec {   // 32 floats, 128 B
 static_assert(sizeof(PrimRec) == 128, "PrimRec must be 128 B");
 static_assert(sizeof(Geo64) == 256, "Geo64 must be 256 B");
 
+// Screen-space cull of one primitive: the pixel-centre conic of the outline
+// of an ellipsoid that contains every point the selection rule can accept
+// (preprocess.cu: bounding_conic).  Pixel (u, v) with U = u - uc, V = v - vc
+// can only be accepted if  A U^2 + B U V + C V^2 + D U + E V + F <= 0
+// (F carries the fp32 evaluation margin; all zero with F = -1 = no cull).
+struct __align__(16) ConicRec {   // 32 B
+    float A, B, C, D, E, F;
+    float uc, vc;         // origin (pixel indices; box centre)
+};
+static_assert(sizeof(ConicRec) == 32, "ConicRec must be 32 B");
+
 struct PrepView {
     Geo64 *geo;
     PrimRec *rec;
+    ConicRec *conic;
     int4 *bbox;
     int32_t *ntiles;
     int64_t *pair_off;    // P+1
@@ -74,6 +86,7 @@ __host__ __device__ inline PrepView prep_view(void *base, int32_t P)
     size_t o = 0;
     v.geo = reinterpret_cast<Geo64 *>(b + o);      o += align256(sizeof(Geo64) * (size_t)P);
     v.rec = reinterpret_cast<PrimRec *>(b + o);    o += align256(sizeof(PrimRec) * (size_t)P);
+    v.conic = reinterpret_cast<ConicRec *>(b + o); o += align256(sizeof(ConicRec) * (size_t)P);
     v.bbox = reinterpret_cast<int4 *>(b + o);      o += align256(sizeof(int4) * (size_t)P);
     v.ntiles = reinterpret_cast<int32_t *>(b + o); o += align256(sizeof(int32_t) * (size_t)P);
     v.pair_off = reinterpret_cast<int64_t *>(b + o);
@@ -83,6 +96,7 @@ __host__ __device__ inline PrepView prep_view(void *base, int32_t P)
 __host__ __device__ inline size_t prep_bytes(int32_t P)
 {
     return align256(sizeof(Geo64) * (size_t)P) + align256(sizeof(PrimRec) * (size_t)P) +
+           align256(sizeof(ConicRec) * (size_t)P) +
            align256(sizeof(int4) * (size_t)P) + align256(sizeof(int32_t) * (size_t)P) +
            align256(sizeof(int64_t) * ((size_t)P + 1)) + 256;
 }

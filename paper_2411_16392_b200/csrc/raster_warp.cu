@@ -95,6 +95,28 @@ __device__ __forceinline__ uint32_t block_lanes(const PrimRec &r, int bu, int bv
     return (cols * 0x01010101u) & rows;
 }
 
+// Conic cull (ConicRec): mask of block pixels in rows [r0, r0 + 2) whose
+// centre lies inside the primitive's bounding-ellipsoid outline.
+__device__ __forceinline__ uint32_t conic_rows(const ConicRec &q, int bu, int bv, int r0)
+{
+    const float U0 = (float)bu - q.uc;
+    uint32_t m = 0u;
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+        const int r = r0 + rr;
+        const float V = (float)(bv + r) - q.vc;
+        const float QV = fmaf(fmaf(q.C, V, q.E), V, q.F);
+        const float BVD = fmaf(q.B, V, q.D);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const float U = U0 + (float)c;
+            const float Q = fmaf(fmaf(q.A, U, BVD), U, QV);
+            m |= (Q <= 0.f ? 1u : 0u) << (8 * r + c);
+        }
+    }
+    return m;
+}
+
 // Per-lane ring view into shared memory.
 struct Ring {
     double *t;   // &ring_t[0][lane], stride 32
@@ -278,7 +300,7 @@ __device__ __forceinline__ size_t mask_index(int start, int n, int blk, int j)
 
 __global__ void __launch_bounds__(32, 16)
 raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
-                  const int32_t *__restrict__ tile_offsets,
+                  const ConicRec *__restrict__ conics, const int32_t *__restrict__ tile_offsets,
                   const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets out)
 {
     __shared__ FwdSmem sm;
@@ -342,21 +364,40 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
     for (int b0 = start; b0 < end; b0 += WB) {
         if (!__any_sync(FULL, alive)) break;
         const int nb = min(WB, end - b0);
-        load_batch32(sm.rec, sm.prim, recs, tile_prims, b0, nb);
-        const uint32_t mymask = lane < nb ? block_lanes(sm.rec[lane], bu, bv) : 0u;
+        const int my = load_batch32(sm.rec, sm.prim, recs, tile_prims, b0, nb);
 
-        // pass 1: coarse test of every in-box candidate
+        // pass 0 (entry-parallel): lane j and j + 16 evaluate entry j's box
+        // and conic cull on rows 0-1 / 2-3 of the block; the masks are then
+        // transposed to per-pixel entry bits
+        uint32_t bm = 0u, cm = 0u;
+        {
+            const int je = lane & 15;
+            const int pj = __shfl_sync(FULL, my, je);
+            if (je < nb) {
+                bm = block_lanes(sm.rec[je], bu, bv);
+                if (bm) cm = conics ? conic_rows(conics[pj], bu, bv, 2 * (lane >> 4)) & bm : bm;
+            }
+            cm |= __shfl_xor_sync(FULL, cm, 16);
+        }
+        uint32_t cand = 0u;
+        for (int j = 0; j < nb; ++j) cand |= ((__shfl_sync(FULL, cm, j) >> lane) & 1u) << j;
+        if (!alive) cand = 0u;
+        if (out.counters) {                           // algorithmic work: in-box candidates
+            for (int j = 0; j < nb; ++j) n_box += alive ? (__shfl_sync(FULL, bm, j) >> lane) & 1u : 0u;
+        }
+
+        // pass 1: coarse test of every candidate that survived the cull
         // (two candidates per iteration: their branch-free stage-1 chains
         // interleave, which hides the SQRT/RCP latencies)
         uint32_t bits = 0u, margb = 0u, secb = 0u;
-        for (int j = 0; j < nb; j += 2) {
-            const int j1 = min(j + 1, nb - 1);
-            const uint32_t m0 = __shfl_sync(FULL, mymask, j);
-            const uint32_t m1 = j + 1 < nb ? __shfl_sync(FULL, mymask, j1) : 0u;
-            if ((m0 | m1) == 0u) continue;            // warp-uniform skip
-            const bool a0 = alive && (m0 & lanebit), a1 = alive && (m1 & lanebit);
+        uint32_t uni = __reduce_or_sync(FULL, cand);
+        while (uni) {
+            const int j = __ffs(uni) - 1;
+            uni &= uni - 1;
+            const int j1 = uni ? __ffs(uni) - 1 : j;
+            uni &= uni - 1;
+            const bool a0 = (cand >> j) & 1u, a1 = j1 != j && ((cand >> j1) & 1u);
             if (!(a0 || a1)) continue;
-            n_box += (unsigned)a0 + (unsigned)a1;
             float r0[2], r1[2], hx0, hy0, hx1, hy1;
             unsigned s0 = coarse_stage1(sm.rec[j], dx, dy, dz, c.t_clip, r0, hx0, hy0);
             unsigned s1 = coarse_stage1(sm.rec[j1], dx, dy, dz, c.t_clip, r1, hx1, hy1);

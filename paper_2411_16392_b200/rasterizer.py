@@ -39,6 +39,9 @@ class RenderSettings:
     t_term: float = 1e-4
     resort: bool = True
     euclidean_density: bool = False
+    # extension (not in the reference): False disables the forward's
+    # screen-space conic cull; outputs are identical either way
+    conic_cull: bool = True
 
 
 # ----------------------------------------------------------------- helpers
@@ -75,6 +78,7 @@ def _settings_struct(st):
     s.t_near_clip, s.alpha_floor = float(st.t_near_clip), float(st.alpha_floor)
     s.alpha_clamp, s.t_term = float(st.alpha_clamp), float(st.t_term)
     s.resort, s.euclidean_density = int(bool(st.resort)), int(bool(st.euclidean_density))
+    s.no_cull = int(not getattr(st, "conic_cull", True))
     return s
 
 
