@@ -383,7 +383,9 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         for (int j = 0; j < nb; ++j) cand |= ((__shfl_sync(FULL, cm, j) >> lane) & 1u) << j;
         if (!alive) cand = 0u;
         if (out.counters) {                           // algorithmic work: in-box candidates
-            for (int j = 0; j < nb; ++j) n_box += alive ? (__shfl_sync(FULL, bm, j) >> lane) & 1u : 0u;
+            uint32_t inbox = 0u;                      // (shuffles outside the select)
+            for (int j = 0; j < nb; ++j) inbox |= ((__shfl_sync(FULL, bm, j) >> lane) & 1u) << j;
+            n_box += alive ? __popc(inbox) : 0u;
         }
 
         // pass 1: coarse test of every candidate that survived the cull
