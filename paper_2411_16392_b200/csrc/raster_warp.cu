@@ -224,7 +224,7 @@ struct BwdSmem {
     int prim[WB];
     double ring_t[RING][32];
     int ring_p[RING][32];
-    float red[1][32][KG];
+    float red[1][33][KG];   // row 32 stays zero (padding reads of the group sums)
 };
 
 struct Cfg {
@@ -680,7 +680,7 @@ __device__ __forceinline__ void frag_grad(const PrimRec &r, const Frag &f, float
 }
 
 // sum the slots of lanes that emitted the same primitive; one atomic per slot
-__device__ __forceinline__ void warp_accumulate(float (*red)[32][KG], bool emit, int prim,
+__device__ __forceinline__ void warp_accumulate(float (*red)[33][KG], bool emit, int prim,
                                                 const float g[KG], float *__restrict__ kg)
 {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -700,7 +700,20 @@ __device__ __forceinline__ void warp_accumulate(float (*red)[32][KG], bool emit,
         const int gp = __shfl_sync(FULL, prim, ld);
         if (lane < 22) {
             float s = 0.f;
-            for (unsigned mm = grp; mm; mm &= mm - 1) s += red[w][__ffs(mm) - 1][lane];
+            // four independent partial sums: the member loads do not wait on
+            // each other (row 32 is zero padding)
+            float s1 = 0.f, s2 = 0.f, s3 = 0.f;
+            for (unsigned mm = grp; mm;) {
+                const int i0 = __ffs(mm) - 1; mm &= mm - 1;
+                const int i1 = mm ? __ffs(mm) - 1 : 32; mm &= mm - 1;
+                const int i2 = mm ? __ffs(mm) - 1 : 32; mm &= mm - 1;
+                const int i3 = mm ? __ffs(mm) - 1 : 32; mm &= mm - 1;
+                s += red[w][i0][lane];
+                s1 += red[w][i1][lane];
+                s2 += red[w][i2][lane];
+                s3 += red[w][i3][lane];
+            }
+            s = (s + s1) + (s2 + s3);
             atomicAdd(kg + (size_t)gp * KG + lane, s);
         }
     }
@@ -715,6 +728,8 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
 {
     __shared__ BwdSmem sm;
     const int lane = threadIdx.x & 31;
+    if (lane < KG) sm.red[0][32][lane] = 0.f;
+    __syncwarp();
     int tile, blk, u, v;
     block_pixel(cam.tiles_x, tile, blk, u, v);
     const bool inside = u < cam.W && v < cam.H;
