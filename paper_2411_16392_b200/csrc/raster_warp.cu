@@ -679,7 +679,11 @@ __device__ __forceinline__ void frag_grad(const PrimRec &r, const Frag &f, float
     (void)dx; (void)dy; (void)dz;
 }
 
-// sum the slots of lanes that emitted the same primitive; one atomic per slot
+// Sum the slots of lanes that emitted the same primitive and add each sum to
+// the primitive's kernel-gradient row.  Groups are served five at a time:
+// lane = 6 * set + q sums float4 slot q (slots 4q .. 4q+3) of the set-th
+// pending group over its members and issues one 16-byte vector atomic
+// (sm_90+ red.global.add.v4.f32): 6 atomics per group instead of 22.
 __device__ __forceinline__ void warp_accumulate(float (*red)[33][KG], bool emit, int prim,
                                                 const float g[KG], float *__restrict__ kg)
 {
@@ -693,28 +697,27 @@ __device__ __forceinline__ void warp_accumulate(float (*red)[33][KG], bool emit,
     const unsigned peers = __match_any_sync(FULL, key);
     unsigned leaders = __ballot_sync(FULL, emit && (peers & ((1u << lane) - 1u)) == 0);
     __syncwarp();
+    const int set = lane / 6, q = lane - 6 * set;
+    const float4 (*red4)[KG / 4] = reinterpret_cast<const float4 (*)[KG / 4]>(red[w]);
     while (leaders) {
-        const int ld = __ffs(leaders) - 1;
-        leaders &= leaders - 1;
-        const unsigned grp = __shfl_sync(FULL, peers, ld);
-        const int gp = __shfl_sync(FULL, prim, ld);
-        if (lane < 22) {
-            float s = 0.f;
-            // four independent partial sums: the member loads do not wait on
-            // each other (row 32 is zero padding)
-            float s1 = 0.f, s2 = 0.f, s3 = 0.f;
-            for (unsigned mm = grp; mm;) {
+        unsigned L = leaders;
+        for (int k = 0; k < set && L; ++k) L &= L - 1;
+        const int ld = (set < 5 && L) ? __ffs(L) - 1 : -1;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) leaders &= leaders - 1;
+        const unsigned grp = __shfl_sync(FULL, peers, ld < 0 ? 0 : ld);
+        const int gp = __shfl_sync(FULL, prim, ld < 0 ? 0 : ld);
+        if (ld >= 0) {
+            float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+            for (unsigned mm = grp; mm;) {             // two independent partial sums
                 const int i0 = __ffs(mm) - 1; mm &= mm - 1;
                 const int i1 = mm ? __ffs(mm) - 1 : 32; mm &= mm - 1;
-                const int i2 = mm ? __ffs(mm) - 1 : 32; mm &= mm - 1;
-                const int i3 = mm ? __ffs(mm) - 1 : 32; mm &= mm - 1;
-                s += red[w][i0][lane];
-                s1 += red[w][i1][lane];
-                s2 += red[w][i2][lane];
-                s3 += red[w][i3][lane];
+                const float4 x = red4[i0][q], y = red4[i1][q];
+                a.x += x.x; a.y += x.y; a.z += x.z; a.w += x.w;
+                b.x += y.x; b.y += y.y; b.z += y.z; b.w += y.w;
             }
-            s = (s + s1) + (s2 + s3);
-            atomicAdd(kg + (size_t)gp * KG + lane, s);
+            a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+            atomicAdd(reinterpret_cast<float4 *>(kg + (size_t)gp * KG) + q, a);
         }
     }
     __syncwarp();
@@ -728,7 +731,7 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
 {
     __shared__ BwdSmem sm;
     const int lane = threadIdx.x & 31;
-    if (lane < KG) sm.red[0][32][lane] = 0.f;
+    if (lane < KG) sm.red[0][32][lane] = 0.f;        // zero row for padded group sums
     __syncwarp();
     int tile, blk, u, v;
     block_pixel(cam.tiles_x, tile, blk, u, v);
