@@ -194,7 +194,7 @@ __global__ void pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, S
 //
 // One CTA per tile, two levels:
 //   1. bucket (MSD) pass: the f32 key bits that vary inside the tile are cut
-//      into nb buckets (nb ~ n/4, a power of two); histogram, scan and an
+//      into nb buckets (nb ~ n/2, a power of two); histogram, scan and an
 //      unstable scatter (shared-memory cursors) into a staging array --
 //      shared memory when the tile fits, else its slice of `tmp` (L2-resident
 //      at these sizes).  Nothing downstream depends on the scatter order.
@@ -209,12 +209,11 @@ constexpr int SORT_W = SORT_T / 32;
 constexpr int SORT_IPT = 4;
 constexpr int SORT_CHUNK = SORT_T * SORT_IPT;     // items per register pass
 constexpr int SORT_SMEM_ITEMS = 8192;             // staged in shared memory up to this
-constexpr int SORT_MAX_BUCKETS = 4096;
+constexpr int SORT_MAX_BUCKETS = 8192;
 
 struct SortSmem {
     uint64_t buf[SORT_SMEM_ITEMS];
-    int bstart[SORT_MAX_BUCKETS + 1];
-    int cursor[SORT_MAX_BUCKETS];
+    int bend[SORT_MAX_BUCKETS];   // counts -> start cursors -> (after the scatter) bucket ends
     int scan_w[32];
     uint32_t kmin, kmax;
 };
@@ -252,19 +251,41 @@ __device__ __forceinline__ int rank_in_bucket(const uint64_t *a, int b0, int b1,
 }
 
 // Emit the sorted order of buckets [g0, g1) whose items sit in a[0 .. ),
-// bucket b at a[bstart[b] - base ...]: every item finds its own rank inside
+// bucket b at a[bucket_start(b) - base ...]: every item finds its own rank inside
 // its bucket (buckets average a few items), item-parallel over the CTA.
 // Ends with __syncthreads.
+__device__ __forceinline__ int bucket_start(const SortSmem &sm, int d)
+{
+    return d == 0 ? 0 : sm.bend[d - 1];
+}
+
+// rank of x among its bucket a[b0, b1): composite compare, with the exact
+// (fp64 key, prim) order only when an equal f32 key is present
+__device__ __forceinline__ int rank_fast(const uint64_t *a, int b0, int b1, uint64_t x, int tile,
+                                         const PrepView &pv, const CamK &cam, const SetK &st)
+{
+    const uint32_t h = (uint32_t)(x >> 32);
+    int r = 0;
+    bool eq = false;
+#pragma unroll 4
+    for (int j = b0; j < b1; ++j) {
+        const uint64_t y = a[j];
+        r += y < x ? 1 : 0;
+        eq |= ((uint32_t)(y >> 32) == h) & (y != x);
+    }
+    return eq ? rank_in_bucket(a, b0, b1, x, tile, pv, cam, st) : r;
+}
+
 __device__ void sort_buckets(SortSmem &sm, const uint64_t *a, int base, int g0, int g1,
                              uint32_t kmin, int shift, int tile, const PrepView &pv,
                              const CamK &cam, const SetK &st, int32_t *out)
 {
-    const int i0 = sm.bstart[g0] - base, i1 = sm.bstart[g1] - base;
+    const int i0 = bucket_start(sm, g0) - base, i1 = bucket_start(sm, g1) - base;
     for (int i = i0 + threadIdx.x; i < i1; i += SORT_T) {
         const uint64_t x = a[i];
         const int d = (int)((((uint32_t)(x >> 32)) - kmin) >> shift);
-        const int b0 = sm.bstart[d], b1 = sm.bstart[d + 1];
-        const int r = b1 - b0 == 1 ? 0 : rank_in_bucket(a, b0 - base, b1 - base, x, tile, pv, cam, st);
+        const int b0 = bucket_start(sm, d), b1 = sm.bend[d];
+        const int r = b1 - b0 == 1 ? 0 : rank_fast(a, b0 - base, b1 - base, x, tile, pv, cam, st);
         out[b0 + r] = (int32_t)(uint32_t)x;
     }
     __syncthreads();
@@ -309,8 +330,8 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
         lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
     }
     int nb = 64;
-    while (nb < SORT_MAX_BUCKETS && nb * 4 < n) nb <<= 1;
-    for (int d = threadIdx.x; d < nb; d += SORT_T) sm.cursor[d] = 0;
+    while (nb < SORT_MAX_BUCKETS && nb * 2 < n) nb <<= 1;
+    for (int d = threadIdx.x; d < nb; d += SORT_T) sm.bend[d] = 0;
     __syncthreads();
     if (lane == 0) { atomicMin(&sm.kmin, lmin); atomicMax(&sm.kmax, lmax); }
     __syncthreads();
@@ -325,19 +346,19 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
             const int i = c0 + k * SORT_T + threadIdx.x;
             if (i < n) {
                 const uint64_t v = regs ? it[k] : src[i];
-                atomicAdd(&sm.cursor[(((uint32_t)(v >> 32)) - kmin) >> shift], 1);
+                atomicAdd(&sm.bend[(((uint32_t)(v >> 32)) - kmin) >> shift], 1);
             }
         }
     }
     __syncthreads();
-    // exclusive scan of the bucket counts (nb <= 4096 = 8 per thread)
+    // exclusive scan of the bucket counts (nb <= 8192 = 16 per thread)
     {
         constexpr int PER = SORT_MAX_BUCKETS / SORT_T;
         int c[PER], sum = 0;
 #pragma unroll
         for (int q = 0; q < PER; ++q) {
             const int d = threadIdx.x * PER + q;
-            c[q] = d < nb ? sm.cursor[d] : 0;
+            c[q] = d < nb ? sm.bend[d] : 0;
             sum += c[q];
         }
         int tot;
@@ -345,10 +366,9 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
 #pragma unroll
         for (int q = 0; q < PER; ++q) {
             const int d = threadIdx.x * PER + q;
-            if (d < nb) { sm.bstart[d] = ex; sm.cursor[d] = ex; }
+            if (d < nb) sm.bend[d] = ex;
             ex += c[q];
         }
-        if (threadIdx.x == 0) sm.bstart[nb] = n;
     }
     __syncthreads();
     // scatter into buckets
@@ -358,7 +378,7 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
             const int i = c0 + k * SORT_T + threadIdx.x;
             if (i < n) {
                 const uint64_t v = regs ? it[k] : src[i];
-                const int pos = atomicAdd(&sm.cursor[(((uint32_t)(v >> 32)) - kmin) >> shift], 1);
+                const int pos = atomicAdd(&sm.bend[(((uint32_t)(v >> 32)) - kmin) >> shift], 1);
                 stage[pos] = v;
             }
         }
@@ -373,17 +393,17 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
         // their buckets out of shared memory
         int g0 = 0;
         while (g0 < nb) {
-            const int base = sm.bstart[g0];
+            const int base = bucket_start(sm, g0);
             // last bucket end within SORT_SMEM_ITEMS of base (binary search)
             int lo = g0 + 1, hi = nb;
             while (lo < hi) {
                 const int mid = (lo + hi + 1) >> 1;
-                if (sm.bstart[mid] - base <= SORT_SMEM_ITEMS) lo = mid; else hi = mid - 1;
+                if (sm.bend[mid - 1] - base <= SORT_SMEM_ITEMS) lo = mid; else hi = mid - 1;
             }
             int g1 = lo;
-            if (sm.bstart[g1] - base > SORT_SMEM_ITEMS) {
+            if (sm.bend[g1 - 1] - base > SORT_SMEM_ITEMS) {
                 // one degenerate bucket larger than shared memory: rank it in place
-                const int b1 = sm.bstart[g1];
+                const int b1 = sm.bend[g1 - 1];
                 for (int i = base + threadIdx.x; i < b1; i += SORT_T) {
                     const uint64_t x = stage[i];
                     out[base + rank_in_bucket(stage, base, b1, x, tile, pv, cam, st)] =
@@ -393,7 +413,7 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
                 g0 = g1;
                 continue;
             }
-            const int cnt = sm.bstart[g1] - base;
+            const int cnt = sm.bend[g1 - 1] - base;
             for (int i = threadIdx.x; i < cnt; i += SORT_T) sm.buf[i] = stage[base + i];
             __syncthreads();
             sort_buckets(sm, sm.buf, base, g0, g1, kmin, shift, tile, pv, cam, st, out);
