@@ -95,11 +95,6 @@ __device__ __forceinline__ uint32_t block_lanes(const PrimRec &r, int bu, int bv
     return (cols * 0x01010101u) & rows;
 }
 
-__device__ __forceinline__ void prefetch_l1(const void *p)
-{
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-}
-
 // Conic cull (ConicRec): mask of block pixels in rows [r0, r0 + 2) whose
 // centre lies inside the primitive's bounding-ellipsoid outline.
 __device__ __forceinline__ uint32_t conic_rows(const ConicRec &q, int bu, int bv, int r0)
@@ -381,8 +376,6 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
             if (je < nb) {
                 bm = block_lanes(sm.rec[je], bu, bv);
                 if (bm) cm = conics ? conic_rows(conics[pj], bu, bv, 2 * (lane >> 4)) & bm : bm;
-                // the exact test (pass 2) reads the head of Geo64 (ohat, M, wv)
-                if (cm && lane < 16) prefetch_l1(geo + pj);
             }
             cm |= __shfl_xor_sync(FULL, cm, 16);
         }
@@ -815,24 +808,16 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         const int nf_max = __reduce_max_sync(FULL, nf);
         if (fwd.frag_prim && fwd.frag_t && nf_max <= fwd.frag_cap) {
             const size_t base = (size_t)blockIdx.x * fwd.frag_cap * 32 + lane;
-            // two-deep pipeline: ids/depths two fragments ahead, the
-            // records of the next fragment prefetched into L1
-            int p0 = -1, p1 = -1;
-            double t0 = 0.0, t1 = 0.0;
-            if (0 < nf) { p0 = fwd.frag_prim[base]; t0 = fwd.frag_t[base]; }
-            if (1 < nf) { p1 = fwd.frag_prim[base + 32]; t1 = fwd.frag_t[base + 32]; }
+            int np_ = -1;
+            double nt_ = 0.0;
+            if (0 < nf) { np_ = fwd.frag_prim[base]; nt_ = fwd.frag_t[base]; }
             for (int k = 0; k < nf_max; ++k) {
                 const bool emit = k < nf;
-                const int ep = p0;
-                const double et = t0;
-                if (k + 1 < nf) {
-                    prefetch_l1(recs + p1);
-                    prefetch_l1(geo + p1);
-                }
-                p0 = p1; t0 = t1;
-                if (k + 2 < nf) {
-                    p1 = fwd.frag_prim[base + (size_t)(k + 2) * 32];
-                    t1 = fwd.frag_t[base + (size_t)(k + 2) * 32];
+                const int ep = np_;
+                const double et = nt_;
+                if (k + 1 < nf) {                // prefetch the next fragment
+                    np_ = fwd.frag_prim[base + (size_t)(k + 1) * 32];
+                    nt_ = fwd.frag_t[base + (size_t)(k + 1) * 32];
                 }
                 emit_grad(emit, ep, et);
             }
