@@ -135,6 +135,7 @@ def run_ours(a):
     import torch.distributed as dist
 
     from paper_2411_16392_b200 import rasterizer as rz
+    from paper_2411_16392_b200.dist import pipelined_prepare
 
     rank, world, local = env_rank()
     torch.cuda.set_device(local)
@@ -153,12 +154,12 @@ def run_ours(a):
            for v in mine]
     grads = rz.GradientBuffer.zeros_flat(dev)
     counters = torch.zeros(3, dtype=torch.int64, device=device)
+    side = torch.cuda.Stream(device=device)
     stream = torch.cuda.current_stream()
 
     def step(ev=None, count=False):
         grads.zero_()
-        for i, v in enumerate(mine):
-            prep = rz.prepare(dev, cams[v], st)
+        for i, v, prep in pipelined_prepare(dev, cams, mine, st, side):
             if ev is not None:
                 ev["f0"][i].record(stream)
             tg = rz.forward(prep, counters=counters if count else None)
@@ -284,6 +285,7 @@ def run_ours(a):
 
 def run_e2e(a, rz, sc, mine, device, st, world):
     import torch.distributed as dist
+    from paper_2411_16392_b200.dist import pipelined_prepare
     pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory()  # noqa: E731
     host = type("H", (), {})()
     for f in rz.DevicePrimitives.FIELDS:
@@ -292,14 +294,14 @@ def run_e2e(a, rz, sc, mine, device, st, world):
     h2d = sum(getattr(host, f).numel() * 4 for f in rz.DevicePrimitives.FIELDS)
     h2d += sum(t.numel() * 4 for u in ups for t in u.values())
     out_host = None
+    side = torch.cuda.Stream(device=device)
 
     def step():
         nonlocal out_host
         dev = rz.DevicePrimitives.from_host(host, device, non_blocking=True)
         grads = rz.GradientBuffer.zeros_flat(dev)
-        for i, v in enumerate(mine):
+        for i, v, prep in pipelined_prepare(dev, sc.cams, mine, st, side):
             up = {k: t.to(device, non_blocking=True) for k, t in ups[i].items()}
-            prep = rz.prepare(dev, sc.cams[v], st)
             tg = rz.forward(prep)
             rz.backward(prep, tg, up, out=grads)
         if world > 1:

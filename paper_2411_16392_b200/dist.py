@@ -76,6 +76,35 @@ def sharded_step(n_views, view_backward, rank, world, shapes, device=None, group
     return unpack(flat, shapes)
 
 
+def pipelined_prepare(dev_prims, cams, views, settings, side=None):
+    """Yield (i, view, PreparedView) for `views`, each ready on the current
+    stream, with view i+1's preprocessing and binning launched on a side
+    stream while the caller's forward/backward of view i run on the current
+    one (the per-view host read of the pair count no longer drains the GPU,
+    and binning overlaps the previous view's raster).  The caller must
+    consume each view (launch its work) before advancing the generator."""
+    from . import rasterizer as rz
+    main = torch.cuda.current_stream()
+    side = side if side is not None else torch.cuda.Stream(device=main.device)
+    side.wait_stream(main)                  # the primitives were uploaded on main
+
+    def launch(v):
+        with torch.cuda.stream(side):
+            prep = rz.prepare(dev_prims, cams[v], settings)
+            ev = torch.cuda.Event()
+            ev.record(side)
+        return prep, ev
+
+    nxt = launch(views[0]) if views else None
+    for i, v in enumerate(views):
+        prep, ev = nxt
+        main.wait_event(ev)
+        for t in (prep.prep, prep.tile_offsets, prep.tile_prims):
+            t.record_stream(main)           # allocated on `side`, used on main
+        yield i, v, prep
+        nxt = launch(views[i + 1]) if i + 1 < len(views) else None
+
+
 def gpu_step(dev_prims, cams, upstreams, settings, rank, world, grads=None, group=None):
     """The B200 step used by bench.py: this rank's views through the sm_100a
     rasterizer, gradients accumulated in one flat device buffer, one NCCL
@@ -85,8 +114,8 @@ def gpu_step(dev_prims, cams, upstreams, settings, rank, world, grads=None, grou
         grads = rz.GradientBuffer.zeros_flat(dev_prims)
     else:
         grads.zero_()
-    for v in shard_views(len(cams), rank, world):
-        prep = rz.prepare(dev_prims, cams[v], settings)
+    for _, v, prep in pipelined_prepare(dev_prims, cams, shard_views(len(cams), rank, world),
+                                         settings):
         tg = rz.forward(prep)
         rz.backward(prep, tg, upstreams[v], out=grads)
     allreduce_(grads.buffer, group)
