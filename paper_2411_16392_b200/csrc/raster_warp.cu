@@ -34,7 +34,7 @@
 
 namespace qgs {
 
-constexpr int WB = 16;        // entries per batch (<= 32); small keeps smem per warp low
+constexpr int WB = 16;        // entries per batch (8, 16 or 32; 16 measured best on C3)
 constexpr int NBLK = 8;       // 8x4 blocks per 16x16 tile
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -95,14 +95,15 @@ __device__ __forceinline__ uint32_t block_lanes(const PrimRec &r, int bu, int bv
     return (cols * 0x01010101u) & rows;
 }
 
-// Conic cull (ConicRec): mask of block pixels in rows [r0, r0 + 2) whose
+// Conic cull (ConicRec): mask of block pixels in rows [r0, r0 + NR) whose
 // centre lies inside the primitive's bounding-ellipsoid outline.
+template <int NR>
 __device__ __forceinline__ uint32_t conic_rows(const ConicRec &q, int bu, int bv, int r0)
 {
     const float U0 = (float)bu - q.uc;
     uint32_t m = 0u;
 #pragma unroll
-    for (int rr = 0; rr < 2; ++rr) {
+    for (int rr = 0; rr < NR; ++rr) {
         const int r = r0 + rr;
         const float V = (float)(bv + r) - q.vc;
         const float QV = fmaf(fmaf(q.C, V, q.E), V, q.F);
@@ -366,18 +367,20 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         const int nb = min(WB, end - b0);
         const int my = load_batch32(sm.rec, sm.prim, recs, tile_prims, b0, nb);
 
-        // pass 0 (entry-parallel): lane j and j + 16 evaluate entry j's box
-        // and conic cull on rows 0-1 / 2-3 of the block; the masks are then
-        // transposed to per-pixel entry bits
+        // pass 0 (entry-parallel): lanes j, j + WB, ... evaluate entry j's
+        // box and conic cull, each on 4 / (32 / WB) rows of the block; the
+        // masks are then transposed to per-pixel entry bits
         uint32_t bm = 0u, cm = 0u;
         {
-            const int je = lane & 15;
+            constexpr int NR = 4 * WB / 32;
+            const int je = lane % WB;
             const int pj = __shfl_sync(FULL, my, je);
             if (je < nb) {
                 bm = block_lanes(sm.rec[je], bu, bv);
-                if (bm) cm = conics ? conic_rows(conics[pj], bu, bv, 2 * (lane >> 4)) & bm : bm;
+                if (bm) cm = conics ? conic_rows<NR>(conics[pj], bu, bv, NR * (lane / WB)) & bm : bm;
             }
-            cm |= __shfl_xor_sync(FULL, cm, 16);
+#pragma unroll
+            for (int o = WB; o < 32; o <<= 1) cm |= __shfl_xor_sync(FULL, cm, o);
         }
         uint32_t cand = 0u;
         for (int j = 0; j < nb; ++j) cand |= ((__shfl_sync(FULL, cm, j) >> lane) & 1u) << j;
