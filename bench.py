@@ -153,7 +153,7 @@ def run_ours(a):
     ups = [{k: torch.from_numpy(np.ascontiguousarray(u)).to(device) for k, u in sc.upstream[v].items()}
            for v in mine]
     grads = rz.GradientBuffer.zeros_flat(dev)
-    counters = torch.zeros(3, dtype=torch.int64, device=device)
+    counters = torch.zeros(5, dtype=torch.int64, device=device)
     side = torch.cuda.Stream(device=device)
     stream = torch.cuda.current_stream()
 
@@ -230,7 +230,7 @@ def run_ours(a):
     peaks, peaks_kind = load_peaks()
     cp = measure_compute_peaks(local)
     # algorithmic work of this rank's views per step
-    n_box, n_acc, n_comp = cnt
+    n_box, n_acc, n_comp, n_cull, n_coarse = cnt
     n_miss = n_box - n_acc
     F_fwd = n_miss * C_MISS + n_acc * C_HIT + n_comp * C_COMP
     S_fwd = n_miss * S_MISS + n_acc * S_HIT
@@ -258,6 +258,7 @@ def run_ours(a):
         "step_roofline_ms": T_roof * 1e3,
         "step_roofline_frac": (T_roof * 1e3) / ms if world == 1 else None,
         "algorithmic": {"candidates": n_box, "accepted": n_acc, "composited": n_comp,
+                        "after_conic_cull": n_cull, "after_coarse_test": n_coarse,
                         "pairs": sum(n_pairs_mine), "flop_fwd": F_fwd, "flop_bwd": F_bwd,
                         "sfu_fwd": S_fwd, "sfu_bwd": S_bwd},
     }

@@ -86,18 +86,18 @@ typedef struct qgs_targets {
     double *aux;               /* QGS_AUX_PLANES*H*W float64 blend sums; required by
                                   qgs_backward, may be NULL for a forward-only call */
     unsigned long long *counters; /* optional, accumulated (+=): [0] candidates inside
-                                  the pixel box, [1] accepted fragments, [2] composited */
-    uint32_t *accept_mask;     /* n_pairs*8: per sorted pair, the accepted-pixel lane
-                                  mask of each of the tile's 8 warps; written by the
-                                  forward, required by qgs_backward (may be NULL for a
-                                  forward-only call) */
+                                  the pixel box, [1] accepted fragments, [2] composited,
+                                  [3] candidates left by the conic cull, [4] candidates
+                                  passing the coarse fp32 test (5 entries) */
     int32_t *frag_prim;        /* optional fragment log (NULL = none): for every pixel, the
                                   primitive of each composited fragment in compositing
                                   order; layout [raster warp][k < frag_cap][lane], one
-                                  raster warp per 8x4 block, 8 per tile (tile-major) */
+                                  raster warp per 8x4 block, 8 per tile (tile-major);
+                                  the backward reads it instead of replaying */
     double *frag_t;            /* same layout: float64 depth of each logged fragment */
     int32_t frag_cap;          /* fragments logged per pixel; a block with a pixel over
-                                  the cap is replayed from accept_mask by the backward */
+                                  the cap (or no log) is replayed by the backward with
+                                  the full candidate test */
 } qgs_targets;
 
 /* Upstream map gradients (rasterizer.py:230-250); NULL = all zero. */

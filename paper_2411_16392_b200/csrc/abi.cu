@@ -218,8 +218,7 @@ int qgs_forward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_se
     if (out->violations)
         QGS_CK(cudaMemsetAsync(out->violations, 0, sizeof(int32_t) * ck.tiles_x * ck.tiles_y, s));
     qgs::raster_fwd_kernel<<<ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE,
-                             qgs::RASTER_THREADS, 0, s>>>(pv.rec, pv.geo,
-                                                            st->no_cull ? nullptr : pv.conic, tile_offsets,
+                             qgs::RASTER_THREADS, 0, s>>>(pv.rec, pv.geo, pv.conic, tile_offsets,
                                                             tile_prims, ck, sk, *out);
     QGS_LAUNCHED("raster_fwd_kernel");
     return 0;
@@ -232,7 +231,7 @@ int qgs_backward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_s
     if (!prep || !st || !fwd || !up || !tile_offsets || (!kg && P > 0))
         return fail(QGS_E_ARG, "NULL argument");
     if (P == 0) return 0;
-    if (!fwd->aux || !fwd->accept_mask) return fail(QGS_E_ARG, "backward needs the forward's aux planes and accept mask");
+    if (!fwd->aux) return fail(QGS_E_ARG, "backward needs the forward's aux planes");
     if (int rc = check_cam(cam)) return rc;
     if (int rc = configure()) return rc;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);

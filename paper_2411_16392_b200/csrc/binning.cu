@@ -205,7 +205,6 @@ __global__ void pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, S
 //      staged in L2 and ranked in groups of whole buckets loaded into
 //      shared memory.
 constexpr int SORT_T = 512;
-constexpr int SORT_W = SORT_T / 32;
 constexpr int SORT_IPT = 4;
 constexpr int SORT_CHUNK = SORT_T * SORT_IPT;     // items per register pass
 constexpr int SORT_SMEM_ITEMS = 8192;             // staged in shared memory up to this
@@ -300,7 +299,7 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
     const int tile = blockIdx.x;
     const int start = tile_offsets[tile], n = tile_offsets[tile + 1] - start;
     if (n == 0) return;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
     const uint64_t *src = keys + start;
     int32_t *out = tile_prims + start;
     if (n == 1) {

@@ -242,9 +242,9 @@ __device__ inline ConicRec bounding_conic(const double s[3], bool planar, bool e
     ConicRec q;
     q.A = q.B = q.C = q.D = q.E = 0.f;
     q.F = -1.f;
-    q.uc = 0.5f * (float)(box[0] + box[1]);
-    q.vc = 0.5f * (float)(box[2] + box[3]);
-    if (box[0] > box[1]) return q;
+    if (box[0] > box[1]) { q.bb_u = 0xffffu; q.bb_v = 0xffffu; return q; }
+    q.bb_u = (uint32_t)box[0] | ((uint32_t)box[1] << 16);
+    q.bb_v = (uint32_t)box[2] | ((uint32_t)box[3] << 16);
     double zc, ax[3];
     bounding_ellipsoid(s, planar, euclid, zc, ax);
     pad_axes(ax);
@@ -271,7 +271,7 @@ __device__ inline ConicRec bounding_conic(const double s[3], bool planar, bool e
     m[1] = cam.fy * mc[1] + cam.cy * mc[2];
     m[2] = mc[2];
     // translate so pixel (u, v) centre = (u0 + U, v0 + V), u0 = uc + 0.5
-    const double u0 = (double)q.uc + 0.5, v0 = (double)q.vc + 0.5;
+    const double u0 = (double)conic_uc(q) + 0.5, v0 = (double)conic_vc(q) + 0.5;
     for (int k = 0; k < 3; ++k) {
         Mq[0][k] -= u0 * Mq[2][k];
         Mq[1][k] -= v0 * Mq[2][k];

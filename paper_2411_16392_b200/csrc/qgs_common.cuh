@@ -64,9 +64,18 @@ static_assert(sizeof(Geo64) == 256, "Geo64 must be 256 B");
 // (F carries the fp32 evaluation margin; all zero with F = -1 = no cull).
 struct __align__(16) ConicRec {   // 32 B
     float A, B, C, D, E, F;
-    float uc, vc;         // origin (pixel indices; box centre)
+    uint32_t bb_u, bb_v;  // the inclusive pixel box (as PrimRec); origin = its centre
 };
 static_assert(sizeof(ConicRec) == 32, "ConicRec must be 32 B");
+
+__host__ __device__ inline float conic_uc(const ConicRec &q)
+{
+    return 0.5f * (float)((q.bb_u & 0xffffu) + (q.bb_u >> 16));
+}
+__host__ __device__ inline float conic_vc(const ConicRec &q)
+{
+    return 0.5f * (float)((q.bb_v & 0xffffu) + (q.bb_v >> 16));
+}
 
 struct PrepView {
     Geo64 *geo;
@@ -111,7 +120,7 @@ struct CamK {
 struct SetK {
     double bg[3];
     double t_clip, alpha_floor, alpha_clamp, t_term;
-    int resort, euclid;
+    int resort, euclid, no_cull;
 };
 
 inline CamK make_camk(const qgs_camera &c)
@@ -132,7 +141,7 @@ inline SetK make_setk(const qgs_settings &s)
     for (int i = 0; i < 3; ++i) k.bg[i] = s.background[i];
     k.t_clip = s.t_near_clip; k.alpha_floor = s.alpha_floor;
     k.alpha_clamp = s.alpha_clamp; k.t_term = s.t_term;
-    k.resort = s.resort; k.euclid = s.euclidean_density;
+    k.resort = s.resort; k.euclid = s.euclidean_density; k.no_cull = s.no_cull;
     return k;
 }
 

@@ -41,6 +41,9 @@ constexpr unsigned FULL = 0xffffffffu;
 struct FwdSmem {
     PrimRec rec[WB];
     int prim[WB];
+    int qprim[WB + 32];       // culled-in entries waiting for the coarse/exact passes
+    uint32_t qmask[WB + 32];  // their conic & box & alive pixel masks
+    uint32_t boxw[32];        // work counters only: pixel-box masks of the window
     double ring_t[RING][32];  // per-lane ring, [slot][lane]: conflict-free
     int ring_p[RING][32];
     double d64[3][32];        // fp64 pixel ray (only the exact path reads it)
@@ -84,11 +87,27 @@ __device__ __forceinline__ int load_batch32(PrimRec *srec, int *sprim,
     return my;
 }
 
-// lane mask of this block covered by the inclusive pixel box of r
-__device__ __forceinline__ uint32_t block_lanes(const PrimRec &r, int bu, int bv)
+// stage the records of queued entries ids[0 .. nb) into shared memory
+// (8 lanes per 128-byte record, coalesced)
+__device__ __forceinline__ void load_batch_ids(PrimRec *srec, const PrimRec *__restrict__ recs,
+                                               const int *ids, int nb)
 {
-    int c0 = max((int)(r.bb_u & 0xffffu) - bu, 0), c1 = min((int)(r.bb_u >> 16) - bu, 7);
-    int r0 = max((int)(r.bb_v & 0xffffu) - bv, 0), r1 = min((int)(r.bb_v >> 16) - bv, 3);
+    const int lane = threadIdx.x & 31;
+    const float4 *src = reinterpret_cast<const float4 *>(recs);
+    float4 *dst = reinterpret_cast<float4 *>(srec);
+#pragma unroll
+    for (int it = 0; it < WB / 4; ++it) {
+        const int j = it * 4 + (lane >> 3), q = lane & 7;
+        if (j < nb) dst[j * 8 + q] = __ldg(src + (size_t)ids[j] * 8 + q);
+    }
+    __syncwarp();
+}
+
+// lane mask of this block covered by an inclusive pixel box (packed words)
+__device__ __forceinline__ uint32_t block_lanes(uint32_t bb_u, uint32_t bb_v, int bu, int bv)
+{
+    int c0 = max((int)(bb_u & 0xffffu) - bu, 0), c1 = min((int)(bb_u >> 16) - bu, 7);
+    int r0 = max((int)(bb_v & 0xffffu) - bv, 0), r1 = min((int)(bb_v >> 16) - bv, 3);
     if (c0 > c1 || r0 > r1) return 0u;
     uint32_t cols = (0xffu >> (7 - c1)) & (0xffu << c0);
     uint32_t rows = (0xffffffffu >> (8 * (3 - r1))) & (0xffffffffu << (8 * r0));
@@ -100,12 +119,12 @@ __device__ __forceinline__ uint32_t block_lanes(const PrimRec &r, int bu, int bv
 template <int NR>
 __device__ __forceinline__ uint32_t conic_rows(const ConicRec &q, int bu, int bv, int r0)
 {
-    const float U0 = (float)bu - q.uc;
+    const float U0 = (float)bu - conic_uc(q), vc = conic_vc(q);
     uint32_t m = 0u;
 #pragma unroll
     for (int rr = 0; rr < NR; ++rr) {
         const int r = r0 + rr;
-        const float V = (float)(bv + r) - q.vc;
+        const float V = (float)(bv + r) - vc;
         const float QV = fmaf(fmaf(q.C, V, q.E), V, q.F);
         const float BVD = fmaf(q.B, V, q.D);
 #pragma unroll
@@ -290,13 +309,6 @@ __device__ __forceinline__ void shade_emitted(const PrimRec &r, const Geo64 &g, 
     normal_curv32(r, f.h, dx, dy, dz, f.nl, f.nc, f.K, f.inrm, f.flip);
 }
 
-// accepted-mask word of entry j (tile-list position start+j) for block blk:
-// block-major inside the tile so a warp reads its words contiguously
-__device__ __forceinline__ size_t mask_index(int start, int n, int blk, int j)
-{
-    return (size_t)start * NBLK + (size_t)blk * n + j;
-}
-
 // ================================================================ forward
 
 __global__ void __launch_bounds__(32, 16)
@@ -311,6 +323,7 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
     const int bu = u - (lane & 7), bv = v - (lane >> 3);
     const bool inside = u < cam.W && v < cam.H;
     const Cfg c = make_cfg(st);
+    const bool cull = st.no_cull == 0;
     float dx, dy, dz;
     {
         double d[3] = {0.0, 0.0, 1.0};
@@ -325,10 +338,9 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
     float median = 0.f;
     double last_t = -1.0e300;
     int nfrag = 0, viol = 0;
-    unsigned n_box = 0, n_acc = 0;
+    unsigned n_box = 0, n_acc = 0, n_cand = 0, n_coarse = 0;
     Ring R{&sm.ring_t[0][lane], &sm.ring_p[0][lane], 0};
     bool alive = inside;
-    const uint32_t lanebit = 1u << lane;
     const bool log_on = out.frag_prim != nullptr && out.frag_t != nullptr;
 
     auto composite = [&](int ep, double t, const Pay &f) {
@@ -361,39 +373,17 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         if (T < c.t_term) alive = false;
     };
 
-    const int start = tile_offsets[tile], end = tile_offsets[tile + 1], n = end - start;
-    for (int b0 = start; b0 < end; b0 += WB) {
-        if (!__any_sync(FULL, alive)) break;
-        const int nb = min(WB, end - b0);
-        const int my = load_batch32(sm.rec, sm.prim, recs, tile_prims, b0, nb);
-
-        // pass 0 (entry-parallel): lanes j, j + WB, ... evaluate entry j's
-        // box and conic cull, each on 4 / (32 / WB) rows of the block; the
-        // masks are then transposed to per-pixel entry bits
-        uint32_t bm = 0u, cm = 0u;
-        {
-            constexpr int NR = 4 * WB / 32;
-            const int je = lane % WB;
-            const int pj = __shfl_sync(FULL, my, je);
-            if (je < nb) {
-                bm = block_lanes(sm.rec[je], bu, bv);
-                if (bm) cm = conics ? conic_rows<NR>(conics[pj], bu, bv, NR * (lane / WB)) & bm : bm;
-            }
-#pragma unroll
-            for (int o = WB; o < 32; o <<= 1) cm |= __shfl_xor_sync(FULL, cm, o);
-        }
+    // Batch of up to WB queued entries: stage their records, run the coarse
+    // test on each pixel's culled-in candidates (pass 1), then the exact
+    // test, ring and compositing in stream order (pass 2).
+    auto run_batch = [&](int nb) {
+        load_batch_ids(sm.rec, recs, sm.qprim, nb);
         uint32_t cand = 0u;
-        for (int j = 0; j < nb; ++j) cand |= ((__shfl_sync(FULL, cm, j) >> lane) & 1u) << j;
+        for (int j = 0; j < nb; ++j) cand |= ((sm.qmask[j] >> lane) & 1u) << j;
         if (!alive) cand = 0u;
-        if (out.counters) {                           // algorithmic work: in-box candidates
-            uint32_t inbox = 0u;                      // (shuffles outside the select)
-            for (int j = 0; j < nb; ++j) inbox |= ((__shfl_sync(FULL, bm, j) >> lane) & 1u) << j;
-            n_box += alive ? __popc(inbox) : 0u;
-        }
 
-        // pass 1: coarse test of every candidate that survived the cull
-        // (two candidates per iteration: their branch-free stage-1 chains
-        // interleave, which hides the SQRT/RCP latencies)
+        // pass 1 (two candidates per iteration: their branch-free stage-1
+        // chains interleave, which hides the SQRT/RCP latencies)
         uint32_t bits = 0u, margb = 0u, secb = 0u;
         uint32_t uni = __reduce_or_sync(FULL, cand);
         while (uni) {
@@ -427,13 +417,13 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
                 }
             }
         }
+        if (out.counters) { n_cand += __popc(cand); n_coarse += __popc(bits); }
 
         // pass 2: exact test, ring and compositing in stream order
-        uint32_t acc = 0u;
         while (bits && alive) {
             const int j = __ffs(bits) - 1;
             bits &= bits - 1;
-            const int p = sm.prim[j];
+            const int p = sm.qprim[j];
             const PrimRec &r = sm.rec[j];
             const double d[3] = {sm.d64[0][lane], sm.d64[1][lane], sm.d64[2][lane]};
             Hit h;
@@ -442,7 +432,6 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
                 continue;
             const float abar = r.alpha * h.G;
             if (abar < c.alpha_floor) continue;
-            acc |= 1u << j;
             n_acc++;
             // fragment payload now, so compositing never re-shades (raster_kernels.py:58-80)
             Pay pin;
@@ -460,18 +449,51 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
             else emit = ring_push_pay(R, sm.pay, lane, h.t64, p, pin, et, ep, pout);
             if (emit) composite(ep, et, pout);
         }
-
-        // record the accepted lanes of every entry for the backward
-        if (out.accept_mask) {
-            uint32_t mine = 0u;
-            for (int j = 0; j < nb; ++j) {
-                const uint32_t m = __ballot_sync(FULL, (acc >> j) & 1u);
-                if (lane == j) mine = m;
-            }
-            if (lane < nb) out.accept_mask[mask_index(start, n, blk, b0 - start + lane)] = mine;
-        }
         __syncwarp();
+    };
+
+    // Stream the tile's depth-sorted list 32 entries at a time, one per lane
+    // (pass 0): pixel box and conic cull of the entry on all 32 block pixels,
+    // restricted to live pixels; entries that keep a pixel join the queue in
+    // stream order, and every WB queued entries run as one batch.
+    const int start = tile_offsets[tile], end = tile_offsets[tile + 1];
+    int qn = 0;
+    for (int b0 = start; b0 < end; b0 += 32) {
+        const uint32_t live = __ballot_sync(FULL, alive);
+        if (!live) break;
+        const int nb = min(32, end - b0);
+        int pj = 0;
+        uint32_t m = 0u;
+        if (lane < nb) {
+            pj = tile_prims[b0 + lane];
+            const ConicRec q = conics[pj];
+            const uint32_t bm = block_lanes(q.bb_u, q.bb_v, bu, bv);
+            if (out.counters) sm.boxw[lane] = bm;
+            if (bm & live) m = (cull ? conic_rows<4>(q, bu, bv, 0) : 0xffffffffu) & bm & live;
+        }
+        if (out.counters) {                           // algorithmic work: in-box candidates
+            __syncwarp();
+            for (int j = 0; j < nb; ++j) n_box += alive ? (sm.boxw[j] >> lane) & 1u : 0u;
+            __syncwarp();
+        }
+        const uint32_t keep = __ballot_sync(FULL, m != 0u);
+        if (m) {
+            const int pos = qn + __popc(keep & ((1u << lane) - 1u));
+            sm.qprim[pos] = pj;
+            sm.qmask[pos] = m;
+        }
+        qn += __popc(keep);
+        __syncwarp();
+        while (qn >= WB) {
+            run_batch(WB);
+            qn -= WB;
+            if (lane < qn) { sm.qprim[lane] = sm.qprim[WB + lane]; sm.qmask[lane] = sm.qmask[WB + lane]; }
+            __syncwarp();
+            if (!__any_sync(FULL, alive)) { qn = 0; break; }
+        }
     }
+    if (qn > 0 && __any_sync(FULL, alive)) run_batch(qn);
+
     while (alive && R.n > 0) {
         double et;
         int ep;
@@ -526,6 +548,8 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         viol += __shfl_xor_sync(FULL, viol, o);
         n_box += __shfl_xor_sync(FULL, n_box, o);
         n_acc += __shfl_xor_sync(FULL, n_acc, o);
+        n_cand += __shfl_xor_sync(FULL, n_cand, o);
+        n_coarse += __shfl_xor_sync(FULL, n_coarse, o);
         nfrag += __shfl_xor_sync(FULL, nfrag, o);
     }
     if (lane == 0) {
@@ -534,6 +558,8 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
             atomicAdd(&out.counters[0], (unsigned long long)n_box);
             atomicAdd(&out.counters[1], (unsigned long long)n_acc);
             atomicAdd(&out.counters[2], (unsigned long long)nfrag);
+            atomicAdd(&out.counters[3], (unsigned long long)n_cand);
+            atomicAdd(&out.counters[4], (unsigned long long)n_coarse);
         }
     }
 }
@@ -828,26 +854,24 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         }
     }
 
-    const int start = tile_offsets[tile], end = tile_offsets[tile + 1], n = end - start;
+    // No log (or a pixel deeper than its capacity): replay the block's
+    // stream with the full candidate test -- the same inline functions as the
+    // forward, so the same accepted set, fp64 depths and ring decisions.
+    const int start = tile_offsets[tile], end = tile_offsets[tile + 1];
     for (int b0 = start; b0 < end; b0 += WB) {
         if (!__any_sync(FULL, alive)) break;
         const int nb = min(WB, end - b0);
-        const uint32_t mymask =
-            lane < nb ? fwd.accept_mask[mask_index(start, n, blk, b0 - start + lane)] : 0u;
-        if (!__any_sync(FULL, mymask != 0u)) continue;   // nothing accepted in this batch
         load_batch32(sm.rec, sm.prim, recs, tile_prims, b0, nb);
         for (int j = 0; j < nb; ++j) {
-            const uint32_t m = __shfl_sync(FULL, mymask, j);
-            if (m == 0u) continue;                    // nobody in this block accepted it
             if (!__any_sync(FULL, alive)) break;
             double et = 0.0;
             int ep = -1;
             bool emit = false;
-            if (alive && (m >> lane & 1u)) {
+            if (alive && in_box(sm.rec[j], u, v)) {
                 const int p = sm.prim[j];
                 double t = 0.0;
-                accept(sm.rec[j], geo[p], d64, dx, dy, dz, c, t);   // same fp64 depth as forward
-                emit = ring_step(c, R, t, p, et, ep);
+                if (accept(sm.rec[j], geo[p], d64, dx, dy, dz, c, t))
+                    emit = ring_step(c, R, t, p, et, ep);
             }
             if (__any_sync(FULL, emit)) emit_grad(emit, ep, et);
         }

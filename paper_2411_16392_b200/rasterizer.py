@@ -231,7 +231,6 @@ class RenderTargets:
     n_fragments: torch.Tensor
     violations: torch.Tensor      # per tile (int32)
     aux: torch.Tensor             # (12, H, W) float64 blend sums for the backward
-    accept_mask: torch.Tensor = None   # (n_pairs * 8,) accepted-lane masks for the backward
     frag_prim: torch.Tensor = None     # fragment log (blocks, cap, 32) int32 primitive ids
     frag_t: torch.Tensor = None        # fragment log (blocks, cap, 32) float64 depths
 
@@ -356,7 +355,8 @@ def prepare(prims, cam, settings: RenderSettings = None, validate=True) -> Prepa
 
 def forward(prep: PreparedView, keep_aux=True, counters=None) -> RenderTargets:
     """rasterizer.py:198-227.  `counters` (optional uint64/int64 CUDA tensor of
-    3) accumulates [in-box candidates, accepted fragments, composited]."""
+    5) accumulates [in-box candidates, accepted fragments, composited,
+    candidates after the conic cull, candidates passing the coarse test]."""
     cam = prep.cam
     H, W = int(cam.height), int(cam.width)
     device = prep.prep.device
@@ -373,9 +373,6 @@ def forward(prep: PreparedView, keep_aux=True, counters=None) -> RenderTargets:
     for k in _MAPS + ("violations",):
         setattr(t, k, _ptr(getattr(tg, k)))
     t.aux = _ptr(tg.aux) if keep_aux else None
-    tg.accept_mask = (torch.empty((max(prep.n_pairs, 1) * 8,), dtype=torch.int32, device=device)
-                      if keep_aux else None)
-    t.accept_mask = _ptr(tg.accept_mask)
     if keep_aux:
         blocks = prep.tiles_x * prep.tiles_y * 8
         cap = int(min(FRAG_CAP, FRAG_LOG_BYTES // (blocks * 32 * 12)))
@@ -417,10 +414,9 @@ def kernel_grads(prep: PreparedView, targets: RenderTargets, upstream, kg=None) 
     t = _lib.Targets()
     for k in _MAPS + ("violations",):
         setattr(t, k, _ptr(getattr(targets, k)))
-    if targets.aux.dim() != 3 or targets.accept_mask is None:
+    if targets.aux.dim() != 3:
         raise ValueError("backward needs forward(prep, keep_aux=True)")
     t.aux = _ptr(targets.aux)
-    t.accept_mask = _ptr(targets.accept_mask)
     if targets.frag_prim is not None:
         t.frag_prim, t.frag_t = _ptr(targets.frag_prim), _ptr(targets.frag_t)
         t.frag_cap = targets.frag_prim.shape[1]

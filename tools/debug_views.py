@@ -28,7 +28,7 @@ for v, cam in enumerate(sc.cams):
     prep = rz.prepare(dev, cam, st)
     torch.cuda.synchronize()
     print(f"view {v} prepare ok pairs={prep.n_pairs} {time.time() - t0:.3f}s", flush=True)
-    cnt = torch.zeros(3, dtype=torch.int64, device="cuda") if a.counters else None
+    cnt = torch.zeros(5, dtype=torch.int64, device="cuda") if a.counters else None
     tg = rz.forward(prep, counters=cnt)
     torch.cuda.synchronize()
     print(f"view {v} forward ok max_frag={int(tg.n_fragments.max())} cnt={None if cnt is None else cnt.tolist()} {time.time() - t0:.3f}s", flush=True)
