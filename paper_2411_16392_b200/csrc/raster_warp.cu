@@ -35,7 +35,6 @@
 namespace qgs {
 
 constexpr int WB = 16;        // entries per batch (8, 16 or 32; 16 measured best on C3)
-constexpr int NBLK = 8;       // 8x4 blocks per 16x16 tile
 constexpr unsigned FULL = 0xffffffffu;
 
 struct FwdSmem {
