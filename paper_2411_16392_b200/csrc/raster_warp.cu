@@ -30,6 +30,8 @@
 // emitted fragment's 22 kernel-level gradient slots across lanes that emitted
 // the same primitive (match_any + shared-memory transpose) before one float
 // atomic per slot.
+#include <cuda_pipeline.h>
+
 #include "shade.cuh"
 
 namespace qgs {
@@ -37,7 +39,14 @@ namespace qgs {
 constexpr int WB = 16;        // entries per batch (8, 16 or 32; 16 measured best on C3)
 constexpr unsigned FULL = 0xffffffffu;
 
+// Geo64 head read by the exact test (ohat, M, wv: its first 15 doubles)
+struct __align__(16) GeoHead {
+    double v[16];
+};
+static_assert(offsetof(Geo64, wv) + 3 * sizeof(double) <= sizeof(GeoHead), "GeoHead covers ohat, M, wv");
+
 struct FwdSmem {
+    GeoHead geoh[WB];
     PrimRec rec[WB];
     int prim[WB];
     int qprim[WB + 32];       // culled-in entries waiting for the coarse/exact passes
@@ -377,6 +386,19 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
     // test, ring and compositing in stream order (pass 2).
     auto run_batch = [&](int nb) {
         load_batch_ids(sm.rec, recs, sm.qprim, nb);
+        // geometry heads for the exact pass, copied asynchronously under pass 1
+        {
+            const char *gsrc = reinterpret_cast<const char *>(geo);
+            char *gdst = reinterpret_cast<char *>(sm.geoh);
+#pragma unroll
+            for (int it = 0; it < WB / 4; ++it) {
+                const int j = it * 4 + (lane >> 3), q = lane & 7;
+                if (j < nb)
+                    __pipeline_memcpy_async(gdst + j * sizeof(GeoHead) + 16 * q,
+                                            gsrc + (size_t)sm.qprim[j] * sizeof(Geo64) + 16 * q, 16);
+            }
+            __pipeline_commit();
+        }
         uint32_t cand = 0u;
         for (int j = 0; j < nb; ++j) cand |= ((sm.qmask[j] >> lane) & 1u) << j;
         if (!alive) cand = 0u;
@@ -418,15 +440,19 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         }
         if (out.counters) { n_cand += __popc(cand); n_coarse += __popc(bits); }
 
+        __pipeline_wait_prior(0);
+        __syncwarp();
+
         // pass 2: exact test, ring and compositing in stream order
         while (bits && alive) {
             const int j = __ffs(bits) - 1;
             bits &= bits - 1;
             const int p = sm.qprim[j];
             const PrimRec &r = sm.rec[j];
+            const Geo64 &gh = *reinterpret_cast<const Geo64 *>(&sm.geoh[j]);   // head only
             const double d[3] = {sm.d64[0][lane], sm.d64[1][lane], sm.d64[2][lane]};
             Hit h;
-            if (!hit_exact_from(r, geo[p], d, dx, dy, dz, c.euclid, c.t_clip, sm.tfirst[j][lane],
+            if (!hit_exact_from(r, gh, d, dx, dy, dz, c.euclid, c.t_clip, sm.tfirst[j][lane],
                                 (secb >> j) & 1u, (margb >> j) & 1u, h))
                 continue;
             const float abar = r.alpha * h.G;
