@@ -56,7 +56,8 @@ def build(force=False, verbose=False):
         obj = os.path.join(OBJ, unit.replace(".cu", ".o"))
         objs.append(obj)
         if force or _stale(obj, [src] + hdrs):
-            cmd = [nvcc(), *ARCH, *COMMON, *flags, "-c", src, "-o", obj]
+            extra = os.environ.get("QGS_NVCC_EXTRA", "").split()   # experiments only
+            cmd = [nvcc(), *ARCH, *COMMON, *flags, *extra, "-c", src, "-o", obj]
             if verbose:
                 print(" ".join(cmd))
             subprocess.check_call(cmd)

@@ -247,12 +247,17 @@ __device__ __forceinline__ void ring_pop_pay(Ring &R, float (*pay)[5][32], int l
 
 enum { A_C0 = 0, A_A = 3, A_D = 4, A_D2 = 5, A_N0 = 6, A_K = 9, A_DIST = 10 };
 
+// row stride of the backward's reduction buffer: 28 floats (112 B) puts the
+// 16-byte stores of 8 consecutive lanes in distinct bank groups (24 would
+// put every 4th lane on the same banks)
+constexpr int KGP = 28;
+
 struct BwdSmem {
     PrimRec rec[WB];
     int prim[WB];
     double ring_t[RING][32];
     int ring_p[RING][32];
-    float red[1][33][KG];   // row 32 stays zero (padding reads of the group sums)
+    float red[1][33][KGP];  // row 32 stays zero (padding reads of the group sums)
 };
 
 struct Cfg {
@@ -738,7 +743,7 @@ __device__ __forceinline__ void frag_grad(const PrimRec &r, const Frag &f, float
 // lane = 6 * set + q sums float4 slot q (slots 4q .. 4q+3) of the set-th
 // pending group over its members and issues one 16-byte vector atomic
 // (sm_90+ red.global.add.v4.f32): 6 atomics per group instead of 22.
-__device__ __forceinline__ void warp_accumulate(float (*red)[33][KG], bool emit, int prim,
+__device__ __forceinline__ void warp_accumulate(float (*red)[33][KGP], bool emit, int prim,
                                                 const float g[KG], float *__restrict__ kg)
 {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -752,7 +757,7 @@ __device__ __forceinline__ void warp_accumulate(float (*red)[33][KG], bool emit,
     unsigned leaders = __ballot_sync(FULL, emit && (peers & ((1u << lane) - 1u)) == 0);
     __syncwarp();
     const int set = lane / 6, q = lane - 6 * set;
-    const float4 (*red4)[KG / 4] = reinterpret_cast<const float4 (*)[KG / 4]>(red[w]);
+    const float4 (*red4)[KGP / 4] = reinterpret_cast<const float4 (*)[KGP / 4]>(red[w]);
     while (leaders) {
         unsigned L = leaders;
         for (int k = 0; k < set && L; ++k) L &= L - 1;
@@ -771,7 +776,11 @@ __device__ __forceinline__ void warp_accumulate(float (*red)[33][KG], bool emit,
                 b.x += y.x; b.y += y.y; b.z += y.z; b.w += y.w;
             }
             a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+#ifndef QGS_EXP_NO_ATOMICS
             atomicAdd(reinterpret_cast<float4 *>(kg + (size_t)gp * KG) + q, a);
+#else       // experiment: reduction without the global atomics
+            if (a.x == 1234.5f) kg[gp] = a.y;
+#endif
         }
     }
     __syncwarp();
@@ -852,7 +861,18 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
             T *= 1.0 - f.abar64;
             if (T < c.t_term) alive = false;
         }
+#if defined(QGS_EXP_DIRECT_ATOMICS)
+        if (emit) {
+            float4 *dst = reinterpret_cast<float4 *>(kg + (size_t)ep * KG);
+#pragma unroll
+            for (int q = 0; q < KG / 4; ++q)
+                atomicAdd(dst + q, make_float4(g[4 * q], g[4 * q + 1], g[4 * q + 2], g[4 * q + 3]));
+        }
+#elif !defined(QGS_EXP_NO_REDUCE)
         warp_accumulate(sm.red, emit, ep, g, kg);
+#else   // experiment: no cross-lane reduction
+        if (emit) { float z = 0.f; for (int q = 0; q < KG; ++q) z += g[q]; if (z == 1234.5f) kg[ep] = z; }
+#endif
     };
 
     // Fragment log written by the forward: the composited sequence of every
