@@ -17,7 +17,7 @@
 // order is (key ascending, prim ascending), a total order.
 //
 // Compiled with -fmad=false (keys must round exactly as the reference).
-#include "qgs_common.cuh"
+#include "shade.cuh"   // coarse_stage1 (the fp32 pre-reject of the key kernel)
 
 namespace qgs {
 
@@ -166,13 +166,21 @@ __global__ void pixel_rays_kernel(CamK cam, double *rays)
     rays[3 * (size_t)i + 2] = cz;
 }
 
-// One warp per primitive; lanes stride over the primitive's tiles.
-__global__ void pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
-                                const double *__restrict__ rays, int32_t *cursor, uint64_t *bucket)
+// One warp per primitive; lanes stride over the primitive's tiles (row-major
+// inside its box).  Per pair: the clamped vertex pixel of the tile, its ray
+// from the table, an fp32 pre-reject (coarse_stage1: roots of the ray
+// quadric and the ellipse test, widened, with a near-tangent band) that
+// settles rays which cannot hit the support -- key = centre distance --
+// and otherwise the float64 key with the reference's operation order.
+__global__ void __launch_bounds__(256, 3)
+pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
+                const double *__restrict__ rays, int32_t *cursor, uint64_t *bucket)
 {
     (void)n_pairs;
     const int lane = threadIdx.x & 31;
     const int warps = gridDim.x * (blockDim.x >> 5);
+    const bool euclid = st.euclid != 0;
+    const float t_clip32 = (float)st.t_clip;
     for (int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); p < P; p += warps) {
         const int nt = pv.ntiles[p];
         if (nt == 0) continue;
@@ -180,12 +188,30 @@ __global__ void pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, S
         const int tx0 = b.x / TILE, ty0 = b.z / TILE;
         const int ncols = b.y / TILE - tx0 + 1;
         const Geo64 &g = pv.geo[p];
+        const PrimRec &r = pv.rec[p];
+        const bool planar = g.planar != 0.0;
+        const long long iu_v = (long long)floor(g.vert_u), iv_v = (long long)floor(g.vert_v);
+        int row = lane / ncols, col = lane - row * ncols;
+        const int drow = 32 / ncols, dcol = 32 - drow * ncols;
         for (int local = lane; local < nt; local += 32) {
-            const int row = local / ncols;
-            const int tile = (ty0 + row) * cam.tiles_x + tx0 + (local - row * ncols);
-            const double key = tile_key_geo(g, tile, cam, st.euclid != 0, st.t_clip, rays);
+            const int tx = tx0 + col, ty = ty0 + row;
+            const int tile = ty * cam.tiles_x + tx;
+            const long long ulo = tx * TILE, uhi = min(cam.W, tx * TILE + TILE) - 1;
+            const long long vlo = ty * TILE, vhi = min(cam.H, ty * TILE + TILE) - 1;
+            const long long iu = iu_v < ulo ? ulo : (iu_v > uhi ? uhi : iu_v);
+            const long long iv = iv_v < vlo ? vlo : (iv_v > vhi ? vhi : iv_v);
+            const double *ray = rays + 3 * ((size_t)iv * cam.W + iu);
+            const double cx = ray[0], cy = ray[1], cz = ray[2];
+            float roots[2], hx, hy;
+            const unsigned cr = coarse_stage1(r, (float)cx, (float)cy, (float)cz, t_clip32, roots, hx, hy);
+            const double key = cr == 0u ? g.dist
+                                        : key_from_ray64(g.ohat, g.M, g.wv, g.sv, planar, g.dist, cx,
+                                                         cy, cz, euclid, st.t_clip);
             const int slot = atomicAdd(&cursor[tile], 1);
             bucket[slot] = ((uint64_t)key_hi(key) << 32) | (uint32_t)p;
+            col += dcol;
+            row += drow;
+            if (col >= ncols) { col -= ncols; ++row; }
         }
     }
 }

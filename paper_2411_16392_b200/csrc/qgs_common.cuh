@@ -265,6 +265,20 @@ __device__ inline void pixel_ray64(const CamK &cam, int u, int v, double &cx, do
     cx = ddx / nrm; cy = ddy / nrm; cz = 1.0 / nrm;
 }
 
+// tile_sort_depths' key for one unit camera ray (cx, cy, cz): the depth of
+// the selected hit, else the centre distance (raster_kernels.py:700-716)
+__device__ inline double key_from_ray64(const double *ohat, const double *M, const double *wv,
+                                        const double *sv, bool planar, double dist, double cx,
+                                        double cy, double cz, bool euclid, double t_clip)
+{
+    double dx = M[0] * cx + M[1] * cy + M[2] * cz;
+    double dy = M[3] * cx + M[4] * cy + M[5] * cz;
+    double dz = M[6] * cx + M[7] * cy + M[8] * cz;
+    double t;
+    if (hit_depth64(wv, sv, ohat, dx, dy, dz, planar, euclid, t_clip, t)) return t;
+    return dist;
+}
+
 // `dirtab` (optional): the W*H*3 table of pixel_ray64, bit-identical.
 __device__ inline double tile_key64(const double *ohat, const double *M, const double *wv,
                                     const double *sv, bool planar, double vu, double vv,
@@ -284,12 +298,7 @@ __device__ inline double tile_key64(const double *ohat, const double *M, const d
     } else {
         pixel_ray64(cam, (int)iu, (int)iv, cx, cy, cz);
     }
-    double dx = M[0] * cx + M[1] * cy + M[2] * cz;
-    double dy = M[3] * cx + M[4] * cy + M[5] * cz;
-    double dz = M[6] * cx + M[7] * cy + M[8] * cz;
-    double t;
-    if (hit_depth64(wv, sv, ohat, dx, dy, dz, planar, euclid, t_clip, t)) return t;
-    return dist;
+    return key_from_ray64(ohat, M, wv, sv, planar, dist, cx, cy, cz, euclid, t_clip);
 }
 
 __device__ inline double tile_key_geo(const Geo64 &g, int tile, const CamK &cam, bool euclid,

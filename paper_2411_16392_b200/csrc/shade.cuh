@@ -159,7 +159,7 @@ __device__ __forceinline__ bool confirm_root(const PrimRec &r, const Geo64 &g, c
 // Near-tangent rays: the fp32 discriminant is within its rounding band of
 // zero, so root existence is decided in fp64 with the reference's own closed
 // form (intersect.py:39-55).  Rare.
-__device__ __noinline__ bool hit_marginal(const PrimRec &r, const Geo64 &g, const double d64[3],
+static __device__ __noinline__ bool hit_marginal(const PrimRec &r, const Geo64 &g, const double d64[3],
                                           bool euclid, float t_clip, Hit &h)
 {
     double dh[3];
