@@ -17,7 +17,7 @@
 // order is (key ascending, prim ascending), a total order.
 //
 // Compiled with -fmad=false (keys must round exactly as the reference).
-#include "shade.cuh"   // coarse_stage1 (the fp32 pre-reject of the key kernel)
+#include "qgs_common.cuh"
 
 namespace qgs {
 
@@ -168,10 +168,9 @@ __global__ void pixel_rays_kernel(CamK cam, double *rays)
 
 // One warp per primitive; lanes stride over the primitive's tiles (row-major
 // inside its box).  Per pair: the clamped vertex pixel of the tile, its ray
-// from the table, an fp32 pre-reject (coarse_stage1: roots of the ray
-// quadric and the ellipse test, widened, with a near-tangent band) that
-// settles rays which cannot hit the support -- key = centre distance --
-// and otherwise the float64 key with the reference's operation order.
+// from the table and the float64 key with the reference's operation order.
+// (An fp32 pre-reject of rays that cannot hit the support was measured
+// slower: most pairs' vertex-nearest pixel does hit.)
 __global__ void __launch_bounds__(256, 3)
 pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
                 const double *__restrict__ rays, int32_t *cursor, uint64_t *bucket)
@@ -180,7 +179,6 @@ pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
     const int lane = threadIdx.x & 31;
     const int warps = gridDim.x * (blockDim.x >> 5);
     const bool euclid = st.euclid != 0;
-    const float t_clip32 = (float)st.t_clip;
     for (int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); p < P; p += warps) {
         const int nt = pv.ntiles[p];
         if (nt == 0) continue;
@@ -188,30 +186,39 @@ pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
         const int tx0 = b.x / TILE, ty0 = b.z / TILE;
         const int ncols = b.y / TILE - tx0 + 1;
         const Geo64 &g = pv.geo[p];
-        const PrimRec &r = pv.rec[p];
         const bool planar = g.planar != 0.0;
         const long long iu_v = (long long)floor(g.vert_u), iv_v = (long long)floor(g.vert_v);
         int row = lane / ncols, col = lane - row * ncols;
         const int drow = 32 / ncols, dcol = 32 - drow * ncols;
-        for (int local = lane; local < nt; local += 32) {
-            const int tx = tx0 + col, ty = ty0 + row;
-            const int tile = ty * cam.tiles_x + tx;
+        // software pipeline: the tile's cursor atomic and the next pair's
+        // ray load are issued before the current key's fp64 work
+        auto pixel_of = [&](int tx, int ty) -> size_t {
             const long long ulo = tx * TILE, uhi = min(cam.W, tx * TILE + TILE) - 1;
             const long long vlo = ty * TILE, vhi = min(cam.H, ty * TILE + TILE) - 1;
             const long long iu = iu_v < ulo ? ulo : (iu_v > uhi ? uhi : iu_v);
             const long long iv = iv_v < vlo ? vlo : (iv_v > vhi ? vhi : iv_v);
-            const double *ray = rays + 3 * ((size_t)iv * cam.W + iu);
-            const double cx = ray[0], cy = ray[1], cz = ray[2];
-            float roots[2], hx, hy;
-            const unsigned cr = coarse_stage1(r, (float)cx, (float)cy, (float)cz, t_clip32, roots, hx, hy);
-            const double key = cr == 0u ? g.dist
-                                        : key_from_ray64(g.ohat, g.M, g.wv, g.sv, planar, g.dist, cx,
-                                                         cy, cz, euclid, st.t_clip);
+            return (size_t)iv * cam.W + iu;
+        };
+        double cx = 0.0, cy = 0.0, cz = 0.0;
+        if (lane < nt) {
+            const double *ray = rays + 3 * pixel_of(tx0 + col, ty0 + row);
+            cx = ray[0]; cy = ray[1]; cz = ray[2];
+        }
+        for (int local = lane; local < nt; local += 32) {
+            const int tile = (ty0 + row) * cam.tiles_x + tx0 + col;
             const int slot = atomicAdd(&cursor[tile], 1);
-            bucket[slot] = ((uint64_t)key_hi(key) << 32) | (uint32_t)p;
             col += dcol;
             row += drow;
             if (col >= ncols) { col -= ncols; ++row; }
+            double nx = 0.0, ny = 0.0, nz = 0.0;
+            if (local + 32 < nt) {
+                const double *ray = rays + 3 * pixel_of(tx0 + col, ty0 + row);
+                nx = ray[0]; ny = ray[1]; nz = ray[2];
+            }
+            const double key = key_from_ray64(g.ohat, g.M, g.wv, g.sv, planar, g.dist, cx, cy, cz,
+                                              euclid, st.t_clip);
+            bucket[slot] = ((uint64_t)key_hi(key) << 32) | (uint32_t)p;
+            cx = nx; cy = ny; cz = nz;
         }
     }
 }
