@@ -42,6 +42,21 @@ def env_rank():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
+def traffic_bytes(kernel):
+    """DRAM bytes (read + write) per launch of `kernel` from the newest committed
+    `ncu --set full` capture (profiles/*_traffic.json, tools/round_summarize.sh),
+    or None.  One launch = one view here, like the roofline's achieved figure."""
+    import glob
+    files = sorted(glob.glob(os.path.join(HERE, "profiles", "*_traffic.json")))
+    if not files:
+        return None
+    with open(files[-1]) as f:
+        t = json.load(f)
+    e = t.get(kernel + "_kernel")
+    return None if e is None else {"bytes_per_launch": e["dram_bytes"],
+                                   "source": os.path.relpath(files[-1], HERE)}
+
+
 def load_peaks():
     p = os.path.join(HERE, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -252,7 +267,7 @@ def run_ours(a):
         "sfu_frac": S / t_k / PSF,
         "roof_frac": max(F / P32, S / PSF) / t_k,
         "kernel_ms_per_step": kms, "fwd_ms_per_step": fwd_ms, "bwd_ms_per_step": bwd_ms,
-        "traffic": None,
+        "traffic": traffic_bytes(dom),
         "peak_source": f"fp32/mufu measured live (tools/peaks.cu); hbm {peaks_kind} "
                        f"MEASURED_PEAKS.json {peaks['hbm_gbs']} GB/s",
         "step_roofline_ms": T_roof * 1e3,
