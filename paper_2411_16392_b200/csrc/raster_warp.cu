@@ -36,6 +36,14 @@
 
 namespace qgs {
 
+// minimum resident warps per SM the register allocation must allow
+#ifndef QGS_BWD_MIN_BLOCKS
+#define QGS_BWD_MIN_BLOCKS 20
+#endif
+#ifndef QGS_FWD_MIN_BLOCKS
+#define QGS_FWD_MIN_BLOCKS 12
+#endif
+
 constexpr int WB = 16;        // entries per batch (8, 16 or 32; 16 measured best on C3)
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -324,7 +332,7 @@ __device__ __forceinline__ void shade_emitted(const PrimRec &r, const Geo64 &g, 
 
 // ================================================================ forward
 
-__global__ void __launch_bounds__(32, 16)
+__global__ void __launch_bounds__(32, QGS_FWD_MIN_BLOCKS)
 raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
                   const ConicRec *__restrict__ conics, const int32_t *__restrict__ tile_offsets,
                   const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets out)
@@ -786,7 +794,7 @@ __device__ __forceinline__ void warp_accumulate(float (*red)[33][KGP], bool emit
     __syncwarp();
 }
 
-__global__ void __launch_bounds__(32, 16)
+__global__ void __launch_bounds__(32, QGS_BWD_MIN_BLOCKS)
 raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
                   const int32_t *__restrict__ tile_offsets,
                   const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets fwd,
