@@ -270,43 +270,85 @@ __device__ inline ConicRec bounding_conic(const double s[3], bool planar, bool e
     m[0] = cam.fx * mc[0] + cam.cx * mc[2];
     m[1] = cam.fy * mc[1] + cam.cy * mc[2];
     m[2] = mc[2];
-    // translate so pixel (u, v) centre = (u0 + U, v0 + V), u0 = uc + 0.5
-    const double u0 = (double)conic_uc(q) + 0.5, v0 = (double)conic_vc(q) + 0.5;
-    for (int k = 0; k < 3; ++k) {
-        Mq[0][k] -= u0 * Mq[2][k];
-        Mq[1][k] -= v0 * Mq[2][k];
+    // Normalised pixel conic about pixel-centre origin (u0, v0): Q(U, V) =
+    // A U^2 + B U V + C V^2 + D U + E V + F <= 0 inside, U = (pixel centre u) - u0
+    double Q6[6];
+    auto conic_about = [&](double u0, double v0) -> bool {
+        double Mt[3][3], mt[3];
+        for (int k = 0; k < 3; ++k) {
+            Mt[0][k] = Mq[0][k] - u0 * Mq[2][k];
+            Mt[1][k] = Mq[1][k] - v0 * Mq[2][k];
+            Mt[2][k] = Mq[2][k];
+        }
+        mt[0] = m[0] - u0 * m[2];
+        mt[1] = m[1] - v0 * m[2];
+        mt[2] = m[2];
+        double D[3][3];
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j)
+                D[i][j] = Mt[i][0] * Mt[j][0] + Mt[i][1] * Mt[j][1] + Mt[i][2] * Mt[j][2] - mt[i] * mt[j];
+        // point conic = adjugate of the dual conic
+        const double P00 = D[1][1] * D[2][2] - D[1][2] * D[2][1];
+        const double P01 = D[0][2] * D[2][1] - D[0][1] * D[2][2];
+        const double P02 = D[0][1] * D[1][2] - D[0][2] * D[1][1];
+        const double P11 = D[0][0] * D[2][2] - D[0][2] * D[2][0];
+        const double P12 = D[0][2] * D[1][0] - D[0][0] * D[1][2];
+        const double P22 = D[0][0] * D[1][1] - D[0][1] * D[1][0];
+        // inside must be negative: evaluate at the projected centre
+        const double cu = mt[0] / mt[2], cv = mt[1] / mt[2];
+        const double at_c = P00 * cu * cu + 2.0 * P01 * cu * cv + P11 * cv * cv + 2.0 * P02 * cu +
+                            2.0 * P12 * cv + P22;
+        const double nrm = fmax(fabs(P00), fabs(P11));
+        if (!(nrm > 0.0) || !(P00 * P11 - P01 * P01 > 0.0)) return false;   // not an ellipse
+        const double k = (at_c > 0.0 ? -1.0 : 1.0) / nrm;
+        Q6[0] = P00 * k; Q6[1] = 2.0 * P01 * k; Q6[2] = P11 * k;
+        Q6[3] = 2.0 * P02 * k; Q6[4] = 2.0 * P12 * k; Q6[5] = P22 * k;
+        return Q6[0] > 0.0 && Q6[2] > 0.0;
+    };
+    // 1. about the reference box centre: the ellipse's own pixel bounds
+    //    (centre from grad Q = 0, half extents sqrt(-Q(c) C / det), sqrt(-Q(c) A / det)),
+    //    one pixel of slack each side, intersected with the reference box
+    double uc = (double)conic_uc(q), vc = (double)conic_vc(q);
+    if (!conic_about(uc + 0.5, vc + 0.5)) return q;
+    {
+        const double A = Q6[0], B = Q6[1], C = Q6[2], Dd = Q6[3], E = Q6[4], F = Q6[5];
+        const double det2 = 4.0 * A * C - B * B;
+        if (!(det2 > 0.0)) return q;
+        const double U0 = (B * E - 2.0 * C * Dd) / det2, V0 = (B * Dd - 2.0 * A * E) / det2;
+        const double kq = -(A * U0 * U0 + B * U0 * V0 + C * V0 * V0 + Dd * U0 + E * V0 + F);
+        if (!(kq > 0.0)) return q;
+        const double hu = sqrt(kq * 4.0 * C / det2), hv = sqrt(kq * 4.0 * A / det2);
+        // pixel index u has centre u + 0.5 = uc + 0.5 + U
+        const double lo_u = floor(uc + U0 - hu) - 1.0, hi_u = ceil(uc + U0 + hu) + 1.0;
+        const double lo_v = floor(vc + V0 - hv) - 1.0, hi_v = ceil(vc + V0 + hv) + 1.0;
+        if (!(isfinite(lo_u) && isfinite(hi_u) && isfinite(lo_v) && isfinite(hi_v))) return q;
+        const long long b0 = max(box[0], (long long)fmax(lo_u, -1.0)), b1 = min(box[1], (long long)fmin(hi_u, 1e9));
+        const long long b2 = max(box[2], (long long)fmax(lo_v, -1.0)), b3 = min(box[3], (long long)fmin(hi_v, 1e9));
+        if (b0 > b1 || b2 > b3) {            // nothing in the reference box can be accepted
+            q.bb_u = 0xffffu; q.bb_v = 0xffffu;
+            return q;
+        }
+        q.bb_u = (uint32_t)b0 | ((uint32_t)b1 << 16);
+        q.bb_v = (uint32_t)b2 | ((uint32_t)b3 << 16);
     }
-    m[0] -= u0 * m[2];
-    m[1] -= v0 * m[2];
-    double D[3][3];
-    for (int i = 0; i < 3; ++i)
-        for (int j = 0; j < 3; ++j)
-            D[i][j] = Mq[i][0] * Mq[j][0] + Mq[i][1] * Mq[j][1] + Mq[i][2] * Mq[j][2] - m[i] * m[j];
-    // point conic = adjugate of the dual conic
-    double P00 = D[1][1] * D[2][2] - D[1][2] * D[2][1];
-    double P01 = D[0][2] * D[2][1] - D[0][1] * D[2][2];
-    double P02 = D[0][1] * D[1][2] - D[0][2] * D[1][1];
-    double P11 = D[0][0] * D[2][2] - D[0][2] * D[2][0];
-    double P12 = D[0][2] * D[1][0] - D[0][0] * D[1][2];
-    double P22 = D[0][0] * D[1][1] - D[0][1] * D[1][0];
-    // inside must be negative: evaluate at the projected centre
-    const double cu = m[0] / m[2], cv = m[1] / m[2];
-    const double at_c = P00 * cu * cu + 2.0 * P01 * cu * cv + P11 * cv * cv + 2.0 * P02 * cu +
-                        2.0 * P12 * cv + P22;
-    const double sg = at_c > 0.0 ? -1.0 : 1.0;
-    const double nrm = fmax(fabs(P00), fabs(P11));
-    if (!(nrm > 0.0) || !(P00 * P11 - P01 * P01 > 0.0)) return q;   // not an ellipse: no cull
-    const double k = sg / nrm;
-    const double A = P00 * k, B = 2.0 * P01 * k, C = P11 * k, Dd = 2.0 * P02 * k,
-                 E = 2.0 * P12 * k, F = P22 * k;
-    const double hu = 0.5 * (double)(box[1] - box[0]) + 1.0, hv = 0.5 * (double)(box[3] - box[2]) + 1.0;
-    const double mag = fabs(A) * hu * hu + fabs(B) * hu * hv + fabs(C) * hv * hv + fabs(Dd) * hu +
-                       fabs(E) * hv + fabs(F);
-    q.A = (float)A; q.B = (float)B; q.C = (float)C; q.D = (float)Dd; q.E = (float)E;
-    q.F = (float)(F - 2e-5 * mag);
+    // 2. the conic again about the culled box's centre, with the fp32 margin
+    uc = (double)conic_uc(q); vc = (double)conic_vc(q);
+    if (!conic_about(uc + 0.5, vc + 0.5)) {
+        q.bb_u = (uint32_t)box[0] | ((uint32_t)box[1] << 16);      // no cull after all
+        q.bb_v = (uint32_t)box[2] | ((uint32_t)box[3] << 16);
+        return q;
+    }
+    const double hu = 0.5 * (double)((q.bb_u >> 16) - (q.bb_u & 0xffffu)) + 1.0;
+    const double hv = 0.5 * (double)((q.bb_v >> 16) - (q.bb_v & 0xffffu)) + 1.0;
+    const double mag = fabs(Q6[0]) * hu * hu + fabs(Q6[1]) * hu * hv + fabs(Q6[2]) * hv * hv +
+                       fabs(Q6[3]) * hu + fabs(Q6[4]) * hv + fabs(Q6[5]);
+    q.A = (float)Q6[0]; q.B = (float)Q6[1]; q.C = (float)Q6[2]; q.D = (float)Q6[3]; q.E = (float)Q6[4];
+    q.F = (float)(Q6[5] - 2e-5 * mag);
     if (!isfinite(q.A + q.B + q.C + q.D + q.E + q.F)) {
         q.A = q.B = q.C = q.D = q.E = 0.f;
         q.F = -1.f;
+        q.bb_u = (uint32_t)box[0] | ((uint32_t)box[1] << 16);
+        q.bb_v = (uint32_t)box[2] | ((uint32_t)box[3] << 16);
     }
     return q;
 }

@@ -59,6 +59,8 @@ struct FwdSmem {
     int prim[WB];
     int qprim[WB + 32];       // culled-in entries waiting for the coarse/exact passes
     uint32_t qmask[WB + 32];  // their conic & box & alive pixel masks
+    int aprim[64];            // box-overlapping entries waiting for the conic test
+    uint32_t amask[64];       // their box & alive pixel masks
     uint32_t boxw[32];        // work counters only: pixel-box masks of the window
     double ring_t[RING][32];  // per-lane ring, [slot][lane]: conflict-free
     int ring_p[RING][32];
@@ -490,29 +492,33 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         __syncwarp();
     };
 
-    // Stream the tile's depth-sorted list 32 entries at a time, one per lane
-    // (pass 0): pixel box and conic cull of the entry on all 32 block pixels,
-    // restricted to live pixels; entries that keep a pixel join the queue in
-    // stream order, and every WB queued entries run as one batch.
+    // Pass 0, two levels, both in stream order.  (a) The tile's depth-sorted
+    // list is streamed 32 entries per window, one per lane: the entry's
+    // culled pixel box (ConicRec) against the block and the live pixels;
+    // overlapping entries join queue A.  (b) Every 32 entries of queue A are
+    // conic-tested on all 32 block pixels, one entry per lane; entries that
+    // keep a pixel join queue B, and every WB entries of queue B run as one
+    // batch.
     const int start = tile_offsets[tile], end = tile_offsets[tile + 1];
-    int qn = 0;
-    for (int b0 = start; b0 < end; b0 += 32) {
-        const uint32_t live = __ballot_sync(FULL, alive);
-        if (!live) break;
-        const int nb = min(32, end - b0);
-        int pj = 0;
-        uint32_t m = 0u;
-        if (lane < nb) {
-            pj = tile_prims[b0 + lane];
-            const ConicRec q = conics[pj];
-            const uint32_t bm = block_lanes(q.bb_u, q.bb_v, bu, bv);
-            if (out.counters) sm.boxw[lane] = bm;
-            if (bm & live) m = (cull ? conic_rows<4>(q, bu, bv, 0) : 0xffffffffu) & bm & live;
+    int qn = 0, an = 0;
+    auto drain_b = [&]() {
+        while (qn >= WB) {
+            run_batch(WB);
+            qn -= WB;
+            if (lane < qn) { sm.qprim[lane] = sm.qprim[WB + lane]; sm.qmask[lane] = sm.qmask[WB + lane]; }
+            __syncwarp();
+            if (!__any_sync(FULL, alive)) { qn = 0; an = 0; return false; }
         }
-        if (out.counters) {                           // algorithmic work: in-box candidates
-            __syncwarp();
-            for (int j = 0; j < nb; ++j) n_box += alive ? (sm.boxw[j] >> lane) & 1u : 0u;
-            __syncwarp();
+        return true;
+    };
+    auto conic_pass = [&](int na) {            // queue A entries [0, na) -> queue B
+        const uint32_t live = __ballot_sync(FULL, alive);
+        uint32_t m = 0u;
+        int pj = 0;
+        if (lane < na) {
+            pj = sm.aprim[lane];
+            m = sm.amask[lane] & live;
+            if (m && cull) m &= conic_rows<4>(conics[pj], bu, bv, 0);
         }
         const uint32_t keep = __ballot_sync(FULL, m != 0u);
         if (m) {
@@ -522,13 +528,49 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         }
         qn += __popc(keep);
         __syncwarp();
-        while (qn >= WB) {
-            run_batch(WB);
-            qn -= WB;
-            if (lane < qn) { sm.qprim[lane] = sm.qprim[WB + lane]; sm.qmask[lane] = sm.qmask[WB + lane]; }
-            __syncwarp();
-            if (!__any_sync(FULL, alive)) { qn = 0; break; }
+    };
+    for (int b0 = start; b0 < end; b0 += 32) {
+        const uint32_t live = __ballot_sync(FULL, alive);
+        if (!live) break;
+        const int nb = min(32, end - b0);
+        int pj = 0;
+        uint32_t bm = 0u;
+        if (lane < nb) {
+            pj = tile_prims[b0 + lane];
+            if (cull) {
+                const uint2 bb = *reinterpret_cast<const uint2 *>(&conics[pj].bb_u);
+                bm = block_lanes(bb.x, bb.y, bu, bv);
+            } else {
+                bm = block_lanes(recs[pj].bb_u, recs[pj].bb_v, bu, bv);
+            }
+            if (out.counters)                  // algorithmic work: the reference's pixel box
+                sm.boxw[lane] = cull ? block_lanes(recs[pj].bb_u, recs[pj].bb_v, bu, bv) : bm;
+            bm &= live;
         }
+        if (out.counters) {
+            __syncwarp();
+            for (int j = 0; j < nb; ++j) n_box += alive ? (sm.boxw[j] >> lane) & 1u : 0u;
+            __syncwarp();
+        }
+        const uint32_t keep = __ballot_sync(FULL, bm != 0u);
+        if (bm) {
+            const int pos = an + __popc(keep & ((1u << lane) - 1u));
+            sm.aprim[pos] = pj;
+            sm.amask[pos] = bm;
+        }
+        an += __popc(keep);
+        __syncwarp();
+        if (an >= 32) {
+            conic_pass(32);
+            an -= 32;
+            if (lane < an) { sm.aprim[lane] = sm.aprim[32 + lane]; sm.amask[lane] = sm.amask[32 + lane]; }
+            __syncwarp();
+            if (!drain_b()) break;
+        }
+    }
+    if (an > 0 && __any_sync(FULL, alive)) {
+        conic_pass(an);
+        drain_b();
     }
     if (qn > 0 && __any_sync(FULL, alive)) run_batch(qn);
 
