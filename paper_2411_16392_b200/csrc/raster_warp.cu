@@ -53,8 +53,14 @@ struct __align__(16) GeoHead {
 };
 static_assert(offsetof(Geo64, wv) + 3 * sizeof(double) <= sizeof(GeoHead), "GeoHead covers ohat, M, wv");
 
+#ifndef QGS_FWD_STAGE_GEO
+#define QGS_FWD_STAGE_GEO 1
+#endif
+
 struct FwdSmem {
+#if QGS_FWD_STAGE_GEO
     GeoHead geoh[WB];
+#endif
     PrimRec rec[WB];
     int prim[WB];
     int qprim[WB + 32];       // culled-in entries waiting for the coarse/exact passes
@@ -402,6 +408,7 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
     auto run_batch = [&](int nb) {
         load_batch_ids(sm.rec, recs, sm.qprim, nb);
         // geometry heads for the exact pass, copied asynchronously under pass 1
+#if QGS_FWD_STAGE_GEO
         {
             const char *gsrc = reinterpret_cast<const char *>(geo);
             char *gdst = reinterpret_cast<char *>(sm.geoh);
@@ -414,6 +421,7 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
             }
             __pipeline_commit();
         }
+#endif
         uint32_t cand = 0u;
         for (int j = 0; j < nb; ++j) cand |= ((sm.qmask[j] >> lane) & 1u) << j;
         if (!alive) cand = 0u;
@@ -455,8 +463,10 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         }
         if (out.counters) { n_cand += __popc(cand); n_coarse += __popc(bits); }
 
+#if QGS_FWD_STAGE_GEO
         __pipeline_wait_prior(0);
         __syncwarp();
+#endif
 
         // pass 2: exact test, ring and compositing in stream order
         while (bits && alive) {
@@ -464,7 +474,11 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
             bits &= bits - 1;
             const int p = sm.qprim[j];
             const PrimRec &r = sm.rec[j];
+#if QGS_FWD_STAGE_GEO
             const Geo64 &gh = *reinterpret_cast<const Geo64 *>(&sm.geoh[j]);   // head only
+#else
+            const Geo64 &gh = geo[p];
+#endif
             const double d[3] = {sm.d64[0][lane], sm.d64[1][lane], sm.d64[2][lane]};
             Hit h;
             if (!hit_exact_from(r, gh, d, dx, dy, dz, c.euclid, c.t_clip, sm.tfirst[j][lane],
