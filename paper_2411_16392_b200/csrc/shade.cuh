@@ -158,9 +158,13 @@ __device__ __forceinline__ bool confirm_root(const PrimRec &r, const Geo64 &g, c
 
 // Near-tangent rays: the fp32 discriminant is within its rounding band of
 // zero, so root existence is decided in fp64 with the reference's own closed
-// form (intersect.py:39-55).  Rare.
-static __device__ __noinline__ bool hit_marginal(const PrimRec &r, const Geo64 &g, const double d64[3],
-                                          bool euclid, float t_clip, Hit &h)
+// form (intersect.py:39-55).  Rare, so kept out of line; it returns only the
+// accepted root (or -1) -- the caller re-confirms it inline, so its Hit stays
+// in registers (a Hit passed by address to an out-of-line call would live in
+// local memory on the hot path).
+static __device__ __noinline__ double marginal_root(const PrimRec &r, const Geo64 &g,
+                                                    const double d64[3], bool euclid,
+                                                    float t_clip)
 {
     double dh[3];
     local_dir64(g, d64, dh);
@@ -172,20 +176,31 @@ static __device__ __noinline__ bool hit_marginal(const PrimRec &r, const Geo64 &
     double roots[2];
     int cnt;
     if (fabs(A) < 1e-6) {
-        if (fabs(B) < 1e-12) return false;
+        if (fabs(B) < 1e-12) return -1.0;
         roots[0] = -C / B;
         cnt = 1;
     } else {
         const double disc = B * B - 4.0 * A * C;
-        if (disc < 0.0) return false;
+        if (disc < 0.0) return -1.0;
         const double sa = A > 0.0 ? 1.0 : -1.0, sq = sqrt(disc);
         roots[0] = (-B - sa * sq) / (2.0 * A);
         roots[1] = (-B + sa * sq) / (2.0 * A);
         cnt = disc == 0.0 ? 1 : 2;
     }
+    Hit h;
     for (int k = 0; k < cnt; ++k)
-        if (confirm_root(r, g, dh, roots[k], false, euclid, t_clip, h)) return true;
-    return false;
+        if (confirm_root(r, g, dh, roots[k], false, euclid, t_clip, h)) return roots[k];
+    return -1.0;
+}
+
+__device__ __forceinline__ bool hit_marginal(const PrimRec &r, const Geo64 &g, const double d64[3],
+                                             bool euclid, float t_clip, Hit &h)
+{
+    const double t = marginal_root(r, g, d64, euclid, t_clip);
+    if (!(t > 0.0)) return false;
+    double dh[3];
+    local_dir64(g, d64, dh);
+    return confirm_root(r, g, dh, t, false, euclid, t_clip, h);
 }
 
 // Coarse fp32 stage (the per-candidate hot path).  Returns a mask: bit k set
