@@ -57,6 +57,7 @@ static_assert(offsetof(Geo64, wv) + 3 * sizeof(double) <= sizeof(GeoHead), "GeoH
 #define QGS_FWD_STAGE_GEO 1
 #endif
 
+
 struct FwdSmem {
 #if QGS_FWD_STAGE_GEO
     GeoHead geoh[WB];
@@ -469,23 +470,22 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
 #endif
 
         // pass 2: exact test, ring and compositing in stream order
-        while (bits && alive) {
-            const int j = __ffs(bits) - 1;
-            bits &= bits - 1;
-            const int p = sm.qprim[j];
-            const PrimRec &r = sm.rec[j];
+        const double d[3] = {sm.d64[0][lane], sm.d64[1][lane], sm.d64[2][lane]};
+        auto exact = [&](int j, Hit &h) -> bool {
 #if QGS_FWD_STAGE_GEO
             const Geo64 &gh = *reinterpret_cast<const Geo64 *>(&sm.geoh[j]);   // head only
 #else
-            const Geo64 &gh = geo[p];
+            const Geo64 &gh = geo[sm.qprim[j]];
 #endif
-            const double d[3] = {sm.d64[0][lane], sm.d64[1][lane], sm.d64[2][lane]};
-            Hit h;
-            if (!hit_exact_from(r, gh, d, dx, dy, dz, c.euclid, c.t_clip, sm.tfirst[j][lane],
-                                (secb >> j) & 1u, (margb >> j) & 1u, h))
-                continue;
+            const PrimRec &r = sm.rec[j];
+            return hit_exact_from(r, gh, d, dx, dy, dz, c.euclid, c.t_clip, sm.tfirst[j][lane],
+                                  (secb >> j) & 1u, (margb >> j) & 1u, h) &&
+                   r.alpha * h.G >= c.alpha_floor;
+        };
+        auto accept_one = [&](int j, const Hit &h) {
+            const int p = sm.qprim[j];
+            const PrimRec &r = sm.rec[j];
             const float abar = r.alpha * h.G;
-            if (abar < c.alpha_floor) continue;
             n_acc++;
             // fragment payload now, so compositing never re-shades (raster_kernels.py:58-80)
             Pay pin;
@@ -502,6 +502,12 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
             if (!c.resort) { et = h.t64; ep = p; pout = pin; emit = true; }
             else emit = ring_push_pay(R, sm.pay, lane, h.t64, p, pin, et, ep, pout);
             if (emit) composite(ep, et, pout);
+        };
+        while (bits && alive) {
+            const int j = __ffs(bits) - 1;
+            bits &= bits - 1;
+            Hit h;
+            if (exact(j, h)) accept_one(j, h);
         }
         __syncwarp();
     };
