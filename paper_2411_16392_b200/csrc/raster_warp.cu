@@ -41,10 +41,16 @@ namespace qgs {
 #define QGS_BWD_MIN_BLOCKS 20
 #endif
 #ifndef QGS_FWD_MIN_BLOCKS
-#define QGS_FWD_MIN_BLOCKS 12
+#define QGS_FWD_MIN_BLOCKS 16
 #endif
 
-constexpr int WB = 16;        // entries per batch (8, 16 or 32; 16 measured best on C3)
+#ifndef QGS_WB
+#define QGS_WB 4
+#endif
+#ifndef QGS_FWD_RAY_REGS
+#define QGS_FWD_RAY_REGS 0    // fp64 pixel ray in registers instead of shared memory
+#endif
+constexpr int WB = QGS_WB;    // queued entries per batch (4, 8 or 16: smem per warp vs batch overhead; 4 measured best)
 constexpr unsigned FULL = 0xffffffffu;
 
 // Geo64 head read by the exact test (ohat, M, wv: its first 15 doubles)
@@ -71,7 +77,9 @@ struct FwdSmem {
     uint32_t boxw[32];        // work counters only: pixel-box masks of the window
     double ring_t[RING][32];  // per-lane ring, [slot][lane]: conflict-free
     int ring_p[RING][32];
+#if !QGS_FWD_RAY_REGS
     double d64[3][32];        // fp64 pixel ray (only the exact path reads it)
+#endif
     double acc[11][32];       // fp64 blend sums, touched once per composited fragment
     float pay[RING][5][32];   // ring payload: abar, camera normal (3), curvature
     float tfirst[WB][32];     // pass 1 -> pass 2: first coarse root that survived
@@ -355,12 +363,12 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
     const Cfg c = make_cfg(st);
     const bool cull = st.no_cull == 0;
     float dx, dy, dz;
-    {
-        double d[3] = {0.0, 0.0, 1.0};
-        if (inside) pixel_dir64(cam, u, v, d);
-        sm.d64[0][lane] = d[0]; sm.d64[1][lane] = d[1]; sm.d64[2][lane] = d[2];
-        dx = (float)d[0]; dy = (float)d[1]; dz = (float)d[2];
-    }
+    double ray64[3] = {0.0, 0.0, 1.0};
+    if (inside) pixel_dir64(cam, u, v, ray64);
+#if !QGS_FWD_RAY_REGS
+    sm.d64[0][lane] = ray64[0]; sm.d64[1][lane] = ray64[1]; sm.d64[2][lane] = ray64[2];
+#endif
+    dx = (float)ray64[0]; dy = (float)ray64[1]; dz = (float)ray64[2];
 #pragma unroll
     for (int k = 0; k < 11; ++k) sm.acc[k][lane] = 0.0;
 
@@ -470,7 +478,11 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
 #endif
 
         // pass 2: exact test, ring and compositing in stream order
+#if QGS_FWD_RAY_REGS
+        const double d[3] = {ray64[0], ray64[1], ray64[2]};
+#else
         const double d[3] = {sm.d64[0][lane], sm.d64[1][lane], sm.d64[2][lane]};
+#endif
         auto exact = [&](int j, Hit &h) -> bool {
 #if QGS_FWD_STAGE_GEO
             const Geo64 &gh = *reinterpret_cast<const Geo64 *>(&sm.geoh[j]);   // head only
