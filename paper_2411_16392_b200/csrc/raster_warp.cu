@@ -41,14 +41,14 @@ namespace qgs {
 #define QGS_BWD_MIN_BLOCKS 20
 #endif
 #ifndef QGS_FWD_MIN_BLOCKS
-#define QGS_FWD_MIN_BLOCKS 16
+#define QGS_FWD_MIN_BLOCKS 18
 #endif
 
 #ifndef QGS_WB
 #define QGS_WB 4
 #endif
 #ifndef QGS_FWD_RAY_REGS
-#define QGS_FWD_RAY_REGS 0    // fp64 pixel ray in registers instead of shared memory
+#define QGS_FWD_RAY_REGS 1    // fp64 pixel ray in registers instead of shared memory
 #endif
 constexpr int WB = QGS_WB;    // queued entries per batch (4, 8 or 16: smem per warp vs batch overhead; 4 measured best)
 constexpr unsigned FULL = 0xffffffffu;
