@@ -170,6 +170,31 @@ __device__ __forceinline__ uint32_t conic_rows(const ConicRec &q, int bu, int bv
     return m;
 }
 
+#ifndef QGS_BWD_VEC_LOADS
+#define QGS_BWD_VEC_LOADS 1
+#endif
+
+__device__ __forceinline__ PrimRec load_rec(const PrimRec *p)
+{
+    PrimRec r;
+    const float4 *src = reinterpret_cast<const float4 *>(p);
+    float4 *dst = reinterpret_cast<float4 *>(&r);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) dst[q] = __ldg(src + q);
+    return r;
+}
+
+// ohat, M, wv (the first 15 doubles) with 16-byte loads; the rest is unset
+__device__ __forceinline__ Geo64 load_geo_head(const Geo64 *p)
+{
+    Geo64 g;
+    const double2 *src = reinterpret_cast<const double2 *>(p);
+    double2 *dst = reinterpret_cast<double2 *>(&g);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) dst[q] = __ldg(src + q);
+    return g;
+}
+
 // Per-lane ring view into shared memory.
 struct Ring {
     double *t;   // &ring_t[0][lane], stride 32
@@ -929,8 +954,16 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         float g[KG];
         if (emit) {
             Frag f;
+#if QGS_BWD_VEC_LOADS
+            // whole records in flight at once (16-byte loads) rather than
+            // field by field as the arithmetic reaches them
+            const PrimRec r = load_rec(recs + ep);
+            const Geo64 gh = load_geo_head(geo + ep);
+#else
             const PrimRec &r = recs[ep];
-            shade_emitted(r, geo[ep], d64, dx, dy, dz, t, c, f);
+            const Geo64 &gh = geo[ep];
+#endif
+            shade_emitted(r, gh, d64, dx, dy, dz, t, c, f);
             const double w = f.abar64 * T;
             const double V = (double)up.c0 * r.col[0] + (double)up.c1 * r.col[1] +
                              (double)up.c2 * r.col[2] + ua64 + (double)up.d * t +
