@@ -171,11 +171,15 @@ __global__ void pixel_rays_kernel(CamK cam, double *rays)
 // from the table and the float64 key with the reference's operation order.
 // (An fp32 pre-reject of rays that cannot hit the support was measured
 // slower: most pairs' vertex-nearest pixel does hit.)
-__global__ void __launch_bounds__(256, 3)
+#ifndef QGS_KEY_MIN_BLOCKS
+#define QGS_KEY_MIN_BLOCKS 3
+#endif
+__global__ void __launch_bounds__(256, QGS_KEY_MIN_BLOCKS)
 pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
                 const double *__restrict__ rays, int32_t *cursor, uint64_t *bucket)
 {
     (void)n_pairs;
+    __shared__ KeyPrim s_kp[8];
     const int lane = threadIdx.x & 31;
     const int warps = gridDim.x * (blockDim.x >> 5);
     const bool euclid = st.euclid != 0;
@@ -186,7 +190,11 @@ pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
         const int tx0 = b.x / TILE, ty0 = b.z / TILE;
         const int ncols = b.y / TILE - tx0 + 1;
         const Geo64 &g = pv.geo[p];
-        const bool planar = g.planar != 0.0;
+        // per-primitive key constants in shared memory (broadcast reads)
+        __syncwarp();
+        if (lane == 0) s_kp[threadIdx.x >> 5] = key_prim(g);
+        __syncwarp();
+        const KeyPrim &kp = s_kp[threadIdx.x >> 5];
         const long long iu_v = (long long)floor(g.vert_u), iv_v = (long long)floor(g.vert_v);
         int row = lane / ncols, col = lane - row * ncols;
         const int drow = 32 / ncols, dcol = 32 - drow * ncols;
@@ -215,8 +223,7 @@ pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
                 const double *ray = rays + 3 * pixel_of(tx0 + col, ty0 + row);
                 nx = ray[0]; ny = ray[1]; nz = ray[2];
             }
-            const double key = key_from_ray64(g.ohat, g.M, g.wv, g.sv, planar, g.dist, cx, cy, cz,
-                                              euclid, st.t_clip);
+            const double key = key_from_ray_fast(kp, cx, cy, cz, euclid, st.t_clip);
             bucket[slot] = ((uint64_t)key_hi(key) << 32) | (uint32_t)p;
             cx = nx; cy = ny; cz = nz;
         }

@@ -279,6 +279,72 @@ __device__ inline double key_from_ray64(const double *ohat, const double *M, con
     return dist;
 }
 
+// hit_depth64 / key_from_ray64 with the per-primitive subexpressions hoisted
+// (identical operations in identical order, so bit-identical keys) and the
+// far root's division done only when the near root is rejected.
+struct KeyPrim {
+    double M[9], ohat[3], w1, w2, iw3, s1, s2, s3;
+    double w1ox, w2oy, C, lim, dist;
+    bool planar;
+};
+
+__device__ inline KeyPrim key_prim(const Geo64 &g)
+{
+    KeyPrim k;
+    for (int i = 0; i < 9; ++i) k.M[i] = g.M[i];
+    for (int i = 0; i < 3; ++i) k.ohat[i] = g.ohat[i];
+    k.w1 = g.wv[0]; k.w2 = g.wv[1]; k.iw3 = g.wv[2];
+    k.s1 = g.sv[0]; k.s2 = g.sv[1]; k.s3 = g.sv[2];
+    const double ox = k.ohat[0], oy = k.ohat[1], oz = k.ohat[2];
+    k.w1ox = k.w1 * ox;
+    k.w2oy = k.w2 * oy;
+    k.C = k.w1 * ox * ox + k.w2 * oy * oy - k.iw3 * oz;
+    const double s1s2 = k.s1 * k.s2;
+    k.lim = 9.0 * s1s2 * s1s2;
+    k.dist = g.dist;
+    k.planar = g.planar != 0.0;
+    return k;
+}
+
+__device__ inline double key_from_ray_fast(const KeyPrim &k, double cx, double cy, double cz,
+                                           bool euclid, double t_clip)
+{
+    const double dx = k.M[0] * cx + k.M[1] * cy + k.M[2] * cz;
+    const double dy = k.M[3] * cx + k.M[4] * cy + k.M[5] * cz;
+    const double dz = k.M[6] * cx + k.M[7] * cy + k.M[8] * cz;
+    const double ox = k.ohat[0], oy = k.ohat[1];
+    if (k.planar) {
+        if (fabs(dz) < 1e-12) return k.dist;
+        const double t = -k.ohat[2] / dz;
+        if (t <= t_clip) return k.dist;
+        const double x = ox + t * dx, y = oy + t * dy;
+        return within_3sigma64(x, y, k.s1, k.s2, 0.0, 0.0, 0.0, true) ? t : k.dist;
+    }
+    const double A = k.w1 * dx * dx + k.w2 * dy * dy;
+    const double B = 2.0 * (k.w1ox * dx + k.w2oy * dy) - k.iw3 * dz;
+    auto try_root = [&](double t) -> bool {
+        if (t <= t_clip) return false;
+        const double x = ox + t * dx, y = oy + t * dy;
+        const double m = (k.s2 * x) * (k.s2 * x) + (k.s1 * y) * (k.s1 * y);
+        if (m > k.lim) return false;
+        return within_3sigma64(x, y, k.s1, k.s2, k.s3, k.w1, k.w2, euclid);
+    };
+    if (fabs(A) < 1e-6) {
+        if (fabs(B) < 1e-12) return k.dist;
+        const double t = -k.C / B;
+        return try_root(t) ? t : k.dist;
+    }
+    const double disc = B * B - 4.0 * A * k.C;
+    if (disc < 0.0) return k.dist;
+    const double sa = A > 0.0 ? 1.0 : -1.0;
+    const double sq = sqrt(disc);
+    const double t0 = (-B - sa * sq) / (2.0 * A);
+    if (try_root(t0)) return t0;
+    if (disc == 0.0) return k.dist;
+    const double t1 = (-B + sa * sq) / (2.0 * A);
+    return try_root(t1) ? t1 : k.dist;
+}
+
 // `dirtab` (optional): the W*H*3 table of pixel_ray64, bit-identical.
 __device__ inline double tile_key64(const double *ohat, const double *M, const double *wv,
                                     const double *sv, bool planar, double vu, double vv,
