@@ -244,10 +244,19 @@ pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
 //      lexsort((prim, key, tile)).  Tiles larger than shared memory are
 //      staged in L2 and ranked in groups of whole buckets loaded into
 //      shared memory.
-constexpr int SORT_T = 512;
+#ifndef QGS_SORT_T
+#define QGS_SORT_T 512
+#endif
+#ifndef QGS_SORT_SMEM_ITEMS
+#define QGS_SORT_SMEM_ITEMS 8192
+#endif
+#ifndef QGS_SORT_MIN_BLOCKS
+#define QGS_SORT_MIN_BLOCKS 2
+#endif
+constexpr int SORT_T = QGS_SORT_T;
 constexpr int SORT_IPT = 4;
 constexpr int SORT_CHUNK = SORT_T * SORT_IPT;     // items per register pass
-constexpr int SORT_SMEM_ITEMS = 8192;             // staged in shared memory up to this
+constexpr int SORT_SMEM_ITEMS = QGS_SORT_SMEM_ITEMS;   // staged in shared memory up to this
 constexpr int SORT_MAX_BUCKETS = 8192;
 
 struct SortSmem {
@@ -330,7 +339,7 @@ __device__ void sort_buckets(SortSmem &sm, const uint64_t *a, int base, int g0, 
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(SORT_T, 2)
+__global__ void __launch_bounds__(SORT_T, QGS_SORT_MIN_BLOCKS)
 tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint64_t *tmp,
                  PrepView pv, CamK cam, SetK st, int32_t *tile_prims)
 {
@@ -489,5 +498,6 @@ __global__ void tile_keys_f64_kernel(int64_t n, const int64_t *pair_tiles,
 }
 
 size_t sort_smem_bytes() { return sizeof(SortSmem); }
+int sort_threads() { return SORT_T; }
 
 }  // namespace qgs

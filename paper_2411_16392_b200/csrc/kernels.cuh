@@ -33,7 +33,7 @@ __global__ void tile_keys_f64_kernel(int64_t n, const int64_t *pair_tiles,
                                      const uint8_t *planar, const double *vu, const double *vv,
                                      const double *dist, CamK cam, SetK st, double *keys);
 size_t sort_smem_bytes();
-constexpr int SORT_THREADS = 512;   // == binning.cu SORT_T
+int sort_threads();                 // binning.cu SORT_T
 
 // raster.cu
 __global__ void raster_fwd_kernel(const PrimRec *recs, const Geo64 *geo, const ConicRec *conics,
