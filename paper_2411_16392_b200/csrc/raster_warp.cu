@@ -866,11 +866,14 @@ __device__ __forceinline__ void warp_accumulate(float (*red)[33][KGP], bool emit
     const int set = lane / 6, q = lane - 6 * set;
     const float4 (*red4)[KGP / 4] = reinterpret_cast<const float4 (*)[KGP / 4]>(red[w]);
     while (leaders) {
-        unsigned L = leaders;
-        for (int k = 0; k < set && L; ++k) L &= L - 1;
-        const int ld = (set < 5 && L) ? __ffs(L) - 1 : -1;
+        // the five lowest pending leaders (warp-uniform), one per lane set
+        int ld = -1;
 #pragma unroll
-        for (int k = 0; k < 5; ++k) leaders &= leaders - 1;
+        for (int k = 0; k < 5; ++k) {
+            const int lk = leaders ? __ffs(leaders) - 1 : -1;
+            ld = set == k ? lk : ld;
+            leaders &= leaders - 1;
+        }
         const unsigned grp = __shfl_sync(FULL, peers, ld < 0 ? 0 : ld);
         const int gp = __shfl_sync(FULL, prim, ld < 0 ? 0 : ld);
         if (ld >= 0) {

@@ -23,6 +23,10 @@
 
 #include "qgs_common.cuh"
 
+#ifndef QGS_NEWTON_EARLY_EXIT
+#define QGS_NEWTON_EARLY_EXIT 0
+#endif
+
 namespace qgs {
 
 struct Hit {
@@ -133,12 +137,19 @@ __device__ __forceinline__ double refine_depth(const Geo64 &g, const double dh[3
     const double w1 = g.wv[0], w2 = g.wv[1], iw3 = g.wv[2];
     const double A = w1 * dh[0] * dh[0] + w2 * dh[1] * dh[1];
     const double Alin = fabs(A) < 1e-6 ? A : 0.0;   // removed on the linear branch
+    double step = 0.0;
 #pragma unroll
     for (int it = 0; it < 3; ++it) {
+#if QGS_NEWTON_EARLY_EXIT
+        // the third step only when the second still moved t by more than
+        // 1e-12 relative (each step contracts the error by >= 1e7)
+        if (it == 2 && !(fabs(step) > 1e-12 * fabs(t))) break;
+#endif
         double x = ox + t * dh[0], y = oy + t * dh[1], z = oz + t * dh[2];
         double F = w1 * x * x + w2 * y * y - iw3 * z - Alin * t * t;
         double Fp = 2.0 * (w1 * x * dh[0] + w2 * y * dh[1]) - iw3 * dh[2] - 2.0 * Alin * t;
-        t -= F * (double)(1.f / (float)Fp);
+        step = F * (double)(1.f / (float)Fp);
+        t -= step;
     }
     return t;
 }
