@@ -62,6 +62,10 @@ static_assert(offsetof(Geo64, wv) + 3 * sizeof(double) <= sizeof(GeoHead), "GeoH
 #ifndef QGS_FWD_STAGE_GEO
 #define QGS_FWD_STAGE_GEO 1
 #endif
+#ifndef QGS_PAY_XY
+#define QGS_PAY_XY 1
+#endif
+constexpr int PAYN = QGS_PAY_XY ? 3 : 5;
 
 
 struct FwdSmem {
@@ -81,12 +85,16 @@ struct FwdSmem {
     double d64[3][32];        // fp64 pixel ray (only the exact path reads it)
 #endif
     double acc[11][32];       // fp64 blend sums, touched once per composited fragment
-    float pay[RING][5][32];   // ring payload: abar, camera normal (3), curvature
+    float pay[RING][PAYN][32];   // ring payload (see Pay)
     float tfirst[WB][32];     // pass 1 -> pass 2: first coarse root that survived
 };
 
+// Ring payload of an accepted fragment.  QGS_PAY_XY: (abar, local hit x, y)
+// -- compositing re-derives the camera normal and curvature from them and
+// the primitive's record (3 floats per slot keep shared memory per warp, the
+// forward's occupancy limiter, low); else (abar, camera normal, curvature).
 struct Pay {
-    float abar, n0, n1, n2, K;
+    float v[PAYN];
 };
 
 // (tile, block) of this CTA and the lane's pixel
@@ -244,15 +252,15 @@ __device__ __forceinline__ void ring_pop(Ring &R, double &et, int &ep)
 }
 
 // forward ring with payload (same ordering rule as ring_push / ring_pop)
-__device__ __forceinline__ bool ring_push_pay(Ring &R, float (*pay)[5][32], int lane, double t,
+__device__ __forceinline__ bool ring_push_pay(Ring &R, float (*pay)[PAYN][32], int lane, double t,
                                               int prim, const Pay &in, double &et, int &ep,
                                               Pay &out)
 {
     if (R.n < RING) {
         R.t[R.n * 32] = t;
         R.p[R.n * 32] = prim;
-        pay[R.n][0][lane] = in.abar; pay[R.n][1][lane] = in.n0; pay[R.n][2][lane] = in.n1;
-        pay[R.n][3][lane] = in.n2; pay[R.n][4][lane] = in.K;
+#pragma unroll
+        for (int f = 0; f < PAYN; ++f) pay[R.n][f][lane] = in.v[f];
         R.n++;
         return false;
     }
@@ -266,16 +274,16 @@ __device__ __forceinline__ bool ring_push_pay(Ring &R, float (*pay)[5][32], int 
     if (t < m) { et = t; ep = prim; out = in; return true; }
     et = m;
     ep = R.p[jm * 32];
-    out.abar = pay[jm][0][lane]; out.n0 = pay[jm][1][lane]; out.n1 = pay[jm][2][lane];
-    out.n2 = pay[jm][3][lane]; out.K = pay[jm][4][lane];
+#pragma unroll
+    for (int f = 0; f < PAYN; ++f) out.v[f] = pay[jm][f][lane];
     R.t[jm * 32] = t;
     R.p[jm * 32] = prim;
-    pay[jm][0][lane] = in.abar; pay[jm][1][lane] = in.n0; pay[jm][2][lane] = in.n1;
-    pay[jm][3][lane] = in.n2; pay[jm][4][lane] = in.K;
+#pragma unroll
+    for (int f = 0; f < PAYN; ++f) pay[jm][f][lane] = in.v[f];
     return true;
 }
 
-__device__ __forceinline__ void ring_pop_pay(Ring &R, float (*pay)[5][32], int lane, double &et,
+__device__ __forceinline__ void ring_pop_pay(Ring &R, float (*pay)[PAYN][32], int lane, double &et,
                                              int &ep, Pay &out)
 {
     double m = R.t[0];
@@ -286,13 +294,13 @@ __device__ __forceinline__ void ring_pop_pay(Ring &R, float (*pay)[5][32], int l
     }
     et = m;
     ep = R.p[jm * 32];
-    out.abar = pay[jm][0][lane]; out.n0 = pay[jm][1][lane]; out.n1 = pay[jm][2][lane];
-    out.n2 = pay[jm][3][lane]; out.K = pay[jm][4][lane];
+#pragma unroll
+    for (int f = 0; f < PAYN; ++f) out.v[f] = pay[jm][f][lane];
     R.n--;
     R.t[jm * 32] = R.t[R.n * 32];
     R.p[jm * 32] = R.p[R.n * 32];
 #pragma unroll
-    for (int f = 0; f < 5; ++f) pay[jm][f][lane] = pay[R.n][f][lane];
+    for (int f = 0; f < PAYN; ++f) pay[jm][f][lane] = pay[R.n][f][lane];
 }
 
 enum { A_C0 = 0, A_A = 3, A_D = 4, A_D2 = 5, A_N0 = 6, A_K = 9, A_DIST = 10 };
@@ -410,7 +418,22 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         const PrimRec &r = recs[ep];
         if (t < last_t - 1e-12) viol++;
         if (t > last_t) last_t = t;
-        const double abar64 = f.abar < 0.f ? c.alpha_clamp64 : (double)f.abar;  // <0: clamped
+        const float fabar = f.v[0];
+#if QGS_PAY_XY
+        float n0, n1, n2, fK;
+        {
+            Hit hh;
+            hh.x = f.v[1];
+            hh.y = f.v[2];
+            hh.branch = (r.flags & 1u) ? BR_PLANAR : BR_QUAD;
+            float nl[3], nc[3], inrm, flip;
+            normal_curv32(r, hh, dx, dy, dz, nl, nc, fK, inrm, flip);
+            n0 = nc[0]; n1 = nc[1]; n2 = nc[2];
+        }
+#else
+        const float n0 = f.v[1], n1 = f.v[2], n2 = f.v[3], fK = f.v[4];
+#endif
+        const double abar64 = fabar < 0.f ? c.alpha_clamp64 : (double)fabar;  // <0: clamped
         const double w = abar64 * T;
         double *a = &sm.acc[0][lane];            // stride 32 doubles per sum
         const double aa = a[A_A * 32], ad = a[A_D * 32], ad2 = a[A_D2 * 32];
@@ -421,10 +444,10 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         a[A_A * 32] = aa + w;
         a[A_D * 32] = ad + w * t;
         a[A_D2 * 32] = ad2 + w * t * t;
-        a[(A_N0 + 0) * 32] += w * (double)f.n0;
-        a[(A_N0 + 1) * 32] += w * (double)f.n1;
-        a[(A_N0 + 2) * 32] += w * (double)f.n2;
-        a[A_K * 32] += w * (double)f.K;
+        a[(A_N0 + 0) * 32] += w * (double)n0;
+        a[(A_N0 + 1) * 32] += w * (double)n1;
+        a[(A_N0 + 2) * 32] += w * (double)n2;
+        a[A_K * 32] += w * (double)fK;
         if (T > 0.5) median = (float)t;
         T *= 1.0 - abar64;
         if (log_on && nfrag < out.frag_cap) {
@@ -526,12 +549,17 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
             n_acc++;
             // fragment payload now, so compositing never re-shades (raster_kernels.py:58-80)
             Pay pin;
+            pin.v[0] = abar > c.alpha_clamp ? -c.alpha_clamp : abar;
+#if QGS_PAY_XY
+            pin.v[1] = h.x;
+            pin.v[2] = h.y;
+#else
             {
                 float nl[3], nc[3], K, inrm, flip;
                 normal_curv32(r, h, dx, dy, dz, nl, nc, K, inrm, flip);
-                pin.abar = abar > c.alpha_clamp ? -c.alpha_clamp : abar;
-                pin.n0 = nc[0]; pin.n1 = nc[1]; pin.n2 = nc[2]; pin.K = K;
+                pin.v[1] = nc[0]; pin.v[2] = nc[1]; pin.v[3] = nc[2]; pin.v[4] = K;
             }
+#endif
             double et;
             int ep;
             Pay pout;
