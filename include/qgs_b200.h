@@ -95,6 +95,9 @@ typedef struct qgs_targets {
                                   raster warp per 8x4 block, 8 per tile (tile-major);
                                   the backward reads it instead of replaying */
     double *frag_t;            /* same layout: float64 depth of each logged fragment */
+    float *frag_xy;            /* optional, same layout x2: the fragment's local hit point
+                                  (x, y) as the forward shaded it; lets the backward re-shade
+                                  in fp32 without the primitive's float64 geometry */
     int32_t frag_cap;          /* fragments logged per pixel; a block with a pixel over
                                   the cap (or no log) is replayed by the backward with
                                   the full candidate test */

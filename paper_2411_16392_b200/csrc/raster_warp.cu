@@ -365,6 +365,9 @@ struct Frag {
 };
 
 // re-shade an emitted fragment at its fp64 depth (raster_kernels.py:40-80)
+__device__ __forceinline__ void finish_frag(const PrimRec &r, float dx, float dy, float dz,
+                                            const Cfg &c, Frag &f);
+
 __device__ __forceinline__ void shade_emitted(const PrimRec &r, const Geo64 &g, const double d64[3],
                                               float dx, float dy, float dz, double t64,
                                               const Cfg &c, Frag &f)
@@ -372,6 +375,13 @@ __device__ __forceinline__ void shade_emitted(const PrimRec &r, const Geo64 &g, 
     double dh[3];
     local_dir64(g, d64, dh);
     shade_at(r, g, dh, t64, c.euclid, f.h);
+    finish_frag(r, dx, dy, dz, c, f);
+}
+
+// weight, alpha and the camera-frame normal of a shaded fragment
+__device__ __forceinline__ void finish_frag(const PrimRec &r, float dx, float dy, float dz,
+                                            const Cfg &c, Frag &f)
+{
     f.h.G = expf(-(f.h.l * f.h.l) / (2.f * f.h.sig * f.h.sig));
     float abar = r.alpha * f.h.G;
     f.clamped = abar > c.alpha_clamp;
@@ -454,6 +464,9 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
             const size_t o = ((size_t)blockIdx.x * out.frag_cap + nfrag) * 32 + lane;
             out.frag_prim[o] = ep;
             out.frag_t[o] = t;
+#if QGS_PAY_XY
+            if (out.frag_xy) reinterpret_cast<float2 *>(out.frag_xy)[o] = make_float2(f.v[1], f.v[2]);
+#endif
         }
         nfrag++;
         if (T < c.t_term) alive = false;
@@ -981,7 +994,7 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
     Ring R{&sm.ring_t[0][lane], &sm.ring_p[0][lane], 0};
     bool alive = inside && has_up;
 
-    auto emit_grad = [&](bool emit, int ep, double t) {
+    auto emit_grad = [&](bool emit, int ep, double t, bool have_xy, float lx, float ly) {
         float g[KG];
         if (emit) {
             Frag f;
@@ -989,12 +1002,20 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
             // whole records in flight at once (16-byte loads) rather than
             // field by field as the arithmetic reaches them
             const PrimRec r = load_rec(recs + ep);
-            const Geo64 gh = load_geo_head(geo + ep);
 #else
             const PrimRec &r = recs[ep];
-            const Geo64 &gh = geo[ep];
 #endif
-            shade_emitted(r, gh, d64, dx, dy, dz, t, c, f);
+            if (have_xy) {                  // logged hit point: fp32 re-shade
+                shade_from_log(r, lx, ly, t, dx, dy, dz, c.euclid, f.h);
+                finish_frag(r, dx, dy, dz, c, f);
+            } else {
+#if QGS_BWD_VEC_LOADS
+                const Geo64 gh = load_geo_head(geo + ep);
+#else
+                const Geo64 &gh = geo[ep];
+#endif
+                shade_emitted(r, gh, d64, dx, dy, dz, t, c, f);
+            }
             const double w = f.abar64 * T;
             const double V = (double)up.c0 * r.col[0] + (double)up.c1 * r.col[1] +
                              (double)up.c2 * r.col[2] + ua64 + (double)up.d * t +
@@ -1028,18 +1049,27 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         const int nf_max = __reduce_max_sync(FULL, nf);
         if (fwd.frag_prim && fwd.frag_t && nf_max <= fwd.frag_cap) {
             const size_t base = (size_t)blockIdx.x * fwd.frag_cap * 32 + lane;
+            const float2 *xy = reinterpret_cast<const float2 *>(fwd.frag_xy);
+            const bool have_xy = xy != nullptr;
             int np_ = -1;
             double nt_ = 0.0;
-            if (0 < nf) { np_ = fwd.frag_prim[base]; nt_ = fwd.frag_t[base]; }
+            float2 nxy = make_float2(0.f, 0.f);
+            if (0 < nf) {
+                np_ = fwd.frag_prim[base]; nt_ = fwd.frag_t[base];
+                if (have_xy) nxy = xy[base];
+            }
             for (int k = 0; k < nf_max; ++k) {
                 const bool emit = k < nf;
                 const int ep = np_;
                 const double et = nt_;
+                const float2 exy = nxy;
                 if (k + 1 < nf) {                // prefetch the next fragment
-                    np_ = fwd.frag_prim[base + (size_t)(k + 1) * 32];
-                    nt_ = fwd.frag_t[base + (size_t)(k + 1) * 32];
+                    const size_t o = base + (size_t)(k + 1) * 32;
+                    np_ = fwd.frag_prim[o];
+                    nt_ = fwd.frag_t[o];
+                    if (have_xy) nxy = xy[o];
                 }
-                emit_grad(emit, ep, et);
+                emit_grad(emit, ep, et, have_xy, exy.x, exy.y);
             }
             return;
         }
@@ -1064,7 +1094,7 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
                 if (accept(sm.rec[j], geo[p], d64, dx, dy, dz, c, t))
                     emit = ring_step(c, R, t, p, et, ep);
             }
-            if (__any_sync(FULL, emit)) emit_grad(emit, ep, et);
+            if (__any_sync(FULL, emit)) emit_grad(emit, ep, et, false, 0.f, 0.f);
         }
         __syncwarp();
     }
@@ -1073,7 +1103,7 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         int ep = -1;
         bool emit = alive && R.n > 0;
         if (emit) ring_pop(R, et, ep);
-        emit_grad(emit, ep, et);
+        emit_grad(emit, ep, et, false, 0.f, 0.f);
     }
 }
 

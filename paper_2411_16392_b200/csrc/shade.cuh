@@ -113,6 +113,40 @@ __device__ __forceinline__ void shade_at(const PrimRec &r, const Geo64 &g, const
     eval_point(r, (float)x, (float)y, planar, euclid, 1.f, h);
 }
 
+// Re-shading of a logged fragment in fp32: the forward's fp32 hit point
+// (x, y) makes rho, theta, l, sigma -- hence G and alpha -- bit-identical to
+// the forward's; dh, z and the root derivative q are re-derived in fp32
+// (gradient-only quantities, ~1e-6 relative).
+__device__ __forceinline__ void shade_from_log(const PrimRec &r, float x, float y, double t64,
+                                               float dx, float dy, float dz, bool euclid, Hit &h)
+{
+    const bool planar = (r.flags & 1u) != 0;
+    const float hx = fmaf(r.M[0], dx, fmaf(r.M[1], dy, r.M[2] * dz));
+    const float hy = fmaf(r.M[3], dx, fmaf(r.M[4], dy, r.M[5] * dz));
+    const float hz = fmaf(r.M[6], dx, fmaf(r.M[7], dy, r.M[8] * dz));
+    h.t64 = t64;
+    h.t = (float)t64;
+    h.dhx = hx; h.dhy = hy; h.dhz = hz;
+    if (planar) {
+        h.branch = BR_PLANAR;
+        h.q = hz;
+        h.z = 0.f;
+    } else {
+        const float A = fmaf(r.w1 * hx, hx, r.w2 * hy * hy);
+        const float Fp = 2.f * fmaf(r.w1 * x, hx, r.w2 * y * hy) - r.iw3 * hz;
+        if (fabsf(A) < 1e-6f) {
+            h.branch = BR_LINEAR;
+            h.q = Fp - 2.f * A * h.t;
+            h.z = fmaf(h.t, hz, r.oz);
+        } else {
+            h.branch = BR_QUAD;
+            h.q = Fp;
+            h.z = r.s3 * fmaf(r.w1 * x, x, r.w2 * y * y);   // on the quadric
+        }
+    }
+    eval_point(r, x, y, planar, euclid, 1.f, h);
+}
+
 __device__ __forceinline__ void local_dir64(const Geo64 &g, const double d[3], double dh[3])
 {
     dh[0] = g.M[0] * d[0] + g.M[1] * d[1] + g.M[2] * d[2];

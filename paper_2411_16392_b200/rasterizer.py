@@ -23,11 +23,12 @@ from .model import ParameterError, PrimitiveSet
 
 T_NEAR_CLIP = 0.01   # intersect.py:22
 TILE = 16            # bounds.py:19
-# Fragment log kept by the forward for the backward: 12 B per logged
-# fragment, at most FRAG_CAP per pixel and FRAG_LOG_BYTES per view (blocks
-# with a deeper pixel are replayed from the accept masks instead).
+# Fragment log kept by the forward for the backward: 20 B per logged
+# fragment (prim, fp64 depth, fp32 local hit point), at most FRAG_CAP per
+# pixel and FRAG_LOG_BYTES per view (blocks with a deeper pixel are replayed
+# with the full candidate test instead).
 FRAG_CAP = 512
-FRAG_LOG_BYTES = 12 << 30
+FRAG_LOG_BYTES = 24 << 30
 
 
 @dataclass
@@ -233,6 +234,7 @@ class RenderTargets:
     aux: torch.Tensor             # (12, H, W) float64 blend sums for the backward
     frag_prim: torch.Tensor = None     # fragment log (blocks, cap, 32) int32 primitive ids
     frag_t: torch.Tensor = None        # fragment log (blocks, cap, 32) float64 depths
+    frag_xy: torch.Tensor = None       # fragment log (blocks, cap, 32, 2) fp32 local hit points
 
     @property
     def order_violations(self):
@@ -375,11 +377,13 @@ def forward(prep: PreparedView, keep_aux=True, counters=None) -> RenderTargets:
     t.aux = _ptr(tg.aux) if keep_aux else None
     if keep_aux:
         blocks = prep.tiles_x * prep.tiles_y * 8
-        cap = int(min(FRAG_CAP, FRAG_LOG_BYTES // (blocks * 32 * 12)))
+        cap = int(min(FRAG_CAP, FRAG_LOG_BYTES // (blocks * 32 * 20)))
         if cap > 0:
             tg.frag_prim = torch.empty((blocks, cap, 32), dtype=torch.int32, device=device)
             tg.frag_t = torch.empty((blocks, cap, 32), dtype=torch.float64, device=device)
+            tg.frag_xy = torch.empty((blocks, cap, 32, 2), dtype=torch.float32, device=device)
             t.frag_prim, t.frag_t, t.frag_cap = _ptr(tg.frag_prim), _ptr(tg.frag_t), cap
+            t.frag_xy = _ptr(tg.frag_xy)
     t.counters = _ptr(counters)
     _lib.check(_lib.load().qgs_forward(_ptr(prep.prep), len(prep.dev), prep._cam_c, prep._st_c,
                                        _ptr(prep.tile_offsets), _ptr(prep.tile_prims), t,
@@ -419,6 +423,7 @@ def kernel_grads(prep: PreparedView, targets: RenderTargets, upstream, kg=None) 
     t.aux = _ptr(targets.aux)
     if targets.frag_prim is not None:
         t.frag_prim, t.frag_t = _ptr(targets.frag_prim), _ptr(targets.frag_t)
+        t.frag_xy = _ptr(targets.frag_xy)
         t.frag_cap = targets.frag_prim.shape[1]
     if kg is None:
         kg = torch.zeros((len(prep.dev), _lib.KG_STRIDE), dtype=torch.float32, device=device)
