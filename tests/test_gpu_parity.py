@@ -175,11 +175,12 @@ def test_backward_replay_fallback(rz, name, mode):
         float((np.abs(a - b) / scale).max())
 
 
-@pytest.mark.parametrize("copies", [5, 40, 300, 700])
+@pytest.mark.parametrize("copies", [5, 40, 300, 700, 8500])
 def test_sort_ties_duplicates(rz, copies):
     """Duplicated primitives give identical (f32 and fp64) keys: the sort must
     still equal lexsort((prim, key, tile)), i.e. break ties by primitive id,
-    through every bucket path (warp bitonic, warp rank count, CTA rank count)."""
+    through every path of the tile sort (shared-memory tile, bucket groups of
+    a large tile, one bucket larger than shared memory)."""
     from oracle import qgs_oracle as qo
     from paper_2411_16392_b200 import scenes
     from paper_2411_16392_b200.model import PrimitiveSet
