@@ -355,6 +355,7 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
         if (threadIdx.x == 0) out[0] = (int32_t)(uint32_t)src[0];
         return;
     }
+    uint64_t *stage = n <= SORT_SMEM_ITEMS ? sm.buf : tmp + start;
     const bool regs = n <= SORT_CHUNK;     // one register pass holds the whole tile
 
     // key range
@@ -418,65 +419,54 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
         }
     }
     __syncthreads();
-    if (n <= SORT_SMEM_ITEMS) {
-        // scatter into buckets in shared memory, then rank
-        for (int c0 = 0; c0 < n; c0 += SORT_CHUNK) {
+    // scatter into buckets
+    for (int c0 = 0; c0 < n; c0 += SORT_CHUNK) {
 #pragma unroll
-            for (int k = 0; k < SORT_IPT; ++k) {
-                const int i = c0 + k * SORT_T + threadIdx.x;
-                if (i < n) {
-                    const uint64_t v = regs ? it[k] : src[i];
-                    const int pos = atomicAdd(&sm.bend[(((uint32_t)(v >> 32)) - kmin) >> shift], 1);
-                    sm.buf[pos] = v;
-                }
+        for (int k = 0; k < SORT_IPT; ++k) {
+            const int i = c0 + k * SORT_T + threadIdx.x;
+            if (i < n) {
+                const uint64_t v = regs ? it[k] : src[i];
+                const int pos = atomicAdd(&sm.bend[(((uint32_t)(v >> 32)) - kmin) >> shift], 1);
+                stage[pos] = v;
             }
         }
-        __syncthreads();
-        sort_buckets(sm, sm.buf, 0, 0, nb, kmin, shift, tile, pv, cam, st, out);
-        return;
     }
-    // Larger tiles: groups of whole buckets holding <= SORT_SMEM_ITEMS items.
-    // Per group, the tile's items (L2-resident) are re-read and those of the
-    // group's buckets scattered straight into shared memory and ranked there
-    // (no staging round trip through L2).  bend holds bucket starts until a
-    // group's scatter turns its entries into bucket ends, which is what
-    // bucket_start() of the later ranks reads.  A single bucket larger than
-    // shared memory (degenerate input) is staged in `tmp` and ranked in place.
-    auto start_of = [&](int d) { return d < nb ? sm.bend[d] : n; };
-    int g0 = 0;
-    while (g0 < nb) {
-        const int base = start_of(g0);
-        int lo = g0 + 1, hi = nb;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (start_of(mid) - base <= SORT_SMEM_ITEMS) lo = mid; else hi = mid - 1;
-        }
-        const int g1 = lo;
-        const int cnt = start_of(g1) - base;
-        const bool big = cnt > SORT_SMEM_ITEMS;        // then g1 == g0 + 1
-        __syncthreads();                               // bend[g0 .. g1] read by all
-        for (int i = threadIdx.x; i < n; i += SORT_T) {
-            const uint64_t v = src[i];
-            const int d = (int)((((uint32_t)(v >> 32)) - kmin) >> shift);
-            if (d >= g0 && d < g1) {
-                const int pos = atomicAdd(&sm.bend[d], 1);
-                if (big) tmp[start + pos] = v;
-                else sm.buf[pos - base] = v;
+    __syncthreads();
+
+    if (n <= SORT_SMEM_ITEMS) {
+        sort_buckets(sm, stage, 0, 0, nb, kmin, shift, tile, pv, cam, st, out);
+    } else {
+        // groups of consecutive buckets that fit in shared memory: one
+        // coalesced bulk load from the L2 staging slice, then warps sort
+        // their buckets out of shared memory
+        int g0 = 0;
+        while (g0 < nb) {
+            const int base = bucket_start(sm, g0);
+            // last bucket end within SORT_SMEM_ITEMS of base (binary search)
+            int lo = g0 + 1, hi = nb;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (sm.bend[mid - 1] - base <= SORT_SMEM_ITEMS) lo = mid; else hi = mid - 1;
             }
-        }
-        __syncthreads();
-        if (big) {
-            const uint64_t *stage = tmp + start;
-            for (int i = base + threadIdx.x; i < base + cnt; i += SORT_T) {
-                const uint64_t x = stage[i];
-                out[base + rank_in_bucket(stage, base, base + cnt, x, tile, pv, cam, st)] =
-                    (int32_t)(uint32_t)x;
+            int g1 = lo;
+            if (sm.bend[g1 - 1] - base > SORT_SMEM_ITEMS) {
+                // one degenerate bucket larger than shared memory: rank it in place
+                const int b1 = sm.bend[g1 - 1];
+                for (int i = base + threadIdx.x; i < b1; i += SORT_T) {
+                    const uint64_t x = stage[i];
+                    out[base + rank_in_bucket(stage, base, b1, x, tile, pv, cam, st)] =
+                        (int32_t)(uint32_t)x;
+                }
+                __syncthreads();
+                g0 = g1;
+                continue;
             }
+            const int cnt = sm.bend[g1 - 1] - base;
+            for (int i = threadIdx.x; i < cnt; i += SORT_T) sm.buf[i] = stage[base + i];
             __syncthreads();
-        } else {
             sort_buckets(sm, sm.buf, base, g0, g1, kmin, shift, tile, pv, cam, st, out);
+            g0 = g1;
         }
-        g0 = g1;
     }
 }
 
