@@ -1005,9 +1005,8 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
 #else
             const PrimRec &r = recs[ep];
 #endif
-            if (have_xy) {                  // logged hit point: fp32 re-shade
-                shade_from_log(r, lx, ly, t, dx, dy, dz, c.euclid, f.h);
-                finish_frag(r, dx, dy, dz, c, f);
+            if (have_xy && shade_from_log(r, lx, ly, t, dx, dy, dz, c.euclid, f.h)) {
+                finish_frag(r, dx, dy, dz, c, f);      // logged hit point: fp32 re-shade
             } else {
 #if QGS_BWD_VEC_LOADS
                 const Geo64 gh = load_geo_head(geo + ep);

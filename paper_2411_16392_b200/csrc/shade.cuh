@@ -116,10 +116,15 @@ __device__ __forceinline__ void shade_at(const PrimRec &r, const Geo64 &g, const
 // Re-shading of a logged fragment in fp32: the forward's fp32 hit point
 // (x, y) makes rho, theta, l, sigma -- hence G and alpha -- bit-identical to
 // the forward's; dh, z and the root derivative q are re-derived in fp32
-// (gradient-only quantities, ~1e-6 relative).
-__device__ __forceinline__ void shade_from_log(const PrimRec &r, float x, float y, double t64,
+// (gradient-only quantities, ~1e-6 relative except q on grazing rays).
+// Returns false when the fp32 root derivative q is ill-conditioned (a
+// grazing ray: |q| below 1e-3 of its terms) or |A| is too close to the
+// linear-branch threshold to trust the fp32 branch; the caller then re-shades
+// that fragment from the float64 geometry.
+__device__ __forceinline__ bool shade_from_log(const PrimRec &r, float x, float y, double t64,
                                                float dx, float dy, float dz, bool euclid, Hit &h)
 {
+    bool ok = true;
     const bool planar = (r.flags & 1u) != 0;
     const float hx = fmaf(r.M[0], dx, fmaf(r.M[1], dy, r.M[2] * dz));
     const float hy = fmaf(r.M[3], dx, fmaf(r.M[4], dy, r.M[5] * dz));
@@ -132,8 +137,15 @@ __device__ __forceinline__ void shade_from_log(const PrimRec &r, float x, float 
         h.q = hz;
         h.z = 0.f;
     } else {
-        const float A = fmaf(r.w1 * hx, hx, r.w2 * hy * hy);
-        const float Fp = 2.f * fmaf(r.w1 * x, hx, r.w2 * y * hy) - r.iw3 * hz;
+        const float a1 = r.w1 * hx * hx, a2 = r.w2 * hy * hy;
+        const float A = a1 + a2;
+        const float t1 = r.w1 * x * hx, t2 = r.w2 * y * hy, t3 = r.iw3 * hz;
+        const float Fp = 2.f * (t1 + t2) - t3;
+        // q well conditioned, and the linear-branch decision |A| < 1e-6
+        // (made in float64 by the forward) not within fp32 reach of a flip
+        // (A cancels on hyperbolic patches: its fp32 error is ~1e-7 of |a1| + |a2|)
+        ok = fabsf(Fp) >= 1e-3f * (2.f * (fabsf(t1) + fabsf(t2)) + fabsf(t3)) &&
+             fabsf(fabsf(A) - 1e-6f) > 1e-6f * (fabsf(a1) + fabsf(a2)) + 1e-12f;
         if (fabsf(A) < 1e-6f) {
             h.branch = BR_LINEAR;
             h.q = Fp - 2.f * A * h.t;
@@ -145,6 +157,7 @@ __device__ __forceinline__ void shade_from_log(const PrimRec &r, float x, float 
         }
     }
     eval_point(r, x, y, planar, euclid, 1.f, h);
+    return ok;
 }
 
 __device__ __forceinline__ void local_dir64(const Geo64 &g, const double d[3], double dh[3])

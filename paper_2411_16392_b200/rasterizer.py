@@ -13,6 +13,7 @@ CUDA stream; the only host synchronisation per view is the read of the
 (tile, primitive) pair count that sizes the sort buffers.
 """
 
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -381,9 +382,10 @@ def forward(prep: PreparedView, keep_aux=True, counters=None) -> RenderTargets:
         if cap > 0:
             tg.frag_prim = torch.empty((blocks, cap, 32), dtype=torch.int32, device=device)
             tg.frag_t = torch.empty((blocks, cap, 32), dtype=torch.float64, device=device)
-            tg.frag_xy = torch.empty((blocks, cap, 32, 2), dtype=torch.float32, device=device)
             t.frag_prim, t.frag_t, t.frag_cap = _ptr(tg.frag_prim), _ptr(tg.frag_t), cap
-            t.frag_xy = _ptr(tg.frag_xy)
+            if not os.environ.get("QGS_NO_FRAG_XY"):   # diagnostic: float64 re-shading
+                tg.frag_xy = torch.empty((blocks, cap, 32, 2), dtype=torch.float32, device=device)
+                t.frag_xy = _ptr(tg.frag_xy)
     t.counters = _ptr(counters)
     _lib.check(_lib.load().qgs_forward(_ptr(prep.prep), len(prep.dev), prep._cam_c, prep._st_c,
                                        _ptr(prep.tile_offsets), _ptr(prep.tile_prims), t,
