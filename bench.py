@@ -153,10 +153,14 @@ def run_ours(a):
     from paper_2411_16392_b200.dist import pipelined_prepare
 
     rank, world, local = env_rank()
+    local = local % torch.cuda.device_count()   # (only the gloo check shares a GPU)
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if a.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:   # functional check of the multi-rank path on a single-GPU box
+            dist.init_process_group(a.dist_backend)
     sc = scene_for(a.config)
     cams = sc.cams
     V = len(cams)
@@ -419,6 +423,8 @@ def main():
     ap.add_argument("--cpu-tiles", type=int, default=96)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo only to exercise the multi-rank path on one GPU")
     a = ap.parse_args()
     if a.warmup < 3:
         a.warmup = 3
