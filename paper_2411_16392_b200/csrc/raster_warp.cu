@@ -181,6 +181,9 @@ __device__ __forceinline__ uint32_t conic_rows(const ConicRec &q, int bu, int bv
 #ifndef QGS_BWD_VEC_LOADS
 #define QGS_BWD_VEC_LOADS 1
 #endif
+#ifndef QGS_RED_SETS
+#define QGS_RED_SETS 10
+#endif
 
 __device__ __forceinline__ PrimRec load_rec(const PrimRec *p)
 {
@@ -904,13 +907,21 @@ __device__ __forceinline__ void warp_accumulate(float (*red)[33][KGP], bool emit
     const unsigned peers = __match_any_sync(FULL, key);
     unsigned leaders = __ballot_sync(FULL, emit && (peers & ((1u << lane) - 1u)) == 0);
     __syncwarp();
+#if QGS_RED_SETS == 10
+    // ten sets of 3 lanes, each lane two float4 slots (q, q + 3)
+    const int set = lane / 3, q = lane - 3 * set;
+    constexpr int NSET = 10;
+#else
+    // five sets of 6 lanes, each lane one float4 slot
     const int set = lane / 6, q = lane - 6 * set;
+    constexpr int NSET = 5;
+#endif
     const float4 (*red4)[KGP / 4] = reinterpret_cast<const float4 (*)[KGP / 4]>(red[w]);
     while (leaders) {
-        // the five lowest pending leaders (warp-uniform), one per lane set
+        // the NSET lowest pending leaders (warp-uniform), one per lane set
         int ld = -1;
 #pragma unroll
-        for (int k = 0; k < 5; ++k) {
+        for (int k = 0; k < NSET; ++k) {
             const int lk = leaders ? __ffs(leaders) - 1 : -1;
             ld = set == k ? lk : ld;
             leaders &= leaders - 1;
@@ -918,6 +929,18 @@ __device__ __forceinline__ void warp_accumulate(float (*red)[33][KGP], bool emit
         const unsigned grp = __shfl_sync(FULL, peers, ld < 0 ? 0 : ld);
         const int gp = __shfl_sync(FULL, prim, ld < 0 ? 0 : ld);
         if (ld >= 0) {
+#if QGS_RED_SETS == 10
+            float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+            for (unsigned mm = grp; mm; mm &= mm - 1) {
+                const int i0 = __ffs(mm) - 1;
+                const float4 x = red4[i0][q], y = red4[i0][q + 3];
+                a.x += x.x; a.y += x.y; a.z += x.z; a.w += x.w;
+                b.x += y.x; b.y += y.y; b.z += y.z; b.w += y.w;
+            }
+            float4 *dst = reinterpret_cast<float4 *>(kg + (size_t)gp * KG);
+            atomicAdd(dst + q, a);
+            atomicAdd(dst + q + 3, b);
+#else
             float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
             for (unsigned mm = grp; mm;) {             // two independent partial sums
                 const int i0 = __ffs(mm) - 1; mm &= mm - 1;
@@ -927,10 +950,7 @@ __device__ __forceinline__ void warp_accumulate(float (*red)[33][KGP], bool emit
                 b.x += y.x; b.y += y.y; b.z += y.z; b.w += y.w;
             }
             a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
-#ifndef QGS_EXP_NO_ATOMICS
             atomicAdd(reinterpret_cast<float4 *>(kg + (size_t)gp * KG) + q, a);
-#else       // experiment: reduction without the global atomics
-            if (a.x == 1234.5f) kg[gp] = a.y;
 #endif
         }
     }
