@@ -315,29 +315,15 @@ def run_e2e(a, rz, sc, mine, device, st, world):
     h2d += sum(t.numel() * 4 for u in ups for t in u.values())
     out_host = None
     side = torch.cuda.Stream(device=device)
-    copy = torch.cuda.Stream(device=device)
 
     def step():
         nonlocal out_host
-        main = torch.cuda.current_stream()
         dev = rz.DevicePrimitives.from_host(host, device, non_blocking=True)
         grads = rz.GradientBuffer.zeros_flat(dev)
-        # every view's upstream maps go up on a copy stream, overlapping the
-        # rasterization of the earlier views
-        copy.wait_stream(main)
-        ups_dev, ready = [], []
-        with torch.cuda.stream(copy):
-            for u in ups:
-                ups_dev.append({k: t.to(device, non_blocking=True) for k, t in u.items()})
-                ev = torch.cuda.Event()
-                ev.record(copy)
-                ready.append(ev)
         for i, v, prep in pipelined_prepare(dev, sc.cams, mine, st, side):
+            up = {k: t.to(device, non_blocking=True) for k, t in ups[i].items()}
             tg = rz.forward(prep)
-            main.wait_event(ready[i])
-            for t in ups_dev[i].values():
-                t.record_stream(main)
-            rz.backward(prep, tg, ups_dev[i], out=grads)
+            rz.backward(prep, tg, up, out=grads)
         if world > 1:
             dist.all_reduce(grads.buffer)
         if out_host is None:
