@@ -65,6 +65,9 @@ static_assert(offsetof(Geo64, wv) + 3 * sizeof(double) <= sizeof(GeoHead), "GeoH
 #ifndef QGS_PAY_XY
 #define QGS_PAY_XY 1
 #endif
+#ifndef QGS_FWD_COMPOSITE_VEC
+#define QGS_FWD_COMPOSITE_VEC 1
+#endif
 constexpr int PAYN = QGS_PAY_XY ? 3 : 5;
 
 
@@ -428,7 +431,11 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
     const bool log_on = out.frag_prim != nullptr && out.frag_t != nullptr;
 
     auto composite = [&](int ep, double t, const Pay &f) {
+#if QGS_FWD_COMPOSITE_VEC
+        const PrimRec r = load_rec(recs + ep);      // all 8 lines of the record in flight
+#else
         const PrimRec &r = recs[ep];
+#endif
         if (t < last_t - 1e-12) viol++;
         if (t > last_t) last_t = t;
         const float fabar = f.v[0];
