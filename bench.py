@@ -42,6 +42,11 @@ def env_rank():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
+def _kg_stride():
+    from paper_2411_16392_b200 import _lib
+    return _lib.KG_STRIDE
+
+
 def traffic_bytes(kernel):
     """DRAM bytes (read + write) per launch of `kernel` from the newest committed
     `ncu --set full` capture (profiles/*_traffic.json, tools/round_summarize.sh),
@@ -184,7 +189,7 @@ def run_ours(a):
             tg = rz.forward(prep, counters=counters if count else None)
             if ev is not None:
                 ev["f1"][i].record(stream)
-            kg = torch.zeros((len(dev), 24), dtype=torch.float32, device=device)
+            kg = torch.zeros((len(dev), _kg_stride()), dtype=torch.float32, device=device)
             if ev is not None:
                 ev["b0"][i].record(stream)
             kg = rz.kernel_grads(prep, tg, ups[i], kg=kg)

@@ -32,7 +32,7 @@ extern "C" {
 typedef struct CUstream_st *qgs_stream_t; /* == cudaStream_t */
 
 #define QGS_TILE 16          /* bounds.py:19 */
-#define QGS_KG_STRIDE 24     /* floats per primitive in the kernel-gradient buffer */
+#define QGS_KG_STRIDE 16     /* floats per primitive in the kernel-gradient buffer */
 #define QGS_AUX_PLANES 12    /* float64 planes per pixel kept for the backward */
 
 enum {
@@ -159,9 +159,10 @@ int qgs_forward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_se
 
 /* ---- stage 4: backward raster (raster_kernels.py:289-681).  kg is
  *      P*QGS_KG_STRIDE floats, zeroed by the caller; slots: ohat 0-2,
- *      X 3-11 (local-frame rotation accumulator, g_R = R X; replaces the
- *      reference's M and Nmat slots), w 12-14 and s 15-17 (with
- *      the lambda terms folded in), alpha 18, colour 19-21. */
+ *      omega 3-5 (the skew part of the local-frame rotation accumulator X,
+ *      g_R = R X, which replaces the reference's M and Nmat slots: the
+ *      quaternion gradient sees only the skew part), w 6-8 and s 9-11 (with
+ *      the lambda terms folded in), alpha 12, colour 13-15. */
 int qgs_backward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settings *st,
                  const int32_t *tile_offsets, const int32_t *tile_prims,
                  const qgs_targets *fwd, const qgs_upstream *up, float *kg,

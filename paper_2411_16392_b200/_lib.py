@@ -11,7 +11,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libqgs_b200.so")
 
-KG_STRIDE = 24
+KG_STRIDE = 16
 AUX_PLANES = 12
 TILE = 16
 

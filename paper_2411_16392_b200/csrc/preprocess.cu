@@ -447,9 +447,9 @@ __global__ void chain_kernel(qgs_params prm, CamK cam, const float *__restrict__
     int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= prm.P) return;
     const float *g = kg + (size_t)p * KG;
-    double gk[22];
+    double gk[KG];
     bool any = false;
-    for (int i = 0; i < 22; ++i) { gk[i] = g[i]; any |= g[i] != 0.f; }
+    for (int i = 0; i < KG; ++i) { gk[i] = g[i]; any |= g[i] != 0.f; }
     if (!any) return;   // no fragment of this primitive was composited
 
     const float *cf = prm.centers + 3 * p;
@@ -477,15 +477,21 @@ __global__ void chain_kernel(qgs_params prm, CamK cam, const float *__restrict__
     }
     out.raw_opacity[p] += (float)(gk[KG_ALPHA] * alpha * (1.0 - alpha));
 
-    // rotation (rasterizer.py:308-311): the raster kernel accumulates
-    // X = sum x_loc (x) g_ohat + dhat (x) dl + g_nl (x) nl, which equals
-    // R^T [R_cw g_M^T + (eye - c) g_ohat^T + R_cw g_Nmat] of the reference,
-    // so g_R = R X.
+    // rotation (rasterizer.py:308-311): the reference's g_R equals R X with
+    // X = sum x_loc (x) g_ohat + dhat (x) dl + g_nl (x) nl
+    // (= R^T [R_cw g_M^T + (eye - c) g_ohat^T + R_cw g_Nmat]).  The raster
+    // kernel accumulates only omega = vee(X - X^T); the symmetric part of X
+    // changes nothing below (it moves R along q, which the normalisation
+    // projects out), so X is replaced by its skew part (X - X^T) / 2.
+    const double om0 = gk[KG_ROT + 0], om1 = gk[KG_ROT + 1], om2 = gk[KG_ROT + 2];
+    const double Xs[9] = {0.0, 0.5 * om2, -0.5 * om1,
+                          -0.5 * om2, 0.0, 0.5 * om0,
+                          0.5 * om1, -0.5 * om0, 0.0};
     double gR[9];
     for (int a = 0; a < 3; ++a)
         for (int b = 0; b < 3; ++b) {
             double acc = 0.0;
-            for (int j = 0; j < 3; ++j) acc += R[3 * a + j] * gk[KG_M + 3 * j + b];
+            for (int j = 0; j < 3; ++j) acc += R[3 * a + j] * Xs[3 * j + b];
             gR[3 * a + b] = acc;
         }
     // quat_rot_backward (model.py:90-110)

@@ -20,8 +20,9 @@ constexpr int RING = 8;             // raster_kernels.py:26 BUFFER_SIZE
 constexpr int KG = QGS_KG_STRIDE;   // kernel-gradient floats per primitive
 constexpr int AUX = QGS_AUX_PLANES;
 
-// kernel-gradient slots (raster_kernels.py:29-37 with Nmat and lambda folded)
-enum { KG_OHAT = 0, KG_M = 3, KG_W = 12, KG_S = 15, KG_ALPHA = 18, KG_COLOR = 19 };
+// kernel-gradient slots (raster_kernels.py:29-37 with M, Nmat folded into the
+// 3-vector omega and lambda into s / w; 16 floats = four 16-byte vectors)
+enum { KG_OHAT = 0, KG_ROT = 3, KG_W = 6, KG_S = 9, KG_ALPHA = 12, KG_COLOR = 13 };
 // fp64 aux planes written by the forward for the backward
 enum { AX_C0 = 0, AX_A = 3, AX_D = 4, AX_D2 = 5, AX_N0 = 6, AX_K = 9, AX_DIST = 10, AX_T = 11 };
 enum { BR_QUAD = 0, BR_LINEAR = 1, BR_PLANAR = 2 };

@@ -185,7 +185,7 @@ __device__ __forceinline__ uint32_t conic_rows(const ConicRec &q, int bu, int bv
 #define QGS_BWD_VEC_LOADS 1
 #endif
 #ifndef QGS_RED_SETS
-#define QGS_RED_SETS 10
+#define QGS_RED_SETS 8
 #endif
 
 __device__ __forceinline__ PrimRec load_rec(const PrimRec *p)
@@ -311,10 +311,10 @@ __device__ __forceinline__ void ring_pop_pay(Ring &R, float (*pay)[PAYN][32], in
 
 enum { A_C0 = 0, A_A = 3, A_D = 4, A_D2 = 5, A_N0 = 6, A_K = 9, A_DIST = 10 };
 
-// row stride of the backward's reduction buffer: 28 floats (112 B) puts the
-// 16-byte stores of 8 consecutive lanes in distinct bank groups (24 would
-// put every 4th lane on the same banks)
-constexpr int KGP = 28;
+// row stride of the backward's reduction buffer: 20 floats (80 B) puts the
+// 16-byte stores of 8 consecutive lanes in distinct bank groups (16 would
+// put every other lane on the same banks)
+constexpr int KGP = KG + 4;
 
 struct BwdSmem {
     PrimRec rec[WB];
@@ -882,17 +882,21 @@ __device__ __forceinline__ void frag_grad(const PrimRec &r, const Frag &f, float
     g[KG_OHAT + 0] = go[0];
     g[KG_OHAT + 1] = go[1];
     g[KG_OHAT + 2] = go[2];
-    // X = x_loc (x) g_ohat + dhat (x) dl + g_nl (x) nl, so that the chain's
-    // rotation gradient is g_R = R X (no cancellation between the ohat and
-    // M = R^T R_cw paths, which are each ~|eye - c| / |x| larger than it).
+    // The chain's rotation gradient is g_R = R X with the local-frame
+    // accumulator X = x_loc (x) g_ohat + dhat (x) dl + g_nl (x) nl (no
+    // cancellation between the ohat and M = R^T R_cw paths, which are each
+    // ~|eye - c| / |x| larger than it).  The quaternion gradient of R(q/|q|)
+    // sees only the skew part of X (its symmetric part moves along q, which
+    // the normalisation projects out), so only
+    // omega = (X12 - X21, X20 - X02, X01 - X10) = x_loc x g_ohat + dhat x dl + g_nl x nl
+    // is accumulated.
     const float xl[3] = {x, y, h.z}, dh3[3] = {hx, hy, hz};
 #pragma unroll
-    for (int j = 0; j < 3; ++j)
-#pragma unroll
-        for (int b = 0; b < 3; ++b)
-            g[KG_M + 3 * j + b] = fmaf(xl[j], go[b], fmaf(dh3[j], dl[b], g_nl[j] * f.nl[b]));
-    g[22] = 0.f;
-    g[23] = 0.f;
+    for (int a = 0; a < 3; ++a) {
+        const int j = (a + 1) % 3, b = (a + 2) % 3;
+        g[KG_ROT + a] = fmaf(xl[j], go[b], -xl[b] * go[j]) + fmaf(dh3[j], dl[b], -dh3[b] * dl[j]) +
+                        fmaf(g_nl[j], f.nl[b], -g_nl[b] * f.nl[j]);
+    }
     (void)dx; (void)dy; (void)dz;
 }
 
@@ -914,14 +918,14 @@ __device__ __forceinline__ void warp_accumulate(float (*red)[33][KGP], bool emit
     const unsigned peers = __match_any_sync(FULL, key);
     unsigned leaders = __ballot_sync(FULL, emit && (peers & ((1u << lane) - 1u)) == 0);
     __syncwarp();
-#if QGS_RED_SETS == 10
-    // ten sets of 3 lanes, each lane two float4 slots (q, q + 3)
-    const int set = lane / 3, q = lane - 3 * set;
-    constexpr int NSET = 10;
+#if QGS_RED_SETS == 16
+    // sixteen sets of 2 lanes, each lane two float4 slots (q, q + 2)
+    const int set = lane >> 1, q = lane & 1;
+    constexpr int NSET = 16;
 #else
-    // five sets of 6 lanes, each lane one float4 slot
-    const int set = lane / 6, q = lane - 6 * set;
-    constexpr int NSET = 5;
+    // eight sets of 4 lanes, each lane one float4 slot
+    const int set = lane >> 2, q = lane & 3;
+    constexpr int NSET = 8;
 #endif
     const float4 (*red4)[KGP / 4] = reinterpret_cast<const float4 (*)[KGP / 4]>(red[w]);
     while (leaders) {
@@ -936,17 +940,17 @@ __device__ __forceinline__ void warp_accumulate(float (*red)[33][KGP], bool emit
         const unsigned grp = __shfl_sync(FULL, peers, ld < 0 ? 0 : ld);
         const int gp = __shfl_sync(FULL, prim, ld < 0 ? 0 : ld);
         if (ld >= 0) {
-#if QGS_RED_SETS == 10
+#if QGS_RED_SETS == 16
             float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
             for (unsigned mm = grp; mm; mm &= mm - 1) {
                 const int i0 = __ffs(mm) - 1;
-                const float4 x = red4[i0][q], y = red4[i0][q + 3];
+                const float4 x = red4[i0][q], y = red4[i0][q + 2];
                 a.x += x.x; a.y += x.y; a.z += x.z; a.w += x.w;
                 b.x += y.x; b.y += y.y; b.z += y.z; b.w += y.w;
             }
             float4 *dst = reinterpret_cast<float4 *>(kg + (size_t)gp * KG);
             atomicAdd(dst + q, a);
-            atomicAdd(dst + q + 3, b);
+            atomicAdd(dst + q + 2, b);
 #else
             float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
             for (unsigned mm = grp; mm;) {             // two independent partial sums
