@@ -264,6 +264,7 @@ struct SortSmem {
     int bend[SORT_MAX_BUCKETS];   // counts -> start cursors -> (after the scatter) bucket ends
     int scan_w[32];
     uint32_t kmin, kmax;
+    int maxcnt;
 };
 
 __device__ __noinline__ double key64_of(uint64_t v, int tile, const PrepView &pv,
@@ -307,6 +308,29 @@ __device__ __forceinline__ int bucket_start(const SortSmem &sm, int d)
     return d == 0 ? 0 : sm.bend[d - 1];
 }
 
+// Bucket of a key: the varying f32 key bits cut linearly (kmin, shift), or --
+// for tiles whose depths cluster so that a linear cut leaves buckets of
+// hundreds of items -- the number of sample splitters <= the key (a sample
+// sort's buckets, balanced whatever the distribution).  Both are monotone in
+// the key, so bucket order is key order.
+constexpr int SORT_SPLIT = 4095;                 // splitters (from a sample of 4096)
+constexpr int SORT_SKEW = 256;                   // largest linear bucket tolerated
+struct BucketFn {
+    uint32_t kmin;
+    int shift;
+    const uint32_t *sp;                          // sorted splitters, or nullptr
+    __device__ __forceinline__ int operator()(uint32_t h) const
+    {
+        if (!sp) return (int)((h - kmin) >> shift);
+        int lo = 0, hi = SORT_SPLIT;             // upper_bound(sp, h)
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (sp[mid] <= h) lo = mid + 1; else hi = mid;
+        }
+        return lo;
+    }
+};
+
 // rank of x among its bucket a[b0, b1): composite compare, with the exact
 // (fp64 key, prim) order only when an equal f32 key is present
 __device__ __forceinline__ int rank_fast(const uint64_t *a, int b0, int b1, uint64_t x, int tile,
@@ -325,13 +349,13 @@ __device__ __forceinline__ int rank_fast(const uint64_t *a, int b0, int b1, uint
 }
 
 __device__ void sort_buckets(SortSmem &sm, const uint64_t *a, int base, int g0, int g1,
-                             uint32_t kmin, int shift, int tile, const PrepView &pv,
+                             const BucketFn &bf, int tile, const PrepView &pv,
                              const CamK &cam, const SetK &st, int32_t *out)
 {
     const int i0 = bucket_start(sm, g0) - base, i1 = bucket_start(sm, g1) - base;
     for (int i = i0 + threadIdx.x; i < i1; i += SORT_T) {
         const uint64_t x = a[i];
-        const int d = (int)((((uint32_t)(x >> 32)) - kmin) >> shift);
+        const int d = bf((uint32_t)(x >> 32));
         const int b0 = bucket_start(sm, d), b1 = sm.bend[d];
         const int r = b1 - b0 == 1 ? 0 : rank_fast(a, b0 - base, b1 - base, x, tile, pv, cam, st);
         out[b0 + r] = (int32_t)(uint32_t)x;
@@ -359,7 +383,7 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
     const bool regs = n <= SORT_CHUNK;     // one register pass holds the whole tile
 
     // key range
-    if (threadIdx.x == 0) { sm.kmin = 0xffffffffu; sm.kmax = 0u; }
+    if (threadIdx.x == 0) { sm.kmin = 0xffffffffu; sm.kmax = 0u; sm.maxcnt = 0; }
     uint64_t it[SORT_IPT];
     uint32_t lmin = 0xffffffffu, lmax = 0u;
     for (int c0 = 0; c0 < n; c0 += SORT_CHUNK) {
@@ -399,6 +423,44 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
         }
     }
     __syncthreads();
+    BucketFn bf{kmin, shift, nullptr};
+    {
+        int mx = 0;
+        for (int d = threadIdx.x; d < nb; d += SORT_T) mx = max(mx, sm.bend[d]);
+        mx = __reduce_max_sync(0xffffffffu, mx);
+        if (lane == 0) atomicMax(&sm.maxcnt, mx);
+    }
+    __syncthreads();
+    if (sm.maxcnt > SORT_SKEW && n > 2 * SORT_SPLIT) {
+        // depths cluster: sample-sort buckets instead.  4096 evenly spaced
+        // keys are sorted in shared memory (bitonic), the 4095 upper ones
+        // become splitters (kept in the upper half of bend) and the
+        // histogram is redone.
+        uint32_t *smp = reinterpret_cast<uint32_t *>(sm.buf);
+        for (int i = threadIdx.x; i < SORT_SPLIT + 1; i += SORT_T)
+            smp[i] = (uint32_t)(src[(size_t)i * n / (SORT_SPLIT + 1)] >> 32);
+        __syncthreads();
+        for (int k = 2; k <= SORT_SPLIT + 1; k <<= 1)
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = threadIdx.x; i < SORT_SPLIT + 1; i += SORT_T) {
+                    const int l = i ^ j;
+                    if (l > i) {
+                        const uint32_t a = smp[i], b = smp[l];
+                        const bool up = (i & k) == 0;
+                        if ((a > b) == up) { smp[i] = b; smp[l] = a; }
+                    }
+                }
+                __syncthreads();
+            }
+        uint32_t *sp = reinterpret_cast<uint32_t *>(sm.bend) + SORT_MAX_BUCKETS / 2 + 1;
+        for (int i = threadIdx.x; i < SORT_SPLIT; i += SORT_T) sp[i] = smp[i + 1];
+        nb = SORT_SPLIT + 1;
+        for (int d = threadIdx.x; d < nb; d += SORT_T) sm.bend[d] = 0;
+        __syncthreads();
+        bf.sp = sp;
+        for (int i = threadIdx.x; i < n; i += SORT_T) atomicAdd(&sm.bend[bf((uint32_t)(src[i] >> 32))], 1);
+        __syncthreads();
+    }
     // exclusive scan of the bucket counts (nb <= 8192 = 16 per thread)
     {
         constexpr int PER = SORT_MAX_BUCKETS / SORT_T;
@@ -426,7 +488,7 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
             const int i = c0 + k * SORT_T + threadIdx.x;
             if (i < n) {
                 const uint64_t v = regs ? it[k] : src[i];
-                const int pos = atomicAdd(&sm.bend[(((uint32_t)(v >> 32)) - kmin) >> shift], 1);
+                const int pos = atomicAdd(&sm.bend[bf((uint32_t)(v >> 32))], 1);
                 stage[pos] = v;
             }
         }
@@ -434,7 +496,7 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
     __syncthreads();
 
     if (n <= SORT_SMEM_ITEMS) {
-        sort_buckets(sm, stage, 0, 0, nb, kmin, shift, tile, pv, cam, st, out);
+        sort_buckets(sm, stage, 0, 0, nb, bf, tile, pv, cam, st, out);
     } else {
         // groups of consecutive buckets that fit in shared memory: one
         // coalesced bulk load from the L2 staging slice, then warps sort
@@ -464,7 +526,7 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
             const int cnt = sm.bend[g1 - 1] - base;
             for (int i = threadIdx.x; i < cnt; i += SORT_T) sm.buf[i] = stage[base + i];
             __syncthreads();
-            sort_buckets(sm, sm.buf, base, g0, g1, kmin, shift, tile, pv, cam, st, out);
+            sort_buckets(sm, sm.buf, base, g0, g1, bf, tile, pv, cam, st, out);
             g0 = g1;
         }
     }
