@@ -162,6 +162,7 @@ int qgs_bin(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settin
     QGS_LAUNCHED("pixel_rays_kernel");
     qgs::pair_key_kernel<<<grid, 256, 0, s>>>(pv, P, n_pairs, ck, sk, ws.rays, ws.cursor, ws.bucket);
     QGS_LAUNCHED("pair_key_kernel");
+    pv.rays = ws.rays;
     qgs::tile_sort_kernel<<<n_tiles, qgs::sort_threads(), qgs::sort_smem_bytes(), s>>>(
         tile_offsets, ws.bucket, ws.tmp, pv, ck, sk, tile_prims);
     QGS_LAUNCHED("tile_sort_kernel");

@@ -267,10 +267,11 @@ struct SortSmem {
     int maxcnt;
 };
 
+// the float64 key of a tied entry (pixel rays from the key kernel's table)
 __device__ __noinline__ double key64_of(uint64_t v, int tile, const PrepView &pv,
                                         const CamK &cam, const SetK &st)
 {
-    return tile_key_geo(pv.geo[(uint32_t)v], tile, cam, st.euclid != 0, st.t_clip);
+    return tile_key_geo(pv.geo[(uint32_t)v], tile, cam, st.euclid != 0, st.t_clip, pv.rays);
 }
 
 // Final position of composite x inside its bucket [b0, b1) of `a`: items
@@ -313,16 +314,17 @@ __device__ __forceinline__ int bucket_start(const SortSmem &sm, int d)
 // hundreds of items -- the number of sample splitters <= the key (a sample
 // sort's buckets, balanced whatever the distribution).  Both are monotone in
 // the key, so bucket order is key order.
-constexpr int SORT_SPLIT = 4095;                 // splitters (from a sample of 4096)
+constexpr int SORT_SPLIT = 4095;                 // most splitters (a sample of 4096)
 constexpr int SORT_SKEW = 256;                   // largest linear bucket tolerated
 struct BucketFn {
     uint32_t kmin;
     int shift;
     const uint32_t *sp;                          // sorted splitters, or nullptr
+    int ns;                                      // number of splitters
     __device__ __forceinline__ int operator()(uint32_t h) const
     {
         if (!sp) return (int)((h - kmin) >> shift);
-        int lo = 0, hi = SORT_SPLIT;             // upper_bound(sp, h)
+        int lo = 0, hi = ns;                     // upper_bound(sp, h)
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
             if (sp[mid] <= h) lo = mid + 1; else hi = mid;
@@ -423,7 +425,7 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
         }
     }
     __syncthreads();
-    BucketFn bf{kmin, shift, nullptr};
+    BucketFn bf{kmin, shift, nullptr, 0};
     {
         int mx = 0;
         for (int d = threadIdx.x; d < nb; d += SORT_T) mx = max(mx, sm.bend[d]);
@@ -431,18 +433,20 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
         if (lane == 0) atomicMax(&sm.maxcnt, mx);
     }
     __syncthreads();
-    if (sm.maxcnt > SORT_SKEW && n > 2 * SORT_SPLIT) {
-        // depths cluster: sample-sort buckets instead.  4096 evenly spaced
-        // keys are sorted in shared memory (bitonic), the 4095 upper ones
-        // become splitters (kept in the upper half of bend) and the
-        // histogram is redone.
+    if (sm.maxcnt > SORT_SKEW && n >= 512) {
+        // depths cluster: sample-sort buckets instead.  S evenly spaced keys
+        // (S a power of two <= n / 2, <= 4096) are sorted in shared memory
+        // (bitonic), the S - 1 upper ones become splitters (kept in the
+        // upper half of bend) and the histogram is redone.
+        int S = 256;
+        while (S < SORT_SPLIT + 1 && 4 * S <= n) S <<= 1;
         uint32_t *smp = reinterpret_cast<uint32_t *>(sm.buf);
-        for (int i = threadIdx.x; i < SORT_SPLIT + 1; i += SORT_T)
-            smp[i] = (uint32_t)(src[(size_t)i * n / (SORT_SPLIT + 1)] >> 32);
+        for (int i = threadIdx.x; i < S; i += SORT_T)
+            smp[i] = (uint32_t)(src[(size_t)i * n / S] >> 32);
         __syncthreads();
-        for (int k = 2; k <= SORT_SPLIT + 1; k <<= 1)
+        for (int k = 2; k <= S; k <<= 1)
             for (int j = k >> 1; j > 0; j >>= 1) {
-                for (int i = threadIdx.x; i < SORT_SPLIT + 1; i += SORT_T) {
+                for (int i = threadIdx.x; i < S; i += SORT_T) {
                     const int l = i ^ j;
                     if (l > i) {
                         const uint32_t a = smp[i], b = smp[l];
@@ -453,8 +457,9 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
                 __syncthreads();
             }
         uint32_t *sp = reinterpret_cast<uint32_t *>(sm.bend) + SORT_MAX_BUCKETS / 2 + 1;
-        for (int i = threadIdx.x; i < SORT_SPLIT; i += SORT_T) sp[i] = smp[i + 1];
-        nb = SORT_SPLIT + 1;
+        for (int i = threadIdx.x; i < S - 1; i += SORT_T) sp[i] = smp[i + 1];
+        nb = S;
+        bf.ns = S - 1;
         for (int d = threadIdx.x; d < nb; d += SORT_T) sm.bend[d] = 0;
         __syncthreads();
         bf.sp = sp;

@@ -82,6 +82,7 @@ struct PrepView {
     Geo64 *geo;
     PrimRec *rec;
     ConicRec *conic;
+    const double *rays;   // optional W*H*3 fp64 pixel-ray table (binning workspace)
     int4 *bbox;
     int32_t *ntiles;
     int64_t *pair_off;    // P+1
@@ -93,6 +94,7 @@ __host__ __device__ inline PrepView prep_view(void *base, int32_t P)
 {
     char *b = static_cast<char *>(base);
     PrepView v;
+    v.rays = nullptr;
     size_t o = 0;
     v.geo = reinterpret_cast<Geo64 *>(b + o);      o += align256(sizeof(Geo64) * (size_t)P);
     v.rec = reinterpret_cast<PrimRec *>(b + o);    o += align256(sizeof(PrimRec) * (size_t)P);
