@@ -146,6 +146,8 @@ int qgs_bin(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settin
     qgs::SetK sk = qgs::make_setk(*st);
     const int n_tiles = ck.tiles_x * ck.tiles_y;
     BinWs ws = bin_ws(workspace, ck.tiles_x, ck.tiles_y, n_pairs);
+    sk.pbits = 1;                                  // id bits of the sort composite
+    while (sk.pbits < 31 && (1LL << sk.pbits) < (long long)P) ++sk.pbits;
     if (ws.bytes > workspace_bytes) return fail(QGS_E_CAPACITY, "bin workspace too small");
     qgs::PrepView pv = qgs::prep_view(const_cast<void *>(prep), P);
     QGS_CK(cudaMemsetAsync(ws.diff, 0, (size_t)(ck.tiles_x + 1) * (ck.tiles_y + 1) * sizeof(int), s));

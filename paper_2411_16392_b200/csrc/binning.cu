@@ -8,8 +8,8 @@
 //   tile_offsets_kernel 2D prefix sum -> per-tile counts -> tile_offsets
 //   pair_key_kernel     one thread per (tile, primitive) pair: fp64 key
 //                       (bit-identical to tile_sort_depths), composite
-//                       (f32_rd(key) << 32 | prim) scattered into its tile
-//                       bucket through a per-tile cursor
+//                       (fp64 key bits truncated to 64 - pbits | prim)
+//                       scattered into its tile bucket through a per-tile cursor
 //   tile_sort_kernel    one CTA per tile: stable LSD radix sort of the bucket
 //                       on the f32 key bits that vary inside the tile, then
 //                       exact fix-up of equal-f32 runs by (fp64 key, prim id)
@@ -148,9 +148,26 @@ __global__ void tile_offsets_kernel(int *diff, int tiles_x, int tiles_y, int32_t
 
 // ------------------------------------------------------------- pair keys
 
-__device__ inline uint32_t key_hi(double key)
+// Sort composite of a (tile, primitive) pair: the float64 key's bit pattern
+// (keys are positive, so bit order is value order) truncated to its top
+// 64 - pbits bits, then the primitive id in the low pbits bits.  Ordering
+// composites orders by (truncated key, id); entries whose truncated keys are
+// equal are put in exact (fp64 key, id) order by the sort.
+__device__ __forceinline__ uint64_t sort_composite(double key, int prim, int pbits)
 {
-    return __float_as_uint(__double2float_rd(key));
+    const uint64_t kb = (uint64_t)__double_as_longlong(key);
+    return (kb >> pbits << pbits) | (uint64_t)(uint32_t)prim;
+}
+__device__ __forceinline__ int comp_prim(uint64_t x, int pbits)
+{
+    return (int)(x & ((1ull << pbits) - 1ull));
+}
+// 32-bit bucketing key of a composite: exponent (offset from 2^-63) and the
+// top 23 mantissa bits of the float64 key -- monotone for keys in
+// [2^-63, 2^448] (depths > t_clip, centre distances >= 1e-12)
+__device__ __forceinline__ uint32_t sort_h(uint64_t x)
+{
+    return (uint32_t)((x >> 29) - (960ull << 23));
 }
 
 // unit ray of every pixel centre, fp64 (the key kernel's pixel rays)
@@ -224,7 +241,7 @@ pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
                 nx = ray[0]; ny = ray[1]; nz = ray[2];
             }
             const double key = key_from_ray_fast(kp, cx, cy, cz, euclid, st.t_clip);
-            bucket[slot] = ((uint64_t)key_hi(key) << 32) | (uint32_t)p;
+            bucket[slot] = sort_composite(key, p, st.pbits);
             cx = nx; cy = ny; cz = nz;
         }
     }
@@ -271,7 +288,7 @@ struct SortSmem {
 __device__ __noinline__ double key64_of(uint64_t v, int tile, const PrepView &pv,
                                         const CamK &cam, const SetK &st)
 {
-    return tile_key_geo(pv.geo[(uint32_t)v], tile, cam, st.euclid != 0, st.t_clip, pv.rays);
+    return tile_key_geo(pv.geo[comp_prim(v, st.pbits)], tile, cam, st.euclid != 0, st.t_clip, pv.rays);
 }
 
 // Final position of composite x inside its bucket [b0, b1) of `a`: items
@@ -282,19 +299,21 @@ __device__ __forceinline__ int rank_in_bucket(const uint64_t *a, int b0, int b1,
                                               int tile, const PrepView &pv, const CamK &cam,
                                               const SetK &st)
 {
-    const uint32_t h = (uint32_t)(x >> 32), p = (uint32_t)x;
+    const int pb = st.pbits;
+    const uint64_t h = x >> pb;
+    const int p = comp_prim(x, pb);
     int r = 0;
     bool have = false;
     double kx = 0.0;
     for (int j = b0; j < b1; ++j) {
         const uint64_t y = a[j];
-        const uint32_t hy = (uint32_t)(y >> 32);
+        const uint64_t hy = y >> pb;
         if (hy < h) {
             ++r;
         } else if (hy == h && y != x) {
             if (!have) { kx = key64_of(x, tile, pv, cam, st); have = true; }
             const double ky = key64_of(y, tile, pv, cam, st);
-            r += (ky < kx || (ky == kx && (uint32_t)y < p)) ? 1 : 0;
+            r += (ky < kx || (ky == kx && comp_prim(y, pb) < p)) ? 1 : 0;
         }
     }
     return r;
@@ -338,14 +357,15 @@ struct BucketFn {
 __device__ __forceinline__ int rank_fast(const uint64_t *a, int b0, int b1, uint64_t x, int tile,
                                          const PrepView &pv, const CamK &cam, const SetK &st)
 {
-    const uint32_t h = (uint32_t)(x >> 32);
+    const int pb = st.pbits;
+    const uint64_t h = x >> pb;
     int r = 0;
     bool eq = false;
 #pragma unroll 4
     for (int j = b0; j < b1; ++j) {
         const uint64_t y = a[j];
         r += y < x ? 1 : 0;
-        eq |= ((uint32_t)(y >> 32) == h) & (y != x);
+        eq |= ((y >> pb) == h) & (y != x);
     }
     return eq ? rank_in_bucket(a, b0, b1, x, tile, pv, cam, st) : r;
 }
@@ -357,10 +377,10 @@ __device__ void sort_buckets(SortSmem &sm, const uint64_t *a, int base, int g0, 
     const int i0 = bucket_start(sm, g0) - base, i1 = bucket_start(sm, g1) - base;
     for (int i = i0 + threadIdx.x; i < i1; i += SORT_T) {
         const uint64_t x = a[i];
-        const int d = bf((uint32_t)(x >> 32));
+        const int d = bf(sort_h(x));
         const int b0 = bucket_start(sm, d), b1 = sm.bend[d];
         const int r = b1 - b0 == 1 ? 0 : rank_fast(a, b0 - base, b1 - base, x, tile, pv, cam, st);
-        out[b0 + r] = (int32_t)(uint32_t)x;
+        out[b0 + r] = comp_prim(x, st.pbits);
     }
     __syncthreads();
 }
@@ -378,7 +398,7 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
     const uint64_t *src = keys + start;
     int32_t *out = tile_prims + start;
     if (n == 1) {
-        if (threadIdx.x == 0) out[0] = (int32_t)(uint32_t)src[0];
+        if (threadIdx.x == 0) out[0] = comp_prim(src[0], st.pbits);
         return;
     }
     uint64_t *stage = n <= SORT_SMEM_ITEMS ? sm.buf : tmp + start;
@@ -394,7 +414,7 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
             const int i = c0 + k * SORT_T + threadIdx.x;
             it[k] = i < n ? src[i] : 0ull;
             if (i < n) {
-                const uint32_t h = (uint32_t)(it[k] >> 32);
+                const uint32_t h = sort_h(it[k]);
                 lmin = min(lmin, h); lmax = max(lmax, h);
             }
         }
@@ -420,7 +440,7 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
             const int i = c0 + k * SORT_T + threadIdx.x;
             if (i < n) {
                 const uint64_t v = regs ? it[k] : src[i];
-                atomicAdd(&sm.bend[(((uint32_t)(v >> 32)) - kmin) >> shift], 1);
+                atomicAdd(&sm.bend[((sort_h(v)) - kmin) >> shift], 1);
             }
         }
     }
@@ -442,7 +462,7 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
         while (S < SORT_SPLIT + 1 && 4 * S <= n) S <<= 1;
         uint32_t *smp = reinterpret_cast<uint32_t *>(sm.buf);
         for (int i = threadIdx.x; i < S; i += SORT_T)
-            smp[i] = (uint32_t)(src[(size_t)i * n / S] >> 32);
+            smp[i] = sort_h(src[(size_t)i * n / S]);
         __syncthreads();
         for (int k = 2; k <= S; k <<= 1)
             for (int j = k >> 1; j > 0; j >>= 1) {
@@ -463,7 +483,7 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
         for (int d = threadIdx.x; d < nb; d += SORT_T) sm.bend[d] = 0;
         __syncthreads();
         bf.sp = sp;
-        for (int i = threadIdx.x; i < n; i += SORT_T) atomicAdd(&sm.bend[bf((uint32_t)(src[i] >> 32))], 1);
+        for (int i = threadIdx.x; i < n; i += SORT_T) atomicAdd(&sm.bend[bf(sort_h(src[i]))], 1);
         __syncthreads();
     }
     // exclusive scan of the bucket counts (nb <= 8192 = 16 per thread)
@@ -493,7 +513,7 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
             const int i = c0 + k * SORT_T + threadIdx.x;
             if (i < n) {
                 const uint64_t v = regs ? it[k] : src[i];
-                const int pos = atomicAdd(&sm.bend[bf((uint32_t)(v >> 32))], 1);
+                const int pos = atomicAdd(&sm.bend[bf(sort_h(v))], 1);
                 stage[pos] = v;
             }
         }
@@ -522,7 +542,7 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
                 for (int i = base + threadIdx.x; i < b1; i += SORT_T) {
                     const uint64_t x = stage[i];
                     out[base + rank_in_bucket(stage, base, b1, x, tile, pv, cam, st)] =
-                        (int32_t)(uint32_t)x;
+                        comp_prim(x, st.pbits);
                 }
                 __syncthreads();
                 g0 = g1;
