@@ -187,6 +187,9 @@ __device__ __forceinline__ uint32_t conic_rows(const ConicRec &q, int bu, int bv
 #ifndef QGS_RED_SETS
 #define QGS_RED_SETS 8
 #endif
+#ifndef QGS_RED_SINGLES
+#define QGS_RED_SINGLES 1
+#endif
 
 __device__ __forceinline__ PrimRec load_rec(const PrimRec *p)
 {
@@ -909,14 +912,27 @@ __device__ __forceinline__ void warp_accumulate(float (*red)[33][KGP], bool emit
                                                 const float g[KG], float *__restrict__ kg)
 {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    if (emit) {
+    const unsigned key = emit ? (unsigned)prim : 0xffffffffu;
+    const unsigned peers = __match_any_sync(FULL, key);
+#if QGS_RED_SINGLES
+    // a lane alone with its primitive adds its row directly
+    const bool single = emit && peers == (1u << lane);
+    if (single) {
+        float4 *dst = reinterpret_cast<float4 *>(kg + (size_t)prim * KG);
+#pragma unroll
+        for (int q = 0; q < KG / 4; ++q)
+            atomicAdd(dst + q, make_float4(g[4 * q], g[4 * q + 1], g[4 * q + 2], g[4 * q + 3]));
+    }
+    const bool shared_grp = emit && !single;
+#else
+    const bool shared_grp = emit;
+#endif
+    if (shared_grp) {
         float4 *dst = reinterpret_cast<float4 *>(red[w][lane]);
 #pragma unroll
         for (int q = 0; q < KG / 4; ++q) dst[q] = make_float4(g[4 * q], g[4 * q + 1], g[4 * q + 2], g[4 * q + 3]);
     }
-    const unsigned key = emit ? (unsigned)prim : 0xffffffffu;
-    const unsigned peers = __match_any_sync(FULL, key);
-    unsigned leaders = __ballot_sync(FULL, emit && (peers & ((1u << lane) - 1u)) == 0);
+    unsigned leaders = __ballot_sync(FULL, shared_grp && (peers & ((1u << lane) - 1u)) == 0);
     __syncwarp();
 #if QGS_RED_SETS == 16
     // sixteen sets of 2 lanes, each lane two float4 slots (q, q + 2)
