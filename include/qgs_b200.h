@@ -98,6 +98,10 @@ typedef struct qgs_targets {
     float *frag_xy;            /* optional, same layout x2: the fragment's local hit point
                                   (x, y) as the forward shaded it; lets the backward re-shade
                                   in fp32 without the primitive's float64 geometry */
+    int32_t *tile_order;       /* optional scratch of tiles_x*tiles_y ints: the forward
+                                  fills it with the tiles by descending pair count and
+                                  both raster kernels run the heaviest tiles first (NULL:
+                                  natural order) */
     int32_t frag_cap;          /* fragments logged per pixel; a block with a pixel over
                                   the cap (or no log) is replayed by the backward with
                                   the full candidate test */

@@ -42,7 +42,7 @@ class Targets(ctypes.Structure):
     _fields_ = [(n, vp) for n in ("color", "color_raw", "alpha", "depth", "depth_sq",
                                   "depth_median", "normal", "curvature", "distortion",
                                   "transmittance", "n_fragments", "violations", "aux",
-                                  "counters", "frag_prim", "frag_t", "frag_xy")] + \
+                                  "counters", "frag_prim", "frag_t", "frag_xy", "tile_order")] + \
         [("frag_cap", i32)]
 
 

@@ -70,6 +70,8 @@ int configure()
     if (smem_configured) return 0;
     QGS_CK(cudaFuncSetAttribute(qgs::tile_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)qgs::sort_smem_bytes()));
+    QGS_CK(cudaFuncSetAttribute(qgs::tile_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                qgs::ORDER_SMEM));
     smem_configured = true;
     return 0;
 }
@@ -220,6 +222,11 @@ int qgs_forward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_se
     qgs::PrepView pv = qgs::prep_view(const_cast<void *>(prep), P);
     if (out->violations)
         QGS_CK(cudaMemsetAsync(out->violations, 0, sizeof(int32_t) * ck.tiles_x * ck.tiles_y, s));
+    if (out->tile_order) {
+        qgs::tile_order_kernel<<<1, 1024, qgs::ORDER_SMEM, s>>>(tile_offsets, ck.tiles_x * ck.tiles_y,
+                                                              out->tile_order);
+        QGS_LAUNCHED("tile_order_kernel");
+    }
     qgs::raster_fwd_kernel<<<ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE,
                              qgs::RASTER_THREADS, 0, s>>>(pv.rec, pv.geo, pv.conic, tile_offsets,
                                                             tile_prims, ck, sk, *out);

@@ -47,6 +47,8 @@ __global__ void trace_pixel_kernel(const PrimRec *recs, const Geo64 *geo, const 
                                    int max, int *acc_prim, float *acc_t, float *acc_abar,
                                    int *em_prim, float *em_t, float *em_abar, double *em_T,
                                    int *counts);
+__global__ void tile_order_kernel(const int32_t *tile_offsets, int n_tiles, int32_t *order);
+constexpr int ORDER_SMEM = 16384 * 8;
 constexpr int RASTER_THREADS = 32;   // one warp per 8x4 block, 8 blocks per tile
 constexpr int RASTER_BLOCKS_PER_TILE = 8;
 

@@ -101,9 +101,10 @@ struct Pay {
 };
 
 // (tile, block) of this CTA and the lane's pixel
-__device__ __forceinline__ void block_pixel(int tiles_x, int &tile, int &blk, int &u, int &v)
+__device__ __forceinline__ void block_pixel(int tiles_x, const int32_t *order, int &tile, int &blk,
+                                            int &u, int &v)
 {
-    tile = blockIdx.x >> 3;
+    tile = order ? order[blockIdx.x >> 3] : (int)(blockIdx.x >> 3);
     blk = blockIdx.x & 7;
     const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
     const int lane = threadIdx.x & 31;
@@ -409,7 +410,8 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
     __shared__ FwdSmem sm;
     const int lane = threadIdx.x & 31;
     int tile, blk, u, v;
-    block_pixel(cam.tiles_x, tile, blk, u, v);
+    block_pixel(cam.tiles_x, out.tile_order, tile, blk, u, v);
+    const int rw = (tile << 3) | blk;                // raster warp id (fragment-log row)
     const int bu = u - (lane & 7), bv = v - (lane >> 3);
     const bool inside = u < cam.W && v < cam.H;
     const Cfg c = make_cfg(st);
@@ -474,7 +476,7 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         if (T > 0.5) median = (float)t;
         T *= 1.0 - abar64;
         if (log_on && nfrag < out.frag_cap) {
-            const size_t o = ((size_t)blockIdx.x * out.frag_cap + nfrag) * 32 + lane;
+            const size_t o = ((size_t)rw * out.frag_cap + nfrag) * 32 + lane;
             out.frag_prim[o] = ep;
             out.frag_t[o] = t;
 #if QGS_PAY_XY
@@ -995,7 +997,8 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
     if (lane < KG) sm.red[0][32][lane] = 0.f;        // zero row for padded group sums
     __syncwarp();
     int tile, blk, u, v;
-    block_pixel(cam.tiles_x, tile, blk, u, v);
+    block_pixel(cam.tiles_x, fwd.tile_order, tile, blk, u, v);
+    const int rw = (tile << 3) | blk;                // raster warp id (fragment-log row)
     const bool inside = u < cam.W && v < cam.H;
     const Cfg c = make_cfg(st);
     const int npx = cam.W * cam.H, px = inside ? v * cam.W + u : 0;
@@ -1094,7 +1097,7 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         const int nf = alive ? fwd.n_fragments[px] : 0;
         const int nf_max = __reduce_max_sync(FULL, nf);
         if (fwd.frag_prim && fwd.frag_t && nf_max <= fwd.frag_cap) {
-            const size_t base = (size_t)blockIdx.x * fwd.frag_cap * 32 + lane;
+            const size_t base = (size_t)rw * fwd.frag_cap * 32 + lane;
             const float2 *xy = reinterpret_cast<const float2 *>(fwd.frag_xy);
             const bool have_xy = xy != nullptr;
             int np_ = -1;
@@ -1151,6 +1154,43 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         if (emit) ring_pop(R, et, ep);
         emit_grad(emit, ep, et, false, 0.f, 0.f);
     }
+}
+
+// ===================================================== raster schedule
+// tiles by descending pair count (ties by tile), so the raster kernels start
+// the longest tiles first; one CTA, bitonic sort of (~count, tile) in smem
+constexpr int ORDER_MAX = 16384;
+__global__ void __launch_bounds__(1024)
+tile_order_kernel(const int32_t *__restrict__ tile_offsets, int n_tiles, int32_t *order)
+{
+    extern __shared__ unsigned long long ord[];
+    if (n_tiles > ORDER_MAX) {                  // natural order
+        for (int i = threadIdx.x; i < n_tiles; i += blockDim.x) order[i] = i;
+        return;
+    }
+    int n2 = 1;
+    while (n2 < n_tiles) n2 <<= 1;
+    for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+        unsigned long long k = ~0ull;
+        if (i < n_tiles) {
+            const uint32_t cnt = (uint32_t)(tile_offsets[i + 1] - tile_offsets[i]);
+            k = ((unsigned long long)(0xffffffffu - cnt) << 32) | (uint32_t)i;
+        }
+        ord[i] = k;
+    }
+    __syncthreads();
+    for (int k = 2; k <= n2; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const unsigned long long a = ord[i], b = ord[l];
+                    if ((a > b) == ((i & k) == 0)) { ord[i] = b; ord[l] = a; }
+                }
+            }
+            __syncthreads();
+        }
+    for (int i = threadIdx.x; i < n_tiles; i += blockDim.x) order[i] = (int32_t)(uint32_t)ord[i];
 }
 
 // ============================================================ diagnostics

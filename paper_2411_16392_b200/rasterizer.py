@@ -236,6 +236,7 @@ class RenderTargets:
     frag_prim: torch.Tensor = None     # fragment log (blocks, cap, 32) int32 primitive ids
     frag_t: torch.Tensor = None        # fragment log (blocks, cap, 32) float64 depths
     frag_xy: torch.Tensor = None       # fragment log (blocks, cap, 32, 2) fp32 local hit points
+    tile_order: torch.Tensor = None    # tiles by descending pair count (raster schedule)
 
     @property
     def order_violations(self):
@@ -386,6 +387,8 @@ def forward(prep: PreparedView, keep_aux=True, counters=None) -> RenderTargets:
             if not os.environ.get("QGS_NO_FRAG_XY"):   # diagnostic: float64 re-shading
                 tg.frag_xy = torch.empty((blocks, cap, 32, 2), dtype=torch.float32, device=device)
                 t.frag_xy = _ptr(tg.frag_xy)
+    tg.tile_order = torch.empty((prep.tiles_x * prep.tiles_y,), dtype=torch.int32, device=device)
+    t.tile_order = _ptr(tg.tile_order)
     t.counters = _ptr(counters)
     _lib.check(_lib.load().qgs_forward(_ptr(prep.prep), len(prep.dev), prep._cam_c, prep._st_c,
                                        _ptr(prep.tile_offsets), _ptr(prep.tile_prims), t,
@@ -423,6 +426,7 @@ def kernel_grads(prep: PreparedView, targets: RenderTargets, upstream, kg=None) 
     if targets.aux.dim() != 3:
         raise ValueError("backward needs forward(prep, keep_aux=True)")
     t.aux = _ptr(targets.aux)
+    t.tile_order = _ptr(targets.tile_order)
     if targets.frag_prim is not None:
         t.frag_prim, t.frag_t = _ptr(targets.frag_prim), _ptr(targets.frag_t)
         t.frag_xy = _ptr(targets.frag_xy)
