@@ -230,11 +230,17 @@ __device__ inline void bounding_ellipsoid(const double s[3], bool planar, bool e
 // sits A t^2 ~ 1e-5 off the quadric, and fp64 rounding
 __device__ inline void pad_axes(double ax[3]) { for (int k = 0; k < 3; ++k) ax[k] *= 1.001; }
 
-// Pixel-centre conic of the ellipsoid's outline (dual quadric projected:
-// C* = Mq Mq^T - m m^T with [Mq | m] = K [R_wc | t_wc] [R diag(ax) | c + zc R e3],
-// point conic = adj(C*)), translated to the box centre, normalised and
-// widened by the fp32 evaluation margin.  No cull (F = -1) when the
-// ellipsoid reaches the camera plane or contains the eye.
+// Pixel-centre conic bounding the screen footprint of the bounding ellipsoid
+// E (centre mc, camera-frame axes Ri scaled by ax).  A pixel whose ray line
+// misses E cannot be accepted.  Non-planar E: the line through the eye along
+// d meets E iff (d.A c)^2 - (d.A d)(c.A c - 1) >= 0 (A = E's shape matrix, c
+// its centre): exact for any E position once the eye is outside E, also for
+// an E that straddles the camera plane (its footprint is then a hyperbola,
+// left unbounded).  Planar E (a disk): the outline of the dual quadric,
+// C* = Mq Mq^T - m m^T, point conic = adj(C*), for a disk in front of the
+// camera.  The conic is taken about pixel-centre origin (u0, v0), normalised,
+// and widened by its fp32 evaluation margin; an elliptic footprint also
+// tightens the pixel box.  No cull (F = -1) when neither form applies.
 __device__ inline ConicRec bounding_conic(const double s[3], bool planar, bool euclid,
                                           const double R[9], const double c[3],
                                           const CamK &cam, const long long box[4])
@@ -249,89 +255,111 @@ __device__ inline ConicRec bounding_conic(const double s[3], bool planar, bool e
     bounding_ellipsoid(s, planar, euclid, zc, ax);
     pad_axes(ax);
     // centre and axes in camera coordinates
-    double cw[3], Mc[3][3], mc[3];
+    double cw[3], Ri[3][3], mc[3];
     for (int i = 0; i < 3; ++i) cw[i] = c[i] + zc * R[3 * i + 2];
     for (int i = 0; i < 3; ++i) {
         mc[i] = cam.Rwc[3 * i] * cw[0] + cam.Rwc[3 * i + 1] * cw[1] + cam.Rwc[3 * i + 2] * cw[2] + cam.twc[i];
         for (int k = 0; k < 3; ++k)
-            Mc[i][k] = (cam.Rwc[3 * i] * R[k] + cam.Rwc[3 * i + 1] * R[3 + k] +
-                        cam.Rwc[3 * i + 2] * R[6 + k]) * ax[k];
+            Ri[i][k] = cam.Rwc[3 * i] * R[k] + cam.Rwc[3 * i + 1] * R[3 + k] + cam.Rwc[3 * i + 2] * R[6 + k];
     }
-    // in front of the camera plane with margin, eye outside
-    const double zr = sqrt(Mc[2][0] * Mc[2][0] + Mc[2][1] * Mc[2][1] + Mc[2][2] * Mc[2][2]);
-    if (!(mc[2] - zr > 1e-6 * fmax(mc[2], 1e-30))) return q;
-    // homogeneous pixel map: rows u = fx X + cx Z, v = fy Y + cy Z, w = Z
-    double Mq[3][3], m[3];
-    for (int k = 0; k < 3; ++k) {
-        Mq[0][k] = cam.fx * Mc[0][k] + cam.cx * Mc[2][k];
-        Mq[1][k] = cam.fy * Mc[1][k] + cam.cy * Mc[2][k];
-        Mq[2][k] = Mc[2][k];
-    }
-    m[0] = cam.fx * mc[0] + cam.cx * mc[2];
-    m[1] = cam.fy * mc[1] + cam.cy * mc[2];
-    m[2] = mc[2];
-    // Normalised pixel conic about pixel-centre origin (u0, v0): Q(U, V) =
-    // A U^2 + B U V + C V^2 + D U + E V + F <= 0 inside, U = (pixel centre u) - u0
-    double Q6[6];
-    auto conic_about = [&](double u0, double v0) -> bool {
-        double Mt[3][3], mt[3];
-        for (int k = 0; k < 3; ++k) {
-            Mt[0][k] = Mq[0][k] - u0 * Mq[2][k];
-            Mt[1][k] = Mq[1][k] - v0 * Mq[2][k];
-            Mt[2][k] = Mq[2][k];
-        }
-        mt[0] = m[0] - u0 * m[2];
-        mt[1] = m[1] - v0 * m[2];
-        mt[2] = m[2];
+    const bool disk = !(ax[2] > 0.0);
+    double K[3][3];                       // quadratic form on camera rays d: >= 0 possible hit
+    if (!disk) {
+        double A[3][3];
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) {
+                double acc = 0.0;
+                for (int k = 0; k < 3; ++k) acc += Ri[i][k] * Ri[j][k] / (ax[k] * ax[k]);
+                A[i][j] = acc;
+            }
+        double ac[3];
+        for (int i = 0; i < 3; ++i) ac[i] = A[i][0] * mc[0] + A[i][1] * mc[1] + A[i][2] * mc[2];
+        const double cac = ac[0] * mc[0] + ac[1] * mc[1] + ac[2] * mc[2];
+        const double gamma = cac - 1.0;
+        if (!(gamma > 1e-6 * cac)) return q;        // eye inside E: every line hits
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) K[i][j] = ac[i] * ac[j] - gamma * A[i][j];
+    } else {
+        // disk: dual-quadric outline, in front of the camera plane only
+        double Mc[3][3];
+        for (int i = 0; i < 3; ++i)
+            for (int k = 0; k < 3; ++k) Mc[i][k] = Ri[i][k] * ax[k];
+        const double zr = sqrt(Mc[2][0] * Mc[2][0] + Mc[2][1] * Mc[2][1]);
+        if (!(mc[2] - zr > 1e-6 * fmax(mc[2], 1e-30))) return q;
         double D[3][3];
         for (int i = 0; i < 3; ++i)
             for (int j = 0; j < 3; ++j)
-                D[i][j] = Mt[i][0] * Mt[j][0] + Mt[i][1] * Mt[j][1] + Mt[i][2] * Mt[j][2] - mt[i] * mt[j];
-        // point conic = adjugate of the dual conic
-        const double P00 = D[1][1] * D[2][2] - D[1][2] * D[2][1];
-        const double P01 = D[0][2] * D[2][1] - D[0][1] * D[2][2];
-        const double P02 = D[0][1] * D[1][2] - D[0][2] * D[1][1];
-        const double P11 = D[0][0] * D[2][2] - D[0][2] * D[2][0];
-        const double P12 = D[0][2] * D[1][0] - D[0][0] * D[1][2];
-        const double P22 = D[0][0] * D[1][1] - D[0][1] * D[1][0];
-        // inside must be negative: evaluate at the projected centre
-        const double cu = mt[0] / mt[2], cv = mt[1] / mt[2];
-        const double at_c = P00 * cu * cu + 2.0 * P01 * cu * cv + P11 * cv * cv + 2.0 * P02 * cu +
-                            2.0 * P12 * cv + P22;
-        const double nrm = fmax(fabs(P00), fabs(P11));
-        if (!(nrm > 0.0) || !(P00 * P11 - P01 * P01 > 0.0)) return false;   // not an ellipse
-        const double k = (at_c > 0.0 ? -1.0 : 1.0) / nrm;
-        Q6[0] = P00 * k; Q6[1] = 2.0 * P01 * k; Q6[2] = P11 * k;
-        Q6[3] = 2.0 * P02 * k; Q6[4] = 2.0 * P12 * k; Q6[5] = P22 * k;
-        return Q6[0] > 0.0 && Q6[2] > 0.0;
+                D[i][j] = Mc[i][0] * Mc[j][0] + Mc[i][1] * Mc[j][1] - mc[i] * mc[j];
+        // adjugate = point conic (up to sign); orient: the centre ray must be inside
+        double P[3][3];
+        P[0][0] = D[1][1] * D[2][2] - D[1][2] * D[2][1];
+        P[0][1] = P[1][0] = D[0][2] * D[2][1] - D[0][1] * D[2][2];
+        P[0][2] = P[2][0] = D[0][1] * D[1][2] - D[0][2] * D[1][1];
+        P[1][1] = D[0][0] * D[2][2] - D[0][2] * D[2][0];
+        P[1][2] = P[2][1] = D[0][2] * D[1][0] - D[0][0] * D[1][2];
+        P[2][2] = D[0][0] * D[1][1] - D[0][1] * D[1][0];
+        double at_c = 0.0;
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) at_c += mc[i] * P[i][j] * mc[j];
+        const double sg = at_c > 0.0 ? 1.0 : -1.0;    // make the centre ray positive
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) K[i][j] = sg * P[i][j];
+    }
+    // Normalised pixel conic about pixel-centre origin (u0, v0): Q(U, V) =
+    // A U^2 + B U V + C V^2 + D U + E V + F <= 0 possible, U = (pixel centre u) - u0
+    double Q6[6];
+    auto conic_about = [&](double u0, double v0) -> bool {
+        // d = T (U, V, 1): u' = (U + u0 - cx) / fx, v' = (V + v0 - cy) / fy
+        const double T[3][3] = {{1.0 / cam.fx, 0.0, (u0 - cam.cx) / cam.fx},
+                                {0.0, 1.0 / cam.fy, (v0 - cam.cy) / cam.fy},
+                                {0.0, 0.0, 1.0}};
+        double KT[3][3], Kp[3][3];
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j)
+                KT[i][j] = K[i][0] * T[0][j] + K[i][1] * T[1][j] + K[i][2] * T[2][j];
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j)
+                Kp[i][j] = T[0][i] * KT[0][j] + T[1][i] * KT[1][j] + T[2][i] * KT[2][j];
+        const double nrm = fmax(fabs(Kp[0][0]), fabs(Kp[1][1]));
+        if (!(nrm > 0.0) || !isfinite(nrm)) return false;
+        const double k = -1.0 / nrm;
+        Q6[0] = Kp[0][0] * k; Q6[1] = 2.0 * Kp[0][1] * k; Q6[2] = Kp[1][1] * k;
+        Q6[3] = 2.0 * Kp[0][2] * k; Q6[4] = 2.0 * Kp[1][2] * k; Q6[5] = Kp[2][2] * k;
+        return true;
     };
-    // 1. about the reference box centre: the ellipse's own pixel bounds
-    //    (centre from grad Q = 0, half extents sqrt(-Q(c) C / det), sqrt(-Q(c) A / det)),
-    //    one pixel of slack each side, intersected with the reference box
+    // 1. about the reference box centre; an ellipse tightens the box to its
+    //    own pixel bounds (centre from grad Q = 0, half extents
+    //    sqrt(-Q(c) C / det), sqrt(-Q(c) A / det)) plus one pixel each side
     double uc = (double)conic_uc(q), vc = (double)conic_vc(q);
     if (!conic_about(uc + 0.5, vc + 0.5)) return q;
     {
         const double A = Q6[0], B = Q6[1], C = Q6[2], Dd = Q6[3], E = Q6[4], F = Q6[5];
         const double det2 = 4.0 * A * C - B * B;
-        if (!(det2 > 0.0)) return q;
-        const double U0 = (B * E - 2.0 * C * Dd) / det2, V0 = (B * Dd - 2.0 * A * E) / det2;
-        const double kq = -(A * U0 * U0 + B * U0 * V0 + C * V0 * V0 + Dd * U0 + E * V0 + F);
-        if (!(kq > 0.0)) return q;
-        const double hu = sqrt(kq * 4.0 * C / det2), hv = sqrt(kq * 4.0 * A / det2);
-        // pixel index u has centre u + 0.5 = uc + 0.5 + U
-        const double lo_u = floor(uc + U0 - hu) - 1.0, hi_u = ceil(uc + U0 + hu) + 1.0;
-        const double lo_v = floor(vc + V0 - hv) - 1.0, hi_v = ceil(vc + V0 + hv) + 1.0;
-        if (!(isfinite(lo_u) && isfinite(hi_u) && isfinite(lo_v) && isfinite(hi_v))) return q;
-        const long long b0 = max(box[0], (long long)fmax(lo_u, -1.0)), b1 = min(box[1], (long long)fmin(hi_u, 1e9));
-        const long long b2 = max(box[2], (long long)fmax(lo_v, -1.0)), b3 = min(box[3], (long long)fmin(hi_v, 1e9));
-        if (b0 > b1 || b2 > b3) {            // nothing in the reference box can be accepted
-            q.bb_u = 0xffffu; q.bb_v = 0xffffu;
-            return q;
+        if (A > 0.0 && C > 0.0 && det2 > 0.0) {
+            const double U0 = (B * E - 2.0 * C * Dd) / det2, V0 = (B * Dd - 2.0 * A * E) / det2;
+            const double kq = -(A * U0 * U0 + B * U0 * V0 + C * V0 * V0 + Dd * U0 + E * V0 + F);
+            if (!(kq > 0.0)) {                           // empty footprint
+                q.bb_u = 0xffffu; q.bb_v = 0xffffu;
+                return q;
+            }
+            const double hu = sqrt(kq * 4.0 * C / det2), hv = sqrt(kq * 4.0 * A / det2);
+            const double lo_u = floor(uc + U0 - hu) - 1.0, hi_u = ceil(uc + U0 + hu) + 1.0;
+            const double lo_v = floor(vc + V0 - hv) - 1.0, hi_v = ceil(vc + V0 + hv) + 1.0;
+            if (isfinite(lo_u) && isfinite(hi_u) && isfinite(lo_v) && isfinite(hi_v)) {
+                const long long b0 = max(box[0], (long long)fmax(lo_u, -1.0));
+                const long long b1 = min(box[1], (long long)fmin(hi_u, 1e9));
+                const long long b2 = max(box[2], (long long)fmax(lo_v, -1.0));
+                const long long b3 = min(box[3], (long long)fmin(hi_v, 1e9));
+                if (b0 > b1 || b2 > b3) {        // nothing in the reference box can be accepted
+                    q.bb_u = 0xffffu; q.bb_v = 0xffffu;
+                    return q;
+                }
+                q.bb_u = (uint32_t)b0 | ((uint32_t)b1 << 16);
+                q.bb_v = (uint32_t)b2 | ((uint32_t)b3 << 16);
+            }
         }
-        q.bb_u = (uint32_t)b0 | ((uint32_t)b1 << 16);
-        q.bb_v = (uint32_t)b2 | ((uint32_t)b3 << 16);
     }
-    // 2. the conic again about the culled box's centre, with the fp32 margin
+    // 2. the conic about the final box's centre, with the fp32 margin
     uc = (double)conic_uc(q); vc = (double)conic_vc(q);
     if (!conic_about(uc + 0.5, vc + 0.5)) {
         q.bb_u = (uint32_t)box[0] | ((uint32_t)box[1] << 16);      // no cull after all
