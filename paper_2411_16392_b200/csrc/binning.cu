@@ -334,7 +334,10 @@ __device__ __forceinline__ int bucket_start(const SortSmem &sm, int d)
 // sort's buckets, balanced whatever the distribution).  Both are monotone in
 // the key, so bucket order is key order.
 constexpr int SORT_SPLIT = 4095;                 // most splitters (a sample of 4096)
-constexpr int SORT_SKEW = 256;                   // largest linear bucket tolerated
+#ifndef QGS_SORT_SKEW
+#define QGS_SORT_SKEW 64
+#endif
+constexpr int SORT_SKEW = QGS_SORT_SKEW;         // largest linear bucket tolerated
 struct BucketFn {
     uint32_t kmin;
     int shift;
