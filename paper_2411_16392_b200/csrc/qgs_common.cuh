@@ -182,7 +182,7 @@ __device__ inline float arc_length32(float a, float rho)
         return rho * (1.f + u2 * (1.f / 6.f + u2 * (-1.f / 40.f + u2 * (1.f / 112.f - u2 * (5.f / 1152.f)))));
     }
     float r = sqrtf(u * u + 1.f);
-    return (copysignf(__logf(fabsf(u) + r), u) + u * r) / (4.f * a);   // |u| + r >= 1.34
+    return __fdividef(copysignf(__logf(fabsf(u) + r), u) + u * r, 4.f * a);   // |u| + r >= 1.34
 }
 
 // The 3-sigma test l <= 3 sigma(theta) at local (x, y) (intersect.py:104-112,
@@ -196,12 +196,14 @@ __device__ inline bool within_3sigma64(double x, double y, double s1, double s2,
         const float xf = (float)x, yf = (float)y;
         const float r2 = xf * xf + yf * yf;
         if (r2 > 1e-18f) {
-            const float rho = sqrtf(r2), c = xf / rho, sn = yf / rho;
+            // approximate rsqrt / reciprocal / log: ~1e-6 relative, far inside the band
+            const float ir = rsqrtf(r2), rho = r2 * ir, c = xf * ir, sn = yf * ir;
             const float a = (float)s3 * ((float)w1 * c * c + (float)w2 * sn * sn);
             const float l = euclid ? rho : arc_length32(a, rho);
             const float f1 = (float)s1, f2 = (float)s2;
-            const float sig = fabsf(f1 * f2) / sqrtf((f2 * c) * (f2 * c) + (f1 * sn) * (f1 * sn));
-            const float q = l / (3.f * sig);
+            const float m = (f2 * c) * (f2 * c) + (f1 * sn) * (f1 * sn);
+            const float isig = m * rsqrtf(m) * __frcp_rn(fabsf(f1 * f2));   // 1 / sigma
+            const float q = l * isig * (1.f / 3.f);
             if (q < 1.f - 1e-4f) return true;
             if (q > 1.f + 1e-4f) return false;
         }
