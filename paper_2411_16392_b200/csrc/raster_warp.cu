@@ -76,20 +76,24 @@ struct FwdSmem {
     GeoHead geoh[WB];
 #endif
     PrimRec rec[WB];
-    int prim[WB];
     int qprim[WB + 32];       // culled-in entries waiting for the coarse/exact passes
     uint32_t qmask[WB + 32];  // their conic & box & alive pixel masks
     int aprim[64];            // box-overlapping entries waiting for the conic test
     uint32_t amask[64];       // their box & alive pixel masks
-    uint32_t boxw[32];        // work counters only: pixel-box masks of the window
     double ring_t[RING][32];  // per-lane ring, [slot][lane]: conflict-free
     int ring_p[RING][32];
 #if !QGS_FWD_RAY_REGS
     double d64[3][32];        // fp64 pixel ray (only the exact path reads it)
 #endif
-    double acc[11][32];       // fp64 blend sums, touched once per composited fragment
+    // fp64 blend sums, touched once per composited fragment (the backward's
+    // suffix sums vtot - prefix need them: fp32 colour / normal / curvature
+    // sums were measured to triple the gradient violations at C2)
+    double acc[11][32];
     float pay[RING][PAYN][32];   // ring payload (see Pay)
-    float tfirst[WB][32];     // pass 1 -> pass 2: first coarse root that survived
+    union {
+        float tfirst[WB][32];    // pass 1 -> pass 2: first coarse root that survived
+        uint32_t boxw[32];       // work counters only (between batches): window box masks
+    };
 };
 
 // Ring payload of an accepted fragment.  QGS_PAY_XY: (abar, local hit x, y)
