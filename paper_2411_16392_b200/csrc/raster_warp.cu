@@ -396,7 +396,7 @@ __device__ __forceinline__ void shade_emitted(const PrimRec &r, const Geo64 &g, 
 __device__ __forceinline__ void finish_frag(const PrimRec &r, float dx, float dy, float dz,
                                             const Cfg &c, Frag &f)
 {
-    f.h.G = expf(-(f.h.l * f.h.l) / (2.f * f.h.sig * f.h.sig));
+    f.h.G = QGS_EXPF(-(f.h.l * f.h.l) / (2.f * f.h.sig * f.h.sig));
     float abar = r.alpha * f.h.G;
     f.clamped = abar > c.alpha_clamp;
     f.abar = f.clamped ? c.alpha_clamp : abar;

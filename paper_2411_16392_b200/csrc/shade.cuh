@@ -23,6 +23,17 @@
 
 #include "qgs_common.cuh"
 
+// the Gaussian weight and the arc length's log: accurate by default
+#ifndef QGS_FAST_EXPLOG
+#define QGS_FAST_EXPLOG 0
+#endif
+#if QGS_FAST_EXPLOG
+#define QGS_EXPF __expf
+#define QGS_LOGF __logf
+#else
+#define QGS_EXPF expf
+#define QGS_LOGF logf
+#endif
 #ifndef QGS_NEWTON64
 #define QGS_NEWTON64 2      // fp64 Newton steps refining an accepted root
 #endif
@@ -46,7 +57,7 @@ __device__ __forceinline__ float arc32(float a, float rho)
         return rho * (1.f + u2 * (1.f / 6.f + u2 * (-1.f / 40.f + u2 * (1.f / 112.f - u2 * (5.f / 1152.f)))));
     }
     float r = sqrtf(fmaf(u, u, 1.f));
-    float as = copysignf(logf(fabsf(u) + r), u);
+    float as = copysignf(QGS_LOGF(fabsf(u) + r), u);
     return (as + u * r) / (4.f * a);
 }
 
@@ -207,7 +218,7 @@ __device__ __forceinline__ bool confirm_root(const PrimRec &r, const Geo64 &g, c
     shade_at(r, g, dh, t64, euclid, h);
     if (!planar && ellipse_out(r, h.x, h.y, 1.f)) return false;
     if (!(h.l <= 3.f * h.sig)) return false;
-    h.G = expf(-(h.l * h.l) / (2.f * h.sig * h.sig));
+    h.G = QGS_EXPF(-(h.l * h.l) / (2.f * h.sig * h.sig));
     return true;
 }
 
