@@ -34,7 +34,7 @@ C_HIT, S_HIT = 136.0, 18.1
 C_COMP = 37.0
 C_GRAD, S_GRAD = 428.0, 36.0
 BIN_BYTES_PER_PAIR = 20.0   # bucketed composite key write + read (16) + tile_prims write (4)
-OUR_LAUNCHES_PER_VIEW = 13  # preprocess, 3 scan, tile_diff, tile_offsets, pixel_rays, pair_key, tile_sort, tile_order, fwd, bwd, chain
+OUR_LAUNCHES_PER_VIEW = 14  # preprocess, 3 scan, tile_diff, tile_offsets, pixel_rays, pair_key, 2 tile_order, tile_sort, fwd, bwd, chain
 
 
 def env_rank():

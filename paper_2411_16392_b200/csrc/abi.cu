@@ -45,6 +45,7 @@ struct BinWs {
     int32_t *cursor;
     uint64_t *bucket, *tmp;
     double *rays;         // W*H*3 unit pixel rays (fp64) for the key kernel
+    int32_t *order;       // tiles by descending pair count (sort schedule)
     size_t bytes;
 };
 
@@ -59,6 +60,7 @@ BinWs bin_ws(void *base, int32_t tiles_x, int32_t tiles_y, int64_t n_pairs)
     w.bucket = reinterpret_cast<uint64_t *>(b + o); o += qgs::align256((size_t)n_pairs * 8);
     w.tmp = reinterpret_cast<uint64_t *>(b + o);    o += qgs::align256((size_t)n_pairs * 8);
     w.rays = reinterpret_cast<double *>(b + o);     o += qgs::align256((size_t)tiles_x * tiles_y * 256 * 24);
+    w.order = reinterpret_cast<int32_t *>(b + o);   o += qgs::align256((size_t)tiles_x * tiles_y * 4);
     w.bytes = o;
     return w;
 }
@@ -132,7 +134,8 @@ size_t qgs_bin_workspace_bytes(int32_t P, int64_t n_pairs, int32_t n_tiles)
     // diff grid is at most (n_tiles + tiles_x + tiles_y + 1) entries; bound it by 2*n_tiles + 2*32768
     size_t ndiff = 2 * (size_t)n_tiles + 65538;
     return qgs::align256(ndiff * sizeof(int)) + qgs::align256((size_t)n_tiles * 4) +
-           2 * qgs::align256((size_t)n_pairs * 8) + qgs::align256((size_t)n_tiles * 256 * 24) + 256;
+           2 * qgs::align256((size_t)n_pairs * 8) + qgs::align256((size_t)n_tiles * 256 * 24) +
+           qgs::align256((size_t)n_tiles * 4) + 256;
 }
 
 int qgs_bin(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settings *st,
@@ -167,8 +170,12 @@ int qgs_bin(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settin
     qgs::pair_key_kernel<<<grid, 256, 0, s>>>(pv, P, n_pairs, ck, sk, ws.rays, ws.cursor, ws.bucket);
     QGS_LAUNCHED("pair_key_kernel");
     pv.rays = ws.rays;
+    // largest tiles first: one CTA sorts a tile, so a 100K-entry tile started
+    // last would be the kernel's tail
+    qgs::tile_order_kernel<<<1, 1024, qgs::ORDER_SMEM, s>>>(tile_offsets, n_tiles, ws.order, 1);
+    QGS_LAUNCHED("tile_order_kernel (sort)");
     qgs::tile_sort_kernel<<<n_tiles, qgs::sort_threads(), qgs::sort_smem_bytes(), s>>>(
-        tile_offsets, ws.bucket, ws.tmp, pv, ck, sk, tile_prims);
+        tile_offsets, ws.bucket, ws.tmp, pv, ck, sk, tile_prims, ws.order);
     QGS_LAUNCHED("tile_sort_kernel");
     return 0;
 }
@@ -224,7 +231,7 @@ int qgs_forward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_se
         QGS_CK(cudaMemsetAsync(out->violations, 0, sizeof(int32_t) * ck.tiles_x * ck.tiles_y, s));
     if (out->tile_order) {
         qgs::tile_order_kernel<<<1, 1024, qgs::ORDER_SMEM, s>>>(tile_offsets, ck.tiles_x * ck.tiles_y,
-                                                              out->tile_order);
+                                                              out->tile_order, 0);
         QGS_LAUNCHED("tile_order_kernel");
     }
     qgs::raster_fwd_kernel<<<ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE,

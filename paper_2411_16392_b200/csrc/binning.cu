@@ -390,11 +390,11 @@ __device__ void sort_buckets(SortSmem &sm, const uint64_t *a, int base, int g0, 
 
 __global__ void __launch_bounds__(SORT_T, QGS_SORT_MIN_BLOCKS)
 tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint64_t *tmp,
-                 PrepView pv, CamK cam, SetK st, int32_t *tile_prims)
+                 PrepView pv, CamK cam, SetK st, int32_t *tile_prims, const int32_t *order)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SortSmem &sm = *reinterpret_cast<SortSmem *>(smem_raw);
-    const int tile = blockIdx.x;
+    const int tile = order ? order[blockIdx.x] : (int)blockIdx.x;
     const int start = tile_offsets[tile], n = tile_offsets[tile + 1] - start;
     if (n == 0) return;
     const int lane = threadIdx.x & 31;

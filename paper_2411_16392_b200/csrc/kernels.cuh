@@ -23,7 +23,8 @@ __global__ void pixel_rays_kernel(CamK cam, double *rays);
 __global__ void pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
                                 const double *rays, int32_t *cursor, uint64_t *bucket);
 __global__ void tile_sort_kernel(const int32_t *tile_offsets, uint64_t *keys, uint64_t *tmp,
-                                 PrepView pv, CamK cam, SetK st, int32_t *tile_prims);
+                                 PrepView pv, CamK cam, SetK st, int32_t *tile_prims,
+                                 const int32_t *order);
 __global__ void sorted_keys_kernel(PrepView pv, const int32_t *tile_offsets,
                                    const int32_t *tile_prims, int n_tiles, CamK cam, SetK st,
                                    double *keys);
@@ -47,7 +48,8 @@ __global__ void trace_pixel_kernel(const PrimRec *recs, const Geo64 *geo, const 
                                    int max, int *acc_prim, float *acc_t, float *acc_abar,
                                    int *em_prim, float *em_t, float *em_abar, double *em_T,
                                    int *counts);
-__global__ void tile_order_kernel(const int32_t *tile_offsets, int n_tiles, int32_t *order);
+__global__ void tile_order_kernel(const int32_t *tile_offsets, int n_tiles, int32_t *order,
+                                  int heavy_only);
 constexpr int ORDER_SMEM = 16384 * 8;
 constexpr int RASTER_THREADS = 32;   // one warp per 8x4 block, 8 blocks per tile
 constexpr int RASTER_BLOCKS_PER_TILE = 8;

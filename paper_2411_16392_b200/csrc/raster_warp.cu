@@ -1164,8 +1164,11 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
 // tiles by descending pair count (ties by tile), so the raster kernels start
 // the longest tiles first; one CTA, bitonic sort of (~count, tile) in smem
 constexpr int ORDER_MAX = 16384;
+// heavy_only: only tiles over 4x the mean count move to the front (by
+// count); the rest keep their natural order (memory locality of the sort)
 __global__ void __launch_bounds__(1024)
-tile_order_kernel(const int32_t *__restrict__ tile_offsets, int n_tiles, int32_t *order)
+tile_order_kernel(const int32_t *__restrict__ tile_offsets, int n_tiles, int32_t *order,
+                  int heavy_only)
 {
     extern __shared__ unsigned long long ord[];
     if (n_tiles > ORDER_MAX) {                  // natural order
@@ -1174,11 +1177,15 @@ tile_order_kernel(const int32_t *__restrict__ tile_offsets, int n_tiles, int32_t
     }
     int n2 = 1;
     while (n2 < n_tiles) n2 <<= 1;
+    const double heavy = 4.0 * (double)tile_offsets[n_tiles] / (double)max(n_tiles, 1);
     for (int i = threadIdx.x; i < n2; i += blockDim.x) {
         unsigned long long k = ~0ull;
         if (i < n_tiles) {
             const uint32_t cnt = (uint32_t)(tile_offsets[i + 1] - tile_offsets[i]);
-            k = ((unsigned long long)(0xffffffffu - cnt) << 32) | (uint32_t)i;
+            if (!heavy_only || (double)cnt > heavy)
+                k = ((unsigned long long)(0x7fffffffu - cnt) << 32) | (uint32_t)i;
+            else
+                k = (1ull << 63) | (uint32_t)i;
         }
         ord[i] = k;
     }
