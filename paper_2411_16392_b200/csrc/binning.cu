@@ -275,6 +275,12 @@ constexpr int SORT_IPT = 4;
 constexpr int SORT_CHUNK = SORT_T * SORT_IPT;     // items per register pass
 constexpr int SORT_SMEM_ITEMS = QGS_SORT_SMEM_ITEMS;   // staged in shared memory up to this
 constexpr int SORT_MAX_BUCKETS = 8192;
+#ifndef QGS_SORT_L2_MIN
+#define QGS_SORT_L2_MIN 6                        // mean first-level bucket that takes the second level
+#endif
+constexpr int SORT_NB2 = 2048;                   // second-level buckets of a staged group
+// a staged group uses the head of buf; its second-level bucket counts the tail
+constexpr int SORT_GROUP_ITEMS = SORT_SMEM_ITEMS - SORT_NB2 / 2;
 
 struct SortSmem {
     uint64_t buf[SORT_SMEM_ITEMS];
@@ -384,6 +390,51 @@ __device__ void sort_buckets(SortSmem &sm, const uint64_t *a, int base, int g0, 
         const int b0 = bucket_start(sm, d), b1 = sm.bend[d];
         const int r = b1 - b0 == 1 ? 0 : rank_fast(a, b0 - base, b1 - base, x, tile, pv, cam, st);
         out[b0 + r] = comp_prim(x, st.pbits);
+    }
+    __syncthreads();
+}
+
+// Second level: the group's key interval [glo, ghi) (from the
+// first-level bucket bounds) cut linearly into SORT_NB2 buckets;
+// histogram from the L2 slice, scatter into shared memory, rank.
+// First-level buckets of big tiles hold tens to hundreds of
+// items, too many for the quadratic in-bucket rank.
+__device__ __noinline__ void sort_group_l2(SortSmem &sm, const uint64_t *stage, int base, int cnt,
+                                           uint64_t glo, uint64_t ghi, int tile,
+                                           const PrepView &pv, const CamK &cam, const SetK &st,
+                                           int32_t *out)
+{
+    int *bend2 = reinterpret_cast<int *>(sm.buf + SORT_GROUP_ITEMS);
+    int s2 = 0;
+    while (((ghi - glo - 1) >> s2) >= (uint64_t)SORT_NB2) ++s2;
+    const BucketFn bf2{(uint32_t)glo, s2, nullptr, 0};
+    for (int d = threadIdx.x; d < SORT_NB2; d += SORT_T) bend2[d] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt; i += SORT_T)
+        atomicAdd(&bend2[bf2(sort_h(stage[base + i]))], 1);
+    __syncthreads();
+    {
+        constexpr int PER = SORT_NB2 / SORT_T;
+        int c[PER], sum = 0;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) { c[q] = bend2[threadIdx.x * PER + q]; sum += c[q]; }
+        int tot;
+        int ex = block_exclusive_scan<int>(sum, sm.scan_w, tot);
+#pragma unroll
+        for (int q = 0; q < PER; ++q) { bend2[threadIdx.x * PER + q] = ex; ex += c[q]; }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt; i += SORT_T) {
+        const uint64_t v = stage[base + i];
+        sm.buf[atomicAdd(&bend2[bf2(sort_h(v))], 1)] = v;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt; i += SORT_T) {
+        const uint64_t x = sm.buf[i];
+        const int d = bf2(sort_h(x));
+        const int b0 = d == 0 ? 0 : bend2[d - 1], b1 = bend2[d];
+        const int r = b1 - b0 == 1 ? 0 : rank_fast(sm.buf, b0, b1, x, tile, pv, cam, st);
+        out[base + b0 + r] = comp_prim(x, st.pbits);
     }
     __syncthreads();
 }
@@ -529,17 +580,23 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
         // groups of consecutive buckets that fit in shared memory: one
         // coalesced bulk load from the L2 staging slice, then warps sort
         // their buckets out of shared memory
+        // lower key bound of first-level bucket d (d = nb: past the top)
+        auto lo_of = [&](int d) -> uint64_t {
+            if (!bf.sp) return (uint64_t)kmin + ((uint64_t)d << shift);
+            if (d == 0) return kmin;
+            return d > bf.ns ? (uint64_t)kmin + range + 1 : (uint64_t)bf.sp[d - 1];
+        };
         int g0 = 0;
         while (g0 < nb) {
             const int base = bucket_start(sm, g0);
-            // last bucket end within SORT_SMEM_ITEMS of base (binary search)
+            // last bucket end within SORT_GROUP_ITEMS of base (binary search)
             int lo = g0 + 1, hi = nb;
             while (lo < hi) {
                 const int mid = (lo + hi + 1) >> 1;
-                if (sm.bend[mid - 1] - base <= SORT_SMEM_ITEMS) lo = mid; else hi = mid - 1;
+                if (sm.bend[mid - 1] - base <= SORT_GROUP_ITEMS) lo = mid; else hi = mid - 1;
             }
             int g1 = lo;
-            if (sm.bend[g1 - 1] - base > SORT_SMEM_ITEMS) {
+            if (sm.bend[g1 - 1] - base > SORT_GROUP_ITEMS) {
                 // one degenerate bucket larger than shared memory: rank it in place
                 const int b1 = sm.bend[g1 - 1];
                 for (int i = base + threadIdx.x; i < b1; i += SORT_T) {
@@ -552,9 +609,15 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
                 continue;
             }
             const int cnt = sm.bend[g1 - 1] - base;
-            for (int i = threadIdx.x; i < cnt; i += SORT_T) sm.buf[i] = stage[base + i];
-            __syncthreads();
-            sort_buckets(sm, sm.buf, base, g0, g1, bf, tile, pv, cam, st, out);
+            if (cnt <= QGS_SORT_L2_MIN * (g1 - g0)) {
+                // first-level buckets already small: rank in them directly
+                for (int i = threadIdx.x; i < cnt; i += SORT_T) sm.buf[i] = stage[base + i];
+                __syncthreads();
+                sort_buckets(sm, sm.buf, base, g0, g1, bf, tile, pv, cam, st, out);
+                g0 = g1;
+                continue;
+            }
+            sort_group_l2(sm, stage, base, cnt, lo_of(g0), lo_of(g1), tile, pv, cam, st, out);
             g0 = g1;
         }
     }
