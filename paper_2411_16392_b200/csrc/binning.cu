@@ -265,7 +265,7 @@ pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
 #define QGS_SORT_T 512
 #endif
 #ifndef QGS_SORT_SMEM_ITEMS
-#define QGS_SORT_SMEM_ITEMS 8192
+#define QGS_SORT_SMEM_ITEMS 6144
 #endif
 #ifndef QGS_SORT_MIN_BLOCKS
 #define QGS_SORT_MIN_BLOCKS 2
