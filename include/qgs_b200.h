@@ -193,6 +193,47 @@ int qgs_trace_pixel(const void *prep, int32_t P, const qgs_camera *cam, const qg
                     int32_t *em_prim, float *em_t, float *em_abar, double *em_T,
                     int32_t *counts, qgs_stream_t stream);
 
+/* ---- Loss producers: the upstream maps for
+ * qgs_backward, computed from the forward's maps in place.  They replace
+ * qgsplat.losses (/root/reference/pkg/src/qgsplat/losses.py) and
+ * qgsplat.ssim (ssim.py); the call sites are train.py:193-211.  All maps are
+ * fp32, row-major (H, W[, C]); arithmetic is fp64; `values` is device fp64.
+ * Gradient outputs are ACCUMULATED (+= weight * d loss / d map) and may be
+ * NULL when only the value is wanted.  Workspace: qgs_loss_workspace_bytes.
+ */
+size_t qgs_loss_workspace_bytes(int32_t H, int32_t W, int32_t C);
+
+/* losses.py:36-50 photometric (1-m) L1 + m (1 - SSIM), ssim.py:41-86 SSIM
+ * (11x11 Gaussian, sigma 1.5, zero padding, crop mean).  C in [1, 4].
+ * values[0] = loss, values[1] = L1 mean, values[2] = SSIM mean (0 when m = 0).
+ * QGS_E_ARG when m > 0 and H or W < 11 (ssim.py:53-54). */
+int qgs_loss_photometric(const float *render, const float *gt, int32_t H, int32_t W,
+                         int32_t C, double lambda_ssim, double weight, float *d_render,
+                         double *values, void *workspace, size_t workspace_bytes,
+                         qgs_stream_t stream);
+
+/* losses.py:53-56: values[0] = mean(distortion); d_dist += weight / (H W). */
+int qgs_loss_distortion(const float *distortion, int32_t H, int32_t W, double weight,
+                        float *d_dist, double *values, void *workspace,
+                        size_t workspace_bytes, qgs_stream_t stream);
+
+/* losses.py:59-89 depth_to_normal: N (H, W, 3) camera-frame normals from
+ * central differences of the back-projected depth (distance along the unit
+ * pixel ray), mask (H, W) u8.  Only intrinsics and size of `cam` are used. */
+int qgs_depth_to_normal(const float *depth, const float *alpha, const qgs_camera *cam,
+                        double alpha_thresh, float *N, uint8_t *mask, qgs_stream_t stream);
+
+/* losses.py:97-113 curvature_guided_normal_consistency.  With depth != NULL
+ * the pseudo ground truth (N, mask) is computed from depth / alpha on the fly
+ * (depth_to_normal fused in; N and mask ignored), else read from N / mask.
+ * values[0] = loss, values[1] = mask count. */
+int qgs_loss_normal_consistency(const float *alpha, const float *normal, const float *curvature,
+                                const float *depth, const float *N, const uint8_t *mask,
+                                const qgs_camera *cam, double alpha_thresh, double eps_curvature,
+                                int32_t guided, double weight, float *d_alpha, float *d_normal,
+                                float *d_curvature, double *values, void *workspace,
+                                size_t workspace_bytes, qgs_stream_t stream);
+
 const char *qgs_last_error(void);
 int qgs_version(void);
 

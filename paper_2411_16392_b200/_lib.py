@@ -88,6 +88,15 @@ def load():
         "qgs_export_prep": (ctypes.c_int, [vp, i32, vp, vp, vp, vp, vp, vp]),
         "qgs_trace_pixel": (ctypes.c_int, [vp, i32, P(Camera), P(Settings), vp, vp, i32, i32,
                                            i32] + [vp] * 9),
+        "qgs_loss_workspace_bytes": (ctypes.c_size_t, [i32, i32, i32]),
+        "qgs_loss_photometric": (ctypes.c_int, [vp, vp, i32, i32, i32, f64, f64, vp, vp, vp,
+                                                ctypes.c_size_t, vp]),
+        "qgs_loss_distortion": (ctypes.c_int, [vp, i32, i32, f64, vp, vp, vp, ctypes.c_size_t,
+                                               vp]),
+        "qgs_depth_to_normal": (ctypes.c_int, [vp, vp, P(Camera), f64, vp, vp, vp]),
+        "qgs_loss_normal_consistency": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, P(Camera), f64, f64,
+                                                       i32, f64, vp, vp, vp, vp, vp,
+                                                       ctypes.c_size_t, vp]),
         "qgs_last_error": (ctypes.c_char_p, []),
         "qgs_version": (ctypes.c_int, []),
     }
@@ -101,7 +110,9 @@ def load():
 
 EXPORTS = ("qgs_prep_bytes", "qgs_preprocess", "qgs_bin_workspace_bytes", "qgs_bin",
            "qgs_sorted_keys", "qgs_tile_keys_f64", "qgs_forward", "qgs_backward", "qgs_chain",
-           "qgs_export_prep", "qgs_trace_pixel", "qgs_last_error", "qgs_version")
+           "qgs_export_prep", "qgs_trace_pixel", "qgs_loss_workspace_bytes",
+           "qgs_loss_photometric", "qgs_loss_distortion", "qgs_depth_to_normal",
+           "qgs_loss_normal_consistency", "qgs_last_error", "qgs_version")
 
 
 def check(rc, what):

@@ -28,6 +28,7 @@ UNITS = {
     # approximate reciprocal / sqrt in the fp32 shading (every decision that
     # must match the reference is confirmed in fp64 first, see shade.cuh)
     "raster_warp.cu": ["-fmad=true", "-prec-div=false", "-prec-sqrt=false", "-ftz=true"],
+    "losses.cu": ["-fmad=false"],
     "abi.cu": [],
 }
 

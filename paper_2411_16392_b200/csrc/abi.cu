@@ -3,6 +3,7 @@
 #include <string>
 
 #include "kernels.cuh"
+#include "losses.cuh"
 
 namespace {
 
@@ -305,6 +306,91 @@ int qgs_export_prep(const void *prep, int32_t P, double *scales, double *alphas,
     qgs::export_prep_kernel<<<cdiv(P, 128), 128, 0, s>>>(pv, P, scales, alphas, colors, pix_bbox,
                                                         planar);
     QGS_LAUNCHED("export_prep_kernel");
+    return 0;
+}
+
+// ------------------------------------------------------------ losses
+
+namespace {
+int check_map(int32_t H, int32_t W)
+{
+    if (H <= 0 || W <= 0 || H > 32767 || W > 32767) return fail(QGS_E_ARG, "map size must be in [1, 32767]");
+    return 0;
+}
+qgs::LossCam loss_cam(const qgs_camera &c)
+{
+    return qgs::LossCam{c.fx, c.fy, c.cx, c.cy, c.width, c.height};
+}
+}  // namespace
+
+size_t qgs_loss_workspace_bytes(int32_t H, int32_t W, int32_t C)
+{
+    return qgs::loss_workspace_bytes(H, W, C);
+}
+
+int qgs_loss_photometric(const float *render, const float *gt, int32_t H, int32_t W, int32_t C,
+                         double lambda_ssim, double weight, float *d_render, double *values,
+                         void *workspace, size_t workspace_bytes, qgs_stream_t stream)
+{
+    if (int rc = check_map(H, W)) return rc;
+    if (!render || !gt || !values || !workspace) return fail(QGS_E_ARG, "NULL argument");
+    if (C < 1 || C > 4) return fail(QGS_E_ARG, "channels must be in [1, 4]");
+    if (!(lambda_ssim >= 0.0 && lambda_ssim <= 1.0))
+        return fail(QGS_E_ARG, "lambda_photo_ssim must lie in [0, 1]");
+    if (lambda_ssim > 0.0 && (H < 11 || W < 11))
+        return fail(QGS_E_ARG, "image smaller than the SSIM window");
+    if (workspace_bytes < qgs::loss_workspace_bytes(H, W, C))
+        return fail(QGS_E_CAPACITY, "loss workspace too small");
+    cudaError_t e = qgs::photometric(render, gt, H, W, C, lambda_ssim, weight, d_render, values,
+                                     workspace, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail("qgs_loss_photometric", e);
+    return 0;
+}
+
+int qgs_loss_distortion(const float *distortion, int32_t H, int32_t W, double weight,
+                        float *d_dist, double *values, void *workspace, size_t workspace_bytes,
+                        qgs_stream_t stream)
+{
+    if (int rc = check_map(H, W)) return rc;
+    if (!distortion || !values || !workspace) return fail(QGS_E_ARG, "NULL argument");
+    if (workspace_bytes < qgs::loss_workspace_bytes(H, W, 1))
+        return fail(QGS_E_CAPACITY, "loss workspace too small");
+    cudaError_t e = qgs::distortion(distortion, H, W, weight, d_dist, values, workspace,
+                                    reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail("qgs_loss_distortion", e);
+    return 0;
+}
+
+int qgs_depth_to_normal(const float *depth, const float *alpha, const qgs_camera *cam,
+                        double alpha_thresh, float *N, uint8_t *mask, qgs_stream_t stream)
+{
+    if (int rc = check_cam(cam)) return rc;
+    if (!depth || !alpha || !N || !mask) return fail(QGS_E_ARG, "NULL argument");
+    cudaError_t e = qgs::depth_to_normal(depth, alpha, loss_cam(*cam), alpha_thresh, N, mask,
+                                         reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail("qgs_depth_to_normal", e);
+    return 0;
+}
+
+int qgs_loss_normal_consistency(const float *alpha, const float *normal, const float *curvature,
+                                const float *depth, const float *N, const uint8_t *mask,
+                                const qgs_camera *cam, double alpha_thresh, double eps_curvature,
+                                int32_t guided, double weight, float *d_alpha, float *d_normal,
+                                float *d_curvature, double *values, void *workspace,
+                                size_t workspace_bytes, qgs_stream_t stream)
+{
+    if (int rc = check_cam(cam)) return rc;
+    if (!alpha || !normal || !values || !workspace) return fail(QGS_E_ARG, "NULL argument");
+    if (guided && !curvature) return fail(QGS_E_ARG, "guided consistency needs the curvature map");
+    if (!depth && (!N || !mask)) return fail(QGS_E_ARG, "need depth, or N and mask");
+    if (workspace_bytes < qgs::loss_workspace_bytes(cam->height, cam->width, 1))
+        return fail(QGS_E_CAPACITY, "loss workspace too small");
+    cudaError_t e = qgs::normal_consistency(alpha, normal, curvature, depth, N, mask,
+                                            loss_cam(*cam), alpha_thresh, eps_curvature, guided,
+                                            weight, d_alpha, d_normal, guided ? d_curvature : nullptr,
+                                            values, workspace,
+                                            reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail("qgs_loss_normal_consistency", e);
     return 0;
 }
 
