@@ -15,7 +15,9 @@ UP_KEYS = ("color", "alpha", "depth", "normal", "curvature", "distortion")
 
 
 def names():
-    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz")))
+    # scenes only (losses.npz holds the loss-producer fixtures, tests/test_losses.py)
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz"))
+                  if os.path.basename(p) != "losses.npz")
 
 
 def load(name):
