@@ -234,6 +234,61 @@ int qgs_loss_normal_consistency(const float *alpha, const float *normal, const f
                                 float *d_curvature, double *values, void *workspace,
                                 size_t workspace_bytes, qgs_stream_t stream);
 
+/* ---- Optimizer step and densification: Adam over
+ * the six groups (optim.py:14-64) and clone / split / prune
+ * (train.py:269-335) on the device.  Call sites: train.py:239-262.  Groups
+ * are in PrimitiveSet order; state (Adam moments) is fp32 with the groups'
+ * shapes; arithmetic is fp64. */
+typedef struct qgs_groups {          /* a writable parameter-group set */
+    float *centers, *quats, *raw_scales, *raw_signs, *raw_opacity, *sh;
+    int32_t P;
+    int32_t sh_coeffs;
+} qgs_groups;
+
+typedef struct qgs_adam_config {
+    double lr[6];                    /* per group */
+    double beta1, beta2, eps;        /* optim.py:15 defaults 0.9, 0.999, 1e-15 */
+    int64_t t;                       /* the step number after the increment */
+    const uint8_t *freeze[6];        /* per-element freeze masks or NULL (optim.py:24) */
+} qgs_adam_config;
+
+typedef struct qgs_densify_stats {   /* train.py:263-267, fp64 */
+    double *grad_accum;              /* P */
+    double *grad_count;              /* P */
+    double *center_accum;            /* P*3 */
+} qgs_densify_stats;
+
+typedef struct qgs_densify_config {  /* config.py:24-43 */
+    double grad_threshold, percent_dense, scene_extent, prune_opacity, clone_nudge;
+    int64_t max_primitives;
+} qgs_densify_config;
+
+/* optim.py:23-47 Adam.step (non-finite gradient rows skip, counted into
+ * *d_skipped; quaternions renormalised), fused with the densification
+ * statistics of train.py:239-244 when stats != NULL. */
+int qgs_adam_step(const qgs_groups *prims, const qgs_grads *grads, const qgs_groups *m,
+                  const qgs_groups *v, const qgs_adam_config *cfg,
+                  const qgs_densify_stats *stats, uint64_t *d_skipped, qgs_stream_t stream);
+
+/* train.py:269-329 in two calls.  plan: decisions and the ordered
+ * compaction offsets into `workspace`; d_counts (device int64[4]) = output
+ * primitives, survivors, clones, split parents (the host reads d_counts[0]
+ * to size the outputs).  apply: writes [survivors | clones | split + |
+ * split -], opacity-pruned, with the survivors' Adam state and zero state
+ * for the new primitives. */
+size_t qgs_densify_workspace_bytes(int32_t P);
+int qgs_densify_plan(const qgs_params *prims, const qgs_densify_stats *stats,
+                     const qgs_densify_config *cfg, void *workspace, size_t workspace_bytes,
+                     int64_t *d_counts, qgs_stream_t stream);
+int qgs_densify_apply(const qgs_params *prims, const qgs_params *m, const qgs_params *v,
+                      const qgs_densify_stats *stats, const qgs_densify_config *cfg,
+                      const void *workspace, const qgs_groups *out, const qgs_groups *out_m,
+                      const qgs_groups *out_v, qgs_stream_t stream);
+
+/* train.py:332-335: opacity capped at `cap` (0.01), its Adam state zeroed. */
+int qgs_reset_opacity(const qgs_groups *prims, const qgs_groups *m, const qgs_groups *v,
+                      double cap, qgs_stream_t stream);
+
 const char *qgs_last_error(void);
 int qgs_version(void);
 

@@ -56,6 +56,25 @@ class Grads(ctypes.Structure):
                                   "raw_opacity", "sh", "screen_center")]
 
 
+class Groups(ctypes.Structure):
+    _fields_ = [(n, vp) for n in ("centers", "quats", "raw_scales", "raw_signs", "raw_opacity",
+                                  "sh")] + [("P", i32), ("sh_coeffs", i32)]
+
+
+class AdamConfig(ctypes.Structure):
+    _fields_ = [("lr", f64 * 6), ("beta1", f64), ("beta2", f64), ("eps", f64), ("t", i64),
+                ("freeze", vp * 6)]
+
+
+class DensifyStats(ctypes.Structure):
+    _fields_ = [("grad_accum", vp), ("grad_count", vp), ("center_accum", vp)]
+
+
+class DensifyConfig(ctypes.Structure):
+    _fields_ = [("grad_threshold", f64), ("percent_dense", f64), ("scene_extent", f64),
+                ("prune_opacity", f64), ("clone_nudge", f64), ("max_primitives", i64)]
+
+
 class QGSError(RuntimeError):
     pass
 
@@ -97,6 +116,15 @@ def load():
         "qgs_loss_normal_consistency": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, P(Camera), f64, f64,
                                                        i32, f64, vp, vp, vp, vp, vp,
                                                        ctypes.c_size_t, vp]),
+        "qgs_adam_step": (ctypes.c_int, [P(Groups), P(Grads), P(Groups), P(Groups),
+                                         P(AdamConfig), P(DensifyStats), vp, vp]),
+        "qgs_densify_workspace_bytes": (ctypes.c_size_t, [i32]),
+        "qgs_densify_plan": (ctypes.c_int, [P(Params), P(DensifyStats), P(DensifyConfig), vp,
+                                            ctypes.c_size_t, vp, vp]),
+        "qgs_densify_apply": (ctypes.c_int, [P(Params), P(Params), P(Params), P(DensifyStats),
+                                             P(DensifyConfig), vp, P(Groups), P(Groups),
+                                             P(Groups), vp]),
+        "qgs_reset_opacity": (ctypes.c_int, [P(Groups), P(Groups), P(Groups), f64, vp]),
         "qgs_last_error": (ctypes.c_char_p, []),
         "qgs_version": (ctypes.c_int, []),
     }
@@ -112,7 +140,9 @@ EXPORTS = ("qgs_prep_bytes", "qgs_preprocess", "qgs_bin_workspace_bytes", "qgs_b
            "qgs_sorted_keys", "qgs_tile_keys_f64", "qgs_forward", "qgs_backward", "qgs_chain",
            "qgs_export_prep", "qgs_trace_pixel", "qgs_loss_workspace_bytes",
            "qgs_loss_photometric", "qgs_loss_distortion", "qgs_depth_to_normal",
-           "qgs_loss_normal_consistency", "qgs_last_error", "qgs_version")
+           "qgs_loss_normal_consistency", "qgs_adam_step", "qgs_densify_workspace_bytes",
+           "qgs_densify_plan", "qgs_densify_apply", "qgs_reset_opacity", "qgs_last_error",
+           "qgs_version")
 
 
 def check(rc, what):

@@ -29,6 +29,7 @@ UNITS = {
     # must match the reference is confirmed in fp64 first, see shade.cuh)
     "raster_warp.cu": ["-fmad=true", "-prec-div=false", "-prec-sqrt=false", "-ftz=true"],
     "losses.cu": ["-fmad=false"],
+    "optim.cu": ["-fmad=false"],
     "abi.cu": [],
 }
 

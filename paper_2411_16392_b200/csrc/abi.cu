@@ -4,6 +4,7 @@
 
 #include "kernels.cuh"
 #include "losses.cuh"
+#include "optim.cuh"
 
 namespace {
 
@@ -391,6 +392,130 @@ int qgs_loss_normal_consistency(const float *alpha, const float *normal, const f
                                             values, workspace,
                                             reinterpret_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail("qgs_loss_normal_consistency", e);
+    return 0;
+}
+
+// ---------------------------------------------------- optimizer / densify
+
+namespace {
+void group_ptrs(const qgs_groups &g, float *out[6])
+{
+    out[0] = g.centers; out[1] = g.quats; out[2] = g.raw_scales;
+    out[3] = g.raw_signs; out[4] = g.raw_opacity; out[5] = g.sh;
+}
+void group_ptrs_ro(const qgs_params &g, const float *out[6])
+{
+    out[0] = g.centers; out[1] = g.quats; out[2] = g.raw_scales;
+    out[3] = g.raw_signs; out[4] = g.raw_opacity; out[5] = g.sh;
+}
+void group_widths(int sh_coeffs, int w[6])
+{
+    w[0] = 3; w[1] = 4; w[2] = 3; w[3] = 3; w[4] = 1; w[5] = 3 * sh_coeffs;
+}
+bool sh_ok(int k) { return k == 1 || k == 4 || k == 9 || k == 16; }
+}  // namespace
+
+int qgs_adam_step(const qgs_groups *prims, const qgs_grads *grads, const qgs_groups *m,
+                  const qgs_groups *v, const qgs_adam_config *cfg,
+                  const qgs_densify_stats *stats, uint64_t *d_skipped, qgs_stream_t stream)
+{
+    if (!prims || !grads || !m || !v || !cfg || !d_skipped) return fail(QGS_E_ARG, "NULL argument");
+    if (prims->P < 0 || !sh_ok(prims->sh_coeffs)) return fail(QGS_E_ARG, "bad parameter set");
+    if (m->P != prims->P || v->P != prims->P || m->sh_coeffs != prims->sh_coeffs ||
+        v->sh_coeffs != prims->sh_coeffs)
+        return fail(QGS_E_ARG, "Adam state does not match the parameters");
+    if (cfg->t < 1) return fail(QGS_E_ARG, "step number must be >= 1");
+    qgs::AdamArgs a{};
+    group_ptrs(*prims, a.p);
+    group_ptrs(*m, a.m);
+    group_ptrs(*v, a.v);
+    const float *g[6] = {grads->centers, grads->quats, grads->raw_scales, grads->raw_signs,
+                         grads->raw_opacity, grads->sh};
+    for (int k = 0; k < 6; ++k) {
+        a.g[k] = g[k];
+        a.freeze[k] = cfg->freeze[k];
+        a.lr[k] = cfg->lr[k];
+        if (!a.p[k] || !a.m[k] || !a.v[k] || !a.g[k]) return fail(QGS_E_ARG, "NULL group");
+    }
+    group_widths(prims->sh_coeffs, a.w);
+    a.b1 = cfg->beta1;
+    a.b2 = cfg->beta2;
+    a.b1c = 1.0 - pow(cfg->beta1, (double)cfg->t);   // optim.py:26-27
+    a.b2c = 1.0 - pow(cfg->beta2, (double)cfg->t);
+    a.eps = cfg->eps;
+    if (stats) {
+        if (!stats->grad_accum || !stats->grad_count || !stats->center_accum || !grads->screen_center)
+            return fail(QGS_E_ARG, "statistics need every buffer and the screen-centre gradient");
+        a.g_screen = grads->screen_center;
+        a.grad_accum = stats->grad_accum;
+        a.grad_count = stats->grad_count;
+        a.center_accum = stats->center_accum;
+    }
+    a.skipped = reinterpret_cast<unsigned long long *>(d_skipped);
+    a.P = prims->P;
+    cudaError_t e = qgs::adam_step(a, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail("qgs_adam_step", e);
+    return 0;
+}
+
+size_t qgs_densify_workspace_bytes(int32_t P) { return qgs::densify_workspace_bytes(P < 0 ? 0 : P); }
+
+int qgs_densify_plan(const qgs_params *prims, const qgs_densify_stats *stats,
+                     const qgs_densify_config *cfg, void *workspace, size_t workspace_bytes,
+                     int64_t *d_counts, qgs_stream_t stream)
+{
+    if (!prims || !stats || !cfg || !workspace || !d_counts) return fail(QGS_E_ARG, "NULL argument");
+    if (prims->P < 0) return fail(QGS_E_ARG, "P < 0");
+    if (workspace_bytes < qgs::densify_workspace_bytes(prims->P))
+        return fail(QGS_E_CAPACITY, "densify workspace too small");
+    qgs::DensifyArgs a{};
+    a.raw_scales = prims->raw_scales;
+    a.raw_signs = prims->raw_signs;
+    a.raw_opacity = prims->raw_opacity;
+    a.grad_accum = stats->grad_accum;
+    a.grad_count = stats->grad_count;
+    a.grad_threshold = cfg->grad_threshold;
+    a.big_threshold = cfg->percent_dense * cfg->scene_extent;
+    a.prune_opacity = cfg->prune_opacity;
+    a.room = (long long)cfg->max_primitives - prims->P;
+    a.P = prims->P;
+    cudaError_t e = qgs::densify_plan(a, workspace, d_counts, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail("qgs_densify_plan", e);
+    return 0;
+}
+
+int qgs_densify_apply(const qgs_params *prims, const qgs_params *m, const qgs_params *v,
+                      const qgs_densify_stats *stats, const qgs_densify_config *cfg,
+                      const void *workspace, const qgs_groups *out, const qgs_groups *out_m,
+                      const qgs_groups *out_v, qgs_stream_t stream)
+{
+    if (!prims || !m || !v || !stats || !cfg || !workspace || !out || !out_m || !out_v)
+        return fail(QGS_E_ARG, "NULL argument");
+    if (!sh_ok(prims->sh_coeffs) || out->sh_coeffs != prims->sh_coeffs)
+        return fail(QGS_E_ARG, "sh_coeffs mismatch");
+    qgs::ApplyArgs a{};
+    group_ptrs_ro(*prims, a.src);
+    group_ptrs_ro(*m, a.m_src);
+    group_ptrs_ro(*v, a.v_src);
+    group_ptrs(*out, a.dst);
+    group_ptrs(*out_m, a.m_dst);
+    group_ptrs(*out_v, a.v_dst);
+    group_widths(prims->sh_coeffs, a.w);
+    a.center_accum = stats->center_accum;
+    a.clone_nudge = cfg->clone_nudge;
+    a.P = prims->P;
+    cudaError_t e = qgs::densify_apply(a, workspace, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail("qgs_densify_apply", e);
+    return 0;
+}
+
+int qgs_reset_opacity(const qgs_groups *prims, const qgs_groups *m, const qgs_groups *v,
+                      double cap, qgs_stream_t stream)
+{
+    if (!prims || !m || !v) return fail(QGS_E_ARG, "NULL argument");
+    cudaError_t e = qgs::reset_opacity(prims->raw_opacity, m->raw_opacity, v->raw_opacity,
+                                       prims->P, cap, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail("qgs_reset_opacity", e);
     return 0;
 }
 
