@@ -29,21 +29,24 @@ constexpr int AD_T = 256;
 __global__ void __launch_bounds__(AD_T)
 adam_kernel(AdamArgs a)
 {
-    __shared__ uint8_t bad[AD_T];
+    __shared__ int bad[AD_T];
     __shared__ int nbad;
     const int p0 = blockIdx.x * AD_T;
     const int np = min(AD_T, a.P - p0);
     const int i = p0 + threadIdx.x;
     if (threadIdx.x == 0) nbad = 0;
+    bad[threadIdx.x] = 0;
+    __syncthreads();
+    // non-finite rows: coalesced sweep of the block's gradient slice
+    for (int g = 0; g < 6; ++g) {
+        const int w = a.w[g];
+        const float *src = a.g[g] + (size_t)p0 * w;
+        for (int e = threadIdx.x; e < np * w; e += AD_T)
+            if (!isfinite(src[e])) bad[e / w] = 1;
+    }
     __syncthreads();
     if (threadIdx.x < np) {
-        bool b = false;
-        for (int g = 0; g < 6; ++g) {
-            const float *row = a.g[g] + (size_t)i * a.w[g];
-            for (int k = 0; k < a.w[g]; ++k) b |= !isfinite(row[k]);
-        }
-        bad[threadIdx.x] = b ? 1 : 0;
-        if (b) atomicAdd(&nbad, 1);
+        if (bad[threadIdx.x]) atomicAdd(&nbad, 1);
         if (a.grad_accum) {
             // train.py:240-244 (before the step; the raw, unmasked gradients)
             const double gx = a.g_screen[2 * (size_t)i], gy = a.g_screen[2 * (size_t)i + 1];
