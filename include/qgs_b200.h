@@ -289,6 +289,34 @@ int qgs_densify_apply(const qgs_params *prims, const qgs_params *m, const qgs_pa
 int qgs_reset_opacity(const qgs_groups *prims, const qgs_groups *m, const qgs_groups *v,
                       double cap, qgs_stream_t stream);
 
+/* ---- Multi-view reprojection + NCC regulariser:
+ * multiview.py:108-311, called at train.py:215-233.  Maps fp32: depth and
+ * alpha (H, W), camera-frame normal (H, W, 3), the ground-truth photo
+ * (H, W, image_channels) reduced to gray by its channel mean. */
+typedef struct qgs_mv_maps {
+    const float *depth, *alpha, *normal, *image;
+    int32_t height, width, image_channels;
+} qgs_mv_maps;
+
+typedef struct qgs_mv_config {       /* multiview.py:17-23 */
+    int32_t patch_size;              /* odd, 7 */
+    double alpha_thresh, min_denom, ncc_eps;
+    int32_t full_chain;
+} qgs_mv_config;
+
+typedef struct qgs_mv_grads {        /* upstream maps the loss accumulates into */
+    float *depth, *alpha, *normal;   /* any may be NULL */
+} qgs_mv_grads;
+
+size_t qgs_multiview_workspace_bytes(int32_t H, int32_t W, int32_t Hn, int32_t Wn);
+/* values (device fp64[4]) = loss, n_valid, mean reprojection error (px), mean
+ * NCC (0, 0, 0, 1 when no pixel is valid).  up_ref / up_nbr (either may
+ * be NULL) ACCUMULATE weight * the loss gradient w.r.t. each view's maps. */
+int qgs_multiview_loss(const qgs_mv_maps *ref, const qgs_camera *cam_ref, const qgs_mv_maps *nbr,
+                       const qgs_camera *cam_nbr, const qgs_mv_config *cfg, double weight,
+                       const qgs_mv_grads *up_ref, const qgs_mv_grads *up_nbr, double *values,
+                       void *workspace, size_t workspace_bytes, qgs_stream_t stream);
+
 const char *qgs_last_error(void);
 int qgs_version(void);
 

@@ -75,6 +75,20 @@ class DensifyConfig(ctypes.Structure):
                 ("prune_opacity", f64), ("clone_nudge", f64), ("max_primitives", i64)]
 
 
+class MvMaps(ctypes.Structure):
+    _fields_ = [(n, vp) for n in ("depth", "alpha", "normal", "image")] + \
+        [("height", i32), ("width", i32), ("image_channels", i32)]
+
+
+class MvConfig(ctypes.Structure):
+    _fields_ = [("patch_size", i32), ("alpha_thresh", f64), ("min_denom", f64),
+                ("ncc_eps", f64), ("full_chain", i32)]
+
+
+class MvGrads(ctypes.Structure):
+    _fields_ = [(n, vp) for n in ("depth", "alpha", "normal")]
+
+
 class QGSError(RuntimeError):
     pass
 
@@ -125,6 +139,10 @@ def load():
                                              P(DensifyConfig), vp, P(Groups), P(Groups),
                                              P(Groups), vp]),
         "qgs_reset_opacity": (ctypes.c_int, [P(Groups), P(Groups), P(Groups), f64, vp]),
+        "qgs_multiview_workspace_bytes": (ctypes.c_size_t, [i32, i32, i32, i32]),
+        "qgs_multiview_loss": (ctypes.c_int, [P(MvMaps), P(Camera), P(MvMaps), P(Camera),
+                                              P(MvConfig), f64, P(MvGrads), P(MvGrads), vp, vp,
+                                              ctypes.c_size_t, vp]),
         "qgs_last_error": (ctypes.c_char_p, []),
         "qgs_version": (ctypes.c_int, []),
     }
@@ -141,7 +159,8 @@ EXPORTS = ("qgs_prep_bytes", "qgs_preprocess", "qgs_bin_workspace_bytes", "qgs_b
            "qgs_export_prep", "qgs_trace_pixel", "qgs_loss_workspace_bytes",
            "qgs_loss_photometric", "qgs_loss_distortion", "qgs_depth_to_normal",
            "qgs_loss_normal_consistency", "qgs_adam_step", "qgs_densify_workspace_bytes",
-           "qgs_densify_plan", "qgs_densify_apply", "qgs_reset_opacity", "qgs_last_error",
+           "qgs_densify_plan", "qgs_densify_apply", "qgs_reset_opacity",
+           "qgs_multiview_workspace_bytes", "qgs_multiview_loss", "qgs_last_error",
            "qgs_version")
 
 

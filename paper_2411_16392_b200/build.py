@@ -30,6 +30,7 @@ UNITS = {
     "raster_warp.cu": ["-fmad=true", "-prec-div=false", "-prec-sqrt=false", "-ftz=true"],
     "losses.cu": ["-fmad=false"],
     "optim.cu": ["-fmad=false"],
+    "multiview.cu": ["-fmad=false"],
     "abi.cu": [],
 }
 

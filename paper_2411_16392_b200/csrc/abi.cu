@@ -5,6 +5,7 @@
 #include "kernels.cuh"
 #include "losses.cuh"
 #include "optim.cuh"
+#include "multiview.cuh"
 
 namespace {
 
@@ -516,6 +517,77 @@ int qgs_reset_opacity(const qgs_groups *prims, const qgs_groups *m, const qgs_gr
     cudaError_t e = qgs::reset_opacity(prims->raw_opacity, m->raw_opacity, v->raw_opacity,
                                        prims->P, cap, reinterpret_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail("qgs_reset_opacity", e);
+    return 0;
+}
+
+// ------------------------------------------------------------ multiview
+
+namespace {
+// multiview.py:31-47 intrinsics and the relative transform X_b = R X_a + T
+void mv_intrinsics(const qgs_camera &c, double K[9], double Kinv[9])
+{
+    const double k[9] = {c.fx, 0.0, c.cx, 0.0, c.fy, c.cy, 0.0, 0.0, 1.0};
+    const double ki[9] = {1.0 / c.fx, 0.0, -c.cx / c.fx, 0.0, 1.0 / c.fy, -c.cy / c.fy, 0.0, 0.0, 1.0};
+    for (int i = 0; i < 9; ++i) { K[i] = k[i]; Kinv[i] = ki[i]; }
+}
+void mv_relative(const qgs_camera &a, const qgs_camera &b, double R[9], double T[3])
+{
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double s = 0.0;
+            for (int k = 0; k < 3; ++k) s += b.R_wc[3 * i + k] * a.R_wc[3 * j + k];
+            R[3 * i + j] = s;
+        }
+    for (int i = 0; i < 3; ++i)
+        T[i] = b.t_wc[i] - (R[3 * i] * a.t_wc[0] + R[3 * i + 1] * a.t_wc[1] + R[3 * i + 2] * a.t_wc[2]);
+}
+}  // namespace
+
+size_t qgs_multiview_workspace_bytes(int32_t H, int32_t W, int32_t Hn, int32_t Wn)
+{
+    return qgs::multiview_workspace_bytes(H, W, Hn, Wn);
+}
+
+int qgs_multiview_loss(const qgs_mv_maps *ref, const qgs_camera *cam_ref, const qgs_mv_maps *nbr,
+                       const qgs_camera *cam_nbr, const qgs_mv_config *cfg, double weight,
+                       const qgs_mv_grads *up_ref, const qgs_mv_grads *up_nbr, double *values,
+                       void *workspace, size_t workspace_bytes, qgs_stream_t stream)
+{
+    if (!ref || !nbr || !cfg || !values || !workspace) return fail(QGS_E_ARG, "NULL argument");
+    if (int rc = check_cam(cam_ref)) return rc;
+    if (int rc = check_cam(cam_nbr)) return rc;
+    const qgs_mv_maps *mm[2] = {ref, nbr};
+    for (const qgs_mv_maps *m : mm) {
+        if (!m->depth || !m->alpha || !m->normal || !m->image) return fail(QGS_E_ARG, "NULL map");
+        if (m->height < 2 || m->width < 2) return fail(QGS_E_ARG, "maps must be at least 2x2");
+        if (m->image_channels < 1 || m->image_channels > 4) return fail(QGS_E_ARG, "image channels in [1, 4]");
+    }
+    if (cfg->patch_size < 1 || cfg->patch_size % 2 == 0 || cfg->patch_size > 31)
+        return fail(QGS_E_ARG, "patch_size must be odd and <= 31");
+    if (workspace_bytes < qgs::multiview_workspace_bytes(ref->height, ref->width, nbr->height, nbr->width))
+        return fail(QGS_E_CAPACITY, "multiview workspace too small");
+    qgs::MvArgs a{};
+    a.D_r = ref->depth; a.A_r = ref->alpha; a.N_r = ref->normal; a.I_r = ref->image;
+    a.D_n = nbr->depth; a.A_n = nbr->alpha; a.N_n = nbr->normal; a.I_n = nbr->image;
+    a.Cr = ref->image_channels; a.Cn = nbr->image_channels;
+    a.H = ref->height; a.W = ref->width; a.Hn = nbr->height; a.Wn = nbr->width;
+    a.fx_r = cam_ref->fx; a.fy_r = cam_ref->fy; a.cx_r = cam_ref->cx; a.cy_r = cam_ref->cy;
+    a.fx_n = cam_nbr->fx; a.fy_n = cam_nbr->fy; a.cx_n = cam_nbr->cx; a.cy_n = cam_nbr->cy;
+    mv_intrinsics(*cam_ref, a.K_r, a.K_r_inv);
+    mv_intrinsics(*cam_nbr, a.K_n, a.K_n_inv);
+    mv_relative(*cam_ref, *cam_nbr, a.R_rn, a.T_rn);
+    mv_relative(*cam_nbr, *cam_ref, a.R_nr, a.T_nr);
+    a.r = cfg->patch_size / 2;
+    a.alpha_thresh = cfg->alpha_thresh;
+    a.min_denom = cfg->min_denom;
+    a.ncc_eps = cfg->ncc_eps;
+    a.full_chain = cfg->full_chain;
+    cudaError_t e = qgs::multiview(
+        a, weight, up_ref ? up_ref->depth : nullptr, up_ref ? up_ref->alpha : nullptr,
+        up_ref ? up_ref->normal : nullptr, up_nbr ? up_nbr->depth : nullptr,
+        up_nbr ? up_nbr->alpha : nullptr, up_nbr ? up_nbr->normal : nullptr, values, workspace,
+        reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail("qgs_multiview_loss", e);
     return 0;
 }
 

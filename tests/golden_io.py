@@ -15,9 +15,9 @@ UP_KEYS = ("color", "alpha", "depth", "normal", "curvature", "distortion")
 
 
 def names():
-    # scenes only (losses.npz / optim.npz: tests/test_losses.py, tests/test_optim.py)
+    # scenes only (losses / optim / multiview fixtures belong to their own tests)
     return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz"))
-                  if os.path.basename(p) not in ("losses.npz", "optim.npz"))
+                  if os.path.basename(p) not in ("losses.npz", "optim.npz", "multiview.npz"))
 
 
 def load(name):
