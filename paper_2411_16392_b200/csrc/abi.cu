@@ -561,9 +561,10 @@ int qgs_multiview_loss(const qgs_mv_maps *ref, const qgs_camera *cam_ref, const 
         if (!m->depth || !m->alpha || !m->normal || !m->image) return fail(QGS_E_ARG, "NULL map");
         if (m->height < 2 || m->width < 2) return fail(QGS_E_ARG, "maps must be at least 2x2");
         if (m->image_channels < 1 || m->image_channels > 4) return fail(QGS_E_ARG, "image channels in [1, 4]");
+        if ((long long)m->height * m->width * 4 >= (1LL << 31)) return fail(QGS_E_ARG, "maps too large");
     }
-    if (cfg->patch_size < 1 || cfg->patch_size % 2 == 0 || cfg->patch_size > 31)
-        return fail(QGS_E_ARG, "patch_size must be odd and <= 31");
+    if (cfg->patch_size < 1 || cfg->patch_size % 2 == 0 || cfg->patch_size > qgs::multiview_max_patch())
+        return fail(QGS_E_ARG, "patch_size must be odd and <= 13");
     if (workspace_bytes < qgs::multiview_workspace_bytes(ref->height, ref->width, nbr->height, nbr->width))
         return fail(QGS_E_CAPACITY, "multiview workspace too small");
     qgs::MvArgs a{};

@@ -12,20 +12,24 @@
 // terms written in place, neighbour terms scattered bilinearly with fp64
 // atomics) and per-CTA partial sums; a finishing CTA folds the sums in a
 // fixed order and the apply kernels scale by weight / n_valid into the fp32
-// upstream maps.  The patch loops recompute the warped points rather than
-// keeping 4 x k^2 doubles per thread.
+// upstream maps.  The warped patch's gray samples are cached in shared
+// memory (fp64, one column per thread); the gradient loop recomputes the
+// warp and the sample derivatives rather than keeping 5 x k^2 values.  One
+// reciprocal per dehomogenised point.
 #include "multiview.cuh"
 
 namespace qgs {
 
 namespace {
 
-constexpr int MV_T = 128;
+constexpr int MV_T = 64;
+constexpr int MV_MAX_KP = 169;                   // patch <= 13 (shared-memory cache, 173 KB)
 
 __device__ __forceinline__ double gray_at(const float *img, int C, int W, int x, int y)
 {
-    const float *p = img + ((size_t)y * W + x) * C;
-    if (C == 1) return (double)p[0];
+    const int i = y * W + x;                    // maps are < 2^31 / 4 elements (ABI check)
+    if (C == 1) return (double)img[i];
+    const float *p = img + i * C;
     double s = 0.0;
     for (int c = 0; c < C; ++c) s += (double)p[c];
     return s / (double)C;                       // multiview.py:26-28 img.mean(axis=2)
@@ -106,15 +110,17 @@ __device__ __forceinline__ Warp warp_point(const double *H, double hx, double hy
     double z = H[6] * hx + H[7] * hy + H[8];
     w.z = z;
     if (fabs(z) < 1e-12) z = 1e-12;
-    w.px = q0 / z;
-    w.py = q1 / z;
+    const double iz = 1.0 / z;
+    w.px = q0 * iz;
+    w.py = q1 * iz;
     return w;
 }
 
-__global__ void __launch_bounds__(MV_T)
+__global__ void __launch_bounds__(MV_T, 6)
 multiview_kernel(MvArgs a)
 {
     __shared__ double red[MV_T / 32][4];
+    extern __shared__ double sbk[];                  // [2][Kp][MV_T] patch samples: warped, reference
     const int W = a.W, H = a.H, r = a.r, k = 2 * r + 1, Kp = k * k;
     const int u = blockIdx.x * 32 + (threadIdx.x & 31);
     const int v = blockIdx.y * (MV_T / 32) + (threadIdx.x >> 5);
@@ -151,12 +157,21 @@ multiview_kernel(MvArgs a)
         for (int i = 0; i < 3; ++i)
             for (int j = 0; j < 3; ++j) Mid[3 * i + j] = a.R_rn[3 * i + j] + a.T_rn[i] * (n[j] / den);
         triple(a.K_n, Mid, a.K_r_inv, Hrn);
-        // every warped patch point in front of the neighbour and inside its frame
+        // every warped patch point in front of the neighbour and inside its
+        // frame; the gray samples of the warped patch go to the cache
+        int ox = -r, oy = -r;
         for (int q = 0; q < Kp && keep; ++q) {
-            const int ox = q % k - r, oy = q / k - r;
             const Warp w = warp_point(Hrn, (double)u + 0.5 + ox, (double)v + 0.5 + oy);
+            sbk[(Kp + q) * MV_T + threadIdx.x] = gray_at(a.I_r, a.Cr, W, u + ox, v + oy);
+            if (++ox > r) { ox = -r; ++oy; }
             keep = w.z > 1e-9 && w.px > 0.6 && w.px < a.Wn - 0.6 && w.py > 0.6 && w.py < a.Hn - 0.6;
             if (q == Kp / 2) wc = w;
+            const Corner c = corner(w.px - 0.5, w.py - 0.5, a.Wn, a.Hn);
+            double b, bx, by;
+            lerp4(gray_at(a.I_n, a.Cn, a.Wn, c.x0, c.y0), gray_at(a.I_n, a.Cn, a.Wn, c.x0 + 1, c.y0),
+                  gray_at(a.I_n, a.Cn, a.Wn, c.x0, c.y0 + 1),
+                  gray_at(a.I_n, a.Cn, a.Wn, c.x0 + 1, c.y0 + 1), c, b, bx, by);
+            sbk[q * MV_T + threadIdx.x] = b;
         }
     }
     // neighbour plane at the warped centre (multiview.py:189-218)
@@ -203,33 +218,26 @@ multiview_kernel(MvArgs a)
     }
     // NCC between the reference patch and the warped neighbour patch
     // (multiview.py:222-235); the patch loops recompute the warp
-    auto sample_b = [&](int q, Warp &w, double &b, double &bx, double &by) {
-        const int ox = q % k - r, oy = q / k - r;
+    auto sample_b = [&](int ox, int oy, Warp &w, double &b, double &bx, double &by) {
         w = warp_point(Hrn, (double)u + 0.5 + ox, (double)v + 0.5 + oy);
         const Corner c = corner(w.px - 0.5, w.py - 0.5, a.Wn, a.Hn);
         lerp4(gray_at(a.I_n, a.Cn, a.Wn, c.x0, c.y0), gray_at(a.I_n, a.Cn, a.Wn, c.x0 + 1, c.y0),
               gray_at(a.I_n, a.Cn, a.Wn, c.x0, c.y0 + 1), gray_at(a.I_n, a.Cn, a.Wn, c.x0 + 1, c.y0 + 1),
               c, b, bx, by);
     };
-    auto sample_a = [&](int q) {
-        return gray_at(a.I_r, a.Cr, W, u + q % k - r, v + q / k - r);
-    };
+    const double *ak = sbk + (size_t)Kp * MV_T + threadIdx.x;
+    auto sample_a = [&](int q) { return ak[q * MV_T]; };
+    const double *bk = sbk + threadIdx.x;
     if (keep) {
         double sa = 0.0, sb = 0.0;
         for (int q = 0; q < Kp; ++q) {
-            Warp w;
-            double b, bx, by;
-            sample_b(q, w, b, bx, by);
             sa += sample_a(q);
-            sb += b;
+            sb += bk[q * MV_T];
         }
         const double ma = sa / Kp, mb = sb / Kp;
         double Va = 0.0, Vb = 0.0, Scc = 0.0;
         for (int q = 0; q < Kp; ++q) {
-            Warp w;
-            double b, bx, by;
-            sample_b(q, w, b, bx, by);
-            const double ca = sample_a(q) - ma, cb = b - mb;
+            const double ca = sample_a(q) - ma, cb = bk[q * MV_T] - mb;
             Va += ca * ca;
             Vb += cb * cb;
             Scc += ca * cb;
@@ -247,22 +255,18 @@ multiview_kernel(MvArgs a)
         const double live = sq > a.ncc_eps ? 1.0 : 0.0;
         const double coef = live * Scc * Va / (denom * denom * denom);
         double md = 0.0;
-        for (int q = 0; q < Kp; ++q) {
-            Warp w;
-            double b, bx, by;
-            sample_b(q, w, b, bx, by);
-            md += (sample_a(q) - ma) / denom - coef * (b - mb);
-        }
+        for (int q = 0; q < Kp; ++q) md += (sample_a(q) - ma) / denom - coef * (bk[q * MV_T] - mb);
         md /= Kp;
-        for (int q = 0; q < Kp; ++q) {
+        for (int q = 0, ox = -r, oy = -r; q < Kp; ++q) {
             Warp w;
             double b, bx, by;
-            sample_b(q, w, b, bx, by);
+            sample_b(ox, oy, w, b, bx, by);
+            if (++ox > r) { ox = -r; ++oy; }
             const double dd = (sample_a(q) - ma) / denom - coef * (b - mb);
             const double gb = -1.0 * (dd - md);
             const double gx = gb * bx, gy = gb * by;
-            const double z = fabs(w.z) < 1e-12 ? 1e-12 : w.z;
-            const double gq[3] = {gx / z, gy / z, -(gx * w.px + gy * w.py) / z};
+            const double iz = 1.0 / (fabs(w.z) < 1e-12 ? 1e-12 : w.z);
+            const double gq[3] = {gx * iz, gy * iz, -(gx * w.px + gy * w.py) * iz};
             const double ph[3] = {w.hx, w.hy, 1.0};
             for (int i = 0; i < 3; ++i)
                 for (int j = 0; j < 3; ++j) gH[3 * i + j] += gq[i] * ph[j];
@@ -425,6 +429,8 @@ inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
 
 }  // namespace
 
+int multiview_max_patch() { return 13; }
+
 size_t multiview_workspace_bytes(int H, int W, int Hn, int Wn)
 {
     const size_t nblk = (size_t)cdiv(W, 32) * cdiv(H, MV_T / 32);
@@ -446,7 +452,15 @@ cudaError_t multiview(MvArgs a, double weight, float *ref_depth, float *ref_alph
     w += al((size_t)nblk * 4 * 8);
     double *scal = reinterpret_cast<double *>(w);
     cudaMemsetAsync(a.g_nbr, 0, (size_t)a.Hn * a.Wn * 4 * 8, s);
-    multiview_kernel<<<grid, MV_T, 0, s>>>(a);
+    const int Kp = (2 * a.r + 1) * (2 * a.r + 1);
+    const size_t smem = (size_t)2 * Kp * MV_T * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(multiview_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(2 * MV_MAX_KP * MV_T * sizeof(double)));
+        attr = true;
+    }
+    multiview_kernel<<<grid, MV_T, smem, s>>>(a);
     mv_finish_kernel<<<1, 256, 0, s>>>(a.partial, nblk, values, scal);
     const int npr = a.H * a.W, npn = a.Hn * a.Wn;
     if (ref_depth || ref_alpha || ref_normal)

@@ -22,6 +22,7 @@ struct MvArgs {
 };
 
 size_t multiview_workspace_bytes(int H, int W, int Hn, int Wn);
+int multiview_max_patch();        // largest odd patch the shared-memory cache holds
 // values (device fp64[4]): loss, n_valid, mean warp error (px), mean NCC
 cudaError_t multiview(MvArgs a, double weight, float *ref_depth, float *ref_alpha,
                       float *ref_normal, float *nbr_depth, float *nbr_alpha, float *nbr_normal,

@@ -162,4 +162,45 @@ if not a.no_cpu:
     t0 = time.perf_counter()
     oo.adam_step(hp, hg, hm, hv, 1, lrs)
     res["cpu_oracle_adam_ms"] = (time.perf_counter() - t0) * 1e3
-print(json.dumps({"workload": f"losses {W}x{H}; adam + densify P={P} SH3", **res}))
+
+# ---- multi-view reprojection + NCC between two C3-size views of a plane
+from paper_2411_16392_b200 import multiview as MV  # noqa: E402
+
+
+class MvCam:
+    def __init__(self, eye_x):
+        self.fx = self.fy = 1400.0
+        self.cx, self.cy = W / 2, H / 2
+        self.width, self.height = W, H
+        w2c = np.eye(4)
+        w2c[:3, 3] = [-eye_x, 0.0, 3.0]
+        self.world_to_camera = w2c
+
+
+def plane_maps(c):
+    uu, vv = np.meshgrid((np.arange(W) + 0.5 - c.cx) / c.fx, (np.arange(H) + 0.5 - c.cy) / c.fy)
+    d = np.stack([uu, vv, np.ones_like(uu)], -1)
+    d /= np.linalg.norm(d, axis=-1, keepdims=True)
+    t = 3.0 / d[..., 2]
+    X = t[..., None] * d - c.world_to_camera[:3, 3]
+    img = 0.5 + 0.25 * np.sin(30 * X[..., 0]) * np.cos(20 * X[..., 1])
+    return {"depth": torch.from_numpy(t.astype(np.float32)).to(dev),
+            "alpha": torch.ones((H, W), device=dev),
+            "normal": torch.tensor([0.0, 0.0, -1.0], device=dev).expand(H, W, 3).contiguous(),
+            "image": torch.from_numpy(img.astype(np.float32)).to(dev)}
+
+
+cr, cn = MvCam(0.0), MvCam(0.05)
+mr, mn = plane_maps(cr), plane_maps(cn)
+up_n = zero_upstream(Cam, dev)
+vals = [None]
+
+
+def mv_step():
+    vals[0] = MV.accumulate_multiview(mr, cr, mn, cn, up, up_n, 0.05)
+
+
+res["multiview_ms"] = timed(mv_step)
+res["multiview_n_valid"] = int(vals[0][1].item())
+print(json.dumps({"workload": f"losses {W}x{H}; adam + densify P={P} SH3; multiview 2x{W}x{H}",
+                  **res}))
