@@ -299,7 +299,7 @@ typedef struct qgs_mv_maps {
 } qgs_mv_maps;
 
 typedef struct qgs_mv_config {       /* multiview.py:17-23 */
-    int32_t patch_size;              /* odd, 7 */
+    int32_t patch_size;              /* odd, <= 13; default 7 */
     double alpha_thresh, min_denom, ncc_eps;
     int32_t full_chain;
 } qgs_mv_config;
