@@ -310,7 +310,7 @@ def run_ours(a):
 
 def run_e2e(a, rz, sc, mine, device, st, world):
     import torch.distributed as dist
-    from paper_2411_16392_b200.dist import pipelined_prepare
+    from paper_2411_16392_b200.dist import pipelined_prepare, upload_async
     pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory()  # noqa: E731
     host = type("H", (), {})()
     for f in rz.DevicePrimitives.FIELDS:
@@ -321,14 +321,21 @@ def run_e2e(a, rz, sc, mine, device, st, world):
     out_host = None
     side = torch.cuda.Stream(device=device)
 
+    copy = torch.cuda.Stream(device=device)
+    dev_ups = [{k: torch.empty(t.shape, dtype=t.dtype, device=device) for k, t in u.items()}
+               for u in ups]
+
     def step():
         nonlocal out_host
         dev = rz.DevicePrimitives.from_host(host, device, non_blocking=True)
+        # every view's upstream maps go over on a copy stream under the raster
+        evs = upload_async(ups, dev_ups, copy)
         grads = rz.GradientBuffer.zeros_flat(dev)
+        main = torch.cuda.current_stream()
         for i, v, prep in pipelined_prepare(dev, sc.cams, mine, st, side):
-            up = {k: t.to(device, non_blocking=True) for k, t in ups[i].items()}
             tg = rz.forward(prep)
-            rz.backward(prep, tg, up, out=grads)
+            main.wait_event(evs[i])
+            rz.backward(prep, tg, dev_ups[i], out=grads)
         if world > 1:
             dist.all_reduce(grads.buffer)
         if out_host is None:

@@ -105,6 +105,26 @@ def pipelined_prepare(dev_prims, cams, views, settings, side=None):
         nxt = launch(views[i + 1]) if i + 1 < len(views) else None
 
 
+def upload_async(host_items, dev_items, copy=None):
+    """Copy a list of dicts of pinned host tensors into the matching device
+    tensors (allocated once by the caller) on a copy stream; returns one
+    event per dict.  The caller's stream waits on event i before using dict
+    i, so the transfers overlap earlier work (e.g. every view's upstream maps
+    while the first views rasterize)."""
+    main = torch.cuda.current_stream()
+    copy = copy if copy is not None else torch.cuda.Stream(device=main.device)
+    copy.wait_stream(main)                   # the previous step is done with the buffers
+    evs = []
+    with torch.cuda.stream(copy):
+        for h, d in zip(host_items, dev_items):
+            for k, t in h.items():
+                d[k].copy_(t, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy)
+            evs.append(ev)
+    return evs
+
+
 def gpu_step(dev_prims, cams, upstreams, settings, rank, world, grads=None, group=None):
     """The B200 step used by bench.py: this rank's views through the sm_100a
     rasterizer, gradients accumulated in one flat device buffer, one NCCL
