@@ -75,8 +75,6 @@ int configure()
     if (smem_configured) return 0;
     QGS_CK(cudaFuncSetAttribute(qgs::tile_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)qgs::sort_smem_bytes()));
-    QGS_CK(cudaFuncSetAttribute(qgs::tile_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                qgs::ORDER_SMEM));
     smem_configured = true;
     return 0;
 }

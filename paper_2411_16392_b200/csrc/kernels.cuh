@@ -50,7 +50,7 @@ __global__ void trace_pixel_kernel(const PrimRec *recs, const Geo64 *geo, const 
                                    int *counts);
 __global__ void tile_order_kernel(const int32_t *tile_offsets, int n_tiles, int32_t *order,
                                   int heavy_only);
-constexpr int ORDER_SMEM = 16384 * 8;
+constexpr int ORDER_SMEM = 0;      // static shared memory only
 constexpr int RASTER_THREADS = 32;   // one warp per 8x4 block, 8 blocks per tile
 constexpr int RASTER_BLOCKS_PER_TILE = 8;
 

@@ -1163,45 +1163,57 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
 // ===================================================== raster schedule
 // tiles by descending pair count (ties by tile), so the raster kernels start
 // the longest tiles first; one CTA, bitonic sort of (~count, tile) in smem
-constexpr int ORDER_MAX = 16384;
-// heavy_only: only tiles over 4x the mean count move to the front (by
-// count); the rest keep their natural order (memory locality of the sort)
+// Schedules (one CTA): tiles grouped by pair count -- quarter-octave bins,
+// largest first, index order inside a bin (a stable counting sort; the
+// schedule only has to put long tiles early, not order them exactly).
+// heavy_only: only tiles over 4x the mean count move to the front; the
+// rest keep their natural order (memory locality of the sort).
+constexpr int ORDER_BINS = 129;                 // 128 count bins + "unranked"
 __global__ void __launch_bounds__(1024)
 tile_order_kernel(const int32_t *__restrict__ tile_offsets, int n_tiles, int32_t *order,
                   int heavy_only)
 {
-    extern __shared__ unsigned long long ord[];
-    if (n_tiles > ORDER_MAX) {                  // natural order
-        for (int i = threadIdx.x; i < n_tiles; i += blockDim.x) order[i] = i;
-        return;
-    }
-    int n2 = 1;
-    while (n2 < n_tiles) n2 <<= 1;
+    __shared__ int hist[ORDER_BINS], run[ORDER_BINS];
+    __shared__ int wcnt[32][ORDER_BINS];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const double heavy = 4.0 * (double)tile_offsets[n_tiles] / (double)max(n_tiles, 1);
-    for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-        unsigned long long k = ~0ull;
-        if (i < n_tiles) {
-            const uint32_t cnt = (uint32_t)(tile_offsets[i + 1] - tile_offsets[i]);
-            if (!heavy_only || (double)cnt > heavy)
-                k = ((unsigned long long)(0x7fffffffu - cnt) << 32) | (uint32_t)i;
-            else
-                k = (1ull << 63) | (uint32_t)i;
-        }
-        ord[i] = k;
+    auto bin_of = [&](int t) {
+        const int cnt = tile_offsets[t + 1] - tile_offsets[t];
+        if (heavy_only && !((double)cnt > heavy)) return ORDER_BINS - 1;
+        const int key = (int)floorf(4.f * __log2f((float)cnt + 1.f));
+        return max(0, 127 - min(key, 127));
+    };
+    for (int b = threadIdx.x; b < ORDER_BINS; b += blockDim.x) { hist[b] = 0; run[b] = 0; }
+    for (int b = threadIdx.x; b < 32 * ORDER_BINS; b += blockDim.x) (&wcnt[0][0])[b] = 0;
+    __syncthreads();
+    for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) atomicAdd(&hist[bin_of(t)], 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {                     // exclusive scan of the bins
+        int acc = 0;
+        for (int b = 0; b < ORDER_BINS; ++b) { const int c = hist[b]; hist[b] = acc; acc += c; }
     }
     __syncthreads();
-    for (int k = 2; k <= n2; k <<= 1)
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-                const int l = i ^ j;
-                if (l > i) {
-                    const unsigned long long a = ord[i], b = ord[l];
-                    if ((a > b) == ((i & k) == 0)) { ord[i] = b; ord[l] = a; }
-                }
-            }
-            __syncthreads();
+    for (int c0 = 0; c0 < n_tiles; c0 += blockDim.x) {
+        const int t = c0 + threadIdx.x;
+        const bool ok = t < n_tiles;
+        const int b = ok ? bin_of(t) : ORDER_BINS;   // ORDER_BINS: no tile
+        const unsigned peers = __match_any_sync(0xffffffffu, b);
+        const int r = __popc(peers & ((1u << lane) - 1u));
+        if (ok && r == 0) wcnt[w][b] = __popc(peers);
+        __syncthreads();
+        if (ok) {
+            int pre = 0;
+            for (int k = 0; k < w; ++k) pre += wcnt[k][b];
+            order[hist[b] + run[b] + pre + r] = t;
         }
-    for (int i = threadIdx.x; i < n_tiles; i += blockDim.x) order[i] = (int32_t)(uint32_t)ord[i];
+        __syncthreads();
+        for (int bb = threadIdx.x; bb < ORDER_BINS; bb += blockDim.x) {
+            int tot = 0;
+            for (int k = 0; k < 32; ++k) { tot += wcnt[k][bb]; wcnt[k][bb] = 0; }
+            run[bb] += tot;
+        }
+        __syncthreads();
+    }
 }
 
 // ============================================================ diagnostics

@@ -221,3 +221,20 @@ def test_conic_cull_is_exact_full_view(rz, cfg):
     sc = scenes.CONFIGS[cfg]()
     _cull_pair(rz, sc.prims, sc.cams[0], rz.RenderSettings())
     _cull_pair(rz, sc.prims, sc.cams[1], rz.RenderSettings(euclidean_density=True))
+
+
+@pytest.mark.gpu
+def test_tile_schedule_is_a_permutation(cuda_device):
+    """raster schedule (tile_order_kernel): every tile exactly once, pair
+    counts non-increasing up to the quarter-octave binning"""
+    from paper_2411_16392_b200 import rasterizer as rz, scenes
+    sc = scenes.CONFIGS["c2"]()
+    prep = rz.prepare(rz.DevicePrimitives.from_host(sc.prims), sc.cams[0])
+    tg = rz.forward(prep)
+    order = tg.tile_order.cpu().numpy()
+    n_tiles = prep.tile_offsets.numel() - 1
+    assert np.array_equal(np.sort(order), np.arange(n_tiles))
+    cnt = np.diff(prep.tile_offsets.cpu().numpy())[order]
+    key = np.floor(4 * np.log2(cnt.astype(np.float64) + 1))
+    assert np.all(np.diff(key) <= 1)           # the kernel bins with an fp32 log2
+    assert key[0] >= key.max() - 1
