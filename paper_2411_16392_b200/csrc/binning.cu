@@ -341,7 +341,7 @@ __device__ __forceinline__ int bucket_start(const SortSmem &sm, int d)
 // the key, so bucket order is key order.
 constexpr int SORT_SPLIT = 4095;                 // most splitters (a sample of 4096)
 #ifndef QGS_SORT_SKEW
-#define QGS_SORT_SKEW 64
+#define QGS_SORT_SKEW 128
 #endif
 constexpr int SORT_SKEW = QGS_SORT_SKEW;         // largest linear bucket tolerated
 struct BucketFn {

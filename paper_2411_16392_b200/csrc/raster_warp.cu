@@ -37,6 +37,9 @@
 namespace qgs {
 
 // minimum resident warps per SM the register allocation must allow
+#ifndef QGS_FWD_LIST_PREFETCH
+#define QGS_FWD_LIST_PREFETCH 1
+#endif
 #ifndef QGS_BWD_MIN_BLOCKS
 #define QGS_BWD_MIN_BLOCKS 20
 #endif
@@ -646,18 +649,43 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         qn += __popc(keep);
         __syncwarp();
     };
+#if QGS_FWD_LIST_PREFETCH
+    // list windows software-pipelined: the ids of window w+2 and the culled
+    // boxes of window w+1 are in flight while window w is processed
+    auto ld_id = [&](int b) { return b + lane < end ? __ldg(tile_prims + b + lane) : 0; };
+    auto ld_bb = [&](int b, int p) {
+        return (cull && b + lane < end) ? __ldg(reinterpret_cast<const uint2 *>(&conics[p].bb_u))
+                                        : make_uint2(0u, 0u);
+    };
+    int id1 = ld_id(start), id2 = ld_id(start + 32);
+    uint2 bb1 = ld_bb(start, id1);
+#endif
     for (int b0 = start; b0 < end; b0 += 32) {
         const uint32_t live = __ballot_sync(FULL, alive);
         if (!live) break;
         const int nb = min(32, end - b0);
         int pj = 0;
         uint32_t bm = 0u;
+#if QGS_FWD_LIST_PREFETCH
+        const int pcur = id1;
+        const uint2 bcur = bb1;
+        id1 = id2;
+        bb1 = ld_bb(b0 + 32, id1);
+        id2 = ld_id(b0 + 64);
+#endif
         if (lane < nb) {
+#if QGS_FWD_LIST_PREFETCH
+            pj = pcur;
+            if (cull) {
+                bm = block_lanes(bcur.x, bcur.y, bu, bv);
+            } else {
+#else
             pj = tile_prims[b0 + lane];
             if (cull) {
                 const uint2 bb = *reinterpret_cast<const uint2 *>(&conics[pj].bb_u);
                 bm = block_lanes(bb.x, bb.y, bu, bv);
             } else {
+#endif
                 bm = block_lanes(recs[pj].bb_u, recs[pj].bb_v, bu, bv);
             }
             if (out.counters)                  // algorithmic work: the reference's pixel box
