@@ -23,6 +23,13 @@ namespace qgs {
 namespace {
 
 constexpr int MV_T = 64;
+#ifndef QGS_MV_CACHE_A
+#define QGS_MV_CACHE_A 1            // cache the reference patch's gray samples too
+#endif
+#ifndef QGS_MV_MINB
+#define QGS_MV_MINB 6
+#endif
+constexpr int MV_NCACHE = QGS_MV_CACHE_A ? 2 : 1;
 constexpr int MV_MAX_KP = 169;                   // patch <= 13 (shared-memory cache, 173 KB)
 
 __device__ __forceinline__ double gray_at(const float *img, int C, int W, int x, int y)
@@ -116,7 +123,7 @@ __device__ __forceinline__ Warp warp_point(const double *H, double hx, double hy
     return w;
 }
 
-__global__ void __launch_bounds__(MV_T, 6)
+__global__ void __launch_bounds__(MV_T, QGS_MV_MINB)
 multiview_kernel(MvArgs a)
 {
     __shared__ double red[MV_T / 32][4];
@@ -162,7 +169,9 @@ multiview_kernel(MvArgs a)
         int ox = -r, oy = -r;
         for (int q = 0; q < Kp && keep; ++q) {
             const Warp w = warp_point(Hrn, (double)u + 0.5 + ox, (double)v + 0.5 + oy);
+#if QGS_MV_CACHE_A
             sbk[(Kp + q) * MV_T + threadIdx.x] = gray_at(a.I_r, a.Cr, W, u + ox, v + oy);
+#endif
             if (++ox > r) { ox = -r; ++oy; }
             keep = w.z > 1e-9 && w.px > 0.6 && w.px < a.Wn - 0.6 && w.py > 0.6 && w.py < a.Hn - 0.6;
             if (q == Kp / 2) wc = w;
@@ -225,8 +234,12 @@ multiview_kernel(MvArgs a)
               gray_at(a.I_n, a.Cn, a.Wn, c.x0, c.y0 + 1), gray_at(a.I_n, a.Cn, a.Wn, c.x0 + 1, c.y0 + 1),
               c, b, bx, by);
     };
+#if QGS_MV_CACHE_A
     const double *ak = sbk + (size_t)Kp * MV_T + threadIdx.x;
     auto sample_a = [&](int q) { return ak[q * MV_T]; };
+#else
+    auto sample_a = [&](int q) { return gray_at(a.I_r, a.Cr, W, u + q % k - r, v + q / k - r); };
+#endif
     const double *bk = sbk + threadIdx.x;
     if (keep) {
         double sa = 0.0, sb = 0.0;
@@ -453,11 +466,11 @@ cudaError_t multiview(MvArgs a, double weight, float *ref_depth, float *ref_alph
     double *scal = reinterpret_cast<double *>(w);
     cudaMemsetAsync(a.g_nbr, 0, (size_t)a.Hn * a.Wn * 4 * 8, s);
     const int Kp = (2 * a.r + 1) * (2 * a.r + 1);
-    const size_t smem = (size_t)2 * Kp * MV_T * sizeof(double);
+    const size_t smem = (size_t)MV_NCACHE * Kp * MV_T * sizeof(double);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(multiview_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(2 * MV_MAX_KP * MV_T * sizeof(double)));
+                             (int)(MV_NCACHE * MV_MAX_KP * MV_T * sizeof(double)));
         attr = true;
     }
     multiview_kernel<<<grid, MV_T, smem, s>>>(a);
