@@ -227,7 +227,7 @@ def _rot_to_quat(Rm):
 
 
 def small_scene(seed, n=12, res=32, sh_deg=1, spread=0.6, z_span=1.5, curved=True,
-                opacity=(0.3, 0.9), eye=(0.0, 0.0, 5.0), focal=None):
+                opacity=(0.3, 0.9), eye=(0.0, 0.0, 5.0), focal=None, width=None, height=None):
     """Small stacked-primitives scene in the style of the reference's unit
     tests (primitives spread in x/y, stacked in z, camera on +z)."""
     rng = np.random.default_rng(seed)
@@ -246,11 +246,12 @@ def small_scene(seed, n=12, res=32, sh_deg=1, spread=0.6, z_span=1.5, curved=Tru
     op = rng.uniform(*opacity, n)
     logit = np.log(op / (1 - op))
     focal = focal or res * 1.2
-    cam = Camera(fx=focal, fy=focal, cx=res / 2, cy=res / 2, width=res, height=res,
+    W, H = width or res, height or res             # ragged sizes: partial tiles and blocks
+    cam = Camera(fx=focal, fy=focal, cx=W / 2, cy=H / 2, width=W, height=H,
                  world_to_camera=look_at(eye, np.zeros(3)))
     ups = _upstream(rng, [cam], all_six=True)
     return _pack(f"small{seed}", c, q, rs, sg, logit, sh, [cam], ups,
-                 {"N": n, "res": [res, res], "sh_deg": sh_deg, "views": 1})
+                 {"N": n, "res": [W, H], "sh_deg": sh_deg, "views": 1})
 
 
 CONFIGS = {"c1": config1, "c2": config2, "c3": config3, "c4": config4, "c5": config5}

@@ -112,7 +112,28 @@ def run(name, prims32, cam, upstream, settings_kw):
           f"viol={tg.order_violations} -> {os.path.getsize(path) / 1e3:.0f} kB")
 
 
+VARIANTS = [
+    ("s_default", dict(seed=0), {}),
+    ("s_background", dict(seed=1), {"background": (0.1, 0.2, 0.3)}),
+    ("s_resort_off", dict(seed=2), {"resort": False}),
+    ("s_euclid", dict(seed=3), {"euclidean_density": True}),
+    ("s_planar", dict(seed=4, curved=False), {}),
+    ("s_overflow", dict(seed=5, n=40, spread=0.4, z_span=0.5, opacity=(0.2, 0.5)), {}),
+    ("s_sh3", dict(seed=6, sh_deg=3, n=20), {"background": (0.25, 0.25, 0.25)}),
+    ("s_sh2", dict(seed=7, sh_deg=2, n=16, res=24), {}),
+    # ragged image: partial tiles and partial 8x4 raster blocks on both axes
+    ("s_ragged", dict(seed=8, n=30, res=32, width=37, height=29), {}),
+]
+
+
 def main():
+    only = set(sys.argv[1:])           # optional: regenerate just these fixtures
+    if only:
+        for name, kw, st in VARIANTS:
+            if name in only:
+                sc = scenes.small_scene(**kw)
+                run(name, sc.prims, sc.cams[0], sc.upstream[0], st)
+        return
     sc = scenes.config1()
     run("c1", sc.prims, sc.cams[0], sc.upstream[0], {})
     # reduced C2 / C5 shapes (SH3, heavy overlap, buffer overflow, degenerate)
@@ -123,17 +144,7 @@ def main():
     sc = scenes.config3(seed=13, n=5000, width=128, height=96, views=1)
     run("c3_small", sc.prims, sc.cams[0], sc.upstream[0], {})
     # unit-test style scenes with every setting variant
-    variants = [
-        ("s_default", dict(seed=0), {}),
-        ("s_background", dict(seed=1), {"background": (0.1, 0.2, 0.3)}),
-        ("s_resort_off", dict(seed=2), {"resort": False}),
-        ("s_euclid", dict(seed=3), {"euclidean_density": True}),
-        ("s_planar", dict(seed=4, curved=False), {}),
-        ("s_overflow", dict(seed=5, n=40, spread=0.4, z_span=0.5, opacity=(0.2, 0.5)), {}),
-        ("s_sh3", dict(seed=6, sh_deg=3, n=20), {"background": (0.25, 0.25, 0.25)}),
-        ("s_sh2", dict(seed=7, sh_deg=2, n=16, res=24), {}),
-    ]
-    for name, kw, st in variants:
+    for name, kw, st in VARIANTS:
         sc = scenes.small_scene(**kw)
         run(name, sc.prims, sc.cams[0], sc.upstream[0], st)
 
