@@ -72,8 +72,18 @@ def _photometric_dev(render, gt, lambda_photo_ssim, weight, d_render, values):
         _ptr(values), _ptr(ws), ws.numel(), _stream()), "qgs_loss_photometric")
 
 
+def _check_images(render, gt, lambda_photo_ssim):
+    """losses.py:40-41 and ssim.py:53-54, on the host before any transfer"""
+    rs, gs = tuple(np.shape(render)), tuple(np.shape(gt))
+    if rs != gs:
+        raise ValueError(f"image shapes differ: {rs} vs {gs}")
+    if lambda_photo_ssim > 0 and (rs[0] < 11 or rs[1] < 11):
+        raise ValueError("image smaller than the SSIM window")
+
+
 def photometric(render, gt, lambda_photo_ssim=0.2):
     """losses.py:36-50: (1-m) L1 + m (1 - SSIM); returns (value, d/d render)."""
+    _check_images(render, gt, lambda_photo_ssim)
     render, gt = _dev(render), _dev(gt)
     g = torch.zeros_like(render)
     values = torch.zeros((3,), dtype=torch.float64, device=render.device)

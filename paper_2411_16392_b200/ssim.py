@@ -5,6 +5,7 @@ The kernels are the photometric loss's (csrc/losses.cu) run with the SSIM
 weight at 1, where the loss gradient is exactly -dSSIM/dx.
 """
 
+import numpy as np
 import torch
 
 from .losses import _dev, _photometric_dev
@@ -18,13 +19,14 @@ C2 = 0.03 ** 2
 def ssim(x, y, return_grad=False):
     """ssim.py:41-86: mean SSIM over the valid (crop) region, averaged over
     channels; with return_grad also dSSIM/dx (CUDA fp32, the shape of x)."""
-    xd, yd = _dev(x), _dev(y)
-    if xd.shape != yd.shape:
+    xs, ys = tuple(np.shape(x)), tuple(np.shape(y))
+    if xs != ys:
         raise ValueError("image shapes differ")
-    if xd.dim() not in (2, 3):
+    if len(xs) not in (2, 3):
         raise ValueError("images must be (H, W) or (H, W, C)")
-    if xd.shape[0] < WINDOW or xd.shape[1] < WINDOW:
+    if xs[0] < WINDOW or xs[1] < WINDOW:
         raise ValueError("image smaller than the SSIM window")
+    xd, yd = _dev(x), _dev(y)
     values = torch.zeros((3,), dtype=torch.float64, device=xd.device)
     g = torch.zeros_like(xd) if return_grad else None
     _photometric_dev(xd, yd, 1.0, 1.0, g, values)

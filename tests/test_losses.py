@@ -330,3 +330,20 @@ def test_full_size_losses_against_oracle(cuda_device):
     close_map(dn.cpu().numpy(), dno)
     close_map(dk.cpu().numpy(), dko)
     torch.cuda.synchronize()
+
+
+def test_host_validation_without_device():
+    """shape / window errors are raised on the host, before any transfer"""
+    from paper_2411_16392_b200 import losses as L
+    from paper_2411_16392_b200 import ssim as S
+    with pytest.raises(ValueError):
+        L.photometric(np.zeros((4, 4, 3)), np.zeros((5, 4, 3)))
+    with pytest.raises(ValueError, match="SSIM window"):
+        L.photometric(np.zeros((8, 40, 3)), np.zeros((8, 40, 3)), 0.2)
+    with pytest.raises(ValueError):
+        S.ssim(np.zeros((12, 12)), np.zeros((12, 13)))
+    with pytest.raises(ValueError):
+        S.ssim(np.zeros((10, 12)), np.zeros((10, 12)))
+    with pytest.raises(ValueError):
+        S.ssim(np.zeros((12,)), np.zeros((12,)))
+
