@@ -27,7 +27,7 @@ constexpr int MV_T = 64;
 #define QGS_MV_CACHE_A 1            // cache the reference patch's gray samples too
 #endif
 #ifndef QGS_MV_MINB
-#define QGS_MV_MINB 6
+#define QGS_MV_MINB 4               // shared memory allows 4 CTAs anyway: no register cap, no spills
 #endif
 constexpr int MV_NCACHE = QGS_MV_CACHE_A ? 2 : 1;
 constexpr int MV_MAX_KP = 169;                   // patch <= 13 (shared-memory cache, 173 KB)
