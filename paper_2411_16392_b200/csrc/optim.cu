@@ -41,8 +41,9 @@ adam_kernel(AdamArgs a)
     for (int g = 0; g < 6; ++g) {
         const int w = a.w[g];
         const float *src = a.g[g] + (size_t)p0 * w;
+        const float iw = 1.f / (float)w;
         for (int e = threadIdx.x; e < np * w; e += AD_T)
-            if (!isfinite(src[e])) bad[e / w] = 1;
+            if (!isfinite(src[e])) bad[(int)(((float)e + 0.5f) * iw)] = 1;
     }
     __syncthreads();
     if (threadIdx.x < np) {
@@ -60,18 +61,21 @@ adam_kernel(AdamArgs a)
     }
     __syncthreads();
     if (threadIdx.x == 0 && nbad) atomicAdd(a.skipped, (unsigned long long)nbad);
+    const double ib1c = 1.0 / a.b1c, ib2c = 1.0 / a.b2c;   // bias corrections as products
     for (int g = 0; g < 6; ++g) {
         const int w = a.w[g];
+        const float iw = 1.f / (float)w;        // row of element e: (e + 0.5) / w is >= 0.5 / w from any integer
         const size_t e0 = (size_t)p0 * w;
         const int ne = np * w;
         const double lr = a.lr[g];
+#pragma unroll 4
         for (int e = threadIdx.x; e < ne; e += AD_T) {
             const size_t idx = e0 + e;
-            double grad = bad[e / w] ? 0.0 : (double)a.g[g][idx];
+            double grad = bad[(int)(((float)e + 0.5f) * iw)] ? 0.0 : (double)a.g[g][idx];
             if (a.freeze[g] && a.freeze[g][idx]) grad = 0.0;
             const double m = a.b1 * (double)a.m[g][idx] + (1.0 - a.b1) * grad;
             const double v = a.b2 * (double)a.v[g][idx] + (1.0 - a.b2) * grad * grad;
-            const double mhat = m / a.b1c, vhat = v / a.b2c;
+            const double mhat = m * ib1c, vhat = v * ib2c;
             a.m[g][idx] = (float)m;
             a.v[g][idx] = (float)v;
             a.p[g][idx] = (float)((double)a.p[g][idx] - lr * mhat / (sqrt(vhat) + a.eps));
