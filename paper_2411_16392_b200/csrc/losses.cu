@@ -28,6 +28,7 @@ constexpr int SS_T = 32;                 // output tile edge
 constexpr int SS_R = 5;                  // window radius (WINDOW 11)
 constexpr int SS_E = SS_T + 2 * SS_R;    // staged edge (42)
 constexpr int SS_THREADS = 256;
+constexpr int SS_VB = 4;                 // outputs per thread along a blur (register run)
 constexpr double SS_C1 = 0.01 * 0.01;    // ssim.py:15
 constexpr double SS_C2 = 0.03 * 0.03;    // ssim.py:16
 
@@ -107,36 +108,58 @@ ssim_moments_kernel(const float *__restrict__ x, const float *__restrict__ y, in
             sm.in[1][r][q] = yv;
         }
         __syncthreads();
-        // first blur: along image rows (axis 0), for every staged column
-        for (int i = threadIdx.x; i < SS_T * SS_E; i += SS_THREADS) {
-            const int r = i / SS_E, q = i - r * SS_E;
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
+        // first blur: along image rows (axis 0), for every staged column;
+        // a thread slides down SS_VB output rows of one column, so each
+        // staged value is read once per run instead of once per tap
+        for (int it = threadIdx.x; it < SS_E * (SS_T / SS_VB); it += SS_THREADS) {
+            const int q = it % SS_E, r0 = (it / SS_E) * SS_VB;
+            double xs[SS_VB + 2 * SS_R], ys[SS_VB + 2 * SS_R];
 #pragma unroll
-            for (int k = 0; k <= 2 * SS_R; ++k) {
-                const double g = gk.k[k];
-                const double xv = sm.in[0][r + k][q], yv = sm.in[1][r + k][q];
-                a0 += g * xv;
-                a1 += g * yv;
-                a2 += g * (xv * xv);
-                a3 += g * (yv * yv);
-                a4 += g * (xv * yv);
+            for (int k = 0; k < SS_VB + 2 * SS_R; ++k) {
+                xs[k] = sm.in[0][r0 + k][q];
+                ys[k] = sm.in[1][r0 + k][q];
             }
-            sm.vb[0][r][q] = a0; sm.vb[1][r][q] = a1; sm.vb[2][r][q] = a2;
-            sm.vb[3][r][q] = a3; sm.vb[4][r][q] = a4;
+#pragma unroll
+            for (int o = 0; o < SS_VB; ++o) {
+                double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
+#pragma unroll
+                for (int k = 0; k <= 2 * SS_R; ++k) {
+                    const double g = gk.k[k];
+                    const double xv = xs[o + k], yv = ys[o + k];
+                    a0 += g * xv;
+                    a1 += g * yv;
+                    a2 += g * (xv * xv);
+                    a3 += g * (yv * yv);
+                    a4 += g * (xv * yv);
+                }
+                sm.vb[0][r0 + o][q] = a0; sm.vb[1][r0 + o][q] = a1; sm.vb[2][r0 + o][q] = a2;
+                sm.vb[3][r0 + o][q] = a3; sm.vb[4][r0 + o][q] = a4;
+            }
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < SS_T * SS_T; i += SS_THREADS) {
-            const int r = i >> 5, q = i & (SS_T - 1);
-            const int u = u0 + q, v = v0 + r;
-            double m[5];
+        // second blur along axis 1: SS_VB consecutive outputs of a row per thread
+        for (int it = threadIdx.x; it < SS_T * (SS_T / SS_VB); it += SS_THREADS) {
+            const int r = it / (SS_T / SS_VB), q0 = (it % (SS_T / SS_VB)) * SS_VB;
+            double mm[5][SS_VB];
 #pragma unroll
             for (int j = 0; j < 5; ++j) {
-                double a = 0.0;
+                double vs[SS_VB + 2 * SS_R];
 #pragma unroll
-                for (int k = 0; k <= 2 * SS_R; ++k) a += gk.k[k] * sm.vb[j][r][q + k];
-                m[j] = a;
+                for (int k = 0; k < SS_VB + 2 * SS_R; ++k) vs[k] = sm.vb[j][r][q0 + k];
+#pragma unroll
+                for (int o = 0; o < SS_VB; ++o) {
+                    double a = 0.0;
+#pragma unroll
+                    for (int k = 0; k <= 2 * SS_R; ++k) a += gk.k[k] * vs[o + k];
+                    mm[j][o] = a;
+                }
             }
-            if (u >= W || v >= H) continue;
+#pragma unroll
+          for (int o = 0; o < SS_VB; ++o) {
+            const int q = q0 + o;
+            const int u = u0 + q, v = v0 + r;
+            const double m[5] = {mm[0][o], mm[1][o], mm[2][o], mm[3][o], mm[4][o]};
+            if (u >= W || v >= H) continue;          // this pixel only
             const double ux = m[0], uy = m[1];
             const double vx = m[2] - ux * ux, vy = m[3] - uy * uy, vxy = m[4] - ux * uy;
             const double A1 = 2 * ux * uy + SS_C1, A2 = 2 * vxy + SS_C2;
@@ -158,6 +181,7 @@ ssim_moments_kernel(const float *__restrict__ x, const float *__restrict__ y, in
             adj[p] = d0;
             adj[p + 1] = d1;
             adj[p + 2] = d2;
+          }
         }
     }
     const double t_l1 = block_sum(l1, red);
@@ -194,17 +218,21 @@ ssim_grad_kernel(const float *__restrict__ x, const float *__restrict__ y, int H
             sm.in[2][r][q] = a2;
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < SS_T * SS_E; i += SS_THREADS) {
-            const int r = i / SS_E, q = i - r * SS_E;
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        for (int it = threadIdx.x; it < SS_E * (SS_T / SS_VB); it += SS_THREADS) {
+            const int q = it % SS_E, r0 = (it / SS_E) * SS_VB;
 #pragma unroll
-            for (int k = 0; k <= 2 * SS_R; ++k) {
-                const double g = gk.k[k];
-                a0 += g * sm.in[0][r + k][q];
-                a1 += g * sm.in[1][r + k][q];
-                a2 += g * sm.in[2][r + k][q];
+            for (int j = 0; j < 3; ++j) {
+                double vs[SS_VB + 2 * SS_R];
+#pragma unroll
+                for (int k = 0; k < SS_VB + 2 * SS_R; ++k) vs[k] = sm.in[j][r0 + k][q];
+#pragma unroll
+                for (int o = 0; o < SS_VB; ++o) {
+                    double a = 0.0;
+#pragma unroll
+                    for (int k = 0; k <= 2 * SS_R; ++k) a += gk.k[k] * vs[o + k];
+                    sm.vb[j][r0 + o][q] = a;
+                }
             }
-            sm.vb[0][r][q] = a0; sm.vb[1][r][q] = a1; sm.vb[2][r][q] = a2;
         }
         __syncthreads();
     }
