@@ -30,8 +30,15 @@ def image_report(gpu, ref):
         bad = d > IMG_TOL
         if k in IMG_MAPS:
             bad_any |= bad
+        r = np.abs(np.asarray(ref[k], dtype=np.float64))
+        if r.ndim == 3:
+            r = r.max(axis=2)
+        rel = d / np.maximum(r, 1.0)            # relative where the map is large (curvature)
         out[k] = {"max_abs": float(d.max()) if d.size else 0.0,
                   "max_abs_same_count": float(d[~flips].max()) if (~flips).any() else 0.0,
+                  "max_rel_same_count": float(rel[~flips].max()) if (~flips).any() else 0.0,
+                  "rel_over_1e-4_same_count": int(((rel > 1e-4) & ~flips).sum()),
+                  "rel_over_1e-3_same_count": int(((rel > 1e-3) & ~flips).sum()),
                   "over_tol": int(bad.sum()), "over_tol_count_flip": int((bad & flips).sum()),
                   "over_tol_same_count": int((bad & ~flips).sum())}
     out["pixels"] = int(flips.size)

@@ -11,7 +11,7 @@ agg=collections.defaultdict(float)
 for r in rows[1:]:
     try: agg[r[ki].split('(')[0]]+=float(r[vi].replace(',',''))/1e6
     except: pass
-print(repr(sys.argv[1]), sys.argv[2], {k.split('::')[-1]: round(v,3) for k,v in sorted(agg.items(), key=lambda x:-x[1])[:4]})
+print(repr(sys.argv[1]), sys.argv[2], {k.split('::')[-1]: round(v,3) for k,v in sorted(agg.items(), key=lambda x:-x[1])[:6]})
 PY
   done
 done

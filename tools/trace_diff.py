@@ -1,6 +1,7 @@
 """Compare per-pixel fragment streams (GPU vs oracle) at the worst pixels.
 
-    python tools/trace_diff.py c1 [--k 6]
+    python tools/trace_diff.py c1 [--k 6]            # a golden scene
+    python tools/trace_diff.py --config c3 [--k 6]   # view 0 of a generated config
 """
 
 import argparse
@@ -19,16 +20,24 @@ from tests import golden_io  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("scene")
+    ap.add_argument("scene", nargs="?")
+    ap.add_argument("--config", default=None)
     ap.add_argument("--k", type=int, default=6)
     a = ap.parse_args()
-    gc = golden_io.load(a.scene)
+    if a.config:
+        from paper_2411_16392_b200 import scenes
+        sc = scenes.CONFIGS[a.config]()
+        gc = type("G", (), {})()
+        gc.prims, gc.cam = sc.prims, sc.cams[0]
+        gc.settings = qo.Settings() if hasattr(qo, "Settings") else rz.RenderSettings()
+    else:
+        gc = golden_io.load(a.scene)
     st = rz.RenderSettings(background=np.asarray(gc.settings.background),
                            resort=gc.settings.resort,
                            euclidean_density=gc.settings.euclidean_density)
     prep = rz.prepare(gc.prims, gc.cam, st)
     tg = rz.forward(prep).to_numpy()
-    vw = qo.prepare(gc.prims, gc.cam, gc.settings)
+    vw = qo.prepare(gc.prims.astype(np.float64) if a.config else gc.prims, gc.cam, gc.settings)
     ref = qo.forward(vw)
     d = np.abs(tg["color"] - ref["color"]).max(axis=2)
     same = tg["n_fragments"] == ref["n_fragments"]
