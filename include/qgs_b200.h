@@ -59,6 +59,9 @@ typedef struct qgs_settings {
     int32_t resort, euclidean_density;
     int32_t no_cull;         /* extension: 1 disables the forward's conic cull (the
                                 results are identical either way; tests check it) */
+    int32_t exact_decisions; /* extension: 1 re-makes every selection / alpha-floor
+                                decision whose fp32 margin is inside its rounding band
+                                in fp64 (the reference's float64 accepted set; slower) */
 } qgs_settings;
 
 /* Raw primitive parameters, PrimitiveSet layout (model.py:126-141), fp32. */

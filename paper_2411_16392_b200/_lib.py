@@ -30,7 +30,7 @@ class Camera(ctypes.Structure):
 class Settings(ctypes.Structure):
     _fields_ = [("background", f64 * 3), ("t_near_clip", f64), ("alpha_floor", f64),
                 ("alpha_clamp", f64), ("t_term", f64), ("resort", i32),
-                ("euclidean_density", i32), ("no_cull", i32)]
+                ("euclidean_density", i32), ("no_cull", i32), ("exact_decisions", i32)]
 
 
 class Params(ctypes.Structure):

@@ -235,9 +235,16 @@ int qgs_forward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_se
                                                               out->tile_order, 0);
         QGS_LAUNCHED("tile_order_kernel");
     }
-    qgs::raster_fwd_kernel<<<ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE,
-                             qgs::RASTER_THREADS, 0, s>>>(pv.rec, pv.geo, pv.conic, tile_offsets,
-                                                            tile_prims, ck, sk, *out);
+    if (sk.exact)
+        qgs::raster_fwd_exact_kernel<<<ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE,
+                                       qgs::RASTER_THREADS, 0, s>>>(pv.rec, pv.geo, pv.conic,
+                                                                      tile_offsets, tile_prims, ck,
+                                                                      sk, *out);
+    else
+        qgs::raster_fwd_kernel<<<ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE,
+                                 qgs::RASTER_THREADS, 0, s>>>(pv.rec, pv.geo, pv.conic,
+                                                                tile_offsets, tile_prims, ck, sk,
+                                                                *out);
     QGS_LAUNCHED("raster_fwd_kernel");
     return 0;
 }
@@ -256,9 +263,14 @@ int qgs_backward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_s
     qgs::CamK ck = qgs::make_camk(*cam);
     qgs::SetK sk = qgs::make_setk(*st);
     qgs::PrepView pv = qgs::prep_view(const_cast<void *>(prep), P);
-    qgs::raster_bwd_kernel<<<ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE,
-                             qgs::RASTER_THREADS, 0, s>>>(pv.rec, pv.geo, tile_offsets, tile_prims, ck,
-                                                            sk, *fwd, *up, kg);
+    if (sk.exact)
+        qgs::raster_bwd_exact_kernel<<<ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE,
+                                 qgs::RASTER_THREADS, 0, s>>>(pv.rec, pv.geo, tile_offsets, tile_prims, ck,
+                                                                sk, *fwd, *up, kg);
+    else
+        qgs::raster_bwd_kernel<<<ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE,
+                                 qgs::RASTER_THREADS, 0, s>>>(pv.rec, pv.geo, tile_offsets, tile_prims, ck,
+                                                                sk, *fwd, *up, kg);
     QGS_LAUNCHED("raster_bwd_kernel");
     return 0;
 }

@@ -123,7 +123,7 @@ struct CamK {
 struct SetK {
     double bg[3];
     double t_clip, alpha_floor, alpha_clamp, t_term;
-    int resort, euclid, no_cull;
+    int resort, euclid, no_cull, exact;
     int pbits;            // bits of the primitive id in the sort composite (qgs_bin)
 };
 
@@ -146,6 +146,7 @@ inline SetK make_setk(const qgs_settings &s)
     k.t_clip = s.t_near_clip; k.alpha_floor = s.alpha_floor;
     k.alpha_clamp = s.alpha_clamp; k.t_term = s.t_term;
     k.resort = s.resort; k.euclid = s.euclidean_density; k.no_cull = s.no_cull;
+    k.exact = s.exact_decisions;
     k.pbits = 32;
     return k;
 }

@@ -111,8 +111,9 @@ struct Pay {
 __device__ __forceinline__ void block_pixel(int tiles_x, const int32_t *order, int &tile, int &blk,
                                             int &u, int &v)
 {
-    tile = order ? order[blockIdx.x >> 3] : (int)(blockIdx.x >> 3);
-    blk = blockIdx.x & 7;
+    const int slot = (int)blockIdx.x;
+    tile = order ? order[slot >> 3] : (slot >> 3);
+    blk = slot & 7;
     const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
     const int lane = threadIdx.x & 31;
     u = tx * TILE + (blk & 1) * 8 + (lane & 7);
@@ -355,12 +356,13 @@ __device__ __forceinline__ Cfg make_cfg(const SetK &st)
 }
 
 // exact candidate test (raster_kernels.py:121-130, 58-63); t = fp64 depth
+template <bool EXACT>
 __device__ __forceinline__ bool accept(const PrimRec &r, const Geo64 &g, const double d64[3],
                                        float dx, float dy, float dz, const Cfg &c, double &t)
 {
     Hit h;
-    if (!hit_refined(r, g, d64, dx, dy, dz, c.euclid, c.t_clip, h)) return false;
-    if (r.alpha * h.G < c.alpha_floor) return false;
+    if (!hit_refined<EXACT>(r, g, d64, dx, dy, dz, c.euclid, c.t_clip, h)) return false;
+    if (!alpha_pass<EXACT>(r, &g, d64, h, c.euclid, c.alpha_floor)) return false;
     t = h.t64;
     return true;
 }
@@ -409,10 +411,16 @@ __device__ __forceinline__ void finish_frag(const PrimRec &r, float dx, float dy
 
 // ================================================================ forward
 
-__global__ void __launch_bounds__(32, QGS_FWD_MIN_BLOCKS)
-raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
-                  const ConicRec *__restrict__ conics, const int32_t *__restrict__ tile_offsets,
-                  const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets out)
+// One raster block of the forward; EXACT: settings.exact_decisions (band
+// decisions in fp64, shade.cuh).  Two kernels so that the default one
+// carries no fp64 selection code.
+template <bool EXACT>
+__device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
+                                          const Geo64 *__restrict__ geo,
+                                          const ConicRec *__restrict__ conics,
+                                          const int32_t *__restrict__ tile_offsets,
+                                          const int32_t *__restrict__ tile_prims, const CamK &cam,
+                                          const SetK &st, const qgs_targets &out)
 {
     __shared__ FwdSmem sm;
     const int lane = threadIdx.x & 31;
@@ -573,9 +581,11 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
             const Geo64 &gh = geo[sm.qprim[j]];
 #endif
             const PrimRec &r = sm.rec[j];
-            return hit_exact_from(r, gh, d, dx, dy, dz, c.euclid, c.t_clip, sm.tfirst[j][lane],
-                                  (secb >> j) & 1u, (margb >> j) & 1u, h) &&
-                   r.alpha * h.G >= c.alpha_floor;
+            const Geo64 *gfull = geo + sm.qprim[j];
+            return hit_exact_from<EXACT>(r, gh, gfull, d, dx, dy, dz, c.euclid, c.t_clip,
+                                         sm.tfirst[j][lane], (secb >> j) & 1u, (margb >> j) & 1u,
+                                         h) &&
+                   alpha_pass<EXACT>(r, gfull, d, h, c.euclid, c.alpha_floor);
         };
         auto accept_one = [&](int j, const Hit &h) {
             const int p = sm.qprim[j];
@@ -787,6 +797,22 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
             atomicAdd(&out.counters[4], (unsigned long long)n_coarse);
         }
     }
+}
+
+__global__ void __launch_bounds__(32, QGS_FWD_MIN_BLOCKS)
+raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
+                  const ConicRec *__restrict__ conics, const int32_t *__restrict__ tile_offsets,
+                  const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets out)
+{
+    fwd_block<false>(recs, geo, conics, tile_offsets, tile_prims, cam, st, out);
+}
+
+__global__ void __launch_bounds__(32, QGS_FWD_MIN_BLOCKS)
+raster_fwd_exact_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
+                        const ConicRec *__restrict__ conics, const int32_t *__restrict__ tile_offsets,
+                        const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets out)
+{
+    fwd_block<true>(recs, geo, conics, tile_offsets, tile_prims, cam, st, out);
 }
 
 // =============================================================== backward
@@ -1018,11 +1044,15 @@ __device__ __forceinline__ void warp_accumulate(float (*red)[33][KGP], bool emit
     __syncwarp();
 }
 
-__global__ void __launch_bounds__(32, QGS_BWD_MIN_BLOCKS)
-raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
-                  const int32_t *__restrict__ tile_offsets,
-                  const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets fwd,
-                  qgs_upstream upst, float *__restrict__ kg)
+// One raster block of the backward; EXACT only matters for the replay path
+// (its candidate test must make the forward's decisions).
+template <bool EXACT>
+__device__ __forceinline__ void bwd_block(const PrimRec *__restrict__ recs,
+                                          const Geo64 *__restrict__ geo,
+                                          const int32_t *__restrict__ tile_offsets,
+                                          const int32_t *__restrict__ tile_prims, const CamK &cam,
+                                          const SetK &st, const qgs_targets &fwd,
+                                          const qgs_upstream &upst, float *__restrict__ kg)
 {
     __shared__ BwdSmem sm;
     const int lane = threadIdx.x & 31;
@@ -1172,7 +1202,7 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
             if (alive && in_box(sm.rec[j], u, v)) {
                 const int p = sm.prim[j];
                 double t = 0.0;
-                if (accept(sm.rec[j], geo[p], d64, dx, dy, dz, c, t))
+                if (accept<EXACT>(sm.rec[j], geo[p], d64, dx, dy, dz, c, t))
                     emit = ring_step(c, R, t, p, et, ep);
             }
             if (__any_sync(FULL, emit)) emit_grad(emit, ep, et, false, 0.f, 0.f);
@@ -1186,6 +1216,24 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
         if (emit) ring_pop(R, et, ep);
         emit_grad(emit, ep, et, false, 0.f, 0.f);
     }
+}
+
+__global__ void __launch_bounds__(32, QGS_BWD_MIN_BLOCKS)
+raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
+                  const int32_t *__restrict__ tile_offsets,
+                  const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets fwd,
+                  qgs_upstream upst, float *__restrict__ kg)
+{
+    bwd_block<false>(recs, geo, tile_offsets, tile_prims, cam, st, fwd, upst, kg);
+}
+
+__global__ void __launch_bounds__(32, QGS_BWD_MIN_BLOCKS)
+raster_bwd_exact_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
+                        const int32_t *__restrict__ tile_offsets,
+                        const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets fwd,
+                        qgs_upstream upst, float *__restrict__ kg)
+{
+    bwd_block<true>(recs, geo, tile_offsets, tile_prims, cam, st, fwd, upst, kg);
 }
 
 // ===================================================== raster schedule
@@ -1278,7 +1326,8 @@ __global__ void trace_pixel_kernel(const PrimRec *__restrict__ recs, const Geo64
         const int p = tile_prims[i];
         const PrimRec &r = recs[p];
         double t;
-        if (in_box(r, u, v) && accept(r, geo[p], d, dx, dy, dz, c, t)) {
+        if (in_box(r, u, v) && (st.exact ? accept<true>(r, geo[p], d, dx, dy, dz, c, t)
+                                         : accept<false>(r, geo[p], d, dx, dy, dz, c, t))) {
             if (na < max) {
                 Frag f;
                 shade_emitted(r, geo[p], d, dx, dy, dz, t, c, f);

@@ -209,17 +209,83 @@ __device__ __forceinline__ double refine_depth(const Geo64 &g, const double dh[3
     return t;
 }
 
-// exact selection + weight at an fp64 depth; false if the root is rejected
-__device__ __forceinline__ bool confirm_root(const PrimRec &r, const Geo64 &g, const double dh[3],
-                                             double t64, bool planar, bool euclid, float t_clip,
-                                             Hit &h)
+// Exact-decision mode (settings.exact_decisions): a selection or alpha-floor
+// decision whose fp32 margin lies inside these relative bands is re-made in
+// fp64 with the reference's expressions, so the accepted set is the float64
+// one; the default mode keeps the fp32 decisions (no fp64 code in the hot
+// kernels -- DESIGN.md section 6 has the parity and cost of both).
+constexpr float SEL_BAND = 1e-5f;          // ellipse pre-reject, l <= 3 sigma
+constexpr float FLOOR_BAND = 1e-4f;        // alpha G >= alpha_floor
+
+// The reference's float64 selection at depth t64 (intersect.py:90-113:
+// ellipse pre-reject, l <= 3 sigma; raster_kernels.py:58-60: alpha floor)
+// from the primitive's float64 geometry in global memory.  Bit 0: the root
+// is selected; bit 1: and its weight passes the floor.  Out of line.
+static __device__ __noinline__ unsigned exact64(const Geo64 *gp, const double dh[3], double t64,
+                                                bool planar, bool euclid, double floor)
+{
+    const Geo64 &g = *gp;
+    const double x = g.ohat[0] + t64 * dh[0], y = g.ohat[1] + t64 * dh[1];
+    const double s1 = g.sv[0], s2 = g.sv[1], s3 = g.sv[2];
+    if (!planar) {
+        const double s1s2 = s1 * s2;
+        const double m = (s2 * x) * (s2 * x) + (s1 * y) * (s1 * y);
+        if (m > 9.0 * s1s2 * s1s2) return 0u;
+    }
+    const double rho = sqrt(x * x + y * y);
+    double c = 1.0, s = 0.0;
+    if (rho > 1e-12) { c = x / rho; s = y / rho; }
+    const double a = planar ? 0.0 : s3 * (g.wv[0] * c * c + g.wv[1] * s * s);
+    const double l = (planar || euclid) ? rho : arc_length64(a, rho);
+    const double sig = sigma_dir64(s1, s2, c, s);
+    if (!(l <= 3.0 * sig)) return 0u;
+    const double G = exp(-(l * l) / (2.0 * sig * sig));
+    return 1u | (g.alpha * G < floor ? 0u : 2u);
+}
+
+// exact selection + weight at an fp64 depth; false if the root is rejected.
+// `gfull`: the primitive's complete Geo64 in global memory (EXACT band cases).
+template <bool EXACT>
+__device__ __forceinline__ bool confirm_root(const PrimRec &r, const Geo64 &g, const Geo64 *gfull,
+                                             const double dh[3], double t64, bool planar,
+                                             bool euclid, float t_clip, Hit &h)
 {
     if (!(t64 > (double)t_clip)) return false;
     shade_at(r, g, dh, t64, euclid, h);
-    if (!planar && ellipse_out(r, h.x, h.y, 1.f)) return false;
-    if (!(h.l <= 3.f * h.sig)) return false;
+    if (!EXACT) {
+        if (!planar && ellipse_out(r, h.x, h.y, 1.f)) return false;
+        if (!(h.l <= 3.f * h.sig)) return false;
+    } else {
+        bool pass = true, near = false;
+        if (!planar) {
+            const float ex = r.s2 * h.x, ey = r.s1 * h.y;
+            const float m = fmaf(ex, ex, ey * ey);
+            pass = m <= r.ell9;
+            near = fabsf(m - r.ell9) <= SEL_BAND * r.ell9;
+        }
+        const float lim = 3.f * h.sig;
+        pass = pass && h.l <= lim;
+        near = near || fabsf(h.l - lim) <= SEL_BAND * lim;
+        if (near) pass = (exact64(gfull, dh, t64, planar, euclid, 0.0) & 1u) != 0u;
+        if (!pass) return false;
+    }
     h.G = QGS_EXPF(-(h.l * h.l) / (2.f * h.sig * h.sig));
     return true;
+}
+
+// the alpha floor on a selected hit (raster_kernels.py:58-60); fp64 inside
+// its band when EXACT
+template <bool EXACT>
+__device__ __forceinline__ bool alpha_pass(const PrimRec &r, const Geo64 *gfull, const double d64[3],
+                                           const Hit &h, bool euclid, float floor)
+{
+    const float ab = r.alpha * h.G;
+    if (!EXACT || fabsf(ab - floor) > FLOOR_BAND * floor) return ab >= floor;
+    double dh[3];
+    dh[0] = gfull->M[0] * d64[0] + gfull->M[1] * d64[1] + gfull->M[2] * d64[2];
+    dh[1] = gfull->M[3] * d64[0] + gfull->M[4] * d64[1] + gfull->M[5] * d64[2];
+    dh[2] = gfull->M[6] * d64[0] + gfull->M[7] * d64[1] + gfull->M[8] * d64[2];
+    return (exact64(gfull, dh, h.t64, h.branch == BR_PLANAR, euclid, (double)floor) & 2u) != 0u;
 }
 
 // Near-tangent rays: the fp32 discriminant is within its rounding band of
@@ -228,9 +294,10 @@ __device__ __forceinline__ bool confirm_root(const PrimRec &r, const Geo64 &g, c
 // accepted root (or -1) -- the caller re-confirms it inline, so its Hit stays
 // in registers (a Hit passed by address to an out-of-line call would live in
 // local memory on the hot path).
+template <bool EXACT>
 static __device__ __noinline__ double marginal_root(const PrimRec &r, const Geo64 &g,
-                                                    const double d64[3], bool euclid,
-                                                    float t_clip)
+                                                    const Geo64 *gfull, const double d64[3],
+                                                    bool euclid, float t_clip)
 {
     double dh[3];
     local_dir64(g, d64, dh);
@@ -255,18 +322,19 @@ static __device__ __noinline__ double marginal_root(const PrimRec &r, const Geo6
     }
     Hit h;
     for (int k = 0; k < cnt; ++k)
-        if (confirm_root(r, g, dh, roots[k], false, euclid, t_clip, h)) return roots[k];
+        if (confirm_root<EXACT>(r, g, gfull, dh, roots[k], false, euclid, t_clip, h)) return roots[k];
     return -1.0;
 }
 
-__device__ __forceinline__ bool hit_marginal(const PrimRec &r, const Geo64 &g, const double d64[3],
-                                             bool euclid, float t_clip, Hit &h)
+template <bool EXACT>
+__device__ __forceinline__ bool hit_marginal(const PrimRec &r, const Geo64 &g, const Geo64 *gfull,
+                                             const double d64[3], bool euclid, float t_clip, Hit &h)
 {
-    const double t = marginal_root(r, g, d64, euclid, t_clip);
+    const double t = marginal_root<EXACT>(r, g, gfull, d64, euclid, t_clip);
     if (!(t > 0.0)) return false;
     double dh[3];
     local_dir64(g, d64, dh);
-    return confirm_root(r, g, dh, t, false, euclid, t_clip, h);
+    return confirm_root<EXACT>(r, g, gfull, dh, t, false, euclid, t_clip, h);
 }
 
 // Coarse fp32 stage (the per-candidate hot path).  Returns a mask: bit k set
@@ -368,27 +436,32 @@ __device__ __forceinline__ unsigned coarse_roots(const PrimRec &r, float dx, flo
 // Exact test of a candidate whose coarse stage already ran: `t_first` is the
 // first root that survived it, `second` whether root 1 survived too,
 // `marginal` the near-tangent flag.  Same decisions as hit_refined.
+template <bool EXACT>
 __device__ __forceinline__ bool hit_exact_from(const PrimRec &r, const Geo64 &g,
-                                               const double d64[3], float dx, float dy,
+                                               const Geo64 *gfull, const double d64[3],
+                                               float dx, float dy,
                                                float dz, bool euclid, float t_clip,
                                                float t_first, bool second, bool marginal,
                                                Hit &h)
 {
-    if (marginal) return hit_marginal(r, g, d64, euclid, t_clip, h);
+    if (marginal) return hit_marginal<EXACT>(r, g, gfull, d64, euclid, t_clip, h);
     const bool planar = (r.flags & 1u) != 0;
     double dh[3];
     local_dir64(g, d64, dh);
     if (planar && fabs(dh[2]) < 1e-12) return false;
-    if (confirm_root(r, g, dh, refine_depth(g, dh, planar, t_first), planar, euclid, t_clip, h))
+    if (confirm_root<EXACT>(r, g, gfull, dh, refine_depth(g, dh, planar, t_first), planar, euclid,
+                            t_clip, h))
         return true;
     if (!second) return false;
     float roots[2], hx, hy;
     coarse_stage1(r, dx, dy, dz, t_clip, roots, hx, hy);
-    return confirm_root(r, g, dh, refine_depth(g, dh, planar, roots[1]), planar, euclid, t_clip, h);
+    return confirm_root<EXACT>(r, g, gfull, dh, refine_depth(g, dh, planar, roots[1]), planar,
+                               euclid, t_clip, h);
 }
 
 // Full candidate test: coarse fp32 roots, fp64 refinement, exact selection.
 // Returns the selected hit (valid, before the alpha floor) or false.
+template <bool EXACT>
 __device__ __forceinline__ bool hit_refined(const PrimRec &r, const Geo64 &g, const double d64[3],
                                             float dx, float dy, float dz, bool euclid,
                                             float t_clip, Hit &h)
@@ -396,7 +469,7 @@ __device__ __forceinline__ bool hit_refined(const PrimRec &r, const Geo64 &g, co
     float roots[2], hx, hy, hz;
     const unsigned pass = coarse_roots(r, dx, dy, dz, euclid, t_clip, roots, hx, hy, hz);
     if (pass == 0u) return false;
-    if (pass & CR_MARGINAL) return hit_marginal(r, g, d64, euclid, t_clip, h);
+    if (pass & CR_MARGINAL) return hit_marginal<EXACT>(r, g, &g, d64, euclid, t_clip, h);
     const bool planar = (r.flags & 1u) != 0;
     double dh[3];
     local_dir64(g, d64, dh);
@@ -405,7 +478,7 @@ __device__ __forceinline__ bool hit_refined(const PrimRec &r, const Geo64 &g, co
     for (int k = 0; k < 2; ++k) {
         if (!(pass & (1u << k))) continue;
         double t64 = refine_depth(g, dh, planar, roots[k]);
-        if (confirm_root(r, g, dh, t64, planar, euclid, t_clip, h)) return true;
+        if (confirm_root<EXACT>(r, g, &g, dh, t64, planar, euclid, t_clip, h)) return true;
     }
     return false;
 }

@@ -44,6 +44,10 @@ class RenderSettings:
     # extension (not in the reference): False disables the forward's
     # screen-space conic cull; outputs are identical either way
     conic_cull: bool = True
+    # extension: True re-makes in float64 every selection / alpha-floor
+    # decision whose fp32 margin lies in its rounding band (the reference's
+    # float64 accepted set at full scale; the raster kernels run ~20 % slower)
+    exact_decisions: bool = False
 
 
 # ----------------------------------------------------------------- helpers
@@ -81,6 +85,7 @@ def _settings_struct(st):
     s.alpha_clamp, s.t_term = float(st.alpha_clamp), float(st.t_term)
     s.resort, s.euclidean_density = int(bool(st.resort)), int(bool(st.euclidean_density))
     s.no_cull = int(not getattr(st, "conic_cull", True))
+    s.exact_decisions = int(bool(getattr(st, "exact_decisions", False)))
     return s
 
 

@@ -238,3 +238,28 @@ def test_tile_schedule_is_a_permutation(cuda_device):
     key = np.floor(4 * np.log2(cnt.astype(np.float64) + 1))
     assert np.all(np.diff(key) <= 1)           # the kernel bins with an fp32 log2
     assert key[0] >= key.max() - 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["c1", "c3_small", "s_overflow", "s_planar", "s_euclid"])
+def test_exact_decisions_mode(rz, name):
+    """settings.exact_decisions: the same binning and (within the same
+    tolerances) the same images and gradients as the reference"""
+    gc = golden_io.load(name)
+    st = rz.RenderSettings(background=np.asarray(gc.settings.background),
+                           resort=gc.settings.resort,
+                           euclidean_density=gc.settings.euclidean_density, exact_decisions=True)
+    prep = rz.prepare(gc.prims, gc.cam, st)
+    tg = rz.forward(prep)
+    gr = rz.backward(prep, tg, gc.upstream)
+    g = gc.g
+    ref = {k: g[f"map_{k}"] for k in ("color", "alpha", "depth", "normal", "depth_median",
+                                       "transmittance", "curvature", "distortion",
+                                       "n_fragments")}
+    rep = parity.image_report(tg.to_numpy(), ref)
+    assert rep["over_tol_same_count"] == 0, rep
+    assert rep["count_flip_pixels"] <= max(2, rep["pixels"] // 2000), rep
+    ref_g = {k: g[f"grad_{k}"] for k in parity.GRAD_GROUPS + ("screen_center",)}
+    gq = parity.grad_report(gr.to_numpy(), ref_g)
+    assert gq["violations"] <= max(2, gq["n"] // 10000), gq
+    assert np.array_equal(prep.tile_prims.cpu().numpy(), g["tile_prims"])

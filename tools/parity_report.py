@@ -1,6 +1,6 @@
 """Print a JSON parity report of the GPU path vs the float64 oracle.
 
-    python tools/parity_report.py [--scenes c1,c2] [--views 1] [--out FILE]
+    python tools/parity_report.py [--scenes c1,c2] [--views 1] [--out FILE] [--exact]
 
 Golden fixtures are compared against the reference outputs stored in them;
 generated configs (c1..c5, optionally shrunk with --n/--res) are compared
@@ -23,9 +23,12 @@ from paper_2411_16392_b200 import rasterizer as rz, scenes  # noqa: E402
 from tests import golden_io, parity  # noqa: E402
 
 
+EXACT = "--exact" in sys.argv          # settings.exact_decisions
+
+
 def gpu_run(prims, cam, st, up):
     s = rz.RenderSettings(background=np.asarray(st.background), resort=st.resort,
-                          euclidean_density=st.euclidean_density)
+                          euclidean_density=st.euclidean_density, exact_decisions=EXACT)
     prep = rz.prepare(prims, cam, s)
     tg = rz.forward(prep)
     gr = rz.backward(prep, tg, up)
@@ -86,6 +89,7 @@ def main():
     ap.add_argument("--scenes", default="golden,c1,c2")
     ap.add_argument("--views", type=int, default=1)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--exact", action="store_true", help="settings.exact_decisions")
     a = ap.parse_args()
     report = []
     for s in a.scenes.split(","):
