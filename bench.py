@@ -171,7 +171,7 @@ def run_ours(a):
     V = len(cams)
     mine = [v for v in range(V) if v % world == rank]
     H, W = cams[0].height, cams[0].width
-    st = rz.RenderSettings()
+    st = rz.RenderSettings(exact_decisions=a.exact)
 
     dev = rz.DevicePrimitives.from_host(sc.prims, device)
     ups = [{k: torch.from_numpy(np.ascontiguousarray(u)).to(device) for k, u in sc.upstream[v].items()}
@@ -294,7 +294,8 @@ def run_ours(a):
         "config": {"workload": workload_desc(sc), "views_per_step": V,
                    "parallelism": f"views sharded over {world} GPU(s), primitives replicated"
                                   + (", 1 NCCL all-reduce/step" if world > 1 else ""),
-                   "l2": "working set > L2 (126 MB): per-view sort buffers + maps are GBs"},
+                   "l2": "working set > L2 (126 MB): per-view sort buffers + maps are GBs",
+                   "exact_decisions": bool(a.exact)},
         "roofline": roof, "clocks": clk.summary(),
         "gpu_launches": OUR_LAUNCHES_PER_VIEW * V * K,
         "compute_peaks": cp,
@@ -441,6 +442,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-tiles", type=int, default=96)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exact", action="store_true",
+                    help="RenderSettings.exact_decisions (band decisions in fp64)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to exercise the multi-rank path on one GPU")
