@@ -40,6 +40,12 @@ namespace qgs {
 #ifndef QGS_FWD_LIST_PREFETCH
 #define QGS_FWD_LIST_PREFETCH 1
 #endif
+#ifndef QGS_FWD_EXACT_MIN_BLOCKS
+#define QGS_FWD_EXACT_MIN_BLOCKS 16   // the fp64 band code needs the registers (measured: 18 -> 16 is -4 %)
+#endif
+#ifndef QGS_BWD_EXACT_MIN_BLOCKS
+#define QGS_BWD_EXACT_MIN_BLOCKS QGS_BWD_MIN_BLOCKS
+#endif
 #ifndef QGS_BWD_MIN_BLOCKS
 #define QGS_BWD_MIN_BLOCKS 20
 #endif
@@ -807,7 +813,7 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
     fwd_block<false>(recs, geo, conics, tile_offsets, tile_prims, cam, st, out);
 }
 
-__global__ void __launch_bounds__(32, QGS_FWD_MIN_BLOCKS)
+__global__ void __launch_bounds__(32, QGS_FWD_EXACT_MIN_BLOCKS)
 raster_fwd_exact_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
                         const ConicRec *__restrict__ conics, const int32_t *__restrict__ tile_offsets,
                         const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets out)
@@ -1227,7 +1233,7 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
     bwd_block<false>(recs, geo, tile_offsets, tile_prims, cam, st, fwd, upst, kg);
 }
 
-__global__ void __launch_bounds__(32, QGS_BWD_MIN_BLOCKS)
+__global__ void __launch_bounds__(32, QGS_BWD_EXACT_MIN_BLOCKS)
 raster_bwd_exact_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
                         const int32_t *__restrict__ tile_offsets,
                         const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets fwd,
