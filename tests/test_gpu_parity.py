@@ -263,3 +263,27 @@ def test_exact_decisions_mode(rz, name):
     gq = parity.grad_report(gr.to_numpy(), ref_g)
     assert gq["violations"] <= max(2, gq["n"] // 10000), gq
     assert np.array_equal(prep.tile_prims.cpu().numpy(), g["tile_prims"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("size", [(1, 1), (3, 5), (17, 2), (9, 33)])
+def test_tiny_and_ragged_images(rz, size):
+    """images smaller than a raster block / a tile, against the oracle"""
+    from oracle import qgs_oracle as qo
+    from paper_2411_16392_b200 import scenes
+    W, H = size
+    sc = scenes.small_scene(seed=11, n=16, res=8, width=W, height=H)
+    cam = sc.cams[0]
+    prims64 = sc.prims.astype(np.float64)
+    vw = qo.prepare(prims64, cam)
+    ref = qo.forward(vw)
+    up = {k: np.asarray(v, np.float64) for k, v in sc.upstream[0].items()}
+    ref_g = qo.backward(vw, ref, up)
+    prep = rz.prepare(sc.prims, cam)
+    assert np.array_equal(prep.tile_prims.cpu().numpy(), vw.tile_prims)
+    tg = rz.forward(prep)
+    rep = parity.image_report(tg.to_numpy(), ref)
+    assert rep["over_tol_same_count"] == 0, rep
+    gr = rz.backward(prep, tg, sc.upstream[0])
+    gq = parity.grad_report(gr.to_numpy(), {k: ref_g[k] for k in parity.GRAD_GROUPS + ("screen_center",)})
+    assert gq["violations"] <= 1, gq
