@@ -287,3 +287,32 @@ def test_tiny_and_ragged_images(rz, size):
     gr = rz.backward(prep, tg, sc.upstream[0])
     gq = parity.grad_report(gr.to_numpy(), {k: ref_g[k] for k in parity.GRAD_GROUPS + ("screen_center",)})
     assert gq["violations"] <= 1, gq
+
+
+@pytest.mark.gpu
+def test_sort_order_at_scale(rz):
+    """size-independent sort properties at 4.2M primitives on a small image
+    (tiles of ~260K pairs: the staged, two-level path with 23 id bits): every
+    tile's list is non-decreasing in its exact float64 key with ties by
+    primitive id, and each primitive appears in exactly its box's tiles"""
+    from paper_2411_16392_b200 import scenes
+    n = (1 << 22) + 12345
+    sc = scenes.small_scene(seed=21, n=n, res=64, spread=0.9, z_span=2.0)
+    prep = rz.prepare(sc.prims, sc.cams[0])
+    keys = prep.sorted_keys().cpu().numpy()
+    off = prep.tile_offsets.cpu().numpy().astype(np.int64)
+    tp = prep.tile_prims.cpu().numpy().astype(np.int64)
+    assert off[-1] == prep.n_pairs == len(tp)
+    tile = np.repeat(np.arange(len(off) - 1), np.diff(off))
+    # lexsort order: (tile, key, prim) strictly increasing along the list
+    same_tile = tile[1:] == tile[:-1]
+    dk = keys[1:] - keys[:-1]
+    ok = ~same_tile | (dk > 0) | ((dk == 0) & (tp[1:] > tp[:-1]))
+    assert ok.all(), int((~ok).sum())
+    # membership: each primitive's pair count equals its tile-box area
+    counts = np.bincount(tp, minlength=n)
+    bb = prep.pix_bbox.cpu().numpy().astype(np.int64)
+    live = bb[:, 0] <= bb[:, 1]
+    area = np.where(live, (bb[:, 1] // 16 - bb[:, 0] // 16 + 1) * (bb[:, 3] // 16 - bb[:, 2] // 16 + 1), 0)
+    assert np.array_equal(counts, area)
+    assert np.diff(off).max() > 100_000
