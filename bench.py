@@ -62,6 +62,14 @@ def traffic_bytes(kernel):
                                    "source": os.path.relpath(files[-1], HERE)}
 
 
+def hbm_view(traffic, t_launch_s, peaks):
+    if not traffic or t_launch_s <= 0:
+        return None
+    gbs = traffic["bytes_per_launch"] / t_launch_s / 1e9
+    return {"bound": "hbm", "unit": "GB/s", "achieved": gbs, "peak": peaks["hbm_gbs"],
+            "frac": gbs / peaks["hbm_gbs"], "traffic": traffic["bytes_per_launch"]}
+
+
 def load_peaks():
     p = os.path.join(HERE, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -277,6 +285,10 @@ def run_ours(a):
         "roof_frac": max(F / P32, S / PSF) / t_k,
         "kernel_ms_per_step": kms, "fwd_ms_per_step": fwd_ms, "bwd_ms_per_step": bwd_ms,
         "traffic": traffic_bytes(dom),
+        # the contract's HBM view of the same kernel: its DRAM bytes per launch
+        # (ncu) over its measured launch time, against MEASURED_PEAKS' copy
+        # bandwidth -- small, because the raster is FP32/SFU-bound, not HBM
+        "hbm_view": hbm_view(traffic_bytes(dom), t_k / max(len(mine), 1), peaks),
         "peak_source": f"fp32/mufu measured live (tools/peaks.cu); hbm {peaks_kind} "
                        f"MEASURED_PEAKS.json {peaks['hbm_gbs']} GB/s",
         "step_roofline_ms": T_roof * 1e3,
