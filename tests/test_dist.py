@@ -99,3 +99,28 @@ def test_single_rank_without_process_group():
     prims, cams, ups = _scene()
     g = qd.sharded_step(len(cams), _view_backward(prims, cams, ups), 0, 1, _shapes(prims))
     assert g["centers"].shape == (96, 3)
+
+
+@pytest.mark.gpu
+def test_upload_async_and_pipelined_prepare(cuda_device):
+    """the e2e helpers: upstream maps copied on a copy stream land intact
+    before the backward that waits on their event, and the pipelined
+    prepare yields the same binning as the plain one"""
+    import numpy as np
+    import torch
+    from paper_2411_16392_b200 import dist as D, rasterizer as rz, scenes
+    sc = scenes.config2(seed=3, n=3000, res=96, views=3)
+    dev = rz.DevicePrimitives.from_host(sc.prims)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    host = [{k: pin(v) for k, v in sc.upstream[i].items()} for i in range(3)]
+    dst = [{k: torch.empty(t.shape, dtype=t.dtype, device=cuda_device) for k, t in h.items()}
+           for h in host]
+    evs = D.upload_async(host, dst)
+    main = torch.cuda.current_stream()
+    st = rz.RenderSettings()
+    for i, v, prep in D.pipelined_prepare(dev, sc.cams, [0, 1, 2], st):
+        ref = rz.prepare(dev, sc.cams[v], st)
+        assert torch.equal(prep.tile_prims, ref.tile_prims)
+        main.wait_event(evs[i])
+        for k, t in host[i].items():
+            assert torch.equal(dst[i][k].cpu(), t), k
