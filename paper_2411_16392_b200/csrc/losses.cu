@@ -20,6 +20,8 @@
 // symmetric, so the adjoint of the blur is the blur, ssim.py:1-7).
 #include "losses.cuh"
 
+#include <type_traits>
+
 namespace qgs {
 
 namespace {
@@ -28,6 +30,10 @@ constexpr int SS_T = 32;                 // output tile edge
 constexpr int SS_R = 5;                  // window radius (WINDOW 11)
 constexpr int SS_E = SS_T + 2 * SS_R;    // staged edge (42)
 constexpr int SS_THREADS = 256;
+#ifndef QGS_SSIM_ADJ_F32
+#define QGS_SSIM_ADJ_F32 1          // adjoint maps in fp32 (the gradient is stored fp32 anyway): -6 %
+#endif
+using AdjT = std::conditional<QGS_SSIM_ADJ_F32, float, double>::type;
 constexpr int SS_VB = 4;                 // outputs per thread along a blur (register run)
 constexpr double SS_C1 = 0.01 * 0.01;    // ssim.py:15
 constexpr double SS_C2 = 0.03 * 0.03;    // ssim.py:16
@@ -74,7 +80,7 @@ __device__ __forceinline__ double block_sum(double v, double *red)
 // and per-CTA partial sums of S over the crop and |x - y| over the tile.
 __global__ void __launch_bounds__(SS_THREADS)
 ssim_moments_kernel(const float *__restrict__ x, const float *__restrict__ y, int H, int W,
-                    int C, int with_ssim, double inv_valid, Gauss gk, double *__restrict__ adj,
+                    int C, int with_ssim, double inv_valid, Gauss gk, AdjT *__restrict__ adj,
                     double *__restrict__ partial)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -178,9 +184,9 @@ ssim_moments_kernel(const float *__restrict__ x, const float *__restrict__ y, in
                 d2 = inv_valid * duxy;
             }
             const size_t p = (((size_t)c * H + v) * W + u) * 3;
-            adj[p] = d0;
-            adj[p + 1] = d1;
-            adj[p + 2] = d2;
+            adj[p] = (AdjT)d0;
+            adj[p + 1] = (AdjT)d1;
+            adj[p + 2] = (AdjT)d2;
           }
         }
     }
@@ -198,7 +204,7 @@ ssim_moments_kernel(const float *__restrict__ x, const float *__restrict__ y, in
 __global__ void __launch_bounds__(SS_THREADS)
 ssim_grad_kernel(const float *__restrict__ x, const float *__restrict__ y, int H, int W, int C,
                  int with_ssim, double l1_scale, double m_ssim, double weight, Gauss gk,
-                 const double *__restrict__ adj, float *__restrict__ d_render)
+                 const AdjT *__restrict__ adj, float *__restrict__ d_render)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SsimSmem &sm = *reinterpret_cast<SsimSmem *>(smem_raw);
@@ -211,7 +217,7 @@ ssim_grad_kernel(const float *__restrict__ x, const float *__restrict__ y, int H
             double a0 = 0.0, a1 = 0.0, a2 = 0.0;
             if (u >= 0 && u < W && v >= 0 && v < H) {
                 const size_t p = (((size_t)c * H + v) * W + u) * 3;
-                a0 = adj[p]; a1 = adj[p + 1]; a2 = adj[p + 2];
+                a0 = (double)adj[p]; a1 = (double)adj[p + 1]; a2 = (double)adj[p + 2];
             }
             sm.in[0][r][q] = a0;
             sm.in[1][r][q] = a1;
@@ -462,7 +468,7 @@ cudaError_t photometric(const float *render, const float *gt, int H, int W, int 
 {
     static const Gauss gk = make_gauss();
     char *w = static_cast<char *>(ws);
-    double *adj = reinterpret_cast<double *>(w);
+    AdjT *adj = reinterpret_cast<AdjT *>(w);
     double *partial = reinterpret_cast<double *>(w + al((size_t)H * W * C * 3 * sizeof(double)));
     const dim3 grid(cdiv(W, SS_T), cdiv(H, SS_T), C);
     const int nblk = grid.x * grid.y * grid.z;
