@@ -15,7 +15,8 @@
 // 42x42 input window (zero outside the image, the reference's
 // correlate1d(mode="constant")) in shared memory, blurs along rows of the
 // image first and columns second (ssim.py:29-31 order), and keeps the five
-// moment maps in registers for the per-pixel SSIM and its three adjoint maps.
+// moment maps in registers for the per-pixel SSIM and its three adjoint maps
+// (stored fp32 between the passes: the gradient they make is stored fp32).
 // The gradient pass blurs the adjoint maps the same way (the Gaussian is
 // symmetric, so the adjoint of the blur is the blur, ssim.py:1-7).
 #include "losses.cuh"
