@@ -163,7 +163,7 @@ def run_ours(a):
     import torch.distributed as dist
 
     from paper_2411_16392_b200 import rasterizer as rz
-    from paper_2411_16392_b200.dist import pipelined_prepare
+    from paper_2411_16392_b200.dist import gpu_step, shard_views
 
     rank, world, local = env_rank()
     local = local % torch.cuda.device_count()   # (only the gloo check shares a GPU)
@@ -177,54 +177,42 @@ def run_ours(a):
     sc = scene_for(a.config)
     cams = sc.cams
     V = len(cams)
-    mine = [v for v in range(V) if v % world == rank]
+    mine = shard_views(V, rank, world)
     H, W = cams[0].height, cams[0].width
-    st = rz.RenderSettings(exact_decisions=a.exact)
+    st = rz.RenderSettings(exact_decisions=not a.fp32_decisions)
 
     dev = rz.DevicePrimitives.from_host(sc.prims, device)
-    ups = [{k: torch.from_numpy(np.ascontiguousarray(u)).to(device) for k, u in sc.upstream[v].items()}
-           for v in mine]
+    ups = {v: {k: torch.from_numpy(np.ascontiguousarray(u)).to(device)
+               for k, u in sc.upstream[v].items()} for v in mine}
     grads = rz.GradientBuffer.zeros_flat(dev)
     counters = torch.zeros(5, dtype=torch.int64, device=device)
     side = torch.cuda.Stream(device=device)
     stream = torch.cuda.current_stream()
 
-    def step(ev=None, count=False):
-        grads.zero_()
-        for i, v, prep in pipelined_prepare(dev, cams, mine, st, side):
-            if ev is not None:
-                ev["f0"][i].record(stream)
-            tg = rz.forward(prep, counters=counters if count else None)
-            if ev is not None:
-                ev["f1"][i].record(stream)
-            kg = torch.zeros((len(dev), _kg_stride()), dtype=torch.float32, device=device)
-            if ev is not None:
-                ev["b0"][i].record(stream)
-            kg = rz.kernel_grads(prep, tg, ups[i], kg=kg)
-            if ev is not None:
-                ev["b1"][i].record(stream)
-            rz.chain(prep, kg, grads)
-            if ev is not None and i == 0:
-                ev["pairs"].append(prep.n_pairs)
-        if world > 1:
-            dist.all_reduce(grads.buffer)
+    def step(hook=None, count=False):
+        # dist.gpu_step: this rank's views (pipelined prepare, forward,
+        # backward, chain) + one all-reduce -- the same call a user makes
+        gpu_step(dev, cams, ups, st, rank, world, grads=grads, views=mine, side=side,
+                 hook=hook, counters=counters if count else None)
 
     # warm-up (also the counted pass for the algorithmic work)
     for w in range(max(a.warmup, 3)):
         step(count=(w == 0))
     torch.cuda.synchronize()
     cnt = counters.cpu().numpy().astype(np.float64)     # this rank's views
-    n_pairs_mine = []
-    for v in mine:
-        n_pairs_mine.append(rz.prepare(dev, cams[v], st).n_pairs)
+    n_pairs_mine = [rz.prepare(dev, cams[v], st).n_pairs for v in mine]
 
-    # timed region
+    # timed region: CUDA events on the launching stream at every hook
     K = a.steps
-    mk = lambda: [torch.cuda.Event(enable_timing=True) for _ in mine]  # noqa: E731
-    ev = {"f0": [], "f1": [], "b0": [], "b1": [], "pairs": []}
-    per_step = []
-    for _ in range(K):
-        per_step.append({"f0": mk(), "f1": mk(), "b0": mk(), "b1": mk(), "pairs": []})
+    evs = []
+
+    def hook_for(rec):
+        def hook(name, i):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            rec.append((name, i, e))
+        return hook
+
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
@@ -232,22 +220,37 @@ def run_ours(a):
     with ClockSampler(local) as clk:
         t0.record(stream)
         for k in range(K):
-            step(ev=per_step[k])
+            rec = []
+            evs.append(rec)
+            step(hook=hook_for(rec))
         t1.record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ms = t0.elapsed_time(t1) / K
-    fwd_ms = sum(per_step[k]["f0"][i].elapsed_time(per_step[k]["f1"][i])
-                 for k in range(K) for i in range(len(mine))) / K
-    bwd_ms = sum(per_step[k]["b0"][i].elapsed_time(per_step[k]["b1"][i])
-                 for k in range(K) for i in range(len(mine))) / K
+
+    def span(rec, a_name, b_name):
+        ev = {(n, i): e for n, i, e in rec}
+        return [ev[(a_name, i)].elapsed_time(ev[(b_name, i)]) for i in range(len(mine))]
+
+    fwd_ms = sum(sum(span(r, "view_begin", "fwd_end")) for r in evs) / K
+    bwd_ms = sum(sum(span(r, "fwd_end", "bwd_end")) for r in evs) / K
+    view_ms = np.mean([span(r, "view_begin", "view_end") for r in evs], axis=0).tolist() \
+        if mine else []
+    red_ms = float(np.mean([{n: e for n, _, e in r}["reduce_begin"].elapsed_time(
+        {n: e for n, _, e in r}["reduce_end"]) for r in evs]))
     t_ms = torch.tensor([ms], dtype=torch.float64, device=device)
     if world > 1:
         dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
     ms_max = float(t_ms.item())
     total_px = V * H * W
     value = total_px / 1e6 / (ms_max / 1e3)
+    mine_rec = {"rank": rank, "views": mine, "ms_per_step": ms, "view_ms": view_ms,
+                "allreduce_ms": red_ms}
+    per_rank = [mine_rec]
+    if world > 1:
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, mine_rec)
 
     # end to end through the public API, host buffers in pinned memory
     e2e = None
@@ -303,27 +306,33 @@ def run_ours(a):
         "warmup": a.warmup, "ms_per_step": ms_max, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "fp32",
         "data": "synthetic (seeded, BASELINE config shapes; scenes.py)",
-        "config": {"workload": workload_desc(sc), "views_per_step": V,
-                   "parallelism": f"views sharded over {world} GPU(s), primitives replicated"
-                                  + (", 1 NCCL all-reduce/step" if world > 1 else ""),
-                   "l2": "working set > L2 (126 MB): per-view sort buffers + maps are GBs",
-                   "exact_decisions": bool(a.exact)},
+        "config": config_of(sc, a),
+        "step": f"{V} full views: prepare + forward + backward + chain each"
+                + (", then 1 NCCL all-reduce" if world > 1 else ""),
+        "parallelism": f"views sharded over {world} GPU(s), primitives replicated",
+        "l2": "working set > L2 (126 MB): per-view sort buffers + maps are GBs",
         "roofline": roof, "clocks": clk.summary(),
         "gpu_launches": OUR_LAUNCHES_PER_VIEW * V * K,
         "compute_peaks": cp,
+        "per_rank": per_rank,
     }
     if e2e is not None:
         out["e2e"] = e2e
     if world == 1 and not a.no_cpu:
-        out["cpu_baseline"] = cpu_baseline(sc, a.cpu_tiles, views=1)
+        out["cpu_baseline"] = cpu_baseline(sc)
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
 def run_e2e(a, rz, sc, mine, device, st, world):
+    """The same step through the public API from HOST buffers: primitives
+    uploaded from pinned memory, every view's upstream maps copied on a copy
+    stream (the backward of view i waits for its maps), dist.gpu_step, and
+    the all-reduced gradient read back to pinned memory -- all inside the
+    timed region."""
     import torch.distributed as dist
-    from paper_2411_16392_b200.dist import pipelined_prepare, upload_async
+    from paper_2411_16392_b200.dist import gpu_step, upload_async
     pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory()  # noqa: E731
     host = type("H", (), {})()
     for f in rz.DevicePrimitives.FIELDS:
@@ -338,20 +347,19 @@ def run_e2e(a, rz, sc, mine, device, st, world):
     down = torch.cuda.Stream(device=device)     # gradient read-back (the D2H copy engine)
     dev_ups = [{k: torch.empty(t.shape, dtype=t.dtype, device=device) for k, t in u.items()}
                for u in ups]
+    by_view = dict(zip(mine, dev_ups))
 
     def step():
         nonlocal out_host
         dev = rz.DevicePrimitives.from_host(host, device, non_blocking=True)
         # every view's upstream maps go over on a copy stream under the raster
         evs = upload_async(ups, dev_ups, copy)
-        grads = rz.GradientBuffer.zeros_flat(dev)
         main = torch.cuda.current_stream()
-        for i, v, prep in pipelined_prepare(dev, sc.cams, mine, st, side):
-            tg = rz.forward(prep)
-            main.wait_event(evs[i])
-            rz.backward(prep, tg, dev_ups[i], out=grads)
-        if world > 1:
-            dist.all_reduce(grads.buffer)
+
+        def hook(name, i):
+            if name == "fwd_end":           # view i's backward needs its maps
+                main.wait_event(evs[i])
+        grads = gpu_step(dev, sc.cams, by_view, st, 0, world, views=mine, side=side, hook=hook)
         if out_host is None:
             out_host = torch.empty(grads.buffer.shape, dtype=grads.buffer.dtype).pin_memory()
         # the read-back runs on its own stream so the next step's upload (the
@@ -392,55 +400,77 @@ def run_e2e(a, rz, sc, mine, device, st, world):
 
 # ---------------------------------------------------------------- CPU side
 
-def cpu_baseline(sc, n_tiles, views=1, seed=0):
-    """The float64 oracle (C + numpy restatement of the reference, OpenMP over
-    tiles) on the host cores, one view, systematic tile sample."""
-    from oracle import qgs_oracle as qo
+def config_of(sc, a):
+    """the workload both arms report (identical dicts)"""
+    return {"workload": workload_desc(sc), "views_per_step": len(sc.cams),
+            "exact_decisions": not a.fp32_decisions}
+
+
+def _cpu_inputs(sc, v=0):
     prims64 = sc.prims.astype(np.float64)
-    cam = sc.cams[0]
-    up = {k: np.asarray(v, np.float64) for k, v in sc.upstream[0].items()}
-    qo.time_sampled_view(prims64, cam, up, n_sample=4, seed=seed + 7)   # warm-up
-    r = qo.time_sampled_view(prims64, cam, up, n_sample=n_tiles, seed=seed)
+    up = {k: np.asarray(x, np.float64) for k, x in sc.upstream[v].items()}
+    return prims64, sc.cams[v], up
+
+
+def cpu_baseline(sc):
+    """The float64 oracle (C + numpy restatement of the reference, OpenMP over
+    tiles for the per-pixel loops) on the host cores: ONE WHOLE VIEW of the
+    workload timed end to end (prepare + forward + backward + chain), nothing
+    sampled or extrapolated."""
+    from oracle import qgs_oracle as qo
+    prims64, cam, up = _cpu_inputs(sc)
+    r = qo.time_full_view(prims64, cam, up)
     px = cam.width * cam.height
-    val = px / 1e6 / r["seconds_per_view_est"]
-    return {"value": val, "unit": UNIT, "cores": r["threads"], "kind": "port",
-            "sample": (f"view 0 of {sc.name}: per-primitive stages timed in full, "
-                       f"{r['tiles_sampled']} of {r['tiles']} tiles (systematic) timed for the "
-                       f"per-pair and per-pixel stages and scaled; est {r['seconds_per_view_est']:.2f}"
-                       f" s/view"), "detail": r}
+    cpu = qo.cpu_model()
+    return {"value": px / 1e6 / r["seconds"], "unit": UNIT, "cores": r["threads"],
+            "kind": "port", "cpu": cpu["model"], "logical_cores": cpu["logical_cores"],
+            "sample": (f"view 0 of {sc.name} in full ({r['pairs']} tile pairs): prepare + "
+                       f"forward + backward + chain in {r['seconds']:.1f} s"), "detail": r}
 
 
 def run_reference(a):
+    """Reference arm: the float64 oracle port of the reference path
+    (oracle/, kind "port": the reference is Python + numba and is not on the
+    GPU box) on all host threads.  One step = ONE WHOLE VIEW of the workload
+    (prepare + forward + backward + chain, nothing sampled); views are timed
+    until --ref-budget seconds are spent (at least one), and `steps` is the
+    number actually timed, so steps x ms_per_step is the measured time."""
     rank, world, _ = env_rank()
     if rank != 0:
         return
-    sc = scene_for(a.config)
     from oracle import qgs_oracle as qo
-    prims64 = sc.prims.astype(np.float64)
+    from paper_2411_16392_b200 import scenes
+    # warm-up on C1 (library load, page-in), then whole views of the workload
+    c1 = scenes.CONFIGS["c1"]()
+    for _ in range(a.warmup):
+        qo.time_full_view(*_cpu_inputs(c1))
+    sc = scene_for(a.config)
+    secs, runs = [], []
+    t_start = time.perf_counter()
+    while len(secs) < max(1, a.steps):
+        v = len(secs) % len(sc.cams)
+        r = qo.time_full_view(*_cpu_inputs(sc, v))
+        secs.append(r["seconds"])
+        runs.append({"view": v, "seconds": r["seconds"], "phases": r["phases"]})
+        if time.perf_counter() - t_start + r["seconds"] > a.ref_budget:
+            break
     cam = sc.cams[0]
-    up = {k: np.asarray(v, np.float64) for k, v in sc.upstream[0].items()}
-    for w in range(a.warmup):
-        qo.time_sampled_view(prims64, cam, up, n_sample=8, seed=100 + w)
-    vals, secs, last = [], [], None
-    for k in range(a.steps):
-        r = qo.time_sampled_view(prims64, cam, up, n_sample=a.cpu_tiles, seed=k)
-        secs.append(r["seconds_per_view_est"])
-        vals.append(cam.width * cam.height / 1e6 / r["seconds_per_view_est"])
-        last = r
-    value = float(np.mean(vals))
-    V = len(sc.cams)
+    px = cam.width * cam.height
+    value = px / 1e6 / float(np.mean(secs))
+    cpu = qo.cpu_model()
     out = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-        "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
-        "ms_per_step": float(np.mean(secs)) * V * 1e3, "higher_is_better": True,
+        "n_gpus": world, "steps": len(secs), "warmup": a.warmup,
+        "ms_per_step": float(np.mean(secs)) * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE config shapes; scenes.py)",
-        "config": {"workload": workload_desc(sc), "views_per_step": V},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": last["threads"], "kind": "port",
-                         "sample": (f"each step: view 0, per-primitive stages in full, "
-                                    f"{last['tiles_sampled']}/{last['tiles']} tiles (systematic, "
-                                    f"seeded offset) for per-pair/per-pixel stages, scaled")},
+        "config": config_of(sc, a),
+        "step": "one whole view of the workload: prepare + forward + backward + chain",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": qo.num_threads(), "kind": "port",
+                         "cpu": cpu["model"], "logical_cores": cpu["logical_cores"],
+                         "sample": f"{len(secs)} whole view(s) of {sc.name}, timed in full"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "views": runs,
     }
     print(json.dumps(out), flush=True)
 
@@ -452,10 +482,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-tiles", type=int, default=96)
+    ap.add_argument("--ref-budget", type=float, default=100.0,
+                    help="reference arm: stop timing whole views after this many seconds")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--exact", action="store_true",
-                    help="RenderSettings.exact_decisions (band decisions in fp64)")
+    ap.add_argument("--fp32-decisions", action="store_true",
+                    help="RenderSettings(exact_decisions=False): selection decisions in fp32 only")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to exercise the multi-rank path on one GPU")

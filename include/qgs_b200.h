@@ -128,9 +128,10 @@ typedef struct qgs_grads {
 /* ---- stage 1: per-primitive preprocessing (rasterizer.py:124-158,
  *      bounds.py:272-292, sh.py:82-88).  Writes the per-primitive state into
  *      `prep` (qgs_prep_bytes(P) bytes) and the total (tile, primitive) pair
- *      count into *d_n_pairs (device int64).  Raises QGS_E_ARG on
- *      non-finite raw scales/signs is NOT checked on device: the Python
- *      layer validates (model.py:37-38). */
+ *      count into *d_n_pairs (device int64) -- or -k when k primitives have
+ *      non-finite raw scales/signs (model.py:37-38: the caller raises
+ *      ParameterError from the one read it makes anyway; qgs_bin must not be
+ *      called then). */
 size_t qgs_prep_bytes(int32_t P);
 int qgs_preprocess(const qgs_params *prims, const qgs_camera *cam,
                    const qgs_settings *st, void *prep, int64_t *d_n_pairs,

@@ -747,6 +747,39 @@ def time_sampled_view(prims, cam, upstream, n_sample=128, seed=0, settings=None)
                        "backward": t2 - t1, "chain": t3 - t2}}
 
 
+def time_full_view(prims, cam, upstream, settings=None):
+    """Time prepare + forward + backward (kernel gradients + chain) of one
+    whole view (CPU baseline and the reference arm of bench.py): nothing
+    sampled, nothing extrapolated."""
+    t0 = time.perf_counter()
+    vw = prepare(prims, cam, settings)
+    t1 = time.perf_counter()
+    fw = forward(vw)
+    t2 = time.perf_counter()
+    kg = kernel_grads(vw, fw, upstream)
+    t3 = time.perf_counter()
+    chain(vw, kg)
+    t4 = time.perf_counter()
+    return {"seconds": t4 - t0, "pairs": int(len(vw.tile_prims)), "threads": num_threads(),
+            "phases": {**{k: round(v, 3) for k, v in vw.timing.items()},
+                       "prepare": round(t1 - t0, 3), "forward": round(t2 - t1, 3),
+                       "backward": round(t3 - t2, 3), "chain": round(t4 - t3, 3)}}
+
+
+def cpu_model():
+    """CPU model string and logical core count of this host."""
+    name = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    name = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"model": name, "logical_cores": os.cpu_count()}
+
+
 def render(prims, cam, settings=None):
     vw = prepare(prims, cam, settings)
     return forward(vw), vw

@@ -68,14 +68,10 @@ BinWs bin_ws(void *base, int32_t tiles_x, int32_t tiles_y, int64_t n_pairs)
     return w;
 }
 
-bool smem_configured = false;
-
 int configure()
 {
-    if (smem_configured) return 0;
-    QGS_CK(cudaFuncSetAttribute(qgs::tile_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)qgs::sort_smem_bytes()));
-    smem_configured = true;
+    QGS_CK(qgs::ensure_smem_attr(reinterpret_cast<const void *>(qgs::tile_sort_kernel),
+                                 (int)qgs::sort_smem_bytes()));
     return 0;
 }
 
@@ -118,12 +114,14 @@ int qgs_preprocess(const qgs_params *prims, const qgs_camera *cam, const qgs_set
         QGS_CK(cudaMemsetAsync(pv.pair_off, 0, sizeof(int64_t), s));
         return 0;
     }
+    QGS_CK(cudaMemsetAsync(pv.nonfinite, 0, sizeof(int32_t), s));
     qgs::preprocess_kernel<<<cdiv(P, 128), 128, 0, s>>>(*prims, ck, pv, st->euclidean_density);
     QGS_LAUNCHED("preprocess_kernel");
     const int nb = (int)scan_blocks(P);
     int64_t *sums = scan_sums_ptr(prep, P);
     qgs::scan_sums_kernel<<<nb, qgs::SCAN_THREADS, 0, s>>>(pv.ntiles, P, sums);
-    qgs::scan_top_kernel<<<1, qgs::SCAN_THREADS, 0, s>>>(sums, nb, d_n_pairs, pv.pair_off, P);
+    qgs::scan_top_kernel<<<1, qgs::SCAN_THREADS, 0, s>>>(sums, nb, d_n_pairs, pv.pair_off, P,
+                                                         pv.nonfinite);
     qgs::scan_out_kernel<<<nb, qgs::SCAN_THREADS, 0, s>>>(pv.ntiles, P, sums, pv.pair_off);
     QGS_LAUNCHED("scan kernels");
     return 0;

@@ -67,7 +67,8 @@ __global__ void scan_sums_kernel(const int32_t *__restrict__ in, int n, int64_t 
 }
 
 // exclusive scan of the block sums (single block, any length)
-__global__ void scan_top_kernel(int64_t *sums, int nb, int64_t *d_total, int64_t *out, int n)
+__global__ void scan_top_kernel(int64_t *sums, int nb, int64_t *d_total, int64_t *out, int n,
+                                const int32_t *nonfinite)   // default nullptr (kernels.cuh)
 {
     __shared__ int64_t s_w[32];
     int64_t carry = 0;
@@ -79,7 +80,13 @@ __global__ void scan_top_kernel(int64_t *sums, int nb, int64_t *d_total, int64_t
         if (i < nb) sums[i] = carry + ex;
         carry += tot;
     }
-    if (threadIdx.x == 0) { *d_total = carry; out[n] = carry; }
+    if (threadIdx.x == 0) {
+        out[n] = carry;
+        // the host's one read per view: the pair count, or -k when k
+        // primitives have non-finite raw scales / signs
+        const int bad = nonfinite ? *nonfinite : 0;
+        *d_total = bad > 0 ? -(int64_t)bad : carry;
+    }
 }
 
 __global__ void scan_out_kernel(const int32_t *__restrict__ in, int n, const int64_t *sums,

@@ -14,7 +14,8 @@ __global__ void export_prep_kernel(PrepView pv, int P, double *scales, double *a
 constexpr int SCAN_THREADS = 1024;
 constexpr int SCAN_ITEMS = SCAN_THREADS * 4;
 __global__ void scan_sums_kernel(const int32_t *in, int n, int64_t *sums);
-__global__ void scan_top_kernel(int64_t *sums, int nb, int64_t *d_total, int64_t *out, int n);
+__global__ void scan_top_kernel(int64_t *sums, int nb, int64_t *d_total, int64_t *out, int n,
+                                const int32_t *nonfinite = nullptr);
 __global__ void scan_out_kernel(const int32_t *in, int n, const int64_t *sums, int64_t *out);
 __global__ void tile_diff_kernel(const int4 *bbox, int P, int tiles_x, int *diff);
 __global__ void tile_offsets_kernel(int *diff, int tiles_x, int tiles_y, int32_t *tile_offsets,

@@ -17,6 +17,7 @@
 // warp and the sample derivatives rather than keeping 5 x k^2 values.  One
 // reciprocal per dehomogenised point.
 #include "multiview.cuh"
+#include "qgs_common.cuh"
 
 namespace qgs {
 
@@ -467,11 +468,10 @@ cudaError_t multiview(MvArgs a, double weight, float *ref_depth, float *ref_alph
     cudaMemsetAsync(a.g_nbr, 0, (size_t)a.Hn * a.Wn * 4 * 8, s);
     const int Kp = (2 * a.r + 1) * (2 * a.r + 1);
     const size_t smem = (size_t)MV_NCACHE * Kp * MV_T * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(multiview_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(MV_NCACHE * MV_MAX_KP * MV_T * sizeof(double)));
-        attr = true;
+    {
+        const cudaError_t e = ensure_smem_attr(reinterpret_cast<const void *>(multiview_kernel),
+                                               (int)(MV_NCACHE * MV_MAX_KP * MV_T * sizeof(double)));
+        if (e != cudaSuccess) return e;
     }
     multiview_kernel<<<grid, MV_T, smem, s>>>(a);
     mv_finish_kernel<<<1, 256, 0, s>>>(a.partial, nblk, values, scal);

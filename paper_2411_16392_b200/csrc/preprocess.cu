@@ -390,6 +390,13 @@ __global__ void preprocess_kernel(qgs_params prm, CamK cam, PrepView pv, int euc
     double s[3];
     bool clamped[3];
     activate(prm.raw_scales + 3 * p, prm.raw_signs + 3 * p, s, clamped);
+    {   // model.py:37-38 (ParameterError): counted here, raised by the host
+        // from the pair-count read it makes anyway (no extra sync)
+        bool fin = true;
+        for (int k = 0; k < 3; ++k)
+            fin = fin && isfinite(prm.raw_scales[3 * p + k]) && isfinite(prm.raw_signs[3 * p + k]);
+        if (!fin) atomicAdd(pv.nonfinite, 1);
+    }
     double alpha = 1.0 / (1.0 + exp(-(double)prm.raw_opacity[p]));
     double R[9], qn[4], qnorm;
     quat_rot(prm.quats + 4 * p, R, qn, qnorm);

@@ -9,11 +9,32 @@
 #pragma once
 
 #include <cstdint>
+#include <mutex>
+#include <set>
+#include <utility>
 #include <cuda_runtime.h>
 
 #include "../../include/qgs_b200.h"
 
 namespace qgs {
+
+// Raise a kernel's dynamic shared-memory limit once per (kernel, device):
+// cudaFuncSetAttribute applies to the current device only, so a process that
+// uses several GPUs needs it on each.  Thread-safe; returns the CUDA status.
+inline cudaError_t ensure_smem_attr(const void *func, int bytes)
+{
+    static std::mutex mu;
+    static std::set<std::pair<const void *, int>> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count({func, dev})) return cudaSuccess;
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.insert({func, dev});
+    return e;
+}
+
 
 constexpr int TILE = 16;            // bounds.py:19
 constexpr int RING = 8;             // raster_kernels.py:26 BUFFER_SIZE
@@ -86,6 +107,7 @@ struct PrepView {
     int4 *bbox;
     int32_t *ntiles;
     int64_t *pair_off;    // P+1
+    int32_t *nonfinite;   // primitives with non-finite raw scales / signs (model.py:37-38)
 };
 
 __host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -101,7 +123,8 @@ __host__ __device__ inline PrepView prep_view(void *base, int32_t P)
     v.conic = reinterpret_cast<ConicRec *>(b + o); o += align256(sizeof(ConicRec) * (size_t)P);
     v.bbox = reinterpret_cast<int4 *>(b + o);      o += align256(sizeof(int4) * (size_t)P);
     v.ntiles = reinterpret_cast<int32_t *>(b + o); o += align256(sizeof(int32_t) * (size_t)P);
-    v.pair_off = reinterpret_cast<int64_t *>(b + o);
+    v.pair_off = reinterpret_cast<int64_t *>(b + o); o += align256(sizeof(int64_t) * ((size_t)P + 1));
+    v.nonfinite = reinterpret_cast<int32_t *>(b + o);
     return v;
 }
 
@@ -110,7 +133,7 @@ __host__ __device__ inline size_t prep_bytes(int32_t P)
     return align256(sizeof(Geo64) * (size_t)P) + align256(sizeof(PrimRec) * (size_t)P) +
            align256(sizeof(ConicRec) * (size_t)P) +
            align256(sizeof(int4) * (size_t)P) + align256(sizeof(int32_t) * (size_t)P) +
-           align256(sizeof(int64_t) * ((size_t)P + 1)) + 256;
+           align256(sizeof(int64_t) * ((size_t)P + 1)) + 256 + 256;
 }
 
 // Camera / settings as kernel arguments (by value).

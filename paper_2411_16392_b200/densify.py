@@ -59,6 +59,30 @@ class DensifyStats:
     def reset(self, n):
         self.__init__(n, self.grad_accum.device)
 
+    def add_view(self, screen_center):
+        """Fold one rendered view's screen-space centre gradient (P, 2) in:
+        train.py:239-243 (norm, seen = norm > 0, accum += norm, count += 1).
+        For several views per step (dist.gpu_step) call once per view."""
+        g = torch.linalg.vector_norm(screen_center.to(torch.float64), dim=1)
+        self.grad_accum += g
+        self.grad_count += (g > 0).to(torch.float64)
+
+    def add_centers(self, centers_grad):
+        """train.py:244: center_accum += grads.centers"""
+        self.center_accum += centers_grad.to(torch.float64)
+
+    def allreduce_(self, group=None):
+        """Sum the per-rank sums and counts (every rank then holds the
+        statistics of all views and makes the same densification plan)."""
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+            flat = torch.cat([self.grad_accum, self.grad_count])
+            dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+            n = self.grad_accum.numel()
+            self.grad_accum.copy_(flat[:n])
+            self.grad_count.copy_(flat[n:])
+        return self
+
 
 _WS = {}
 

@@ -7,7 +7,8 @@ primitives, so rank r takes views {v : v mod W == r}, accumulates its views'
 raw gradients on device (rasterizer.backward(..., out=grads)), and a single
 NCCL all-reduce (SUM) over NVLink makes every rank hold the full gradient.
 The per-view screen-space centre gradient (a densification statistic, not a
-parameter gradient, train.py:239-244) is kept per rank and not reduced.
+parameter gradient, train.py:239-244) is folded per view into the
+densification statistics, which are all-reduced with the gradients.
 
 The same code runs over gloo on CPU in the tests, with the per-view backward
 supplied by the caller.
@@ -125,18 +126,44 @@ def upload_async(host_items, dev_items, copy=None):
     return evs
 
 
-def gpu_step(dev_prims, cams, upstreams, settings, rank, world, grads=None, group=None):
-    """The B200 step used by bench.py: this rank's views through the sm_100a
-    rasterizer, gradients accumulated in one flat device buffer, one NCCL
-    all-reduce.  `upstreams[v]` is the upstream dict of view v (device tensors)."""
+def gpu_step(dev_prims, cams, upstreams, settings, rank, world, grads=None, group=None,
+             views=None, side=None, hook=None, counters=None, stats=None):
+    """The B200 step (bench.py runs exactly this): this rank's views through
+    the sm_100a rasterizer, raw gradients accumulated in one flat device
+    buffer, one all-reduce (NCCL over NVLink; gloo in the tests).
+
+    upstreams[v]: the upstream dict of view v (device tensors; a dict keyed
+    by view or a list over all views).  views: this rank's views (default:
+    the round-robin shard).  hook(event, i): called on the host at
+    "view_begin" / "fwd_end" / "bwd_end" / "view_end" of the i-th local view
+    and at "reduce_begin" / "reduce_end" (bench.py records CUDA events there).
+    counters: forward work counters (rasterizer.forward).  stats: a
+    densify.DensifyStats -- each view's screen-space centre gradient norm is
+    folded in per view (train.py:239-244 semantics: one norm per rendered
+    view), and the sums and counts are all-reduced with the gradients, so
+    every rank makes the same densification decisions."""
     from . import rasterizer as rz
+    hook = hook or (lambda *_: None)
     if grads is None:
         grads = rz.GradientBuffer.zeros_flat(dev_prims)
     else:
         grads.zero_()
-    for _, v, prep in pipelined_prepare(dev_prims, cams, shard_views(len(cams), rank, world),
-                                         settings):
-        tg = rz.forward(prep)
-        rz.backward(prep, tg, upstreams[v], out=grads)
+    views = shard_views(len(cams), rank, world) if views is None else views
+    for i, v, prep in pipelined_prepare(dev_prims, cams, views, settings, side):
+        hook("view_begin", i)
+        tg = rz.forward(prep, counters=counters)
+        hook("fwd_end", i)
+        kg = rz.kernel_grads(prep, tg, upstreams[v])
+        hook("bwd_end", i)
+        if stats is not None:
+            grads.screen_center.zero_()
+        rz.chain(prep, kg, grads)
+        if stats is not None:
+            stats.add_view(grads.screen_center)
+        hook("view_end", i)
+    hook("reduce_begin", len(views))
     allreduce_(grads.buffer, group)
+    if stats is not None:
+        stats.allreduce_(group)
+    hook("reduce_end", len(views))
     return grads

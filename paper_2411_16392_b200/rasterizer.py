@@ -44,10 +44,11 @@ class RenderSettings:
     # extension (not in the reference): False disables the forward's
     # screen-space conic cull; outputs are identical either way
     conic_cull: bool = True
-    # extension: True re-makes in float64 every selection / alpha-floor
-    # decision whose fp32 margin lies in its rounding band (the reference's
-    # float64 accepted set at full scale; the raster kernels run ~20 % slower)
-    exact_decisions: bool = False
+    # extension: True (the default) re-makes in float64 every selection /
+    # alpha-floor decision whose fp32 margin lies in its rounding band, so the
+    # accepted set is the reference's float64 one at full scale; False keeps
+    # the fp32 decisions (faster, a few acceptance flips per million pixels)
+    exact_decisions: bool = True
 
 
 # ----------------------------------------------------------------- helpers
@@ -85,7 +86,7 @@ def _settings_struct(st):
     s.alpha_clamp, s.t_term = float(st.alpha_clamp), float(st.t_term)
     s.resort, s.euclidean_density = int(bool(st.resort)), int(bool(st.euclidean_density))
     s.no_cull = int(not getattr(st, "conic_cull", True))
-    s.exact_decisions = int(bool(getattr(st, "exact_decisions", False)))
+    s.exact_decisions = int(bool(getattr(st, "exact_decisions", True)))
     return s
 
 
@@ -131,13 +132,13 @@ class DevicePrimitives:
         return p
 
 
-def _validate(prims):
-    """model.py:37-38: non-finite raw scales / signs raise ParameterError."""
+def _validate_host(prims):
+    """model.py:37-38 for host (numpy) inputs: non-finite raw scales / signs
+    raise ParameterError before anything is uploaded.  Device inputs are
+    checked by the preprocess kernel (a negative pair count, no extra sync)."""
     for f in ("raw_scales", "raw_signs"):
         a = getattr(prims, f)
-        ok = bool(torch.isfinite(a).all()) if isinstance(a, torch.Tensor) else \
-            bool(np.isfinite(np.asarray(a)).all())
-        if not ok:
+        if not isinstance(a, torch.Tensor) and not np.isfinite(np.asarray(a)).all():
             raise ParameterError("non-finite raw scale/sign")
 
 
@@ -336,7 +337,7 @@ def prepare(prims, cam, settings: RenderSettings = None, validate=True) -> Prepa
     settings = settings or RenderSettings()
     L = _lib.load()
     if validate:
-        _validate(prims)
+        _validate_host(prims)
     dev = DevicePrimitives.from_host(prims)
     device = dev.centers.device
     P = len(dev)
@@ -349,6 +350,8 @@ def prepare(prims, cam, settings: RenderSettings = None, validate=True) -> Prepa
     _lib.check(L.qgs_preprocess(pp, cam_c, st_c, _ptr(prep), _ptr(n_dev), _stream()),
                "qgs_preprocess")
     n_pairs = int(n_dev.item())              # the one host sync per view
+    if n_pairs < 0:                          # -k: k primitives with non-finite raw scales/signs
+        raise ParameterError(f"non-finite raw scale/sign ({-n_pairs} primitives)")
     n_tiles = tiles_x * tiles_y
     ws_bytes = L.qgs_bin_workspace_bytes(P, n_pairs, n_tiles)
     ws = torch.empty((ws_bytes,), dtype=torch.uint8, device=device)

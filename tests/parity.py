@@ -65,3 +65,79 @@ def grad_report(gpu, ref):
     out["violations"] = tot_bad
     out["n"] = tot
     return out
+
+
+def over_tol_mask(gpu, ref):
+    """pixels over IMG_TOL on any of colour / alpha / depth / normal"""
+    bad = np.zeros(np.asarray(ref["alpha"]).shape, dtype=bool)
+    for k in IMG_MAPS:
+        d = np.abs(np.asarray(gpu[k], dtype=np.float64) - np.asarray(ref[k], dtype=np.float64))
+        bad |= (d.max(axis=2) if d.ndim == 3 else d) > IMG_TOL
+    return bad
+
+
+def classify_stream(g_prims, o_prims):
+    """SURVEY.md 8(c).3 class of one pixel from its two emitted streams
+    (primitive ids in compositing order, GPU vs oracle)."""
+    g, o = np.asarray(g_prims), np.asarray(o_prims)
+    if len(g) != len(o):
+        return "count_flip"
+    if np.array_equal(g, o):
+        return "continuous"            # same fragments, same order: unexplained
+    if np.array_equal(np.sort(g), np.sort(o)):
+        return "order_swap"
+    return "membership"
+
+
+def classify_pixels(prep, vw, gpu, ref, mask=None, limit=400):
+    """Classify every pixel of `mask` (default: over tolerance) by comparing
+    the GPU's emitted stream (PreparedView.trace_pixel: the same inline
+    functions as the raster kernels) with the oracle's (qgs_oracle.trace_pixel:
+    the C restatement of forward_kernel).  Returns counts per class plus the
+    first few pixels of each class; pixels beyond `limit` count as
+    'unclassified'."""
+    from oracle import qgs_oracle as qo
+    mask = over_tol_mask(gpu, ref) if mask is None else mask
+    vs, us = np.nonzero(mask)
+    out = {"count_flip": 0, "order_swap": 0, "membership": 0, "continuous": 0,
+           "unclassified": 0, "examples": {}}
+    for i, (v, u) in enumerate(zip(vs.tolist(), us.tolist())):
+        if i >= limit:
+            out["unclassified"] += 1
+            continue
+        if int(np.asarray(gpu["n_fragments"])[v, u]) != int(np.asarray(ref["n_fragments"])[v, u]):
+            c = "count_flip"
+        else:
+            _, ge = prep.trace_pixel(u, v)
+            _, oe = qo.trace_pixel(vw, u, v)
+            c = classify_stream(ge["prim"], oe["prim"])
+        out[c] += 1
+        out["examples"].setdefault(c, [])
+        if len(out["examples"][c]) < 4:
+            out["examples"][c].append((u, v))
+    return out
+
+
+def median_flips(prep, vw, gpu, ref, tol=IMG_TOL, band=1e-5, limit=200):
+    """depth_median is t of the last fragment composited while T > 0.5
+    (raster_kernels.py:152): a discontinuous decision.  Same-count pixels
+    whose median differs by more than `tol` must be T = 0.5 crossings within
+    `band` in the oracle's own stream (or differ in their streams).  Returns
+    (n_mismatch, n_unexplained)."""
+    from oracle import qgs_oracle as qo
+    same = np.asarray(gpu["n_fragments"]) == np.asarray(ref["n_fragments"])
+    d = np.abs(np.asarray(gpu["depth_median"], np.float64) - np.asarray(ref["depth_median"], np.float64))
+    vs, us = np.nonzero((d > tol) & same)
+    bad = 0
+    for i, (v, u) in enumerate(zip(vs.tolist(), us.tolist())):
+        if i >= limit:
+            bad += 1
+            continue
+        _, oe = qo.trace_pixel(vw, u, v)
+        _, ge = prep.trace_pixel(u, v)
+        if classify_stream(ge["prim"], oe["prim"]) != "continuous":
+            continue                  # a different stream explains it
+        T = np.asarray(oe["T"])       # T before each fragment
+        if not np.any(np.abs(T - 0.5) <= band):
+            bad += 1
+    return len(vs), bad

@@ -26,3 +26,6 @@ def test_reference_arm_json_line():
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
     assert d["config"]["workload"].startswith("c1")
+    # whole views timed (no extrapolation): steps x ms_per_step is real time
+    assert "whole view" in d["step"] and cb["cpu"] and cb["logical_cores"] >= 1
+    assert d["views"][0]["seconds"] * 1e3 == d["ms_per_step"]

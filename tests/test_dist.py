@@ -124,3 +124,104 @@ def test_upload_async_and_pipelined_prepare(cuda_device):
         main.wait_event(evs[i])
         for k, t in host[i].items():
             assert torch.equal(dst[i][k].cpu(), t), k
+
+
+# ------------------------------------------------ densification statistics
+
+def _stats_worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2411_16392_b200.densify import DensifyStats
+    sc_views = _screen_views()
+    st = DensifyStats(7, device=torch.device("cpu"))
+    for v in qd.shard_views(len(sc_views), rank, world):
+        st.add_view(sc_views[v])
+    st.allreduce_()
+    np.savez(os.path.join(out_dir, f"stats{rank}.npz"), accum=st.grad_accum.numpy(),
+             count=st.grad_count.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _screen_views():
+    rng = np.random.default_rng(9)
+    out = []
+    for v in range(5):
+        sc = rng.normal(size=(7, 2))
+        sc[rng.random(7) < 0.4] = 0.0           # unseen primitives in this view
+        out.append(torch.from_numpy(sc.astype(np.float32)))
+    return out
+
+
+@pytest.mark.timeout(300)
+def test_densify_stats_allreduce_matches_single_process(tmp_path):
+    """each rank folds ONE norm per rendered view (train.py:239-243)
+    and the sums / counts are all-reduced, so every rank makes the same
+    densification plan as one process rendering all the views."""
+    from paper_2411_16392_b200.densify import DensifyStats
+    world = 2
+    mp.spawn(_stats_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    ref = DensifyStats(7, device=torch.device("cpu"))
+    acc = np.zeros(7)
+    cnt = np.zeros(7)
+    for sc in _screen_views():
+        ref.add_view(sc)
+        g = np.linalg.norm(sc.numpy().astype(np.float64), axis=1)   # train.py:239-243
+        acc[g > 0] += g[g > 0]
+        cnt[g > 0] += 1
+    assert np.allclose(ref.grad_accum.numpy(), acc, rtol=1e-12)
+    assert np.array_equal(ref.grad_count.numpy(), cnt)
+    for r in range(world):
+        d = np.load(tmp_path / f"stats{r}.npz")
+        assert np.allclose(d["accum"], acc, rtol=1e-12), r
+        assert np.array_equal(d["count"], cnt), r
+
+
+# ------------------------------------- the CUDA step over two ranks (gloo)
+
+def _gpu_worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2411_16392_b200 import rasterizer as rz, scenes
+    from paper_2411_16392_b200.densify import DensifyStats
+    sc = scenes.config2(seed=3, n=4000, res=96, views=4)
+    dev = rz.DevicePrimitives.from_host(sc.prims)
+    ups = {v: {k: torch.from_numpy(np.ascontiguousarray(a)).cuda() for k, a in sc.upstream[v].items()}
+           for v in range(4)}
+    stats = DensifyStats(len(dev))
+    g = qd.gpu_step(dev, sc.cams, ups, rz.RenderSettings(), rank, world, stats=stats)
+    torch.cuda.synchronize()
+    np.savez(os.path.join(out_dir, f"gpu{rank}.npz"), flat=g.buffer.cpu().numpy(),
+             accum=stats.grad_accum.cpu().numpy(), count=stats.grad_count.cpu().numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(600)
+def test_two_rank_cuda_step_matches_single_process(tmp_path, cuda_device):
+    """dist.gpu_step with the sm_100a rasterizer on two ranks (gloo, both on
+    cuda:0): every rank ends with the single-process sum over all four views
+    (to fp32-atomic reordering), and the same densification statistics."""
+    from paper_2411_16392_b200 import rasterizer as rz, scenes
+    from paper_2411_16392_b200.densify import DensifyStats
+    world = 2
+    mp.spawn(_gpu_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    sc = scenes.config2(seed=3, n=4000, res=96, views=4)
+    dev = rz.DevicePrimitives.from_host(sc.prims)
+    ups = {v: {k: torch.from_numpy(np.ascontiguousarray(a)).cuda() for k, a in sc.upstream[v].items()}
+           for v in range(4)}
+    stats = DensifyStats(len(dev))
+    ref = qd.gpu_step(dev, sc.cams, ups, rz.RenderSettings(), 0, 1, stats=stats)
+    ref_flat = ref.buffer.cpu().numpy()
+    scale = np.abs(ref_flat).max()
+    assert scale > 0
+    r = [np.load(tmp_path / f"gpu{k}.npz") for k in range(world)]
+    assert np.array_equal(r[0]["flat"], r[1]["flat"])          # identical on every rank
+    assert np.allclose(r[0]["flat"], ref_flat, rtol=1e-4, atol=1e-6 * scale)
+    for k in range(world):
+        assert np.array_equal(r[k]["count"], stats.grad_count.cpu().numpy())
+        assert np.allclose(r[k]["accum"], stats.grad_accum.cpu().numpy(), rtol=1e-5, atol=1e-9)
