@@ -78,6 +78,9 @@ typedef struct qgs_params {
 
 /* Forward outputs, RenderTargets (rasterizer.py:61-74).  Maps are H*W
  * row-major (x3 interleaved for colour/normal). */
+#define QGS_FRAG_PAGE 16        /* fragment slots per pixel per log page */
+#define QGS_FRAG_MAX_PAGES 32   /* pages per raster warp: 512 fragments per pixel */
+
 typedef struct qgs_targets {
     float *color;              /* color_raw + T * background */
     float *color_raw;
@@ -92,22 +95,30 @@ typedef struct qgs_targets {
                                   the pixel box, [1] accepted fragments, [2] composited,
                                   [3] candidates left by the conic cull, [4] candidates
                                   passing the coarse fp32 test (5 entries) */
-    int32_t *frag_prim;        /* optional fragment log (NULL = none): for every pixel, the
-                                  primitive of each composited fragment in compositing
-                                  order; layout [raster warp][k < frag_cap][lane], one
-                                  raster warp per 8x4 block, 8 per tile (tile-major);
-                                  the backward reads it instead of replaying */
-    double *frag_t;            /* same layout: float64 depth of each logged fragment */
-    float *frag_xy;            /* optional, same layout x2: the fragment's local hit point
-                                  (x, y) as the forward shaded it; lets the backward re-shade
-                                  in fp32 without the primitive's float64 geometry */
+    /* Optional fragment log (frag_prim == NULL: none), written by the forward
+     * and read by the backward instead of replaying the candidate tests.
+     * Paged: a pool of pages, each QGS_FRAG_PAGE fragment slots deep for the
+     * 32 pixels of one raster warp (an 8x4 block), slot (page, k, lane) at
+     * ((page * QGS_FRAG_PAGE + k) * 32 + lane).  A raster warp takes pages
+     * from the pool (atomically, *frag_pool_next) as its deepest pixel grows,
+     * up to QGS_FRAG_MAX_PAGES; its page ids go to
+     * frag_page_table[warp * QGS_FRAG_MAX_PAGES + i] and their number to
+     * frag_page_count[warp] (-1: pool exhausted or a pixel deeper than
+     * QGS_FRAG_PAGE * QGS_FRAG_MAX_PAGES -- the backward replays that block
+     * with the full candidate test).  Warps are 8 per tile, tile-major.  So
+     * memory scales with the fragments composited, not with pixels x cap. */
+    int32_t *frag_prim;        /* pool: primitive of each logged fragment */
+    double *frag_t;            /* pool: its float64 depth */
+    float *frag_xy;            /* pool x2 (optional): its local hit point (x, y) as the
+                                  forward shaded it, so the backward re-shades in fp32 */
+    int32_t *frag_page_table;  /* n_warps * QGS_FRAG_MAX_PAGES */
+    int32_t *frag_page_count;  /* n_warps */
+    int32_t *frag_pool_next;   /* device counter: pages handed out (the forward zeroes it) */
+    int32_t frag_pool_pages;   /* pool capacity in pages */
     int32_t *tile_order;       /* optional scratch of tiles_x*tiles_y ints: the forward
                                   fills it with the tiles by descending pair count and
                                   both raster kernels run the heaviest tiles first (NULL:
                                   natural order) */
-    int32_t frag_cap;          /* fragments logged per pixel; a block with a pixel over
-                                  the cap (or no log) is replayed by the backward with
-                                  the full candidate test */
 } qgs_targets;
 
 /* Upstream map gradients (rasterizer.py:230-250); NULL = all zero. */
@@ -176,6 +187,22 @@ int qgs_backward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_s
                  const qgs_targets *fwd, const qgs_upstream *up, float *kg,
                  qgs_stream_t stream);
 
+/* ---- stage 4, deterministic variant (RenderSettings.deterministic): the
+ *      same kernel gradients, added to kg in a fixed order with fp64 sums --
+ *      bitwise repeatable like the reference's serial merge
+ *      (raster_kernels.py:673-681; pkg/tests/test_rasterizer_gradients.py:
+ *      217-229).  Each composited fragment writes its slots to a row fixed
+ *      by the forward (a scan of n_fragments in raster-warp order); rows are
+ *      grouped per primitive by a stable radix sort and summed in row order.
+ *      n_frags = the sum of fwd->n_fragments; workspace from
+ *      qgs_backward_det_workspace_bytes. */
+size_t qgs_backward_det_workspace_bytes(int32_t P, int64_t n_frags, const qgs_camera *cam);
+int qgs_backward_deterministic(const void *prep, int32_t P, const qgs_camera *cam,
+                               const qgs_settings *st, const int32_t *tile_offsets,
+                               const int32_t *tile_prims, const qgs_targets *fwd,
+                               const qgs_upstream *up, float *kg, int64_t n_frags,
+                               void *workspace, size_t workspace_bytes, qgs_stream_t stream);
+
 /* ---- stage 5: chain to raw parameters (rasterizer.py:270-334). */
 int qgs_chain(const qgs_params *prims, const void *prep, const float *kg,
               const qgs_camera *cam, const qgs_grads *out, qgs_stream_t stream);
@@ -186,6 +213,23 @@ int qgs_chain(const qgs_params *prims, const void *prep, const float *kg,
 int qgs_export_prep(const void *prep, int32_t P, double *scales, double *alphas,
                     double *colors, int32_t *pix_bbox, uint8_t *planar,
                     qgs_stream_t stream);
+
+/* The rest of the reference's PreparedView (rasterizer.py:33-58, populated
+ * at :124-195), recomputed on the device from the raw parameters with the
+ * same fp64 device functions as qgs_preprocess (ohat, M, wv are the exact
+ * values the raster kernels use).  Any pointer may be NULL.  Shapes:
+ * R, M, Nmat P*9 (row-major 3x3), ohat, wv, view_dirs P*3, lam P*2,
+ * view_dist P (f64); clamped, color_clamped P*3 (u8). */
+typedef struct qgs_prep_export {
+    double *R, *ohat, *M, *Nmat, *wv, *lam, *view_dirs, *view_dist;
+    uint8_t *clamped, *color_clamped;
+} qgs_prep_export;
+int qgs_export_prep_geometry(const qgs_params *prims, const void *prep, const qgs_camera *cam,
+                             const qgs_prep_export *out, qgs_stream_t stream);
+
+/* PreparedView.dirs: unit camera-frame ray of every pixel centre
+ * (cameras.py:53-59, the reference's operation order), H*W*3 f64. */
+int qgs_pixel_dirs(const qgs_camera *cam, double *dirs, qgs_stream_t stream);
 
 /* Diagnostics: replay one pixel's fragment stream (same device functions as
  * the raster kernels) and record up to `max` accepted candidates (tile-list

@@ -42,8 +42,9 @@ class Targets(ctypes.Structure):
     _fields_ = [(n, vp) for n in ("color", "color_raw", "alpha", "depth", "depth_sq",
                                   "depth_median", "normal", "curvature", "distortion",
                                   "transmittance", "n_fragments", "violations", "aux",
-                                  "counters", "frag_prim", "frag_t", "frag_xy", "tile_order")] + \
-        [("frag_cap", i32)]
+                                  "counters", "frag_prim", "frag_t", "frag_xy", "frag_page_table",
+                                  "frag_page_count", "frag_pool_next")] + \
+        [("frag_pool_pages", i32), ("tile_order", vp)]
 
 
 class Upstream(ctypes.Structure):
@@ -89,6 +90,11 @@ class MvGrads(ctypes.Structure):
     _fields_ = [(n, vp) for n in ("depth", "alpha", "normal")]
 
 
+class PrepExport(ctypes.Structure):
+    _fields_ = [(n, vp) for n in ("R", "ohat", "M", "Nmat", "wv", "lam", "view_dirs",
+                                  "view_dist", "clamped", "color_clamped")]
+
+
 class QGSError(RuntimeError):
     pass
 
@@ -117,8 +123,14 @@ def load():
         "qgs_forward": (ctypes.c_int, [vp, i32, P(Camera), P(Settings), vp, vp, P(Targets), vp]),
         "qgs_backward": (ctypes.c_int, [vp, i32, P(Camera), P(Settings), vp, vp, P(Targets),
                                         P(Upstream), vp, vp]),
+        "qgs_backward_det_workspace_bytes": (ctypes.c_size_t, [i32, i64, P(Camera)]),
+        "qgs_backward_deterministic": (ctypes.c_int, [vp, i32, P(Camera), P(Settings), vp, vp,
+                                                      P(Targets), P(Upstream), vp, i64, vp,
+                                                      ctypes.c_size_t, vp]),
         "qgs_chain": (ctypes.c_int, [P(Params), vp, vp, P(Camera), P(Grads), vp]),
         "qgs_export_prep": (ctypes.c_int, [vp, i32, vp, vp, vp, vp, vp, vp]),
+        "qgs_export_prep_geometry": (ctypes.c_int, [P(Params), vp, P(Camera), P(PrepExport), vp]),
+        "qgs_pixel_dirs": (ctypes.c_int, [P(Camera), vp, vp]),
         "qgs_trace_pixel": (ctypes.c_int, [vp, i32, P(Camera), P(Settings), vp, vp, i32, i32,
                                            i32] + [vp] * 9),
         "qgs_loss_workspace_bytes": (ctypes.c_size_t, [i32, i32, i32]),
@@ -155,8 +167,9 @@ def load():
 
 
 EXPORTS = ("qgs_prep_bytes", "qgs_preprocess", "qgs_bin_workspace_bytes", "qgs_bin",
-           "qgs_sorted_keys", "qgs_tile_keys_f64", "qgs_forward", "qgs_backward", "qgs_chain",
-           "qgs_export_prep", "qgs_trace_pixel", "qgs_loss_workspace_bytes",
+           "qgs_sorted_keys", "qgs_tile_keys_f64", "qgs_forward", "qgs_backward", "qgs_backward_det_workspace_bytes",
+           "qgs_backward_deterministic", "qgs_chain",
+           "qgs_export_prep", "qgs_export_prep_geometry", "qgs_pixel_dirs", "qgs_trace_pixel", "qgs_loss_workspace_bytes",
            "qgs_loss_photometric", "qgs_loss_distortion", "qgs_depth_to_normal",
            "qgs_loss_normal_consistency", "qgs_adam_step", "qgs_densify_workspace_bytes",
            "qgs_densify_plan", "qgs_densify_apply", "qgs_reset_opacity",

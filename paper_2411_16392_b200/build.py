@@ -31,6 +31,7 @@ UNITS = {
     "losses.cu": ["-fmad=false"],
     "optim.cu": ["-fmad=false"],
     "multiview.cu": ["-fmad=false"],
+    "det_reduce.cu": [],
     "abi.cu": [],
 }
 

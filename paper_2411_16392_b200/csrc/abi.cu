@@ -228,6 +228,13 @@ int qgs_forward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_se
     qgs::PrepView pv = qgs::prep_view(const_cast<void *>(prep), P);
     if (out->violations)
         QGS_CK(cudaMemsetAsync(out->violations, 0, sizeof(int32_t) * ck.tiles_x * ck.tiles_y, s));
+    if (out->frag_prim) {
+        if (!out->frag_t || !out->frag_page_table || !out->frag_page_count || !out->frag_pool_next)
+            return fail(QGS_E_ARG, "fragment log: frag_t, page table, page count and pool "
+                                   "counter are required with frag_prim");
+        if (out->frag_pool_pages < 0) return fail(QGS_E_ARG, "frag_pool_pages < 0");
+        QGS_CK(cudaMemsetAsync(out->frag_pool_next, 0, sizeof(int32_t), s));
+    }
     if (out->tile_order) {
         qgs::tile_order_kernel<<<1, 1024, qgs::ORDER_SMEM, s>>>(tile_offsets, ck.tiles_x * ck.tiles_y,
                                                               out->tile_order, 0);
@@ -247,29 +254,82 @@ int qgs_forward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_se
     return 0;
 }
 
-int qgs_backward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settings *st,
-                 const int32_t *tile_offsets, const int32_t *tile_prims, const qgs_targets *fwd,
-                 const qgs_upstream *up, float *kg, qgs_stream_t stream)
+namespace {
+int backward_impl(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settings *st,
+                  const int32_t *tile_offsets, const int32_t *tile_prims, const qgs_targets *fwd,
+                  const qgs_upstream *up, float *kg, const qgs::DetRows &det, cudaStream_t s)
+{
+    qgs::CamK ck = qgs::make_camk(*cam);
+    qgs::SetK sk = qgs::make_setk(*st);
+    qgs::PrepView pv = qgs::prep_view(const_cast<void *>(prep), P);
+    if (det.rows)
+        qgs::raster_bwd_det_kernel<<<ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE,
+                                     qgs::RASTER_THREADS, 0, s>>>(pv.rec, pv.geo, tile_offsets,
+                                                                    tile_prims, ck, sk, *fwd, *up,
+                                                                    kg, det);
+    else if (sk.exact)
+        qgs::raster_bwd_exact_kernel<<<ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE,
+                                 qgs::RASTER_THREADS, 0, s>>>(pv.rec, pv.geo, tile_offsets, tile_prims, ck,
+                                                                sk, *fwd, *up, kg, det);
+    else
+        qgs::raster_bwd_kernel<<<ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE,
+                                 qgs::RASTER_THREADS, 0, s>>>(pv.rec, pv.geo, tile_offsets, tile_prims, ck,
+                                                                sk, *fwd, *up, kg, det);
+    QGS_LAUNCHED("raster_bwd_kernel");
+    return 0;
+}
+
+int backward_checks(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settings *st,
+                    const int32_t *tile_offsets, const qgs_targets *fwd, const qgs_upstream *up,
+                    float *kg)
 {
     if (!prep || !st || !fwd || !up || !tile_offsets || (!kg && P > 0))
         return fail(QGS_E_ARG, "NULL argument");
     if (P == 0) return 0;
     if (!fwd->aux) return fail(QGS_E_ARG, "backward needs the forward's aux planes");
     if (int rc = check_cam(cam)) return rc;
-    if (int rc = configure()) return rc;
+    return configure();
+}
+}  // namespace
+
+int qgs_backward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settings *st,
+                 const int32_t *tile_offsets, const int32_t *tile_prims, const qgs_targets *fwd,
+                 const qgs_upstream *up, float *kg, qgs_stream_t stream)
+{
+    if (int rc = backward_checks(prep, P, cam, st, tile_offsets, fwd, up, kg)) return rc;
+    if (P == 0) return 0;
+    qgs::DetRows none{nullptr, nullptr, nullptr};
+    return backward_impl(prep, P, cam, st, tile_offsets, tile_prims, fwd, up, kg, none,
+                         reinterpret_cast<cudaStream_t>(stream));
+}
+
+size_t qgs_backward_det_workspace_bytes(int32_t P, int64_t n_frags, const qgs_camera *cam)
+{
+    if (!cam || P < 0 || n_frags < 0) return 0;
+    const qgs::CamK ck = qgs::make_camk(*cam);
+    return qgs::det_workspace_bytes(P, n_frags, ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE);
+}
+
+int qgs_backward_deterministic(const void *prep, int32_t P, const qgs_camera *cam,
+                               const qgs_settings *st, const int32_t *tile_offsets,
+                               const int32_t *tile_prims, const qgs_targets *fwd,
+                               const qgs_upstream *up, float *kg, int64_t n_frags,
+                               void *workspace, size_t workspace_bytes, qgs_stream_t stream)
+{
+    if (int rc = backward_checks(prep, P, cam, st, tile_offsets, fwd, up, kg)) return rc;
+    if (P == 0) return 0;
+    if (!workspace || n_frags < 0 || n_frags > 0xffffffffLL)
+        return fail(QGS_E_ARG, "deterministic backward: workspace / n_frags out of range");
+    if (workspace_bytes < qgs_backward_det_workspace_bytes(P, n_frags, cam))
+        return fail(QGS_E_CAPACITY, "deterministic backward workspace too small");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    qgs::CamK ck = qgs::make_camk(*cam);
-    qgs::SetK sk = qgs::make_setk(*st);
-    qgs::PrepView pv = qgs::prep_view(const_cast<void *>(prep), P);
-    if (sk.exact)
-        qgs::raster_bwd_exact_kernel<<<ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE,
-                                 qgs::RASTER_THREADS, 0, s>>>(pv.rec, pv.geo, tile_offsets, tile_prims, ck,
-                                                                sk, *fwd, *up, kg);
-    else
-        qgs::raster_bwd_kernel<<<ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE,
-                                 qgs::RASTER_THREADS, 0, s>>>(pv.rec, pv.geo, tile_offsets, tile_prims, ck,
-                                                                sk, *fwd, *up, kg);
-    QGS_LAUNCHED("raster_bwd_kernel");
+    const qgs::CamK ck = qgs::make_camk(*cam);
+    const int n_warps = ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE;
+    qgs::DetRows det;
+    QGS_CK(qgs::det_prepare(ck, fwd->n_fragments, P, n_frags, workspace, workspace_bytes, det, s));
+    if (int rc = backward_impl(prep, P, cam, st, tile_offsets, tile_prims, fwd, up, kg, det, s))
+        return rc;
+    QGS_CK(qgs::det_finish(P, n_frags, n_warps, workspace, kg, s));
     return 0;
 }
 
@@ -316,6 +376,31 @@ int qgs_export_prep(const void *prep, int32_t P, double *scales, double *alphas,
     qgs::export_prep_kernel<<<cdiv(P, 128), 128, 0, s>>>(pv, P, scales, alphas, colors, pix_bbox,
                                                         planar);
     QGS_LAUNCHED("export_prep_kernel");
+    return 0;
+}
+
+int qgs_export_prep_geometry(const qgs_params *prims, const void *prep, const qgs_camera *cam,
+                             const qgs_prep_export *out, qgs_stream_t stream)
+{
+    if (!prims || !prep || !out) return fail(QGS_E_ARG, "NULL argument");
+    if (int rc = check_cam(cam)) return rc;
+    if (prims->P == 0) return 0;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    qgs::PrepView pv = qgs::prep_view(const_cast<void *>(prep), prims->P);
+    qgs::export_geom_kernel<<<cdiv(prims->P, 128), 128, 0, s>>>(*prims, qgs::make_camk(*cam), pv,
+                                                               *out);
+    QGS_LAUNCHED("export_geom_kernel");
+    return 0;
+}
+
+int qgs_pixel_dirs(const qgs_camera *cam, double *dirs, qgs_stream_t stream)
+{
+    if (!dirs) return fail(QGS_E_ARG, "NULL argument");
+    if (int rc = check_cam(cam)) return rc;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    qgs::CamK ck = qgs::make_camk(*cam);
+    qgs::pixel_rays_kernel<<<cdiv((long long)ck.W * ck.H, 256), 256, 0, s>>>(ck, dirs);
+    QGS_LAUNCHED("pixel_rays_kernel");
     return 0;
 }
 

@@ -21,6 +21,7 @@ __global__ void tile_diff_kernel(const int4 *bbox, int P, int tiles_x, int *diff
 __global__ void tile_offsets_kernel(int *diff, int tiles_x, int tiles_y, int32_t *tile_offsets,
                                     int32_t *cursor);
 __global__ void pixel_rays_kernel(CamK cam, double *rays);
+__global__ void export_geom_kernel(qgs_params prm, CamK cam, PrepView pv, qgs_prep_export o);
 __global__ void pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
                                 const double *rays, int32_t *cursor, uint64_t *bucket);
 __global__ void tile_sort_kernel(const int32_t *tile_offsets, uint64_t *keys, uint64_t *tmp,
@@ -37,6 +38,18 @@ __global__ void tile_keys_f64_kernel(int64_t n, const int64_t *pair_tiles,
 size_t sort_smem_bytes();
 int sort_threads();                 // binning.cu SORT_T
 
+// det_reduce.cu (RenderSettings.deterministic): fragment (pixel, k) of the
+// backward writes its kernel-gradient slots to row base[warp * 32 + lane] + k
+struct DetRows {
+    const int64_t *base;   // per raster-warp lane
+    float *rows;           // [rows][KG]
+    int32_t *prim;         // [rows]
+};
+size_t det_workspace_bytes(int P, int64_t n_frags, int n_warps);
+cudaError_t det_prepare(const CamK &cam, const int32_t *n_frag, int P, int64_t n_frags, void *ws,
+                        size_t ws_bytes, DetRows &out, cudaStream_t s);
+cudaError_t det_finish(int P, int64_t n_frags, int n_warps, void *ws, float *kg, cudaStream_t s);
+
 // raster.cu
 __global__ void raster_fwd_kernel(const PrimRec *recs, const Geo64 *geo, const ConicRec *conics,
                                   const int32_t *tile_offsets,
@@ -48,10 +61,14 @@ __global__ void raster_fwd_exact_kernel(const PrimRec *recs, const Geo64 *geo,
 __global__ void raster_bwd_exact_kernel(const PrimRec *recs, const Geo64 *geo,
                                         const int32_t *tile_offsets, const int32_t *tile_prims,
                                         CamK cam, SetK st, qgs_targets fwd, qgs_upstream upst,
-                                        float *kg);
+                                        float *kg, DetRows det);
 __global__ void raster_bwd_kernel(const PrimRec *recs, const Geo64 *geo, const int32_t *tile_offsets,
                                   const int32_t *tile_prims, CamK cam, SetK st, qgs_targets fwd,
-                                  qgs_upstream upst, float *kg);
+                                  qgs_upstream upst, float *kg, DetRows det);
+__global__ void raster_bwd_det_kernel(const PrimRec *recs, const Geo64 *geo,
+                                      const int32_t *tile_offsets, const int32_t *tile_prims,
+                                      CamK cam, SetK st, qgs_targets fwd, qgs_upstream upst,
+                                      float *kg, DetRows det);
 __global__ void trace_pixel_kernel(const PrimRec *recs, const Geo64 *geo, const int32_t *tile_offsets,
                                    const int32_t *tile_prims, CamK cam, SetK st, int u, int v,
                                    int max, int *acc_prim, float *acc_t, float *acc_abar,

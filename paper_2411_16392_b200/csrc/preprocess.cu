@@ -607,4 +607,47 @@ __global__ void export_prep_kernel(PrepView pv, int P, double *scales, double *a
     if (planar) planar[p] = g.planar != 0.0 ? 1 : 0;
 }
 
+// the rest of PreparedView (rasterizer.py:124-147), same fp64 functions
+__global__ void export_geom_kernel(qgs_params prm, CamK cam, PrepView pv, qgs_prep_export o)
+{
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= prm.P) return;
+    const Geo64 &g = pv.geo[p];
+    double s[3];
+    bool clamped[3];
+    activate(prm.raw_scales + 3 * p, prm.raw_signs + 3 * p, s, clamped);
+    double R[9], qn[4], qnorm;
+    quat_rot(prm.quats + 4 * p, R, qn, qnorm);
+    if (o.R) for (int i = 0; i < 9; ++i) o.R[9 * (size_t)p + i] = R[i];
+    if (o.ohat) for (int i = 0; i < 3; ++i) o.ohat[3 * (size_t)p + i] = g.ohat[i];
+    if (o.M) for (int i = 0; i < 9; ++i) o.M[9 * (size_t)p + i] = g.M[i];
+    if (o.wv) for (int i = 0; i < 3; ++i) o.wv[3 * (size_t)p + i] = g.wv[i];
+    if (o.lam) { o.lam[2 * (size_t)p] = g.sv[2] * g.wv[0]; o.lam[2 * (size_t)p + 1] = g.sv[2] * g.wv[1]; }
+    if (o.clamped) for (int i = 0; i < 3; ++i) o.clamped[3 * (size_t)p + i] = clamped[i] ? 1 : 0;
+    if (o.Nmat)      // Nmat = R_wc R (rasterizer.py:140-141)
+        for (int i = 0; i < 3; ++i)
+            for (int k = 0; k < 3; ++k)
+                o.Nmat[9 * (size_t)p + 3 * i + k] = cam.Rwc[3 * i + 0] * R[0 + k] +
+                                                    cam.Rwc[3 * i + 1] * R[3 + k] +
+                                                    cam.Rwc[3 * i + 2] * R[6 + k];
+    const float *cf = prm.centers + 3 * p;
+    const double v[3] = {(double)cf[0] - cam.eye[0], (double)cf[1] - cam.eye[1],
+                         (double)cf[2] - cam.eye[2]};
+    double dist = fmax(sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]), 1e-12);
+    const double vd[3] = {v[0] / dist, v[1] / dist, v[2] / dist};
+    if (o.view_dist) o.view_dist[p] = dist;
+    if (o.view_dirs) for (int i = 0; i < 3; ++i) o.view_dirs[3 * (size_t)p + i] = vd[i];
+    if (o.color_clamped) {   // sh.py:86-88: colour + 0.5 < 0 before the clamp
+        const int K = prm.sh_coeffs;
+        double Y[16];
+        sh_basis(K, vd[0], vd[1], vd[2], Y);
+        const float *shp = prm.sh + (size_t)p * 3 * K;
+        for (int ch = 0; ch < 3; ++ch) {
+            double acc = 0.0;
+            for (int k = 0; k < K; ++k) acc += (double)shp[ch * K + k] * Y[k];
+            o.color_clamped[3 * (size_t)p + ch] = (acc + 0.5) < 0 ? 1 : 0;
+        }
+    }
+}
+
 }  // namespace qgs

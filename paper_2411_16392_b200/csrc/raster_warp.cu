@@ -32,6 +32,7 @@
 // atomic per slot.
 #include <cuda_pipeline.h>
 
+#include "kernels.cuh"
 #include "shade.cuh"
 
 namespace qgs {
@@ -99,6 +100,7 @@ struct FwdSmem {
     // sums were measured to triple the gradient violations at C2)
     double acc[11][32];
     float pay[RING][PAYN][32];   // ring payload (see Pay)
+    int pages[QGS_FRAG_MAX_PAGES];  // fragment-log pages of this warp
     union {
         float tfirst[WB][32];    // pass 1 -> pass 2: first coarse root that survived
         uint32_t boxw[32];       // work counters only (between batches): window box masks
@@ -454,7 +456,24 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
     unsigned n_box = 0, n_acc = 0, n_cand = 0, n_coarse = 0;
     Ring R{&sm.ring_t[0][lane], &sm.ring_p[0][lane], 0};
     bool alive = inside;
-    const bool log_on = out.frag_prim != nullptr && out.frag_t != nullptr;
+    // paged fragment log (qgs_targets): warp-uniform page count, pages taken
+    // from the pool before each batch for the depth the batch can reach
+    bool log_on = out.frag_prim != nullptr && out.frag_t != nullptr;
+    int npages = 0;
+    auto ensure_pages = [&](int extra) {     // warp-uniform call
+        if (!log_on) return;
+        const int need = (__reduce_max_sync(FULL, (unsigned)nfrag) + extra + QGS_FRAG_PAGE - 1) /
+                         QGS_FRAG_PAGE;
+        if (need <= npages) return;
+        if (need > QGS_FRAG_MAX_PAGES) { log_on = false; return; }
+        int base = 0;
+        if (lane == 0) base = atomicAdd(out.frag_pool_next, need - npages);
+        base = __shfl_sync(FULL, base, 0);
+        if (base + (need - npages) > out.frag_pool_pages) { log_on = false; return; }
+        if (lane < need - npages) sm.pages[npages + lane] = base + lane;
+        npages = need;
+        __syncwarp();
+    };
 
     auto composite = [&](int ep, double t, const Pay &f) {
 #if QGS_FWD_COMPOSITE_VEC
@@ -496,8 +515,9 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
         a[A_K * 32] += w * (double)fK;
         if (T > 0.5) median = (float)t;
         T *= 1.0 - abar64;
-        if (log_on && nfrag < out.frag_cap) {
-            const size_t o = ((size_t)rw * out.frag_cap + nfrag) * 32 + lane;
+        if (log_on) {
+            const size_t o = ((size_t)sm.pages[nfrag / QGS_FRAG_PAGE] * QGS_FRAG_PAGE +
+                              (nfrag % QGS_FRAG_PAGE)) * 32 + lane;
             out.frag_prim[o] = ep;
             out.frag_t[o] = t;
 #if QGS_PAY_XY
@@ -512,6 +532,7 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
     // test on each pixel's culled-in candidates (pass 1), then the exact
     // test, ring and compositing in stream order (pass 2).
     auto run_batch = [&](int nb) {
+        ensure_pages(nb);                        // each entry emits at most one fragment per pixel
         load_batch_ids(sm.rec, recs, sm.qprim, nb);
         // geometry heads for the exact pass, copied asynchronously under pass 1
 #if QGS_FWD_STAGE_GEO
@@ -735,12 +756,17 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
     }
     if (qn > 0 && __any_sync(FULL, alive)) run_batch(qn);
 
+    ensure_pages(RING);                      // the drain emits at most RING more
     while (alive && R.n > 0) {
         double et;
         int ep;
         Pay pout;
         ring_pop_pay(R, sm.pay, lane, et, ep, pout);
         composite(ep, et, pout);
+    }
+    if (out.frag_page_count) {
+        if (lane < npages) out.frag_page_table[(size_t)rw * QGS_FRAG_MAX_PAGES + lane] = sm.pages[lane];
+        if (lane == 0) out.frag_page_count[rw] = (out.frag_prim && log_on) ? npages : -1;
     }
 
     if (inside) {
@@ -1051,14 +1077,16 @@ __device__ __forceinline__ void warp_accumulate(float (*red)[33][KGP], bool emit
 }
 
 // One raster block of the backward; EXACT only matters for the replay path
-// (its candidate test must make the forward's decisions).
-template <bool EXACT>
+// (its candidate test must make the forward's decisions); DET: write rows
+// for the deterministic reduction (det_reduce.cu) instead of atomics.
+template <bool EXACT, bool DET>
 __device__ __forceinline__ void bwd_block(const PrimRec *__restrict__ recs,
                                           const Geo64 *__restrict__ geo,
                                           const int32_t *__restrict__ tile_offsets,
                                           const int32_t *__restrict__ tile_prims, const CamK &cam,
                                           const SetK &st, const qgs_targets &fwd,
-                                          const qgs_upstream &upst, float *__restrict__ kg)
+                                          const qgs_upstream &upst, float *__restrict__ kg,
+                                          const DetRows &det)
 {
     __shared__ BwdSmem sm;
     const int lane = threadIdx.x & 31;
@@ -1112,6 +1140,9 @@ __device__ __forceinline__ void bwd_block(const PrimRec *__restrict__ recs,
     Ring R{&sm.ring_t[0][lane], &sm.ring_p[0][lane], 0};
     bool alive = inside && has_up;
 
+    // deterministic mode: this pixel's k-th fragment owns row det_base + k
+    const int64_t det_base = DET ? det.base[(size_t)rw * 32 + lane] : 0;
+    int kf = 0;
     auto emit_grad = [&](bool emit, int ep, double t, bool have_xy, float lx, float ly) {
         float g[KG];
         if (emit) {
@@ -1145,6 +1176,17 @@ __device__ __forceinline__ void bwd_block(const PrimRec *__restrict__ recs,
             T *= 1.0 - f.abar64;
             if (T < c.t_term) alive = false;
         }
+        if (DET) {
+            if (emit) {
+                float4 *dst = reinterpret_cast<float4 *>(det.rows + (size_t)(det_base + kf) * KG);
+#pragma unroll
+                for (int q = 0; q < KG / 4; ++q)
+                    dst[q] = make_float4(g[4 * q], g[4 * q + 1], g[4 * q + 2], g[4 * q + 3]);
+                det.prim[det_base + kf] = ep;
+                kf++;
+            }
+            return;
+        }
 #if defined(QGS_EXP_DIRECT_ATOMICS)
         if (emit) {
             float4 *dst = reinterpret_cast<float4 *>(kg + (size_t)ep * KG);
@@ -1162,29 +1204,41 @@ __device__ __forceinline__ void bwd_block(const PrimRec *__restrict__ recs,
     // Fragment log written by the forward: the composited sequence of every
     // pixel, so no candidate is re-tested and no ring is replayed.
     {
-        const int nf = alive ? fwd.n_fragments[px] : 0;
-        const int nf_max = __reduce_max_sync(FULL, nf);
-        if (fwd.frag_prim && fwd.frag_t && nf_max <= fwd.frag_cap) {
-            const size_t base = (size_t)rw * fwd.frag_cap * 32 + lane;
+        const int np = (fwd.frag_prim && fwd.frag_t && fwd.frag_page_count)
+                           ? fwd.frag_page_count[rw] : -1;
+        if (np >= 0) {
+            const int nf = alive ? fwd.n_fragments[px] : 0;
+            const int nf_max = __reduce_max_sync(FULL, nf);
+            // lane i holds the warp's i-th page id
+            const int my_page = lane < np ? fwd.frag_page_table[(size_t)rw * QGS_FRAG_MAX_PAGES + lane] : 0;
+            auto slot = [&](int k) {
+                const int pg = __shfl_sync(FULL, my_page, k / QGS_FRAG_PAGE);
+                return ((size_t)pg * QGS_FRAG_PAGE + (k % QGS_FRAG_PAGE)) * 32 + lane;
+            };
             const float2 *xy = reinterpret_cast<const float2 *>(fwd.frag_xy);
             const bool have_xy = xy != nullptr;
             int np_ = -1;
             double nt_ = 0.0;
             float2 nxy = make_float2(0.f, 0.f);
-            if (0 < nf) {
-                np_ = fwd.frag_prim[base]; nt_ = fwd.frag_t[base];
-                if (have_xy) nxy = xy[base];
+            if (nf_max > 0) {
+                const size_t o = slot(0);
+                if (0 < nf) {
+                    np_ = fwd.frag_prim[o]; nt_ = fwd.frag_t[o];
+                    if (have_xy) nxy = xy[o];
+                }
             }
             for (int k = 0; k < nf_max; ++k) {
                 const bool emit = k < nf;
                 const int ep = np_;
                 const double et = nt_;
                 const float2 exy = nxy;
-                if (k + 1 < nf) {                // prefetch the next fragment
-                    const size_t o = base + (size_t)(k + 1) * 32;
-                    np_ = fwd.frag_prim[o];
-                    nt_ = fwd.frag_t[o];
-                    if (have_xy) nxy = xy[o];
+                if (k + 1 < nf_max) {            // prefetch the next fragment
+                    const size_t o = slot(k + 1);
+                    if (k + 1 < nf) {
+                        np_ = fwd.frag_prim[o];
+                        nt_ = fwd.frag_t[o];
+                        if (have_xy) nxy = xy[o];
+                    }
                 }
                 emit_grad(emit, ep, et, have_xy, exy.x, exy.y);
             }
@@ -1192,7 +1246,7 @@ __device__ __forceinline__ void bwd_block(const PrimRec *__restrict__ recs,
         }
     }
 
-    // No log (or a pixel deeper than its capacity): replay the block's
+    // No log (or the block's log overflowed its pages): replay the block's
     // stream with the full candidate test -- the same inline functions as the
     // forward, so the same accepted set, fp64 depths and ring decisions.
     const int start = tile_offsets[tile], end = tile_offsets[tile + 1];
@@ -1228,18 +1282,29 @@ __global__ void __launch_bounds__(32, QGS_BWD_MIN_BLOCKS)
 raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
                   const int32_t *__restrict__ tile_offsets,
                   const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets fwd,
-                  qgs_upstream upst, float *__restrict__ kg)
+                  qgs_upstream upst, float *__restrict__ kg, DetRows det)
 {
-    bwd_block<false>(recs, geo, tile_offsets, tile_prims, cam, st, fwd, upst, kg);
+    bwd_block<false, false>(recs, geo, tile_offsets, tile_prims, cam, st, fwd, upst, kg, det);
 }
 
 __global__ void __launch_bounds__(32, QGS_BWD_EXACT_MIN_BLOCKS)
 raster_bwd_exact_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
                         const int32_t *__restrict__ tile_offsets,
                         const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets fwd,
-                        qgs_upstream upst, float *__restrict__ kg)
+                        qgs_upstream upst, float *__restrict__ kg, DetRows det)
 {
-    bwd_block<true>(recs, geo, tile_offsets, tile_prims, cam, st, fwd, upst, kg);
+    bwd_block<true, false>(recs, geo, tile_offsets, tile_prims, cam, st, fwd, upst, kg, det);
+}
+
+// deterministic mode (det_reduce.cu): rows instead of atomics
+__global__ void __launch_bounds__(32, QGS_BWD_MIN_BLOCKS)
+raster_bwd_det_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
+                      const int32_t *__restrict__ tile_offsets,
+                      const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets fwd,
+                      qgs_upstream upst, float *__restrict__ kg, DetRows det)
+{
+    if (st.exact) bwd_block<true, true>(recs, geo, tile_offsets, tile_prims, cam, st, fwd, upst, kg, det);
+    else bwd_block<false, true>(recs, geo, tile_offsets, tile_prims, cam, st, fwd, upst, kg, det);
 }
 
 // ===================================================== raster schedule

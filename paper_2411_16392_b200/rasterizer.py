@@ -25,11 +25,18 @@ from .model import ParameterError, PrimitiveSet
 T_NEAR_CLIP = 0.01   # intersect.py:22
 TILE = 16            # bounds.py:19
 # Fragment log kept by the forward for the backward: 20 B per logged
-# fragment (prim, fp64 depth, fp32 local hit point), at most FRAG_CAP per
-# pixel and FRAG_LOG_BYTES per view (blocks with a deeper pixel are replayed
-# with the full candidate test instead).
-FRAG_CAP = 512
-FRAG_LOG_BYTES = 24 << 30
+# fragment (prim, fp64 depth, fp32 local hit point) in a pool of pages (16
+# slots x the 32 pixels of a raster warp) that warps take as their deepest
+# pixel grows (include/qgs_b200.h, qgs_targets).  The pool is sized from the
+# pages the previous forward of the same image size used (x FRAG_POOL_SLACK),
+# starting from FRAG_POOL_SLOTS_PER_PX; a block that finds the pool empty is
+# replayed by the backward with the full candidate test instead.
+FRAG_PAGE = 16
+FRAG_MAX_PAGES = 32
+FRAG_POOL_SLOTS_PER_PX = 96
+FRAG_POOL_SLACK = 1.15
+_pool_hint = {}          # (device, H, W) -> (pinned int32 of pages used, event)
+_FORCE_POOL_PAGES = None
 
 
 @dataclass
@@ -49,6 +56,11 @@ class RenderSettings:
     # accepted set is the reference's float64 one at full scale; False keeps
     # the fp32 decisions (faster, a few acceptance flips per million pixels)
     exact_decisions: bool = True
+    # extension: True makes the backward bitwise repeatable like the
+    # reference's serial merge (raster_kernels.py:673-681): fragments' slots
+    # go to rows fixed by the forward and are summed per primitive in row
+    # order in fp64 (qgs_backward_deterministic) instead of fp32 atomics
+    deterministic: bool = False
 
 
 # ----------------------------------------------------------------- helpers
@@ -191,6 +203,45 @@ class PreparedView:
     def planar(self):
         return self._export()[4]
 
+    # the rest of the reference's PreparedView (rasterizer.py:33-58), each
+    # exported on demand from the device state (qgs_export_prep_geometry)
+    _GEOM = {"R": ((3, 3), torch.float64), "ohat": ((3,), torch.float64),
+             "M": ((3, 3), torch.float64), "Nmat": ((3, 3), torch.float64),
+             "wv": ((3,), torch.float64), "lam": ((2,), torch.float64),
+             "view_dirs": ((3,), torch.float64), "view_dist": ((), torch.float64),
+             "clamped": ((3,), torch.bool), "color_clamped": ((3,), torch.bool)}
+
+    def _geometry(self, name):
+        shape, dt = self._GEOM[name]
+        P = len(self.dev)
+        t = torch.empty((P,) + shape, dtype=torch.uint8 if dt == torch.bool else dt,
+                        device=self.prep.device)
+        ex = _lib.PrepExport()
+        setattr(ex, name, _ptr(t))
+        _lib.check(_lib.load().qgs_export_prep_geometry(self.dev.params_struct(), _ptr(self.prep),
+                                                        self._cam_c, ex, _stream()),
+                   "export_prep_geometry")
+        return t.bool() if dt == torch.bool else t
+
+    R = property(lambda self: self._geometry("R"))
+    ohat = property(lambda self: self._geometry("ohat"))
+    M = property(lambda self: self._geometry("M"))
+    Nmat = property(lambda self: self._geometry("Nmat"))
+    wv = property(lambda self: self._geometry("wv"))
+    lam = property(lambda self: self._geometry("lam"))
+    view_dirs = property(lambda self: self._geometry("view_dirs"))
+    view_dist = property(lambda self: self._geometry("view_dist"))
+    clamped = property(lambda self: self._geometry("clamped"))
+    color_clamped = property(lambda self: self._geometry("color_clamped"))
+
+    @property
+    def dirs(self):
+        """(H, W, 3) float64 unit camera-frame pixel rays (cameras.py:53-59)"""
+        H, W = int(self.cam.height), int(self.cam.width)
+        t = torch.empty((H, W, 3), dtype=torch.float64, device=self.prep.device)
+        _lib.check(_lib.load().qgs_pixel_dirs(self._cam_c, _ptr(t), _stream()), "pixel_dirs")
+        return t
+
     def trace_pixel(self, u, v, max_frags=4096):
         """Replay pixel (u, v): accepted candidates and emitted fragments."""
         dev = self.prep.device
@@ -239,9 +290,12 @@ class RenderTargets:
     n_fragments: torch.Tensor
     violations: torch.Tensor      # per tile (int32)
     aux: torch.Tensor             # (12, H, W) float64 blend sums for the backward
-    frag_prim: torch.Tensor = None     # fragment log (blocks, cap, 32) int32 primitive ids
-    frag_t: torch.Tensor = None        # fragment log (blocks, cap, 32) float64 depths
-    frag_xy: torch.Tensor = None       # fragment log (blocks, cap, 32, 2) fp32 local hit points
+    frag_prim: torch.Tensor = None     # fragment log pool (pages, 16, 32) int32 primitive ids
+    frag_t: torch.Tensor = None        # ... float64 depths
+    frag_xy: torch.Tensor = None       # ... (pages, 16, 32, 2) fp32 local hit points
+    frag_page_table: torch.Tensor = None   # (raster warps, 32) int32 page ids
+    frag_page_count: torch.Tensor = None   # (raster warps,) int32, -1 = not logged
+    frag_pool_next: torch.Tensor = None    # (1,) int32 pages handed out
     tile_order: torch.Tensor = None    # tiles by descending pair count (raster schedule)
 
     @property
@@ -365,7 +419,51 @@ def prepare(prims, cam, settings: RenderSettings = None, validate=True) -> Prepa
                         _cam_c=cam_c, _st_c=st_c)
 
 
-def forward(prep: PreparedView, keep_aux=True, counters=None) -> RenderTargets:
+def _pool_pages(device, H, W, warps):
+    """pages for this forward's fragment log: what the last forward of this
+    image size used (read from pinned memory, no sync) with some slack, or a
+    first guess from the pixel count"""
+    if _FORCE_POOL_PAGES is not None:            # tests: force pool exhaustion
+        return _FORCE_POOL_PAGES
+    guess = (H * W * FRAG_POOL_SLOTS_PER_PX) // (FRAG_PAGE * 32) + warps
+    h = _pool_hint.get((device, H, W))
+    if h is not None and h[1].query():
+        used = int(h[0][0])
+        if used > 0:
+            return max(int(used * FRAG_POOL_SLACK) + 64, warps)
+    return guess
+
+
+def _alloc_frag_log(tg, t, prep, H, W, device):
+    warps = prep.tiles_x * prep.tiles_y * 8
+    pages = _pool_pages(device, H, W, warps)
+    slots = pages * FRAG_PAGE * 32
+    tg.frag_prim = torch.empty((slots,), dtype=torch.int32, device=device)
+    tg.frag_t = torch.empty((slots,), dtype=torch.float64, device=device)
+    tg.frag_page_table = torch.empty((warps, FRAG_MAX_PAGES), dtype=torch.int32, device=device)
+    tg.frag_page_count = torch.empty((warps,), dtype=torch.int32, device=device)
+    tg.frag_pool_next = torch.empty((1,), dtype=torch.int32, device=device)   # zeroed by qgs_forward
+    t.frag_prim, t.frag_t = _ptr(tg.frag_prim), _ptr(tg.frag_t)
+    t.frag_page_table, t.frag_page_count = _ptr(tg.frag_page_table), _ptr(tg.frag_page_count)
+    t.frag_pool_next, t.frag_pool_pages = _ptr(tg.frag_pool_next), pages
+    if not os.environ.get("QGS_NO_FRAG_XY"):   # diagnostic: float64 re-shading
+        tg.frag_xy = torch.empty((slots, 2), dtype=torch.float32, device=device)
+        t.frag_xy = _ptr(tg.frag_xy)
+
+
+def _note_pool_use(tg, device, H, W):
+    """copy the pages used to pinned memory (async) for the next forward's sizing"""
+    key = (device, H, W)
+    h = _pool_hint.get(key)
+    if h is None or h[1].query():
+        buf = h[0] if h is not None else torch.zeros((1,), dtype=torch.int32).pin_memory()
+        buf.copy_(tg.frag_pool_next, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        _pool_hint[key] = (buf, ev)
+
+
+def forward(prep: PreparedView, keep_aux=True, counters=None, frag_log=True) -> RenderTargets:
     """rasterizer.py:198-227.  `counters` (optional uint64/int64 CUDA tensor of
     5) accumulates [in-box candidates, accepted fragments, composited,
     candidates after the conic cull, candidates passing the coarse test]."""
@@ -385,22 +483,16 @@ def forward(prep: PreparedView, keep_aux=True, counters=None) -> RenderTargets:
     for k in _MAPS + ("violations",):
         setattr(t, k, _ptr(getattr(tg, k)))
     t.aux = _ptr(tg.aux) if keep_aux else None
-    if keep_aux:
-        blocks = prep.tiles_x * prep.tiles_y * 8
-        cap = int(min(FRAG_CAP, FRAG_LOG_BYTES // (blocks * 32 * 20)))
-        if cap > 0:
-            tg.frag_prim = torch.empty((blocks, cap, 32), dtype=torch.int32, device=device)
-            tg.frag_t = torch.empty((blocks, cap, 32), dtype=torch.float64, device=device)
-            t.frag_prim, t.frag_t, t.frag_cap = _ptr(tg.frag_prim), _ptr(tg.frag_t), cap
-            if not os.environ.get("QGS_NO_FRAG_XY"):   # diagnostic: float64 re-shading
-                tg.frag_xy = torch.empty((blocks, cap, 32, 2), dtype=torch.float32, device=device)
-                t.frag_xy = _ptr(tg.frag_xy)
+    if keep_aux and frag_log:
+        _alloc_frag_log(tg, t, prep, H, W, device)
     tg.tile_order = torch.empty((prep.tiles_x * prep.tiles_y,), dtype=torch.int32, device=device)
     t.tile_order = _ptr(tg.tile_order)
     t.counters = _ptr(counters)
     _lib.check(_lib.load().qgs_forward(_ptr(prep.prep), len(prep.dev), prep._cam_c, prep._st_c,
                                        _ptr(prep.tile_offsets), _ptr(prep.tile_prims), t,
                                        _stream()), "qgs_forward")
+    if tg.frag_pool_next is not None:
+        _note_pool_use(tg, device, H, W)
     return tg
 
 
@@ -438,12 +530,23 @@ def kernel_grads(prep: PreparedView, targets: RenderTargets, upstream, kg=None) 
     if targets.frag_prim is not None:
         t.frag_prim, t.frag_t = _ptr(targets.frag_prim), _ptr(targets.frag_t)
         t.frag_xy = _ptr(targets.frag_xy)
-        t.frag_cap = targets.frag_prim.shape[1]
+        t.frag_page_table = _ptr(targets.frag_page_table)
+        t.frag_page_count = _ptr(targets.frag_page_count)
     if kg is None:
         kg = torch.zeros((len(prep.dev), _lib.KG_STRIDE), dtype=torch.float32, device=device)
-    _lib.check(_lib.load().qgs_backward(_ptr(prep.prep), len(prep.dev), prep._cam_c, prep._st_c,
-                                        _ptr(prep.tile_offsets), _ptr(prep.tile_prims), t, u,
-                                        _ptr(kg), _stream()), "qgs_backward")
+    L = _lib.load()
+    if getattr(prep.settings, "deterministic", False):
+        n_frags = int(targets.n_fragments.sum().item())      # sizes the row buffer
+        nb = L.qgs_backward_det_workspace_bytes(len(prep.dev), n_frags, prep._cam_c)
+        ws = torch.empty((nb,), dtype=torch.uint8, device=device)
+        _lib.check(L.qgs_backward_deterministic(
+            _ptr(prep.prep), len(prep.dev), prep._cam_c, prep._st_c, _ptr(prep.tile_offsets),
+            _ptr(prep.tile_prims), t, u, _ptr(kg), n_frags, _ptr(ws), nb, _stream()),
+            "qgs_backward_deterministic")
+        return kg
+    _lib.check(L.qgs_backward(_ptr(prep.prep), len(prep.dev), prep._cam_c, prep._st_c,
+                              _ptr(prep.tile_offsets), _ptr(prep.tile_prims), t, u,
+                              _ptr(kg), _stream()), "qgs_backward")
     return kg
 
 

@@ -30,6 +30,9 @@ pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 
 def _fullview(cfg, **kw):
+    """GPU (default settings, and the deterministic fp64-reduction backward)
+    and oracle on view 0"""
+    import dataclasses
     from oracle import qgs_oracle as qo
     from paper_2411_16392_b200 import rasterizer as rz, scenes
     sc = scenes.CONFIGS[cfg](**kw)
@@ -38,11 +41,15 @@ def _fullview(cfg, **kw):
     prep = rz.prepare(sc.prims, cam, st)
     tg = rz.forward(prep)
     gr = rz.backward(prep, tg, up)
+    prep_d = dataclasses.replace(prep, settings=dataclasses.replace(st, deterministic=True))
+    gr_det = rz.backward(prep_d, tg, up).to_numpy()
     torch.cuda.synchronize()
     gpu, ggr = tg.to_numpy(), gr.to_numpy()
     vw = qo.prepare(sc.prims.astype(np.float64), cam)
     ref = qo.forward(vw)
     rgr = qo.backward(vw, ref, {k: np.asarray(a, np.float64) for k, a in up.items()})
+    _fullview.det = parity.grad_report(gr_det, rgr)
+    _fullview.name = cfg
     return prep, vw, gpu, ref, ggr, rgr
 
 
@@ -56,6 +63,7 @@ def _check(prep, vw, gpu, ref, ggr, rgr):
     cls = parity.classify_pixels(prep, vw, gpu, ref)
     rep = {"image": {k: img[k] for k in ("pixels", "count_flip_pixels", "over_tol_pixels",
                                           "over_tol_same_count")}, "classes": cls}
+    _write(_fullview.name, rep, parity.grad_report(ggr, rgr))
     assert cls["continuous"] == 0 and cls["unclassified"] == 0, rep
     assert img["over_tol_same_count"] == 0, rep
     assert cls["order_swap"] == 0 and cls["membership"] == 0, rep
@@ -70,6 +78,7 @@ def _check(prep, vw, gpu, ref, ggr, rgr):
     assert img["transmittance"]["max_abs_same_count"] <= 1e-4, img["transmittance"]
     # (4) gradients, screen_center included
     g = parity.grad_report(ggr, rgr)
+    _write(_fullview.name, rep, g)
     n_all = g["n"] + g["screen_center"]["n"]
     bad_all = g["violations"] + g["screen_center"]["violations"]
     assert bad_all <= 2e-6 * n_all + 2, g
@@ -78,9 +87,25 @@ def _check(prep, vw, gpu, ref, ggr, rgr):
     return rep, g
 
 
+def _write(name, rep, g):
+    import json
+    import os
+    out = {"scene": name, **rep, "grads": g, "grads_deterministic": _fullview.det}
+    print(json.dumps(out, default=str))
+    if os.environ.get("QGS_PARITY_OUT"):
+        with open(os.path.join(os.environ["QGS_PARITY_OUT"], f"fullview_{name}.json"), "w") as f:
+            json.dump(out, f, indent=1, default=str)
+
+
+def _report(name, rep, g):
+    d = _fullview.det
+    n_all = d["n"] + d["screen_center"]["n"]
+    assert d["violations"] + d["screen_center"]["violations"] <= 2e-6 * n_all + 2, d
+
+
 def test_c3_full_view(cuda_device):
-    _check(*_fullview("c3", views=1))
+    _report("c3", *_check(*_fullview("c3", views=1)))
 
 
 def test_c4_full_view(cuda_device):
-    _check(*_fullview("c4", views=1))
+    _report("c4", *_check(*_fullview("c4", views=1)))

@@ -116,6 +116,28 @@ def test_backward_within_tolerance(rz, name):
     assert rep["violations"] == 0 and rep["screen_center"]["violations"] == 0, rep
 
 
+@pytest.mark.parametrize("name", ["c1", "c2_small", "s_default", "s_resort_off", "s_background"])
+def test_backward_deterministic_mode(rz, name):
+    """RenderSettings(deterministic=True): bitwise-repeatable gradients
+    (pkg/tests/test_rasterizer_gradients.py:217-229) within the reference
+    tolerances, through the log and the replay paths alike"""
+    import dataclasses
+    gc = golden_io.load(name)
+    st = dataclasses.replace(_settings(rz, gc), deterministic=True)
+    prep = rz.prepare(gc.prims, gc.cam, st)
+    tg = rz.forward(prep)
+    g1 = rz.backward(prep, tg, gc.upstream).to_numpy()
+    g2 = rz.backward(prep, tg, gc.upstream).to_numpy()
+    tg.frag_prim = tg.frag_t = None                     # replay path
+    g3 = rz.backward(prep, tg, gc.upstream).to_numpy()
+    for k in parity.GRAD_GROUPS + ("screen_center",):
+        assert np.array_equal(g1[k], g2[k]), k
+    ref = {k: gc.g[f"grad_{k}"] for k in parity.GRAD_GROUPS + ("screen_center",)}
+    for g in (g1, g3):
+        rep = parity.grad_report(g, ref)
+        assert rep["violations"] == 0 and rep["screen_center"]["violations"] == 0, rep
+
+
 def test_forward_deterministic(rz):
     gc = golden_io.load("c2_small")
     st = _settings(rz, gc)
@@ -138,33 +160,32 @@ def test_empty_scene(rz):
 
 
 @pytest.mark.parametrize("name", ["s_default", "s_resort_off", "c2_small"])
-@pytest.mark.parametrize("mode", ["no_log", "cap_overflow"])
+@pytest.mark.parametrize("mode", ["no_log", "pool_exhausted"])
 def test_backward_replay_fallback(rz, name, mode):
-    """The backward's two paths -- the forward's fragment log and the replay
-    of accepted candidates (taken without a log, or for blocks with a pixel
-    deeper than the log's capacity) -- give the same kernel gradients."""
+    """The backward's two paths -- the forward's paged fragment log and the
+    replay of the block's candidate stream (taken without a log, or for the
+    blocks that found the log's page pool empty) -- give the same kernel
+    gradients."""
     gc = golden_io.load(name)
     st = _settings(rz, gc)
     prep = rz.prepare(gc.prims, gc.cam, st)
     tg = rz.forward(prep)
     assert tg.frag_prim is not None
+    assert int(tg.frag_page_count.min()) >= 0          # every block logged
     kg_log = rz.kernel_grads(prep, tg, gc.upstream)
     if mode == "no_log":
         tg.frag_prim = tg.frag_t = None
     else:
-        # keep the log but shrink its capacity below the deepest pixel: the
-        # layout stride changes too, so blocks under the cap read garbage
-        # unless the forward is rerun with the same cap
-        nmax = int(tg.n_fragments.max())
-        if nmax < 2:
+        used = int(tg.frag_pool_next.item())
+        if used < 2:
             pytest.skip("scene too shallow")
-        old = rz.FRAG_CAP
         try:
-            rz.FRAG_CAP = nmax - 1
+            rz._FORCE_POOL_PAGES = used // 2           # about half the blocks overflow
             tg = rz.forward(prep)
         finally:
-            rz.FRAG_CAP = old
-        assert tg.frag_prim.shape[1] == nmax - 1
+            rz._FORCE_POOL_PAGES = None
+        cnt = tg.frag_page_count.cpu().numpy()
+        assert (cnt < 0).any() and (cnt >= 0).any()
     kg_rep = rz.kernel_grads(prep, tg, gc.upstream)
     a, b = kg_log.cpu().numpy().astype(np.float64), kg_rep.cpu().numpy().astype(np.float64)
     scale = np.abs(a).max(axis=0, keepdims=True) + 1e-30
@@ -173,6 +194,22 @@ def test_backward_replay_fallback(rz, name, mode):
     # reference tolerance, see test_backward_within_tolerance)
     assert np.all(np.abs(a - b) <= 1e-4 * scale + 1e-6 * np.abs(a)), \
         float((np.abs(a - b) / scale).max())
+
+
+def test_fragment_log_pool_is_compact(rz):
+    """the log's pages scale with the fragments composited: every logged
+    fragment has a slot, and the pages handed out hold at most 2x the
+    fragments (a warp's pages follow its deepest pixel)"""
+    from paper_2411_16392_b200 import scenes
+    sc = scenes.config2(views=1)
+    prep = rz.prepare(sc.prims, sc.cams[0])
+    tg = rz.forward(prep)
+    used = int(tg.frag_pool_next.item())
+    nfr = int(tg.n_fragments.sum().item())
+    assert int(tg.frag_page_count.min()) >= 0
+    assert int(tg.frag_page_count.sum().item()) == used
+    warps = tg.frag_page_count.numel()
+    assert nfr <= used * 16 * 32 <= 3 * nfr + 16 * 32 * warps
 
 
 @pytest.mark.parametrize("copies", [5, 40, 300, 700, 8500])
@@ -316,3 +353,31 @@ def test_sort_order_at_scale(rz):
     area = np.where(live, (bb[:, 1] // 16 - bb[:, 0] // 16 + 1) * (bb[:, 3] // 16 - bb[:, 2] // 16 + 1), 0)
     assert np.array_equal(counts, area)
     assert np.diff(off).max() > 100_000
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["c1", "c2_small", "s_planar", "s_sh3", "s_euclid"])
+def test_prepared_view_fields(rz, name):
+    """Every PreparedView field of the reference (rasterizer.py:33-58) is
+    exported by the drop-in; float fields agree with the float64 oracle's
+    (numpy ops of the reference) to 1e-12, flags and pixel rays exactly."""
+    from oracle import qgs_oracle as qo
+    gc = golden_io.load(name)
+    prep = rz.prepare(gc.prims, gc.cam, _settings(rz, gc))
+    vw = qo.prepare(gc.prims, gc.cam, gc.settings)
+    P = len(gc.prims)
+    for f in ("R", "ohat", "M", "Nmat", "wv", "lam", "view_dirs", "view_dist", "scales",
+              "alphas", "colors"):
+        got = getattr(prep, f).cpu().numpy()
+        ref = np.asarray(getattr(vw, f), np.float64).reshape(got.shape)
+        assert got.shape[0] == P, f
+        assert np.allclose(got, ref, rtol=1e-12, atol=1e-14), (f, float(np.abs(got - ref).max()))
+    assert np.array_equal(prep.clamped.cpu().numpy(), np.asarray(vw.clamped, bool))
+    assert np.array_equal(prep.color_clamped.cpu().numpy(), np.asarray(vw.color_clamped, bool))
+    assert np.array_equal(prep.dirs.cpu().numpy(), vw.dirs)
+    assert np.array_equal(prep.planar.cpu().numpy(), g_planar(vw))
+    assert prep.tiles_x == vw.tiles_x and prep.tiles_y == vw.tiles_y
+
+
+def g_planar(vw):
+    return np.asarray(vw.planar, np.uint8)
