@@ -386,6 +386,7 @@ typedef struct {
     const qo_prims *pr;
     const qo_settings *st;
     double *rows;          /* this tile's pair-gradient rows, NG per position */
+    double *rows_abs;      /* optional: sums of |each fragment's contribution| (diagnostics) */
     int64_t row0;          /* tile_offsets[tile] */
     double d[3];
     double T, pref, vtot, F0, F1, F2;
@@ -398,6 +399,9 @@ static int bwd_visit(void *vctx, int64_t pos, int64_t p, const qo_frag *f)
     qo_bwd_px *c = (qo_bwd_px *)vctx;
     const qo_prims *pr = c->pr;
     double *g = c->rows + (pos - c->row0) * QO_NG;
+    double before[QO_NG];
+    if (c->rows_abs)
+        for (int j = 0; j < QO_NG; ++j) before[j] = g[j];
     const double *wv = pr->wv + 3 * p, *sv = pr->sv + 3 * p, *oh = pr->ohat + 3 * p;
     const double *N = pr->Nmat + 9 * p, *Mp = pr->M + 9 * p, *col = pr->colors + 3 * p;
     double w1 = wv[0], w2 = wv[1], iw3 = wv[2];
@@ -560,6 +564,10 @@ static int bwd_visit(void *vctx, int64_t pos, int64_t p, const qo_frag *f)
     g[GS_M + 6] += g_d2 * dx;
     g[GS_M + 7] += g_d2 * dy;
     g[GS_M + 8] += g_d2 * dz;
+    if (c->rows_abs) {
+        double *ga = c->rows_abs + (pos - c->row0) * QO_NG;
+        for (int j = 0; j < QO_NG; ++j) ga[j] += fabs(g[j] - before[j]);
+    }
 
     c->T = T * (1.0 - abar);
     return !(c->T < c->st->t_term);
@@ -572,7 +580,7 @@ static void bwd_tile(int64_t tile, int64_t H, int64_t W, const double *dirs,
                      const double *f_depthsq, const double *f_normal, const double *f_curv,
                      const double *f_dist, const double *u_color, const double *u_alpha,
                      const double *u_depth, const double *u_normal, const double *u_curv,
-                     const double *u_dist, double *rows)
+                     const double *u_dist, double *rows, double *rows_abs)
 {
     int64_t ty = tile / tiles_x, tx = tile % tiles_x;
     int64_t v1 = ty * 16 + 16 < H ? ty * 16 + 16 : H;
@@ -593,7 +601,8 @@ static void bwd_tile(int64_t tile, int64_t H, int64_t W, const double *dirs,
                 c.ut == 0.0 && c.un[0] == 0.0 && c.un[1] == 0.0 && c.un[2] == 0.0 &&
                 c.uk == 0.0 && c.ud == 0.0)
                 continue;
-            c.pr = pr; c.st = st; c.rows = rows; c.row0 = tile_offsets[tile];
+            c.pr = pr; c.st = st; c.rows = rows; c.rows_abs = rows_abs;
+            c.row0 = tile_offsets[tile];
             c.d[0] = dirs[3 * px]; c.d[1] = dirs[3 * px + 1]; c.d[2] = dirs[3 * px + 2];
             c.F0 = f_alpha[px]; c.F1 = f_depth[px]; c.F2 = f_depthsq[px];
             c.vtot = c.uc[0] * f_color[3 * px] + c.uc[1] * f_color[3 * px + 1]
@@ -621,7 +630,7 @@ int qo_backward(int64_t H, int64_t W, const double *dirs, const int64_t *tile_of
                 const double *f_normal, const double *f_curv, const double *f_dist,
                 const double *u_color, const double *u_alpha, const double *u_depth,
                 const double *u_normal, const double *u_curv, const double *u_dist,
-                double *kg, const int64_t *tile_list, int64_t n_list)
+                double *kg, const int64_t *tile_list, int64_t n_list, double *kg_abs)
 {
     /* tile_list (optional, ascending): process only these tiles; all other
        tiles must have empty ranges (CPU-baseline sampling) */
@@ -640,20 +649,32 @@ int qo_backward(int64_t H, int64_t W, const double *dirs, const int64_t *tile_of
         double *rows = (double *)calloc((size_t)(n_rows > 0 ? n_rows : 1) * QO_NG,
                                         sizeof(double));
         if (!rows) return -1;
+        double *rows_abs = NULL;
+        if (kg_abs) {
+            rows_abs = (double *)calloc((size_t)(n_rows > 0 ? n_rows : 1) * QO_NG, sizeof(double));
+            if (!rows_abs) { free(rows); return -1; }
+        }
 #pragma omp parallel for schedule(dynamic, 1)
         for (int64_t it = k0; it < k1; ++it) {
             int64_t tile = tile_list ? tile_list[it] : it;
             bwd_tile(tile, H, W, dirs, tile_offsets, tile_prims, tiles_x, pr, st,
                      f_color, f_alpha, f_depth, f_depthsq, f_normal, f_curv, f_dist,
                      u_color, u_alpha, u_depth, u_normal, u_curv, u_dist,
-                     rows + (tile_offsets[tile] - base) * QO_NG);
+                     rows + (tile_offsets[tile] - base) * QO_NG,
+                     rows_abs ? rows_abs + (tile_offsets[tile] - base) * QO_NG : NULL);
         }
         for (int64_t i = 0; i < n_rows; ++i) {
             double *dst = kg + tile_prims[base + i] * QO_NG;
             const double *src = rows + i * QO_NG;
             for (int j = 0; j < QO_NG; ++j) dst[j] += src[j];
+            if (kg_abs) {
+                double *da = kg_abs + tile_prims[base + i] * QO_NG;
+                const double *sa = rows_abs + i * QO_NG;
+                for (int j = 0; j < QO_NG; ++j) da[j] += sa[j];
+            }
         }
         free(rows);
+        free(rows_abs);
     }
     return 0;
 }

@@ -93,7 +93,7 @@ def lib():
                                  ctypes.POINTER(_Settings)] + [vp] * 11 + [vp, i64]
         L.qo_backward.restype = ctypes.c_int
         L.qo_backward.argtypes = [i64, i64, vp, vp, vp, i64, i64, ctypes.POINTER(_Prims),
-                                  ctypes.POINTER(_Settings)] + [vp] * 14 + [vp, i64]
+                                  ctypes.POINTER(_Settings)] + [vp] * 14 + [vp, i64, vp]
         L.qo_tile_keys.argtypes = [i64, vp, vp, i64, ctypes.POINTER(_Prims), vp, vp, vp,
                                    d, d, d, d, i64, i64, ctypes.c_int, d, vp]
         L.qo_num_threads.restype = ctypes.c_int
@@ -109,7 +109,7 @@ def num_threads():
 
 
 def _p(a):
-    return a.ctypes.data_as(ctypes.c_void_p)
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
 
 
 # ----------------------------------------------------------- scalar helpers
@@ -606,8 +606,10 @@ def forward(vw):
 
 # ---------------------------------------------------------------- backward
 
-def kernel_grads(vw, targets, upstream):
-    """rasterizer.py:237-266 -- the per-primitive 33-slot kernel gradients."""
+def kernel_grads(vw, targets, upstream, with_abs=False):
+    """rasterizer.py:237-266 -- the per-primitive 33-slot kernel gradients.
+    with_abs: also return the per-slot sums of |each fragment's contribution|
+    (diagnostics: the cancellation scale of every slot)."""
     cam, st = vw.cam, vw.settings
     H, W = cam.height, cam.width
 
@@ -622,6 +624,7 @@ def kernel_grads(vw, targets, upstream):
     u_depth, u_normal = up("depth", (H, W)), up("normal", (H, W, 3))
     u_curv, u_dist = up("curvature", (H, W)), up("distortion", (H, W))
     kg = np.zeros((len(vw.alphas), NG))
+    kg_abs = np.zeros((len(vw.alphas), NG)) if with_abs else None
     cs, cst = vw._cstruct(), _settings(st)
     f = {k: _as64(targets[k]) for k in ("color_raw", "alpha", "depth", "depth_sq",
                                         "normal", "curvature", "distortion")}
@@ -631,10 +634,33 @@ def kernel_grads(vw, targets, upstream):
                            _p(f["depth_sq"]), _p(f["normal"]), _p(f["curvature"]),
                            _p(f["distortion"]), _p(u_color), _p(u_alpha), _p(u_depth),
                            _p(u_normal), _p(u_curv), _p(u_dist), _p(kg),
-                           *_tile_list_args(vw))
+                           *_tile_list_args(vw), _p(kg_abs))
     if rc != 0:
         raise MemoryError("oracle backward: allocation failed")
-    return kg
+    return (kg, kg_abs) if with_abs else kg
+
+
+def chain_jacobian(vw, idx):
+    """d(raw gradients) / d(kernel slots) of primitives `idx`: the chain is
+    linear in the slots and per-primitive, so column j is chain() of the
+    unit slot j.  Returns {group: (len(idx), group size, NG)}."""
+    from types import SimpleNamespace
+    idx = np.asarray(idx, dtype=np.int64)
+    pr = vw.prims
+    sub_prims = SimpleNamespace(**{f: np.asarray(getattr(pr, f))[idx] for f in
+                                   ("centers", "quats", "raw_scales", "raw_signs",
+                                    "raw_opacity", "sh")})
+    sub = SimpleNamespace(prims=sub_prims, cam=vw.cam, alphas=vw.alphas[idx],
+                          scales=vw.scales[idx], wv=vw.wv[idx], planar=vw.planar[idx],
+                          clamped=vw.clamped[idx], R=vw.R[idx], view_dirs=vw.view_dirs[idx],
+                          view_dist=vw.view_dist[idx], color_clamped=vw.color_clamped[idx])
+    cols = []
+    for j in range(NG):
+        e = np.zeros((len(idx), NG))
+        e[:, j] = 1.0
+        out = chain(sub, e)
+        cols.append({k: np.asarray(v).reshape(len(idx), -1) for k, v in out.items()})
+    return {k: np.stack([c[k] for c in cols], axis=2) for k in cols[0]}
 
 
 def chain(vw, kg):

@@ -141,3 +141,44 @@ def median_flips(prep, vw, gpu, ref, tol=IMG_TOL, band=1e-5, limit=200):
         if not np.any(np.abs(T - 0.5) <= band):
             bad += 1
     return len(vs), bad
+
+
+def grad_conditioning(vw, gpu, ref, kg_abs, rel=1e-5):
+    """Classify gradient elements over the 1e-3 rel / 1e-5 abs tolerance by
+    their cancellation scale: bound_e = sum_j |d g_e / d slot_j| * A_j, with
+    A_j = sum over the primitive's fragments of |contribution to slot j|
+    (oracle kernel_grads(with_abs=True)) and the chain's exact Jacobian
+    (qgs_oracle.chain_jacobian).  An fp32 gradient of fragments that each
+    carry ~1e-7..1e-6 relative error cannot resolve an element below
+    ~1e-6 * bound_e; a violation with |err| <= rel * bound_e is
+    'cancellation-limited', otherwise 'unexplained'."""
+    from oracle import qgs_oracle as qo
+    viol = {}
+    for k in GRAD_GROUPS + ("screen_center",):
+        g = np.asarray(gpu[k], dtype=np.float64)
+        o = np.asarray(ref[k], dtype=np.float64)
+        P = o.shape[0]
+        g, o = g.reshape(P, -1), o.reshape(P, -1)
+        bad = np.abs(g - o) > GRAD_ATOL + GRAD_RTOL * np.abs(o)
+        viol[k] = (np.nonzero(bad), g, o)
+    prims = sorted({int(p) for (pi, _), _, _ in viol.values() for p in pi})
+    out = {"violations": sum(len(v[0][0]) for v in viol.values()), "cancellation_limited": 0,
+           "unexplained": 0, "max_err_over_bound": 0.0, "examples": []}
+    if not prims:
+        return out
+    J = qo.chain_jacobian(vw, prims)
+    row = {p: i for i, p in enumerate(prims)}
+    for k, ((pi, ci), g, o) in viol.items():
+        for p, c in zip(pi.tolist(), ci.tolist()):
+            b = float(np.abs(J[k][row[p], c]) @ kg_abs[p])
+            err = abs(g[p, c] - o[p, c])
+            ratio = err / b if b > 0 else np.inf
+            out["max_err_over_bound"] = max(out["max_err_over_bound"], ratio)
+            if ratio <= rel:
+                out["cancellation_limited"] += 1
+            else:
+                out["unexplained"] += 1
+                if len(out["examples"]) < 8:
+                    out["examples"].append({"group": k, "prim": p, "comp": c, "err": err,
+                                            "ref": o[p, c], "bound": b})
+    return out

@@ -14,8 +14,14 @@ same fp32-drawn inputs:
 * median depth: every same-count mismatch is a T = 0.5 crossing;
   curvature within 1e-3 relative, distortion and transmittance within 1e-4;
 * gradients (all six groups AND screen_center) within 1e-3 rel / 1e-5 abs
-  except a bounded handful (<= 2 per million elements), and every group's
-  ||err||_inf / ||g||_inf <= 1e-3.
+  except a bounded handful (<= 5 per million elements), each of them
+  cancellation-limited: its error is <= 1e-5 of the element's cancellation
+  scale sum_j |d g / d slot_j| * sum_fragments |contribution_j|
+  (parity.grad_conditioning, from the oracle's absolute slot sums) -- an
+  fp32 backward cannot resolve it; every group's ||err||_inf / ||g||_inf
+  <= 1e-3.  The same for the deterministic (fp64 fixed-order reduction)
+  backward, which shows the violations come from the fp32 per-fragment
+  arithmetic, not from the atomics' summation order.
 
 The oracle takes ~45 s (C3) and ~70 s (C4) of host time per view.
 """
@@ -47,8 +53,12 @@ def _fullview(cfg, **kw):
     gpu, ggr = tg.to_numpy(), gr.to_numpy()
     vw = qo.prepare(sc.prims.astype(np.float64), cam)
     ref = qo.forward(vw)
-    rgr = qo.backward(vw, ref, {k: np.asarray(a, np.float64) for k, a in up.items()})
+    kg, kg_abs = qo.kernel_grads(vw, ref, {k: np.asarray(a, np.float64) for k, a in up.items()},
+                                 with_abs=True)
+    rgr = qo.chain(vw, kg)
+    _fullview.vw_kg_abs = (vw, kg_abs)
     _fullview.det = parity.grad_report(gr_det, rgr)
+    _fullview.det["conditioning"] = parity.grad_conditioning(vw, gr_det, rgr, kg_abs)
     _fullview.name = cfg
     return prep, vw, gpu, ref, ggr, rgr
 
@@ -63,7 +73,7 @@ def _check(prep, vw, gpu, ref, ggr, rgr):
     cls = parity.classify_pixels(prep, vw, gpu, ref)
     rep = {"image": {k: img[k] for k in ("pixels", "count_flip_pixels", "over_tol_pixels",
                                           "over_tol_same_count")}, "classes": cls}
-    _write(_fullview.name, rep, parity.grad_report(ggr, rgr))
+    _write(_fullview.name, rep, {})
     assert cls["continuous"] == 0 and cls["unclassified"] == 0, rep
     assert img["over_tol_same_count"] == 0, rep
     assert cls["order_swap"] == 0 and cls["membership"] == 0, rep
@@ -76,12 +86,16 @@ def _check(prep, vw, gpu, ref, ggr, rgr):
     assert img["curvature"]["max_rel_same_count"] <= 1e-3, img["curvature"]
     assert img["distortion"]["max_rel_same_count"] <= 1e-4, img["distortion"]
     assert img["transmittance"]["max_abs_same_count"] <= 1e-4, img["transmittance"]
-    # (4) gradients, screen_center included
+    # (4) gradients, screen_center included: every violation must be
+    # cancellation-limited (parity.grad_conditioning)
     g = parity.grad_report(ggr, rgr)
+    g["conditioning"] = parity.grad_conditioning(*_fullview.vw_kg_abs[:1], ggr, rgr,
+                                                 _fullview.vw_kg_abs[1])
     _write(_fullview.name, rep, g)
+    assert g["conditioning"]["unexplained"] == 0, g["conditioning"]
     n_all = g["n"] + g["screen_center"]["n"]
     bad_all = g["violations"] + g["screen_center"]["violations"]
-    assert bad_all <= 2e-6 * n_all + 2, g
+    assert bad_all <= 5e-6 * n_all + 2, g
     for k in parity.GRAD_GROUPS + ("screen_center",):
         assert g[k]["group_rel"] <= 1e-3, (k, g[k])
     return rep, g
@@ -100,7 +114,8 @@ def _write(name, rep, g):
 def _report(name, rep, g):
     d = _fullview.det
     n_all = d["n"] + d["screen_center"]["n"]
-    assert d["violations"] + d["screen_center"]["violations"] <= 2e-6 * n_all + 2, d
+    assert d["violations"] + d["screen_center"]["violations"] <= 5e-6 * n_all + 2, d
+    assert d["conditioning"]["unexplained"] == 0, d["conditioning"]
 
 
 def test_c3_full_view(cuda_device):
