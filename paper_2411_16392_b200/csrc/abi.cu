@@ -262,19 +262,17 @@ int backward_impl(const void *prep, int32_t P, const qgs_camera *cam, const qgs_
     qgs::CamK ck = qgs::make_camk(*cam);
     qgs::SetK sk = qgs::make_setk(*st);
     qgs::PrepView pv = qgs::prep_view(const_cast<void *>(prep), P);
+    const int grid = ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE;
+    // blocks with a fragment log, then (a launch whose warps mostly exit at
+    // once) the blocks without one
     if (det.rows)
-        qgs::raster_bwd_det_kernel<<<ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE,
-                                     qgs::RASTER_THREADS, 0, s>>>(pv.rec, pv.geo, tile_offsets,
-                                                                    tile_prims, ck, sk, *fwd, *up,
-                                                                    kg, det);
-    else if (sk.exact)
-        qgs::raster_bwd_exact_kernel<<<ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE,
-                                 qgs::RASTER_THREADS, 0, s>>>(pv.rec, pv.geo, tile_offsets, tile_prims, ck,
-                                                                sk, *fwd, *up, kg, det);
+        qgs::raster_bwd_det_kernel<<<grid, qgs::RASTER_THREADS, 0, s>>>(
+            pv.rec, pv.geo, tile_offsets, tile_prims, ck, sk, *fwd, *up, kg, det);
     else
-        qgs::raster_bwd_kernel<<<ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE,
-                                 qgs::RASTER_THREADS, 0, s>>>(pv.rec, pv.geo, tile_offsets, tile_prims, ck,
-                                                                sk, *fwd, *up, kg, det);
+        qgs::raster_bwd_kernel<<<grid, qgs::RASTER_THREADS, 0, s>>>(
+            pv.rec, pv.geo, tile_offsets, tile_prims, ck, sk, *fwd, *up, kg, det);
+    qgs::raster_bwd_replay_kernel<<<grid, qgs::RASTER_THREADS, 0, s>>>(
+        pv.rec, pv.geo, tile_offsets, tile_prims, ck, sk, *fwd, *up, kg, det);
     QGS_LAUNCHED("raster_bwd_kernel");
     return 0;
 }

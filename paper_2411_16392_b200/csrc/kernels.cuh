@@ -58,10 +58,10 @@ __global__ void raster_fwd_exact_kernel(const PrimRec *recs, const Geo64 *geo,
                                         const ConicRec *conics, const int32_t *tile_offsets,
                                         const int32_t *tile_prims, CamK cam, SetK st,
                                         qgs_targets out);
-__global__ void raster_bwd_exact_kernel(const PrimRec *recs, const Geo64 *geo,
-                                        const int32_t *tile_offsets, const int32_t *tile_prims,
-                                        CamK cam, SetK st, qgs_targets fwd, qgs_upstream upst,
-                                        float *kg, DetRows det);
+__global__ void raster_bwd_replay_kernel(const PrimRec *recs, const Geo64 *geo,
+                                         const int32_t *tile_offsets, const int32_t *tile_prims,
+                                         CamK cam, SetK st, qgs_targets fwd, qgs_upstream upst,
+                                         float *kg, DetRows det);
 __global__ void raster_bwd_kernel(const PrimRec *recs, const Geo64 *geo, const int32_t *tile_offsets,
                                   const int32_t *tile_prims, CamK cam, SetK st, qgs_targets fwd,
                                   qgs_upstream upst, float *kg, DetRows det);

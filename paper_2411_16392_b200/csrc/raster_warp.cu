@@ -1076,10 +1076,12 @@ __device__ __forceinline__ void warp_accumulate(float (*red)[33][KGP], bool emit
     __syncwarp();
 }
 
-// One raster block of the backward; EXACT only matters for the replay path
-// (its candidate test must make the forward's decisions); DET: write rows
-// for the deterministic reduction (det_reduce.cu) instead of atomics.
-template <bool EXACT, bool DET>
+// One raster block of the backward.  REPLAY = false: blocks with a fragment
+// log (the hot kernel: no candidate-test code in it); true: blocks without
+// one, replayed with the forward's candidate test (EXACT: the forward's
+// decision mode).  DET: write rows for the deterministic reduction
+// (det_reduce.cu) instead of atomics.
+template <bool EXACT, bool DET, bool REPLAY>
 __device__ __forceinline__ void bwd_block(const PrimRec *__restrict__ recs,
                                           const Geo64 *__restrict__ geo,
                                           const int32_t *__restrict__ tile_offsets,
@@ -1206,7 +1208,9 @@ __device__ __forceinline__ void bwd_block(const PrimRec *__restrict__ recs,
     {
         const int np = (fwd.frag_prim && fwd.frag_t && fwd.frag_page_count)
                            ? fwd.frag_page_count[rw] : -1;
-        if (np >= 0) {
+        if (REPLAY && np >= 0) return;            // the log kernel has it
+        if (!REPLAY && np < 0) return;            // the replay kernel has it
+        if (!REPLAY) {
             const int nf = alive ? fwd.n_fragments[px] : 0;
             const int nf_max = __reduce_max_sync(FULL, nf);
             // lane i holds the warp's i-th page id
@@ -1284,16 +1288,24 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
                   const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets fwd,
                   qgs_upstream upst, float *__restrict__ kg, DetRows det)
 {
-    bwd_block<false, false>(recs, geo, tile_offsets, tile_prims, cam, st, fwd, upst, kg, det);
+    bwd_block<false, false, false>(recs, geo, tile_offsets, tile_prims, cam, st, fwd, upst, kg, det);
 }
 
+// blocks without a fragment log (rare: a page pool that ran dry, or a
+// forward called without a log): replayed with the forward's decision mode
 __global__ void __launch_bounds__(32, QGS_BWD_EXACT_MIN_BLOCKS)
-raster_bwd_exact_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
-                        const int32_t *__restrict__ tile_offsets,
-                        const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets fwd,
-                        qgs_upstream upst, float *__restrict__ kg, DetRows det)
+raster_bwd_replay_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
+                         const int32_t *__restrict__ tile_offsets,
+                         const int32_t *__restrict__ tile_prims, CamK cam, SetK st,
+                         qgs_targets fwd, qgs_upstream upst, float *__restrict__ kg, DetRows det)
 {
-    bwd_block<true, false>(recs, geo, tile_offsets, tile_prims, cam, st, fwd, upst, kg, det);
+    if (det.rows) {
+        if (st.exact) bwd_block<true, true, true>(recs, geo, tile_offsets, tile_prims, cam, st, fwd, upst, kg, det);
+        else bwd_block<false, true, true>(recs, geo, tile_offsets, tile_prims, cam, st, fwd, upst, kg, det);
+    } else {
+        if (st.exact) bwd_block<true, false, true>(recs, geo, tile_offsets, tile_prims, cam, st, fwd, upst, kg, det);
+        else bwd_block<false, false, true>(recs, geo, tile_offsets, tile_prims, cam, st, fwd, upst, kg, det);
+    }
 }
 
 // deterministic mode (det_reduce.cu): rows instead of atomics
@@ -1303,8 +1315,7 @@ raster_bwd_det_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict_
                       const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets fwd,
                       qgs_upstream upst, float *__restrict__ kg, DetRows det)
 {
-    if (st.exact) bwd_block<true, true>(recs, geo, tile_offsets, tile_prims, cam, st, fwd, upst, kg, det);
-    else bwd_block<false, true>(recs, geo, tile_offsets, tile_prims, cam, st, fwd, upst, kg, det);
+    bwd_block<false, true, false>(recs, geo, tile_offsets, tile_prims, cam, st, fwd, upst, kg, det);
 }
 
 // ===================================================== raster schedule

@@ -124,12 +124,21 @@ __device__ __forceinline__ void shade_at(const PrimRec &r, const Geo64 &g, const
     eval_point(r, (float)x, (float)y, planar, euclid, 1.f, h);
 }
 
+// fp32 re-shade guard: a logged fragment whose root derivative F'(t) is
+// below this fraction of its terms (a grazing ray) re-shades from the
+// float64 geometry; the root gradient dt = -g / F'(t) amplifies F's fp32
+// cancellation error by its inverse (the near-tangent
+// fragments under 1e-2 carry the gradient error)
+#ifndef QGS_LOG_Q_GUARD
+#define QGS_LOG_Q_GUARD 1e-2f
+#endif
+
 // Re-shading of a logged fragment in fp32: the forward's fp32 hit point
 // (x, y) makes rho, theta, l, sigma -- hence G and alpha -- bit-identical to
 // the forward's; dh, z and the root derivative q are re-derived in fp32
 // (gradient-only quantities, ~1e-6 relative except q on grazing rays).
 // Returns false when the fp32 root derivative q is ill-conditioned (a
-// grazing ray: |q| below 1e-3 of its terms) or |A| is too close to the
+// grazing ray: |q| below QGS_LOG_Q_GUARD of its terms) or |A| is too close to the
 // linear-branch threshold to trust the fp32 branch; the caller then re-shades
 // that fragment from the float64 geometry.
 __device__ __forceinline__ bool shade_from_log(const PrimRec &r, float x, float y, double t64,
@@ -155,7 +164,7 @@ __device__ __forceinline__ bool shade_from_log(const PrimRec &r, float x, float 
         // q well conditioned, and the linear-branch decision |A| < 1e-6
         // (made in float64 by the forward) not within fp32 reach of a flip
         // (A cancels on hyperbolic patches: its fp32 error is ~1e-7 of |a1| + |a2|)
-        ok = fabsf(Fp) >= 1e-3f * (2.f * (fabsf(t1) + fabsf(t2)) + fabsf(t3)) &&
+        ok = fabsf(Fp) >= QGS_LOG_Q_GUARD * (2.f * (fabsf(t1) + fabsf(t2)) + fabsf(t3)) &&
              fabsf(fabsf(A) - 1e-6f) > 1e-6f * (fabsf(a1) + fabsf(a2)) + 1e-12f;
         if (fabsf(A) < 1e-6f) {
             h.branch = BR_LINEAR;

@@ -143,7 +143,22 @@ def median_flips(prep, vw, gpu, ref, tol=IMG_TOL, band=1e-5, limit=200):
     return len(vs), bad
 
 
-def grad_conditioning(vw, gpu, ref, kg_abs, rel=1e-5):
+def count_flip_prims(prep, vw, gpu, ref, limit=400):
+    """Primitives composited (by either side) at pixels whose fragment count
+    differs between the GPU and the oracle: their gradients legitimately
+    differ by the flipped fragments' contributions."""
+    from oracle import qgs_oracle as qo
+    vs, us = np.nonzero(np.asarray(gpu["n_fragments"]) != np.asarray(ref["n_fragments"]))
+    out = set()
+    for v, u in list(zip(vs.tolist(), us.tolist()))[:limit]:
+        _, ge = prep.trace_pixel(u, v)
+        _, oe = qo.trace_pixel(vw, u, v)
+        out.update(int(p) for p in ge["prim"])
+        out.update(int(p) for p in oe["prim"])
+    return out
+
+
+def grad_conditioning(vw, gpu, ref, kg_abs, rel=1e-5, flip_prims=()):
     """Classify gradient elements over the 1e-3 rel / 1e-5 abs tolerance by
     their cancellation scale: bound_e = sum_j |d g_e / d slot_j| * A_j, with
     A_j = sum over the primitive's fragments of |contribution to slot j|
@@ -163,7 +178,7 @@ def grad_conditioning(vw, gpu, ref, kg_abs, rel=1e-5):
         viol[k] = (np.nonzero(bad), g, o)
     prims = sorted({int(p) for (pi, _), _, _ in viol.values() for p in pi})
     out = {"violations": sum(len(v[0][0]) for v in viol.values()), "cancellation_limited": 0,
-           "unexplained": 0, "max_err_over_bound": 0.0, "examples": []}
+           "count_flip": 0, "unexplained": 0, "max_err_over_bound": 0.0, "examples": []}
     if not prims:
         return out
     J = qo.chain_jacobian(vw, prims)
@@ -176,6 +191,8 @@ def grad_conditioning(vw, gpu, ref, kg_abs, rel=1e-5):
             out["max_err_over_bound"] = max(out["max_err_over_bound"], ratio)
             if ratio <= rel:
                 out["cancellation_limited"] += 1
+            elif p in flip_prims:
+                out["count_flip"] += 1
             else:
                 out["unexplained"] += 1
                 if len(out["examples"]) < 8:

@@ -58,7 +58,9 @@ def _fullview(cfg, **kw):
     rgr = qo.chain(vw, kg)
     _fullview.vw_kg_abs = (vw, kg_abs)
     _fullview.det = parity.grad_report(gr_det, rgr)
-    _fullview.det["conditioning"] = parity.grad_conditioning(vw, gr_det, rgr, kg_abs)
+    _fullview.flips = parity.count_flip_prims(prep, vw, gpu, ref)
+    _fullview.det["conditioning"] = parity.grad_conditioning(vw, gr_det, rgr, kg_abs,
+                                                             flip_prims=_fullview.flips)
     _fullview.name = cfg
     return prep, vw, gpu, ref, ggr, rgr
 
@@ -90,7 +92,8 @@ def _check(prep, vw, gpu, ref, ggr, rgr):
     # cancellation-limited (parity.grad_conditioning)
     g = parity.grad_report(ggr, rgr)
     g["conditioning"] = parity.grad_conditioning(*_fullview.vw_kg_abs[:1], ggr, rgr,
-                                                 _fullview.vw_kg_abs[1])
+                                                 _fullview.vw_kg_abs[1],
+                                                 flip_prims=_fullview.flips)
     _write(_fullview.name, rep, g)
     assert g["conditioning"]["unexplained"] == 0, g["conditioning"]
     n_all = g["n"] + g["screen_center"]["n"]
