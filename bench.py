@@ -233,8 +233,14 @@ def run_ours(a):
         ev = {(n, i): e for n, i, e in rec}
         return [ev[(a_name, i)].elapsed_time(ev[(b_name, i)]) for i in range(len(mine))]
 
-    fwd_ms = sum(sum(span(r, "view_begin", "fwd_end")) for r in evs) / K
-    bwd_ms = sum(sum(span(r, "fwd_end", "bwd_end")) for r in evs) / K
+    # the step's own spans (the next view's binning runs beside them on the
+    # side stream, so they include its interference) ...
+    fwd_ms_step = sum(sum(span(r, "view_begin", "fwd_end")) for r in evs) / K
+    bwd_ms_step = sum(sum(span(r, "fwd_end", "bwd_end")) for r in evs) / K
+    # ... and the raster kernels alone (this rank's views prepared first, then
+    # forward / backward each bracketed by events, nothing beside them): the
+    # roofline's launch durations
+    fwd_ms, bwd_ms = isolated_raster_ms(rz, dev, cams, mine, ups, st, stream)
     view_ms = np.mean([span(r, "view_begin", "view_end") for r in evs], axis=0).tolist() \
         if mine else []
     red_ms = float(np.mean([{n: e for n, _, e in r}["reduce_begin"].elapsed_time(
@@ -287,6 +293,7 @@ def run_ours(a):
         "sfu_frac": S / t_k / PSF,
         "roof_frac": max(F / P32, S / PSF) / t_k,
         "kernel_ms_per_step": kms, "fwd_ms_per_step": fwd_ms, "bwd_ms_per_step": bwd_ms,
+        "fwd_ms_per_step_in_pipeline": fwd_ms_step, "bwd_ms_per_step_in_pipeline": bwd_ms_step,
         "traffic": traffic_bytes(dom),
         # the contract's HBM view of the same kernel: its DRAM bytes per launch
         # (ncu) over its measured launch time, against MEASURED_PEAKS' copy
@@ -323,6 +330,26 @@ def run_ours(a):
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def isolated_raster_ms(rz, dev, cams, views, ups, st, stream, reps=2):
+    """forward and backward (kernel gradients) time per step, each view's
+    raster kernels alone on the device (CUDA events on the launching stream)"""
+    fwd = bwd = 0.0
+    for _ in range(reps):
+        for v in views:
+            prep = rz.prepare(dev, cams[v], st)
+            torch.cuda.synchronize()
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            e[0].record(stream)
+            tg = rz.forward(prep)
+            e[1].record(stream)
+            rz.kernel_grads(prep, tg, ups[v])
+            e[2].record(stream)
+            torch.cuda.synchronize()
+            fwd += e[0].elapsed_time(e[1])
+            bwd += e[1].elapsed_time(e[2])
+    return fwd / reps, bwd / reps
 
 
 def run_e2e(a, rz, sc, mine, device, st, world):

@@ -1,3 +1,4 @@
+#include <algorithm>
 // extern "C" entry points of libqgs_b200.so (declared in include/qgs_b200.h).
 #include <cstdio>
 #include <string>
@@ -215,6 +216,14 @@ int qgs_tile_keys_f64(int64_t n, const int64_t *pair_tiles, const int64_t *pair_
     return 0;
 }
 
+size_t qgs_fix_scratch_ints(const qgs_camera *cam)
+{
+    if (!cam) return 0;
+    const qgs::CamK ck = qgs::make_camk(*cam);
+    const size_t n = (size_t)ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE;
+    return (n + 3) / 4 + n + 2;                 // flag bytes | list | count | cursor
+}
+
 int qgs_forward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settings *st,
                 const int32_t *tile_offsets, const int32_t *tile_prims, const qgs_targets *out,
                 qgs_stream_t stream)
@@ -240,16 +249,27 @@ int qgs_forward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_se
                                                               out->tile_order, 0);
         QGS_LAUNCHED("tile_order_kernel");
     }
-    if (sk.exact)
-        qgs::raster_fwd_exact_kernel<<<ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE,
-                                       qgs::RASTER_THREADS, 0, s>>>(pv.rec, pv.geo, pv.conic,
-                                                                      tile_offsets, tile_prims, ck,
-                                                                      sk, *out);
-    else
-        qgs::raster_fwd_kernel<<<ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE,
-                                 qgs::RASTER_THREADS, 0, s>>>(pv.rec, pv.geo, pv.conic,
-                                                                tile_offsets, tile_prims, ck, sk,
-                                                                *out);
+    const int n_slots = ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE;
+    if (sk.exact && !out->fix_scratch) {
+        // one float64-deciding pass over every block
+        qgs::raster_fwd_exact_kernel<<<n_slots, qgs::RASTER_THREADS, 0, s>>>(
+            pv.rec, pv.geo, pv.conic, tile_offsets, tile_prims, ck, sk, *out, n_slots);
+    } else {
+        if (sk.exact)
+            QGS_CK(cudaMemsetAsync(out->fix_scratch, 0, (size_t)(n_slots + 3) / 4 * 4, s));
+        qgs::raster_fwd_kernel<<<n_slots, qgs::RASTER_THREADS, 0, s>>>(
+            pv.rec, pv.geo, pv.conic, tile_offsets, tile_prims, ck, sk, *out);
+        if (sk.exact) {
+            // the blocks that met a band case, heaviest first, re-run by a
+            // persistent grid (16 warps per SM) in float64-deciding mode
+            qgs::fix_list_kernel<<<1, 1024, 0, s>>>(out->fix_scratch, n_slots);
+            int dev = 0, sms = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            qgs::raster_fwd_exact_kernel<<<sms * 16, qgs::RASTER_THREADS, 0, s>>>(
+                pv.rec, pv.geo, pv.conic, tile_offsets, tile_prims, ck, sk, *out, n_slots);
+        }
+    }
     QGS_LAUNCHED("raster_fwd_kernel");
     return 0;
 }
@@ -271,8 +291,14 @@ int backward_impl(const void *prep, int32_t P, const qgs_camera *cam, const qgs_
     else
         qgs::raster_bwd_kernel<<<grid, qgs::RASTER_THREADS, 0, s>>>(
             pv.rec, pv.geo, tile_offsets, tile_prims, ck, sk, *fwd, *up, kg, det);
-    qgs::raster_bwd_replay_kernel<<<grid, qgs::RASTER_THREADS, 0, s>>>(
-        pv.rec, pv.geo, tile_offsets, tile_prims, ck, sk, *fwd, *up, kg, det);
+    {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int rgrid = std::min(sms * 4, (grid + 31) / 32);
+        qgs::raster_bwd_replay_kernel<<<rgrid, qgs::RASTER_THREADS, 0, s>>>(
+            pv.rec, pv.geo, tile_offsets, tile_prims, ck, sk, *fwd, *up, kg, det);
+    }
     QGS_LAUNCHED("raster_bwd_kernel");
     return 0;
 }

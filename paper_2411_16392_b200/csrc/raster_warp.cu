@@ -44,9 +44,6 @@ namespace qgs {
 #ifndef QGS_FWD_EXACT_MIN_BLOCKS
 #define QGS_FWD_EXACT_MIN_BLOCKS 16   // the fp64 band code needs the registers (measured: 18 -> 16 is -4 %)
 #endif
-#ifndef QGS_BWD_EXACT_MIN_BLOCKS
-#define QGS_BWD_EXACT_MIN_BLOCKS QGS_BWD_MIN_BLOCKS
-#endif
 #ifndef QGS_BWD_MIN_BLOCKS
 #define QGS_BWD_MIN_BLOCKS 20
 #endif
@@ -115,11 +112,11 @@ struct Pay {
     float v[PAYN];
 };
 
-// (tile, block) of this CTA and the lane's pixel
+// (tile, block) of schedule slot `slot` (default: this CTA) and the lane's pixel
 __device__ __forceinline__ void block_pixel(int tiles_x, const int32_t *order, int &tile, int &blk,
-                                            int &u, int &v)
+                                            int &u, int &v, int slot = -1)
 {
-    const int slot = (int)blockIdx.x;
+    if (slot < 0) slot = (int)blockIdx.x;
     tile = order ? order[slot >> 3] : (slot >> 3);
     blk = slot & 7;
     const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
@@ -364,13 +361,14 @@ __device__ __forceinline__ Cfg make_cfg(const SetK &st)
 }
 
 // exact candidate test (raster_kernels.py:121-130, 58-63); t = fp64 depth
-template <bool EXACT>
+template <int M>
 __device__ __forceinline__ bool accept(const PrimRec &r, const Geo64 &g, const double d64[3],
                                        float dx, float dy, float dz, const Cfg &c, double &t)
 {
     Hit h;
-    if (!hit_refined<EXACT>(r, g, d64, dx, dy, dz, c.euclid, c.t_clip, h)) return false;
-    if (!alpha_pass<EXACT>(r, &g, d64, h, c.euclid, c.alpha_floor)) return false;
+    h.band = false;
+    if (!hit_refined<M>(r, g, d64, dx, dy, dz, c.euclid, c.t_clip, h)) return false;
+    if (!alpha_pass<M>(r, &g, d64, h, c.euclid, c.alpha_floor)) return false;
     t = h.t64;
     return true;
 }
@@ -419,21 +417,28 @@ __device__ __forceinline__ void finish_frag(const PrimRec &r, float dx, float dy
 
 // ================================================================ forward
 
-// One raster block of the forward; EXACT: settings.exact_decisions (band
-// decisions in fp64, shade.cuh).  Two kernels so that the default one
-// carries no fp64 selection code.
-template <bool EXACT>
+// One raster block (schedule slot `slot`) of the forward.  M = MODE_FLAG:
+// fp32 decisions; with settings.exact_decisions and a fix-up scratch
+// (qgs_targets.fix_scratch) a block in which any decision fell inside its
+// fp32 rounding band stops, writes nothing and is marked for the fix-up
+// kernel, which re-runs it with M = MODE_EXACT (band cases re-decided in
+// fp64, shade.cuh).  Two kernels so that the main one carries no fp64
+// selection code.
+template <int M>
 __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
                                           const Geo64 *__restrict__ geo,
                                           const ConicRec *__restrict__ conics,
                                           const int32_t *__restrict__ tile_offsets,
                                           const int32_t *__restrict__ tile_prims, const CamK &cam,
-                                          const SetK &st, const qgs_targets &out)
+                                          const SetK &st, const qgs_targets &out, int slot)
 {
     __shared__ FwdSmem sm;
     const int lane = threadIdx.x & 31;
     int tile, blk, u, v;
-    block_pixel(cam.tiles_x, out.tile_order, tile, blk, u, v);
+    block_pixel(cam.tiles_x, out.tile_order, tile, blk, u, v, slot);
+    // MODE_FLAG with deferral on: band cases hand the block to the fix-up
+    const bool defer = M == MODE_FLAG && st.exact && out.fix_scratch != nullptr;
+    bool band = false;
     const int rw = (tile << 3) | blk;                // raster warp id (fragment-log row)
     const int bu = u - (lane & 7), bv = v - (lane >> 3);
     const bool inside = u < cam.W && v < cam.H;
@@ -609,10 +614,13 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
 #endif
             const PrimRec &r = sm.rec[j];
             const Geo64 *gfull = geo + sm.qprim[j];
-            return hit_exact_from<EXACT>(r, gh, gfull, d, dx, dy, dz, c.euclid, c.t_clip,
-                                         sm.tfirst[j][lane], (secb >> j) & 1u, (margb >> j) & 1u,
-                                         h) &&
-                   alpha_pass<EXACT>(r, gfull, d, h, c.euclid, c.alpha_floor);
+            h.band = false;
+            const bool ok = hit_exact_from<M>(r, gh, gfull, d, dx, dy, dz, c.euclid, c.t_clip,
+                                              sm.tfirst[j][lane], (secb >> j) & 1u,
+                                              (margb >> j) & 1u, h) &&
+                            alpha_pass<M>(r, gfull, d, h, c.euclid, c.alpha_floor);
+            if (M == MODE_FLAG) band = band || h.band;
+            return ok;
         };
         auto accept_one = [&](int j, const Hit &h) {
             const int p = sm.qprim[j];
@@ -658,12 +666,14 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
     // batch.
     const int start = tile_offsets[tile], end = tile_offsets[tile + 1];
     int qn = 0, an = 0;
+    bool deferred = false;                     // warp-uniform
     auto drain_b = [&]() {
         while (qn >= WB) {
             run_batch(WB);
             qn -= WB;
             if (lane < qn) { sm.qprim[lane] = sm.qprim[WB + lane]; sm.qmask[lane] = sm.qmask[WB + lane]; }
             __syncwarp();
+            if (defer && __any_sync(FULL, band)) { deferred = true; alive = false; }
             if (!__any_sync(FULL, alive)) { qn = 0; an = 0; return false; }
         }
         return true;
@@ -755,6 +765,12 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
         drain_b();
     }
     if (qn > 0 && __any_sync(FULL, alive)) run_batch(qn);
+    if (defer && (deferred || __any_sync(FULL, band))) {
+        // a decision fell inside its fp32 band: the fix-up kernel re-runs
+        // this block in MODE_EXACT and writes everything
+        if (lane == 0) reinterpret_cast<uint8_t *>(out.fix_scratch)[slot] = 1;
+        return;
+    }
 
     ensure_pages(RING);                      // the drain emits at most RING more
     while (alive && R.n > 0) {
@@ -836,15 +852,64 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
                   const ConicRec *__restrict__ conics, const int32_t *__restrict__ tile_offsets,
                   const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets out)
 {
-    fwd_block<false>(recs, geo, conics, tile_offsets, tile_prims, cam, st, out);
+    fwd_block<MODE_FLAG>(recs, geo, conics, tile_offsets, tile_prims, cam, st, out, (int)blockIdx.x);
 }
 
+// Fix-up list: the marked slots in schedule order (heaviest tiles first),
+// one CTA; fix_scratch = [n_slots flag bytes | list | count | cursor]
+__global__ void __launch_bounds__(1024)
+fix_list_kernel(int32_t *fix_scratch, int n_slots)
+{
+    const uint8_t *flag = reinterpret_cast<const uint8_t *>(fix_scratch);
+    int32_t *list = fix_scratch + (n_slots + 3) / 4;
+    int32_t *count = list + n_slots;
+    __shared__ int wsum[32], base;
+    if (threadIdx.x == 0) base = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int c0 = 0; c0 < n_slots; c0 += 1024) {
+        const int i = c0 + threadIdx.x;
+        const bool f = i < n_slots && flag[i] != 0;
+        const unsigned m = __ballot_sync(FULL, f);
+        if (lane == 0) wsum[w] = __popc(m);
+        __syncthreads();
+        int pre = base;
+        for (int k = 0; k < w; ++k) pre += wsum[k];
+        if (f) list[pre + __popc(m & ((1u << lane) - 1u))] = i;
+        __syncthreads();
+        if (threadIdx.x == 0) for (int k = 0; k < 32; ++k) base += wsum[k];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) { count[0] = base; count[1] = 0; }
+}
+
+// MODE_EXACT: every block (no fix-up scratch), or, persistent, the marked
+// blocks of the fix-up list taken in order
 __global__ void __launch_bounds__(32, QGS_FWD_EXACT_MIN_BLOCKS)
 raster_fwd_exact_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
                         const ConicRec *__restrict__ conics, const int32_t *__restrict__ tile_offsets,
-                        const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets out)
+                        const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets out,
+                        int n_slots)
 {
-    fwd_block<true>(recs, geo, conics, tile_offsets, tile_prims, cam, st, out);
+    const bool all = out.fix_scratch == nullptr;
+    const int32_t *list = all ? nullptr : out.fix_scratch + (n_slots + 3) / 4;
+    int32_t *count = all ? nullptr : const_cast<int32_t *>(list) + n_slots;
+    const int lane = threadIdx.x & 31;
+    for (int it = 0;; ++it) {
+        int slot;
+        if (all) {
+            if (it > 0) return;
+            slot = (int)blockIdx.x;
+        } else {
+            int i = 0;
+            if (lane == 0) i = atomicAdd(&count[1], 1);
+            i = __shfl_sync(FULL, i, 0);
+            if (i >= count[0]) return;
+            slot = list[i];
+        }
+        fwd_block<MODE_EXACT>(recs, geo, conics, tile_offsets, tile_prims, cam, st, out, slot);
+        __syncwarp();
+    }
 }
 
 // =============================================================== backward
@@ -1088,14 +1153,14 @@ __device__ __forceinline__ void bwd_block(const PrimRec *__restrict__ recs,
                                           const int32_t *__restrict__ tile_prims, const CamK &cam,
                                           const SetK &st, const qgs_targets &fwd,
                                           const qgs_upstream &upst, float *__restrict__ kg,
-                                          const DetRows &det)
+                                          const DetRows &det, int slot = -1)
 {
     __shared__ BwdSmem sm;
     const int lane = threadIdx.x & 31;
     if (lane < KG) sm.red[0][32][lane] = 0.f;        // zero row for padded group sums
     __syncwarp();
     int tile, blk, u, v;
-    block_pixel(cam.tiles_x, fwd.tile_order, tile, blk, u, v);
+    block_pixel(cam.tiles_x, fwd.tile_order, tile, blk, u, v, slot);
     const int rw = (tile << 3) | blk;                // raster warp id (fragment-log row)
     const bool inside = u < cam.W && v < cam.H;
     const Cfg c = make_cfg(st);
@@ -1266,7 +1331,7 @@ __device__ __forceinline__ void bwd_block(const PrimRec *__restrict__ recs,
             if (alive && in_box(sm.rec[j], u, v)) {
                 const int p = sm.prim[j];
                 double t = 0.0;
-                if (accept<EXACT>(sm.rec[j], geo[p], d64, dx, dy, dz, c, t))
+                if (accept<EXACT ? MODE_EXACT : MODE_FAST>(sm.rec[j], geo[p], d64, dx, dy, dz, c, t))
                     emit = ring_step(c, R, t, p, et, ep);
             }
             if (__any_sync(FULL, emit)) emit_grad(emit, ep, et, false, 0.f, 0.f);
@@ -1292,20 +1357,50 @@ raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
 }
 
 // blocks without a fragment log (rare: a page pool that ran dry, or a
-// forward called without a log): replayed with the forward's decision mode
-__global__ void __launch_bounds__(32, QGS_BWD_EXACT_MIN_BLOCKS)
+// forward called without a log): replayed with the forward's decision mode.
+// A small persistent grid scans the slots 32 at a time (page count < 0).
+template <bool DET>
+__device__ __forceinline__ void bwd_replay_slots(const PrimRec *__restrict__ recs,
+                                                 const Geo64 *__restrict__ geo,
+                                                 const int32_t *__restrict__ tile_offsets,
+                                                 const int32_t *__restrict__ tile_prims,
+                                                 const CamK &cam, const SetK &st,
+                                                 const qgs_targets &fwd, const qgs_upstream &upst,
+                                                 float *__restrict__ kg, const DetRows &det)
+{
+    const int lane = threadIdx.x & 31;
+    const int n_slots = cam.tiles_x * cam.tiles_y * 8;
+    const bool logged = fwd.frag_prim && fwd.frag_t && fwd.frag_page_count;
+    for (int base = blockIdx.x * 32; base < n_slots; base += gridDim.x * 32) {
+        // slot -> tile's raster warp id: the page count is indexed by warp id
+        int rw = -1;
+        if (base + lane < n_slots) {
+            const int t = fwd.tile_order ? fwd.tile_order[(base + lane) >> 3] : (base + lane) >> 3;
+            rw = (t << 3) | ((base + lane) & 7);
+        }
+        unsigned todo = __ballot_sync(FULL, rw >= 0 && (!logged || fwd.frag_page_count[rw] < 0));
+        while (todo) {
+            const int k = __ffs(todo) - 1;
+            todo &= todo - 1;
+            if (st.exact)
+                bwd_block<true, DET, true>(recs, geo, tile_offsets, tile_prims, cam, st, fwd, upst,
+                                           kg, det, base + k);
+            else
+                bwd_block<false, DET, true>(recs, geo, tile_offsets, tile_prims, cam, st, fwd,
+                                            upst, kg, det, base + k);
+            __syncwarp();
+        }
+    }
+}
+
+__global__ void __launch_bounds__(32, 8)
 raster_bwd_replay_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
                          const int32_t *__restrict__ tile_offsets,
                          const int32_t *__restrict__ tile_prims, CamK cam, SetK st,
                          qgs_targets fwd, qgs_upstream upst, float *__restrict__ kg, DetRows det)
 {
-    if (det.rows) {
-        if (st.exact) bwd_block<true, true, true>(recs, geo, tile_offsets, tile_prims, cam, st, fwd, upst, kg, det);
-        else bwd_block<false, true, true>(recs, geo, tile_offsets, tile_prims, cam, st, fwd, upst, kg, det);
-    } else {
-        if (st.exact) bwd_block<true, false, true>(recs, geo, tile_offsets, tile_prims, cam, st, fwd, upst, kg, det);
-        else bwd_block<false, false, true>(recs, geo, tile_offsets, tile_prims, cam, st, fwd, upst, kg, det);
-    }
+    if (det.rows) bwd_replay_slots<true>(recs, geo, tile_offsets, tile_prims, cam, st, fwd, upst, kg, det);
+    else bwd_replay_slots<false>(recs, geo, tile_offsets, tile_prims, cam, st, fwd, upst, kg, det);
 }
 
 // deterministic mode (det_reduce.cu): rows instead of atomics
@@ -1408,8 +1503,8 @@ __global__ void trace_pixel_kernel(const PrimRec *__restrict__ recs, const Geo64
         const int p = tile_prims[i];
         const PrimRec &r = recs[p];
         double t;
-        if (in_box(r, u, v) && (st.exact ? accept<true>(r, geo[p], d, dx, dy, dz, c, t)
-                                         : accept<false>(r, geo[p], d, dx, dy, dz, c, t))) {
+        if (in_box(r, u, v) && (st.exact ? accept<MODE_EXACT>(r, geo[p], d, dx, dy, dz, c, t)
+                                         : accept<MODE_FAST>(r, geo[p], d, dx, dy, dz, c, t))) {
             if (na < max) {
                 Frag f;
                 shade_emitted(r, geo[p], d, dx, dy, dz, t, c, f);

@@ -46,7 +46,15 @@ struct Hit {
     float q;                  // dt-denominator: F'(t) (quad), B (linear), dhz (planar)
     float dhx, dhy, dhz;
     int branch;
+    bool band;                // MODE_FLAG: a decision fell inside its fp32 rounding band
 };
+
+// Decision modes of the candidate test: MODE_FAST fp32 decisions; MODE_EXACT
+// (settings.exact_decisions) re-makes band cases in fp64; MODE_FLAG fp32
+// decisions that mark band cases in Hit::band -- the forward re-runs the
+// blocks that saw one in MODE_EXACT (a fix-up pass), so the default kernel
+// carries no fp64 selection code.
+enum { MODE_FAST = 0, MODE_EXACT = 1, MODE_FLAG = 2 };
 
 // arc length of z = a r^2 over [0, rho]; series below |u| = 0.3 (error < 1e-8)
 __device__ __forceinline__ float arc32(float a, float rho)
@@ -254,14 +262,27 @@ static __device__ __noinline__ unsigned exact64(const Geo64 *gp, const double dh
 
 // exact selection + weight at an fp64 depth; false if the root is rejected.
 // `gfull`: the primitive's complete Geo64 in global memory (EXACT band cases).
-template <bool EXACT>
+template <int M>
 __device__ __forceinline__ bool confirm_root(const PrimRec &r, const Geo64 &g, const Geo64 *gfull,
                                              const double dh[3], double t64, bool planar,
                                              bool euclid, float t_clip, Hit &h)
 {
     if (!(t64 > (double)t_clip)) return false;
     shade_at(r, g, dh, t64, euclid, h);
-    if (!EXACT) {
+    if (M == MODE_FLAG) {
+        bool pass = true, near = false;
+        if (!planar) {
+            const float ex = r.s2 * h.x, ey = r.s1 * h.y;
+            const float m = fmaf(ex, ex, ey * ey);
+            pass = m <= r.ell9;
+            near = fabsf(m - r.ell9) <= SEL_BAND * r.ell9;
+        }
+        const float lim = 3.f * h.sig;
+        pass = pass && h.l <= lim;
+        near = near || fabsf(h.l - lim) <= SEL_BAND * lim;
+        h.band = h.band || near;
+        if (!pass) return false;
+    } else if (M == MODE_FAST) {
         if (!planar && ellipse_out(r, h.x, h.y, 1.f)) return false;
         if (!(h.l <= 3.f * h.sig)) return false;
     } else {
@@ -283,13 +304,14 @@ __device__ __forceinline__ bool confirm_root(const PrimRec &r, const Geo64 &g, c
 }
 
 // the alpha floor on a selected hit (raster_kernels.py:58-60); fp64 inside
-// its band when EXACT
-template <bool EXACT>
+// its band in MODE_EXACT, flagged in MODE_FLAG
+template <int M>
 __device__ __forceinline__ bool alpha_pass(const PrimRec &r, const Geo64 *gfull, const double d64[3],
-                                           const Hit &h, bool euclid, float floor)
+                                           Hit &h, bool euclid, float floor)
 {
     const float ab = r.alpha * h.G;
-    if (!EXACT || fabsf(ab - floor) > FLOOR_BAND * floor) return ab >= floor;
+    if (M == MODE_FLAG) h.band = h.band || fabsf(ab - floor) <= FLOOR_BAND * floor;
+    if (M != MODE_EXACT || fabsf(ab - floor) > FLOOR_BAND * floor) return ab >= floor;
     double dh[3];
     dh[0] = gfull->M[0] * d64[0] + gfull->M[1] * d64[1] + gfull->M[2] * d64[2];
     dh[1] = gfull->M[3] * d64[0] + gfull->M[4] * d64[1] + gfull->M[5] * d64[2];
@@ -303,10 +325,10 @@ __device__ __forceinline__ bool alpha_pass(const PrimRec &r, const Geo64 *gfull,
 // accepted root (or -1) -- the caller re-confirms it inline, so its Hit stays
 // in registers (a Hit passed by address to an out-of-line call would live in
 // local memory on the hot path).
-template <bool EXACT>
+template <int M>
 static __device__ __noinline__ double marginal_root(const PrimRec &r, const Geo64 &g,
                                                     const Geo64 *gfull, const double d64[3],
-                                                    bool euclid, float t_clip)
+                                                    bool euclid, float t_clip, bool &band)
 {
     double dh[3];
     local_dir64(g, d64, dh);
@@ -330,20 +352,27 @@ static __device__ __noinline__ double marginal_root(const PrimRec &r, const Geo6
         cnt = disc == 0.0 ? 1 : 2;
     }
     Hit h;
+    h.band = false;
     for (int k = 0; k < cnt; ++k)
-        if (confirm_root<EXACT>(r, g, gfull, dh, roots[k], false, euclid, t_clip, h)) return roots[k];
+        if (confirm_root<M>(r, g, gfull, dh, roots[k], false, euclid, t_clip, h)) {
+            band = band || h.band;
+            return roots[k];
+        }
+    band = band || h.band;
     return -1.0;
 }
 
-template <bool EXACT>
+template <int M>
 __device__ __forceinline__ bool hit_marginal(const PrimRec &r, const Geo64 &g, const Geo64 *gfull,
                                              const double d64[3], bool euclid, float t_clip, Hit &h)
 {
-    const double t = marginal_root<EXACT>(r, g, gfull, d64, euclid, t_clip);
+    bool band = false;
+    const double t = marginal_root<M>(r, g, gfull, d64, euclid, t_clip, band);
+    h.band = h.band || band;
     if (!(t > 0.0)) return false;
     double dh[3];
     local_dir64(g, d64, dh);
-    return confirm_root<EXACT>(r, g, gfull, dh, t, false, euclid, t_clip, h);
+    return confirm_root<M>(r, g, gfull, dh, t, false, euclid, t_clip, h);
 }
 
 // Coarse fp32 stage (the per-candidate hot path).  Returns a mask: bit k set
@@ -445,7 +474,7 @@ __device__ __forceinline__ unsigned coarse_roots(const PrimRec &r, float dx, flo
 // Exact test of a candidate whose coarse stage already ran: `t_first` is the
 // first root that survived it, `second` whether root 1 survived too,
 // `marginal` the near-tangent flag.  Same decisions as hit_refined.
-template <bool EXACT>
+template <int M>
 __device__ __forceinline__ bool hit_exact_from(const PrimRec &r, const Geo64 &g,
                                                const Geo64 *gfull, const double d64[3],
                                                float dx, float dy,
@@ -453,24 +482,24 @@ __device__ __forceinline__ bool hit_exact_from(const PrimRec &r, const Geo64 &g,
                                                float t_first, bool second, bool marginal,
                                                Hit &h)
 {
-    if (marginal) return hit_marginal<EXACT>(r, g, gfull, d64, euclid, t_clip, h);
+    if (marginal) return hit_marginal<M>(r, g, gfull, d64, euclid, t_clip, h);
     const bool planar = (r.flags & 1u) != 0;
     double dh[3];
     local_dir64(g, d64, dh);
     if (planar && fabs(dh[2]) < 1e-12) return false;
-    if (confirm_root<EXACT>(r, g, gfull, dh, refine_depth(g, dh, planar, t_first), planar, euclid,
-                            t_clip, h))
+    if (confirm_root<M>(r, g, gfull, dh, refine_depth(g, dh, planar, t_first), planar, euclid,
+                        t_clip, h))
         return true;
     if (!second) return false;
     float roots[2], hx, hy;
     coarse_stage1(r, dx, dy, dz, t_clip, roots, hx, hy);
-    return confirm_root<EXACT>(r, g, gfull, dh, refine_depth(g, dh, planar, roots[1]), planar,
-                               euclid, t_clip, h);
+    return confirm_root<M>(r, g, gfull, dh, refine_depth(g, dh, planar, roots[1]), planar,
+                           euclid, t_clip, h);
 }
 
 // Full candidate test: coarse fp32 roots, fp64 refinement, exact selection.
 // Returns the selected hit (valid, before the alpha floor) or false.
-template <bool EXACT>
+template <int M>
 __device__ __forceinline__ bool hit_refined(const PrimRec &r, const Geo64 &g, const double d64[3],
                                             float dx, float dy, float dz, bool euclid,
                                             float t_clip, Hit &h)
@@ -478,7 +507,7 @@ __device__ __forceinline__ bool hit_refined(const PrimRec &r, const Geo64 &g, co
     float roots[2], hx, hy, hz;
     const unsigned pass = coarse_roots(r, dx, dy, dz, euclid, t_clip, roots, hx, hy, hz);
     if (pass == 0u) return false;
-    if (pass & CR_MARGINAL) return hit_marginal<EXACT>(r, g, &g, d64, euclid, t_clip, h);
+    if (pass & CR_MARGINAL) return hit_marginal<M>(r, g, &g, d64, euclid, t_clip, h);
     const bool planar = (r.flags & 1u) != 0;
     double dh[3];
     local_dir64(g, d64, dh);
@@ -487,7 +516,7 @@ __device__ __forceinline__ bool hit_refined(const PrimRec &r, const Geo64 &g, co
     for (int k = 0; k < 2; ++k) {
         if (!(pass & (1u << k))) continue;
         double t64 = refine_depth(g, dh, planar, roots[k]);
-        if (confirm_root<EXACT>(r, g, &g, dh, t64, planar, euclid, t_clip, h)) return true;
+        if (confirm_root<M>(r, g, &g, dh, t64, planar, euclid, t_clip, h)) return true;
     }
     return false;
 }
