@@ -115,13 +115,6 @@ typedef struct qgs_targets {
     int32_t *frag_page_count;  /* n_warps */
     int32_t *frag_pool_next;   /* device counter: pages handed out (the forward zeroes it) */
     int32_t frag_pool_pages;   /* pool capacity in pages */
-    int32_t *fix_scratch;      /* optional scratch of qgs_fix_scratch_ints(cam) ints for
-                                  exact decisions (settings->exact_decisions): the main
-                                  forward kernel decides in fp32 and hands every block
-                                  that met a decision inside its fp32 rounding band to a
-                                  fix-up kernel that re-runs it with the band cases
-                                  re-decided in float64.  NULL: one float64-deciding
-                                  pass over all blocks (same results, slower) */
     int32_t *tile_order;       /* optional scratch of tiles_x*tiles_y ints: the forward
                                   fills it with the tiles by descending pair count and
                                   both raster kernels run the heaviest tiles first (NULL:
@@ -179,7 +172,6 @@ int qgs_tile_keys_f64(int64_t n, const int64_t *pair_tiles, const int64_t *pair_
                       qgs_stream_t stream);
 
 /* ---- stage 3: forward raster (raster_kernels.py:83-286, rasterizer.py:198-227) */
-size_t qgs_fix_scratch_ints(const qgs_camera *cam);
 int qgs_forward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settings *st,
                 const int32_t *tile_offsets, const int32_t *tile_prims,
                 const qgs_targets *out, qgs_stream_t stream);

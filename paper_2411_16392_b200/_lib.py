@@ -44,7 +44,7 @@ class Targets(ctypes.Structure):
                                   "transmittance", "n_fragments", "violations", "aux",
                                   "counters", "frag_prim", "frag_t", "frag_xy", "frag_page_table",
                                   "frag_page_count", "frag_pool_next")] + \
-        [("frag_pool_pages", i32), ("fix_scratch", vp), ("tile_order", vp)]
+        [("frag_pool_pages", i32), ("tile_order", vp)]
 
 
 class Upstream(ctypes.Structure):
@@ -120,7 +120,6 @@ def load():
         "qgs_sorted_keys": (ctypes.c_int, [vp, i32, P(Camera), P(Settings), vp, vp, i64, vp, vp]),
         "qgs_tile_keys_f64": (ctypes.c_int, [i64, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp,
                                              P(Camera), P(Settings), vp, vp]),
-        "qgs_fix_scratch_ints": (ctypes.c_size_t, [P(Camera)]),
         "qgs_forward": (ctypes.c_int, [vp, i32, P(Camera), P(Settings), vp, vp, P(Targets), vp]),
         "qgs_backward": (ctypes.c_int, [vp, i32, P(Camera), P(Settings), vp, vp, P(Targets),
                                         P(Upstream), vp, vp]),
@@ -168,7 +167,7 @@ def load():
 
 
 EXPORTS = ("qgs_prep_bytes", "qgs_preprocess", "qgs_bin_workspace_bytes", "qgs_bin",
-           "qgs_sorted_keys", "qgs_tile_keys_f64", "qgs_fix_scratch_ints", "qgs_forward", "qgs_backward", "qgs_backward_det_workspace_bytes",
+           "qgs_sorted_keys", "qgs_tile_keys_f64", "qgs_forward", "qgs_backward", "qgs_backward_det_workspace_bytes",
            "qgs_backward_deterministic", "qgs_chain",
            "qgs_export_prep", "qgs_export_prep_geometry", "qgs_pixel_dirs", "qgs_trace_pixel", "qgs_loss_workspace_bytes",
            "qgs_loss_photometric", "qgs_loss_distortion", "qgs_depth_to_normal",

@@ -216,14 +216,6 @@ int qgs_tile_keys_f64(int64_t n, const int64_t *pair_tiles, const int64_t *pair_
     return 0;
 }
 
-size_t qgs_fix_scratch_ints(const qgs_camera *cam)
-{
-    if (!cam) return 0;
-    const qgs::CamK ck = qgs::make_camk(*cam);
-    const size_t n = (size_t)ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE;
-    return (n + 3) / 4 + n + 2;                 // flag bytes | list | count | cursor
-}
-
 int qgs_forward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settings *st,
                 const int32_t *tile_offsets, const int32_t *tile_prims, const qgs_targets *out,
                 qgs_stream_t stream)
@@ -250,26 +242,12 @@ int qgs_forward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_se
         QGS_LAUNCHED("tile_order_kernel");
     }
     const int n_slots = ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE;
-    if (sk.exact && !out->fix_scratch) {
-        // one float64-deciding pass over every block
+    if (sk.exact)       // selection decisions inside their fp32 band re-made in float64
         qgs::raster_fwd_exact_kernel<<<n_slots, qgs::RASTER_THREADS, 0, s>>>(
-            pv.rec, pv.geo, pv.conic, tile_offsets, tile_prims, ck, sk, *out, n_slots);
-    } else {
-        if (sk.exact)
-            QGS_CK(cudaMemsetAsync(out->fix_scratch, 0, (size_t)(n_slots + 3) / 4 * 4, s));
+            pv.rec, pv.geo, pv.conic, tile_offsets, tile_prims, ck, sk, *out);
+    else
         qgs::raster_fwd_kernel<<<n_slots, qgs::RASTER_THREADS, 0, s>>>(
             pv.rec, pv.geo, pv.conic, tile_offsets, tile_prims, ck, sk, *out);
-        if (sk.exact) {
-            // the blocks that met a band case, heaviest first, re-run by a
-            // persistent grid (16 warps per SM) in float64-deciding mode
-            qgs::fix_list_kernel<<<1, 1024, 0, s>>>(out->fix_scratch, n_slots);
-            int dev = 0, sms = 148;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            qgs::raster_fwd_exact_kernel<<<sms * 16, qgs::RASTER_THREADS, 0, s>>>(
-                pv.rec, pv.geo, pv.conic, tile_offsets, tile_prims, ck, sk, *out, n_slots);
-        }
-    }
     QGS_LAUNCHED("raster_fwd_kernel");
     return 0;
 }

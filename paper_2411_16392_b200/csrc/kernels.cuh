@@ -57,8 +57,7 @@ __global__ void raster_fwd_kernel(const PrimRec *recs, const Geo64 *geo, const C
 __global__ void raster_fwd_exact_kernel(const PrimRec *recs, const Geo64 *geo,
                                         const ConicRec *conics, const int32_t *tile_offsets,
                                         const int32_t *tile_prims, CamK cam, SetK st,
-                                        qgs_targets out, int n_slots);
-__global__ void fix_list_kernel(int32_t *fix_scratch, int n_slots);
+                                        qgs_targets out);
 __global__ void raster_bwd_replay_kernel(const PrimRec *recs, const Geo64 *geo,
                                          const int32_t *tile_offsets, const int32_t *tile_prims,
                                          CamK cam, SetK st, qgs_targets fwd, qgs_upstream upst,

@@ -366,7 +366,6 @@ __device__ __forceinline__ bool accept(const PrimRec &r, const Geo64 &g, const d
                                        float dx, float dy, float dz, const Cfg &c, double &t)
 {
     Hit h;
-    h.band = false;
     if (!hit_refined<M>(r, g, d64, dx, dy, dz, c.euclid, c.t_clip, h)) return false;
     if (!alpha_pass<M>(r, &g, d64, h, c.euclid, c.alpha_floor)) return false;
     t = h.t64;
@@ -417,13 +416,13 @@ __device__ __forceinline__ void finish_frag(const PrimRec &r, float dx, float dy
 
 // ================================================================ forward
 
-// One raster block (schedule slot `slot`) of the forward.  M = MODE_FLAG:
-// fp32 decisions; with settings.exact_decisions and a fix-up scratch
-// (qgs_targets.fix_scratch) a block in which any decision fell inside its
-// fp32 rounding band stops, writes nothing and is marked for the fix-up
-// kernel, which re-runs it with M = MODE_EXACT (band cases re-decided in
-// fp64, shade.cuh).  Two kernels so that the main one carries no fp64
-// selection code.
+// One raster block (schedule slot `slot`) of the forward.  M = MODE_FAST:
+// fp32 decisions; MODE_EXACT (settings.exact_decisions): decisions inside
+// their fp32 rounding band re-made in fp64 (shade.cuh).  Two kernels so
+// that the fast one carries no fp64 selection code.  (Measured and
+// rejected: an fp32 pass that hands blocks with band cases to a float64
+// fix-up pass -- ~15 % of C3's blocks meet one, and the fix-up's tail cost
+// more than the exact kernel's register pressure.)
 template <int M>
 __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
                                           const Geo64 *__restrict__ geo,
@@ -436,9 +435,6 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
     const int lane = threadIdx.x & 31;
     int tile, blk, u, v;
     block_pixel(cam.tiles_x, out.tile_order, tile, blk, u, v, slot);
-    // MODE_FLAG with deferral on: band cases hand the block to the fix-up
-    const bool defer = M == MODE_FLAG && st.exact && out.fix_scratch != nullptr;
-    bool band = false;
     const int rw = (tile << 3) | blk;                // raster warp id (fragment-log row)
     const int bu = u - (lane & 7), bv = v - (lane >> 3);
     const bool inside = u < cam.W && v < cam.H;
@@ -614,13 +610,9 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
 #endif
             const PrimRec &r = sm.rec[j];
             const Geo64 *gfull = geo + sm.qprim[j];
-            h.band = false;
-            const bool ok = hit_exact_from<M>(r, gh, gfull, d, dx, dy, dz, c.euclid, c.t_clip,
-                                              sm.tfirst[j][lane], (secb >> j) & 1u,
-                                              (margb >> j) & 1u, h) &&
-                            alpha_pass<M>(r, gfull, d, h, c.euclid, c.alpha_floor);
-            if (M == MODE_FLAG) band = band || h.band;
-            return ok;
+            return hit_exact_from<M>(r, gh, gfull, d, dx, dy, dz, c.euclid, c.t_clip,
+                                     sm.tfirst[j][lane], (secb >> j) & 1u, (margb >> j) & 1u, h) &&
+                   alpha_pass<M>(r, gfull, d, h, c.euclid, c.alpha_floor);
         };
         auto accept_one = [&](int j, const Hit &h) {
             const int p = sm.qprim[j];
@@ -666,14 +658,12 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
     // batch.
     const int start = tile_offsets[tile], end = tile_offsets[tile + 1];
     int qn = 0, an = 0;
-    bool deferred = false;                     // warp-uniform
     auto drain_b = [&]() {
         while (qn >= WB) {
             run_batch(WB);
             qn -= WB;
             if (lane < qn) { sm.qprim[lane] = sm.qprim[WB + lane]; sm.qmask[lane] = sm.qmask[WB + lane]; }
             __syncwarp();
-            if (defer && __any_sync(FULL, band)) { deferred = true; alive = false; }
             if (!__any_sync(FULL, alive)) { qn = 0; an = 0; return false; }
         }
         return true;
@@ -765,12 +755,6 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
         drain_b();
     }
     if (qn > 0 && __any_sync(FULL, alive)) run_batch(qn);
-    if (defer && (deferred || __any_sync(FULL, band))) {
-        // a decision fell inside its fp32 band: the fix-up kernel re-runs
-        // this block in MODE_EXACT and writes everything
-        if (lane == 0) reinterpret_cast<uint8_t *>(out.fix_scratch)[slot] = 1;
-        return;
-    }
 
     ensure_pages(RING);                      // the drain emits at most RING more
     while (alive && R.n > 0) {
@@ -852,64 +836,15 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
                   const ConicRec *__restrict__ conics, const int32_t *__restrict__ tile_offsets,
                   const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets out)
 {
-    fwd_block<MODE_FLAG>(recs, geo, conics, tile_offsets, tile_prims, cam, st, out, (int)blockIdx.x);
+    fwd_block<MODE_FAST>(recs, geo, conics, tile_offsets, tile_prims, cam, st, out, (int)blockIdx.x);
 }
 
-// Fix-up list: the marked slots in schedule order (heaviest tiles first),
-// one CTA; fix_scratch = [n_slots flag bytes | list | count | cursor]
-__global__ void __launch_bounds__(1024)
-fix_list_kernel(int32_t *fix_scratch, int n_slots)
-{
-    const uint8_t *flag = reinterpret_cast<const uint8_t *>(fix_scratch);
-    int32_t *list = fix_scratch + (n_slots + 3) / 4;
-    int32_t *count = list + n_slots;
-    __shared__ int wsum[32], base;
-    if (threadIdx.x == 0) base = 0;
-    __syncthreads();
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int c0 = 0; c0 < n_slots; c0 += 1024) {
-        const int i = c0 + threadIdx.x;
-        const bool f = i < n_slots && flag[i] != 0;
-        const unsigned m = __ballot_sync(FULL, f);
-        if (lane == 0) wsum[w] = __popc(m);
-        __syncthreads();
-        int pre = base;
-        for (int k = 0; k < w; ++k) pre += wsum[k];
-        if (f) list[pre + __popc(m & ((1u << lane) - 1u))] = i;
-        __syncthreads();
-        if (threadIdx.x == 0) for (int k = 0; k < 32; ++k) base += wsum[k];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) { count[0] = base; count[1] = 0; }
-}
-
-// MODE_EXACT: every block (no fix-up scratch), or, persistent, the marked
-// blocks of the fix-up list taken in order
 __global__ void __launch_bounds__(32, QGS_FWD_EXACT_MIN_BLOCKS)
 raster_fwd_exact_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
                         const ConicRec *__restrict__ conics, const int32_t *__restrict__ tile_offsets,
-                        const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets out,
-                        int n_slots)
+                        const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets out)
 {
-    const bool all = out.fix_scratch == nullptr;
-    const int32_t *list = all ? nullptr : out.fix_scratch + (n_slots + 3) / 4;
-    int32_t *count = all ? nullptr : const_cast<int32_t *>(list) + n_slots;
-    const int lane = threadIdx.x & 31;
-    for (int it = 0;; ++it) {
-        int slot;
-        if (all) {
-            if (it > 0) return;
-            slot = (int)blockIdx.x;
-        } else {
-            int i = 0;
-            if (lane == 0) i = atomicAdd(&count[1], 1);
-            i = __shfl_sync(FULL, i, 0);
-            if (i >= count[0]) return;
-            slot = list[i];
-        }
-        fwd_block<MODE_EXACT>(recs, geo, conics, tile_offsets, tile_prims, cam, st, out, slot);
-        __syncwarp();
-    }
+    fwd_block<MODE_EXACT>(recs, geo, conics, tile_offsets, tile_prims, cam, st, out, (int)blockIdx.x);
 }
 
 // =============================================================== backward

@@ -46,15 +46,11 @@ struct Hit {
     float q;                  // dt-denominator: F'(t) (quad), B (linear), dhz (planar)
     float dhx, dhy, dhz;
     int branch;
-    bool band;                // MODE_FLAG: a decision fell inside its fp32 rounding band
 };
 
 // Decision modes of the candidate test: MODE_FAST fp32 decisions; MODE_EXACT
-// (settings.exact_decisions) re-makes band cases in fp64; MODE_FLAG fp32
-// decisions that mark band cases in Hit::band -- the forward re-runs the
-// blocks that saw one in MODE_EXACT (a fix-up pass), so the default kernel
-// carries no fp64 selection code.
-enum { MODE_FAST = 0, MODE_EXACT = 1, MODE_FLAG = 2 };
+// (settings.exact_decisions) re-makes band cases in fp64.
+enum { MODE_FAST = 0, MODE_EXACT = 1 };
 
 // arc length of z = a r^2 over [0, rho]; series below |u| = 0.3 (error < 1e-8)
 __device__ __forceinline__ float arc32(float a, float rho)
@@ -269,20 +265,7 @@ __device__ __forceinline__ bool confirm_root(const PrimRec &r, const Geo64 &g, c
 {
     if (!(t64 > (double)t_clip)) return false;
     shade_at(r, g, dh, t64, euclid, h);
-    if (M == MODE_FLAG) {
-        bool pass = true, near = false;
-        if (!planar) {
-            const float ex = r.s2 * h.x, ey = r.s1 * h.y;
-            const float m = fmaf(ex, ex, ey * ey);
-            pass = m <= r.ell9;
-            near = fabsf(m - r.ell9) <= SEL_BAND * r.ell9;
-        }
-        const float lim = 3.f * h.sig;
-        pass = pass && h.l <= lim;
-        near = near || fabsf(h.l - lim) <= SEL_BAND * lim;
-        h.band = h.band || near;
-        if (!pass) return false;
-    } else if (M == MODE_FAST) {
+    if (M == MODE_FAST) {
         if (!planar && ellipse_out(r, h.x, h.y, 1.f)) return false;
         if (!(h.l <= 3.f * h.sig)) return false;
     } else {
@@ -304,13 +287,12 @@ __device__ __forceinline__ bool confirm_root(const PrimRec &r, const Geo64 &g, c
 }
 
 // the alpha floor on a selected hit (raster_kernels.py:58-60); fp64 inside
-// its band in MODE_EXACT, flagged in MODE_FLAG
+// its band in MODE_EXACT
 template <int M>
 __device__ __forceinline__ bool alpha_pass(const PrimRec &r, const Geo64 *gfull, const double d64[3],
                                            Hit &h, bool euclid, float floor)
 {
     const float ab = r.alpha * h.G;
-    if (M == MODE_FLAG) h.band = h.band || fabsf(ab - floor) <= FLOOR_BAND * floor;
     if (M != MODE_EXACT || fabsf(ab - floor) > FLOOR_BAND * floor) return ab >= floor;
     double dh[3];
     dh[0] = gfull->M[0] * d64[0] + gfull->M[1] * d64[1] + gfull->M[2] * d64[2];
@@ -328,7 +310,7 @@ __device__ __forceinline__ bool alpha_pass(const PrimRec &r, const Geo64 *gfull,
 template <int M>
 static __device__ __noinline__ double marginal_root(const PrimRec &r, const Geo64 &g,
                                                     const Geo64 *gfull, const double d64[3],
-                                                    bool euclid, float t_clip, bool &band)
+                                                    bool euclid, float t_clip)
 {
     double dh[3];
     local_dir64(g, d64, dh);
@@ -352,13 +334,8 @@ static __device__ __noinline__ double marginal_root(const PrimRec &r, const Geo6
         cnt = disc == 0.0 ? 1 : 2;
     }
     Hit h;
-    h.band = false;
     for (int k = 0; k < cnt; ++k)
-        if (confirm_root<M>(r, g, gfull, dh, roots[k], false, euclid, t_clip, h)) {
-            band = band || h.band;
-            return roots[k];
-        }
-    band = band || h.band;
+        if (confirm_root<M>(r, g, gfull, dh, roots[k], false, euclid, t_clip, h)) return roots[k];
     return -1.0;
 }
 
@@ -366,9 +343,7 @@ template <int M>
 __device__ __forceinline__ bool hit_marginal(const PrimRec &r, const Geo64 &g, const Geo64 *gfull,
                                              const double d64[3], bool euclid, float t_clip, Hit &h)
 {
-    bool band = false;
-    const double t = marginal_root<M>(r, g, gfull, d64, euclid, t_clip, band);
-    h.band = h.band || band;
+    const double t = marginal_root<M>(r, g, gfull, d64, euclid, t_clip);
     if (!(t > 0.0)) return false;
     double dh[3];
     local_dir64(g, d64, dh);

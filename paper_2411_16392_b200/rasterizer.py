@@ -297,7 +297,6 @@ class RenderTargets:
     frag_page_count: torch.Tensor = None   # (raster warps,) int32, -1 = not logged
     frag_pool_next: torch.Tensor = None    # (1,) int32 pages handed out
     tile_order: torch.Tensor = None    # tiles by descending pair count (raster schedule)
-    fix_scratch: torch.Tensor = None   # exact-decision fix-up list (qgs_targets.fix_scratch)
 
     @property
     def order_violations(self):
@@ -486,11 +485,6 @@ def forward(prep: PreparedView, keep_aux=True, counters=None, frag_log=True) -> 
     t.aux = _ptr(tg.aux) if keep_aux else None
     if keep_aux and frag_log:
         _alloc_frag_log(tg, t, prep, H, W, device)
-    if getattr(prep.settings, "exact_decisions", True):
-        # fp32 main pass + float64 fix-up of the blocks with band cases
-        n = int(_lib.load().qgs_fix_scratch_ints(prep._cam_c))
-        tg.fix_scratch = torch.empty((n,), dtype=torch.int32, device=device)
-        t.fix_scratch = _ptr(tg.fix_scratch)
     tg.tile_order = torch.empty((prep.tiles_x * prep.tiles_y,), dtype=torch.int32, device=device)
     t.tile_order = _ptr(tg.tile_order)
     t.counters = _ptr(counters)
