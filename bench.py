@@ -240,7 +240,7 @@ def run_ours(a):
     # ... and the raster kernels alone (this rank's views prepared first, then
     # forward / backward each bracketed by events, nothing beside them): the
     # roofline's launch durations
-    fwd_ms, bwd_ms = isolated_raster_ms(rz, dev, cams, mine, ups, st, stream)
+    fwd_ms, bwd_ms, frag_log = isolated_raster_ms(rz, dev, cams, mine, ups, st, stream)
     view_ms = np.mean([span(r, "view_begin", "view_end") for r in evs], axis=0).tolist() \
         if mine else []
     red_ms = float(np.mean([{n: e for n, _, e in r}["reduce_begin"].elapsed_time(
@@ -322,6 +322,7 @@ def run_ours(a):
         "gpu_launches": OUR_LAUNCHES_PER_VIEW * V * K,
         "compute_peaks": cp,
         "per_rank": per_rank,
+        "fragment_log": frag_log,
     }
     if e2e is not None:
         out["e2e"] = e2e
@@ -336,7 +337,8 @@ def isolated_raster_ms(rz, dev, cams, views, ups, st, stream, reps=2):
     """forward and backward (kernel gradients) time per step, each view's
     raster kernels alone on the device (CUDA events on the launching stream)"""
     fwd = bwd = 0.0
-    for _ in range(reps):
+    log = {"pages_used": 0, "bytes_used": 0, "bytes_allocated": 0, "fragments": 0}
+    for r in range(reps):
         for v in views:
             prep = rz.prepare(dev, cams[v], st)
             torch.cuda.synchronize()
@@ -349,7 +351,17 @@ def isolated_raster_ms(rz, dev, cams, views, ups, st, stream, reps=2):
             torch.cuda.synchronize()
             fwd += e[0].elapsed_time(e[1])
             bwd += e[1].elapsed_time(e[2])
-    return fwd / reps, bwd / reps
+            if r == 0 and tg.frag_prim is not None:     # fragment log footprint
+                pages = int(tg.frag_pool_next.item())
+                slot_b = 4 + 8 + (8 if tg.frag_xy is not None else 0)
+                log["pages_used"] += pages
+                log["bytes_used"] += pages * rz.FRAG_PAGE * 32 * slot_b
+                log["bytes_allocated"] += tg.frag_prim.numel() * slot_b
+                log["fragments"] += int(tg.n_fragments.sum().item())
+    n = max(len(views), 1)
+    log = {k: v // n for k, v in log.items()}
+    log["note"] = "per view, paged fragment log (include/qgs_b200.h qgs_targets)"
+    return fwd / reps, bwd / reps, log
 
 
 def run_e2e(a, rz, sc, mine, device, st, world):

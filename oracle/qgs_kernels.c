@@ -387,11 +387,24 @@ typedef struct {
     const qo_settings *st;
     double *rows;          /* this tile's pair-gradient rows, NG per position */
     double *rows_abs;      /* optional: sums of |each fragment's contribution| (diagnostics) */
+    int64_t px;            /* pixel index (diagnostics) */
     int64_t row0;          /* tile_offsets[tile] */
     double d[3];
     double T, pref, vtot, F0, F1, F2;
     double uc[3], ua, ut, un[3], uk, ud;
 } qo_bwd_px;
+
+/* diagnostics: per-fragment contributions of one primitive
+ * (qo_set_diag_prim): rows of [pixel, t, 33 slot deltas] */
+static int64_t diag_prim = -1, diag_n = 0, diag_max = 0;
+static double *diag_buf = NULL;
+
+void qo_set_diag_prim(int64_t prim, double *buf, int64_t max_rows)
+{
+    diag_prim = prim; diag_buf = buf; diag_max = max_rows; diag_n = 0;
+}
+
+int64_t qo_diag_rows(void) { return diag_n; }
 
 /* _grad_fragment, raster_kernels.py:289-502 */
 static int bwd_visit(void *vctx, int64_t pos, int64_t p, const qo_frag *f)
@@ -400,7 +413,7 @@ static int bwd_visit(void *vctx, int64_t pos, int64_t p, const qo_frag *f)
     const qo_prims *pr = c->pr;
     double *g = c->rows + (pos - c->row0) * QO_NG;
     double before[QO_NG];
-    if (c->rows_abs)
+    if (c->rows_abs || p == diag_prim)
         for (int j = 0; j < QO_NG; ++j) before[j] = g[j];
     const double *wv = pr->wv + 3 * p, *sv = pr->sv + 3 * p, *oh = pr->ohat + 3 * p;
     const double *N = pr->Nmat + 9 * p, *Mp = pr->M + 9 * p, *col = pr->colors + 3 * p;
@@ -568,6 +581,17 @@ static int bwd_visit(void *vctx, int64_t pos, int64_t p, const qo_frag *f)
         double *ga = c->rows_abs + (pos - c->row0) * QO_NG;
         for (int j = 0; j < QO_NG; ++j) ga[j] += fabs(g[j] - before[j]);
     }
+    if (p == diag_prim && diag_buf) {
+#pragma omp critical(qo_diag)
+        {
+            if (diag_n < diag_max) {
+                double *r = diag_buf + diag_n * (QO_NG + 2);
+                r[0] = (double)c->px; r[1] = t;
+                for (int j = 0; j < QO_NG; ++j) r[2 + j] = g[j] - before[j];
+            }
+            diag_n++;
+        }
+    }
 
     c->T = T * (1.0 - abar);
     return !(c->T < c->st->t_term);
@@ -601,7 +625,7 @@ static void bwd_tile(int64_t tile, int64_t H, int64_t W, const double *dirs,
                 c.ut == 0.0 && c.un[0] == 0.0 && c.un[1] == 0.0 && c.un[2] == 0.0 &&
                 c.uk == 0.0 && c.ud == 0.0)
                 continue;
-            c.pr = pr; c.st = st; c.rows = rows; c.rows_abs = rows_abs;
+            c.pr = pr; c.st = st; c.rows = rows; c.rows_abs = rows_abs; c.px = px;
             c.row0 = tile_offsets[tile];
             c.d[0] = dirs[3 * px]; c.d[1] = dirs[3 * px + 1]; c.d[2] = dirs[3 * px + 2];
             c.F0 = f_alpha[px]; c.F1 = f_depth[px]; c.F2 = f_depthsq[px];

@@ -97,6 +97,8 @@ def lib():
         L.qo_tile_keys.argtypes = [i64, vp, vp, i64, ctypes.POINTER(_Prims), vp, vp, vp,
                                    d, d, d, d, i64, i64, ctypes.c_int, d, vp]
         L.qo_num_threads.restype = ctypes.c_int
+        L.qo_set_diag_prim.argtypes = [i64, vp, i64]
+        L.qo_diag_rows.restype = i64
         L.qo_trace_pixel.restype = ctypes.c_int
         L.qo_trace_pixel.argtypes = [i64, vp, vp, vp, i64, ctypes.POINTER(_Prims),
                                      ctypes.POINTER(_Settings), i64, i64, ctypes.c_int] + [vp] * 8
@@ -638,6 +640,22 @@ def kernel_grads(vw, targets, upstream, with_abs=False):
     if rc != 0:
         raise MemoryError("oracle backward: allocation failed")
     return (kg, kg_abs) if with_abs else kg
+
+
+def fragment_contributions(vw, targets, upstream, prim, max_rows=1 << 16):
+    """diagnostics: every composited fragment of primitive `prim` with its 33
+    slot contributions -> (pixel index, t, (n, 33) slots)"""
+    buf = np.zeros((max_rows, NG + 2))
+    lib().qo_set_diag_prim(int(prim), _p(buf), max_rows)
+    try:
+        kernel_grads(vw, targets, upstream)
+        n = min(lib().qo_diag_rows(), max_rows)
+    finally:
+        lib().qo_set_diag_prim(-1, None, 0)
+    rows = buf[:n]
+    order = np.lexsort((rows[:, 1], rows[:, 0]))
+    rows = rows[order]
+    return rows[:, 0].astype(np.int64), rows[:, 1], rows[:, 2:]
 
 
 def chain_jacobian(vw, idx):

@@ -531,9 +531,13 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
 
     // Batch of up to WB queued entries: stage their records, run the coarse
     // test on each pixel's culled-in candidates (pass 1), then the exact
-    // test, ring and compositing in stream order (pass 2).
-    auto run_batch = [&](int nb) {
-        ensure_pages(nb);                        // each entry emits at most one fragment per pixel
+    // test, ring and compositing in stream order (pass 2).  drain: after the
+    // last batch (nb = 0) -- pass 2 empties the ring instead.  ONE call site
+    // (as for every phase below): each inlined copy of this body costs ~3K
+    // instructions, and the instruction cache is the forward's second
+    // largest stall (ncu no_instruction).
+    auto run_batch = [&](int nb, bool drain) {
+        ensure_pages(drain ? RING : nb);         // each entry emits at most one fragment per pixel
         load_batch_ids(sm.rec, recs, sm.qprim, nb);
         // geometry heads for the exact pass, copied asynchronously under pass 1
 #if QGS_FWD_STAGE_GEO
@@ -640,11 +644,23 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
             else emit = ring_push_pay(R, sm.pay, lane, h.t64, p, pin, et, ep, pout);
             if (emit) composite(ep, et, pout);
         };
-        while (bits && alive) {
-            const int j = __ffs(bits) - 1;
-            bits &= bits - 1;
-            Hit h;
-            if (exact(j, h)) accept_one(j, h);
+        if (!drain) {
+            while (bits && alive) {
+                const int j = __ffs(bits) - 1;
+                bits &= bits - 1;
+                Hit h;
+                if (exact(j, h)) accept_one(j, h);
+            }
+        } else {
+            // raster_kernels.py:227-270: drain while alive (first minimum,
+            // swap with last)
+            while (alive && R.n > 0) {
+                double et;
+                int ep;
+                Pay pout;
+                ring_pop_pay(R, sm.pay, lane, et, ep, pout);
+                composite(ep, et, pout);
+            }
         }
         __syncwarp();
     };
@@ -658,16 +674,6 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
     // batch.
     const int start = tile_offsets[tile], end = tile_offsets[tile + 1];
     int qn = 0, an = 0;
-    auto drain_b = [&]() {
-        while (qn >= WB) {
-            run_batch(WB);
-            qn -= WB;
-            if (lane < qn) { sm.qprim[lane] = sm.qprim[WB + lane]; sm.qmask[lane] = sm.qmask[WB + lane]; }
-            __syncwarp();
-            if (!__any_sync(FULL, alive)) { qn = 0; an = 0; return false; }
-        }
-        return true;
-    };
     auto conic_pass = [&](int na) {            // queue A entries [0, na) -> queue B
         const uint32_t live = __ballot_sync(FULL, alive);
         uint32_t m = 0u;
@@ -697,7 +703,33 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
     int id1 = ld_id(start), id2 = ld_id(start + 32);
     uint2 bb1 = ld_bb(start, id1);
 #endif
-    for (int b0 = start; b0 < end; b0 += 32) {
+    // One loop, warp-uniform decisions, each phase at one call site: a batch
+    // as soon as queue B holds WB entries (or nothing more can come), else a
+    // conic pass as soon as queue A holds 32 (or the list is done), else the
+    // next 32-entry window of the list; the ring is drained last.
+    int b0 = start;
+    for (;;) {
+        const bool list_done = b0 >= end;
+        const bool upstream_done = list_done && an == 0;
+        if (qn >= WB || (upstream_done && qn > 0) || (upstream_done && qn == 0)) {
+            const bool drain = upstream_done && qn == 0;
+            const int nb = min(qn, WB);
+            run_batch(nb, drain);
+            if (drain) break;
+            qn -= nb;
+            if (lane < qn) { sm.qprim[lane] = sm.qprim[nb + lane]; sm.qmask[lane] = sm.qmask[nb + lane]; }
+            __syncwarp();
+            if (!__any_sync(FULL, alive)) break;
+            continue;
+        }
+        if (an >= 32 || list_done) {             // list_done here implies an > 0
+            const int na = min(an, 32);
+            conic_pass(na);
+            an -= na;
+            if (lane < an) { sm.aprim[lane] = sm.aprim[32 + lane]; sm.amask[lane] = sm.amask[32 + lane]; }
+            __syncwarp();
+            continue;
+        }
         const uint32_t live = __ballot_sync(FULL, alive);
         if (!live) break;
         const int nb = min(32, end - b0);
@@ -742,28 +774,9 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
         }
         an += __popc(keep);
         __syncwarp();
-        if (an >= 32) {
-            conic_pass(32);
-            an -= 32;
-            if (lane < an) { sm.aprim[lane] = sm.aprim[32 + lane]; sm.amask[lane] = sm.amask[32 + lane]; }
-            __syncwarp();
-            if (!drain_b()) break;
-        }
+        b0 += 32;
     }
-    if (an > 0 && __any_sync(FULL, alive)) {
-        conic_pass(an);
-        drain_b();
-    }
-    if (qn > 0 && __any_sync(FULL, alive)) run_batch(qn);
 
-    ensure_pages(RING);                      // the drain emits at most RING more
-    while (alive && R.n > 0) {
-        double et;
-        int ep;
-        Pay pout;
-        ring_pop_pay(R, sm.pay, lane, et, ep, pout);
-        composite(ep, et, pout);
-    }
     if (out.frag_page_count) {
         if (lane < npages) out.frag_page_table[(size_t)rw * QGS_FRAG_MAX_PAGES + lane] = sm.pages[lane];
         if (lane == 0) out.frag_page_count[rw] = (out.frag_prim && log_on) ? npages : -1;
