@@ -242,12 +242,17 @@ int qgs_forward(const void *prep, int32_t P, const qgs_camera *cam, const qgs_se
         QGS_LAUNCHED("tile_order_kernel");
     }
     const int n_slots = ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE;
+    const size_t fsm = qgs::FWD_WPC * qgs::fwd_smem_per_warp();
+    QGS_CK(qgs::ensure_smem_attr(reinterpret_cast<const void *>(qgs::raster_fwd_exact_kernel), (int)fsm));
+    QGS_CK(qgs::ensure_smem_attr(reinterpret_cast<const void *>(qgs::raster_fwd_kernel), (int)fsm));
     if (sk.exact)       // selection decisions inside their fp32 band re-made in float64
-        qgs::raster_fwd_exact_kernel<<<n_slots, qgs::RASTER_THREADS, 0, s>>>(
-            pv.rec, pv.geo, pv.conic, tile_offsets, tile_prims, ck, sk, *out);
+        qgs::raster_fwd_exact_kernel<<<n_slots / qgs::FWD_WPC, qgs::RASTER_THREADS * qgs::FWD_WPC,
+                                       fsm, s>>>(pv.rec, pv.geo, pv.conic, tile_offsets,
+                                                 tile_prims, ck, sk, *out);
     else
-        qgs::raster_fwd_kernel<<<n_slots, qgs::RASTER_THREADS, 0, s>>>(
-            pv.rec, pv.geo, pv.conic, tile_offsets, tile_prims, ck, sk, *out);
+        qgs::raster_fwd_kernel<<<n_slots / qgs::FWD_WPC, qgs::RASTER_THREADS * qgs::FWD_WPC, fsm,
+                                 s>>>(pv.rec, pv.geo, pv.conic, tile_offsets, tile_prims, ck, sk,
+                                      *out);
     QGS_LAUNCHED("raster_fwd_kernel");
     return 0;
 }
@@ -263,18 +268,22 @@ int backward_impl(const void *prep, int32_t P, const qgs_camera *cam, const qgs_
     const int grid = ck.tiles_x * ck.tiles_y * qgs::RASTER_BLOCKS_PER_TILE;
     // blocks with a fragment log, then (a launch whose warps mostly exit at
     // once) the blocks without one
+    const size_t bsm = qgs::BWD_WPC * qgs::bwd_smem_per_warp();
+    QGS_CK(qgs::ensure_smem_attr(reinterpret_cast<const void *>(qgs::raster_bwd_det_kernel), (int)bsm));
+    QGS_CK(qgs::ensure_smem_attr(reinterpret_cast<const void *>(qgs::raster_bwd_kernel), (int)bsm));
     if (det.rows)
-        qgs::raster_bwd_det_kernel<<<grid, qgs::RASTER_THREADS, 0, s>>>(
-            pv.rec, pv.geo, tile_offsets, tile_prims, ck, sk, *fwd, *up, kg, det);
+        qgs::raster_bwd_det_kernel<<<grid / qgs::BWD_WPC, qgs::RASTER_THREADS * qgs::BWD_WPC, bsm,
+                                     s>>>(pv.rec, pv.geo, tile_offsets, tile_prims, ck, sk, *fwd,
+                                          *up, kg, det);
     else
-        qgs::raster_bwd_kernel<<<grid, qgs::RASTER_THREADS, 0, s>>>(
+        qgs::raster_bwd_kernel<<<grid / qgs::BWD_WPC, qgs::RASTER_THREADS * qgs::BWD_WPC, bsm, s>>>(
             pv.rec, pv.geo, tile_offsets, tile_prims, ck, sk, *fwd, *up, kg, det);
     {
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int rgrid = std::min(sms * 4, (grid + 31) / 32);
-        qgs::raster_bwd_replay_kernel<<<rgrid, qgs::RASTER_THREADS, 0, s>>>(
+        qgs::raster_bwd_replay_kernel<<<rgrid, qgs::RASTER_THREADS, qgs::bwd_smem_per_warp(), s>>>(
             pv.rec, pv.geo, tile_offsets, tile_prims, ck, sk, *fwd, *up, kg, det);
     }
     QGS_LAUNCHED("raster_bwd_kernel");

@@ -79,5 +79,17 @@ __global__ void tile_order_kernel(const int32_t *tile_offsets, int n_tiles, int3
 constexpr int ORDER_SMEM = 0;      // static shared memory only
 constexpr int RASTER_THREADS = 32;   // one warp per 8x4 block, 8 blocks per tile
 constexpr int RASTER_BLOCKS_PER_TILE = 8;
+// raster warps per CTA (independent warps; a CTA of several puts a tile's
+// blocks on one SM, where they share the L1 for the tile's list and records)
+#ifndef QGS_FWD_WPC
+#define QGS_FWD_WPC 1
+#endif
+#ifndef QGS_BWD_WPC
+#define QGS_BWD_WPC 1
+#endif
+constexpr int FWD_WPC = QGS_FWD_WPC;
+constexpr int BWD_WPC = QGS_BWD_WPC;
+size_t fwd_smem_per_warp();
+size_t bwd_smem_per_warp();
 
 }  // namespace qgs

@@ -54,6 +54,9 @@ namespace qgs {
 #ifndef QGS_WB
 #define QGS_WB 4
 #endif
+#ifndef QGS_FWD_SINGLE_SITE
+#define QGS_FWD_SINGLE_SITE 0     // 1: one loop, one call site per phase (half the code, measured slower)
+#endif
 #ifndef QGS_FWD_RAY_REGS
 #define QGS_FWD_RAY_REGS 1    // fp64 pixel ray in registers instead of shared memory
 #endif
@@ -112,11 +115,12 @@ struct Pay {
     float v[PAYN];
 };
 
-// (tile, block) of schedule slot `slot` (default: this CTA) and the lane's pixel
+// (tile, block) of schedule slot `slot` (default: this warp of this CTA)
+// and the lane's pixel
 __device__ __forceinline__ void block_pixel(int tiles_x, const int32_t *order, int &tile, int &blk,
                                             int &u, int &v, int slot = -1)
 {
-    if (slot < 0) slot = (int)blockIdx.x;
+    if (slot < 0) slot = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
     tile = order ? order[slot >> 3] : (slot >> 3);
     blk = slot & 7;
     const int ty = tile / tiles_x, tx = tile - ty * tiles_x;
@@ -431,7 +435,9 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
                                           const int32_t *__restrict__ tile_prims, const CamK &cam,
                                           const SetK &st, const qgs_targets &out, int slot)
 {
-    __shared__ FwdSmem sm;
+    // one FwdSmem per warp (dynamic shared memory: QGS_FWD_WPC warps per CTA)
+    extern __shared__ __align__(16) unsigned char raster_smem[];
+    FwdSmem &sm = reinterpret_cast<FwdSmem *>(raster_smem)[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
     int tile, blk, u, v;
     block_pixel(cam.tiles_x, out.tile_order, tile, blk, u, v, slot);
@@ -674,6 +680,7 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
     // batch.
     const int start = tile_offsets[tile], end = tile_offsets[tile + 1];
     int qn = 0, an = 0;
+#if QGS_FWD_SINGLE_SITE
     auto conic_pass = [&](int na) {            // queue A entries [0, na) -> queue B
         const uint32_t live = __ballot_sync(FULL, alive);
         uint32_t m = 0u;
@@ -777,6 +784,114 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
         b0 += 32;
     }
 
+#else
+    auto drain_b = [&]() {
+        while (qn >= WB) {
+            run_batch(WB, false);
+            qn -= WB;
+            if (lane < qn) { sm.qprim[lane] = sm.qprim[WB + lane]; sm.qmask[lane] = sm.qmask[WB + lane]; }
+            __syncwarp();
+            if (!__any_sync(FULL, alive)) { qn = 0; an = 0; return false; }
+        }
+        return true;
+    };
+    auto conic_pass = [&](int na) {            // queue A entries [0, na) -> queue B
+        const uint32_t live = __ballot_sync(FULL, alive);
+        uint32_t m = 0u;
+        int pj = 0;
+        if (lane < na) {
+            pj = sm.aprim[lane];
+            m = sm.amask[lane] & live;
+            if (m && cull) m &= conic_rows<4>(conics[pj], bu, bv, 0);
+        }
+        const uint32_t keep = __ballot_sync(FULL, m != 0u);
+        if (m) {
+            const int pos = qn + __popc(keep & ((1u << lane) - 1u));
+            sm.qprim[pos] = pj;
+            sm.qmask[pos] = m;
+        }
+        qn += __popc(keep);
+        __syncwarp();
+    };
+#if QGS_FWD_LIST_PREFETCH
+    // list windows software-pipelined: the ids of window w+2 and the culled
+    // boxes of window w+1 are in flight while window w is processed
+    auto ld_id = [&](int b) { return b + lane < end ? __ldg(tile_prims + b + lane) : 0; };
+    auto ld_bb = [&](int b, int p) {
+        return (cull && b + lane < end) ? __ldg(reinterpret_cast<const uint2 *>(&conics[p].bb_u))
+                                        : make_uint2(0u, 0u);
+    };
+    int id1 = ld_id(start), id2 = ld_id(start + 32);
+    uint2 bb1 = ld_bb(start, id1);
+#endif
+    for (int b0 = start; b0 < end; b0 += 32) {
+        const uint32_t live = __ballot_sync(FULL, alive);
+        if (!live) break;
+        const int nb = min(32, end - b0);
+        int pj = 0;
+        uint32_t bm = 0u;
+#if QGS_FWD_LIST_PREFETCH
+        const int pcur = id1;
+        const uint2 bcur = bb1;
+        id1 = id2;
+        bb1 = ld_bb(b0 + 32, id1);
+        id2 = ld_id(b0 + 64);
+#endif
+        if (lane < nb) {
+#if QGS_FWD_LIST_PREFETCH
+            pj = pcur;
+            if (cull) {
+                bm = block_lanes(bcur.x, bcur.y, bu, bv);
+            } else {
+#else
+            pj = tile_prims[b0 + lane];
+            if (cull) {
+                const uint2 bb = *reinterpret_cast<const uint2 *>(&conics[pj].bb_u);
+                bm = block_lanes(bb.x, bb.y, bu, bv);
+            } else {
+#endif
+                bm = block_lanes(recs[pj].bb_u, recs[pj].bb_v, bu, bv);
+            }
+            if (out.counters)                  // algorithmic work: the reference's pixel box
+                sm.boxw[lane] = cull ? block_lanes(recs[pj].bb_u, recs[pj].bb_v, bu, bv) : bm;
+            bm &= live;
+        }
+        if (out.counters) {
+            __syncwarp();
+            for (int j = 0; j < nb; ++j) n_box += alive ? (sm.boxw[j] >> lane) & 1u : 0u;
+            __syncwarp();
+        }
+        const uint32_t keep = __ballot_sync(FULL, bm != 0u);
+        if (bm) {
+            const int pos = an + __popc(keep & ((1u << lane) - 1u));
+            sm.aprim[pos] = pj;
+            sm.amask[pos] = bm;
+        }
+        an += __popc(keep);
+        __syncwarp();
+        if (an >= 32) {
+            conic_pass(32);
+            an -= 32;
+            if (lane < an) { sm.aprim[lane] = sm.aprim[32 + lane]; sm.amask[lane] = sm.amask[32 + lane]; }
+            __syncwarp();
+            if (!drain_b()) break;
+        }
+    }
+    if (an > 0 && __any_sync(FULL, alive)) {
+        conic_pass(an);
+        drain_b();
+    }
+    if (qn > 0 && __any_sync(FULL, alive)) run_batch(qn, false);
+
+    ensure_pages(RING);                      // the drain emits at most RING more
+    while (alive && R.n > 0) {
+        double et;
+        int ep;
+        Pay pout;
+        ring_pop_pay(R, sm.pay, lane, et, ep, pout);
+        composite(ep, et, pout);
+    }
+#endif
     if (out.frag_page_count) {
         if (lane < npages) out.frag_page_table[(size_t)rw * QGS_FRAG_MAX_PAGES + lane] = sm.pages[lane];
         if (lane == 0) out.frag_page_count[rw] = (out.frag_prim && log_on) ? npages : -1;
@@ -844,20 +959,20 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
     }
 }
 
-__global__ void __launch_bounds__(32, QGS_FWD_MIN_BLOCKS)
+__global__ void __launch_bounds__(32 * FWD_WPC, QGS_FWD_MIN_BLOCKS / FWD_WPC)
 raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
                   const ConicRec *__restrict__ conics, const int32_t *__restrict__ tile_offsets,
                   const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets out)
 {
-    fwd_block<MODE_FAST>(recs, geo, conics, tile_offsets, tile_prims, cam, st, out, (int)blockIdx.x);
+    fwd_block<MODE_FAST>(recs, geo, conics, tile_offsets, tile_prims, cam, st, out, -1);
 }
 
-__global__ void __launch_bounds__(32, QGS_FWD_EXACT_MIN_BLOCKS)
+__global__ void __launch_bounds__(32 * FWD_WPC, QGS_FWD_EXACT_MIN_BLOCKS / FWD_WPC)
 raster_fwd_exact_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
                         const ConicRec *__restrict__ conics, const int32_t *__restrict__ tile_offsets,
                         const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets out)
 {
-    fwd_block<MODE_EXACT>(recs, geo, conics, tile_offsets, tile_prims, cam, st, out, (int)blockIdx.x);
+    fwd_block<MODE_EXACT>(recs, geo, conics, tile_offsets, tile_prims, cam, st, out, -1);
 }
 
 // =============================================================== backward
@@ -1016,7 +1131,7 @@ __device__ __forceinline__ void frag_grad(const PrimRec &r, const Frag &f, float
 __device__ __forceinline__ void warp_accumulate(float (*red)[33][KGP], bool emit, int prim,
                                                 const float g[KG], float *__restrict__ kg)
 {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, w = 0;   // red: this warp's own buffer
     const unsigned key = emit ? (unsigned)prim : 0xffffffffu;
     const unsigned peers = __match_any_sync(FULL, key);
 #if QGS_RED_SINGLES
@@ -1103,7 +1218,10 @@ __device__ __forceinline__ void bwd_block(const PrimRec *__restrict__ recs,
                                           const qgs_upstream &upst, float *__restrict__ kg,
                                           const DetRows &det, int slot = -1)
 {
-    __shared__ BwdSmem sm;
+    // one BwdSmem per warp (dynamic shared memory: QGS_BWD_WPC warps per CTA;
+    // the replay kernel: one warp per CTA)
+    extern __shared__ __align__(16) unsigned char raster_smem[];
+    BwdSmem &sm = reinterpret_cast<BwdSmem *>(raster_smem)[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
     if (lane < KG) sm.red[0][32][lane] = 0.f;        // zero row for padded group sums
     __syncwarp();
@@ -1295,7 +1413,7 @@ __device__ __forceinline__ void bwd_block(const PrimRec *__restrict__ recs,
     }
 }
 
-__global__ void __launch_bounds__(32, QGS_BWD_MIN_BLOCKS)
+__global__ void __launch_bounds__(32 * BWD_WPC, QGS_BWD_MIN_BLOCKS / BWD_WPC)
 raster_bwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
                   const int32_t *__restrict__ tile_offsets,
                   const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets fwd,
@@ -1352,7 +1470,7 @@ raster_bwd_replay_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restri
 }
 
 // deterministic mode (det_reduce.cu): rows instead of atomics
-__global__ void __launch_bounds__(32, QGS_BWD_MIN_BLOCKS)
+__global__ void __launch_bounds__(32 * BWD_WPC, QGS_BWD_MIN_BLOCKS / BWD_WPC)
 raster_bwd_det_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
                       const int32_t *__restrict__ tile_offsets,
                       const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets fwd,
@@ -1360,6 +1478,9 @@ raster_bwd_det_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict_
 {
     bwd_block<false, true, false>(recs, geo, tile_offsets, tile_prims, cam, st, fwd, upst, kg, det);
 }
+
+size_t fwd_smem_per_warp() { return sizeof(FwdSmem); }
+size_t bwd_smem_per_warp() { return sizeof(BwdSmem); }
 
 // ===================================================== raster schedule
 // tiles by descending pair count (ties by tile), so the raster kernels start
