@@ -54,9 +54,6 @@ namespace qgs {
 #ifndef QGS_WB
 #define QGS_WB 4
 #endif
-#ifndef QGS_FWD_SINGLE_SITE
-#define QGS_FWD_SINGLE_SITE 0     // 1: one loop, one call site per phase (half the code, measured slower)
-#endif
 #ifndef QGS_FWD_RAY_REGS
 #define QGS_FWD_RAY_REGS 1    // fp64 pixel ray in registers instead of shared memory
 #endif
@@ -537,13 +534,12 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
 
     // Batch of up to WB queued entries: stage their records, run the coarse
     // test on each pixel's culled-in candidates (pass 1), then the exact
-    // test, ring and compositing in stream order (pass 2).  drain: after the
-    // last batch (nb = 0) -- pass 2 empties the ring instead.  ONE call site
-    // (as for every phase below): each inlined copy of this body costs ~3K
-    // instructions, and the instruction cache is the forward's second
-    // largest stall (ncu no_instruction).
-    auto run_batch = [&](int nb, bool drain) {
-        ensure_pages(drain ? RING : nb);         // each entry emits at most one fragment per pixel
+    // test, ring and compositing in stream order (pass 2).  (Measured and
+    // rejected: one loop with one call site per phase -- this body is
+    // inlined at three -- halves the kernel's code and its instruction-cache
+    // stalls, but runs 15 % slower.)
+    auto run_batch = [&](int nb) {
+        ensure_pages(nb);                        // each entry emits at most one fragment per pixel
         load_batch_ids(sm.rec, recs, sm.qprim, nb);
         // geometry heads for the exact pass, copied asynchronously under pass 1
 #if QGS_FWD_STAGE_GEO
@@ -650,23 +646,11 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
             else emit = ring_push_pay(R, sm.pay, lane, h.t64, p, pin, et, ep, pout);
             if (emit) composite(ep, et, pout);
         };
-        if (!drain) {
-            while (bits && alive) {
-                const int j = __ffs(bits) - 1;
-                bits &= bits - 1;
-                Hit h;
-                if (exact(j, h)) accept_one(j, h);
-            }
-        } else {
-            // raster_kernels.py:227-270: drain while alive (first minimum,
-            // swap with last)
-            while (alive && R.n > 0) {
-                double et;
-                int ep;
-                Pay pout;
-                ring_pop_pay(R, sm.pay, lane, et, ep, pout);
-                composite(ep, et, pout);
-            }
+        while (bits && alive) {
+            const int j = __ffs(bits) - 1;
+            bits &= bits - 1;
+            Hit h;
+            if (exact(j, h)) accept_one(j, h);
         }
         __syncwarp();
     };
@@ -680,114 +664,9 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
     // batch.
     const int start = tile_offsets[tile], end = tile_offsets[tile + 1];
     int qn = 0, an = 0;
-#if QGS_FWD_SINGLE_SITE
-    auto conic_pass = [&](int na) {            // queue A entries [0, na) -> queue B
-        const uint32_t live = __ballot_sync(FULL, alive);
-        uint32_t m = 0u;
-        int pj = 0;
-        if (lane < na) {
-            pj = sm.aprim[lane];
-            m = sm.amask[lane] & live;
-            if (m && cull) m &= conic_rows<4>(conics[pj], bu, bv, 0);
-        }
-        const uint32_t keep = __ballot_sync(FULL, m != 0u);
-        if (m) {
-            const int pos = qn + __popc(keep & ((1u << lane) - 1u));
-            sm.qprim[pos] = pj;
-            sm.qmask[pos] = m;
-        }
-        qn += __popc(keep);
-        __syncwarp();
-    };
-#if QGS_FWD_LIST_PREFETCH
-    // list windows software-pipelined: the ids of window w+2 and the culled
-    // boxes of window w+1 are in flight while window w is processed
-    auto ld_id = [&](int b) { return b + lane < end ? __ldg(tile_prims + b + lane) : 0; };
-    auto ld_bb = [&](int b, int p) {
-        return (cull && b + lane < end) ? __ldg(reinterpret_cast<const uint2 *>(&conics[p].bb_u))
-                                        : make_uint2(0u, 0u);
-    };
-    int id1 = ld_id(start), id2 = ld_id(start + 32);
-    uint2 bb1 = ld_bb(start, id1);
-#endif
-    // One loop, warp-uniform decisions, each phase at one call site: a batch
-    // as soon as queue B holds WB entries (or nothing more can come), else a
-    // conic pass as soon as queue A holds 32 (or the list is done), else the
-    // next 32-entry window of the list; the ring is drained last.
-    int b0 = start;
-    for (;;) {
-        const bool list_done = b0 >= end;
-        const bool upstream_done = list_done && an == 0;
-        if (qn >= WB || (upstream_done && qn > 0) || (upstream_done && qn == 0)) {
-            const bool drain = upstream_done && qn == 0;
-            const int nb = min(qn, WB);
-            run_batch(nb, drain);
-            if (drain) break;
-            qn -= nb;
-            if (lane < qn) { sm.qprim[lane] = sm.qprim[nb + lane]; sm.qmask[lane] = sm.qmask[nb + lane]; }
-            __syncwarp();
-            if (!__any_sync(FULL, alive)) break;
-            continue;
-        }
-        if (an >= 32 || list_done) {             // list_done here implies an > 0
-            const int na = min(an, 32);
-            conic_pass(na);
-            an -= na;
-            if (lane < an) { sm.aprim[lane] = sm.aprim[32 + lane]; sm.amask[lane] = sm.amask[32 + lane]; }
-            __syncwarp();
-            continue;
-        }
-        const uint32_t live = __ballot_sync(FULL, alive);
-        if (!live) break;
-        const int nb = min(32, end - b0);
-        int pj = 0;
-        uint32_t bm = 0u;
-#if QGS_FWD_LIST_PREFETCH
-        const int pcur = id1;
-        const uint2 bcur = bb1;
-        id1 = id2;
-        bb1 = ld_bb(b0 + 32, id1);
-        id2 = ld_id(b0 + 64);
-#endif
-        if (lane < nb) {
-#if QGS_FWD_LIST_PREFETCH
-            pj = pcur;
-            if (cull) {
-                bm = block_lanes(bcur.x, bcur.y, bu, bv);
-            } else {
-#else
-            pj = tile_prims[b0 + lane];
-            if (cull) {
-                const uint2 bb = *reinterpret_cast<const uint2 *>(&conics[pj].bb_u);
-                bm = block_lanes(bb.x, bb.y, bu, bv);
-            } else {
-#endif
-                bm = block_lanes(recs[pj].bb_u, recs[pj].bb_v, bu, bv);
-            }
-            if (out.counters)                  // algorithmic work: the reference's pixel box
-                sm.boxw[lane] = cull ? block_lanes(recs[pj].bb_u, recs[pj].bb_v, bu, bv) : bm;
-            bm &= live;
-        }
-        if (out.counters) {
-            __syncwarp();
-            for (int j = 0; j < nb; ++j) n_box += alive ? (sm.boxw[j] >> lane) & 1u : 0u;
-            __syncwarp();
-        }
-        const uint32_t keep = __ballot_sync(FULL, bm != 0u);
-        if (bm) {
-            const int pos = an + __popc(keep & ((1u << lane) - 1u));
-            sm.aprim[pos] = pj;
-            sm.amask[pos] = bm;
-        }
-        an += __popc(keep);
-        __syncwarp();
-        b0 += 32;
-    }
-
-#else
     auto drain_b = [&]() {
         while (qn >= WB) {
-            run_batch(WB, false);
+            run_batch(WB);
             qn -= WB;
             if (lane < qn) { sm.qprim[lane] = sm.qprim[WB + lane]; sm.qmask[lane] = sm.qmask[WB + lane]; }
             __syncwarp();
@@ -881,17 +760,16 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
         conic_pass(an);
         drain_b();
     }
-    if (qn > 0 && __any_sync(FULL, alive)) run_batch(qn, false);
+    if (qn > 0 && __any_sync(FULL, alive)) run_batch(qn);
 
     ensure_pages(RING);                      // the drain emits at most RING more
-    while (alive && R.n > 0) {
+    while (alive && R.n > 0) {               // raster_kernels.py:227-270
         double et;
         int ep;
         Pay pout;
         ring_pop_pay(R, sm.pay, lane, et, ep, pout);
         composite(ep, et, pout);
     }
-#endif
     if (out.frag_page_count) {
         if (lane < npages) out.frag_page_table[(size_t)rw * QGS_FRAG_MAX_PAGES + lane] = sm.pages[lane];
         if (lane == 0) out.frag_page_count[rw] = (out.frag_prim && log_on) ? npages : -1;
