@@ -3,33 +3,38 @@
 // Reference: raster_kernels.py:83-286 (forward_kernel), :289-502
 // (_grad_fragment), :505-670 (backward_kernel), :673-681 (merge).
 //
-// Work unit = one warp = one 8x4 block of a 16x16 tile (a tile is 8 such
-// blocks); each warp is its own CTA and streams its tile's depth-sorted list
-// independently -- no CTA barriers, and a warp stops as soon as its own 32
-// pixels have terminated.  The list is consumed in batches of 32 fp32
-// records staged in shared memory (8 lanes per 128-byte record, coalesced;
-// the 8 blocks of a tile hit the same lines in L2).
+// Work unit = one warp = one 8x4 block of a 16x16 tile (8 blocks per tile).
+// Warps never synchronise with each other: a forward CTA holds the 8 warps of
+// one tile (a backward CTA 4), only so that they share the SM's L1 for the
+// tile's list, boxes and records; each warp stops as soon as its own 32
+// pixels have terminated.  Tiles run heaviest first (tile_order_kernel).
 //
-// Forward, per batch:
-//   mask    lane j intersects record j's pixel box with the block -> a 32-bit
-//           lane mask, broadcast by shuffle; empty masks are skipped
-//   pass 1  coarse fp32 test (shade.cuh: coarse_roots) of every in-box
-//           candidate -> per-lane candidate bits
-//   pass 2  set bits in stream order: fp64 depth refinement + exact selection
-//           + alpha floor, the 8-entry min-depth ring and fp64 compositing of
-//           emitted fragments (re-shaded at their fp64 depth)
-//   record  accepted-lane mask of every streamed entry (ballot), stored
-//           block-major per tile, so the backward replays ONLY those
+// Forward, per block:
+//   pass 0  the tile's depth-sorted list streamed 32 entries per window, one
+//           per lane: culled pixel box against the block, then the screen
+//           conic test on all 32 pixels; survivors queue up in stream order
+//   batch   WB = 4 queued entries at a time: records staged in shared memory
+//           (8 lanes per 128-byte record), fp64 geometry heads by cp.async
+//   pass 1  coarse fp32 test (shade.cuh: coarse_stage1/2) of each pixel's
+//           culled-in candidates
+//   pass 2  set bits in stream order: fp64 depth refinement + exact
+//           selection + alpha floor (MODE_EXACT: decisions inside their fp32
+//           band re-made in fp64), the 8-entry min-depth ring, fp64
+//           compositing of emitted fragments
+//   log     every composited fragment (prim, fp64 depth, fp32 local hit
+//           point) appended to the paged fragment log
 //
 // Transmittance, blend weights and the eleven blend sums are fp64: the
 // backward's suffix sums (vtot - prefix, the front-to-back rewrite of
 // raster_kernels.py:340) are exact to ~1e-15.
 //
-// Backward: replays the recorded accepted candidates through the same ring
-// (same inline functions -> same fp64 depths and decisions) and reduces each
-// emitted fragment's 22 kernel-level gradient slots across lanes that emitted
-// the same primitive (match_any + shared-memory transpose) before one float
-// atomic per slot.
+// Backward: each pixel's logged fragments re-shaded in fp32 from the logged
+// hit point (grazing rays from the fp64 geometry), 16 kernel-level gradient
+// slots per fragment (ohat, the rotation accumulator's skew part, w, s,
+// alpha, colour), reduced across lanes that emitted the same primitive
+// (match_any + padded shared-memory transpose) into 16-byte vector atomics --
+// or, deterministic mode, written to rows for det_reduce.cu.  Blocks without
+// a log are replayed by a separate kernel with the forward's candidate test.
 #include <cuda_pipeline.h>
 
 #include "kernels.cuh"
