@@ -9,7 +9,9 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libqgs_b200.so")
+# QGS_LIB_VARIANT=debug: the bounds-checking build (tests/test_debug_checks.py)
+LIB_PATH = os.path.join(_HERE, "lib", "libqgs_b200_debug.so"
+                        if os.environ.get("QGS_LIB_VARIANT") == "debug" else "libqgs_b200.so")
 
 KG_STRIDE = 16
 AUX_PLANES = 12

@@ -16,6 +16,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "lib", "obj")
 LIB = os.path.join(HERE, "lib", "libqgs_b200.so")
+# the same sources with device bounds checks (QGS_DEBUG_CHECKS: a failed check
+# traps), loaded instead of LIB when QGS_LIB_VARIANT=debug (tests only)
+LIB_DEBUG = os.path.join(HERE, "lib", "libqgs_b200_debug.so")
 PEAKS_LIB = os.path.join(HERE, "lib", "libqgs_peaks.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
@@ -50,26 +53,41 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force=False, verbose=False):
-    os.makedirs(OBJ, exist_ok=True)
+def build(force=False, verbose=False, debug=None):
+    """the product library, and (debug, default unless QGS_BUILD_DEBUG=0) its
+    bounds-checking twin"""
+    if debug is None:
+        debug = os.environ.get("QGS_BUILD_DEBUG", "1") != "0"
+    _build(OBJ, LIB, [], force, verbose)
+    if debug:
+        _build(OBJ + "_debug", LIB_DEBUG, ["-DQGS_DEBUG_CHECKS=1"], force, verbose)
+    _build_peaks(force, verbose)
+    return LIB
+
+
+def _build(obj_dir, lib, defines, force, verbose):
+    os.makedirs(obj_dir, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in sorted(os.listdir(CSRC)) if h.endswith(".cuh")]
     hdrs.append(os.path.join(INCLUDE, "qgs_b200.h"))
     objs = []
     for unit, flags in UNITS.items():
         src = os.path.join(CSRC, unit)
-        obj = os.path.join(OBJ, unit.replace(".cu", ".o"))
+        obj = os.path.join(obj_dir, unit.replace(".cu", ".o"))
         objs.append(obj)
         if force or _stale(obj, [src] + hdrs):
             extra = os.environ.get("QGS_NVCC_EXTRA", "").split()   # experiments only
-            cmd = [nvcc(), *ARCH, *COMMON, *flags, *extra, "-c", src, "-o", obj]
+            cmd = [nvcc(), *ARCH, *COMMON, *flags, *defines, *extra, "-c", src, "-o", obj]
             if verbose:
                 print(" ".join(cmd))
             subprocess.check_call(cmd)
-    if force or _stale(LIB, objs):
-        cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs]
+    if force or _stale(lib, objs):
+        cmd = [nvcc(), *ARCH, "-shared", "-o", lib, *objs]
         if verbose:
             print(" ".join(cmd))
         subprocess.check_call(cmd)
+
+
+def _build_peaks(force, verbose):
     # measurement helper (not part of the product ABI): FP32 / MUFU peaks
     src = os.path.join(os.path.dirname(HERE), "tools", "peaks.cu")
     if os.path.exists(src) and (force or _stale(PEAKS_LIB, [src])):
@@ -77,7 +95,6 @@ def build(force=False, verbose=False):
         if verbose:
             print(" ".join(cmd))
         subprocess.check_call(cmd)
-    return LIB
 
 
 if __name__ == "__main__":

@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(256, QGS_KEY_MIN_BLOCKS)
 pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
                 const double *__restrict__ rays, int32_t *cursor, uint64_t *bucket)
 {
-    (void)n_pairs;
+    (void)n_pairs;                 // bounds checks of the debug build only
     __shared__ KeyPrim s_kp[8];
     const int lane = threadIdx.x & 31;
     const int warps = gridDim.x * (blockDim.x >> 5);
@@ -248,6 +248,7 @@ pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
                 nx = ray[0]; ny = ray[1]; nz = ray[2];
             }
             const double key = key_from_ray_fast(kp, cx, cy, cz, euclid, st.t_clip);
+            QGS_CHECK(slot >= 0 && slot < n_pairs);
             bucket[slot] = sort_composite(key, p, st.pbits);
             cx = nx; cy = ny; cz = nz;
         }
@@ -396,6 +397,7 @@ __device__ void sort_buckets(SortSmem &sm, const uint64_t *a, int base, int g0, 
         const int d = bf(sort_h(x));
         const int b0 = bucket_start(sm, d), b1 = sm.bend[d];
         const int r = b1 - b0 == 1 ? 0 : rank_fast(a, b0 - base, b1 - base, x, tile, pv, cam, st);
+        QGS_CHECK(r >= 0 && r < b1 - b0);
         out[b0 + r] = comp_prim(x, st.pbits);
     }
     __syncthreads();

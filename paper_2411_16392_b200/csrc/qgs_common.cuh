@@ -9,12 +9,33 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <mutex>
 #include <set>
 #include <utility>
 #include <cuda_runtime.h>
 
 #include "../../include/qgs_b200.h"
+
+// Device bounds checks of the debug build (libqgs_b200_debug.so, built with
+// -DQGS_DEBUG_CHECKS=1 by build.py; tests/test_debug_checks.py runs every
+// path under it): a failed check traps the kernel (cudaErrorLaunchFailure /
+// illegal instruction), which the host reports.  compute-sanitizer is not
+// available on the GPU pool, so these are the memory-safety net.
+#ifndef QGS_DEBUG_CHECKS
+#define QGS_DEBUG_CHECKS 0
+#endif
+#if QGS_DEBUG_CHECKS
+#define QGS_CHECK(cond)                                                                  \
+    do {                                                                                 \
+        if (!(cond)) {                                                                   \
+            printf("QGS_CHECK failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__);        \
+            __trap();                                                                    \
+        }                                                                                \
+    } while (0)
+#else
+#define QGS_CHECK(cond) do { } while (0)
+#endif
 
 namespace qgs {
 

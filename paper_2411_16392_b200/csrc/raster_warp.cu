@@ -244,6 +244,7 @@ struct Ring {
 __device__ __forceinline__ bool ring_push(Ring &R, double t, int prim, double &et, int &ep)
 {
     if (R.n < RING) {
+        QGS_CHECK(R.n >= 0);
         R.t[R.n * 32] = t;
         R.p[R.n * 32] = prim;
         R.n++;
@@ -479,6 +480,7 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
         if (lane == 0) base = atomicAdd(out.frag_pool_next, need - npages);
         base = __shfl_sync(FULL, base, 0);
         if (base + (need - npages) > out.frag_pool_pages) { log_on = false; return; }
+        QGS_CHECK(need <= QGS_FRAG_MAX_PAGES && base >= 0);
         if (lane < need - npages) sm.pages[npages + lane] = base + lane;
         npages = need;
         __syncwarp();
@@ -525,6 +527,8 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
         if (T > 0.5) median = (float)t;
         T *= 1.0 - abar64;
         if (log_on) {
+            QGS_CHECK(nfrag / QGS_FRAG_PAGE < npages);
+            QGS_CHECK(sm.pages[nfrag / QGS_FRAG_PAGE] < out.frag_pool_pages);
             const size_t o = ((size_t)sm.pages[nfrag / QGS_FRAG_PAGE] * QGS_FRAG_PAGE +
                               (nfrag % QGS_FRAG_PAGE)) * 32 + lane;
             out.frag_prim[o] = ep;
@@ -691,6 +695,7 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
         const uint32_t keep = __ballot_sync(FULL, m != 0u);
         if (m) {
             const int pos = qn + __popc(keep & ((1u << lane) - 1u));
+            QGS_CHECK(pos < WB + 32);
             sm.qprim[pos] = pj;
             sm.qmask[pos] = m;
         }
@@ -748,6 +753,7 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
         const uint32_t keep = __ballot_sync(FULL, bm != 0u);
         if (bm) {
             const int pos = an + __popc(keep & ((1u << lane) - 1u));
+            QGS_CHECK(pos < 64);
             sm.aprim[pos] = pj;
             sm.amask[pos] = bm;
         }
@@ -1159,6 +1165,7 @@ __device__ __forceinline__ void bwd_block(const PrimRec *__restrict__ recs,
     // deterministic mode: this pixel's k-th fragment owns row det_base + k
     const int64_t det_base = DET ? det.base[(size_t)rw * 32 + lane] : 0;
     int kf = 0;
+    const int nf_of_pixel = (QGS_DEBUG_CHECKS && inside) ? fwd.n_fragments[px] : 1 << 30;
     auto emit_grad = [&](bool emit, int ep, double t, bool have_xy, float lx, float ly) {
         float g[KG];
         if (emit) {
@@ -1198,6 +1205,7 @@ __device__ __forceinline__ void bwd_block(const PrimRec *__restrict__ recs,
 #pragma unroll
                 for (int q = 0; q < KG / 4; ++q)
                     dst[q] = make_float4(g[4 * q], g[4 * q + 1], g[4 * q + 2], g[4 * q + 3]);
+                QGS_CHECK(ep >= 0 && kf < nf_of_pixel);
                 det.prim[det_base + kf] = ep;
                 kf++;
             }
@@ -1228,6 +1236,7 @@ __device__ __forceinline__ void bwd_block(const PrimRec *__restrict__ recs,
             const int nf = alive ? fwd.n_fragments[px] : 0;
             const int nf_max = __reduce_max_sync(FULL, nf);
             // lane i holds the warp's i-th page id
+            QGS_CHECK(np <= QGS_FRAG_MAX_PAGES && nf_max <= np * QGS_FRAG_PAGE);
             const int my_page = lane < np ? fwd.frag_page_table[(size_t)rw * QGS_FRAG_MAX_PAGES + lane] : 0;
             auto slot = [&](int k) {
                 const int pg = __shfl_sync(FULL, my_page, k / QGS_FRAG_PAGE);

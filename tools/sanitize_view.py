@@ -1,6 +1,7 @@
-"""One small view through every path of the CUDA rasterizer, for
-compute-sanitizer (tools/sanitize.sh): prepare, forward (exact and fp32
-decisions), backward (atomics, deterministic, replay), chain, the exports.
+"""One small view through every path of the CUDA rasterizer: prepare,
+forward (exact and fp32 decisions, a page pool that runs dry), backward
+(atomics, deterministic, log and replay), chain, the exports.  Run with
+QGS_LIB_VARIANT=debug for the bounds-checking build (tests/test_debug_checks.py).
 
     python tools/sanitize_view.py [--config c1] [--n N] [--res R]
 """
@@ -27,12 +28,16 @@ if a.res:
     kw["res"] = a.res
 sc = scenes.CONFIGS[a.config](**kw)
 cam, up = sc.cams[0], sc.upstream[0]
+check = []
 for st in (rz.RenderSettings(), rz.RenderSettings(exact_decisions=False),
            rz.RenderSettings(deterministic=True), rz.RenderSettings(resort=False),
            rz.RenderSettings(euclidean_density=True, background=np.array([0.2, 0.3, 0.4]))):
     prep = rz.prepare(sc.prims, cam, st)
     tg = rz.forward(prep)
     g = rz.backward(prep, tg, up)
+    check.append(float(tg.color.double().sum()))          # the forward is deterministic
+    if st.deterministic:
+        check.append(float(g.centers.double().abs().sum()))
     tg.frag_prim = tg.frag_t = None           # replay path
     g2 = rz.backward(prep, tg, up)
     for f in ("R", "ohat", "M", "Nmat", "wv", "lam", "view_dirs", "view_dist", "clamped",
@@ -40,5 +45,15 @@ for st in (rz.RenderSettings(), rz.RenderSettings(exact_decisions=False),
         getattr(prep, f)
     prep.sorted_keys()
     prep.trace_pixel(cam.width // 2, cam.height // 2)
+# a fragment-log pool far too small: most blocks overflow -> replay
+prep = rz.prepare(sc.prims, cam)
+rz._FORCE_POOL_PAGES = 8
+try:
+    tg = rz.forward(prep)
+finally:
+    rz._FORCE_POOL_PAGES = None
+g3 = rz.backward(prep, tg, up)
 torch.cuda.synchronize()
-print("ok", prep.n_pairs, float(g.centers.abs().sum()), float(g2.centers.abs().sum()))
+from paper_2411_16392_b200 import _lib  # noqa: E402
+print("lib", os.path.basename(_lib.LIB_PATH))
+print("ok", prep.n_pairs, " ".join(f"{v:.17g}" for v in check))
