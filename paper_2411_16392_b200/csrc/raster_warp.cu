@@ -1165,7 +1165,9 @@ __device__ __forceinline__ void bwd_block(const PrimRec *__restrict__ recs,
     // deterministic mode: this pixel's k-th fragment owns row det_base + k
     const int64_t det_base = DET ? det.base[(size_t)rw * 32 + lane] : 0;
     int kf = 0;
-    const int nf_of_pixel = (QGS_DEBUG_CHECKS && inside) ? fwd.n_fragments[px] : 1 << 30;
+#if QGS_DEBUG_CHECKS
+    const int nf_of_pixel = inside ? fwd.n_fragments[px] : 0;
+#endif
     auto emit_grad = [&](bool emit, int ep, double t, bool have_xy, float lx, float ly) {
         float g[KG];
         if (emit) {

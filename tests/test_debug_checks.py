@@ -37,4 +37,9 @@ def test_every_path_under_bounds_checks(cuda_device, args):
     dbg = _run("debug", *args)
     assert "lib libqgs_b200_debug.so" in dbg
     ref = _run(None, *args)
-    assert dbg.splitlines()[-1] == ref.splitlines()[-1]      # same pair count and sums
+    # the same pair count and (deterministic) forward maps, bit for bit; the
+    # deterministic backward to rounding (the check branches change how the
+    # compiler contracts a few products)
+    assert dbg.splitlines()[-1] == ref.splitlines()[-1]
+    d, r = (float(ln.split()[1]) for ln in (dbg.splitlines()[-2], ref.splitlines()[-2]))
+    assert abs(d - r) <= 1e-6 * abs(r)

@@ -28,7 +28,7 @@ if a.res:
     kw["res"] = a.res
 sc = scenes.CONFIGS[a.config](**kw)
 cam, up = sc.cams[0], sc.upstream[0]
-check = []
+check, det = [], []
 for st in (rz.RenderSettings(), rz.RenderSettings(exact_decisions=False),
            rz.RenderSettings(deterministic=True), rz.RenderSettings(resort=False),
            rz.RenderSettings(euclidean_density=True, background=np.array([0.2, 0.3, 0.4]))):
@@ -37,7 +37,7 @@ for st in (rz.RenderSettings(), rz.RenderSettings(exact_decisions=False),
     g = rz.backward(prep, tg, up)
     check.append(float(tg.color.double().sum()))          # the forward is deterministic
     if st.deterministic:
-        check.append(float(g.centers.double().abs().sum()))
+        det.append(float(g.centers.double().abs().sum()))
     tg.frag_prim = tg.frag_t = None           # replay path
     g2 = rz.backward(prep, tg, up)
     for f in ("R", "ohat", "M", "Nmat", "wv", "lam", "view_dirs", "view_dist", "clamped",
@@ -56,4 +56,5 @@ g3 = rz.backward(prep, tg, up)
 torch.cuda.synchronize()
 from paper_2411_16392_b200 import _lib  # noqa: E402
 print("lib", os.path.basename(_lib.LIB_PATH))
+print("det", " ".join(f"{v:.17g}" for v in det))
 print("ok", prep.n_pairs, " ".join(f"{v:.17g}" for v in check))
