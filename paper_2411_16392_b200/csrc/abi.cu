@@ -73,8 +73,6 @@ int configure()
 {
     QGS_CK(qgs::ensure_smem_attr(reinterpret_cast<const void *>(qgs::tile_sort_kernel),
                                  (int)qgs::sort_smem_bytes()));
-    QGS_CK(qgs::ensure_smem_attr(reinterpret_cast<const void *>(qgs::tile_sort_res_kernel),
-                                 (int)qgs::sort_res_smem_bytes()));
     return 0;
 }
 
@@ -176,17 +174,10 @@ int qgs_bin(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settin
     // last would be the kernel's tail
     qgs::tile_order_kernel<<<1, 1024, qgs::ORDER_SMEM, s>>>(tile_offsets, n_tiles, ws.order, 1);
     QGS_LAUNCHED("tile_order_kernel (sort)");
-#ifndef QGS_NO_RES_SORT
-    sk.res_sort = 1;
-#endif
     qgs::tile_sort_kernel<<<n_tiles, qgs::sort_threads(), qgs::sort_smem_bytes(), s>>>(
         tile_offsets, ws.bucket, ws.tmp, pv, ck, sk, tile_prims, ws.order);
     QGS_LAUNCHED("tile_sort_kernel");
-    if (sk.res_sort) {          // the tiles that fit in shared memory, one HBM read each
-        qgs::tile_sort_res_kernel<<<n_tiles, qgs::sort_res_threads(), qgs::sort_res_smem_bytes(), s>>>(
-            tile_offsets, ws.bucket, pv, ck, sk, tile_prims);
-        QGS_LAUNCHED("tile_sort_res_kernel");
-    }
+
     return 0;
 }
 

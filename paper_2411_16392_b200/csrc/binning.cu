@@ -269,14 +269,6 @@ pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
 //      lexsort((prim, key, tile)).  Tiles larger than shared memory are
 //      staged in L2 and ranked in groups of whole buckets loaded into
 //      shared memory.
-#ifndef QGS_SORT_RES_N
-#define QGS_SORT_RES_N 18944
-#endif
-#ifndef QGS_SORT_RES_T
-#define QGS_SORT_RES_T 1024
-#endif
-constexpr int SORT_RES_T = QGS_SORT_RES_T;
-constexpr int SORT_RES_N = QGS_SORT_RES_N;
 #ifndef QGS_SORT_T
 #define QGS_SORT_T 512
 #endif
@@ -464,7 +456,7 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
     SortSmem &sm = *reinterpret_cast<SortSmem *>(smem_raw);
     const int tile = order ? order[blockIdx.x] : (int)blockIdx.x;
     const int start = tile_offsets[tile], n = tile_offsets[tile + 1] - start;
-    if (n == 0 || (st.res_sort && n <= SORT_RES_N)) return;   // tile_sort_res_kernel has it
+    if (n == 0) return;
     const int lane = threadIdx.x & 31;
     const uint64_t *src = keys + start;
     int32_t *out = tile_prims + start;
@@ -639,193 +631,6 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
         }
     }
 }
-
-// ------------------------------------------- shared-memory-resident sort
-//
-// Tiles of up to SORT_RES_N entries (most of C2/C3's) sorted by one 1024-
-// thread CTA entirely in shared memory: the tile's composites are read from
-// HBM ONCE (every load of the pass in flight), the key range and the bucket
-// histogram come from shared memory, and the bucket scatter moves 16-bit
-// indices rather than the 64-bit composites (so a ~19K-entry tile fits in the
-// 227 KB); ranks inside buckets read the composites through the indices.
-// Same buckets, same in-bucket ranking (composite compare, exact fp64 key
-// for equal prefixes) and the same sample-sort buckets for clustered depths
-// as tile_sort_kernel, which keeps the larger tiles.
-constexpr int SORT_RES_NB = 4096;                // most buckets (a multiple of SORT_RES_T)
-constexpr int SORT_RES_SPLIT = 2047;             // most splitters (a sample of 2048)
-
-struct SortResSmem {
-    uint64_t key[SORT_RES_N];                    // the tile's composites, load order
-    uint16_t idx[SORT_RES_N];                    // bucket-grouped permutation of key
-    int bend[SORT_RES_NB];                       // counts -> cursors -> bucket ends
-    uint32_t split[SORT_RES_SPLIT + 1];          // sample splitters (clustered tiles)
-    int scan_w[32];
-    uint32_t kmin, kmax;
-    int maxcnt;
-};
-
-// rank of x among key[idx[b0 .. b1)] (rank_fast / rank_in_bucket through the
-// index permutation)
-__device__ __forceinline__ int rank_res(const SortResSmem &sm, int b0, int b1, uint64_t x,
-                                        int tile, const PrepView &pv, const CamK &cam,
-                                        const SetK &st)
-{
-    const int pb = st.pbits;
-    const uint64_t h = x >> pb;
-    int r = 0;
-    bool eq = false;
-    for (int j = b0; j < b1; ++j) {
-        const uint64_t y = sm.key[sm.idx[j]];
-        r += y < x ? 1 : 0;
-        eq |= ((y >> pb) == h) & (y != x);
-    }
-    if (!eq) return r;
-    const int p = comp_prim(x, pb);
-    const double kx = key64_of(x, tile, pv, cam, st);
-    r = 0;
-    for (int j = b0; j < b1; ++j) {
-        const uint64_t y = sm.key[sm.idx[j]];
-        const uint64_t hy = y >> pb;
-        if (hy < h) {
-            ++r;
-        } else if (hy == h && y != x) {
-            const double ky = key64_of(y, tile, pv, cam, st);
-            r += (ky < kx || (ky == kx && comp_prim(y, pb) < p)) ? 1 : 0;
-        }
-    }
-    return r;
-}
-
-__global__ void __launch_bounds__(SORT_RES_T, 1)
-tile_sort_res_kernel(const int32_t *__restrict__ tile_offsets, const uint64_t *__restrict__ keys,
-                     PrepView pv, CamK cam, SetK st, int32_t *tile_prims)
-{
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    SortResSmem &sm = *reinterpret_cast<SortResSmem *>(smem_raw);
-    const int tile = (int)blockIdx.x;
-    const int start = tile_offsets[tile], n = tile_offsets[tile + 1] - start;
-    if (n == 0 || n > SORT_RES_N) return;        // larger tiles: tile_sort_kernel
-    const uint64_t *src = keys + start;
-    int32_t *out = tile_prims + start;
-    if (n == 1) {
-        if (threadIdx.x == 0) out[0] = comp_prim(src[0], st.pbits);
-        return;
-    }
-    const int lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) { sm.kmin = 0xffffffffu; sm.kmax = 0u; sm.maxcnt = 0; }
-    // 1. the tile's composites into shared memory (one HBM read), key range
-    uint32_t lmin = 0xffffffffu, lmax = 0u;
-#pragma unroll 4
-    for (int i = threadIdx.x; i < n; i += SORT_RES_T) {
-        const uint64_t v = src[i];
-        sm.key[i] = v;
-        const uint32_t h = sort_h(v);
-        lmin = min(lmin, h); lmax = max(lmax, h);
-    }
-    for (int o = 16; o; o >>= 1) {
-        lmin = min(lmin, __shfl_xor_sync(0xffffffffu, lmin, o));
-        lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
-    }
-    int nb = 64;
-    while (nb < SORT_RES_NB && nb * 2 < n) nb <<= 1;
-    for (int d = threadIdx.x; d < nb; d += SORT_RES_T) sm.bend[d] = 0;
-    __syncthreads();
-    if (lane == 0) { atomicMin(&sm.kmin, lmin); atomicMax(&sm.kmax, lmax); }
-    __syncthreads();
-    const uint32_t kmin = sm.kmin, range = sm.kmax - sm.kmin;
-    int shift = 0;
-    while ((range >> shift) >= (uint32_t)nb) ++shift;
-    // 2. histogram
-    for (int i = threadIdx.x; i < n; i += SORT_RES_T)
-        atomicAdd(&sm.bend[(sort_h(sm.key[i]) - kmin) >> shift], 1);
-    __syncthreads();
-    BucketFn bf{kmin, shift, nullptr, 0};
-    {
-        int mx = 0;
-        for (int d = threadIdx.x; d < nb; d += SORT_RES_T) mx = max(mx, sm.bend[d]);
-        mx = __reduce_max_sync(0xffffffffu, mx);
-        if (lane == 0) atomicMax(&sm.maxcnt, mx);
-    }
-    __syncthreads();
-    if (sm.maxcnt > SORT_SKEW && n >= 512) {
-        // clustered depths: sample-sort buckets (S evenly spaced keys of the
-        // tile, bitonic-sorted; the S - 1 upper ones are the splitters)
-        int S = 256;
-        while (S < SORT_RES_SPLIT + 1 && 4 * S <= n) S <<= 1;
-        uint32_t *smp = sm.split;
-        for (int i = threadIdx.x; i < S; i += SORT_RES_T) smp[i] = sort_h(sm.key[(size_t)i * n / S]);
-        __syncthreads();
-        for (int k = 2; k <= S; k <<= 1)
-            for (int j = k >> 1; j > 0; j >>= 1) {
-                for (int i = threadIdx.x; i < S; i += SORT_RES_T) {
-                    const int l = i ^ j;
-                    if (l > i) {
-                        const uint32_t a = smp[i], b = smp[l];
-                        const bool up = (i & k) == 0;
-                        if ((a > b) == up) { smp[i] = b; smp[l] = a; }
-                    }
-                }
-                __syncthreads();
-            }
-        // splitters = smp[1 .. S): shift down by one in place
-        uint32_t carry = 0;
-        for (int i0 = 0; i0 < S; i0 += SORT_RES_T) {
-            const int i = i0 + threadIdx.x;
-            if (i + 1 < S) carry = smp[i + 1];
-            __syncthreads();
-            if (i + 1 < S) smp[i] = carry;
-            __syncthreads();
-        }
-        nb = S;
-        bf.sp = smp;
-        bf.ns = S - 1;
-        for (int d = threadIdx.x; d < nb; d += SORT_RES_T) sm.bend[d] = 0;
-        __syncthreads();
-        for (int i = threadIdx.x; i < n; i += SORT_RES_T) atomicAdd(&sm.bend[bf(sort_h(sm.key[i]))], 1);
-        __syncthreads();
-    }
-    // 3. exclusive scan of the bucket counts (nb <= 4096: 4 per thread)
-    {
-        constexpr int PER = SORT_RES_NB / SORT_RES_T;
-        int c[PER], sum = 0;
-#pragma unroll
-        for (int q = 0; q < PER; ++q) {
-            const int d = threadIdx.x * PER + q;
-            c[q] = d < nb ? sm.bend[d] : 0;
-            sum += c[q];
-        }
-        int tot;
-        int ex = block_exclusive_scan<int>(sum, sm.scan_w, tot);
-#pragma unroll
-        for (int q = 0; q < PER; ++q) {
-            const int d = threadIdx.x * PER + q;
-            if (d < nb) sm.bend[d] = ex;
-            ex += c[q];
-        }
-    }
-    __syncthreads();
-    // 4. scatter the indices into their buckets (order inside a bucket is
-    // irrelevant: every item ranks itself)
-    for (int i = threadIdx.x; i < n; i += SORT_RES_T) {
-        const int pos = atomicAdd(&sm.bend[bf(sort_h(sm.key[i]))], 1);
-        QGS_CHECK(pos >= 0 && pos < n);
-        sm.idx[pos] = (uint16_t)i;
-    }
-    __syncthreads();
-    // 5. every item ranks itself inside its bucket
-    for (int i = threadIdx.x; i < n; i += SORT_RES_T) {
-        const uint64_t x = sm.key[i];
-        const int d = bf(sort_h(x));
-        const int b0 = d == 0 ? 0 : sm.bend[d - 1], b1 = sm.bend[d];
-        const int r = b1 - b0 == 1 ? 0 : rank_res(sm, b0, b1, x, tile, pv, cam, st);
-        QGS_CHECK(r >= 0 && r < b1 - b0);
-        out[b0 + r] = comp_prim(x, st.pbits);
-    }
-}
-
-size_t sort_res_smem_bytes() { return sizeof(SortResSmem); }
-int sort_res_max_items() { return SORT_RES_N; }
-int sort_res_threads() { return SORT_RES_T; }
 
 // -------------------------------------------------------- debug / unit
 

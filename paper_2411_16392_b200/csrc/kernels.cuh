@@ -35,12 +35,7 @@ __global__ void tile_keys_f64_kernel(int64_t n, const int64_t *pair_tiles,
                                      const double *M, const double *wv, const double *sv,
                                      const uint8_t *planar, const double *vu, const double *vv,
                                      const double *dist, CamK cam, SetK st, double *keys);
-__global__ void tile_sort_res_kernel(const int32_t *tile_offsets, const uint64_t *keys, PrepView pv,
-                                     CamK cam, SetK st, int32_t *tile_prims);
 size_t sort_smem_bytes();
-size_t sort_res_smem_bytes();
-int sort_res_max_items();
-int sort_res_threads();
 int sort_threads();                 // binning.cu SORT_T
 
 // det_reduce.cu (RenderSettings.deterministic): fragment (pixel, k) of the

@@ -169,7 +169,6 @@ struct SetK {
     double t_clip, alpha_floor, alpha_clamp, t_term;
     int resort, euclid, no_cull, exact;
     int pbits;            // bits of the primitive id in the sort composite (qgs_bin)
-    int res_sort;         // qgs_bin: tiles up to sort_res_max_items() sorted in shared memory
 };
 
 inline CamK make_camk(const qgs_camera &c)
@@ -193,7 +192,6 @@ inline SetK make_setk(const qgs_settings &s)
     k.resort = s.resort; k.euclid = s.euclidean_density; k.no_cull = s.no_cull;
     k.exact = s.exact_decisions;
     k.pbits = 32;
-    k.res_sort = 0;
     return k;
 }
 
