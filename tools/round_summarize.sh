@@ -1,5 +1,5 @@
 # usage: bash tools/round_summarize.sh TAG  (here, after round_profile.sh ran on the GPU box)
-TAG=${1:-r01}
+TAG=${1:-r02}
 set -e
 tail -1 gpurun_out/${TAG}_bench.log > profiles/${TAG}_bench_c3.json
 python tools/ncu_summary.py gpurun_out/${TAG}_full.ncu-rep . --json profiles/${TAG}_traffic.json > profiles/${TAG}_ncu_summary.txt
