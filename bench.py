@@ -47,19 +47,24 @@ def _kg_stride():
     return _lib.KG_STRIDE
 
 
-def traffic_bytes(kernel):
+def traffic_bytes(kernel, exact=True):
     """DRAM bytes (read + write) per launch of `kernel` from the newest committed
     `ncu --set full` capture (profiles/*_traffic.json, tools/round_summarize.sh),
-    or None.  One launch = one view here, like the roofline's achieved figure."""
+    or None.  One launch = one view here, like the roofline's achieved figure.
+    The forward of the exact-decision mode is raster_fwd_exact_kernel."""
     import glob
     files = sorted(glob.glob(os.path.join(HERE, "profiles", "*_traffic.json")))
     if not files:
         return None
     with open(files[-1]) as f:
         t = json.load(f)
-    e = t.get(kernel + "_kernel")
-    return None if e is None else {"bytes_per_launch": e["dram_bytes"],
-                                   "source": os.path.relpath(files[-1], HERE)}
+    names = [kernel + "_exact_kernel", kernel + "_kernel"] if exact else [kernel + "_kernel"]
+    for nm in names:
+        e = t.get(nm)
+        if e is not None:
+            return {"bytes_per_launch": e["dram_bytes"], "kernel": nm,
+                    "source": os.path.relpath(files[-1], HERE)}
+    return None
 
 
 def hbm_view(traffic, t_launch_s, peaks):
@@ -294,11 +299,14 @@ def run_ours(a):
         "roof_frac": max(F / P32, S / PSF) / t_k,
         "kernel_ms_per_step": kms, "fwd_ms_per_step": fwd_ms, "bwd_ms_per_step": bwd_ms,
         "fwd_ms_per_step_in_pipeline": fwd_ms_step, "bwd_ms_per_step_in_pipeline": bwd_ms_step,
-        "traffic": traffic_bytes(dom),
+        # dram__bytes_read + dram__bytes_write per launch (one view) of the
+        # dominant kernel from the committed ncu --set full capture
+        "traffic": (traffic_bytes(dom, st.exact_decisions) or {}).get("bytes_per_launch"),
+        "traffic_source": traffic_bytes(dom, st.exact_decisions),
         # the contract's HBM view of the same kernel: its DRAM bytes per launch
         # (ncu) over its measured launch time, against MEASURED_PEAKS' copy
         # bandwidth -- small, because the raster is FP32/SFU-bound, not HBM
-        "hbm_view": hbm_view(traffic_bytes(dom), t_k / max(len(mine), 1), peaks),
+        "hbm_view": hbm_view(traffic_bytes(dom, st.exact_decisions), t_k / max(len(mine), 1), peaks),
         "peak_source": f"fp32/mufu measured live (tools/peaks.cu); hbm {peaks_kind} "
                        f"MEASURED_PEAKS.json {peaks['hbm_gbs']} GB/s",
         "step_roofline_ms": T_roof * 1e3,
