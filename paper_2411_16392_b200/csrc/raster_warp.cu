@@ -59,6 +59,9 @@ namespace qgs {
 #ifndef QGS_WB
 #define QGS_WB 4
 #endif
+#ifndef QGS_UTIL_COUNTERS
+#define QGS_UTIL_COUNTERS 0        // diagnostics build: lane utilisation of passes 1 and 2
+#endif
 #ifndef QGS_FWD_RAY_REGS
 #define QGS_FWD_RAY_REGS 1    // fp64 pixel ray in registers instead of shared memory
 #endif
@@ -464,6 +467,9 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
     double last_t = -1.0e300;
     int nfrag = 0, viol = 0;
     unsigned n_box = 0, n_acc = 0, n_cand = 0, n_coarse = 0;
+#if QGS_UTIL_COUNTERS
+    unsigned long long u_p1 = 0, u_p2 = 0;        // diagnostics: pass-1 / pass-2 lane slots
+#endif
     Ring R{&sm.ring_t[0][lane], &sm.ring_p[0][lane], 0};
     bool alive = inside;
     // paged fragment log (qgs_targets): warp-uniform page count, pages taken
@@ -578,6 +584,9 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
             uni &= uni - 1;
             const int j1 = uni ? __ffs(uni) - 1 : j;
             uni &= uni - 1;
+#if QGS_UTIL_COUNTERS
+            u_p1 += (j1 != j) ? 2 : 1;
+#endif
             const bool a0 = (cand >> j) & 1u, a1 = j1 != j && ((cand >> j1) & 1u);
             if (!(a0 || a1)) continue;
             float r0[2], r1[2], hx0, hy0, hx1, hy1;
@@ -655,6 +664,9 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
             else emit = ring_push_pay(R, sm.pay, lane, h.t64, p, pin, et, ep, pout);
             if (emit) composite(ep, et, pout);
         };
+#if QGS_UTIL_COUNTERS
+        u_p2 += __reduce_max_sync(FULL, alive ? (unsigned)__popc(bits) : 0u);
+#endif
         while (bits && alive) {
             const int j = __ffs(bits) - 1;
             bits &= bits - 1;
@@ -844,6 +856,10 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
             atomicAdd(&out.counters[2], (unsigned long long)nfrag);
             atomicAdd(&out.counters[3], (unsigned long long)n_cand);
             atomicAdd(&out.counters[4], (unsigned long long)n_coarse);
+#if QGS_UTIL_COUNTERS
+            atomicAdd(&out.counters[5], 32ull * u_p1);     // lane slots of pass 1 (per candidate)
+            atomicAdd(&out.counters[6], 32ull * u_p2);     // lane slots of pass 2
+#endif
         }
     }
 }

@@ -1,6 +1,6 @@
 """Print a JSON parity report of the GPU path vs the float64 oracle.
 
-    python tools/parity_report.py [--scenes c1,c2] [--views 1] [--out FILE] [--exact]
+    python tools/parity_report.py [--scenes c1,c2] [--views 1] [--out FILE] [--fp32-decisions]
 
 Golden fixtures are compared against the reference outputs stored in them;
 generated configs (c1..c5, optionally shrunk with --n/--res) are compared
@@ -23,7 +23,7 @@ from paper_2411_16392_b200 import rasterizer as rz, scenes  # noqa: E402
 from tests import golden_io, parity  # noqa: E402
 
 
-EXACT = "--exact" in sys.argv          # settings.exact_decisions
+EXACT = "--fp32-decisions" not in sys.argv    # settings.exact_decisions (the default)
 
 
 def gpu_run(prims, cam, st, up):
@@ -89,7 +89,8 @@ def main():
     ap.add_argument("--scenes", default="golden,c1,c2")
     ap.add_argument("--views", type=int, default=1)
     ap.add_argument("--out", default=None)
-    ap.add_argument("--exact", action="store_true", help="settings.exact_decisions")
+    ap.add_argument("--fp32-decisions", action="store_true",
+                    help="RenderSettings(exact_decisions=False)")
     a = ap.parse_args()
     report = []
     for s in a.scenes.split(","):
