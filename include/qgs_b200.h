@@ -231,6 +231,11 @@ int qgs_export_prep_geometry(const qgs_params *prims, const void *prep, const qg
  * (cameras.py:53-59, the reference's operation order), H*W*3 f64. */
 int qgs_pixel_dirs(const qgs_camera *cam, double *dirs, qgs_stream_t stream);
 
+/* Diagnostics build counters (QGS_UTIL_COUNTERS; 0 entries otherwise): copies
+ * and clears up to n of [float64 band re-decisions, near-tangent roots decided
+ * by the fp64 closed form].  Returns the number copied. */
+int qgs_diag_counters(unsigned long long *out, int n);
+
 /* Diagnostics: replay one pixel's fragment stream (same device functions as
  * the raster kernels) and record up to `max` accepted candidates (tile-list
  * order) and emitted fragments (compositing order, with T before each).

@@ -157,6 +157,7 @@ def load():
         "qgs_multiview_loss": (ctypes.c_int, [P(MvMaps), P(Camera), P(MvMaps), P(Camera),
                                               P(MvConfig), f64, P(MvGrads), P(MvGrads), vp, vp,
                                               ctypes.c_size_t, vp]),
+        "qgs_diag_counters": (ctypes.c_int, [vp, i32]),
         "qgs_last_error": (ctypes.c_char_p, []),
         "qgs_version": (ctypes.c_int, []),
     }
@@ -175,7 +176,7 @@ EXPORTS = ("qgs_prep_bytes", "qgs_preprocess", "qgs_bin_workspace_bytes", "qgs_b
            "qgs_loss_photometric", "qgs_loss_distortion", "qgs_depth_to_normal",
            "qgs_loss_normal_consistency", "qgs_adam_step", "qgs_densify_workspace_bytes",
            "qgs_densify_plan", "qgs_densify_apply", "qgs_reset_opacity",
-           "qgs_multiview_workspace_bytes", "qgs_multiview_loss", "qgs_last_error",
+           "qgs_multiview_workspace_bytes", "qgs_multiview_loss", "qgs_diag_counters", "qgs_last_error",
            "qgs_version")
 
 

@@ -90,6 +90,12 @@ int check_cam(const qgs_camera *cam)
 extern "C" {
 
 const char *qgs_last_error(void) { return g_err.c_str(); }
+
+int qgs_diag_counters(unsigned long long *out, int n)
+{
+    if (!out || n < 0) return fail(QGS_E_ARG, "NULL argument");
+    return qgs::diag_counters(out, n);
+}
 int qgs_version(void) { return 1; }
 
 size_t qgs_prep_bytes(int32_t P)

@@ -90,6 +90,7 @@ constexpr int RASTER_BLOCKS_PER_TILE = 8;
 constexpr int FWD_WPC = QGS_FWD_WPC;
 constexpr int BWD_WPC = QGS_BWD_WPC;
 size_t fwd_smem_per_warp();
+int diag_counters(unsigned long long *out, int n);
 size_t bwd_smem_per_warp();
 
 }  // namespace qgs

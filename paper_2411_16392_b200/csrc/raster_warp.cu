@@ -1390,6 +1390,21 @@ raster_bwd_det_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict_
 }
 
 size_t fwd_smem_per_warp() { return sizeof(FwdSmem); }
+
+// diagnostics build (QGS_UTIL_COUNTERS): copy and clear the device counters
+int diag_counters(unsigned long long *out, int n)
+{
+#if QGS_UTIL_COUNTERS
+    if (n > 4) n = 4;
+    if (cudaMemcpyFromSymbol(out, qgs_diag, sizeof(unsigned long long) * n) != cudaSuccess) return -1;
+    const unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(qgs_diag, z, sizeof(z));
+    return n;
+#else
+    (void)out; (void)n;
+    return 0;
+#endif
+}
 size_t bwd_smem_per_warp() { return sizeof(BwdSmem); }
 
 // ===================================================== raster schedule

@@ -234,9 +234,21 @@ constexpr float FLOOR_BAND = 1e-4f;        // alpha G >= alpha_floor
 // ellipse pre-reject, l <= 3 sigma; raster_kernels.py:58-60: alpha floor)
 // from the primitive's float64 geometry in global memory.  Bit 0: the root
 // is selected; bit 1: and its weight passes the floor.  Out of line.
+#ifndef QGS_UTIL_COUNTERS
+#define QGS_UTIL_COUNTERS 0
+#endif
+#if QGS_UTIL_COUNTERS
+// diagnostics build: [0] exact64 calls (band cases), [1] near-tangent roots
+// decided by the fp64 closed form; read by tools/lane_util_fwd.py
+__device__ unsigned long long qgs_diag[4];
+#endif
+
 static __device__ __noinline__ unsigned exact64(const Geo64 *gp, const double dh[3], double t64,
                                                 bool planar, bool euclid, double floor)
 {
+#if QGS_UTIL_COUNTERS
+    atomicAdd(&qgs_diag[0], 1ull);
+#endif
     const Geo64 &g = *gp;
     const double x = g.ohat[0] + t64 * dh[0], y = g.ohat[1] + t64 * dh[1];
     const double s1 = g.sv[0], s2 = g.sv[1], s3 = g.sv[2];
@@ -312,6 +324,9 @@ static __device__ __noinline__ double marginal_root(const PrimRec &r, const Geo6
                                                     const Geo64 *gfull, const double d64[3],
                                                     bool euclid, float t_clip)
 {
+#if QGS_UTIL_COUNTERS
+    atomicAdd(&qgs_diag[1], 1ull);
+#endif
     double dh[3];
     local_dir64(g, d64, dh);
     const double w1 = g.wv[0], w2 = g.wv[1], iw3 = g.wv[2];
