@@ -309,9 +309,11 @@ __device__ __noinline__ double key64_of(uint64_t v, int tile, const PrepView &pv
 // with a smaller f32 key, plus items with the same f32 key that precede it in
 // (fp64 key, prim) order.  Composites are distinct (prim ids are), and equal
 // f32 keys are rare, so the fp64 keys are recomputed only for those.
-__device__ __forceinline__ int rank_in_bucket(const uint64_t *a, int b0, int b1, uint64_t x,
-                                              int tile, const PrepView &pv, const CamK &cam,
-                                              const SetK &st)
+// (the rare tie path, out of line: its fp64 key calls would otherwise set the
+// register allocation -- and the spills -- of the whole sort kernel)
+__device__ __noinline__ int rank_in_bucket(const uint64_t *a, int b0, int b1, uint64_t x,
+                                           int tile, const PrepView &pv, const CamK &cam,
+                                           const SetK &st)
 {
     const int pb = st.pbits;
     const uint64_t h = x >> pb;
@@ -549,23 +551,27 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
         for (int i = threadIdx.x; i < n; i += SORT_T) atomicAdd(&sm.bend[bf(sort_h(src[i]))], 1);
         __syncthreads();
     }
-    // exclusive scan of the bucket counts (nb <= 8192 = 16 per thread)
+    // exclusive scan of the bucket counts (nb <= 8192 = 16 per thread; the
+    // thread's counts are re-read from shared memory rather than held in 16
+    // registers -- the kernel runs at 64 and spilled)
     {
         constexpr int PER = SORT_MAX_BUCKETS / SORT_T;
-        int c[PER], sum = 0;
-#pragma unroll
+        int sum = 0;
+#pragma unroll 4
         for (int q = 0; q < PER; ++q) {
             const int d = threadIdx.x * PER + q;
-            c[q] = d < nb ? sm.bend[d] : 0;
-            sum += c[q];
+            sum += d < nb ? sm.bend[d] : 0;
         }
         int tot;
         int ex = block_exclusive_scan<int>(sum, sm.scan_w, tot);
-#pragma unroll
+#pragma unroll 4
         for (int q = 0; q < PER; ++q) {
             const int d = threadIdx.x * PER + q;
-            if (d < nb) sm.bend[d] = ex;
-            ex += c[q];
+            if (d < nb) {
+                const int c = sm.bend[d];
+                sm.bend[d] = ex;
+                ex += c;
+            }
         }
     }
     __syncthreads();

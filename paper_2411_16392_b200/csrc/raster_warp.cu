@@ -872,7 +872,11 @@ raster_fwd_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ ge
     fwd_block<MODE_FAST>(recs, geo, conics, tile_offsets, tile_prims, cam, st, out, -1);
 }
 
+#ifdef QGS_FWD_EXACT_MAXNREG
+__global__ void __maxnreg__(QGS_FWD_EXACT_MAXNREG)
+#else
 __global__ void __launch_bounds__(32 * FWD_WPC, QGS_FWD_EXACT_MIN_BLOCKS / FWD_WPC)
+#endif
 raster_fwd_exact_kernel(const PrimRec *__restrict__ recs, const Geo64 *__restrict__ geo,
                         const ConicRec *__restrict__ conics, const int32_t *__restrict__ tile_offsets,
                         const int32_t *__restrict__ tile_prims, CamK cam, SetK st, qgs_targets out)
