@@ -314,55 +314,41 @@ __device__ __forceinline__ bool alpha_pass(const PrimRec &r, const Geo64 *gfull,
 }
 
 // Near-tangent rays: the fp32 discriminant is within its rounding band of
-// zero, so root existence is decided in fp64 with the reference's own closed
-// form (intersect.py:39-55).  Rare, so kept out of line; it returns only the
-// accepted root (or -1) -- the caller re-confirms it inline, so its Hit stays
-// in registers (a Hit passed by address to an out-of-line call would live in
-// local memory on the hot path).
-template <int M>
-static __device__ __noinline__ double marginal_root(const PrimRec &r, const Geo64 &g,
-                                                    const Geo64 *gfull, const double d64[3],
-                                                    bool euclid, float t_clip)
+// zero, so the roots come from the reference's own fp64 closed form
+// (intersect.py:39-55).  Out of line and a leaf (geometry by pointer, the
+// local ray by value, the roots back in registers): the caller confirms the
+// roots with the same inline code as every other candidate.
+struct Roots2 {
+    double r0, r1;
+    int cnt;
+};
+
+static __device__ __noinline__ Roots2 marginal_roots(const Geo64 *gp, double dh0, double dh1,
+                                                     double dh2)
 {
 #if QGS_UTIL_COUNTERS
     atomicAdd(&qgs_diag[1], 1ull);
 #endif
-    double dh[3];
-    local_dir64(g, d64, dh);
+    const Geo64 &g = *gp;
     const double w1 = g.wv[0], w2 = g.wv[1], iw3 = g.wv[2];
     const double ox = g.ohat[0], oy = g.ohat[1], oz = g.ohat[2];
-    const double A = w1 * dh[0] * dh[0] + w2 * dh[1] * dh[1];
-    const double B = 2.0 * (w1 * ox * dh[0] + w2 * oy * dh[1]) - iw3 * dh[2];
+    const double A = w1 * dh0 * dh0 + w2 * dh1 * dh1;
+    const double B = 2.0 * (w1 * ox * dh0 + w2 * oy * dh1) - iw3 * dh2;
     const double C = w1 * ox * ox + w2 * oy * oy - iw3 * oz;
-    double roots[2];
-    int cnt;
+    Roots2 rr{0.0, 0.0, 0};
     if (fabs(A) < 1e-6) {
-        if (fabs(B) < 1e-12) return -1.0;
-        roots[0] = -C / B;
-        cnt = 1;
+        if (fabs(B) < 1e-12) return rr;
+        rr.r0 = -C / B;
+        rr.cnt = 1;
     } else {
         const double disc = B * B - 4.0 * A * C;
-        if (disc < 0.0) return -1.0;
+        if (disc < 0.0) return rr;
         const double sa = A > 0.0 ? 1.0 : -1.0, sq = sqrt(disc);
-        roots[0] = (-B - sa * sq) / (2.0 * A);
-        roots[1] = (-B + sa * sq) / (2.0 * A);
-        cnt = disc == 0.0 ? 1 : 2;
+        rr.r0 = (-B - sa * sq) / (2.0 * A);
+        rr.r1 = (-B + sa * sq) / (2.0 * A);
+        rr.cnt = disc == 0.0 ? 1 : 2;
     }
-    Hit h;
-    for (int k = 0; k < cnt; ++k)
-        if (confirm_root<M>(r, g, gfull, dh, roots[k], false, euclid, t_clip, h)) return roots[k];
-    return -1.0;
-}
-
-template <int M>
-__device__ __forceinline__ bool hit_marginal(const PrimRec &r, const Geo64 &g, const Geo64 *gfull,
-                                             const double d64[3], bool euclid, float t_clip, Hit &h)
-{
-    const double t = marginal_root<M>(r, g, gfull, d64, euclid, t_clip);
-    if (!(t > 0.0)) return false;
-    double dh[3];
-    local_dir64(g, d64, dh);
-    return confirm_root<M>(r, g, gfull, dh, t, false, euclid, t_clip, h);
+    return rr;
 }
 
 // Coarse fp32 stage (the per-candidate hot path).  Returns a mask: bit k set
@@ -472,19 +458,30 @@ __device__ __forceinline__ bool hit_exact_from(const PrimRec &r, const Geo64 &g,
                                                float t_first, bool second, bool marginal,
                                                Hit &h)
 {
-    if (marginal) return hit_marginal<M>(r, g, gfull, d64, euclid, t_clip, h);
-    const bool planar = (r.flags & 1u) != 0;
+    const bool planar = (r.flags & 1u) != 0;     // (near-tangent rays are never planar)
     double dh[3];
     local_dir64(g, d64, dh);
     if (planar && fabs(dh[2]) < 1e-12) return false;
-    if (confirm_root<M>(r, g, gfull, dh, refine_depth(g, dh, planar, t_first), planar, euclid,
-                        t_clip, h))
-        return true;
-    if (!second) return false;
-    float roots[2], hx, hy;
-    coarse_stage1(r, dx, dy, dz, t_clip, roots, hx, hy);
-    return confirm_root<M>(r, g, gfull, dh, refine_depth(g, dh, planar, roots[1]), planar,
-                           euclid, t_clip, h);
+    double ta, tb = 0.0;
+    bool hb;
+    if (marginal) {
+        const Roots2 rr = marginal_roots(&g, dh[0], dh[1], dh[2]);
+        if (rr.cnt == 0) return false;
+        ta = rr.r0;
+        tb = rr.r1;
+        hb = rr.cnt == 2;
+    } else {
+        ta = refine_depth(g, dh, planar, t_first);
+        hb = second;
+    }
+    if (confirm_root<M>(r, g, gfull, dh, ta, planar, euclid, t_clip, h)) return true;
+    if (!hb) return false;
+    if (!marginal) {
+        float roots[2], hx, hy;
+        coarse_stage1(r, dx, dy, dz, t_clip, roots, hx, hy);
+        tb = refine_depth(g, dh, planar, roots[1]);
+    }
+    return confirm_root<M>(r, g, gfull, dh, tb, planar, euclid, t_clip, h);
 }
 
 // Full candidate test: coarse fp32 roots, fp64 refinement, exact selection.
@@ -497,10 +494,16 @@ __device__ __forceinline__ bool hit_refined(const PrimRec &r, const Geo64 &g, co
     float roots[2], hx, hy, hz;
     const unsigned pass = coarse_roots(r, dx, dy, dz, euclid, t_clip, roots, hx, hy, hz);
     if (pass == 0u) return false;
-    if (pass & CR_MARGINAL) return hit_marginal<M>(r, g, &g, d64, euclid, t_clip, h);
     const bool planar = (r.flags & 1u) != 0;
     double dh[3];
     local_dir64(g, d64, dh);
+    if (pass & CR_MARGINAL) {
+        const Roots2 rr = marginal_roots(&g, dh[0], dh[1], dh[2]);
+        for (int k = 0; k < rr.cnt; ++k)
+            if (confirm_root<M>(r, g, &g, dh, k == 0 ? rr.r0 : rr.r1, false, euclid, t_clip, h))
+                return true;
+        return false;
+    }
     if (planar && fabs(dh[2]) < 1e-12) return false;
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
