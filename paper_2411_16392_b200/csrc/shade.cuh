@@ -37,6 +37,9 @@
 #ifndef QGS_NEWTON64
 #define QGS_NEWTON64 2      // fp64 Newton steps refining an accepted root
 #endif
+#ifndef QGS_NEWTON_RCP64
+#define QGS_NEWTON_RCP64 0  // approximate derivative inverse from rcp.approx.f64 (experiment)
+#endif
 
 namespace qgs {
 
@@ -217,7 +220,13 @@ __device__ __forceinline__ double refine_depth(const Geo64 &g, const double dh[3
         double x = ox + t * dh[0], y = oy + t * dh[1], z = oz + t * dh[2];
         double F = w1 * x * x + w2 * y * y - iw3 * z - Alin * t * t;
         double Fp = 2.0 * (w1 * x * dh[0] + w2 * y * dh[1]) - iw3 * dh[2] - 2.0 * Alin * t;
+#if QGS_NEWTON_RCP64
+        double rf;      // ~2^-20 reciprocal straight from the fp64 MUFU (no conversions)
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rf) : "d"(Fp));
+        t -= F * rf;
+#else
         t -= F * (double)(1.f / (float)Fp);
+#endif
     }
     return t;
 }
