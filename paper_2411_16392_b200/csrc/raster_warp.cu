@@ -343,21 +343,11 @@ enum { A_C0 = 0, A_A = 3, A_D = 4, A_D2 = 5, A_N0 = 6, A_K = 9, A_DIST = 10 };
 // put every other lane on the same banks)
 constexpr int KGP = KG + 4;
 
-#ifndef QGS_BWD_PREFETCH
-#define QGS_BWD_PREFETCH 0        // next fragment's record staged by cp.async (experiment)
-#endif
 struct BwdSmem {
-    union {
-        struct {                 // replay path
-            PrimRec rec[WB];
-            int prim[WB];
-            double ring_t[RING][32];
-            int ring_p[RING][32];
-        };
-#if QGS_BWD_PREFETCH
-        PrimRec pre[2][32];      // log path: double-buffered per-lane record of the next fragment
-#endif
-    };
+    PrimRec rec[WB];        // replay path
+    int prim[WB];
+    double ring_t[RING][32];
+    int ring_p[RING][32];
     float red[1][33][KGP];  // row 32 stays zero (padding reads of the group sums)
 };
 
@@ -1287,47 +1277,6 @@ __device__ __forceinline__ void bwd_block(const PrimRec *__restrict__ recs,
                     if (have_xy) nxy = xy[o];
                 }
             }
-#if QGS_BWD_PREFETCH
-            // records one fragment ahead in shared memory (cp.async), the log
-            // two ahead in registers
-            auto stage = [&](int buf, int prim) {
-                const char *src = reinterpret_cast<const char *>(recs + prim);
-                char *dst = reinterpret_cast<char *>(&sm.pre[buf][lane]);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) __pipeline_memcpy_async(dst + 16 * q, src + 16 * q, 16);
-            };
-            if (0 < nf) stage(0, np_);
-            __pipeline_commit();
-            int np2 = -1;
-            double nt2 = 0.0;
-            float2 nxy2 = make_float2(0.f, 0.f);
-            if (1 < nf_max) {
-                const size_t o = slot(1);
-                if (1 < nf) {
-                    np2 = fwd.frag_prim[o]; nt2 = fwd.frag_t[o];
-                    if (have_xy) nxy2 = xy[o];
-                }
-            }
-            for (int k = 0; k < nf_max; ++k) {
-                const bool emit = k < nf;
-                const int ep = np_;
-                const double et = nt_;
-                const float2 exy = nxy;
-                np_ = np2; nt_ = nt2; nxy = nxy2;
-                if (k + 1 < nf) stage((k + 1) & 1, np_);          // record k+1 in flight
-                __pipeline_commit();
-                if (k + 2 < nf_max) {                             // log k+2 in flight
-                    const size_t o = slot(k + 2);
-                    if (k + 2 < nf) {
-                        np2 = fwd.frag_prim[o]; nt2 = fwd.frag_t[o];
-                        if (have_xy) nxy2 = xy[o];
-                    }
-                }
-                __pipeline_wait_prior(1);                          // record k has landed
-                emit_grad(emit, ep, et, have_xy, exy.x, exy.y, emit ? &sm.pre[k & 1][lane] : nullptr);
-            }
-            return;
-#else
             for (int k = 0; k < nf_max; ++k) {
                 const bool emit = k < nf;
                 const int ep = np_;
@@ -1344,7 +1293,6 @@ __device__ __forceinline__ void bwd_block(const PrimRec *__restrict__ recs,
                 emit_grad(emit, ep, et, have_xy, exy.x, exy.y, nullptr);
             }
             return;
-#endif
         }
     }
 
