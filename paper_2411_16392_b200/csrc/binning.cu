@@ -196,7 +196,7 @@ __global__ void pixel_rays_kernel(CamK cam, double *rays)
 // (An fp32 pre-reject of rays that cannot hit the support was measured
 // slower: most pairs' vertex-nearest pixel does hit.)
 #ifndef QGS_KEY_MIN_BLOCKS
-#define QGS_KEY_MIN_BLOCKS 3
+#define QGS_KEY_MIN_BLOCKS 2     // 128 registers, no spills: 2.74 -> 2.60 ms at C3 (3 and 4 measured)
 #endif
 __global__ void __launch_bounds__(256, QGS_KEY_MIN_BLOCKS)
 pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
