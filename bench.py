@@ -311,6 +311,11 @@ def run_ours(a):
                        f"MEASURED_PEAKS.json {peaks['hbm_gbs']} GB/s",
         "step_roofline_ms": T_roof * 1e3,
         "step_roofline_frac": (T_roof * 1e3) / ms if world == 1 else None,
+        # both raster kernels against the same peaks (the dominant one is above)
+        "per_kernel": {k: {"achieved_tflops": v[0] / (v[2] / 1e3) / 1e12,
+                           "frac": v[0] / (v[2] / 1e3) / P32,
+                           "sfu_frac": v[1] / (v[2] / 1e3) / PSF, "ms_per_step": v[2]}
+                       for k, v in kernels.items() if v[2] > 0},
         "algorithmic": {"candidates": n_box, "accepted": n_acc, "composited": n_comp,
                         "after_conic_cull": n_cull, "after_coarse_test": n_coarse,
                         "pairs": sum(n_pairs_mine), "flop_fwd": F_fwd, "flop_bwd": F_bwd,
