@@ -50,6 +50,7 @@ struct BinWs {
     uint64_t *bucket, *tmp;
     double *rays;         // W*H*3 unit pixel rays (fp64) for the key kernel
     int32_t *order;       // tiles by descending pair count (sort schedule)
+    qgs::HugeSort *huge;  // the huge tiles' buckets between the two sort stages
     size_t bytes;
 };
 
@@ -65,6 +66,7 @@ BinWs bin_ws(void *base, int32_t tiles_x, int32_t tiles_y, int64_t n_pairs)
     w.tmp = reinterpret_cast<uint64_t *>(b + o);    o += qgs::align256((size_t)n_pairs * 8);
     w.rays = reinterpret_cast<double *>(b + o);     o += qgs::align256((size_t)tiles_x * tiles_y * 256 * 24);
     w.order = reinterpret_cast<int32_t *>(b + o);   o += qgs::align256((size_t)tiles_x * tiles_y * 4);
+    w.huge = reinterpret_cast<qgs::HugeSort *>(b + o); o += qgs::align256(qgs::huge_sort_bytes());
     w.bytes = o;
     return w;
 }
@@ -72,6 +74,8 @@ BinWs bin_ws(void *base, int32_t tiles_x, int32_t tiles_y, int64_t n_pairs)
 int configure()
 {
     QGS_CK(qgs::ensure_smem_attr(reinterpret_cast<const void *>(qgs::tile_sort_kernel),
+                                 (int)qgs::sort_smem_bytes()));
+    QGS_CK(qgs::ensure_smem_attr(reinterpret_cast<const void *>(qgs::tile_sort_chunks_kernel),
                                  (int)qgs::sort_smem_bytes()));
     return 0;
 }
@@ -141,7 +145,7 @@ size_t qgs_bin_workspace_bytes(int32_t P, int64_t n_pairs, int32_t n_tiles)
     size_t ndiff = 2 * (size_t)n_tiles + 65538;
     return qgs::align256(ndiff * sizeof(int)) + qgs::align256((size_t)n_tiles * 4) +
            2 * qgs::align256((size_t)n_pairs * 8) + qgs::align256((size_t)n_tiles * 256 * 24) +
-           qgs::align256((size_t)n_tiles * 4) + 256;
+           qgs::align256((size_t)n_tiles * 4) + qgs::align256(qgs::huge_sort_bytes()) + 256;
 }
 
 int qgs_bin(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settings *st,
@@ -180,9 +184,15 @@ int qgs_bin(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settin
     // last would be the kernel's tail
     qgs::tile_order_kernel<<<1, 1024, qgs::ORDER_SMEM, s>>>(tile_offsets, n_tiles, ws.order, 1);
     QGS_LAUNCHED("tile_order_kernel (sort)");
+    QGS_CK(cudaMemsetAsync(&ws.huge->count, 0, sizeof(int), s));
     qgs::tile_sort_kernel<<<n_tiles, qgs::sort_threads(), qgs::sort_smem_bytes(), s>>>(
-        tile_offsets, ws.bucket, ws.tmp, pv, ck, sk, tile_prims, ws.order);
+        tile_offsets, ws.bucket, ws.tmp, pv, ck, sk, tile_prims, ws.order, ws.huge);
     QGS_LAUNCHED("tile_sort_kernel");
+    // the huge tiles' buckets, SORT_CHUNKS CTAs per tile (most CTAs exit at once)
+    qgs::tile_sort_chunks_kernel<<<qgs::SORT_MAX_HUGE * qgs::sort_chunks(), qgs::sort_threads(),
+                                   qgs::sort_smem_bytes(), s>>>(tile_offsets, ws.tmp, pv, ck, sk,
+                                                                tile_prims, ws.huge);
+    QGS_LAUNCHED("tile_sort_chunks_kernel");
 
     return 0;
 }

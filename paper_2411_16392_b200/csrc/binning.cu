@@ -17,7 +17,7 @@
 // order is (key ascending, prim ascending), a total order.
 //
 // Compiled with -fmad=false (keys must round exactly as the reference).
-#include "qgs_common.cuh"
+#include "kernels.cuh"
 
 namespace qgs {
 
@@ -282,13 +282,19 @@ constexpr int SORT_T = QGS_SORT_T;
 constexpr int SORT_IPT = 4;
 constexpr int SORT_CHUNK = SORT_T * SORT_IPT;     // items per register pass
 constexpr int SORT_SMEM_ITEMS = QGS_SORT_SMEM_ITEMS;   // staged in shared memory up to this
-constexpr int SORT_MAX_BUCKETS = 8192;
+static_assert(SORT_MAX_BUCKETS == 8192, "kernels.cuh");
 #ifndef QGS_SORT_L2_MIN
 #define QGS_SORT_L2_MIN 6                        // mean first-level bucket that takes the second level
 #endif
 constexpr int SORT_NB2 = 2048;                   // second-level buckets of a staged group
 // a staged group uses the head of buf; its second-level bucket counts the tail
 constexpr int SORT_GROUP_ITEMS = SORT_SMEM_ITEMS - SORT_NB2 / 2;
+
+#ifndef QGS_SORT_HUGE
+#define QGS_SORT_HUGE 49152
+#endif
+constexpr int SORT_HUGE = QGS_SORT_HUGE;        // tiles over this many entries: multi-CTA stage 2
+constexpr int SORT_CHUNKS = 16;                  // CTAs per huge tile in stage 2
 
 struct SortSmem {
     uint64_t buf[SORT_SMEM_ITEMS];
@@ -450,9 +456,15 @@ __device__ __noinline__ void sort_group_l2(SortSmem &sm, const uint64_t *stage, 
     __syncthreads();
 }
 
+__device__ __forceinline__ void sort_groups(SortSmem &sm, const uint64_t *stage, int c0, int c1, int nb,
+                                         const BucketFn &bf, uint32_t kmin, uint32_t range,
+                                         int shift, int tile, const PrepView &pv, const CamK &cam,
+                                         const SetK &st, int32_t *out);
+
 __global__ void __launch_bounds__(SORT_T, QGS_SORT_MIN_BLOCKS)
 tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint64_t *tmp,
-                 PrepView pv, CamK cam, SetK st, int32_t *tile_prims, const int32_t *order)
+                 PrepView pv, CamK cam, SetK st, int32_t *tile_prims, const int32_t *order,
+                 HugeSort *huge)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SortSmem &sm = *reinterpret_cast<SortSmem *>(smem_raw);
@@ -594,18 +606,49 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
     } else {
         // groups of consecutive buckets that fit in shared memory: one
         // coalesced bulk load from the L2 staging slice, then warps sort
-        // their buckets out of shared memory
-        // lower key bound of first-level bucket d (d = nb: past the top)
+        // their buckets out of shared memory.  A tile over SORT_HUGE entries
+        // hands its buckets to tile_sort_chunks_kernel instead (SORT_CHUNKS
+        // CTAs per tile: one CTA would be the kernel's tail -- C4's largest
+        // tiles hold 391K entries).
+        if (n > SORT_HUGE && huge) {
+            __shared__ int s_h;
+            if (threadIdx.x == 0) {
+                const int h = atomicAdd(&huge->count, 1);
+                s_h = h;
+                if (h < SORT_MAX_HUGE) {
+                    HugeTile &t = huge->t[h];
+                    t.tile = tile; t.nb = nb; t.kmin = kmin; t.range = range; t.shift = shift;
+                    t.ns = bf.sp ? bf.ns : -1;
+                }
+            }
+            __syncthreads();
+            if (s_h < SORT_MAX_HUGE) {
+                int *dst = huge->bend_of(s_h);
+                for (int d = threadIdx.x; d < SORT_MAX_BUCKETS; d += SORT_T) dst[d] = sm.bend[d];
+                return;
+            }
+        }
+        sort_groups(sm, stage, 0, nb, nb, bf, kmin, range, shift, tile, pv, cam, st, out);
+    }
+}
+
+// The buckets [c0, c1) of a tile, staged in L2 (`stage`), in groups that fit
+// in shared memory (see tile_sort_kernel); sm.bend holds the bucket ends.
+__device__ __forceinline__ void sort_groups(SortSmem &sm, const uint64_t *stage, int c0, int c1, int nb,
+                                         const BucketFn &bf, uint32_t kmin, uint32_t range,
+                                         int shift, int tile, const PrepView &pv, const CamK &cam,
+                                         const SetK &st, int32_t *out)
+{
         auto lo_of = [&](int d) -> uint64_t {
             if (!bf.sp) return (uint64_t)kmin + ((uint64_t)d << shift);
             if (d == 0) return kmin;
             return d > bf.ns ? (uint64_t)kmin + range + 1 : (uint64_t)bf.sp[d - 1];
         };
-        int g0 = 0;
-        while (g0 < nb) {
+        int g0 = c0;
+        while (g0 < c1) {
             const int base = bucket_start(sm, g0);
             // last bucket end within SORT_GROUP_ITEMS of base (binary search)
-            int lo = g0 + 1, hi = nb;
+            int lo = g0 + 1, hi = c1;
             while (lo < hi) {
                 const int mid = (lo + hi + 1) >> 1;
                 if (sm.bend[mid - 1] - base <= SORT_GROUP_ITEMS) lo = mid; else hi = mid - 1;
@@ -635,7 +678,33 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
             sort_group_l2(sm, stage, base, cnt, lo_of(g0), lo_of(g1), tile, pv, cam, st, out);
             g0 = g1;
         }
+}
+
+// second stage of the tiles over SORT_HUGE entries: CTA (h, j) sorts chunk j
+// of huge tile h's buckets (first stage: tile_sort_kernel)
+__global__ void __launch_bounds__(SORT_T, QGS_SORT_MIN_BLOCKS)
+tile_sort_chunks_kernel(const int32_t *__restrict__ tile_offsets, const uint64_t *tmp, PrepView pv,
+                        CamK cam, SetK st, int32_t *tile_prims, const HugeSort *huge)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SortSmem &sm = *reinterpret_cast<SortSmem *>(smem_raw);
+    const int h = (int)blockIdx.x / SORT_CHUNKS, j = (int)blockIdx.x % SORT_CHUNKS;
+    if (h >= min(huge->count, SORT_MAX_HUGE)) return;
+    const HugeTile t = huge->t[h];
+    const int start = tile_offsets[t.tile];
+    const int *src = const_cast<HugeSort *>(huge)->bend_of(h);
+    for (int d = threadIdx.x; d < SORT_MAX_BUCKETS; d += SORT_T) sm.bend[d] = src[d];
+    __syncthreads();
+    BucketFn bf{t.kmin, t.shift, nullptr, 0};
+    if (t.ns >= 0) {
+        bf.sp = reinterpret_cast<const uint32_t *>(sm.bend) + SORT_MAX_BUCKETS / 2 + 1;
+        bf.ns = t.ns;
     }
+    const int c0 = (int)((long long)t.nb * j / SORT_CHUNKS);
+    const int c1 = (int)((long long)t.nb * (j + 1) / SORT_CHUNKS);
+    if (c0 < c1)
+        sort_groups(sm, tmp + start, c0, c1, t.nb, bf, t.kmin, t.range, t.shift, t.tile, pv, cam,
+                    st, tile_prims + start);
 }
 
 // -------------------------------------------------------- debug / unit
@@ -666,6 +735,8 @@ __global__ void tile_keys_f64_kernel(int64_t n, const int64_t *pair_tiles,
 }
 
 size_t sort_smem_bytes() { return sizeof(SortSmem); }
+int sort_chunks() { return SORT_CHUNKS; }
+size_t huge_sort_bytes() { return sizeof(HugeSort) + (size_t)SORT_MAX_HUGE * SORT_MAX_BUCKETS * sizeof(int); }
 int sort_threads() { return SORT_T; }
 
 }  // namespace qgs

@@ -24,9 +24,33 @@ __global__ void pixel_rays_kernel(CamK cam, double *rays);
 __global__ void export_geom_kernel(qgs_params prm, CamK cam, PrepView pv, qgs_prep_export o);
 __global__ void pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
                                 const double *rays, int32_t *cursor, uint64_t *bucket);
+// tiles over SORT_HUGE entries: stage 1 (tile_sort_kernel) buckets them and
+// records the buckets here; stage 2 (tile_sort_chunks_kernel) sorts the
+// buckets with sort_chunks() CTAs per tile
+constexpr int SORT_MAX_BUCKETS = 8192;
+constexpr int SORT_MAX_HUGE = 512;
+struct HugeTile {
+    int tile, nb, shift, ns;          // ns: splitters (sample-sort buckets), -1: linear buckets
+    uint32_t kmin, range;
+    int pad[2];
+};
+struct HugeSort {
+    int count;
+    int pad[7];
+    HugeTile t[SORT_MAX_HUGE];
+    __device__ int *bend_of(int h)    // bucket ends (+ splitters), SORT_MAX_BUCKETS ints per tile
+    {
+        return reinterpret_cast<int *>(this + 1) + (size_t)h * SORT_MAX_BUCKETS;
+    }
+};
 __global__ void tile_sort_kernel(const int32_t *tile_offsets, uint64_t *keys, uint64_t *tmp,
                                  PrepView pv, CamK cam, SetK st, int32_t *tile_prims,
-                                 const int32_t *order);
+                                 const int32_t *order, HugeSort *huge);
+__global__ void tile_sort_chunks_kernel(const int32_t *tile_offsets, const uint64_t *tmp,
+                                        PrepView pv, CamK cam, SetK st, int32_t *tile_prims,
+                                        const HugeSort *huge);
+int sort_chunks();
+size_t huge_sort_bytes();
 __global__ void sorted_keys_kernel(PrepView pv, const int32_t *tile_offsets,
                                    const int32_t *tile_prims, int n_tiles, CamK cam, SetK st,
                                    double *keys);
