@@ -381,7 +381,14 @@ __device__ inline ConicRec bounding_conic(const double s[3], bool planar, bool e
     return q;
 }
 
-__global__ void preprocess_kernel(qgs_params prm, CamK cam, PrepView pv, int euclid)
+#ifndef QGS_PRE_MIN_BLOCKS
+#define QGS_PRE_MIN_BLOCKS 1
+#endif
+#ifndef QGS_CHAIN_MIN_BLOCKS
+#define QGS_CHAIN_MIN_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(128, QGS_PRE_MIN_BLOCKS)
+preprocess_kernel(qgs_params prm, CamK cam, PrepView pv, int euclid)
 {
     int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= prm.P) return;
@@ -476,7 +483,8 @@ __global__ void preprocess_kernel(qgs_params prm, CamK cam, PrepView pv, int euc
 
 // ------------------------------------------------------------- K7 chain
 
-__global__ void chain_kernel(qgs_params prm, CamK cam, const float *__restrict__ kg,
+__global__ void __launch_bounds__(128, QGS_CHAIN_MIN_BLOCKS)
+chain_kernel(qgs_params prm, CamK cam, const float *__restrict__ kg,
                              qgs_grads out)
 {
     int p = blockIdx.x * blockDim.x + threadIdx.x;
