@@ -37,9 +37,6 @@
 #ifndef QGS_NEWTON64
 #define QGS_NEWTON64 2      // fp64 Newton steps refining an accepted root
 #endif
-#ifndef QGS_NEWTON_F32_FIRST
-#define QGS_NEWTON_F32_FIRST 0  // first Newton step in fp32 (experiment)
-#endif
 #ifndef QGS_NEWTON_RCP64
 #define QGS_NEWTON_RCP64 1  // derivative inverse from rcp.approx.f64 (C3 forward -1.6 %)
 #endif
@@ -218,30 +215,8 @@ __device__ __forceinline__ double refine_depth(const Geo64 &g, const double dh[3
     // error by >= 1e6 plus the quadratic term) take the coarse root's <= 1e-4
     // to full precision; a third was measured to change nothing
     constexpr int NEWTON64 = QGS_NEWTON64;
-    int n64 = NEWTON64;
-#if QGS_NEWTON_F32_FIRST
-    // the first step in fp32 on the point form (its x = o + t d cancels only
-    // ~|o|/|x| ~ 1e2: good to ~1e-6 of t), then one fp64 step (-> ~1e-12),
-    // unless the ray grazes the surface or |A| is near the linear-branch
-    // threshold -- then both steps in fp64
-    if (Alin == 0.0 && fabs(A) > 2e-6) {
-        const float hx = (float)dh[0], hy = (float)dh[1], hz = (float)dh[2];
-        const float fw1 = (float)w1, fw2 = (float)w2, fiw3 = (float)iw3;
-        const float tf = t0;
-        const float x = fmaf(tf, hx, (float)ox), y = fmaf(tf, hy, (float)oy);
-        const float z = fmaf(tf, hz, (float)oz);
-        const float a1 = fw1 * x * hx, a2 = fw2 * y * hy, a3 = fiw3 * hz;
-        const float Fp = 2.f * (a1 + a2) - a3;
-        if (fabsf(Fp) > 0.05f * (2.f * (fabsf(a1) + fabsf(a2)) + fabsf(a3))) {
-            const float F = fmaf(fw1 * x, x, fw2 * y * y) - fiw3 * z;
-            t = (double)(tf - __fdividef(F, Fp));
-            n64 = NEWTON64 - 1;
-        }
-    }
-#endif
 #pragma unroll
     for (int it = 0; it < NEWTON64; ++it) {
-        if (it >= n64) break;
         double x = ox + t * dh[0], y = oy + t * dh[1], z = oz + t * dh[2];
         double F = w1 * x * x + w2 * y * y - iw3 * z - Alin * t * t;
         double Fp = 2.0 * (w1 * x * dh[0] + w2 * y * dh[1]) - iw3 * dh[2] - 2.0 * Alin * t;
