@@ -115,6 +115,7 @@ def _write(name, rep, g):
     out = {"scene": name, **rep, "grads": g, "grads_deterministic": _fullview.det}
     print(json.dumps(out, default=str))
     if os.environ.get("QGS_PARITY_OUT"):
+        os.makedirs(os.environ["QGS_PARITY_OUT"], exist_ok=True)
         with open(os.path.join(os.environ["QGS_PARITY_OUT"], f"fullview_{name}.json"), "w") as f:
             json.dump(out, f, indent=1, default=str)
 
