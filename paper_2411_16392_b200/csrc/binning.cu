@@ -311,7 +311,13 @@ pair_key_flat_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
         }
         p0 = lo;
     }
-    for (long long ch = c_begin; ch < c_end; ++ch) {
+    // software pipeline: chunk ch+1's primitive lookup, cursor atomic and ray
+    // load are issued before chunk ch's fp64 key
+    struct Next {
+        int p, slot;
+        double cx, cy, cz;
+    };
+    auto lookup = [&](long long ch) -> Next {
         const long long i = (ch << 5) + lane;
         const bool valid = i < n_pairs;
         // this lane's primitive: p0 + #{k : off[p0 + 1 + k] <= i}, 32 offsets
@@ -330,21 +336,32 @@ pair_key_flat_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
             if (__all_sync(0xffffffffu, done)) break;
         }
         p0 = __shfl_sync(0xffffffffu, p, 31);
-        if (!valid) continue;
+        Next n{-1, 0, 0.0, 0.0, 0.0};
+        if (!valid) return n;
         const KeyRec &kr = krec[p];
         const int local = (int)(i - off[p]);
         const int ncols = kr.ncols;
         const int row = local / ncols, col = local - row * ncols;
         const int tx = kr.tx0 + col, ty = kr.ty0 + row;
-        const int tile = ty * cam.tiles_x + tx;
-        const int slot = atomicAdd(&cursor[tile], 1);
+        n.p = p;
+        n.slot = atomicAdd(&cursor[ty * cam.tiles_x + tx], 1);
         const int ulo = tx * TILE, uhi = min(cam.W, tx * TILE + TILE) - 1;
         const int vlo = ty * TILE, vhi = min(cam.H, ty * TILE + TILE) - 1;
         const int iu = min(max(kr.iu_v, ulo), uhi), iv = min(max(kr.iv_v, vlo), vhi);
         const double *ray = rays + 3 * ((size_t)iv * cam.W + iu);
-        const double key = key_from_ray_fast(kr.kp, ray[0], ray[1], ray[2], euclid, st.t_clip);
-        QGS_CHECK(slot >= 0 && slot < n_pairs);
-        bucket[slot] = sort_composite(key, p, st.pbits);
+        n.cx = ray[0]; n.cy = ray[1]; n.cz = ray[2];
+        return n;
+    };
+    Next cur = lookup(c_begin);
+    for (long long ch = c_begin; ch < c_end; ++ch) {
+        const Next nxt = ch + 1 < c_end ? lookup(ch + 1) : Next{-1, 0, 0.0, 0.0, 0.0};
+        if (cur.p >= 0) {
+            const double key = key_from_ray_fast(krec[cur.p].kp, cur.cx, cur.cy, cur.cz, euclid,
+                                                 st.t_clip);
+            QGS_CHECK(cur.slot >= 0 && cur.slot < n_pairs);
+            bucket[cur.slot] = sort_composite(key, cur.p, st.pbits);
+        }
+        cur = nxt;
     }
 }
 

@@ -10,6 +10,6 @@ agg=collections.defaultdict(float)
 for r in rows[1:]:
     try: agg[r[ki].split('(')[0]]+=float(r[vi].replace(',',''))/1e6
     except: pass
-print(repr(sys.argv[1]), {k.split('::')[-1]: round(v,3) for k,v in sorted(agg.items(), key=lambda x:-x[1])[:7]})
+print(repr(sys.argv[1]), {k.split('::')[-1]: round(v,3) for k,v in sorted(agg.items(), key=lambda x:-x[1])[:9]})
 PY
 done

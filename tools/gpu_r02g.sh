@@ -1,8 +1,6 @@
+# flat pair-key kernel, software-pipelined: bit-exactness, then per-kernel A/B
 mkdir -p gpurun_out
-timeout 600 python tools/grad_prim_diag.py --config c4 --prims 1269412 > gpurun_out/r02g_diag.log 2>&1; echo "diag rc=$?"
-cat gpurun_out/r02g_diag.log | tail -12
-for mb in 16 17 18; do
-  QGS_NVCC_EXTRA="-DQGS_FWD_EXACT_MIN_BLOCKS=$mb" python -c "from paper_2411_16392_b200 import build as b; b.build(force=True)" > /dev/null 2>&1 || echo "build failed"
-  timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu --no-e2e > gpurun_out/r02g_mb$mb.log 2>&1
-  tail -1 gpurun_out/r02g_mb$mb.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print('mb $mb value',d['value'],'fwd',r['fwd_ms_per_step']/8,'bwd',r['bwd_ms_per_step']/8)"
-done
+QGS_BUILD_DEBUG=0 python -c "from paper_2411_16392_b200 import build as b; b.build(force=True)" > /dev/null 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "bin or key or sort or golden" 2>&1 | tail -2
+bash tools/gpu_launch_cmp.sh "" "-DQGS_KEY_MIN_BLOCKS=3" "-DQGS_KEY_FLAT=0" 2>&1 | sed 's/raster_[a-z_]*kernel[^,]*,//g'
+grep -h key_rec /tmp/l.csv | head -0
