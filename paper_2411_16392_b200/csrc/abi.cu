@@ -51,11 +51,10 @@ struct BinWs {
     double *rays;         // W*H*3 unit pixel rays (fp64) for the key kernel
     int32_t *order;       // tiles by descending pair count (sort schedule)
     qgs::HugeSort *huge;  // the huge tiles' buckets between the two sort stages
-    qgs::KeyRec *keyrec;  // per-primitive key constants (flat key kernel)
     size_t bytes;
 };
 
-BinWs bin_ws(void *base, int32_t P, int32_t tiles_x, int32_t tiles_y, int64_t n_pairs)
+BinWs bin_ws(void *base, int32_t tiles_x, int32_t tiles_y, int64_t n_pairs)
 {
     char *b = static_cast<char *>(base);
     BinWs w;
@@ -68,7 +67,6 @@ BinWs bin_ws(void *base, int32_t P, int32_t tiles_x, int32_t tiles_y, int64_t n_
     w.rays = reinterpret_cast<double *>(b + o);     o += qgs::align256((size_t)tiles_x * tiles_y * 256 * 24);
     w.order = reinterpret_cast<int32_t *>(b + o);   o += qgs::align256((size_t)tiles_x * tiles_y * 4);
     w.huge = reinterpret_cast<qgs::HugeSort *>(b + o); o += qgs::align256(qgs::huge_sort_bytes());
-    w.keyrec = reinterpret_cast<qgs::KeyRec *>(b + o); o += qgs::align256(qgs::key_rec_bytes(P));
     w.bytes = o;
     return w;
 }
@@ -142,12 +140,12 @@ int qgs_preprocess(const qgs_params *prims, const qgs_camera *cam, const qgs_set
 
 size_t qgs_bin_workspace_bytes(int32_t P, int64_t n_pairs, int32_t n_tiles)
 {
+    (void)P;
     // diff grid is at most (n_tiles + tiles_x + tiles_y + 1) entries; bound it by 2*n_tiles + 2*32768
     size_t ndiff = 2 * (size_t)n_tiles + 65538;
     return qgs::align256(ndiff * sizeof(int)) + qgs::align256((size_t)n_tiles * 4) +
            2 * qgs::align256((size_t)n_pairs * 8) + qgs::align256((size_t)n_tiles * 256 * 24) +
-           qgs::align256((size_t)n_tiles * 4) + qgs::align256(qgs::huge_sort_bytes()) +
-           qgs::align256(qgs::key_rec_bytes(P)) + 256;
+           qgs::align256((size_t)n_tiles * 4) + qgs::align256(qgs::huge_sort_bytes()) + 256;
 }
 
 int qgs_bin(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settings *st,
@@ -162,7 +160,7 @@ int qgs_bin(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settin
     qgs::CamK ck = qgs::make_camk(*cam);
     qgs::SetK sk = qgs::make_setk(*st);
     const int n_tiles = ck.tiles_x * ck.tiles_y;
-    BinWs ws = bin_ws(workspace, P, ck.tiles_x, ck.tiles_y, n_pairs);
+    BinWs ws = bin_ws(workspace, ck.tiles_x, ck.tiles_y, n_pairs);
     sk.pbits = 1;                                  // id bits of the sort composite
     while (sk.pbits < 31 && (1LL << sk.pbits) < (long long)P) ++sk.pbits;
     if (ws.bytes > workspace_bytes) return fail(QGS_E_CAPACITY, "bin workspace too small");
@@ -179,23 +177,8 @@ int qgs_bin(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settin
     const int grid = (int)std::min<long long>(cdiv(n_pairs, 256), 148LL * 32);
     qgs::pixel_rays_kernel<<<cdiv((long long)ck.W * ck.H, 256), 256, 0, s>>>(ck, ws.rays);
     QGS_LAUNCHED("pixel_rays_kernel");
-#if QGS_KEY_FLAT
-    qgs::key_rec_kernel<<<cdiv(P, 256), 256, 0, s>>>(pv, P, ck, ws.keyrec);
-    QGS_LAUNCHED("key_rec_kernel");
-    // persistent: one wave of resident CTAs, equal contiguous pair ranges per warp
-    int kdev = 0, ksms = 148, kocc = QGS_KEY_MIN_BLOCKS;
-    cudaGetDevice(&kdev);
-    cudaDeviceGetAttribute(&ksms, cudaDevAttrMultiProcessorCount, kdev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &kocc, reinterpret_cast<const void *>(qgs::pair_key_flat_kernel), 256, 0);
-    const int kgrid = (int)std::min<long long>(cdiv(n_pairs, 256), (long long)ksms * std::max(kocc, 1));
-    qgs::pair_key_flat_kernel<<<kgrid, 256, 0, s>>>(pv, P, n_pairs, ck, sk, ws.rays,
-                                                                      ws.keyrec, ws.cursor, ws.bucket);
-    QGS_LAUNCHED("pair_key_flat_kernel");
-#else
     qgs::pair_key_kernel<<<grid, 256, 0, s>>>(pv, P, n_pairs, ck, sk, ws.rays, ws.cursor, ws.bucket);
     QGS_LAUNCHED("pair_key_kernel");
-#endif
     pv.rays = ws.rays;
     // largest tiles first: one CTA sorts a tile, so a 100K-entry tile started
     // last would be the kernel's tail

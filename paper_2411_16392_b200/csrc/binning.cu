@@ -195,6 +195,9 @@ __global__ void pixel_rays_kernel(CamK cam, double *rays)
 // from the table and the float64 key with the reference's operation order.
 // (An fp32 pre-reject of rays that cannot hit the support was measured
 // slower: most pairs' vertex-nearest pixel does hit.)
+#ifndef QGS_KEY_MIN_BLOCKS
+#define QGS_KEY_MIN_BLOCKS 2     // 128 registers, no spills: 2.74 -> 2.60 ms at C3 (3 and 4 measured)
+#endif
 __global__ void __launch_bounds__(256, QGS_KEY_MIN_BLOCKS)
 pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
                 const double *__restrict__ rays, int32_t *cursor, uint64_t *bucket)
@@ -251,121 +254,6 @@ pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
         }
     }
 }
-
-// Flat variant: a warp takes 32 consecutive pairs of the global (primitive,
-// local tile) order, one per lane, so no lane idles at the end of a
-// primitive's tile list and no lane waits while one lane builds the
-// primitive's constants (the warp-per-primitive kernel above runs at 65 %
-// lane utilisation on C3).  The per-primitive constants come from a table
-// written by key_rec_kernel; each lane finds its primitive by a search over
-// the 32 pair offsets after the chunk's first primitive.  Same key function,
-// so the same bits.
-struct alignas(16) KeyRec {
-    KeyPrim kp;
-    int tx0, ty0, ncols, iu_v, iv_v;
-};
-
-__global__ void __launch_bounds__(256)
-key_rec_kernel(PrepView pv, int P, CamK cam, KeyRec *out)
-{
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= P || pv.ntiles[p] == 0) return;
-    const Geo64 &g = pv.geo[p];
-    const int4 b = pv.bbox[p];
-    KeyRec r;
-    r.kp = key_prim(g);
-    r.tx0 = b.x / TILE;
-    r.ty0 = b.z / TILE;
-    r.ncols = b.y / TILE - r.tx0 + 1;
-    // the vertex pixel is clamped into the pair's tile; pre-clamped to
-    // [-1, W] x [-1, H] first so it fits an int (same clamp result)
-    const double fu = fmin(fmax(floor(g.vert_u), -1.0), (double)cam.W);
-    const double fv = fmin(fmax(floor(g.vert_v), -1.0), (double)cam.H);
-    r.iu_v = (int)fu;
-    r.iv_v = (int)fv;
-    out[p] = r;
-}
-
-__global__ void __launch_bounds__(256, QGS_KEY_MIN_BLOCKS)
-pair_key_flat_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
-                     const double *__restrict__ rays, const KeyRec *__restrict__ krec,
-                     int32_t *cursor, uint64_t *bucket)
-{
-    const int lane = threadIdx.x & 31;
-    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-    const long long wid = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const long long n_chunks = (n_pairs + 31) >> 5;
-    const long long per = (n_chunks + warps - 1) / warps;
-    const long long c_begin = wid * per, c_end = min(n_chunks, c_begin + per);
-    if (c_begin >= c_end) return;
-    const bool euclid = st.euclid != 0;
-    const int64_t *__restrict__ off = pv.pair_off;
-    // primitive of the first pair: last p with off[p] <= i0 (off[P] = n_pairs)
-    int p0;
-    {
-        const long long i0 = c_begin << 5;
-        int lo = 0, hi = P;              // off[lo] <= i0 < off[hi]
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (off[mid] <= i0) lo = mid; else hi = mid;
-        }
-        p0 = lo;
-    }
-    // software pipeline: chunk ch+1's primitive lookup, cursor atomic and ray
-    // load are issued before chunk ch's fp64 key
-    struct Next {
-        int p, slot;
-        double cx, cy, cz;
-    };
-    auto lookup = [&](long long ch) -> Next {
-        const long long i = (ch << 5) + lane;
-        const bool valid = i < n_pairs;
-        // this lane's primitive: p0 + #{k : off[p0 + 1 + k] <= i}, 32 offsets
-        // per window (more windows only across runs of empty primitives)
-        int p = p0;
-        bool done = !valid;
-        for (int pw = p0;; pw += 32) {
-            const int q = pw + 1 + lane;
-            const long long o = q <= P ? off[q] : 0x7fffffffffffffffLL;
-            int cnt = 0;
-#pragma unroll
-            for (int s = 16; s >= 1; s >>= 1)
-                if (__shfl_sync(0xffffffffu, o, cnt + s - 1) <= i) cnt += s;
-            if (__shfl_sync(0xffffffffu, o, 31) <= i) cnt = 32;
-            if (!done && cnt < 32) { p = pw + cnt; done = true; }
-            if (__all_sync(0xffffffffu, done)) break;
-        }
-        p0 = __shfl_sync(0xffffffffu, p, 31);
-        Next n{-1, 0, 0.0, 0.0, 0.0};
-        if (!valid) return n;
-        const KeyRec &kr = krec[p];
-        const int local = (int)(i - off[p]);
-        const int ncols = kr.ncols;
-        const int row = local / ncols, col = local - row * ncols;
-        const int tx = kr.tx0 + col, ty = kr.ty0 + row;
-        n.p = p;
-        n.slot = atomicAdd(&cursor[ty * cam.tiles_x + tx], 1);
-        const int ulo = tx * TILE, uhi = min(cam.W, tx * TILE + TILE) - 1;
-        const int vlo = ty * TILE, vhi = min(cam.H, ty * TILE + TILE) - 1;
-        const int iu = min(max(kr.iu_v, ulo), uhi), iv = min(max(kr.iv_v, vlo), vhi);
-        const double *ray = rays + 3 * ((size_t)iv * cam.W + iu);
-        n.cx = ray[0]; n.cy = ray[1]; n.cz = ray[2];
-        return n;
-    };
-    Next cur = lookup(c_begin);
-    for (long long ch = c_begin; ch < c_end; ++ch) {
-        const Next nxt = ch + 1 < c_end ? lookup(ch + 1) : Next{-1, 0, 0.0, 0.0, 0.0};
-        if (cur.p >= 0) {
-            const double key = key_from_ray_fast(krec[cur.p].kp, cur.cx, cur.cy, cur.cz, euclid,
-                                                 st.t_clip);
-            QGS_CHECK(cur.slot >= 0 && cur.slot < n_pairs);
-            bucket[cur.slot] = sort_composite(key, cur.p, st.pbits);
-        }
-        cur = nxt;
-    }
-}
-
-size_t key_rec_bytes(int P) { return sizeof(KeyRec) * (size_t)(P > 0 ? P : 0); }
 
 // ------------------------------------------------------- per-tile sort
 //

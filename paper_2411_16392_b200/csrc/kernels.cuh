@@ -11,12 +11,6 @@ __global__ void export_prep_kernel(PrepView pv, int P, double *scales, double *a
                                    double *colors, int32_t *bbox, uint8_t *planar);
 
 // binning.cu
-#ifndef QGS_KEY_MIN_BLOCKS
-#define QGS_KEY_MIN_BLOCKS 2     // 128 registers, no spills: 2.74 -> 2.60 ms at C3 (3 and 4 measured)
-#endif
-#ifndef QGS_KEY_FLAT
-#define QGS_KEY_FLAT 1           // pair keys: flat pair ranges per warp (else a warp per primitive)
-#endif
 constexpr int SCAN_THREADS = 1024;
 constexpr int SCAN_ITEMS = SCAN_THREADS * 4;
 __global__ void scan_sums_kernel(const int32_t *in, int n, int64_t *sums);
@@ -30,12 +24,6 @@ __global__ void pixel_rays_kernel(CamK cam, double *rays);
 __global__ void export_geom_kernel(qgs_params prm, CamK cam, PrepView pv, qgs_prep_export o);
 __global__ void pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
                                 const double *rays, int32_t *cursor, uint64_t *bucket);
-struct KeyRec;
-size_t key_rec_bytes(int P);
-__global__ void key_rec_kernel(PrepView pv, int P, CamK cam, KeyRec *out);
-__global__ void pair_key_flat_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
-                                     const double *rays, const KeyRec *krec, int32_t *cursor,
-                                     uint64_t *bucket);
 // tiles over SORT_HUGE entries: stage 1 (tile_sort_kernel) buckets them and
 // records the buckets here; stage 2 (tile_sort_chunks_kernel) sorts the
 // buckets with sort_chunks() CTAs per tile
