@@ -544,7 +544,14 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
 #endif
         }
         nfrag++;
-        if (T < c.t_term) alive = false;
+        if (M == MODE_EXACT && log_on && fabs(T - c.t_term) <= QGS_TERM_BAND * c.t_term) {
+            if (exact_transmittance(geo, out.frag_prim, out.frag_t, sm.pages, nfrag, lane,
+                                    ray64[0], ray64[1], ray64[2], c.euclid,
+                                    c.alpha_clamp64) < c.t_term)
+                alive = false;
+        } else if (T < c.t_term) {
+            alive = false;
+        }
     };
 
     // Batch of up to WB queued entries: stage their records, run the coarse
@@ -1188,6 +1195,13 @@ __device__ __forceinline__ void bwd_block(const PrimRec *__restrict__ recs,
 #if QGS_DEBUG_CHECKS
     const int nf_of_pixel = inside ? fwd.n_fragments[px] : 0;
 #endif
+    // replay: the pixel stops after the forward's fragment count (its
+    // termination decision may have been made on the float64 transmittance)
+    int n_left = 0;
+    if (REPLAY && alive) {
+        n_left = fwd.n_fragments[px];
+        alive = n_left > 0;
+    }
     auto emit_grad = [&](bool emit, int ep, double t, bool have_xy, float lx, float ly,
                          const PrimRec *staged) {
         float g[KG];
@@ -1220,7 +1234,7 @@ __device__ __forceinline__ void bwd_block(const PrimRec *__restrict__ recs,
             const float g_abar = (float)(T * V) - (float)(vtot - pref) / (float)(1.0 - f.abar64);
             frag_grad(r, f, dx, dy, dz, (float)w, g_abar, (float)(t * F0 - F1), up, c.euclid, g);
             T *= 1.0 - f.abar64;
-            if (T < c.t_term) alive = false;
+            if (REPLAY ? --n_left == 0 : T < c.t_term) alive = false;
         }
         if (DET) {
             if (emit) {

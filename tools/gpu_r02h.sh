@@ -1,11 +1,12 @@
+# float64 termination decision: parity (count flips), event count, A/B cost
 mkdir -p gpurun_out
-TAG=r02h
-timeout 600 python bench.py --steps 5 --warmup 3 > gpurun_out/${TAG}_bench.log 2>&1; echo "bench rc=$?"
-tail -1 gpurun_out/${TAG}_bench.log | cut -c1-200
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-  --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e \
-  > gpurun_out/${TAG}_ncu_launch.log 2>&1; echo "launch list rc=$?"
-timeout 1500 ncu --set full --clock-control none --import-source on \
-  -k regex:"raster_fwd|raster_bwd_kernel|tile_sort|pair_key|preprocess|chain" -c 8 -o gpurun_out/${TAG}_full \
-  python tools/profile_view.py --config c3 > gpurun_out/${TAG}_ncu_full.log 2>&1; echo "ncu full rc=$?"
-ls -la gpurun_out/${TAG}_full.ncu-rep
+python -m paper_2411_16392_b200.build > /dev/null 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_known_answers.py tests/test_debug_checks.py -q -x 2>&1 | tail -2
+QGS_PARITY_OUT=gpurun_out/r02h_parity timeout 900 python -m pytest tests/test_gpu_fullview.py -q -x 2>&1 | tail -2
+for c in c3 c4; do python -c "
+import json; d=json.load(open('gpurun_out/r02h_parity/fullview_$c.json'))
+print('$c', d['image'], d['grads'].get('violations'), d['grads'].get('conditioning',{}).get('count_flip'))"; done
+QGS_BUILD_DEBUG=0 QGS_NVCC_EXTRA="-DQGS_UTIL_COUNTERS=1" python -c "from paper_2411_16392_b200 import build as b; b.build(force=True)" > /dev/null 2>&1
+python tools/lane_util_fwd.py --config c3 | head -1
+python tools/lane_util_fwd.py --config c4 | head -1
+bash tools/gpu_wpc.sh "" "-DQGS_TERM_BAND=-1.0"
