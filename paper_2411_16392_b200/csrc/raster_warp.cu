@@ -545,9 +545,13 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
         }
         nfrag++;
         if (M == MODE_EXACT && log_on && fabs(T - c.t_term) <= QGS_TERM_BAND * c.t_term) {
+#if QGS_TERM_NOP
+            const double T_ref = T;
+#else
             const double T_ref = exact_transmittance(geo, out.frag_prim, out.frag_t, sm.pages,
                                                      nfrag, lane, ray64[0], ray64[1], ray64[2],
                                                      c.euclid, c.alpha_clamp64);
+#endif
 #if QGS_UTIL_COUNTERS
             {   // [3..6]: |T - T_ref| / t_term above 1e-5, 3e-5, 1e-4, 3e-4; [7] flips
                 const double r = fabs(T - T_ref) / c.t_term;

@@ -1,5 +1,5 @@
-mkdir -p gpurun_out/r02k
-(time QGS_PARITY_OUT=gpurun_out/r02k timeout 1500 python -m pytest tests -m gpu -q -rf) > gpurun_out/r02k_tests.log 2>&1; echo "tests rc=$?"
-tail -4 gpurun_out/r02k_tests.log
-timeout 900 python bench.py > gpurun_out/r02k_bench.log 2>&1; echo "bench rc=$?"
-tail -1 gpurun_out/r02k_bench.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print('value',d['value'],'e2e',d['e2e']['value'],'fwd',r['fwd_ms_per_step']/8,'bwd',r['bwd_ms_per_step']/8, 'frac', r['frac'], 'cpu', d['cpu_baseline']['value'], d['cpu_baseline']['sample'])"
+for f in "" "-DQGS_TERM_BAND=1e-30" "-DQGS_TERM_NOP=1" "-DQGS_TERM_BAND=-1.0"; do
+  QGS_BUILD_DEBUG=0 QGS_NVCC_EXTRA="$f" python -c "from paper_2411_16392_b200 import build as b; b.build(force=True)" > /dev/null 2>&1
+  echo "== $f"; timeout 300 python tools/term_debug.py c1 s_sh3 2>&1 | grep flips
+  timeout 300 python tools/term_debug.py c1 2>&1 | grep flips
+done
