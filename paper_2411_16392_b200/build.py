@@ -70,17 +70,27 @@ def _build(obj_dir, lib, defines, force, verbose):
     hdrs = [os.path.join(CSRC, h) for h in sorted(os.listdir(CSRC)) if h.endswith(".cuh")]
     hdrs.append(os.path.join(INCLUDE, "qgs_b200.h"))
     objs = []
+    relinked = False
+    extra = os.environ.get("QGS_NVCC_EXTRA", "").split()   # experiments only
     for unit, flags in UNITS.items():
         src = os.path.join(CSRC, unit)
         obj = os.path.join(obj_dir, unit.replace(".cu", ".o"))
         objs.append(obj)
-        if force or _stale(obj, [src] + hdrs):
-            extra = os.environ.get("QGS_NVCC_EXTRA", "").split()   # experiments only
-            cmd = [nvcc(), *ARCH, *COMMON, *flags, *defines, *extra, "-c", src, "-o", obj]
+        cmd = [nvcc(), *ARCH, *COMMON, *flags, *defines, *extra, "-c", src, "-o", obj]
+        # the command line is part of the object's identity: an experiment
+        # build (QGS_NVCC_EXTRA) is never mistaken for the product
+        stamp = obj + ".cmd"
+        same_cmd = os.path.exists(stamp) and open(stamp).read() == " ".join(cmd)
+        if force or not same_cmd or _stale(obj, [src] + hdrs):
             if verbose:
                 print(" ".join(cmd))
+            if os.path.exists(stamp):
+                os.remove(stamp)
             subprocess.check_call(cmd)
-    if force or _stale(lib, objs):
+            with open(stamp, "w") as f:
+                f.write(" ".join(cmd))
+            relinked = True
+    if force or relinked or _stale(lib, objs):
         cmd = [nvcc(), *ARCH, "-shared", "-o", lib, *objs]
         if verbose:
             print(" ".join(cmd))

@@ -1,3 +1,7 @@
-python -c "from paper_2411_16392_b200 import build as b; b.build(force=True, debug=False)" > /dev/null 2>&1
-timeout 600 python bench.py --steps 4 --warmup 3 --no-cpu --no-e2e --fp32-decisions > /tmp/b.log 2>&1; tail -1 /tmp/b.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print('fp32 value %.2f fwd %.3f bwd %.3f' % (d['value'], r['fwd_ms_per_step']/8, r['bwd_ms_per_step']/8))"
-timeout 600 python bench.py --steps 4 --warmup 3 --no-cpu --no-e2e > /tmp/b.log 2>&1; tail -1 /tmp/b.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print('exact value %.2f fwd %.3f bwd %.3f' % (d['value'], r['fwd_ms_per_step']/8, r['bwd_ms_per_step']/8))"
+python -m paper_2411_16392_b200.build > /dev/null 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_known_answers.py tests/test_debug_checks.py -q 2>&1 | grep -E "FAILED|passed|failed" | head -20
+echo "== counters build"
+QGS_BUILD_DEBUG=0 QGS_NVCC_EXTRA="-DQGS_UTIL_COUNTERS=1" python -m paper_2411_16392_b200.build > /dev/null 2>&1
+timeout 300 python tools/term_debug.py c1 s_sh3 2>&1 | grep flips
+python tools/lane_util_fwd.py --config c3 | head -2
+bash tools/gpu_wpc.sh "-DQGS_TERM_BAND=2e-5" "-DQGS_TERM_BAND=-1.0" "-DQGS_TERM_BAND=1e-4"
