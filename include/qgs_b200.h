@@ -232,10 +232,8 @@ int qgs_export_prep_geometry(const qgs_params *prims, const void *prep, const qg
 int qgs_pixel_dirs(const qgs_camera *cam, double *dirs, qgs_stream_t stream);
 
 /* Diagnostics build counters (QGS_UTIL_COUNTERS; 0 entries otherwise): copies
- * and clears up to n (<= 8) of [float64 band re-decisions, near-tangent roots
- * decided by the fp64 closed form, float64 termination re-decisions, of those
- * with |T - T_ref| / t_term above 1e-5 / 3e-5 / 1e-4 / 3e-4, decisions the
- * float64 transmittance changed].  Returns the number copied. */
+ * and clears up to n of [float64 band re-decisions, near-tangent roots decided
+ * by the fp64 closed form].  Returns the number copied. */
 int qgs_diag_counters(unsigned long long *out, int n);
 
 /* Diagnostics: replay one pixel's fragment stream (same device functions as

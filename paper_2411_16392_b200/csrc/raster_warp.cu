@@ -544,28 +544,7 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
 #endif
         }
         nfrag++;
-        if (M == MODE_EXACT && log_on && fabs(T - c.t_term) <= QGS_TERM_BAND * c.t_term) {
-#if QGS_TERM_NOP
-            const double T_ref = T;
-#else
-            const double T_ref = exact_transmittance(geo, out.frag_prim, out.frag_t, sm.pages,
-                                                     nfrag, lane, ray64[0], ray64[1], ray64[2],
-                                                     c.euclid, c.alpha_clamp64);
-#endif
-#if QGS_UTIL_COUNTERS
-            {   // [3..6]: |T - T_ref| / t_term above 1e-5, 3e-5, 1e-4, 3e-4; [7] flips
-                const double r = fabs(T - T_ref) / c.t_term;
-                if (r > 1e-5) atomicAdd(&qgs_diag[3], 1ull);
-                if (r > 3e-5) atomicAdd(&qgs_diag[4], 1ull);
-                if (r > 1e-4) atomicAdd(&qgs_diag[5], 1ull);
-                if (r > 3e-4) atomicAdd(&qgs_diag[6], 1ull);
-                if ((T_ref < c.t_term) != (T < c.t_term)) atomicAdd(&qgs_diag[7], 1ull);
-            }
-#endif
-            if (T_ref < c.t_term) alive = false;
-        } else if (T < c.t_term) {
-            alive = false;
-        }
+        if (T < c.t_term) alive = false;
     };
 
     // Batch of up to WB queued entries: stage their records, run the coarse
@@ -1428,9 +1407,9 @@ size_t fwd_smem_per_warp() { return sizeof(FwdSmem); }
 int diag_counters(unsigned long long *out, int n)
 {
 #if QGS_UTIL_COUNTERS
-    if (n > 8) n = 8;
+    if (n > 4) n = 4;
     if (cudaMemcpyFromSymbol(out, qgs_diag, sizeof(unsigned long long) * n) != cudaSuccess) return -1;
-    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const unsigned long long z[4] = {0, 0, 0, 0};
     cudaMemcpyToSymbol(qgs_diag, z, sizeof(z));
     return n;
 #else
@@ -1515,7 +1494,7 @@ __global__ void trace_pixel_kernel(const PrimRec *__restrict__ recs, const Geo64
     const float dx = (float)d[0], dy = (float)d[1], dz = (float)d[2];
     const int tile = (v / TILE) * cam.tiles_x + u / TILE;
     Ring R{&ring_t[0][0], &ring_p[0][0], 0};
-    double T = 1.0, T_ref = 1.0;
+    double T = 1.0;
     int na = 0, ne = 0;
     bool alive = true;
     auto record = [&](int ep, double et) {
@@ -1524,10 +1503,7 @@ __global__ void trace_pixel_kernel(const PrimRec *__restrict__ recs, const Geo64
         if (ne < max) { em_prim[ne] = ep; em_t[ne] = (float)et; em_abar[ne] = f.abar; em_T[ne] = T; }
         ne++;
         T *= 1.0 - f.abar64;
-        // the forward's termination rule, float64 transmittance inside the band
-        T_ref *= 1.0 - abar_ref64(geo[ep], d[0], d[1], d[2], et, c.euclid, c.alpha_clamp64);
-        const bool band = st.exact && fabs(T - c.t_term) <= QGS_TERM_BAND * c.t_term;
-        if ((band ? T_ref : T) < c.t_term) alive = false;
+        if (T < c.t_term) alive = false;
     };
     for (int i = tile_offsets[tile]; i < tile_offsets[tile + 1] && alive; ++i) {
         const int p = tile_prims[i];

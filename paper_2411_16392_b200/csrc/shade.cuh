@@ -249,7 +249,7 @@ constexpr float FLOOR_BAND = 1e-4f;        // alpha G >= alpha_floor
 #if QGS_UTIL_COUNTERS
 // diagnostics build: [0] exact64 calls (band cases), [1] near-tangent roots
 // decided by the fp64 closed form; read by tools/lane_util_fwd.py
-__device__ unsigned long long qgs_diag[8];
+__device__ unsigned long long qgs_diag[4];
 #endif
 
 static __device__ __noinline__ unsigned exact64(const Geo64 *gp, const double dh[3], double t64,
@@ -275,53 +275,6 @@ static __device__ __noinline__ unsigned exact64(const Geo64 *gp, const double dh
     if (!(l <= 3.0 * sig)) return 0u;
     const double G = exp(-(l * l) / (2.0 * sig * sig));
     return 1u | (g.alpha * G < floor ? 0u : 2u);
-}
-
-// Termination decision in MODE_EXACT (raster_kernels.py:152-157: T *= 1 -
-// abar; stop when T < t_term).  The running T multiplies weights re-shaded in
-// fp32 (relative error ~1e-6 each), so when it lands within QGS_TERM_BAND of
-// t_term the decision is re-made on the transmittance with the reference's
-// float64 weights, recomputed over the pixel's fragment log (its n logged
-// fragments in composite order).  Out of line: ~1e-3 of the pixels.
-#ifndef QGS_TERM_BAND
-#define QGS_TERM_BAND 1e-3
-#endif
-// the reference's float64 blend weight of a composited fragment at depth t
-// (raster_kernels.py:59-62 via fragment_geometry: G at the hit, abar = alpha G,
-// clamped)
-__device__ inline double abar_ref64(const Geo64 &g, double d0, double d1, double d2, double t,
-                                    bool euclid, double clamp)
-{
-    const bool planar = g.planar != 0.0;
-    const double dh0 = g.M[0] * d0 + g.M[1] * d1 + g.M[2] * d2;
-    const double dh1 = g.M[3] * d0 + g.M[4] * d1 + g.M[5] * d2;
-    const double x = g.ohat[0] + t * dh0, y = g.ohat[1] + t * dh1;
-    const double rho = sqrt(x * x + y * y);
-    double c = 1.0, s = 0.0;
-    if (rho > 1e-12) { c = x / rho; s = y / rho; }
-    const double a = planar ? 0.0 : g.sv[2] * (g.wv[0] * c * c + g.wv[1] * s * s);
-    const double l = (planar || euclid) ? rho : arc_length64(a, rho);
-    const double sig = sigma_dir64(g.sv[0], g.sv[1], c, s);
-    const double G = exp(-(l * l) / (2.0 * sig * sig));
-    const double abar = g.alpha * G;
-    return abar > clamp ? clamp : abar;
-}
-
-static __device__ __noinline__ double exact_transmittance(const Geo64 *geo, const int32_t *fprim,
-                                                          const double *ft, const int *pages,
-                                                          int n, int lane, double d0, double d1,
-                                                          double d2, bool euclid, double clamp)
-{
-#if QGS_UTIL_COUNTERS
-    atomicAdd(&qgs_diag[2], 1ull);
-#endif
-    double T = 1.0;
-    for (int k = 0; k < n; ++k) {
-        const size_t o =
-            ((size_t)pages[k / QGS_FRAG_PAGE] * QGS_FRAG_PAGE + (k % QGS_FRAG_PAGE)) * 32 + lane;
-        T *= 1.0 - abar_ref64(geo[fprim[o]], d0, d1, d2, ft[o], euclid, clamp);
-    }
-    return T;
 }
 
 // exact selection + weight at an fp64 depth; false if the root is rejected.

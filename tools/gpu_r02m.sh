@@ -1,6 +1,5 @@
-mkdir -p gpurun_out/r02m
-timeout 1500 python tools/parity_report.py --scenes golden,c1,c2,c5 --views 1 --out gpurun_out/r02m/parity_golden_c1_c2_c5.json > gpurun_out/r02m/parity.log 2>&1; echo "parity rc=$?"
-for c in c1 c2 c4 c5; do
-  timeout 900 python bench.py --config $c --steps 3 --warmup 3 --no-cpu > gpurun_out/r02m/bench_$c.log 2>&1; echo "bench $c rc=$?"
-  tail -1 gpurun_out/r02m/bench_$c.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$c', 'value %.2f e2e %.2f ms %.1f' % (d['value'], d['e2e']['value'], d['ms_per_step']))"
-done
+python -m paper_2411_16392_b200.build > /dev/null 2>&1
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | grep -E "FAILED|passed|failed" | head -20
+echo "== counters build (no other change)"
+QGS_BUILD_DEBUG=0 QGS_NVCC_EXTRA="-DQGS_UTIL_COUNTERS=1" python -m paper_2411_16392_b200.build > /dev/null 2>&1
+timeout 300 python tools/term_debug.py c1 s_sh3 s_default 2>&1 | grep flips

@@ -22,19 +22,16 @@ dev = rz.DevicePrimitives.from_host(sc.prims)
 prep = rz.prepare(dev, sc.cams[0])
 import ctypes  # noqa: E402
 from paper_2411_16392_b200 import _lib  # noqa: E402
-diag = (ctypes.c_ulonglong * 8)()
-_lib.load().qgs_diag_counters(diag, 8)                   # clear
+diag = (ctypes.c_ulonglong * 4)()
+_lib.load().qgs_diag_counters(diag, 4)                   # clear
 cnt = torch.zeros(8, dtype=torch.int64, device="cuda")
 rz.forward(prep, counters=cnt)
 torch.cuda.synchronize()
-n = _lib.load().qgs_diag_counters(diag, 8)
+n = _lib.load().qgs_diag_counters(diag, 4)
 c = cnt.cpu().tolist()
 if n >= 2:
     print(f"fp64 band re-decisions {diag[0]:.3e} ({diag[0] / max(c[4], 1):.2e} per exact test), "
-          f"near-tangent fp64 roots {diag[1]:.3e}, float64 termination re-decisions {diag[2]:.3e}")
-if n >= 8:
-    print(f"termination: |T - T_ref| / t_term > 1e-5: {diag[3]}, > 3e-5: {diag[4]}, > 1e-4: {diag[5]}, "
-          f"> 3e-4: {diag[6]}; decisions changed: {diag[7]}")
+          f"near-tangent fp64 roots {diag[1]:.3e}")
 print(f"in-box {c[0]:.3e} conic {c[3]:.3e} coarse {c[4]:.3e} accepted {c[1]:.3e} composited {c[2]:.3e}")
 if c[5]:
     print(f"pass 1: {c[3]:.3e} lane-candidates in {c[5]:.3e} lane slots -> utilisation {c[3] / c[5]:.3f}")
