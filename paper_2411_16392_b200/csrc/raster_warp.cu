@@ -689,7 +689,12 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
         while (qn >= WB) {
             run_batch(WB);
             qn -= WB;
-            if (lane < qn) { sm.qprim[lane] = sm.qprim[WB + lane]; sm.qmask[lane] = sm.qmask[WB + lane]; }
+            // shift the queue down by WB (overlapping ranges: read, sync, write)
+            int qp = 0;
+            uint32_t qm = 0u;
+            if (lane < qn) { qp = sm.qprim[WB + lane]; qm = sm.qmask[WB + lane]; }
+            __syncwarp();
+            if (lane < qn) { sm.qprim[lane] = qp; sm.qmask[lane] = qm; }
             __syncwarp();
             if (!__any_sync(FULL, alive)) { qn = 0; an = 0; return false; }
         }
