@@ -213,9 +213,6 @@ __device__ __forceinline__ uint32_t conic_rows(const ConicRec &q, int bu, int bv
 #ifndef QGS_RED_SINGLES
 #define QGS_RED_SINGLES 1
 #endif
-#ifndef QGS_RED_DUAL
-#define QGS_RED_DUAL 0        // group rows stored twice (XOR-swizzled halves): conflict-free
-#endif
 
 __device__ __forceinline__ PrimRec load_rec(const PrimRec *p)
 {
@@ -344,16 +341,7 @@ enum { A_C0 = 0, A_A = 3, A_D = 4, A_D2 = 5, A_N0 = 6, A_K = 9, A_DIST = 10 };
 // row stride of the backward's reduction buffer: 20 floats (80 B) puts the
 // 16-byte stores of 8 consecutive lanes in distinct bank groups (16 would
 // put every other lane on the same banks)
-#if QGS_RED_DUAL
-// a 128-byte row per lane: float4 q of the row's gradient at slot q ^ (row & 3)
-// (copy A, banks 0-15) and 4 + (q ^ (row & 3)) (copy B, banks 16-31).  The
-// reading lane sets alternate copies, so a quarter-warp's two sets never share
-// a bank; writers alternate copies by lane so 8 lanes hit 8 distinct slots.
-constexpr int KGP = 2 * KG;
-static_assert(KG == 16 && QGS_RED_SETS == 8, "dual reduction rows: 16 slots, 8 lane sets");
-#else
 constexpr int KGP = KG + 4;
-#endif
 
 struct BwdSmem {
     PrimRec rec[WB];        // replay path
@@ -1075,17 +1063,8 @@ __device__ __forceinline__ void warp_accumulate(float (*red)[33][KGP], bool emit
 #endif
     if (shared_grp) {
         float4 *dst = reinterpret_cast<float4 *>(red[w][lane]);
-#if QGS_RED_DUAL
-        const int sw = lane & 3, hsel = (lane >> 2) & 1;
-#pragma unroll
-        for (int m = 0; m < 2 * KG / 4; ++m) {
-            const int q = m >> 1, half = (m ^ hsel) & 1;
-            dst[half * 4 + (q ^ sw)] = make_float4(g[4 * q], g[4 * q + 1], g[4 * q + 2], g[4 * q + 3]);
-        }
-#else
 #pragma unroll
         for (int q = 0; q < KG / 4; ++q) dst[q] = make_float4(g[4 * q], g[4 * q + 1], g[4 * q + 2], g[4 * q + 3]);
-#endif
     }
     unsigned leaders = __ballot_sync(FULL, shared_grp && (peers & ((1u << lane) - 1u)) == 0);
     __syncwarp();
@@ -1127,12 +1106,7 @@ __device__ __forceinline__ void warp_accumulate(float (*red)[33][KGP], bool emit
             for (unsigned mm = grp; mm;) {             // two independent partial sums
                 const int i0 = __ffs(mm) - 1; mm &= mm - 1;
                 const int i1 = mm ? __ffs(mm) - 1 : 32; mm &= mm - 1;
-#if QGS_RED_DUAL
-                const int h4 = (set & 1) * 4;         // this set's copy
-                const float4 x = red4[i0][h4 + (q ^ (i0 & 3))], y = red4[i1][h4 + (q ^ (i1 & 3))];
-#else
                 const float4 x = red4[i0][q], y = red4[i1][q];
-#endif
                 a.x += x.x; a.y += x.y; a.z += x.z; a.w += x.w;
                 b.x += y.x; b.y += y.y; b.z += y.z; b.w += y.w;
             }
@@ -1163,7 +1137,7 @@ __device__ __forceinline__ void bwd_block(const PrimRec *__restrict__ recs,
     extern __shared__ __align__(16) unsigned char raster_smem[];
     BwdSmem &sm = reinterpret_cast<BwdSmem *>(raster_smem)[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
-    if (lane < KGP) sm.red[0][32][lane] = 0.f;       // zero row for padded group sums
+    if (lane < KG) sm.red[0][32][lane] = 0.f;        // zero row for padded group sums
     __syncwarp();
     int tile, blk, u, v;
     block_pixel(cam.tiles_x, fwd.tile_order, tile, blk, u, v, slot);

@@ -1,4 +1,4 @@
-# conflict-free dual reduction rows in the backward: parity + A/B
-QGS_BUILD_DEBUG=0 QGS_NVCC_EXTRA="-DQGS_RED_DUAL=1" python -m paper_2411_16392_b200.build > /dev/null 2>&1
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_known_answers.py -q 2>&1 | tail -1
-bash tools/gpu_wpc.sh "" "-DQGS_RED_DUAL=1" "-DQGS_RED_DUAL=1 -DQGS_BWD_MIN_BLOCKS=16" ""
+QGS_BUILD_DEBUG=0 QGS_NVCC_EXTRA="-DQGS_UTIL_COUNTERS=1" python -c "from paper_2411_16392_b200 import build as b; b.build(force=True)" > /dev/null 2>&1
+python tools/lane_util_fwd.py --config c3
+python tools/lane_util_fwd.py --config c4
+python tools/lane_util_fwd.py --config c5
