@@ -1246,18 +1246,7 @@ __device__ __forceinline__ void bwd_block(const PrimRec *__restrict__ recs,
             }
             return;
         }
-#if defined(QGS_EXP_DIRECT_ATOMICS)
-        if (emit) {
-            float4 *dst = reinterpret_cast<float4 *>(kg + (size_t)ep * KG);
-#pragma unroll
-            for (int q = 0; q < KG / 4; ++q)
-                atomicAdd(dst + q, make_float4(g[4 * q], g[4 * q + 1], g[4 * q + 2], g[4 * q + 3]));
-        }
-#elif !defined(QGS_EXP_NO_REDUCE)
         warp_accumulate(sm.red, emit, ep, g, kg);
-#else   // experiment: no cross-lane reduction
-        if (emit) { float z = 0.f; for (int q = 0; q < KG; ++q) z += g[q]; if (z == 1234.5f) kg[ep] = z; }
-#endif
     };
 
     // Fragment log written by the forward: the composited sequence of every
