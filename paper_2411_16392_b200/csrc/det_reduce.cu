@@ -13,11 +13,17 @@
 //   2. The backward kernel writes each fragment's 16 kernel-gradient slots
 //      to its row (and the primitive id beside it) instead of adding them.
 //   3. A stable radix sort of (primitive id, row) groups the rows of each
-//      primitive in row order; det_reduce_kernel sums each primitive's rows
-//      in that order in fp64 (warp per primitive, fixed lane assignment and
-//      a fixed shuffle tree) and adds the rounded sum to kg.
+//      primitive in row order.  Each primitive's segment is cut into chunks
+//      whose length depends on the segment length alone (256 rows, ~sqrt(n)
+//      for long segments); a warp per chunk sums its rows in fp64 (fixed lane
+//      assignment, one fixed shuffle), then the chunk sums of a primitive are
+//      added in chunk order and the rounded total goes to kg.  (A warp per
+//      whole primitive left the screen-sized primitives of C4 -- 10^5-10^6
+//      rows each -- as a 90 ms serial tail.)
 //
 // Same bits on every run, and fp64 accumulation instead of fp32 atomics.
+#include <algorithm>
+
 #include <cub/cub.cuh>
 
 #include "kernels.cuh"
@@ -58,22 +64,68 @@ __global__ void det_bounds_kernel(const uint32_t *__restrict__ keys, int64_t n, 
     start[p] = lo;
 }
 
-// warp per primitive: lane l sums slot (l & 15) over rows half (l >> 4),
-// (l >> 4) + 2, ... of the primitive's segment in fp64; halves combined by
-// one shuffle (fixed order)
-__global__ void det_reduce_kernel(const int64_t *__restrict__ start,
-                                  const uint32_t *__restrict__ order,
-                                  const float *__restrict__ rows, int P, float *__restrict__ kg)
+// rows per chunk of a primitive's sorted segment: a function of its length only
+__device__ __forceinline__ int64_t det_chunk_rows(int64_t len)
 {
-    const int p = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
-    const int lane = threadIdx.x & 31;
+    const int64_t r = (int64_t)sqrt((double)len);
+    return r > 256 ? (r + 31) & ~(int64_t)31 : 256;
+}
+
+__global__ void det_nchunks_kernel(const int64_t *__restrict__ start, int P,
+                                   int32_t *__restrict__ nchunk)
+{
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p > P) return;
+    int32_t n = 0;
+    if (p < P) {
+        const int64_t len = start[p + 1] - start[p];
+        if (len > 0) n = (int32_t)((len + det_chunk_rows(len) - 1) / det_chunk_rows(len));
+    }
+    nchunk[p] = n;
+}
+
+// chunk -> primitive map (chunks of a primitive are consecutive)
+__global__ void det_owner_kernel(const int64_t *__restrict__ coff, int P, int32_t *__restrict__ owner)
+{
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= P) return;
-    const int slot = lane & 15, half = lane >> 4;
-    const int64_t a = start[p], b = start[p + 1];
+    for (int64_t c = coff[p]; c < coff[p + 1]; ++c) owner[c] = p;
+}
+
+// warp per chunk: lane l sums slot (l & 15) over the chunk's rows half
+// (l >> 4), (l >> 4) + 2, ... in fp64; the halves combine by one shuffle
+__global__ void det_chunk_kernel(const int64_t *__restrict__ start, const int64_t *__restrict__ coff,
+                                 const int32_t *__restrict__ owner, const uint32_t *__restrict__ order,
+                                 const float *__restrict__ rows, int P, double *__restrict__ part)
+{
+    const int64_t n_chunks = coff[P];
+    const int lane = threadIdx.x & 31, slot = lane & 15, half = lane >> 4;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < n_chunks;
+         c += warps) {
+        const int p = owner[c];
+        const int64_t s0 = start[p], len = start[p + 1] - s0, cr = det_chunk_rows(len);
+        const int64_t a = s0 + (c - coff[p]) * cr, b = min(a + cr, s0 + len);
+        double s = 0.0;
+#pragma unroll 4
+        for (int64_t j = a + half; j < b; j += 2) s += (double)rows[(size_t)order[j] * KG + slot];
+        s += __shfl_down_sync(0xffffffffu, s, 16);
+        if (half == 0) part[(size_t)c * KG + slot] = s;
+    }
+}
+
+// half-warp per primitive: the chunk sums in chunk order
+__global__ void det_combine_kernel(const int64_t *__restrict__ coff, const double *__restrict__ part,
+                                   int P, float *__restrict__ kg)
+{
+    const int p = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 4);
+    const int slot = threadIdx.x & 15;
+    if (p >= P) return;
+    const int64_t c0 = coff[p], c1 = coff[p + 1];
+    if (c1 == c0) return;
     double s = 0.0;
-    for (int64_t j = a + half; j < b; j += 2) s += (double)rows[(size_t)order[j] * KG + slot];
-    s += __shfl_down_sync(0xffffffffu, s, 16);
-    if (half == 0 && b > a) kg[(size_t)p * KG + slot] += (float)s;
+    for (int64_t c = c0; c < c1; ++c) s += part[(size_t)c * KG + slot];
+    kg[(size_t)p * KG + slot] += (float)s;
 }
 
 namespace {
@@ -86,15 +138,23 @@ struct DetWs {
     float *rows;
     uint32_t *prim, *prim_sorted, *idx, *idx_sorted;
     int64_t *start;
+    int32_t *nchunk, *owner;
+    int64_t *coff;
+    double *part;
     void *temp;
     size_t temp_bytes;
     size_t bytes;
 };
 
-size_t cub_temp_bytes(int64_t n_frags, int n_slots)
+// chunks of all segments: at most n_frags / 256 + one partial chunk per primitive
+inline int64_t max_chunks(int P, int64_t n_frags) { return n_frags / 256 + (int64_t)P + 1; }
+
+size_t cub_temp_bytes(int P, int64_t n_frags, int n_slots)
 {
-    size_t a = 0, b = 0;
+    size_t a = 0, b = 0, c = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, a, (const int32_t *)nullptr, (int64_t *)nullptr, n_slots);
+    cub::DeviceScan::ExclusiveSum(nullptr, c, (const int32_t *)nullptr, (int64_t *)nullptr, P + 1);
+    a = a > c ? a : c;
     cub::DeviceRadixSort::SortPairs(nullptr, b, (const uint32_t *)nullptr, (uint32_t *)nullptr,
                                     (const uint32_t *)nullptr, (uint32_t *)nullptr,
                                     (int64_t)(n_frags > 0 ? n_frags : 1));
@@ -115,7 +175,12 @@ DetWs det_ws(void *base, int P, int64_t n_frags, int n_slots)
     w.idx = reinterpret_cast<uint32_t *>(b + o);        o += al(nf * 4);
     w.idx_sorted = reinterpret_cast<uint32_t *>(b + o); o += al(nf * 4);
     w.start = reinterpret_cast<int64_t *>(b + o);       o += al(((size_t)P + 1) * 8);
-    w.temp_bytes = cub_temp_bytes(n_frags, n_slots);
+    w.nchunk = reinterpret_cast<int32_t *>(b + o);      o += al(((size_t)P + 1) * 4);
+    w.coff = reinterpret_cast<int64_t *>(b + o);        o += al(((size_t)P + 1) * 8);
+    const size_t nc = (size_t)max_chunks(P, n_frags);
+    w.owner = reinterpret_cast<int32_t *>(b + o);       o += al(nc * 4);
+    w.part = reinterpret_cast<double *>(b + o);         o += al(nc * KG * 8);
+    w.temp_bytes = cub_temp_bytes(P, n_frags, n_slots);
     w.temp = b + o;                                     o += al(w.temp_bytes);
     w.bytes = o;
     return w;
@@ -159,8 +224,18 @@ cudaError_t det_finish(int P, int64_t n_frags, int n_warps, void *ws, float *kg,
     }
     det_bounds_kernel<<<cdiv64((int64_t)P + 1, 256), 256, 0, s>>>(w.prim_sorted, n_frags, P,
                                                                   w.start);
-    det_reduce_kernel<<<cdiv64((int64_t)P * 32, 256), 256, 0, s>>>(w.start, w.idx_sorted, w.rows,
-                                                                    P, kg);
+    det_nchunks_kernel<<<cdiv64((int64_t)P + 1, 256), 256, 0, s>>>(w.start, P, w.nchunk);
+    size_t tb = w.temp_bytes;
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(w.temp, tb, w.nchunk, w.coff, P + 1, s);
+    if (e != cudaSuccess) return e;
+    det_owner_kernel<<<cdiv64(P, 256), 256, 0, s>>>(w.coff, P, w.owner);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t nc = max_chunks(P, n_frags);
+    const int grid = (int)std::min<int64_t>(cdiv64(nc * 32, 256), (int64_t)sms * 16);
+    det_chunk_kernel<<<grid, 256, 0, s>>>(w.start, w.coff, w.owner, w.idx_sorted, w.rows, P, w.part);
+    det_combine_kernel<<<cdiv64((int64_t)P * 16, 256), 256, 0, s>>>(w.coff, w.part, P, kg);
     return cudaGetLastError();
 }
 
