@@ -213,6 +213,9 @@ __device__ __forceinline__ uint32_t conic_rows(const ConicRec &q, int bu, int bv
 #ifndef QGS_RED_SINGLES
 #define QGS_RED_SINGLES 1
 #endif
+#ifndef QGS_RING_TREE
+#define QGS_RING_TREE 1       // full-ring minimum as a 3-level tree (same slot as the scan)
+#endif
 
 __device__ __forceinline__ PrimRec load_rec(const PrimRec *p)
 {
@@ -242,6 +245,40 @@ struct Ring {
     int n;
 };
 
+// minimum of a full ring, first slot among equal minima (the reference's
+// strict-< scan, raster_kernels.py:160-164).  A tree (left subtree = lower
+// slots, right replaces left only when strictly smaller) gives the same slot
+// as the linear scan with a 3-deep instead of an 8-deep compare chain.
+// Depths in the ring are never NaN (confirm_root rejects !(t > t_clip)).
+__device__ __forceinline__ void ring_min_full(const Ring &R, double &m, int &jm)
+{
+#if QGS_RING_TREE
+    static_assert(RING == 8, "tree minimum of 8 slots");
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = R.t[k * 32];
+    int i[8] = {0, 1, 2, 3, 4, 5, 6, 7};
+#pragma unroll
+    for (int w = 1; w < 8; w <<= 1)
+#pragma unroll
+        for (int k = 0; k < 8; k += 2 * w) {
+            const bool r = v[k + w] < v[k];
+            v[k] = r ? v[k + w] : v[k];
+            i[k] = r ? i[k + w] : i[k];
+        }
+    m = v[0];
+    jm = i[0];
+#else
+    m = R.t[0];
+    jm = 0;
+#pragma unroll
+    for (int k = 1; k < RING; ++k) {
+        const double tk = R.t[k * 32];
+        if (tk < m) { m = tk; jm = k; }
+    }
+#endif
+}
+
 // push an accepted fragment; true with (et, ep) when one is emitted
 // (raster_kernels.py:159-226: first minimum, strict <, emit incoming if nearer)
 __device__ __forceinline__ bool ring_push(Ring &R, double t, int prim, double &et, int &ep)
@@ -253,13 +290,9 @@ __device__ __forceinline__ bool ring_push(Ring &R, double t, int prim, double &e
         R.n++;
         return false;
     }
-    double m = R.t[0];
-    int jm = 0;
-#pragma unroll
-    for (int k = 1; k < RING; ++k) {
-        double tk = R.t[k * 32];
-        if (tk < m) { m = tk; jm = k; }
-    }
+    double m;
+    int jm;
+    ring_min_full(R, m, jm);
     if (t < m) { et = t; ep = prim; return true; }
     et = m;
     ep = R.p[jm * 32];
@@ -297,13 +330,9 @@ __device__ __forceinline__ bool ring_push_pay(Ring &R, float (*pay)[PAYN][32], i
         R.n++;
         return false;
     }
-    double m = R.t[0];
-    int jm = 0;
-#pragma unroll
-    for (int k = 1; k < RING; ++k) {
-        double tk = R.t[k * 32];
-        if (tk < m) { m = tk; jm = k; }
-    }
+    double m;
+    int jm;
+    ring_min_full(R, m, jm);
     if (t < m) { et = t; ep = prim; out = in; return true; }
     et = m;
     ep = R.p[jm * 32];

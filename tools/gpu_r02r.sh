@@ -1,0 +1,4 @@
+# full-ring minimum as a tree: parity (ties through the duplicate tests) + A/B
+python -m paper_2411_16392_b200.build > /dev/null 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_known_answers.py -q 2>&1 | tail -1
+bash tools/gpu_wpc.sh "" "-DQGS_RING_TREE=0" "" "-DQGS_RING_TREE=0"
