@@ -250,13 +250,13 @@ struct Ring {
 // slots, right replaces left only when strictly smaller) gives the same slot
 // as the linear scan with a 3-deep instead of an 8-deep compare chain.
 // Depths in the ring are never NaN (confirm_root rejects !(t > t_clip)).
-__device__ __forceinline__ void ring_min_full(const Ring &R, double &m, int &jm)
+__device__ __forceinline__ void ring_min(const Ring &R, int n, double &m, int &jm)
 {
 #if QGS_RING_TREE
     static_assert(RING == 8, "tree minimum of 8 slots");
     double v[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = R.t[k * 32];
+    for (int k = 0; k < 8; ++k) v[k] = k < n ? R.t[k * 32] : __longlong_as_double(0x7ff0000000000000LL);  // empty: +inf
     int i[8] = {0, 1, 2, 3, 4, 5, 6, 7};
 #pragma unroll
     for (int w = 1; w < 8; w <<= 1)
@@ -271,12 +271,15 @@ __device__ __forceinline__ void ring_min_full(const Ring &R, double &m, int &jm)
 #else
     m = R.t[0];
     jm = 0;
-#pragma unroll
-    for (int k = 1; k < RING; ++k) {
+    for (int k = 1; k < n; ++k) {
         const double tk = R.t[k * 32];
         if (tk < m) { m = tk; jm = k; }
     }
 #endif
+}
+__device__ __forceinline__ void ring_min_full(const Ring &R, double &m, int &jm)
+{
+    ring_min(R, RING, m, jm);
 }
 
 // push an accepted fragment; true with (et, ep) when one is emitted
@@ -304,12 +307,9 @@ __device__ __forceinline__ bool ring_push(Ring &R, double t, int prim, double &e
 // drain one entry (raster_kernels.py:227-270: first minimum, swap with last)
 __device__ __forceinline__ void ring_pop(Ring &R, double &et, int &ep)
 {
-    double m = R.t[0];
-    int jm = 0;
-    for (int k = 1; k < R.n; ++k) {
-        double tk = R.t[k * 32];
-        if (tk < m) { m = tk; jm = k; }
-    }
+    double m;
+    int jm;
+    ring_min(R, R.n, m, jm);
     et = m;
     ep = R.p[jm * 32];
     R.n--;
@@ -348,12 +348,9 @@ __device__ __forceinline__ bool ring_push_pay(Ring &R, float (*pay)[PAYN][32], i
 __device__ __forceinline__ void ring_pop_pay(Ring &R, float (*pay)[PAYN][32], int lane, double &et,
                                              int &ep, Pay &out)
 {
-    double m = R.t[0];
-    int jm = 0;
-    for (int k = 1; k < R.n; ++k) {
-        double tk = R.t[k * 32];
-        if (tk < m) { m = tk; jm = k; }
-    }
+    double m;
+    int jm;
+    ring_min(R, R.n, m, jm);
     et = m;
     ep = R.p[jm * 32];
 #pragma unroll
