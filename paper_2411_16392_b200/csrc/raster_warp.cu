@@ -1249,11 +1249,14 @@ __device__ __forceinline__ void bwd_block(const PrimRec *__restrict__ recs,
                 shade_emitted(r, gh, d64, dx, dy, dz, t, c, f);
             }
             const double w = f.abar64 * T;
-            const double V = (double)up.c0 * r.col[0] + (double)up.c1 * r.col[1] +
-                             (double)up.c2 * r.col[2] + ua64 + (double)up.d * t +
-                             (double)up.n0 * f.nc[0] + (double)up.n1 * f.nc[1] +
-                             (double)up.n2 * f.nc[2] + (double)up.k * f.K +
-                             (double)up.dist * (t * t * F0 - 2.0 * t * F1 + F2);
+            // the upstream-weighted value of the fragment, summed as a balanced
+            // tree (a 4-deep instead of a 10-deep float64 dependency chain)
+            const double V =
+                (((double)up.c0 * r.col[0] + (double)up.c1 * r.col[1]) +
+                 ((double)up.c2 * r.col[2] + ua64)) +
+                (((double)up.d * t + (double)up.n0 * f.nc[0]) +
+                 ((double)up.n1 * f.nc[1] + (double)up.n2 * f.nc[2])) +
+                ((double)up.k * f.K + (double)up.dist * (t * t * F0 - 2.0 * t * F1 + F2));
             pref += w * V;
             const float g_abar = (float)(T * V) - (float)(vtot - pref) / (float)(1.0 - f.abar64);
             frag_grad(r, f, dx, dy, dz, (float)w, g_abar, (float)(t * F0 - F1), up, c.euclid, g);
