@@ -1,0 +1,4 @@
+python -m paper_2411_16392_b200.build > /dev/null 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_known_answers.py -q 2>&1 | tail -1
+QGS_PARITY_OUT=gpurun_out/r02s2_parity timeout 900 python -m pytest tests/test_gpu_fullview.py -q 2>&1 | tail -1
+bash tools/gpu_wpc.sh "" ""
