@@ -37,12 +37,6 @@
 #ifndef QGS_NEWTON64
 #define QGS_NEWTON64 2      // fp64 Newton steps refining an accepted root
 #endif
-#ifndef QGS_NEWTON_BAL
-#define QGS_NEWTON_BAL 0      // balanced fp64 sums in the Newton step (measured: no gain)
-#endif
-#ifndef QGS_EVAL_RSQRT
-#define QGS_EVAL_RSQRT 0      // rho and direction from one rsqrt (measured: no gain)
-#endif
 #ifndef QGS_NEWTON_RCP64
 #define QGS_NEWTON_RCP64 1  // derivative inverse from rcp.approx.f64 (C3 forward -1.6 %)
 #endif
@@ -95,18 +89,9 @@ __device__ __forceinline__ void arc32_grad(float a, float rho, float l, float &d
 __device__ __forceinline__ bool eval_point(const PrimRec &r, float x, float y, bool planar,
                                            bool euclid, float k, Hit &h)
 {
-#if QGS_EVAL_RSQRT
-    // one reciprocal square root gives rho and the direction (no sqrt -> rcp chain)
-    const float r2 = fmaf(x, x, y * y);
-    const float ir = rsqrtf(fmaxf(r2, 1e-30f));
-    const float rho = r2 * ir;
-    float c = 1.f, s = 0.f;
-    if (rho > 1e-12f) { c = x * ir; s = y * ir; }
-#else
     float rho = sqrtf(fmaf(x, x, y * y));
     float c = 1.f, s = 0.f;
     if (rho > 1e-12f) { float ir = 1.f / rho; c = x * ir; s = y * ir; }
-#endif
     float a = planar ? 0.f : r.s3 * fmaf(r.w1 * c, c, r.w2 * s * s);
     float l = (planar || euclid) ? rho : arc32(a, rho);
     float sc = r.s2 * c, ss = r.s1 * s;
@@ -233,14 +218,8 @@ __device__ __forceinline__ double refine_depth(const Geo64 &g, const double dh[3
 #pragma unroll
     for (int it = 0; it < NEWTON64; ++it) {
         double x = ox + t * dh[0], y = oy + t * dh[1], z = oz + t * dh[2];
-#if QGS_NEWTON_BAL
-        // balanced sums: two independent halves per value (shorter fp64 chains)
-        double F = (w1 * x * x + w2 * y * y) - (iw3 * z + Alin * t * t);
-        double Fp = 2.0 * (w1 * x * dh[0] + w2 * y * dh[1]) - (iw3 * dh[2] + 2.0 * Alin * t);
-#else
         double F = w1 * x * x + w2 * y * y - iw3 * z - Alin * t * t;
         double Fp = 2.0 * (w1 * x * dh[0] + w2 * y * dh[1]) - iw3 * dh[2] - 2.0 * Alin * t;
-#endif
 #if QGS_NEWTON_RCP64
         double rf;      // ~2^-20 reciprocal straight from the fp64 MUFU (no conversions)
         asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rf) : "d"(Fp));
