@@ -213,6 +213,9 @@ __device__ __forceinline__ uint32_t conic_rows(const ConicRec &q, int bu, int bv
 #ifndef QGS_RED_SINGLES
 #define QGS_RED_SINGLES 1
 #endif
+#ifndef QGS_RED_RANKS
+#define QGS_RED_RANKS 1       // group leaders listed by rank in shared memory (no 8-step scan)
+#endif
 #ifndef QGS_RING_TREE
 #define QGS_RING_TREE 1       // full-ring minimum as a 3-level tree (same slot as the scan)
 #endif
@@ -375,6 +378,7 @@ struct BwdSmem {
     double ring_t[RING][32];
     int ring_p[RING][32];
     float red[1][33][KGP];  // row 32 stays zero (padding reads of the group sums)
+    int lead[32];           // reduction: lane of the r-th group leader
 };
 
 struct Cfg {
@@ -1068,8 +1072,9 @@ __device__ __forceinline__ void frag_grad(const PrimRec &r, const Frag &f, float
 // lane = 6 * set + q sums float4 slot q (slots 4q .. 4q+3) of the set-th
 // pending group over its members and issues one 16-byte vector atomic
 // (sm_90+ red.global.add.v4.f32): 6 atomics per group instead of 22.
-__device__ __forceinline__ void warp_accumulate(float (*red)[33][KGP], bool emit, int prim,
-                                                const float g[KG], float *__restrict__ kg)
+__device__ __forceinline__ void warp_accumulate(float (*red)[33][KGP], int *lead, bool emit,
+                                                int prim, const float g[KG],
+                                                float *__restrict__ kg)
 {
     const int lane = threadIdx.x & 31, w = 0;   // red: this warp's own buffer
     const unsigned key = emit ? (unsigned)prim : 0xffffffffu;
@@ -1092,7 +1097,11 @@ __device__ __forceinline__ void warp_accumulate(float (*red)[33][KGP], bool emit
 #pragma unroll
         for (int q = 0; q < KG / 4; ++q) dst[q] = make_float4(g[4 * q], g[4 * q + 1], g[4 * q + 2], g[4 * q + 3]);
     }
-    unsigned leaders = __ballot_sync(FULL, shared_grp && (peers & ((1u << lane) - 1u)) == 0);
+    const bool is_leader = shared_grp && (peers & ((1u << lane) - 1u)) == 0;
+    unsigned leaders = __ballot_sync(FULL, is_leader);
+#if QGS_RED_RANKS
+    if (is_leader) lead[__popc(leaders & ((1u << lane) - 1u))] = lane;
+#endif
     __syncwarp();
 #if QGS_RED_SETS == 16
     // sixteen sets of 2 lanes, each lane two float4 slots (q, q + 2)
@@ -1104,6 +1113,12 @@ __device__ __forceinline__ void warp_accumulate(float (*red)[33][KGP], bool emit
     constexpr int NSET = 8;
 #endif
     const float4 (*red4)[KGP / 4] = reinterpret_cast<const float4 (*)[KGP / 4]>(red[w]);
+#if QGS_RED_RANKS
+    const int n_lead = __popc(leaders);
+    for (int base = 0; base < n_lead; base += NSET) {
+        // leaders base .. base + NSET - 1 in lane order, one per lane set
+        const int ld = base + set < n_lead ? lead[base + set] : -1;
+#else
     while (leaders) {
         // the NSET lowest pending leaders (warp-uniform), one per lane set
         int ld = -1;
@@ -1113,6 +1128,7 @@ __device__ __forceinline__ void warp_accumulate(float (*red)[33][KGP], bool emit
             ld = set == k ? lk : ld;
             leaders &= leaders - 1;
         }
+#endif
         const unsigned grp = __shfl_sync(FULL, peers, ld < 0 ? 0 : ld);
         const int gp = __shfl_sync(FULL, prim, ld < 0 ? 0 : ld);
         if (ld >= 0) {
@@ -1275,7 +1291,7 @@ __device__ __forceinline__ void bwd_block(const PrimRec *__restrict__ recs,
             }
             return;
         }
-        warp_accumulate(sm.red, emit, ep, g, kg);
+        warp_accumulate(sm.red, sm.lead, emit, ep, g, kg);
     };
 
     // Fragment log written by the forward: the composited sequence of every
