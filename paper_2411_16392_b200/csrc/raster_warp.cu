@@ -213,9 +213,6 @@ __device__ __forceinline__ uint32_t conic_rows(const ConicRec &q, int bu, int bv
 #ifndef QGS_RED_SINGLES
 #define QGS_RED_SINGLES 1
 #endif
-#ifndef QGS_RED_COMPACT
-#define QGS_RED_COMPACT 1     // group rows contiguous (scan of group sizes): no member bit scan
-#endif
 #ifndef QGS_RED_RANKS
 #define QGS_RED_RANKS 1       // group leaders listed by rank in shared memory (no 8-step scan)
 #endif
@@ -1095,61 +1092,6 @@ __device__ __forceinline__ void warp_accumulate(float (*red)[33][KGP], int *lead
 #else
     const bool shared_grp = emit;
 #endif
-#if QGS_RED_COMPACT
-    // Rows of a group are made contiguous, groups in leader-lane order: an
-    // exclusive scan of the group sizes over the leaders gives each group's
-    // first row, each member writes at first row + its rank in the group.  A
-    // lane set then sums a run of rows (members in lane order, two partial
-    // sums -- the same order as a member bit scan, without its ffs chain).
-    static_assert(QGS_RED_SETS == 8, "compact reduction: eight sets of four lanes");
-    const unsigned lt = (1u << lane) - 1u;
-    const bool is_leader = shared_grp && (peers & lt) == 0;
-    const unsigned leaders = __ballot_sync(FULL, is_leader);
-    const int sz = is_leader ? __popc(peers) : 0;
-    int incl = sz;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(FULL, incl, o);
-        if (lane >= o) incl += y;
-    }
-    const int first = incl - sz;                       // at a leader: its group's first row
-    const int gfirst = __shfl_sync(FULL, first, shared_grp ? __ffs(peers) - 1 : lane);
-    if (shared_grp) {
-        float4 *dst = reinterpret_cast<float4 *>(red[w][gfirst + __popc(peers & lt)]);
-#pragma unroll
-        for (int q = 0; q < KG / 4; ++q) dst[q] = make_float4(g[4 * q], g[4 * q + 1], g[4 * q + 2], g[4 * q + 3]);
-    }
-    if (is_leader) lead[__popc(leaders & lt)] = lane;
-    __syncwarp();
-    {
-        const int set = lane >> 2, q = lane & 3;
-        constexpr int NSET = 8;
-        const float4 (*red4)[KGP / 4] = reinterpret_cast<const float4 (*)[KGP / 4]>(red[w]);
-        const int n_lead = __popc(leaders);
-        for (int base = 0; base < n_lead; base += NSET) {
-            const int ld = base + set < n_lead ? lead[base + set] : -1;
-            const int src = ld < 0 ? 0 : ld;
-            const int r0 = __shfl_sync(FULL, first, src), n = __shfl_sync(FULL, sz, src);
-            const int gp = __shfl_sync(FULL, prim, src);
-            if (ld >= 0) {
-                float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-                int i = r0;
-                for (; i + 1 < r0 + n; i += 2) {
-                    const float4 x = red4[i][q], y = red4[i + 1][q];
-                    a.x += x.x; a.y += x.y; a.z += x.z; a.w += x.w;
-                    b.x += y.x; b.y += y.y; b.z += y.z; b.w += y.w;
-                }
-                if (i < r0 + n) {
-                    const float4 x = red4[i][q];
-                    a.x += x.x; a.y += x.y; a.z += x.z; a.w += x.w;
-                }
-                a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
-                atomicAdd(reinterpret_cast<float4 *>(kg + (size_t)gp * KG) + q, a);
-            }
-        }
-    }
-    __syncwarp();
-#else
     if (shared_grp) {
         float4 *dst = reinterpret_cast<float4 *>(red[w][lane]);
 #pragma unroll
@@ -1216,7 +1158,6 @@ __device__ __forceinline__ void warp_accumulate(float (*red)[33][KGP], int *lead
         }
     }
     __syncwarp();
-#endif
 }
 
 // One raster block of the backward.  REPLAY = false: blocks with a fragment
