@@ -1072,43 +1072,16 @@ __device__ __forceinline__ void frag_grad(const PrimRec &r, const Frag &f, float
 // lane = 6 * set + q sums float4 slot q (slots 4q .. 4q+3) of the set-th
 // pending group over its members and issues one 16-byte vector atomic
 // (sm_90+ red.global.add.v4.f32): 6 atomics per group instead of 22.
-// The lane grouping of one reduction round depends only on which primitive
-// each lane emits, so it is computed before the fragment is shaded
-// (red_plan): the match / ballot latency then overlaps the shading instead
-// of following the gradient on the critical path.
-struct RedPlan {
-    unsigned peers, leaders;
-    bool single, shared_grp;
-};
-
-__device__ __forceinline__ RedPlan red_plan(int *lead, bool emit, int prim)
-{
-    const int lane = threadIdx.x & 31;
-    RedPlan pl;
-    pl.peers = __match_any_sync(FULL, emit ? (unsigned)prim : 0xffffffffu);
-#if QGS_RED_SINGLES
-    pl.single = emit && pl.peers == (1u << lane);
-#else
-    pl.single = false;
-#endif
-    pl.shared_grp = emit && !pl.single;
-    const bool is_leader = pl.shared_grp && (pl.peers & ((1u << lane) - 1u)) == 0;
-    pl.leaders = __ballot_sync(FULL, is_leader);
-#if QGS_RED_RANKS
-    if (is_leader) lead[__popc(pl.leaders & ((1u << lane) - 1u))] = lane;
-#endif
-    return pl;
-}
-
 __device__ __forceinline__ void warp_accumulate(float (*red)[33][KGP], int *lead, bool emit,
                                                 int prim, const float g[KG],
-                                                float *__restrict__ kg, const RedPlan &pl)
+                                                float *__restrict__ kg)
 {
     const int lane = threadIdx.x & 31, w = 0;   // red: this warp's own buffer
-    const unsigned peers = pl.peers;
+    const unsigned key = emit ? (unsigned)prim : 0xffffffffu;
+    const unsigned peers = __match_any_sync(FULL, key);
 #if QGS_RED_SINGLES
     // a lane alone with its primitive adds its row directly
-    const bool single = pl.single;
+    const bool single = emit && peers == (1u << lane);
     if (single) {
         float4 *dst = reinterpret_cast<float4 *>(kg + (size_t)prim * KG);
 #pragma unroll
@@ -1124,7 +1097,11 @@ __device__ __forceinline__ void warp_accumulate(float (*red)[33][KGP], int *lead
 #pragma unroll
         for (int q = 0; q < KG / 4; ++q) dst[q] = make_float4(g[4 * q], g[4 * q + 1], g[4 * q + 2], g[4 * q + 3]);
     }
-    unsigned leaders = pl.leaders;              // (lead[] filled by red_plan)
+    const bool is_leader = shared_grp && (peers & ((1u << lane) - 1u)) == 0;
+    unsigned leaders = __ballot_sync(FULL, is_leader);
+#if QGS_RED_RANKS
+    if (is_leader) lead[__popc(leaders & ((1u << lane) - 1u))] = lane;
+#endif
     __syncwarp();
 #if QGS_RED_SETS == 16
     // sixteen sets of 2 lanes, each lane two float4 slots (q, q + 2)
@@ -1267,7 +1244,6 @@ __device__ __forceinline__ void bwd_block(const PrimRec *__restrict__ recs,
     }
     auto emit_grad = [&](bool emit, int ep, double t, bool have_xy, float lx, float ly,
                          const PrimRec *staged) {
-        const RedPlan pl = DET ? RedPlan{0u, 0u, false, false} : red_plan(sm.lead, emit, ep);
         float g[KG];
         if (emit) {
             Frag f;
@@ -1315,7 +1291,7 @@ __device__ __forceinline__ void bwd_block(const PrimRec *__restrict__ recs,
             }
             return;
         }
-        warp_accumulate(sm.red, sm.lead, emit, ep, g, kg, pl);
+        warp_accumulate(sm.red, sm.lead, emit, ep, g, kg);
     };
 
     // Fragment log written by the forward: the composited sequence of every
