@@ -195,9 +195,6 @@ __global__ void pixel_rays_kernel(CamK cam, double *rays)
 // from the table and the float64 key with the reference's operation order.
 // (An fp32 pre-reject of rays that cannot hit the support was measured
 // slower: most pairs' vertex-nearest pixel does hit.)
-#ifndef QGS_KEY_PAIR2
-#define QGS_KEY_PAIR2 0          // two pairs per lane per iteration
-#endif
 #ifndef QGS_KEY_MIN_BLOCKS
 #define QGS_KEY_MIN_BLOCKS 2     // 128 registers, no spills: 2.74 -> 2.60 ms at C3 (3 and 4 measured)
 #endif
@@ -234,34 +231,6 @@ pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
             const long long iv = iv_v < vlo ? vlo : (iv_v > vhi ? vhi : iv_v);
             return (size_t)iv * cam.W + iu;
         };
-#if QGS_KEY_PAIR2
-        // two pairs per lane per iteration (pairs local and local + 32): their
-        // fp64 chains are independent
-        for (int local = lane; local < nt; local += 64) {
-            const bool hasb = local + 32 < nt;
-            const int tile_a = (ty0 + row) * cam.tiles_x + tx0 + col;
-            const size_t px_a = pixel_of(tx0 + col, ty0 + row);
-            col += dcol;
-            row += drow;
-            if (col >= ncols) { col -= ncols; ++row; }
-            const int tile_b = (ty0 + row) * cam.tiles_x + tx0 + col;
-            const size_t px_b = hasb ? pixel_of(tx0 + col, ty0 + row) : px_a;
-            col += dcol;
-            row += drow;
-            if (col >= ncols) { col -= ncols; ++row; }
-            const int slot_a = atomicAdd(&cursor[tile_a], 1);
-            const int slot_b = hasb ? atomicAdd(&cursor[tile_b], 1) : 0;
-            const double *ra = rays + 3 * px_a, *rb = rays + 3 * px_b;
-            const double ax = ra[0], ay = ra[1], az = ra[2], bx = rb[0], by = rb[1], bz = rb[2];
-            const double key_a = key_from_ray_fast(kp, ax, ay, az, euclid, st.t_clip);
-            const double key_b = key_from_ray_fast(kp, bx, by, bz, euclid, st.t_clip);
-            QGS_CHECK(slot_a >= 0 && slot_a < n_pairs);
-            bucket[slot_a] = sort_composite(key_a, p, st.pbits);
-            if (hasb) bucket[slot_b] = sort_composite(key_b, p, st.pbits);
-        }
-        (void)rays;
-        continue;
-#endif
         double cx = 0.0, cy = 0.0, cz = 0.0;
         if (lane < nt) {
             const double *ray = rays + 3 * pixel_of(tx0 + col, ty0 + row);
