@@ -215,40 +215,16 @@ __device__ inline void bounding_ellipsoid(const double s[3], bool planar, bool e
     double z0 = 9.0 * s[2] * (s[2] >= 0.0 ? lo : hi), z1 = 9.0 * s[2] * (s[2] >= 0.0 ? hi : lo);
     if (!euclid) { z0 = fmax(z0, -3.0 * smax); z1 = fmin(z1, 3.0 * smax); }
     const double h = 0.5 * (z1 - z0);
-#if QGS_CONIC_LAM_OPT
-    // E2 bounds the slab for any lam in (0, 1); pick the lam, and E1 or E2,
-    // with the smallest screen footprint, measured as the sum of the three
-    // axis-plane cross-sections ax ay + ax az + ay az (flat primitives want
-    // lam -> 1: tight in-plane axes; the volume criterion's lam = 0.75 widened
-    // them by 15 %).  Any choice is a valid bound: the cull stays exact.
-    const double a = 3.0 * m1, b = 3.0 * m2;
-    double lam = 0.75, best = 1e300;
-    const double cand[9] = {0.5, 0.6, 0.7, 0.8, 0.87, 0.92, 0.95, 0.97, 0.985};
-    for (int i = 0; i < 9; ++i) {
-        const double L = cand[i];
-        const double S = a * b / L + (a + b) * h / sqrt(L * (1.0 - L));
-        if (S < best) { best = S; lam = L; }
-    }
-    if (!euclid && a * b + (a + b) * 3.0 * smax <= best) {
-        zc = 0.0; ax[0] = 3.0 * m1; ax[1] = 3.0 * m2; ax[2] = 3.0 * smax;
-        return;
-    }
-#else
     const double lam = 0.75;
     // volumes: E1 27 m1 m2 smax, E2 9 m1 m2 h / (lam sqrt(1 - lam))
     if (!euclid && 27.0 * smax <= 9.0 * h / (lam * sqrt(1.0 - lam))) {
         zc = 0.0; ax[0] = 3.0 * m1; ax[1] = 3.0 * m2; ax[2] = 3.0 * smax;
         return;
     }
-#endif
     zc = 0.5 * (z0 + z1);
     const double il = 1.0 / sqrt(lam);
     ax[0] = 3.0 * m1 * il; ax[1] = 3.0 * m2 * il; ax[2] = h / sqrt(1.0 - lam);
 }
-
-#ifndef QGS_CONIC_LAM_OPT
-#define QGS_CONIC_LAM_OPT 1   // bounding-ellipsoid shape chosen for the smallest footprint
-#endif
 
 // 0.1% slack on every axis: the linear-branch root (|A| < 1e-6, t = -C/B)
 // sits A t^2 ~ 1e-5 off the quadric, and fp64 rounding
