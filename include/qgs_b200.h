@@ -233,7 +233,8 @@ int qgs_pixel_dirs(const qgs_camera *cam, double *dirs, qgs_stream_t stream);
 
 /* Diagnostics build counters (QGS_UTIL_COUNTERS; 0 entries otherwise): copies
  * and clears up to n of [float64 band re-decisions, near-tangent roots decided
- * by the fp64 closed form].  Returns the number copied. */
+ * by the fp64 closed form, candidates rejected by the coarse test's stage 1,
+ * by its stage 2].  Returns the number copied. */
 int qgs_diag_counters(unsigned long long *out, int n);
 
 /* Diagnostics: replay one pixel's fragment stream (same device functions as

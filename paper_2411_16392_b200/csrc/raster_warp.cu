@@ -624,8 +624,17 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
             unsigned s1 = coarse_stage1(sm.rec[j1], dx, dy, dz, c.t_clip, r1, hx1, hy1);
             s0 = a0 ? s0 : 0u;
             s1 = a1 ? s1 : 0u;
+#if QGS_UTIL_COUNTERS
+            // [2]: candidates the stage-1 test rejects (no root, behind the
+            // clip, or outside the widened ellipse); [3]: rejected by stage 2
+            if (a0 && !s0) atomicAdd(&qgs_diag[2], 1ull);
+            if (a1 && !s1) atomicAdd(&qgs_diag[2], 1ull);
+#endif
             if (s0) {
                 const unsigned p = (s0 & CR_MARGINAL) ? s0 : coarse_stage2(sm.rec[j], c.euclid, s0, r0, hx0, hy0);
+#if QGS_UTIL_COUNTERS
+                if (!p) atomicAdd(&qgs_diag[3], 1ull);
+#endif
                 if (p) {
                     bits |= 1u << j;
                     if (p & CR_MARGINAL) margb |= 1u << j;
@@ -635,6 +644,9 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
             }
             if (s1) {
                 const unsigned p = (s1 & CR_MARGINAL) ? s1 : coarse_stage2(sm.rec[j1], c.euclid, s1, r1, hx1, hy1);
+#if QGS_UTIL_COUNTERS
+                if (!p) atomicAdd(&qgs_diag[3], 1ull);
+#endif
                 if (p) {
                     bits |= 1u << j1;
                     if (p & CR_MARGINAL) margb |= 1u << j1;
