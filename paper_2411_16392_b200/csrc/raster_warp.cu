@@ -213,9 +213,6 @@ __device__ __forceinline__ uint32_t conic_rows(const ConicRec &q, int bu, int bv
 #ifndef QGS_RED_SINGLES
 #define QGS_RED_SINGLES 1
 #endif
-#ifndef QGS_RED_UNROLL4
-#define QGS_RED_UNROLL4 0     // four members per step of the group sum
-#endif
 #ifndef QGS_RED_RANKS
 #define QGS_RED_RANKS 1       // group leaders listed by rank in shared memory (no 8-step scan)
 #endif
@@ -1160,22 +1157,6 @@ __device__ __forceinline__ void warp_accumulate(float (*red)[33][KGP], int *lead
             atomicAdd(dst + q + 2, b);
 #else
             float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-#if QGS_RED_UNROLL4
-            float4 c4 = a, d4 = a;
-            for (unsigned mm = grp; mm;) {             // four independent partial sums
-                const int i0 = __ffs(mm) - 1; mm &= mm - 1;
-                const int i1 = mm ? __ffs(mm) - 1 : 32; mm &= mm - 1;
-                const int i2 = mm ? __ffs(mm) - 1 : 32; mm &= mm - 1;
-                const int i3 = mm ? __ffs(mm) - 1 : 32; mm &= mm - 1;
-                const float4 x = red4[i0][q], y = red4[i1][q], z = red4[i2][q], u = red4[i3][q];
-                a.x += x.x; a.y += x.y; a.z += x.z; a.w += x.w;
-                b.x += y.x; b.y += y.y; b.z += y.z; b.w += y.w;
-                c4.x += z.x; c4.y += z.y; c4.z += z.z; c4.w += z.w;
-                d4.x += u.x; d4.y += u.y; d4.z += u.z; d4.w += u.w;
-            }
-            a.x += c4.x; a.y += c4.y; a.z += c4.z; a.w += c4.w;
-            b.x += d4.x; b.y += d4.y; b.z += d4.z; b.w += d4.w;
-#else
             for (unsigned mm = grp; mm;) {             // two independent partial sums
                 const int i0 = __ffs(mm) - 1; mm &= mm - 1;
                 const int i1 = mm ? __ffs(mm) - 1 : 32; mm &= mm - 1;
@@ -1183,7 +1164,6 @@ __device__ __forceinline__ void warp_accumulate(float (*red)[33][KGP], int *lead
                 a.x += x.x; a.y += x.y; a.z += x.z; a.w += x.w;
                 b.x += y.x; b.y += y.y; b.z += y.z; b.w += y.w;
             }
-#endif
             a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
             atomicAdd(reinterpret_cast<float4 *>(kg + (size_t)gp * KG) + q, a);
 #endif
