@@ -620,8 +620,17 @@ __device__ __forceinline__ void fwd_block(const PrimRec *__restrict__ recs,
             const bool a0 = (cand >> j) & 1u, a1 = j1 != j && ((cand >> j1) & 1u);
             if (!(a0 || a1)) continue;
             float r0[2], r1[2], hx0, hy0, hx1, hy1;
+#if QGS_UTIL_COUNTERS
+            bool ok0 = true, ok1 = true;
+            unsigned s0 = coarse_stage1(sm.rec[j], dx, dy, dz, c.t_clip, r0, hx0, hy0, &ok0);
+            unsigned s1 = coarse_stage1(sm.rec[j1], dx, dy, dz, c.t_clip, r1, hx1, hy1, &ok1);
+            // [1] is reused here (near-tangent roots are counted in the exact pass)
+            if (a0 && !ok0) atomicAdd(&qgs_diag[1], 1ull << 32);
+            if (a1 && !ok1) atomicAdd(&qgs_diag[1], 1ull << 32);
+#else
             unsigned s0 = coarse_stage1(sm.rec[j], dx, dy, dz, c.t_clip, r0, hx0, hy0);
             unsigned s1 = coarse_stage1(sm.rec[j1], dx, dy, dz, c.t_clip, r1, hx1, hy1);
+#endif
             s0 = a0 ? s0 : 0u;
             s1 = a1 ? s1 : 0u;
 #if QGS_UTIL_COUNTERS

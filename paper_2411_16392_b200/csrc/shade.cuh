@@ -385,7 +385,7 @@ constexpr float COARSE_K = 1.05f;         // margin on the 3-sigma tests
 // Returns bit k = root k survives, CR_MARGINAL = near-tangent (fp64 decides).
 __device__ __forceinline__ unsigned coarse_stage1(const PrimRec &r, float dx, float dy, float dz,
                                                   float t_clip, float roots[2], float &hx,
-                                                  float &hy)
+                                                  float &hy, bool *has_root = nullptr)
 {
     const bool planar = (r.flags & 1u) != 0;
     hx = fmaf(r.M[0], dx, fmaf(r.M[1], dy, r.M[2] * dz));
@@ -419,6 +419,7 @@ __device__ __forceinline__ unsigned coarse_stage1(const PrimRec &r, float dx, fl
     const bool in1 = ok && quad && t1 > tmin && m1 <= lim;
     roots[0] = t0;
     roots[1] = t1;
+    if (has_root) *has_root = ok;          // diagnostics only
     return marg ? CR_MARGINAL : ((in0 ? 1u : 0u) | (in1 ? 2u : 0u));
 }
 

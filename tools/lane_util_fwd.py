@@ -31,10 +31,10 @@ n = _lib.load().qgs_diag_counters(diag, 4)
 c = cnt.cpu().tolist()
 if n >= 2:
     print(f"fp64 band re-decisions {diag[0]:.3e} ({diag[0] / max(c[4], 1):.2e} per exact test), "
-          f"near-tangent fp64 roots {diag[1]:.3e}")
+          f"near-tangent fp64 roots {diag[1] & 0xffffffff:.3e}")
 if n >= 4:
-    print(f"coarse rejects: stage 1 (no root / behind / outside the widened ellipse) {diag[2]:.3e}, "
-          f"stage 2 (geodesic 3 sigma) {diag[3]:.3e}")
+    print(f"coarse rejects: stage 1 {diag[2]:.3e} (of which the ray misses the quadric: "
+          f"{diag[1] >> 32:.3e}), stage 2 (geodesic 3 sigma) {diag[3]:.3e}")
 print(f"in-box {c[0]:.3e} conic {c[3]:.3e} coarse {c[4]:.3e} accepted {c[1]:.3e} composited {c[2]:.3e}")
 if c[5]:
     print(f"pass 1: {c[3]:.3e} lane-candidates in {c[5]:.3e} lane slots -> utilisation {c[3] / c[5]:.3f}")
