@@ -26,7 +26,9 @@ same fp32-drawn inputs:
   backward, which shows the violations come from the fp32 per-fragment
   arithmetic, not from the atomics' summation order.
 
-The oracle takes ~45 s (C3) and ~70 s (C4) of host time per view.
+C2 (100K primitives, 800x800) and C5 (300K degenerate primitives,
+1024x1024) get the same checks.  The oracle takes ~45 s (C3), ~70 s (C4)
+and a few seconds (C2, C5) of host time per view.
 """
 
 import numpy as np
@@ -133,3 +135,12 @@ def test_c3_full_view(cuda_device):
 
 def test_c4_full_view(cuda_device):
     _report("c4", *_check(*_fullview("c4", views=1)))
+
+
+def test_c2_full_view(cuda_device):
+    _report("c2", *_check(*_fullview("c2", views=1)))
+
+
+def test_c5_full_view(cuda_device):
+    # degenerate geometry: near-planar and needle primitives, grazing rays
+    _report("c5", *_check(*_fullview("c5", views=1)))
