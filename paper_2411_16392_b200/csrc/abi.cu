@@ -189,9 +189,11 @@ int qgs_bin(const void *prep, int32_t P, const qgs_camera *cam, const qgs_settin
         tile_offsets, ws.bucket, ws.tmp, pv, ck, sk, tile_prims, ws.order, ws.huge);
     QGS_LAUNCHED("tile_sort_kernel");
     // the huge tiles' buckets, SORT_CHUNKS CTAs per tile (most CTAs exit at once)
-    qgs::tile_sort_chunks_kernel<<<qgs::SORT_MAX_HUGE * qgs::sort_chunks(), qgs::sort_threads(),
-                                   qgs::sort_smem_bytes(), s>>>(tile_offsets, ws.tmp, pv, ck, sk,
-                                                                tile_prims, ws.huge);
+    int cdev = 0, csms = 148;
+    cudaGetDevice(&cdev);
+    cudaDeviceGetAttribute(&csms, cudaDevAttrMultiProcessorCount, cdev);
+    qgs::tile_sort_chunks_kernel<<<csms * 2, qgs::sort_threads(), qgs::sort_smem_bytes(), s>>>(
+        tile_offsets, ws.tmp, pv, ck, sk, tile_prims, ws.huge);
     QGS_LAUNCHED("tile_sort_chunks_kernel");
 
     return 0;

@@ -688,8 +688,12 @@ tile_sort_chunks_kernel(const int32_t *__restrict__ tile_offsets, const uint64_t
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SortSmem &sm = *reinterpret_cast<SortSmem *>(smem_raw);
-    const int h = (int)blockIdx.x / SORT_CHUNKS, j = (int)blockIdx.x % SORT_CHUNKS;
-    if (h >= min(huge->count, SORT_MAX_HUGE)) return;
+    // a persistent grid over the (huge tile, chunk) items: the count is only
+    // known on the device, and a grid sized for the maximum cost 0.15 ms of
+    // empty CTAs per view when there is no huge tile
+    const int n_items = min(huge->count, SORT_MAX_HUGE) * SORT_CHUNKS;
+    for (int w = (int)blockIdx.x; w < n_items; w += (int)gridDim.x) {
+    const int h = w / SORT_CHUNKS, j = w % SORT_CHUNKS;
     const HugeTile t = huge->t[h];
     const int start = tile_offsets[t.tile];
     const int *src = const_cast<HugeSort *>(huge)->bend_of(h);
@@ -705,6 +709,8 @@ tile_sort_chunks_kernel(const int32_t *__restrict__ tile_offsets, const uint64_t
     if (c0 < c1)
         sort_groups(sm, tmp + start, c0, c1, t.nb, bf, t.kmin, t.range, t.shift, t.tile, pv, cam,
                     st, tile_prims + start);
+    __syncthreads();                    // sm.bend is reloaded by the next item
+    }
 }
 
 // -------------------------------------------------------- debug / unit
