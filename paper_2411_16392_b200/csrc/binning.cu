@@ -17,6 +17,8 @@
 // order is (key ascending, prim ascending), a total order.
 //
 // Compiled with -fmad=false (keys must round exactly as the reference).
+#include <cuda_pipeline.h>
+
 #include "kernels.cuh"
 
 namespace qgs {
@@ -287,6 +289,17 @@ static_assert(SORT_MAX_BUCKETS == 8192, "kernels.cuh");
 #define QGS_SORT_L2_MIN 6                        // mean first-level bucket that takes the second level
 #endif
 constexpr int SORT_NB2 = 2048;                   // second-level buckets of a staged group
+// one register pass of items c0 + k * SORT_T + threadIdx.x (k < SORT_IPT) of
+// a[0, n): every load issued before any is used
+__device__ __forceinline__ void load_chunk(uint64_t (&v)[SORT_IPT], const uint64_t *a, int c0, int n)
+{
+#pragma unroll
+    for (int k = 0; k < SORT_IPT; ++k) {
+        const int i = c0 + k * SORT_T + (int)threadIdx.x;
+        v[k] = i < n ? a[i] : 0ull;
+    }
+}
+
 // a staged group uses the head of buf; its second-level bucket counts the tail
 constexpr int SORT_GROUP_ITEMS = SORT_SMEM_ITEMS - SORT_NB2 / 2;
 
@@ -427,8 +440,13 @@ __device__ __noinline__ void sort_group_l2(SortSmem &sm, const uint64_t *stage, 
     const BucketFn bf2{(uint32_t)glo, s2, nullptr, 0};
     for (int d = threadIdx.x; d < SORT_NB2; d += SORT_T) bend2[d] = 0;
     __syncthreads();
-    for (int i = threadIdx.x; i < cnt; i += SORT_T)
-        atomicAdd(&bend2[bf2(sort_h(stage[base + i]))], 1);
+    for (int c0 = 0; c0 < cnt; c0 += SORT_CHUNK) {
+        uint64_t v[SORT_IPT];
+        load_chunk(v, stage + base, c0, cnt);
+#pragma unroll
+        for (int k = 0; k < SORT_IPT; ++k)
+            if (c0 + k * SORT_T + (int)threadIdx.x < cnt) atomicAdd(&bend2[bf2(sort_h(v[k]))], 1);
+    }
     __syncthreads();
     {
         constexpr int PER = SORT_NB2 / SORT_T;
@@ -441,9 +459,12 @@ __device__ __noinline__ void sort_group_l2(SortSmem &sm, const uint64_t *stage, 
         for (int q = 0; q < PER; ++q) { bend2[threadIdx.x * PER + q] = ex; ex += c[q]; }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < cnt; i += SORT_T) {
-        const uint64_t v = stage[base + i];
-        sm.buf[atomicAdd(&bend2[bf2(sort_h(v))], 1)] = v;
+    for (int c0 = 0; c0 < cnt; c0 += SORT_CHUNK) {
+        uint64_t v[SORT_IPT];
+        load_chunk(v, stage + base, c0, cnt);
+#pragma unroll
+        for (int k = 0; k < SORT_IPT; ++k)
+            if (c0 + k * SORT_T + (int)threadIdx.x < cnt) sm.buf[atomicAdd(&bend2[bf2(sort_h(v[k]))], 1)] = v[k];
     }
     __syncthreads();
     for (int i = threadIdx.x; i < cnt; i += SORT_T) {
@@ -510,15 +531,15 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
     int shift = 0;
     while ((range >> shift) >= (uint32_t)nb) ++shift;
 
-    // histogram
+    // histogram (a tile over one register pass: the chunk's SORT_IPT loads
+    // are all issued before the first use -- load, use, load, use left one
+    // L2 read in flight per thread)
     for (int c0 = 0; c0 < n; c0 += SORT_CHUNK) {
+        if (!regs) load_chunk(it, src, c0, n);
 #pragma unroll
         for (int k = 0; k < SORT_IPT; ++k) {
             const int i = c0 + k * SORT_T + threadIdx.x;
-            if (i < n) {
-                const uint64_t v = regs ? it[k] : src[i];
-                atomicAdd(&sm.bend[((sort_h(v)) - kmin) >> shift], 1);
-            }
+            if (i < n) atomicAdd(&sm.bend[((sort_h(it[k])) - kmin) >> shift], 1);
         }
     }
     __syncthreads();
@@ -589,13 +610,13 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
     __syncthreads();
     // scatter into buckets
     for (int c0 = 0; c0 < n; c0 += SORT_CHUNK) {
+        if (!regs) load_chunk(it, src, c0, n);
 #pragma unroll
         for (int k = 0; k < SORT_IPT; ++k) {
             const int i = c0 + k * SORT_T + threadIdx.x;
             if (i < n) {
-                const uint64_t v = regs ? it[k] : src[i];
-                const int pos = atomicAdd(&sm.bend[bf(sort_h(v))], 1);
-                stage[pos] = v;
+                const int pos = atomicAdd(&sm.bend[bf(sort_h(it[k]))], 1);
+                stage[pos] = it[k];
             }
         }
     }
@@ -669,7 +690,10 @@ __device__ __forceinline__ void sort_groups(SortSmem &sm, const uint64_t *stage,
             const int cnt = sm.bend[g1 - 1] - base;
             if (cnt <= QGS_SORT_L2_MIN * (g1 - g0)) {
                 // first-level buckets already small: rank in them directly
-                for (int i = threadIdx.x; i < cnt; i += SORT_T) sm.buf[i] = stage[base + i];
+                for (int i = threadIdx.x; i < cnt; i += SORT_T)
+                    __pipeline_memcpy_async(&sm.buf[i], &stage[base + i], sizeof(uint64_t));
+                __pipeline_commit();
+                __pipeline_wait_prior(0);
                 __syncthreads();
                 sort_buckets(sm, sm.buf, base, g0, g1, bf, tile, pv, cam, st, out);
                 g0 = g1;
