@@ -395,15 +395,15 @@ struct BucketFn {
 __device__ __forceinline__ int rank_fast(const uint64_t *a, int b0, int b1, uint64_t x, int tile,
                                          const PrepView &pv, const CamK &cam, const SetK &st)
 {
-    const int pb = st.pbits;
-    const uint64_t h = x >> pb;
+    // y has x's key prefix and another id  <=>  0 < (y ^ x) < 2^pbits
+    const uint64_t pm1 = (1ull << st.pbits) - 1ull;
     int r = 0;
     bool eq = false;
 #pragma unroll 4
     for (int j = b0; j < b1; ++j) {
         const uint64_t y = a[j];
         r += y < x ? 1 : 0;
-        eq |= ((y >> pb) == h) & (y != x);
+        eq |= ((y ^ x) - 1ull) < pm1;
     }
     return eq ? rank_in_bucket(a, b0, b1, x, tile, pv, cam, st) : r;
 }
