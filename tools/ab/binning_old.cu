@@ -286,7 +286,7 @@ constexpr int SORT_CHUNK = SORT_T * SORT_IPT;     // items per register pass
 constexpr int SORT_SMEM_ITEMS = QGS_SORT_SMEM_ITEMS;   // staged in shared memory up to this
 static_assert(SORT_MAX_BUCKETS == 8192, "kernels.cuh");
 #ifndef QGS_SORT_L2_MIN
-#define QGS_SORT_L2_MIN 12   // mean first-level bucket that takes the second level (6 8 12 16 never: 2.25 2.24 2.20 2.20 2.21 ms at C3)
+#define QGS_SORT_L2_MIN 6                        // mean first-level bucket that takes the second level
 #endif
 constexpr int SORT_NB2 = 2048;                   // second-level buckets of a staged group
 // one register pass of items c0 + k * SORT_T + threadIdx.x (k < SORT_IPT) of
@@ -395,15 +395,15 @@ struct BucketFn {
 __device__ __forceinline__ int rank_fast(const uint64_t *a, int b0, int b1, uint64_t x, int tile,
                                          const PrepView &pv, const CamK &cam, const SetK &st)
 {
-    // y has x's key prefix and another id  <=>  0 < (y ^ x) < 2^pbits
-    const uint64_t pm1 = (1ull << st.pbits) - 1ull;
+    const int pb = st.pbits;
+    const uint64_t h = x >> pb;
     int r = 0;
     bool eq = false;
 #pragma unroll 4
     for (int j = b0; j < b1; ++j) {
         const uint64_t y = a[j];
         r += y < x ? 1 : 0;
-        eq |= ((y ^ x) - 1ull) < pm1;
+        eq |= ((y >> pb) == h) & (y != x);
     }
     return eq ? rank_in_bucket(a, b0, b1, x, tile, pv, cam, st) : r;
 }
