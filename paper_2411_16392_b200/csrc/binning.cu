@@ -197,6 +197,9 @@ __global__ void pixel_rays_kernel(CamK cam, double *rays)
 // from the table and the float64 key with the reference's operation order.
 // (An fp32 pre-reject of rays that cannot hit the support was measured
 // slower: most pairs' vertex-nearest pixel does hit.)
+#ifndef QGS_KEY_PREFETCH
+#define QGS_KEY_PREFETCH 1
+#endif
 #ifndef QGS_KEY_MIN_BLOCKS
 #define QGS_KEY_MIN_BLOCKS 2     // 128 registers, no spills: 2.74 -> 2.60 ms at C3 (3 and 4 measured)
 #endif
@@ -209,6 +212,42 @@ pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
     const int lane = threadIdx.x & 31;
     const int warps = gridDim.x * (blockDim.x >> 5);
     const bool euclid = st.euclid != 0;
+#if QGS_KEY_PREFETCH
+    // The warp's next primitive is fetched while this one's keys are
+    // computed: its Geo64 one double per lane (one coalesced 256-B read),
+    // its box (lanes 0-3) and tile count (lane 4).  Without it every
+    // primitive began with a chain of dependent loads (count, box, geometry
+    // read by one lane, first ray) that ~7 key iterations could not hide.
+    __shared__ double s_geo[8][32];
+    static_assert(sizeof(Geo64) == 32 * sizeof(double), "one double per lane");
+    double gv = 0.0;
+    int meta = 0;
+    auto fetch = [&](int q) {
+        if (q < P) {
+            gv = __ldg(reinterpret_cast<const double *>(pv.geo + q) + lane);
+            meta = lane < 4 ? __ldg(reinterpret_cast<const int *>(pv.bbox + q) + lane)
+                            : (lane == 4 ? __ldg(pv.ntiles + q) : 0);
+        }
+    };
+    int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    fetch(p);
+    for (; p < P; p += warps) {
+        const double cur_gv = gv;
+        const int cur_meta = meta;
+        fetch(p + warps);
+        const int nt = __shfl_sync(0xffffffffu, cur_meta, 4);
+        if (nt == 0) continue;
+        int4 b;
+        b.x = __shfl_sync(0xffffffffu, cur_meta, 0);
+        b.y = __shfl_sync(0xffffffffu, cur_meta, 1);
+        b.z = __shfl_sync(0xffffffffu, cur_meta, 2);
+        const int tx0 = b.x / TILE, ty0 = b.z / TILE;
+        const int ncols = b.y / TILE - tx0 + 1;
+        __syncwarp();
+        s_geo[threadIdx.x >> 5][lane] = cur_gv;
+        __syncwarp();
+        const Geo64 &g = *reinterpret_cast<const Geo64 *>(s_geo[threadIdx.x >> 5]);
+#else
     for (int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); p < P; p += warps) {
         const int nt = pv.ntiles[p];
         if (nt == 0) continue;
@@ -216,8 +255,9 @@ pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
         const int tx0 = b.x / TILE, ty0 = b.z / TILE;
         const int ncols = b.y / TILE - tx0 + 1;
         const Geo64 &g = pv.geo[p];
-        // per-primitive key constants in shared memory (broadcast reads)
         __syncwarp();
+#endif
+        // per-primitive key constants in shared memory (broadcast reads)
         if (lane == 0) s_kp[threadIdx.x >> 5] = key_prim(g);
         __syncwarp();
         const KeyPrim &kp = s_kp[threadIdx.x >> 5];
