@@ -1,6 +1,6 @@
-# float64 termination: which test failed, and the error distribution of T at the events
-mkdir -p gpurun_out
+# round profile r02i at HEAD: GPU suite (with full-view reports), smoke, bench, launch list, ncu full
+mkdir -p gpurun_out/r02i_parity
 python -m paper_2411_16392_b200.build > /dev/null 2>&1
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_known_answers.py tests/test_debug_checks.py -q 2>&1 | grep -E "FAILED|passed|failed|Error|assert" | head -20
-QGS_BUILD_DEBUG=0 QGS_NVCC_EXTRA="-DQGS_UTIL_COUNTERS=1" python -c "from paper_2411_16392_b200 import build as b; b.build(force=True)" > /dev/null 2>&1
-for c in c3 c4 c2 c5; do python tools/lane_util_fwd.py --config $c | head -2; done
+QGS_PARITY_OUT=gpurun_out/r02i_parity timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/r02i_tests.log 2>&1; echo "tests rc=$?"; tail -1 gpurun_out/r02i_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+bash tools/round_profile.sh r02i
