@@ -403,24 +403,36 @@ __device__ __forceinline__ int bucket_start(const SortSmem &sm, int d)
     return d == 0 ? 0 : sm.bend[d - 1];
 }
 
-// Bucket of a key: the varying f32 key bits cut linearly (kmin, shift), or --
-// for tiles whose depths cluster so that a linear cut leaves buckets of
-// hundreds of items -- the number of sample splitters <= the key (a sample
-// sort's buckets, balanced whatever the distribution).  Both are monotone in
-// the key, so bucket order is key order.
+// Bucket of a composite: the tile's key range cut linearly in depth -- the
+// float64 key (low bits: the id) rounded to fp32, (f - dmin) * dscale,
+// truncated and clamped -- or, for tiles whose depths cluster so that a
+// linear cut leaves buckets of hundreds of items, the number of sample
+// splitters <= its sort_h (a sample sort's buckets, balanced whatever the
+// distribution).  Both are monotone in the composite (rounding, subtraction
+// and scaling by a positive factor never reverse an order; fminf sends inf
+// and NaN to the last bucket), so bucket order is key order.  (Linear in
+// sort_h -- the top 32 bits of the key's bit pattern, log-like across
+// octaves -- left 9.6 items per rank at C3; linear in depth 6.2,
+// tools/sort_stats.py.)
 constexpr int SORT_SPLIT = 4095;                 // most splitters (a sample of 4096)
 #ifndef QGS_SORT_SKEW
 #define QGS_SORT_SKEW 128
 #endif
 constexpr int SORT_SKEW = QGS_SORT_SKEW;         // largest linear bucket tolerated
+__device__ __forceinline__ float key_f32(uint64_t x)
+{
+    return __double2float_rn(__longlong_as_double((long long)x));
+}
 struct BucketFn {
-    uint32_t kmin;
-    int shift;
+    float dmin, dscale;                          // linear buckets
+    int nbm1;                                    // last bucket
     const uint32_t *sp;                          // sorted splitters, or nullptr
     int ns;                                      // number of splitters
-    __device__ __forceinline__ int operator()(uint32_t h) const
+    __device__ __forceinline__ float pos(uint64_t x) const { return (key_f32(x) - dmin) * dscale; }
+    __device__ __forceinline__ int operator()(uint64_t x) const
     {
-        if (!sp) return (int)((h - kmin) >> shift);
+        if (!sp) return __float2int_rz(fminf(pos(x), (float)nbm1));
+        const uint32_t h = sort_h(x);
         int lo = 0, hi = ns;                     // upper_bound(sp, h)
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
@@ -455,7 +467,7 @@ __device__ void sort_buckets(SortSmem &sm, const uint64_t *a, int base, int g0, 
     const int i0 = bucket_start(sm, g0) - base, i1 = bucket_start(sm, g1) - base;
     for (int i = i0 + threadIdx.x; i < i1; i += SORT_T) {
         const uint64_t x = a[i];
-        const int d = bf(sort_h(x));
+        const int d = bf(x);
         const int b0 = bucket_start(sm, d), b1 = sm.bend[d];
         const int r = b1 - b0 == 1 ? 0 : rank_fast(a, b0 - base, b1 - base, x, tile, pv, cam, st);
         QGS_CHECK(r >= 0 && r < b1 - b0);
@@ -469,15 +481,31 @@ __device__ void sort_buckets(SortSmem &sm, const uint64_t *a, int base, int g0, 
 // histogram from the L2 slice, scatter into shared memory, rank.
 // First-level buckets of big tiles hold tens to hundreds of
 // items, too many for the quadratic in-bucket rank.
+// The second-level bucket: linear in the first level's depth coordinate
+// over the group's buckets [g0, g1), or (sample-sort first level) linear in
+// sort_h over the group's key interval [glo, ghi).
+struct SubFn {
+    const BucketFn &bf;
+    float g0, s2f;
+    uint32_t glo;
+    int s2;
+    __device__ __forceinline__ int operator()(uint64_t x) const
+    {
+        if (!bf.sp) return __float2int_rz(fminf((bf.pos(x) - g0) * s2f, (float)(SORT_NB2 - 1)));
+        return (int)((sort_h(x) - glo) >> s2);
+    }
+};
+
 __device__ __noinline__ void sort_group_l2(SortSmem &sm, const uint64_t *stage, int base, int cnt,
-                                           uint64_t glo, uint64_t ghi, int tile,
-                                           const PrepView &pv, const CamK &cam, const SetK &st,
-                                           int32_t *out)
+                                           const BucketFn &bf, int g0, int g1, uint64_t glo,
+                                           uint64_t ghi, int tile, const PrepView &pv,
+                                           const CamK &cam, const SetK &st, int32_t *out)
 {
     int *bend2 = reinterpret_cast<int *>(sm.buf + SORT_GROUP_ITEMS);
     int s2 = 0;
-    while (((ghi - glo - 1) >> s2) >= (uint64_t)SORT_NB2) ++s2;
-    const BucketFn bf2{(uint32_t)glo, s2, nullptr, 0};
+    if (bf.sp)
+        while (((ghi - glo - 1) >> s2) >= (uint64_t)SORT_NB2) ++s2;
+    const SubFn bf2{bf, (float)g0, (float)SORT_NB2 / (float)(g1 - g0), (uint32_t)glo, s2};
     for (int d = threadIdx.x; d < SORT_NB2; d += SORT_T) bend2[d] = 0;
     __syncthreads();
     for (int c0 = 0; c0 < cnt; c0 += SORT_CHUNK) {
@@ -485,7 +513,7 @@ __device__ __noinline__ void sort_group_l2(SortSmem &sm, const uint64_t *stage, 
         load_chunk(v, stage + base, c0, cnt);
 #pragma unroll
         for (int k = 0; k < SORT_IPT; ++k)
-            if (c0 + k * SORT_T + (int)threadIdx.x < cnt) atomicAdd(&bend2[bf2(sort_h(v[k]))], 1);
+            if (c0 + k * SORT_T + (int)threadIdx.x < cnt) atomicAdd(&bend2[bf2(v[k])], 1);
     }
     __syncthreads();
     {
@@ -504,12 +532,12 @@ __device__ __noinline__ void sort_group_l2(SortSmem &sm, const uint64_t *stage, 
         load_chunk(v, stage + base, c0, cnt);
 #pragma unroll
         for (int k = 0; k < SORT_IPT; ++k)
-            if (c0 + k * SORT_T + (int)threadIdx.x < cnt) sm.buf[atomicAdd(&bend2[bf2(sort_h(v[k]))], 1)] = v[k];
+            if (c0 + k * SORT_T + (int)threadIdx.x < cnt) sm.buf[atomicAdd(&bend2[bf2(v[k])], 1)] = v[k];
     }
     __syncthreads();
     for (int i = threadIdx.x; i < cnt; i += SORT_T) {
         const uint64_t x = sm.buf[i];
-        const int d = bf2(sort_h(x));
+        const int d = bf2(x);
         const int b0 = d == 0 ? 0 : bend2[d - 1], b1 = bend2[d];
         const int r = b1 - b0 == 1 ? 0 : rank_fast(sm.buf, b0, b1, x, tile, pv, cam, st);
         out[base + b0 + r] = comp_prim(x, st.pbits);
@@ -570,6 +598,10 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
     const uint32_t kmin = sm.kmin, range = sm.kmax - sm.kmin;
     int shift = 0;
     while ((range >> shift) >= (uint32_t)nb) ++shift;
+    // the key range as fp32 depths: composites below / above every key of the tile
+    const float dmin = key_f32(((uint64_t)kmin + (960ull << 23)) << 29);
+    const float rf = key_f32(((uint64_t)sm.kmax + (960ull << 23) + 1ull) << 29) - dmin;
+    BucketFn bf{dmin, rf > 0.f ? fminf((float)nb / rf, 1e30f) : 0.f, nb - 1, nullptr, 0};
 
     // histogram (a tile over one register pass: the chunk's SORT_IPT loads
     // are all issued before the first use -- load, use, load, use left one
@@ -579,11 +611,10 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
 #pragma unroll
         for (int k = 0; k < SORT_IPT; ++k) {
             const int i = c0 + k * SORT_T + threadIdx.x;
-            if (i < n) atomicAdd(&sm.bend[((sort_h(it[k])) - kmin) >> shift], 1);
+            if (i < n) atomicAdd(&sm.bend[bf(it[k])], 1);
         }
     }
     __syncthreads();
-    BucketFn bf{kmin, shift, nullptr, 0};
     {
         int mx = 0;
         for (int d = threadIdx.x; d < nb; d += SORT_T) mx = max(mx, sm.bend[d]);
@@ -621,7 +652,7 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
         for (int d = threadIdx.x; d < nb; d += SORT_T) sm.bend[d] = 0;
         __syncthreads();
         bf.sp = sp;
-        for (int i = threadIdx.x; i < n; i += SORT_T) atomicAdd(&sm.bend[bf(sort_h(src[i]))], 1);
+        for (int i = threadIdx.x; i < n; i += SORT_T) atomicAdd(&sm.bend[bf(src[i])], 1);
         __syncthreads();
     }
     // exclusive scan of the bucket counts (nb <= 8192 = 16 per thread; the
@@ -655,7 +686,7 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
         for (int k = 0; k < SORT_IPT; ++k) {
             const int i = c0 + k * SORT_T + threadIdx.x;
             if (i < n) {
-                const int pos = atomicAdd(&sm.bend[bf(sort_h(it[k]))], 1);
+                const int pos = atomicAdd(&sm.bend[bf(it[k])], 1);
                 stage[pos] = it[k];
             }
         }
@@ -680,6 +711,7 @@ tile_sort_kernel(const int32_t *__restrict__ tile_offsets, uint64_t *keys, uint6
                     HugeTile &t = huge->t[h];
                     t.tile = tile; t.nb = nb; t.kmin = kmin; t.range = range; t.shift = shift;
                     t.ns = bf.sp ? bf.ns : -1;
+                    t.dmin = bf.dmin; t.dscale = bf.dscale;
                 }
             }
             __syncthreads();
@@ -700,8 +732,8 @@ __device__ __forceinline__ void sort_groups(SortSmem &sm, const uint64_t *stage,
                                          int shift, int tile, const PrepView &pv, const CamK &cam,
                                          const SetK &st, int32_t *out)
 {
-        auto lo_of = [&](int d) -> uint64_t {
-            if (!bf.sp) return (uint64_t)kmin + ((uint64_t)d << shift);
+        (void)shift;
+        auto lo_of = [&](int d) -> uint64_t {     // sample-sort buckets only
             if (d == 0) return kmin;
             return d > bf.ns ? (uint64_t)kmin + range + 1 : (uint64_t)bf.sp[d - 1];
         };
@@ -739,7 +771,8 @@ __device__ __forceinline__ void sort_groups(SortSmem &sm, const uint64_t *stage,
                 g0 = g1;
                 continue;
             }
-            sort_group_l2(sm, stage, base, cnt, lo_of(g0), lo_of(g1), tile, pv, cam, st, out);
+            sort_group_l2(sm, stage, base, cnt, bf, g0, g1, bf.sp ? lo_of(g0) : 0ull,
+                          bf.sp ? lo_of(g1) : 0ull, tile, pv, cam, st, out);
             g0 = g1;
         }
 }
@@ -763,7 +796,7 @@ tile_sort_chunks_kernel(const int32_t *__restrict__ tile_offsets, const uint64_t
     const int *src = const_cast<HugeSort *>(huge)->bend_of(h);
     for (int d = threadIdx.x; d < SORT_MAX_BUCKETS; d += SORT_T) sm.bend[d] = src[d];
     __syncthreads();
-    BucketFn bf{t.kmin, t.shift, nullptr, 0};
+    BucketFn bf{t.dmin, t.dscale, t.nb - 1, nullptr, 0};
     if (t.ns >= 0) {
         bf.sp = reinterpret_cast<const uint32_t *>(sm.bend) + SORT_MAX_BUCKETS / 2 + 1;
         bf.ns = t.ns;

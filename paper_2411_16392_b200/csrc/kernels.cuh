@@ -32,7 +32,7 @@ constexpr int SORT_MAX_HUGE = 512;
 struct HugeTile {
     int tile, nb, shift, ns;          // ns: splitters (sample-sort buckets), -1: linear buckets
     uint32_t kmin, range;
-    int pad[2];
+    float dmin, dscale;               // linear buckets (BucketFn)
 };
 struct HugeSort {
     int count;

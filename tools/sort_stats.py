@@ -80,3 +80,39 @@ if skew.any():
     fr = torch.tensor(fr)
     print(f"skewed tiles: range share of the top 1 % of keys: median {fr.median():.3f}, "
           f"p10 {fr.quantile(0.1):.3f}, p90 {fr.quantile(0.9):.3f}")
+
+# ---- what other first-level bucketings would give (rank length sum c^2 / n)
+# over the L2-staged tiles (n > SMEM), nb buckets each as the kernel picks
+m = (cnt > SMEM)
+sel = m[tile]
+ti, hh, kk = tile[sel], h[sel], keys[sel]
+nbt = nb[ti]
+
+
+def rank_len(bid):
+    g = ti * MAXB + bid.clamp(0, MAXB - 1)
+    c = torch.bincount(g, minlength=T * MAXB).double()
+    return ((c ** 2).sum() / sel.sum()).item()
+
+
+print(f"L2-staged tiles: rank length, linear in sort_h {rank_len((hh - kmin[ti]) >> shift[ti]):.2f}")
+kmin_d = torch.full((T,), float('inf'), dtype=torch.float64, device=h.device).scatter_reduce(0, tile, keys, "amin")
+kmax_d = torch.full((T,), -float('inf'), dtype=torch.float64, device=h.device).scatter_reduce(0, tile, keys, "amax")
+lin = ((kk - kmin_d[ti]) / (kmax_d[ti] - kmin_d[ti]).clamp(min=1e-300) * (nbt - 1)).floor().long()
+print(f"  linear in depth {rank_len(lin):.2f}")
+# equi-depth coarse cells from a strided sample of S keys, L linear sub-buckets each
+for S in (256, 1024):
+    L = MAXB // S
+    starts = off[:-1]
+    # position of each item inside its tile (keys are sorted per tile)
+    pos = torch.arange(keys.numel(), device=h.device) - starts[tile]
+    # the sorted sample's splitters: key at rank floor(i * n / S), i = 1..S-1 -> for sorted
+    # keys, the coarse cell of an item is the number of splitters <= its key ~ pos * S // n
+    coarse = (pos[sel] * S) // cnt[ti]
+    # sub-bucket linear inside the cell's key range
+    cell = ti * S + coarse
+    lo = torch.full((T * S,), float('inf'), dtype=torch.float64, device=h.device).scatter_reduce(0, cell, kk, "amin")
+    hi = torch.full((T * S,), -float('inf'), dtype=torch.float64, device=h.device).scatter_reduce(0, cell, kk, "amax")
+    sub = ((kk - lo[cell]) / (hi[cell] - lo[cell]).clamp(min=1e-300) * (L - 1)).floor().long()
+    print(f"  equi-depth {S} cells x {L} linear sub-buckets {rank_len(coarse * L + sub):.2f}")
+print(f"  Poisson ideal (n / nb per bucket) {(1 + cnt[m].double() / nb[m].double()).mul(cnt[m].double()).sum().item() / cnt[m].sum().item():.2f}")
