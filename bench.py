@@ -403,7 +403,9 @@ def run_e2e(a, rz, sc, mine, device, st, world):
 
     def step():
         nonlocal out_host
-        dev = rz.DevicePrimitives.from_host(host, device, non_blocking=True)
+        # the SH coefficients (~3/4 of the bytes) on the copy stream: view 0
+        # is binned from the geometry while they are on their way
+        dev = rz.DevicePrimitives.from_host(host, device, non_blocking=True, sh_stream=copy)
         # every view's upstream maps go over on a copy stream under the raster
         evs = upload_async(ups, dev_ups, copy)
         main = torch.cuda.current_stream()

@@ -147,6 +147,16 @@ size_t qgs_prep_bytes(int32_t P);
 int qgs_preprocess(const qgs_params *prims, const qgs_camera *cam,
                    const qgs_settings *st, void *prep, int64_t *d_n_pairs,
                    qgs_stream_t stream);
+/* qgs_preprocess in two parts, together bit-identical to it: everything but
+ * the SH colour (geometry, boxes, tile counts, pair offsets), then the colour
+ * (sh.py:82-88) -- so that the SH coefficients (3/4 of the parameter bytes at
+ * degree 3) can still be on their way from the host while the view is binned.
+ * qgs_preprocess_color must run before qgs_forward. */
+int qgs_preprocess_geometry(const qgs_params *prims, const qgs_camera *cam,
+                            const qgs_settings *st, void *prep, int64_t *d_n_pairs,
+                            qgs_stream_t stream);
+int qgs_preprocess_color(const qgs_params *prims, const qgs_camera *cam, void *prep,
+                         qgs_stream_t stream);
 
 /* ---- stage 2: key duplication + per-tile (depth key, id) sort
  *      (rasterizer.py:159-181, raster_kernels.py:684-716).  tile_offsets has

@@ -116,6 +116,8 @@ def load():
     sigs = {
         "qgs_prep_bytes": (ctypes.c_size_t, [i32]),
         "qgs_preprocess": (ctypes.c_int, [P(Params), P(Camera), P(Settings), vp, vp, vp]),
+        "qgs_preprocess_geometry": (ctypes.c_int, [P(Params), P(Camera), P(Settings), vp, vp, vp]),
+        "qgs_preprocess_color": (ctypes.c_int, [P(Params), P(Camera), vp, vp]),
         "qgs_bin_workspace_bytes": (ctypes.c_size_t, [i32, i64, i32]),
         "qgs_bin": (ctypes.c_int, [vp, i32, P(Camera), P(Settings), i64, vp, ctypes.c_size_t,
                                    vp, vp, vp]),
@@ -169,7 +171,8 @@ def load():
     return L
 
 
-EXPORTS = ("qgs_prep_bytes", "qgs_preprocess", "qgs_bin_workspace_bytes", "qgs_bin",
+EXPORTS = ("qgs_prep_bytes", "qgs_preprocess", "qgs_preprocess_geometry", "qgs_preprocess_color",
+           "qgs_bin_workspace_bytes", "qgs_bin",
            "qgs_sorted_keys", "qgs_tile_keys_f64", "qgs_forward", "qgs_backward", "qgs_backward_det_workspace_bytes",
            "qgs_backward_deterministic", "qgs_chain",
            "qgs_export_prep", "qgs_export_prep_geometry", "qgs_pixel_dirs", "qgs_trace_pixel", "qgs_loss_workspace_bytes",

@@ -107,8 +107,8 @@ size_t qgs_prep_bytes(int32_t P)
     return qgs::prep_bytes(P) + qgs::align256(scan_blocks(P) * sizeof(int64_t));
 }
 
-int qgs_preprocess(const qgs_params *prims, const qgs_camera *cam, const qgs_settings *st,
-                   void *prep, int64_t *d_n_pairs, qgs_stream_t stream)
+static int preprocess_impl(const qgs_params *prims, const qgs_camera *cam, const qgs_settings *st,
+                           void *prep, int64_t *d_n_pairs, qgs_stream_t stream, int with_color)
 {
     if (!prims || !st || !prep || !d_n_pairs) return fail(QGS_E_ARG, "NULL argument");
     if (int rc = check_cam(cam)) return rc;
@@ -126,7 +126,8 @@ int qgs_preprocess(const qgs_params *prims, const qgs_camera *cam, const qgs_set
         return 0;
     }
     QGS_CK(cudaMemsetAsync(pv.nonfinite, 0, sizeof(int32_t), s));
-    qgs::preprocess_kernel<<<cdiv(P, 128), 128, 0, s>>>(*prims, ck, pv, st->euclidean_density);
+    qgs::preprocess_kernel<<<cdiv(P, 128), 128, 0, s>>>(*prims, ck, pv, st->euclidean_density,
+                                                         with_color);
     QGS_LAUNCHED("preprocess_kernel");
     const int nb = (int)scan_blocks(P);
     int64_t *sums = scan_sums_ptr(prep, P);
@@ -135,6 +136,36 @@ int qgs_preprocess(const qgs_params *prims, const qgs_camera *cam, const qgs_set
                                                          pv.nonfinite);
     qgs::scan_out_kernel<<<nb, qgs::SCAN_THREADS, 0, s>>>(pv.ntiles, P, sums, pv.pair_off);
     QGS_LAUNCHED("scan kernels");
+    return 0;
+}
+
+int qgs_preprocess(const qgs_params *prims, const qgs_camera *cam, const qgs_settings *st,
+                   void *prep, int64_t *d_n_pairs, qgs_stream_t stream)
+{
+    return preprocess_impl(prims, cam, st, prep, d_n_pairs, stream, 1);
+}
+
+int qgs_preprocess_geometry(const qgs_params *prims, const qgs_camera *cam,
+                            const qgs_settings *st, void *prep, int64_t *d_n_pairs,
+                            qgs_stream_t stream)
+{
+    return preprocess_impl(prims, cam, st, prep, d_n_pairs, stream, 0);
+}
+
+int qgs_preprocess_color(const qgs_params *prims, const qgs_camera *cam, void *prep,
+                         qgs_stream_t stream)
+{
+    if (!prims || !prep) return fail(QGS_E_ARG, "NULL argument");
+    if (int rc = check_cam(cam)) return rc;
+    if (prims->P < 0) return fail(QGS_E_ARG, "P < 0");
+    if (prims->sh_coeffs != 1 && prims->sh_coeffs != 4 && prims->sh_coeffs != 9 &&
+        prims->sh_coeffs != 16)
+        return fail(QGS_E_ARG, "sh_coeffs must be 1, 4, 9 or 16");
+    if (prims->P == 0) return 0;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    qgs::color_kernel<<<cdiv(prims->P, 128), 128, 0, s>>>(*prims, qgs::make_camk(*cam),
+                                                          qgs::prep_view(prep, prims->P));
+    QGS_LAUNCHED("color_kernel");
     return 0;
 }
 

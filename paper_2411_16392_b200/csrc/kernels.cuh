@@ -5,7 +5,8 @@
 namespace qgs {
 
 // preprocess.cu
-__global__ void preprocess_kernel(qgs_params prm, CamK cam, PrepView pv, int euclid);
+__global__ void preprocess_kernel(qgs_params prm, CamK cam, PrepView pv, int euclid, int with_color);
+__global__ void color_kernel(qgs_params prm, CamK cam, PrepView pv);
 __global__ void chain_kernel(qgs_params prm, CamK cam, const float *kg, qgs_grads out);
 __global__ void export_prep_kernel(PrepView pv, int P, double *scales, double *alphas,
                                    double *colors, int32_t *bbox, uint8_t *planar);

@@ -387,8 +387,27 @@ __device__ inline ConicRec bounding_conic(const double s[3], bool planar, bool e
 #ifndef QGS_CHAIN_MIN_BLOCKS
 #define QGS_CHAIN_MIN_BLOCKS 1
 #endif
+// SH colour of primitive p seen along the unit direction vd (sh.py:82-88)
+__device__ __forceinline__ void sh_colour(const qgs_params &prm, int p, const double vd[3],
+                                          double col[3])
+{
+    int K = prm.sh_coeffs;
+    double Y[16];
+    sh_basis(K, vd[0], vd[1], vd[2], Y);
+    const float *shp = prm.sh + (size_t)p * 3 * K;
+    for (int ch = 0; ch < 3; ++ch) {
+        double acc = 0.0;
+        for (int k = 0; k < K; ++k) acc += (double)shp[ch * K + k] * Y[k];
+        acc = acc + 0.5;
+        col[ch] = acc < 0 ? 0.0 : acc;
+    }
+}
+
+// with_color = 0: everything but the SH colour (left 0; color_kernel fills it
+// in once the coefficients are on the device -- their upload, ~3/4 of the
+// parameter bytes at SH degree 3, then overlaps the binning)
 __global__ void __launch_bounds__(128, QGS_PRE_MIN_BLOCKS)
-preprocess_kernel(qgs_params prm, CamK cam, PrepView pv, int euclid)
+preprocess_kernel(qgs_params prm, CamK cam, PrepView pv, int euclid, int with_color)
 {
     int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= prm.P) return;
@@ -428,16 +447,8 @@ preprocess_kernel(qgs_params prm, CamK cam, PrepView pv, int euclid)
     g.dist = dist;
     double vd[3] = {v[0] / dist, v[1] / dist, v[2] / dist};
     // SH colour (sh.py:82-88)
-    int K = prm.sh_coeffs;
-    double Y[16];
-    sh_basis(K, vd[0], vd[1], vd[2], Y);
-    const float *shp = prm.sh + (size_t)p * 3 * K;
-    for (int ch = 0; ch < 3; ++ch) {
-        double acc = 0.0;
-        for (int k = 0; k < K; ++k) acc += (double)shp[ch * K + k] * Y[k];
-        acc = acc + 0.5;
-        g.col[ch] = acc < 0 ? 0.0 : acc;
-    }
+    if (with_color) sh_colour(prm, p, vd, g.col);
+    else g.col[0] = g.col[1] = g.col[2] = 0.0;
     g.alpha = alpha;
     g.planar = planar ? 1.0 : 0.0;
     // projected vertex (cameras.py:73-79)
@@ -479,6 +490,27 @@ preprocess_kernel(qgs_params prm, CamK cam, PrepView pv, int euclid)
     r.pad[0] = r.pad[1] = 0.f;
     pv.rec[p] = r;
     pv.conic[p] = bounding_conic(s, planar, euclid != 0, R, c, cam, box);
+}
+
+// the SH colour of every primitive (preprocess_kernel's with_color part, the
+// same operations): Geo64.col and PrimRec.col
+__global__ void __launch_bounds__(128)
+color_kernel(qgs_params prm, CamK cam, PrepView pv)
+{
+    int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= prm.P) return;
+    const float *cf = prm.centers + 3 * p;
+    double c[3] = {cf[0], cf[1], cf[2]};
+    double v[3] = {c[0] - cam.eye[0], c[1] - cam.eye[1], c[2] - cam.eye[2]};
+    double dist = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+    dist = fmax(dist, 1e-12);
+    double vd[3] = {v[0] / dist, v[1] / dist, v[2] / dist};
+    double col[3];
+    sh_colour(prm, p, vd, col);
+    for (int ch = 0; ch < 3; ++ch) {
+        pv.geo[p].col[ch] = col[ch];
+        pv.rec[p].col[ch] = (float)col[ch];
+    }
 }
 
 // ------------------------------------------------------------- K7 chain

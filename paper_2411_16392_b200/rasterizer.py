@@ -107,26 +107,45 @@ class DevicePrimitives:
 
     FIELDS = PrimitiveSet.FIELDS
 
-    def __init__(self, centers, quats, raw_scales, raw_signs, raw_opacity, sh):
+    def __init__(self, centers, quats, raw_scales, raw_signs, raw_opacity, sh, sh_ready=None):
         self.centers, self.quats = centers, quats
         self.raw_scales, self.raw_signs = raw_scales, raw_signs
         self.raw_opacity, self.sh = raw_opacity, sh
+        # event after the SH coefficients' upload on a copy stream (from_host
+        # with sh_stream), or None: prepare() bins a view before it is done
+        self.sh_ready = sh_ready
 
     @staticmethod
-    def from_host(prims, device=None, non_blocking=False):
+    def from_host(prims, device=None, non_blocking=False, sh_stream=None):
+        """Upload to the device.  sh_stream (with pinned host tensors and
+        non_blocking): the SH coefficients go over on that stream instead,
+        and prepare() runs the view's geometry and binning while they are on
+        their way (qgs_preprocess_geometry / qgs_preprocess_color)."""
         if isinstance(prims, DevicePrimitives):
             return prims
         device = device or torch.device("cuda", torch.cuda.current_device())
-        out = []
-        for f in PrimitiveSet.FIELDS:
-            a = getattr(prims, f)
+
+        def up(a):
             if isinstance(a, torch.Tensor):
                 t = a.to(device=device, dtype=torch.float32, non_blocking=non_blocking)
             else:
                 t = torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float32)))
                 t = t.to(device=device, non_blocking=non_blocking)
-            out.append(t.contiguous())
-        return DevicePrimitives(*out)
+            return t.contiguous()
+
+        split = sh_stream is not None and non_blocking
+        out = [up(getattr(prims, f)) for f in PrimitiveSet.FIELDS if not (split and f == "sh")]
+        ev = None
+        if split:
+            main = torch.cuda.current_stream(device)
+            sh_stream.wait_stream(main)          # the previous user of the buffers is done
+            with torch.cuda.stream(sh_stream):
+                sh = up(prims.sh)
+                ev = torch.cuda.Event()
+                ev.record(sh_stream)
+            sh.record_stream(main)
+            out.append(sh)
+        return DevicePrimitives(*out, sh_ready=ev)
 
     def __len__(self):
         return self.centers.shape[0]
@@ -401,8 +420,15 @@ def prepare(prims, cam, settings: RenderSettings = None, validate=True) -> Prepa
     prep = torch.empty((L.qgs_prep_bytes(P),), dtype=torch.uint8, device=device)
     n_dev = torch.empty((1,), dtype=torch.int64, device=device)
     pp = dev.params_struct()
-    _lib.check(L.qgs_preprocess(pp, cam_c, st_c, _ptr(prep), _ptr(n_dev), _stream()),
-               "qgs_preprocess")
+    # SH coefficients still on their way (DevicePrimitives.from_host with
+    # sh_stream): geometry and binning first, the colour after them
+    defer = dev.sh_ready is not None and not dev.sh_ready.query()
+    if defer:
+        _lib.check(L.qgs_preprocess_geometry(pp, cam_c, st_c, _ptr(prep), _ptr(n_dev), _stream()),
+                   "qgs_preprocess_geometry")
+    else:
+        _lib.check(L.qgs_preprocess(pp, cam_c, st_c, _ptr(prep), _ptr(n_dev), _stream()),
+                   "qgs_preprocess")
     n_pairs = int(n_dev.item())              # the one host sync per view
     if n_pairs < 0:                          # -k: k primitives with non-finite raw scales/signs
         raise ParameterError(f"non-finite raw scale/sign ({-n_pairs} primitives)")
@@ -413,6 +439,9 @@ def prepare(prims, cam, settings: RenderSettings = None, validate=True) -> Prepa
     tile_prims = torch.empty((max(n_pairs, 1),), dtype=torch.int32, device=device)
     _lib.check(L.qgs_bin(_ptr(prep), P, cam_c, st_c, n_pairs, _ptr(ws), ws_bytes,
                          _ptr(tile_offsets), _ptr(tile_prims), _stream()), "qgs_bin")
+    if defer:
+        torch.cuda.current_stream(device).wait_event(dev.sh_ready)
+        _lib.check(L.qgs_preprocess_color(pp, cam_c, _ptr(prep), _stream()), "qgs_preprocess_color")
     return PreparedView(cam=cam, settings=settings, prims=prims, dev=dev, prep=prep,
                         n_pairs=n_pairs, tile_offsets=tile_offsets,
                         tile_prims=tile_prims[:n_pairs], tiles_x=tiles_x, tiles_y=tiles_y,

@@ -126,6 +126,41 @@ def test_upload_async_and_pipelined_prepare(cuda_device):
             assert torch.equal(dst[i][k].cpu(), t), k
 
 
+@pytest.mark.gpu
+def test_deferred_sh_upload_prepare_is_identical(cuda_device):
+    """SH coefficients still in flight on a copy stream: prepare() bins the
+    view from the geometry (qgs_preprocess_geometry) and adds the colour when
+    they land (qgs_preprocess_color) -- the prepared state, the sort and the
+    images are bit-identical to the one-kernel qgs_preprocess"""
+    import numpy as np
+    import torch
+    from paper_2411_16392_b200 import rasterizer as rz, scenes
+    sc = scenes.config2(seed=5, n=4000, res=96, views=2)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    host = type("H", (), {f: pin(getattr(sc.prims, f)) for f in rz.DevicePrimitives.FIELDS})()
+    st = rz.RenderSettings()
+    ref_dev = rz.DevicePrimitives.from_host(sc.prims)
+    copy = torch.cuda.Stream()
+    for v in range(2):
+        with torch.cuda.stream(copy):
+            torch.cuda._sleep(200_000_000)      # keep the SH copy pending at prepare()
+        dev = rz.DevicePrimitives.from_host(host, cuda_device, non_blocking=True, sh_stream=copy)
+        assert dev.sh_ready is not None and not dev.sh_ready.query()
+        prep = rz.prepare(dev, sc.cams[v], st)
+        ref = rz.prepare(ref_dev, sc.cams[v], st)
+        P = len(ref_dev)
+        a256 = lambda n: (n + 255) // 256 * 256  # noqa: E731  (qgs_common.cuh prep_view)
+        o = 0
+        for size in (256 * P, 128 * P, 32 * P, 16 * P, 4 * P, 8 * (P + 1)):
+            # Geo64, PrimRec, ConicRec, boxes, tile counts, pair offsets
+            assert torch.equal(prep.prep[o:o + size], ref.prep[o:o + size]), o
+            o += a256(size)
+        assert torch.equal(prep.tile_offsets, ref.tile_offsets)
+        assert torch.equal(prep.tile_prims, ref.tile_prims)
+        a, b = rz.forward(prep), rz.forward(ref)
+        assert torch.equal(a.color, b.color) and torch.equal(a.alpha, b.alpha)
+
+
 # ------------------------------------------------ densification statistics
 
 def _stats_worker(rank, world, port, out_dir):
