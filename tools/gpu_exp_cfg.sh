@@ -11,7 +11,7 @@ agg=collections.defaultdict(float)
 for r in rows[1:]:
     try: agg[r[ki].split('(')[0]]+=float(r[vi].replace(',',''))/1e6
     except: pass
-print(repr(sys.argv[1]), sys.argv[2], {k.split('::')[-1]: round(v,3) for k,v in sorted(agg.items(), key=lambda x:-x[1])[:5] if 'sort' in k or 'key' in k})
+print(repr(sys.argv[1]), sys.argv[2], {k.split('::')[-1]: round(v,3) for k,v in sorted(agg.items(), key=lambda x:-x[1]) if "sort" in k or "key" in k})
 PY
   done
 done
