@@ -321,7 +321,10 @@ pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
 #define QGS_SORT_MIN_BLOCKS 2
 #endif
 constexpr int SORT_T = QGS_SORT_T;
-constexpr int SORT_IPT = 4;
+#ifndef QGS_SORT_IPT
+#define QGS_SORT_IPT 8      // 2 4 6 8: C3 2.16 2.08 2.08 2.07 ms
+#endif
+constexpr int SORT_IPT = QGS_SORT_IPT;            // items per thread per register pass
 constexpr int SORT_CHUNK = SORT_T * SORT_IPT;     // items per register pass
 constexpr int SORT_SMEM_ITEMS = QGS_SORT_SMEM_ITEMS;   // staged in shared memory up to this
 static_assert(SORT_MAX_BUCKETS == 8192, "kernels.cuh");
