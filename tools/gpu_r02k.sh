@@ -1,5 +1,6 @@
-for f in "" "-DQGS_TERM_BAND=1e-30" "-DQGS_TERM_NOP=1" "-DQGS_TERM_BAND=-1.0"; do
-  QGS_BUILD_DEBUG=0 QGS_NVCC_EXTRA="$f" python -c "from paper_2411_16392_b200 import build as b; b.build(force=True)" > /dev/null 2>&1
-  echo "== $f"; timeout 300 python tools/term_debug.py c1 s_sh3 2>&1 | grep flips
-  timeout 300 python tools/term_debug.py c1 2>&1 | grep flips
-done
+# round profile r02k at HEAD: GPU suite (with full-view reports), smoke, bench, launch list, ncu full
+mkdir -p gpurun_out/r02k_parity
+python -m paper_2411_16392_b200.build > /dev/null 2>&1
+QGS_PARITY_OUT=gpurun_out/r02k_parity timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/r02k_tests.log 2>&1; echo "tests rc=$?"; tail -1 gpurun_out/r02k_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+bash tools/round_profile.sh r02k
