@@ -6,13 +6,15 @@
 // Pipeline (all stream-ordered, one host read of the pair count before it):
 //   tile_diff_kernel    4 atomics per primitive into a 2D difference grid
 //   tile_offsets_kernel 2D prefix sum -> per-tile counts -> tile_offsets
-//   pair_key_kernel     one thread per (tile, primitive) pair: fp64 key
-//                       (bit-identical to tile_sort_depths), composite
-//                       (fp64 key bits truncated to 64 - pbits | prim)
+//   pair_key_kernel     a warp per primitive, a lane per (tile, primitive)
+//                       pair: fp64 key (bit-identical to tile_sort_depths),
+//                       composite (fp64 key bits truncated to 64 - pbits | prim)
 //                       scattered into its tile bucket through a per-tile cursor
-//   tile_sort_kernel    one CTA per tile: stable LSD radix sort of the bucket
-//                       on the f32 key bits that vary inside the tile, then
-//                       exact fix-up of equal-f32 runs by (fp64 key, prim id)
+//   tile_sort_kernel    one CTA per tile (heavy tiles first): bucket pass
+//                       linear in depth, then every item ranks itself in its
+//                       bucket by the composite, equal key prefixes by
+//                       (fp64 key, prim id); tiles over SORT_HUGE entries
+//                       finish in tile_sort_chunks_kernel
 // The result equals lexsort((prim, key, tile)) exactly: within a tile the
 // order is (key ascending, prim ascending), a total order.
 //
@@ -300,17 +302,20 @@ pair_key_kernel(PrepView pv, int P, int64_t n_pairs, CamK cam, SetK st,
 // ------------------------------------------------------- per-tile sort
 //
 // One CTA per tile, two levels:
-//   1. bucket (MSD) pass: the f32 key bits that vary inside the tile are cut
-//      into nb buckets (nb ~ n/2, a power of two); histogram, scan and an
+//   1. bucket (MSD) pass: the tile's depth range (the keys rounded to fp32)
+//      cut linearly into nb buckets (nb ~ n/2, a power of two, <= 8192;
+//      sample-sort buckets when a linear one exceeds SORT_SKEW items);
+//      histogram, scan and an
 //      unstable scatter (shared-memory cursors) into a staging array --
 //      shared memory when the tile fits, else its slice of `tmp` (L2-resident
 //      at these sizes).  Nothing downstream depends on the scatter order.
-//   2. every item ranks itself inside its bucket by the composite (f32 key
-//      bits, prim id) -- buckets hold a few items -- and items with equal f32
-//      keys by (fp64 key, prim) (rank_in_bucket), which gives exactly
+//   2. every item ranks itself inside its bucket by the composite (key
+//      prefix, prim id) -- buckets hold a few items -- and items with equal
+//      key prefixes by (fp64 key, prim) (rank_in_bucket), which gives exactly
 //      lexsort((prim, key, tile)).  Tiles larger than shared memory are
 //      staged in L2 and ranked in groups of whole buckets loaded into
-//      shared memory.
+//      shared memory (cut again into second-level buckets when they average
+//      over QGS_SORT_L2_MIN items).
 #ifndef QGS_SORT_T
 #define QGS_SORT_T 512
 #endif
