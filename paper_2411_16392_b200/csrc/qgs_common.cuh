@@ -358,6 +358,9 @@ __device__ inline KeyPrim key_prim(const Geo64 &g)
     return k;
 }
 
+#ifndef QGS_KEY_SHARED_RCP
+#define QGS_KEY_SHARED_RCP 1
+#endif
 __device__ inline double key_from_ray_fast(const KeyPrim &k, double cx, double cy, double cz,
                                            bool euclid, double t_clip)
 {
@@ -390,10 +393,27 @@ __device__ inline double key_from_ray_fast(const KeyPrim &k, double cx, double c
     if (disc < 0.0) return k.dist;
     const double sa = A > 0.0 ? 1.0 : -1.0;
     const double sq = sqrt(disc);
-    const double t0 = (-B - sa * sq) / (2.0 * A);
+#if QGS_KEY_SHARED_RCP
+    // both roots divide by 2A: one correctly rounded reciprocal y, then per
+    // root q = n y and the FMA correction q + (n - 2A q) y, which is the
+    // correctly rounded n / 2A (Markstein: y = RN(1/b), q within an ulp;
+    // no over/underflow for these magnitudes) -- bit-identical to the
+    // reference's division, checked against it in the debug build
+    const double den = 2.0 * A;
+    const double y = __drcp_rn(den);
+    auto qdiv = [&](double n) {
+        const double q = n * y;
+        return __fma_rn(__fma_rn(-den, q, n), y, q);
+    };
+#else
+    auto qdiv = [&](double n) { return n / (2.0 * A); };
+#endif
+    const double t0 = qdiv(-B - sa * sq);
+    QGS_CHECK(t0 == (-B - sa * sq) / (2.0 * A) || t0 != t0);
     if (try_root(t0)) return t0;
     if (disc == 0.0) return k.dist;
-    const double t1 = (-B + sa * sq) / (2.0 * A);
+    const double t1 = qdiv(-B + sa * sq);
+    QGS_CHECK(t1 == (-B + sa * sq) / (2.0 * A) || t1 != t1);
     return try_root(t1) ? t1 : k.dist;
 }
 
