@@ -118,7 +118,10 @@ __device__ inline void project_box(const double cs[8][3], const double R[9], con
         double Z = w0 * cam.Rwc[6] + w1 * cam.Rwc[7] + w2 * cam.Rwc[8] + cam.twc[2];
         if (Z > 1e-6) {
             any = true;
-            double u = cam.fx * X / Z + cam.cx, v = cam.fy * Y / Z + cam.cy;
+            // both coordinates divide by Z: one reciprocal (div_rcp)
+            const double iz = __drcp_rn(Z);
+            double u = div_rcp(cam.fx * X, Z, iz) + cam.cx, v = div_rcp(cam.fy * Y, Z, iz) + cam.cy;
+            QGS_CHECK(u == cam.fx * X / Z + cam.cx && v == cam.fy * Y / Z + cam.cy);
             umin = fmin(umin, u); umax = fmax(umax, u);
             vmin = fmin(vmin, v); vmax = fmax(vmax, v);
         } else {

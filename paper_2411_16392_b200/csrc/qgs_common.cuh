@@ -361,6 +361,15 @@ __device__ inline KeyPrim key_prim(const Geo64 &g)
 #ifndef QGS_KEY_SHARED_RCP
 #define QGS_KEY_SHARED_RCP 1
 #endif
+// n / b correctly rounded from y = RN(1/b) (__drcp_rn): q = n y, then the FMA
+// correction q + (n - b q) y (Markstein: exact for y = RN(1/b) and q within
+// an ulp, barring over/underflow, which these magnitudes never reach) -- for
+// several quotients with one divisor, bit-identical to the divisions
+__device__ __forceinline__ double div_rcp(double n, double b, double y)
+{
+    const double q = n * y;
+    return __fma_rn(__fma_rn(-b, q, n), y, q);
+}
 __device__ inline double key_from_ray_fast(const KeyPrim &k, double cx, double cy, double cz,
                                            bool euclid, double t_clip)
 {
@@ -394,17 +403,11 @@ __device__ inline double key_from_ray_fast(const KeyPrim &k, double cx, double c
     const double sa = A > 0.0 ? 1.0 : -1.0;
     const double sq = sqrt(disc);
 #if QGS_KEY_SHARED_RCP
-    // both roots divide by 2A: one correctly rounded reciprocal y, then per
-    // root q = n y and the FMA correction q + (n - 2A q) y, which is the
-    // correctly rounded n / 2A (Markstein: y = RN(1/b), q within an ulp;
-    // no over/underflow for these magnitudes) -- bit-identical to the
-    // reference's division, checked against it in the debug build
+    // both roots divide by 2A: one correctly rounded reciprocal (div_rcp),
+    // bit-identical to the reference's divisions (checked in the debug build)
     const double den = 2.0 * A;
     const double y = __drcp_rn(den);
-    auto qdiv = [&](double n) {
-        const double q = n * y;
-        return __fma_rn(__fma_rn(-den, q, n), y, q);
-    };
+    auto qdiv = [&](double n) { return div_rcp(n, den, y); };
 #else
     auto qdiv = [&](double n) { return n / (2.0 * A); };
 #endif
