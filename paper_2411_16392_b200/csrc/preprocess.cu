@@ -17,7 +17,12 @@ __device__ inline void quat_rot(const float *q4, double R[9], double qn[4], doub
 {
     double w = q4[0], x = q4[1], y = q4[2], z = q4[3];
     norm = sqrt(w * w + x * x + y * y + z * z);
-    w = w / norm; x = x / norm; y = y / norm; z = z / norm;
+    {   // four quotients, one divisor: one reciprocal (div_rcp, bit-identical)
+        const double in = __drcp_rn(norm);
+        QGS_CHECK(div_rcp(w, norm, in) == w / norm && div_rcp(z, norm, in) == z / norm);
+        w = div_rcp(w, norm, in); x = div_rcp(x, norm, in);
+        y = div_rcp(y, norm, in); z = div_rcp(z, norm, in);
+    }
     qn[0] = w; qn[1] = x; qn[2] = y; qn[3] = z;
     R[0] = 1 - 2 * (y * y + z * z);
     R[1] = 2 * (x * y - w * z);
@@ -448,7 +453,9 @@ preprocess_kernel(qgs_params prm, CamK cam, PrepView pv, int euclid, int with_co
     double dist = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
     dist = fmax(dist, 1e-12);
     g.dist = dist;
-    double vd[3] = {v[0] / dist, v[1] / dist, v[2] / dist};
+    const double idist = __drcp_rn(dist);
+    double vd[3] = {div_rcp(v[0], dist, idist), div_rcp(v[1], dist, idist), div_rcp(v[2], dist, idist)};
+    QGS_CHECK(vd[0] == v[0] / dist && vd[1] == v[1] / dist && vd[2] == v[2] / dist);
     // SH colour (sh.py:82-88)
     if (with_color) sh_colour(prm, p, vd, g.col);
     else g.col[0] = g.col[1] = g.col[2] = 0.0;
@@ -458,8 +465,10 @@ preprocess_kernel(qgs_params prm, CamK cam, PrepView pv, int euclid, int with_co
     double X = c[0] * cam.Rwc[0] + c[1] * cam.Rwc[1] + c[2] * cam.Rwc[2] + cam.twc[0];
     double Yc = c[0] * cam.Rwc[3] + c[1] * cam.Rwc[4] + c[2] * cam.Rwc[5] + cam.twc[1];
     double Z = c[0] * cam.Rwc[6] + c[1] * cam.Rwc[7] + c[2] * cam.Rwc[8] + cam.twc[2];
-    g.vert_u = cam.fx * X / Z + cam.cx;
-    g.vert_v = cam.fy * Yc / Z + cam.cy;
+    const double iZ = __drcp_rn(Z);
+    g.vert_u = div_rcp(cam.fx * X, Z, iZ) + cam.cx;
+    g.vert_v = div_rcp(cam.fy * Yc, Z, iZ) + cam.cy;
+    QGS_CHECK(g.vert_u == cam.fx * X / Z + cam.cx && g.vert_v == cam.fy * Yc / Z + cam.cy);
     for (int i = 0; i < 6; ++i) g.pad[i] = 0.0;
     pv.geo[p] = g;
 
@@ -507,7 +516,9 @@ color_kernel(qgs_params prm, CamK cam, PrepView pv)
     double v[3] = {c[0] - cam.eye[0], c[1] - cam.eye[1], c[2] - cam.eye[2]};
     double dist = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
     dist = fmax(dist, 1e-12);
-    double vd[3] = {v[0] / dist, v[1] / dist, v[2] / dist};
+    const double idist = __drcp_rn(dist);
+    double vd[3] = {div_rcp(v[0], dist, idist), div_rcp(v[1], dist, idist), div_rcp(v[2], dist, idist)};
+    QGS_CHECK(vd[0] == v[0] / dist && vd[1] == v[1] / dist && vd[2] == v[2] / dist);
     double col[3];
     sh_colour(prm, p, vd, col);
     for (int ch = 0; ch < 3; ++ch) {
@@ -584,7 +595,8 @@ chain_kernel(qgs_params prm, CamK cam, const float *__restrict__ kg,
         gu[2] += gR[i] * dY[i]; gu[3] += gR[i] * dZ[i];
     }
     double dq = gu[0] * qn[0] + gu[1] * qn[1] + gu[2] * qn[2] + gu[3] * qn[3];
-    for (int i = 0; i < 4; ++i) out.quats[4 * p + i] += (float)((gu[i] - qn[i] * dq) / qnorm);
+    const double iqn = __drcp_rn(qnorm);
+    for (int i = 0; i < 4; ++i) out.quats[4 * p + i] += (float)div_rcp(gu[i] - qn[i] * dq, qnorm, iqn);
 
     // centres through ohat and the SH view direction
     double gc[3];
@@ -593,7 +605,9 @@ chain_kernel(qgs_params prm, CamK cam, const float *__restrict__ kg,
                   R[3 * i + 2] * gk[KG_OHAT + 2]);
     double v[3] = {c[0] - cam.eye[0], c[1] - cam.eye[1], c[2] - cam.eye[2]};
     double dist = fmax(sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]), 1e-12);
-    double vd[3] = {v[0] / dist, v[1] / dist, v[2] / dist};
+    const double idist = __drcp_rn(dist);
+    double vd[3] = {div_rcp(v[0], dist, idist), div_rcp(v[1], dist, idist), div_rcp(v[2], dist, idist)};
+    QGS_CHECK(vd[0] == v[0] / dist && vd[1] == v[1] / dist && vd[2] == v[2] / dist);
     int K = prm.sh_coeffs;
     double Y[16], J[16][3];
     sh_basis(K, vd[0], vd[1], vd[2], Y);
@@ -613,7 +627,7 @@ chain_kernel(qgs_params prm, CamK cam, const float *__restrict__ kg,
         }
     }
     double dd = gdir[0] * vd[0] + gdir[1] * vd[1] + gdir[2] * vd[2];
-    for (int i = 0; i < 3; ++i) gc[i] += (gdir[i] - vd[i] * dd) / dist;
+    for (int i = 0; i < 3; ++i) gc[i] += div_rcp(gdir[i] - vd[i] * dd, dist, idist);
     for (int i = 0; i < 3; ++i) out.centers[3 * p + i] += (float)gc[i];
 
     // screen-space centre gradient (rasterizer.py:323-333)
@@ -621,10 +635,12 @@ chain_kernel(qgs_params prm, CamK cam, const float *__restrict__ kg,
     double Yc = c[0] * cam.Rwc[3] + c[1] * cam.Rwc[4] + c[2] * cam.Rwc[5] + cam.twc[1];
     double Z = c[0] * cam.Rwc[6] + c[1] * cam.Rwc[7] + c[2] * cam.Rwc[8] + cam.twc[2];
     double Zs = fabs(Z) < 1e-9 ? 1e-9 : Z;
+    const double Zs2 = Zs * Zs, iZs = __drcp_rn(Zs), iZs2 = __drcp_rn(Zs2);
     double gu_s = 0.0, gv_s = 0.0;
     for (int i = 0; i < 3; ++i) {
-        double Ju = cam.fx * (cam.Rwc[i] / Zs - X * cam.Rwc[6 + i] / (Zs * Zs));
-        double Jv = cam.fy * (cam.Rwc[3 + i] / Zs - Yc * cam.Rwc[6 + i] / (Zs * Zs));
+        double Ju = cam.fx * (div_rcp(cam.Rwc[i], Zs, iZs) - div_rcp(X * cam.Rwc[6 + i], Zs2, iZs2));
+        double Jv = cam.fy * (div_rcp(cam.Rwc[3 + i], Zs, iZs) - div_rcp(Yc * cam.Rwc[6 + i], Zs2, iZs2));
+        QGS_CHECK(Ju == cam.fx * (cam.Rwc[i] / Zs - X * cam.Rwc[6 + i] / (Zs * Zs)));
         gu_s += Ju * gc[i];
         gv_s += Jv * gc[i];
     }
